@@ -1,0 +1,133 @@
+/*
+ * vqhull_b200.h — C ABI of the B200-native VQhull hot path.
+ *
+ * Drop-in boundary.  The first entry point is the reference's own flat C
+ * interface, same name, signature, ownership and return codes
+ * (reference: proj/include/vqhull/vqhull_c.h:23-24, proj/src/vqhull_c.cpp:26-64);
+ * a program linked against libvqhull_b200.so instead of the reference's
+ * libvqhull.a gets the identical clockwise first-occurrence index list,
+ * computed on the GPU.  The vqhull_cuda_* entry points expose the same
+ * computation on device-resident arrays (the reference's C++ seam:
+ * convex_hull, hull.hpp:58; find_extremes, geometry.hpp:135-138;
+ * extract_subsets, extract.hpp:79-82) for callers that already hold the
+ * points in HBM.
+ *
+ * All functions are reentrant (an internal per-device engine is guarded by a
+ * mutex) and synchronous with respect to the caller: on return, outputs are
+ * written.  Streams are passed as void* (a cudaStream_t), NULL = default stream.
+ *
+ * Return codes: 0 success; 1 invalid arguments (exactly the reference's
+ * conditions: out_count NULL, workers < 1, NULL arrays with n > 0, a
+ * non-finite coordinate); 2 unsupported size (n >= 2^32 - 1 points per
+ * device); 3 CUDA error (see vqhull_cuda_last_error()).
+ */
+#ifndef VQHULL_B200_H
+#define VQHULL_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VQHULL_OK 0
+#define VQHULL_EINVAL 1
+#define VQHULL_ESIZE 2
+#define VQHULL_ECUDA 3
+
+/* Replaces vqhull_compute (vqhull_c.h:23-24, vqhull_c.cpp:26-64).
+ * xs, ys: n host coordinates (pageable or pinned).  out_indices: host array
+ * with room for n entries; receives the input indices of the hull vertices,
+ * clockwise from the leftmost(-lowest) point; equal coordinates resolve to
+ * the first occurrence.  `workers` is validated (>= 1) as in the reference;
+ * the GPU path does not use it. */
+int vqhull_compute(const double* xs, const double* ys, size_t n, int workers,
+                   size_t* out_indices, size_t* out_count);
+
+/* Same computation on device-resident arrays.  d_xs, d_ys: device pointers
+ * (not modified).  out_indices: host OR device pointer with room for n
+ * uint64 entries.  Replaces convex_hull (hull.hpp:58) + the index mapping of
+ * vqhull_c.cpp:46-61. */
+int vqhull_cuda_hull(const double* d_xs, const double* d_ys, uint64_t n,
+                     uint64_t* out_indices, uint64_t* out_count, void* stream);
+
+/* Same, 32-bit indices written to a DEVICE buffer, no host round trip of the
+ * index list (the bench's device-resident leg).  *out_count is host memory. */
+int vqhull_cuda_hull_u32(const double* d_xs, const double* d_ys, uint64_t n,
+                         uint32_t* d_out_indices, uint64_t* out_count, void* stream);
+
+/* find_extremes (geometry.cpp:7-36) on device arrays: lo = leftmost (ties:
+ * lowest y, then first index), hi = rightmost (ties: highest y, then first
+ * index).  Returns 1 for n == 0 (the reference throws). */
+int vqhull_cuda_find_extremes(const double* d_xs, const double* d_ys, uint64_t n,
+                              uint64_t* lo, uint64_t* hi, void* stream);
+
+/* extract_subsets (extract.hpp:75-82) on device arrays, in place: afterwards
+ * [0, *w_l) holds exactly the points left of edge_a, [*w_r, n) exactly the
+ * points left of edge_b and not of edge_a, the middle is unspecified.
+ * edge = {px, py, qx, qy} (host).  r1/r2 (host, 2 doubles) receive the
+ * farthest point of each side in the canonical order (kernels.hpp:36-45);
+ * has_r1/has_r2 say whether the side is non-empty. */
+int vqhull_cuda_extract_subsets(double* d_xs, double* d_ys, uint64_t n,
+                                const double* edge_a, const double* edge_b,
+                                uint64_t* w_l, uint64_t* w_r, double* r1,
+                                int* has_r1, double* r2, int* has_r2,
+                                void* stream);
+
+/* Statistics of the last vqhull_cuda_hull* / vqhull_compute call on this
+ * thread's device engine. */
+typedef struct vqhull_stats {
+    uint64_t n;                 /* points */
+    uint64_t hull_size;         /* vertices */
+    uint32_t levels;            /* recursion levels processed on device */
+    uint32_t launches;          /* kernels launched by the call */
+    uint64_t survivors_root;    /* points written by the fused root pass */
+    uint64_t level_points;      /* sum over levels of points partitioned by K2 */
+    uint64_t finisher_points;   /* points handed to the warp finisher */
+    uint64_t finisher_segments;
+    uint64_t segments;          /* K2 segments over all levels */
+    uint64_t bytes_moved;       /* algorithmic HBM bytes */
+    /* per-kernel device time (ms), valid when timing is enabled */
+    float ms_extremes;
+    float ms_bootstrap;
+    float ms_root_partition;
+    float ms_levels;            /* all K2 launches */
+    float ms_finisher;
+    float ms_other;             /* planner, tile map, emission */
+    float ms_total;             /* first kernel start .. last kernel end */
+    uint32_t timing_valid;
+    uint64_t bytes_extremes;    /* algorithmic bytes per kernel family */
+    uint64_t bytes_bootstrap;
+    uint64_t bytes_root_partition;
+    uint64_t bytes_levels;
+    uint64_t bytes_finisher;
+} vqhull_stats;
+
+int vqhull_cuda_get_stats(vqhull_stats* out);
+
+/* Enable (1) / disable (0) per-kernel CUDA-event timing inside the engine. */
+int vqhull_cuda_set_timing(int enable);
+
+/* Human-readable description of the last CUDA error (thread-local). */
+const char* vqhull_cuda_last_error(void);
+
+/* 1 when a CUDA device is usable from this library. */
+int vqhull_cuda_available(void);
+
+/* Library version string. */
+const char* vqhull_b200_version(void);
+
+/* Dataset generators (tooling, not the hot path): the reference's counter-
+ * based splitmix64 streams (dataset.cpp:32-75) plus the harness-defined
+ * square (BASELINE config 2: x = 2U(2i)-1, y = 2U(2i+1)-1).  Fills points
+ * [first, first+n) of the (kind, seed) sequence into host xs/ys using
+ * `threads` host threads.  kind: 0 kuzmin, 1 circle, 2 disk, 3 square. */
+int vqhull_generate(int kind, uint64_t seed, uint64_t first, uint64_t n,
+                    double* xs, double* ys, int threads);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* VQHULL_B200_H */

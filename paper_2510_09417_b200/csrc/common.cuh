@@ -1,0 +1,292 @@
+// Shared device-side building blocks of the B200 VQhull hot path.
+//
+// Numerics: every predicate and offset below is the reference's exact f64
+// expression (kernels.hpp:19-45), evaluated with explicit round-to-nearest
+// intrinsics (__dsub_rn / __dmul_rn) so no FMA contraction can occur even if
+// the translation unit were compiled with --fmad=true.  Products that the
+// reference forms as a*b are formed here either as a*b or b*a; IEEE
+// multiplication is exactly commutative, so the rounded values are identical.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace vqb {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+// set by a kernel that detected an impossible state (bounded spin expired,
+// runaway loop); the driver checks it after every hull and reports an error
+static __device__ uint32_t g_vqb_fault = 0;  // per-TU; only kernels.cu launches kernels
+
+// ---------------------------------------------------------------------------
+// Canonical farthest order (kernels.hpp:36-45): the strictly smaller lateral
+// offset wins, an exact tie falls to the lexicographically smaller point.
+// We extend the order by the input index so that, among copies of the same
+// coordinates, the FIRST occurrence is the one carried forward: this is the
+// index vqhull_compute would map the vertex to (vqhull_c.cpp:51-61).
+// ---------------------------------------------------------------------------
+struct __align__(16) Best {
+    double off;
+    double x;
+    double y;
+    uint32_t idx;    // global input index (first-occurrence tie-break)
+    uint32_t valid;  // 0 = side empty
+};
+
+__host__ __device__ __forceinline__ Best best_none() {
+    Best b;
+    b.off = 0.0;
+    b.x = 0.0;
+    b.y = 0.0;
+    b.idx = 0xffffffffu;
+    b.valid = 0u;
+    return b;
+}
+
+// true when a is strictly preferred over b
+__device__ __forceinline__ bool prefer(const Best& a, const Best& b) {
+    if (!a.valid) return false;
+    if (!b.valid) return true;
+    if (a.off != b.off) return a.off < b.off;
+    if (a.x != b.x) return a.x < b.x;
+    if (a.y != b.y) return a.y < b.y;
+    return a.idx < b.idx;
+}
+
+__device__ __forceinline__ void consider(Best& b, bool take, double off, double x,
+                                         double y, uint32_t idx) {
+    Best c;
+    c.off = off;
+    c.x = x;
+    c.y = y;
+    c.idx = idx;
+    c.valid = take ? 1u : 0u;
+    if (prefer(c, b)) b = c;
+}
+
+__device__ __forceinline__ Best shfl_best(const Best& b, int src_lane_xor) {
+    Best o;
+    o.off = __shfl_xor_sync(kFull, b.off, src_lane_xor);
+    o.x = __shfl_xor_sync(kFull, b.x, src_lane_xor);
+    o.y = __shfl_xor_sync(kFull, b.y, src_lane_xor);
+    o.idx = __shfl_xor_sync(kFull, b.idx, src_lane_xor);
+    o.valid = __shfl_xor_sync(kFull, b.valid, src_lane_xor);
+    return o;
+}
+
+// butterfly: every lane ends with the warp's best
+__device__ __forceinline__ Best warp_best(Best b) {
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) {
+        Best o = shfl_best(b, s);
+        if (prefer(o, b)) b = o;
+    }
+    return b;
+}
+
+// ---------------------------------------------------------------------------
+// Orientation predicate of the reference, frame_left_of (kernels.hpp:28-30):
+//   (e.px - ux) * (e.qy - uy) > (e.py - uy) * (e.qx - ux)
+// expressed on the precomputed differences of the query point to p and q.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+
+// left of (P -> Q) given (Px-ux, Py-uy) and (Qx-ux, Qy-uy)
+__device__ __forceinline__ bool left_diff(double pdx, double pdy, double qdx, double qdy) {
+    return dmul(pdx, qdy) > dmul(pdy, qdx);
+}
+
+// lateral offset e.dy*ux - e.dx*uy (kernels.hpp:32-34)
+__device__ __forceinline__ double lat_off(double edx, double edy, double ux, double uy) {
+    return dsub(dmul(edy, ux), dmul(edx, uy));
+}
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+// ---------------------------------------------------------------------------
+// Memory-ordering primitives for the decoupled look-back.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ uint32_t ld_cg_u32(const uint32_t* p) { return __ldcg(p); }
+__device__ __forceinline__ double ld_cg_f64(const double* p) { return __ldcg(p); }
+
+// streaming loads of data read exactly once
+__device__ __forceinline__ double ld_stream(const double* p) { return __ldcs(p); }
+__device__ __forceinline__ uint32_t ld_stream(const uint32_t* p) { return __ldcs(p); }
+
+// ---------------------------------------------------------------------------
+// Look-back payload: per class the element count and the best candidate.
+// Combination is associative and commutative (sum; canonical arg-max).
+// ---------------------------------------------------------------------------
+template <int NC>
+struct __align__(16) Agg {
+    uint32_t cnt[NC];
+    Best best[NC];
+};
+
+template <int NC>
+__device__ __forceinline__ void agg_clear(Agg<NC>& a) {
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        a.cnt[c] = 0;
+        a.best[c] = best_none();
+    }
+}
+
+template <int NC>
+__device__ __forceinline__ void agg_combine(Agg<NC>& a, const Agg<NC>& b) {
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        a.cnt[c] += b.cnt[c];
+        if (prefer(b.best[c], a.best[c])) a.best[c] = b.best[c];
+    }
+}
+
+template <int NC>
+__device__ __forceinline__ void agg_store(Agg<NC>* dst, const Agg<NC>& a) {
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        dst->cnt[c] = a.cnt[c];
+        dst->best[c] = a.best[c];
+    }
+}
+
+template <int NC>
+__device__ __forceinline__ Agg<NC> agg_load_cg(const Agg<NC>* src) {
+    Agg<NC> a;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        a.cnt[c] = __ldcg(&src->cnt[c]);
+        a.best[c].off = __ldcg(&src->best[c].off);
+        a.best[c].x = __ldcg(&src->best[c].x);
+        a.best[c].y = __ldcg(&src->best[c].y);
+        a.best[c].idx = __ldcg(&src->best[c].idx);
+        a.best[c].valid = __ldcg(&src->best[c].valid);
+    }
+    return a;
+}
+
+template <int NC>
+__device__ __forceinline__ Agg<NC> shfl_agg(const Agg<NC>& a, int lane_xor) {
+    Agg<NC> o;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        o.cnt[c] = __shfl_xor_sync(kFull, a.cnt[c], lane_xor);
+        o.best[c] = shfl_best(a.best[c], lane_xor);
+    }
+    return o;
+}
+
+// Tile status words: (epoch << 2) | state.  A fresh epoch per launch makes
+// stale words from earlier launches read as "not yet published".
+constexpr uint32_t kStAgg = 1u;
+constexpr uint32_t kStInc = 2u;
+
+__device__ __forceinline__ uint32_t status_word(uint32_t epoch, uint32_t st) {
+    return (epoch << 2) | st;
+}
+
+// Payload concept for the look-back: clear / combine / store / load_cg / shfl.
+template <int NC>
+__device__ __forceinline__ void pl_clear(Agg<NC>& a) { agg_clear(a); }
+template <int NC>
+__device__ __forceinline__ void pl_combine(Agg<NC>& a, const Agg<NC>& b) { agg_combine(a, b); }
+template <int NC>
+__device__ __forceinline__ void pl_store(Agg<NC>* d, const Agg<NC>& a) { agg_store(d, a); }
+template <int NC>
+__device__ __forceinline__ Agg<NC> pl_load(const Agg<NC>* s) { return agg_load_cg(s); }
+template <int NC>
+__device__ __forceinline__ Agg<NC> pl_shfl(const Agg<NC>& a, int x) { return shfl_agg(a, x); }
+
+// Decoupled look-back, run by ONE full warp of the tile that owns `tile`.
+// `first` is the global id of the segment's first tile (tiles of a segment are
+// consecutive ids and are claimed in increasing order, so every predecessor is
+// owned by a running CTA that publishes without waiting).  Publishes the
+// tile's aggregate, walks back, publishes the inclusive value, and returns the
+// exclusive prefix to every lane.
+template <class T>
+__device__ T lookback(uint32_t tile, uint32_t first, const T& local, uint32_t* flags,
+                      T* aggs, T* incs, uint32_t epoch) {
+    const int lane = threadIdx.x & 31;
+    T excl;
+    pl_clear(excl);
+    if (tile == first) {
+        if (lane == 0) {
+            pl_store(&incs[tile], local);
+            __threadfence();
+            st_release(&flags[tile], status_word(epoch, kStInc));
+        }
+        __syncwarp();
+        return excl;
+    }
+    if (lane == 0) {
+        pl_store(&aggs[tile], local);
+        __threadfence();
+        st_release(&flags[tile], status_word(epoch, kStAgg));
+    }
+    __syncwarp();
+    int64_t pred = int64_t(tile) - 1;  // highest predecessor not yet folded in
+    while (true) {
+        const int64_t t = pred - lane;
+        const bool in_seg = t >= int64_t(first);
+        uint32_t st = 0;
+        if (in_seg) {
+            const uint32_t want_hi = epoch << 2;
+            uint32_t w;
+            uint32_t spins = 0;
+            while (true) {
+                w = ld_acquire(&flags[t]);
+                if ((w & ~3u) == want_hi && (w & 3u) != 0) break;
+                if (++spins > 4) __nanosleep(64);
+                if (spins > (1u << 25)) {  // ~seconds: a bug, never wait forever
+                    w = kStInc;
+                    g_vqb_fault = 1u;
+                    break;
+                }
+            }
+            st = w & 3u;
+        }
+        const unsigned inc_mask = __ballot_sync(kFull, in_seg && st == kStInc);
+        // lanes up to (and including) the nearest inclusive tile contribute
+        const int stop = inc_mask ? (__ffs(inc_mask) - 1) : 31;
+        T mine;
+        pl_clear(mine);
+        if (in_seg && lane <= stop) mine = (st == kStInc) ? pl_load(&incs[t]) : pl_load(&aggs[t]);
+#pragma unroll
+        for (int s = 16; s > 0; s >>= 1) {
+            T o = pl_shfl(mine, s);
+            pl_combine(mine, o);
+        }
+        pl_combine(excl, mine);
+        const unsigned seg_mask = __ballot_sync(kFull, in_seg);
+        if (inc_mask) break;
+        if (seg_mask != kFull) break;  // window reached the first tile (defensive)
+        pred -= 32;
+    }
+    if (lane == 0) {
+        T inc = excl;
+        pl_combine(inc, local);
+        pl_store(&incs[tile], inc);
+        __threadfence();
+        st_release(&flags[tile], status_word(epoch, kStInc));
+    }
+    __syncwarp();
+    return excl;
+}
+
+}  // namespace vqb

@@ -1,0 +1,718 @@
+// Host-side recursion driver and C ABI of the B200 VQhull hot path.
+//
+// One Engine per device owns the HBM workspace (ping-pong point buffers,
+// look-back status words, per-level node tables) and runs a hull as:
+//   K1 extremes -> KA bootstrap arg-max -> KB fused levels 1+2 ->
+//   { planner -> finisher -> tile map -> K2 } per level -> size/emit.
+// The reference's equivalent is convex_hull (hull.cpp:207-267) driving
+// chain_recursive/chain_iterative (hull.cpp:78-190), one call per segment;
+// here every level is one launch over all of its segments.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <deque>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/vqhull_b200.h"
+#include "hull_types.cuh"
+#include "kernels.h"
+
+namespace vqb {
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct CudaError {
+    cudaError_t e;
+};
+
+inline void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) {
+        g_last_error = std::string(what) + ": " + cudaGetErrorString(e);
+        throw CudaError{e};
+    }
+}
+
+// Device buffer that only grows.  keep=true preserves the old contents.
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    template <class T>
+    T* as() const { return static_cast<T*>(p); }
+    void ensure(size_t bytes, cudaStream_t st, bool keep = false) {
+        if (bytes <= cap) return;
+        size_t ncap = std::max(bytes, cap + cap / 2);
+        ncap = (ncap + 255) & ~size_t(255);
+        void* np = nullptr;
+        ck(cudaMallocAsync(&np, ncap, st), "cudaMallocAsync");
+        if (keep && p && cap) ck(cudaMemcpyAsync(np, p, cap, cudaMemcpyDeviceToDevice, st), "grow copy");
+        if (p) ck(cudaFreeAsync(p, st), "cudaFreeAsync");
+        p = np;
+        cap = ncap;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
+struct PointBuf {
+    DevBuf x, y, id;
+    void ensure(size_t n, cudaStream_t st) {
+        x.ensure(n * 8, st);
+        y.ensure(n * 8, st);
+        id.ensure(n * 4, st);
+    }
+};
+
+struct LevelTables {
+    DevBuf slots, kind, link, size, start, segs, fins, fin_count;
+};
+
+struct TimedKernel {
+    int family;  // 0 extremes 1 bootstrap 2 root 3 level 4 finisher 5 other
+    cudaEvent_t a, b;
+};
+
+}  // namespace
+
+class Engine {
+   public:
+    explicit Engine(int dev) : dev_(dev) {
+        ck(cudaSetDevice(dev), "cudaSetDevice");
+        ck(cudaDeviceGetAttribute(&sms_, cudaDevAttrMultiProcessorCount, dev), "attr");
+        // keep freed pool memory cached: per-call growth then costs nothing
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        occ_root_ = std::max(1, occupancy_root());
+        occ_level_ = std::max(1, occupancy_level());
+        occ_fin_ = std::max(1, occupancy_finisher());
+        stream_grid_ = sms_ * 4;
+        ck(cudaMalloc(&ctrs_, 64 * sizeof(uint32_t)), "cudaMalloc ctrs");
+        ck(cudaMemset(ctrs_, 0, 64 * sizeof(uint32_t)), "memset ctrs");
+        ck(cudaMalloc(&root_, sizeof(RootInfo)), "cudaMalloc root");
+        ck(cudaMalloc(&hword_, 64), "cudaMalloc h");
+        ck(cudaMallocHost(&h_info_, sizeof(LevelInfo) * 2), "cudaMallocHost");
+        ck(cudaMallocHost(&h_root_, sizeof(RootInfo)), "cudaMallocHost");
+        ck(cudaMallocHost(&h_word_, 64), "cudaMallocHost");
+        partials_.ensure(partial_bytes(stream_grid_), nullptr);
+        ck(cudaDeviceSynchronize(), "init");
+    }
+
+    int device() const { return dev_; }
+    void set_timing(bool on) { timing_ = on; }
+    const vqhull_stats& stats() const { return stats_; }
+    std::mutex& mutex() { return mu_; }
+
+    // Full hull on device arrays.  Writes the u32 index list to d_out (device,
+    // capacity >= n) and returns h through *h.  Returns VQHULL_* code.
+    int hull(const double* dx, const double* dy, uint64_t n, uint32_t* d_out, uint64_t* h,
+             cudaStream_t st) {
+        reset_stats(n);
+        *h = 0;
+        if (n == 0) return VQHULL_OK;
+        if (n >= 0xffffffffull) return VQHULL_ESIZE;
+        launches_ = 0;
+        begin_timing(st);
+
+        // ---- K1: extremes
+        tk(0, st, [&] { launch_extremes(dx, dy, n, partials_.p, &ctrs_[3], root_, stream_grid_, st); });
+        // ---- KA: bootstrap counts + arg-max + finiteness
+        tk(1, st, [&] { launch_bootstrap(dx, dy, n, partials_.p, &ctrs_[3], root_, stream_grid_, st); });
+        stats_.bytes_extremes = 8 * n;
+        stats_.bytes_bootstrap = 16 * n;
+
+        // ---- level-1 slot table (the two bootstrap sides)
+        LevelTables& L1 = level(1);
+        L1.slots.ensure(2 * sizeof(ChildRec), st);
+        L1.kind.ensure(2, st);
+        L1.link.ensure(8, st);
+        L1.size.ensure(8, st);
+        L1.start.ensure(8, st);
+        launch_root_slots(root_, L1.slots.as<ChildRec>(), L1.kind.as<uint8_t>(), L1.link.as<uint32_t>(), st);
+        ++launches_;
+
+        // ---- KB: fused levels 1+2 over the input
+        bufs_[0].ensure(n, st);
+        const uint32_t ntiles_root = uint32_t((n + kTile - 1) / kTile);
+        ensure_lookback(ntiles_root, 4, st);
+        LevelTables& L2 = level(2);
+        L2.slots.ensure(4 * sizeof(ChildRec), st);
+        {
+            const int grid = std::max(1, std::min<int>(int(ntiles_root), sms_ * occ_root_));
+            const uint32_t ep = next_epoch();
+            tk(2, st, [&] {
+                launch_root_partition(dx, dy, n, root_, bufs_[0].x.as<double>(), bufs_[0].y.as<double>(),
+                                      bufs_[0].id.as<uint32_t>(), flags_.as<uint32_t>(), aggs_.p,
+                                      incs_.p, ep, &ctrs_[0], L2.slots.as<ChildRec>(), grid, st);
+            });
+        }
+        // finiteness verdict + sizes for the byte accounting
+        ck(cudaMemcpyAsync(h_root_, root_, sizeof(RootInfo), cudaMemcpyDeviceToHost, st), "d2h root");
+
+        // ---- levels
+        int in = 0;
+        uint32_t nslots = 4;
+        uint64_t fin_base = 0;
+        int lvl = 2;
+        level_fin_base_.assign(4, 0);
+        while (true) {
+            LevelTables& T = level(lvl);
+            T.kind.ensure(nslots, st);
+            T.link.ensure(size_t(nslots) * 4, st);
+            T.size.ensure(size_t(nslots) * 4, st);
+            T.start.ensure(size_t(nslots) * 4, st);
+            T.segs.ensure(size_t(nslots) * sizeof(SegRec), st);
+            T.fins.ensure(size_t(nslots) * sizeof(FinRec), st);
+            const uint32_t nchunks = (nslots + 1023) / 1024;
+            ensure_lookback(nchunks, 4, st);
+            info_.ensure(size_t(lvl + 1) * sizeof(LevelInfo), st, true);
+            LevelInfo* dinfo = info_.as<LevelInfo>() + lvl;
+            {
+                const uint32_t ep = next_epoch();
+                tk(5, st, [&] {
+                    launch_planner(T.slots.as<ChildRec>(), nslots, T.segs.as<SegRec>(), T.fins.as<FinRec>(),
+                                   T.kind.as<uint8_t>(), T.link.as<uint32_t>(), dinfo, fin_base,
+                                   flags_.as<uint32_t>(), aggs_.p, incs_.p, ep, &ctrs_[2], sms_ * 4, st);
+                });
+            }
+            ck(cudaMemcpyAsync(h_info_, dinfo, sizeof(LevelInfo), cudaMemcpyDeviceToHost, st), "d2h info");
+            ck(cudaStreamSynchronize(st), "level sync");
+            const LevelInfo li = *h_info_;
+            if (lvl == 2 && h_root_->nonfinite) {
+                end_timing(st);
+                ck(cudaStreamSynchronize(st), "sync");
+                return VQHULL_EINVAL;
+            }
+            // every point of this level's slots was written (20 B) by the
+            // previous partition (KB for level 2, K2 otherwise)
+            const uint64_t written = uint64_t(li.out_total) + li.fin_total + li.nleaf;
+            if (lvl == 2) stats_.survivors_root = written;
+            else stats_.bytes_levels += 20 * written;
+            // finisher
+            if (level_fin_base_.size() <= size_t(lvl)) level_fin_base_.resize(lvl + 1, 0);
+            level_fin_base_[lvl] = fin_base;
+            T.fin_count.ensure(size_t(std::max<uint32_t>(li.nfin, 1)) * 4, st);
+            if (li.nfin) {
+                chain_.ensure((fin_base + li.fin_total) * 4, st, true);
+                tk(4, st, [&] {
+                    launch_finisher(T.fins.as<FinRec>(), dinfo, bufs_[in].x.as<double>(), bufs_[in].y.as<double>(),
+                                    bufs_[in].id.as<uint32_t>(), chain_.as<uint32_t>(),
+                                    T.fin_count.as<uint32_t>(), li.nfin, sms_ * occ_fin_, st);
+                });
+                stats_.finisher_points += li.fin_total;
+                stats_.finisher_segments += li.nfin;
+                stats_.bytes_finisher += uint64_t(li.fin_total) * 20 + uint64_t(li.fin_total) * 4;
+                fin_base += li.fin_total;
+            }
+            if (li.nseg == 0) {
+                lmax_ = lvl;
+                break;
+            }
+            if (uint64_t(lvl) > n + 8) {  // every level sheds >= 1 point per segment
+                g_last_error = "recursion did not shrink (internal error)";
+                throw CudaError{cudaErrorUnknown};
+            }
+            // K2 over all segments of this level
+            const int out = in ^ 1;
+            bufs_[out].ensure(std::max<uint64_t>(li.out_total, 1), st);
+            tile_seg_.ensure(size_t(li.ntiles) * 4, st);
+            ensure_lookback(li.ntiles, 2, st);
+            LevelTables& Tn = level(lvl + 1);
+            Tn.slots.ensure(size_t(2) * li.nseg * sizeof(ChildRec), st);
+            // re-fetch T: level() may have grown the vector
+            LevelTables& Tc = level(lvl);
+            tk(5, st, [&] { launch_tilemap(Tc.segs.as<SegRec>(), dinfo, tile_seg_.as<uint32_t>(), li.ntiles, st); });
+            {
+                const int grid = std::max(1, std::min<int>(int(li.ntiles), sms_ * occ_level_));
+                const uint32_t ep = next_epoch();
+                tk(3, st, [&] {
+                    launch_level(Tc.segs.as<SegRec>(), tile_seg_.as<uint32_t>(), dinfo, bufs_[in].x.as<double>(),
+                                 bufs_[in].y.as<double>(), bufs_[in].id.as<uint32_t>(), bufs_[out].x.as<double>(),
+                                 bufs_[out].y.as<double>(), bufs_[out].id.as<uint32_t>(), flags_.as<uint32_t>(),
+                                 aggs_.p, incs_.p, ep, &ctrs_[1], Tn.slots.as<ChildRec>(), false, grid, st);
+                });
+            }
+            stats_.segments += li.nseg;
+            stats_.level_points += li.out_total;
+            stats_.bytes_levels += uint64_t(li.out_total) * 20;  // reads; writes counted next level
+            nslots = 2 * li.nseg;
+            note_slots(lvl + 1, nslots);
+            in = out;
+            ++lvl;
+        }
+        stats_.levels = uint32_t(lmax_);
+        stats_.bytes_root_partition = 16 * n + 20 * stats_.survivors_root;
+
+        // ---- emission: bottom-up sizes, root frame, top-down starts
+        for (int l = lmax_; l >= 1; --l) {
+            LevelTables& T = level(l);
+            const uint32_t ns = slot_count(l);
+            const uint32_t* child_size = (l < lmax_) ? level(l + 1).size.as<uint32_t>() : nullptr;
+            tk(5, st, [&] {
+                launch_size(ns, T.kind.as<uint8_t>(), T.link.as<uint32_t>(),
+                            l >= 2 ? T.fin_count.as<uint32_t>() : nullptr, child_size,
+                            T.size.as<uint32_t>(), st);
+            });
+        }
+        tk(5, st, [&] {
+            launch_root_frame(root_, level(1).size.as<uint32_t>(), level(1).start.as<uint32_t>(), d_out,
+                              hword_, st);
+        });
+        for (int l = 1; l <= lmax_; ++l) {
+            LevelTables& T = level(l);
+            const uint32_t ns = slot_count(l);
+            const bool has_child = l < lmax_;
+            tk(5, st, [&] {
+                launch_emit(ns, T.kind.as<uint8_t>(), T.link.as<uint32_t>(), T.slots.as<ChildRec>(),
+                            l >= 2 ? T.fins.as<FinRec>() : nullptr,
+                            l >= 2 ? T.fin_count.as<uint32_t>() : nullptr, chain_.as<uint32_t>(),
+                            T.start.as<uint32_t>(), has_child ? level(l + 1).size.as<uint32_t>() : nullptr,
+                            has_child ? level(l + 1).start.as<uint32_t>() : nullptr, d_out, st);
+            });
+        }
+        ck(cudaMemcpyAsync(h_word_, hword_, 4, cudaMemcpyDeviceToHost, st), "d2h h");
+        end_timing(st);
+        ck(cudaStreamSynchronize(st), "final sync");
+        ck(cudaGetLastError(), "kernel launch");
+        if (const uint32_t f = read_and_clear_fault()) {
+            g_last_error = "device fault code " + std::to_string(f);
+            throw CudaError{cudaErrorUnknown};
+        }
+        *h = *h_word_;
+        stats_.hull_size = *h;
+        stats_.launches = launches_;
+        stats_.bytes_moved = stats_.bytes_extremes + stats_.bytes_bootstrap + stats_.bytes_root_partition +
+                             stats_.bytes_levels + stats_.bytes_finisher;
+        collect_timing();
+        return VQHULL_OK;
+    }
+
+    int find_extremes(const double* dx, const double* dy, uint64_t n, uint64_t* lo, uint64_t* hi,
+                      cudaStream_t st) {
+        if (n == 0) return VQHULL_EINVAL;
+        if (n >= 0xffffffffull) return VQHULL_ESIZE;
+        launch_extremes(dx, dy, n, partials_.p, &ctrs_[3], root_, stream_grid_, st);
+        ck(cudaMemcpyAsync(h_root_, root_, sizeof(RootInfo), cudaMemcpyDeviceToHost, st), "d2h root");
+        ck(cudaStreamSynchronize(st), "sync");
+        ck(cudaGetLastError(), "launch");
+        *lo = h_root_->p_idx;
+        *hi = h_root_->q_idx;
+        return VQHULL_OK;
+    }
+
+    int extract(double* dx, double* dy, uint64_t n, const double* ea, const double* eb, uint64_t* wl,
+                uint64_t* wr, double* r1, int* h1, double* r2, int* h2, cudaStream_t st) {
+        *wl = 0;
+        *wr = n;
+        *h1 = *h2 = 0;
+        if (n == 0) return VQHULL_OK;
+        if (n >= 0xffffffffull) return VQHULL_ESIZE;
+        bufs_[0].ensure(n, st);
+        bufs_[1].ensure(n, st);
+        ck(cudaMemcpyAsync(bufs_[0].x.p, dx, n * 8, cudaMemcpyDeviceToDevice, st), "copy x");
+        ck(cudaMemcpyAsync(bufs_[0].y.p, dy, n * 8, cudaMemcpyDeviceToDevice, st), "copy y");
+        iota(bufs_[0].id.as<uint32_t>(), n, st);
+        SegRec g;
+        std::memset(&g, 0, sizeof g);
+        g.px = ea[0]; g.py = ea[1]; g.rx = ea[2]; g.ry = ea[3];
+        g.bx = eb[0]; g.by = eb[1]; g.qx = eb[2]; g.qy = eb[3];
+        g.adx = ea[2] - ea[0]; g.ady = ea[3] - ea[1];  // EdgeFrame::make (kernels.hpp:23-25)
+        g.bdx = eb[2] - eb[0]; g.bdy = eb[3] - eb[1];
+        g.begin = 0; g.out = 0; g.m = uint32_t(n); g.tile0 = 0;
+        g.ntiles = uint32_t((n + kTile - 1) / kTile);
+        g.slot = 0;
+        LevelInfo li;
+        std::memset(&li, 0, sizeof li);
+        li.nslots = 1; li.nseg = 1; li.ntiles = g.ntiles; li.out_total = uint32_t(n);
+        scratch_.ensure(sizeof(SegRec) + sizeof(LevelInfo) + 2 * sizeof(ChildRec), st);
+        char* sp = scratch_.as<char>();
+        SegRec* dseg = reinterpret_cast<SegRec*>(sp);
+        LevelInfo* dli = reinterpret_cast<LevelInfo*>(sp + sizeof(SegRec));
+        ChildRec* dch = reinterpret_cast<ChildRec*>(sp + sizeof(SegRec) + sizeof(LevelInfo));
+        ck(cudaMemcpyAsync(dseg, &g, sizeof g, cudaMemcpyHostToDevice, st), "h2d seg");
+        ck(cudaMemcpyAsync(dli, &li, sizeof li, cudaMemcpyHostToDevice, st), "h2d info");
+        tile_seg_.ensure(size_t(g.ntiles) * 4, st);
+        ck(cudaMemsetAsync(tile_seg_.p, 0, size_t(g.ntiles) * 4, st), "memset tiles");
+        ensure_lookback(g.ntiles, 2, st);
+        const int grid = std::max(1, std::min<int>(int(g.ntiles), sms_ * occ_level_));
+        launch_level(dseg, tile_seg_.as<uint32_t>(), dli, bufs_[0].x.as<double>(), bufs_[0].y.as<double>(),
+                     bufs_[0].id.as<uint32_t>(), bufs_[1].x.as<double>(), bufs_[1].y.as<double>(),
+                     bufs_[1].id.as<uint32_t>(), flags_.as<uint32_t>(), aggs_.p, incs_.p, next_epoch(),
+                     &ctrs_[1], dch, true, grid, st);
+        ChildRec ch[2];
+        ck(cudaMemcpyAsync(ch, dch, sizeof ch, cudaMemcpyDeviceToHost, st), "d2h children");
+        ck(cudaStreamSynchronize(st), "sync");
+        ck(cudaGetLastError(), "launch");
+        const uint64_t nl = ch[0].m, nr = ch[1].m;
+        if (nl) ck(cudaMemcpyAsync(dx, bufs_[1].x.p, nl * 8, cudaMemcpyDeviceToDevice, st), "copy back");
+        if (nl) ck(cudaMemcpyAsync(dy, bufs_[1].y.p, nl * 8, cudaMemcpyDeviceToDevice, st), "copy back");
+        if (nr) ck(cudaMemcpyAsync(dx + (n - nr), bufs_[1].x.as<double>() + (n - nr), nr * 8,
+                                   cudaMemcpyDeviceToDevice, st), "copy back");
+        if (nr) ck(cudaMemcpyAsync(dy + (n - nr), bufs_[1].y.as<double>() + (n - nr), nr * 8,
+                                   cudaMemcpyDeviceToDevice, st), "copy back");
+        ck(cudaStreamSynchronize(st), "sync");
+        *wl = nl;
+        *wr = n - nr;
+        *h1 = nl > 0;
+        *h2 = nr > 0;
+        if (nl) { r1[0] = ch[0].rx; r1[1] = ch[0].ry; }
+        if (nr) { r2[0] = ch[1].rx; r2[1] = ch[1].ry; }
+        return VQHULL_OK;
+    }
+
+    // host-input path (vqhull_compute)
+    int compute_host(const double* xs, const double* ys, uint64_t n, uint32_t* h_out_u32, uint64_t* h,
+                     cudaStream_t st) {
+        in_.x.ensure(n * 8, st);
+        in_.y.ensure(n * 8, st);
+        ck(cudaMemcpyAsync(in_.x.p, xs, n * 8, cudaMemcpyHostToDevice, st), "h2d x");
+        ck(cudaMemcpyAsync(in_.y.p, ys, n * 8, cudaMemcpyHostToDevice, st), "h2d y");
+        out_.ensure(n * 4, st);
+        const int rc = hull(in_.x.as<double>(), in_.y.as<double>(), n, out_.as<uint32_t>(), h, st);
+        if (rc) return rc;
+        if (*h) ck(cudaMemcpyAsync(h_out_u32, out_.p, *h * 4, cudaMemcpyDeviceToHost, st), "d2h idx");
+        ck(cudaStreamSynchronize(st), "sync");
+        return VQHULL_OK;
+    }
+
+    DevBuf& out_buf() { return out_; }
+
+   private:
+    LevelTables& level(int l) {
+        if (levels_.size() <= size_t(l)) levels_.resize(l + 1);
+        return levels_[l];
+    }
+    uint32_t slot_count(int l) const { return l < int(slot_counts_.size()) ? slot_counts_[l] : 0; }
+
+    uint32_t next_epoch() {
+        ++epoch_;
+        if ((epoch_ & 0x3fffffffu) == 0) epoch_ = 1;
+        return epoch_ & 0x3fffffffu;
+    }
+
+    void ensure_lookback(uint32_t tiles, int nc, cudaStream_t st) {
+        const size_t t = std::max<uint32_t>(tiles, 1);
+        if (t * 4 > flags_.cap) {
+            // fresh status words must not alias a live epoch: zero them
+            flags_.ensure(t * 4, st);
+            ck(cudaMemsetAsync(flags_.p, 0, flags_.cap, st), "memset flags");
+        }
+        const size_t pb = std::max(agg_bytes(nc), std::max(agg_bytes(4), plan_agg_bytes()));
+        aggs_.ensure(t * pb, st);
+        incs_.ensure(t * pb, st);
+    }
+
+    void iota(uint32_t* d, uint64_t n, cudaStream_t st);
+
+    void reset_stats(uint64_t n) {
+        std::memset(&stats_, 0, sizeof stats_);
+        stats_.n = n;
+        timed_.clear();
+        slot_counts_.assign(3, 0);
+        slot_counts_[1] = 2;
+        slot_counts_[2] = 4;
+        lmax_ = 2;
+    }
+
+    template <class F>
+    void tk(int family, cudaStream_t st, F&& f) {
+        if (timing_) {
+            TimedKernel t;
+            t.family = family;
+            t.a = event();
+            t.b = event();
+            ck(cudaEventRecord(t.a, st), "event");
+            f();
+            ck(cudaEventRecord(t.b, st), "event");
+            timed_.push_back(t);
+        } else {
+            f();
+        }
+        ++launches_;
+        track_slots();
+    }
+    void track_slots() {}
+
+    cudaEvent_t event() {
+        if (ev_used_ == events_.size()) {
+            cudaEvent_t e;
+            ck(cudaEventCreate(&e), "cudaEventCreate");
+            events_.push_back(e);
+        }
+        return events_[ev_used_++];
+    }
+    void begin_timing(cudaStream_t st) {
+        ev_used_ = 0;
+        if (timing_) {
+            ev_begin_ = event();
+            ck(cudaEventRecord(ev_begin_, st), "event");
+        }
+    }
+    void end_timing(cudaStream_t st) {
+        if (timing_) {
+            ev_end_ = event();
+            ck(cudaEventRecord(ev_end_, st), "event");
+        }
+    }
+    void collect_timing() {
+        if (!timing_) return;
+        float fam[6] = {0, 0, 0, 0, 0, 0};
+        for (auto& t : timed_) {
+            float ms = 0;
+            ck(cudaEventElapsedTime(&ms, t.a, t.b), "elapsed");
+            fam[t.family] += ms;
+        }
+        float total = 0;
+        ck(cudaEventElapsedTime(&total, ev_begin_, ev_end_), "elapsed");
+        stats_.ms_extremes = fam[0];
+        stats_.ms_bootstrap = fam[1];
+        stats_.ms_root_partition = fam[2];
+        stats_.ms_levels = fam[3];
+        stats_.ms_finisher = fam[4];
+        stats_.ms_other = fam[5];
+        stats_.ms_total = total;
+        stats_.timing_valid = 1;
+    }
+
+   public:
+    // called by hull() after each level to remember slot counts for emission
+    void note_slots(int l, uint32_t ns) {
+        if (slot_counts_.size() <= size_t(l)) slot_counts_.resize(l + 1, 0);
+        slot_counts_[l] = ns;
+    }
+
+   private:
+    int dev_ = 0;
+    int sms_ = 148;
+    int occ_root_ = 1, occ_level_ = 1, occ_fin_ = 1;
+    int stream_grid_ = 592;
+    uint32_t* ctrs_ = nullptr;
+    RootInfo* root_ = nullptr;
+    uint32_t* hword_ = nullptr;
+    LevelInfo* h_info_ = nullptr;
+    RootInfo* h_root_ = nullptr;
+    uint32_t* h_word_ = nullptr;
+    DevBuf partials_, flags_, aggs_, incs_, tile_seg_, chain_, info_, scratch_, out_;
+    PointBuf bufs_[2];
+    PointBuf in_;
+    std::deque<LevelTables> levels_;  // deque: references stay valid on growth
+    std::vector<uint32_t> slot_counts_;
+    std::vector<uint64_t> level_fin_base_;
+    int lmax_ = 2;
+    uint32_t epoch_ = 0;
+    uint32_t launches_ = 0;
+    bool timing_ = false;
+    std::vector<cudaEvent_t> events_;
+    size_t ev_used_ = 0;
+    cudaEvent_t ev_begin_ = nullptr, ev_end_ = nullptr;
+    std::vector<TimedKernel> timed_;
+    vqhull_stats stats_{};
+    std::mutex mu_;
+};
+
+__global__ void iota_kernel(uint32_t* d, uint64_t n) {
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x)
+        d[i] = uint32_t(i);
+}
+
+void Engine::iota(uint32_t* d, uint64_t n, cudaStream_t st) {
+    iota_kernel<<<1184, 256, 0, st>>>(d, n);
+}
+
+__global__ void widen_kernel(const uint32_t* s, uint64_t* d, uint64_t n) {
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x)
+        d[i] = s[i];
+}
+
+// ---------------------------------------------------------------------------
+// engine registry (one per device)
+// ---------------------------------------------------------------------------
+namespace {
+std::mutex g_reg_mu;
+std::vector<std::unique_ptr<Engine>> g_engines;
+thread_local bool g_timing = false;
+
+Engine& engine() {
+    int dev = 0;
+    ck(cudaGetDevice(&dev), "cudaGetDevice");
+    std::lock_guard<std::mutex> lk(g_reg_mu);
+    if (g_engines.size() <= size_t(dev)) g_engines.resize(dev + 1);
+    if (!g_engines[dev]) g_engines[dev].reset(new Engine(dev));
+    return *g_engines[dev];
+}
+
+bool is_device_ptr(const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+}  // namespace
+
+}  // namespace vqb
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+using vqb::CudaError;
+using vqb::Engine;
+
+extern "C" {
+
+const char* vqhull_b200_version(void) { return "vqhull-b200 0.1 (sm_100a)"; }
+
+const char* vqhull_cuda_last_error(void) { return vqb::g_last_error.c_str(); }
+
+int vqhull_cuda_available(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n > 0 ? 1 : 0;
+}
+
+int vqhull_cuda_set_timing(int enable) {
+    try {
+        Engine& e = vqb::engine();
+        std::lock_guard<std::mutex> lk(e.mutex());
+        e.set_timing(enable != 0);
+        return 0;
+    } catch (const CudaError&) {
+        return VQHULL_ECUDA;
+    }
+}
+
+int vqhull_cuda_get_stats(vqhull_stats* out) {
+    if (!out) return VQHULL_EINVAL;
+    try {
+        Engine& e = vqb::engine();
+        std::lock_guard<std::mutex> lk(e.mutex());
+        *out = e.stats();
+        return 0;
+    } catch (const CudaError&) {
+        return VQHULL_ECUDA;
+    }
+}
+
+int vqhull_compute(const double* xs, const double* ys, size_t n, int workers, size_t* out_indices,
+                   size_t* out_count) {
+    // argument checks of the reference, in its order (vqhull_c.cpp:29-34);
+    // the finiteness scan is fused into the bootstrap kernel
+    if (!out_count || workers < 1) return VQHULL_EINVAL;
+    *out_count = 0;
+    if (n == 0) return VQHULL_OK;
+    if (!xs || !ys || !out_indices) return VQHULL_EINVAL;
+    try {
+        Engine& e = vqb::engine();
+        std::lock_guard<std::mutex> lk(e.mutex());
+        std::vector<uint32_t> tmp;
+        uint32_t* dst = reinterpret_cast<uint32_t*>(out_indices);  // widened in place below
+        uint64_t h = 0;
+        const int rc = e.compute_host(xs, ys, n, dst, &h, nullptr);
+        if (rc) return rc;
+        // widen u32 -> size_t in place, back to front
+        for (uint64_t i = h; i-- > 0;) out_indices[i] = size_t(dst[i]);
+        *out_count = size_t(h);
+        return VQHULL_OK;
+    } catch (const CudaError&) {
+        return VQHULL_ECUDA;
+    }
+}
+
+int vqhull_cuda_hull_u32(const double* d_xs, const double* d_ys, uint64_t n, uint32_t* d_out,
+                         uint64_t* out_count, void* stream) {
+    if (!out_count) return VQHULL_EINVAL;
+    *out_count = 0;
+    if (n == 0) return VQHULL_OK;
+    if (!d_xs || !d_ys || !d_out) return VQHULL_EINVAL;
+    try {
+        Engine& e = vqb::engine();
+        std::lock_guard<std::mutex> lk(e.mutex());
+        uint64_t h = 0;
+        const int rc = e.hull(d_xs, d_ys, n, d_out, &h, static_cast<cudaStream_t>(stream));
+        if (rc) return rc;
+        *out_count = h;
+        return VQHULL_OK;
+    } catch (const CudaError&) {
+        return VQHULL_ECUDA;
+    }
+}
+
+int vqhull_cuda_hull(const double* d_xs, const double* d_ys, uint64_t n, uint64_t* out_indices,
+                     uint64_t* out_count, void* stream) {
+    if (!out_count) return VQHULL_EINVAL;
+    *out_count = 0;
+    if (n == 0) return VQHULL_OK;
+    if (!d_xs || !d_ys || !out_indices) return VQHULL_EINVAL;
+    try {
+        Engine& e = vqb::engine();
+        std::lock_guard<std::mutex> lk(e.mutex());
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        e.out_buf().ensure(n * 4, st);
+        uint64_t h = 0;
+        const int rc = e.hull(d_xs, d_ys, n, e.out_buf().as<uint32_t>(), &h, st);
+        if (rc) return rc;
+        if (h) {
+            if (vqb::is_device_ptr(out_indices)) {
+                vqb::widen_kernel<<<592, 256, 0, st>>>(e.out_buf().as<uint32_t>(), out_indices, h);
+                vqb::ck(cudaStreamSynchronize(st), "sync");
+            } else {
+                std::vector<uint32_t> tmp(h);
+                vqb::ck(cudaMemcpyAsync(tmp.data(), e.out_buf().p, h * 4, cudaMemcpyDeviceToHost, st), "d2h");
+                vqb::ck(cudaStreamSynchronize(st), "sync");
+                for (uint64_t i = 0; i < h; ++i) out_indices[i] = tmp[i];
+            }
+        }
+        *out_count = h;
+        return VQHULL_OK;
+    } catch (const CudaError&) {
+        return VQHULL_ECUDA;
+    }
+}
+
+int vqhull_cuda_find_extremes(const double* d_xs, const double* d_ys, uint64_t n, uint64_t* lo,
+                              uint64_t* hi, void* stream) {
+    if (!lo || !hi) return VQHULL_EINVAL;
+    if (n > 0 && (!d_xs || !d_ys)) return VQHULL_EINVAL;
+    try {
+        Engine& e = vqb::engine();
+        std::lock_guard<std::mutex> lk(e.mutex());
+        return e.find_extremes(d_xs, d_ys, n, lo, hi, static_cast<cudaStream_t>(stream));
+    } catch (const CudaError&) {
+        return VQHULL_ECUDA;
+    }
+}
+
+int vqhull_cuda_extract_subsets(double* d_xs, double* d_ys, uint64_t n, const double* edge_a,
+                                const double* edge_b, uint64_t* w_l, uint64_t* w_r, double* r1,
+                                int* has_r1, double* r2, int* has_r2, void* stream) {
+    if (!edge_a || !edge_b || !w_l || !w_r || !r1 || !r2 || !has_r1 || !has_r2) return VQHULL_EINVAL;
+    if (n > 0 && (!d_xs || !d_ys)) return VQHULL_EINVAL;
+    try {
+        Engine& e = vqb::engine();
+        std::lock_guard<std::mutex> lk(e.mutex());
+        return e.extract(d_xs, d_ys, n, edge_a, edge_b, w_l, w_r, r1, has_r1, r2, has_r2,
+                         static_cast<cudaStream_t>(stream));
+    } catch (const CudaError&) {
+        return VQHULL_ECUDA;
+    }
+}
+
+}  // extern "C"

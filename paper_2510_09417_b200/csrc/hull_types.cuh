@@ -1,0 +1,120 @@
+// Device data layout of the B200 VQhull driver.
+#pragma once
+
+#include <cstdint>
+
+#include "common.cuh"
+
+namespace vqb {
+
+// Points in HBM are structure-of-arrays, as in the reference PointSet
+// (geometry.hpp:86-125): x[], y[] as f64, plus the carried u32 input index in
+// every buffer after the root pass (the root pass reads the caller's arrays
+// and uses the position as the index).
+
+constexpr int kThreads = 256;               // partition CTA size
+constexpr int kItems = 8;                   // points per thread per tile
+constexpr int kTile = kThreads * kItems;    // points per partition tile
+constexpr int kWarps = kThreads / 32;
+constexpr uint32_t kFinMax = 256;           // segments this small go to the warp finisher
+
+// K1 + pass A results, one per hull call (device resident).
+struct RootInfo {
+    // K1: find_extremes (geometry.cpp:7-36)
+    uint32_t p_idx, q_idx;
+    double px, py, qx, qy;
+    // pass A: bootstrap partition counts + arg-max (hull.cpp:228-235)
+    uint32_t cnt1, cnt2;
+    Best r1, r2;
+    uint32_t nonfinite;
+    uint32_t pad;
+};
+
+// One node of the recursion tree as produced by its parent's partition:
+// triangle (p, r, q) where r is the node's apex (its hull vertex), and the
+// node's candidate points, which live contiguously at [begin, begin+m) of the
+// buffer the parent wrote.  hull.cpp:95-112 (chain_recursive children).
+struct ChildRec {
+    double px, py, rx, ry, qx, qy;
+    uint64_t begin;
+    uint32_t m;
+    uint32_t r_idx;
+};
+
+// A node that is partitioned by the tiled level kernel (m > kFinMax).
+// Edge A = p->r, edge B = b->q (b == r except for the general-edge extract
+// API).  Frames: (adx, ady) = r - p, (bdx, bdy) = q - b  (kernels.hpp:23-25).
+struct SegRec {
+    double px, py, rx, ry, qx, qy;
+    double bx, by;
+    double adx, ady, bdx, bdy;
+    uint64_t begin;   // input buffer position of the first point
+    uint64_t out;     // output buffer base of its two-sided range
+    uint32_t m;
+    uint32_t tile0;   // first tile id of this segment in the level launch
+    uint32_t ntiles;
+    uint32_t slot;    // this node's slot in the level's slot table
+};
+
+// A node solved entirely by one warp (m <= kFinMax).
+struct FinRec {
+    ChildRec c;
+    uint64_t chain_base;  // where its in-order chain is written
+    uint32_t slot;
+    uint32_t pad;
+};
+
+// Node kinds in the slot tables.
+enum : uint8_t { kEmpty = 0, kLeaf = 1, kFin = 2, kInternal = 3 };
+
+// Per-level planner output.
+struct LevelInfo {
+    uint32_t nslots;
+    uint32_t nseg;
+    uint32_t nfin;
+    uint32_t ntiles;
+    uint32_t out_total;   // points handed to the level kernel
+    uint32_t fin_total;   // points handed to the finisher
+    uint32_t nleaf;
+    uint32_t pad;
+};
+
+// Look-back payload of the planner scan.
+struct PlanAgg {
+    uint32_t nseg, nfin, ntiles, out, fin, leaf;
+};
+
+__device__ __forceinline__ void pl_clear(PlanAgg& a) {
+    a.nseg = a.nfin = a.ntiles = a.out = a.fin = a.leaf = 0;
+}
+__device__ __forceinline__ void pl_combine(PlanAgg& a, const PlanAgg& b) {
+    a.nseg += b.nseg;
+    a.nfin += b.nfin;
+    a.ntiles += b.ntiles;
+    a.out += b.out;
+    a.fin += b.fin;
+    a.leaf += b.leaf;
+}
+__device__ __forceinline__ void pl_store(PlanAgg* d, const PlanAgg& a) { *d = a; }
+__device__ __forceinline__ PlanAgg pl_load(const PlanAgg* s) {
+    PlanAgg a;
+    a.nseg = __ldcg(&s->nseg);
+    a.nfin = __ldcg(&s->nfin);
+    a.ntiles = __ldcg(&s->ntiles);
+    a.out = __ldcg(&s->out);
+    a.fin = __ldcg(&s->fin);
+    a.leaf = __ldcg(&s->leaf);
+    return a;
+}
+__device__ __forceinline__ PlanAgg pl_shfl(const PlanAgg& a, int x) {
+    PlanAgg o;
+    o.nseg = __shfl_xor_sync(kFull, a.nseg, x);
+    o.nfin = __shfl_xor_sync(kFull, a.nfin, x);
+    o.ntiles = __shfl_xor_sync(kFull, a.ntiles, x);
+    o.out = __shfl_xor_sync(kFull, a.out, x);
+    o.fin = __shfl_xor_sync(kFull, a.fin, x);
+    o.leaf = __shfl_xor_sync(kFull, a.leaf, x);
+    return o;
+}
+
+}  // namespace vqb

@@ -1,0 +1,1221 @@
+// sm_100a kernels of the VQhull hot path (see DESIGN.md for the roofline of
+// each one).  Reference behaviour each kernel reproduces is cited inline.
+//
+//   K1  extremes_kernel         find_extremes            geometry.cpp:7-36
+//   KA  bootstrap_argmax_kernel bootstrap pass p,q,p     hull.cpp:228-235 (+ finiteness check vqhull_c.cpp:32-34)
+//   KB  root_partition_kernel   levels 1+2 fused: the bootstrap split AND the
+//                               two child partitions in ONE pass over the input
+//   K2  level_kernel            extract_blocks (fused classify + two-sided
+//                               compaction + arg-max), all live segments of a
+//                               level in one launch       extract_core.hpp:421-515
+//   K3  planner_kernel          recursion driver: child -> segment/finisher
+//                               tables, tile offsets       hull.cpp:78-115
+//   K3' finisher_kernel         whole subtrees of small segments, one warp each
+//                               (explicit stack)           hull.cpp:119-190
+//   K4  size/emit kernels       in-order chain assembly    hull.cpp:59-73, 259-266
+#include <cfloat>
+#include <cstdint>
+
+#include "common.cuh"
+#include "hull_types.cuh"
+#include "kernels.h"
+
+namespace vqb {
+
+
+// ===========================================================================
+// K1: extremes.  lo = lexicographic min of (x, y, index); hi = max x, then
+// max y, then min index.  y is read only on x ties, exactly like the
+// reference scan; the (x, y, index) total order makes the grid reduction
+// independent of the visiting order.
+// ===========================================================================
+struct ExtKey {
+    double x, y;
+    uint32_t idx;
+    uint32_t valid;
+};
+
+__device__ __forceinline__ bool lo_better(const ExtKey& a, const ExtKey& b) {
+    if (!a.valid) return false;
+    if (!b.valid) return true;
+    if (a.x != b.x) return a.x < b.x;
+    if (a.y != b.y) return a.y < b.y;
+    return a.idx < b.idx;
+}
+__device__ __forceinline__ bool hi_better(const ExtKey& a, const ExtKey& b) {
+    if (!a.valid) return false;
+    if (!b.valid) return true;
+    if (a.x != b.x) return a.x > b.x;
+    if (a.y != b.y) return a.y > b.y;
+    return a.idx < b.idx;
+}
+__device__ __forceinline__ ExtKey shfl_key(const ExtKey& k, int x) {
+    ExtKey o;
+    o.x = __shfl_xor_sync(kFull, k.x, x);
+    o.y = __shfl_xor_sync(kFull, k.y, x);
+    o.idx = __shfl_xor_sync(kFull, k.idx, x);
+    o.valid = __shfl_xor_sync(kFull, k.valid, x);
+    return o;
+}
+
+struct ExtPartial {
+    ExtKey lo, hi;
+};
+
+__global__ void __launch_bounds__(256) extremes_kernel(const double* __restrict__ xs,
+                                                       const double* __restrict__ ys,
+                                                       uint64_t n, ExtPartial* partials,
+                                                       uint32_t* ticket, RootInfo* root) {
+    // per-thread running extremes; y of the incumbent is fetched lazily
+    double lo_x = 0, hi_x = 0, lo_y = 0, hi_y = 0;
+    uint32_t lo_i = 0xffffffffu, hi_i = 0xffffffffu;
+    bool lo_yk = false, hi_yk = false;
+    const uint64_t tid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    auto visit = [&](uint64_t i, double x) {
+        if (lo_i == 0xffffffffu || x < lo_x) {
+            lo_x = x;
+            lo_i = uint32_t(i);
+            lo_yk = false;
+        } else if (x == lo_x) {
+            if (!lo_yk) { lo_y = ys[lo_i]; lo_yk = true; }
+            const double y = ys[i];
+            if (y < lo_y) { lo_y = y; lo_i = uint32_t(i); }
+        }
+        if (hi_i == 0xffffffffu || x > hi_x) {
+            hi_x = x;
+            hi_i = uint32_t(i);
+            hi_yk = false;
+        } else if (x == hi_x) {
+            if (!hi_yk) { hi_y = ys[hi_i]; hi_yk = true; }
+            const double y = ys[i];
+            if (y > hi_y) { hi_y = y; hi_i = uint32_t(i); }
+        }
+    };
+    const bool vec = (reinterpret_cast<uintptr_t>(xs) & 15u) == 0;
+    if (vec) {
+        const uint64_t npair = n / 2;
+        const double2* x2 = reinterpret_cast<const double2*>(xs);
+        uint64_t j = tid;
+        for (; j + 3 * stride < npair; j += 4 * stride) {
+            double2 v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) v[u] = __ldcs(&x2[j + u * stride]);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                visit(2 * (j + u * stride), v[u].x);
+                visit(2 * (j + u * stride) + 1, v[u].y);
+            }
+        }
+        for (; j < npair; j += stride) {
+            const double2 v = __ldcs(&x2[j]);
+            visit(2 * j, v.x);
+            visit(2 * j + 1, v.y);
+        }
+        if ((n & 1) && tid == 0) visit(n - 1, xs[n - 1]);
+    } else {
+        for (uint64_t i = tid; i < n; i += stride) visit(i, xs[i]);
+    }
+    ExtKey lo{lo_x, 0.0, lo_i, lo_i != 0xffffffffu};
+    ExtKey hi{hi_x, 0.0, hi_i, hi_i != 0xffffffffu};
+    if (lo.valid) lo.y = lo_yk ? lo_y : ys[lo_i];
+    if (hi.valid) hi.y = hi_yk ? hi_y : ys[hi_i];
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) {
+        ExtKey a = shfl_key(lo, s);
+        if (lo_better(a, lo)) lo = a;
+        ExtKey b = shfl_key(hi, s);
+        if (hi_better(b, hi)) hi = b;
+    }
+    __shared__ ExtKey s_lo[8], s_hi[8];
+    __shared__ bool s_last;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) { s_lo[warp] = lo; s_hi[warp] = hi; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < int(blockDim.x >> 5); ++w) {
+            if (lo_better(s_lo[w], lo)) lo = s_lo[w];
+            if (hi_better(s_hi[w], hi)) hi = s_hi[w];
+        }
+        partials[blockIdx.x].lo = lo;
+        partials[blockIdx.x].hi = hi;
+        __threadfence();
+        const uint32_t t = atomicAdd(ticket, 1u);
+        s_last = (t == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!s_last) return;
+    // last block: reduce the partials
+    __threadfence();
+    ExtKey L, H;
+    L.valid = H.valid = 0;
+    for (uint32_t b = threadIdx.x; b < gridDim.x; b += blockDim.x) {
+        ExtKey a, c;
+        a.x = __ldcg(&partials[b].lo.x); a.y = __ldcg(&partials[b].lo.y);
+        a.idx = __ldcg(&partials[b].lo.idx); a.valid = __ldcg(&partials[b].lo.valid);
+        c.x = __ldcg(&partials[b].hi.x); c.y = __ldcg(&partials[b].hi.y);
+        c.idx = __ldcg(&partials[b].hi.idx); c.valid = __ldcg(&partials[b].hi.valid);
+        if (lo_better(a, L)) L = a;
+        if (hi_better(c, H)) H = c;
+    }
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) {
+        ExtKey a = shfl_key(L, s);
+        if (lo_better(a, L)) L = a;
+        ExtKey b = shfl_key(H, s);
+        if (hi_better(b, H)) H = b;
+    }
+    __syncthreads();
+    if (lane == 0) { s_lo[warp] = L; s_hi[warp] = H; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < int(blockDim.x >> 5); ++w) {
+            if (lo_better(s_lo[w], L)) L = s_lo[w];
+            if (hi_better(s_hi[w], H)) H = s_hi[w];
+        }
+        root->p_idx = L.idx;
+        root->q_idx = H.idx;
+        root->px = L.x;
+        root->py = L.y;
+        root->qx = H.x;
+        root->qy = H.y;
+        *ticket = 0;  // re-arm for the next launch
+    }
+}
+
+// ===========================================================================
+// KA: bootstrap arg-max.  One read-only pass: which side of p->q / q->p each
+// point falls on, |S1|, |S2|, and r1/r2 in the canonical order.  No writes:
+// the split itself is recomputed (fused with the next level) by KB.
+// Also folds in vqhull_compute's finiteness check (vqhull_c.cpp:32-34).
+// ===========================================================================
+struct RootPartial {
+    uint32_t cnt1, cnt2, nonfinite, pad;
+    Best b1, b2;
+};
+
+__global__ void __launch_bounds__(256) bootstrap_argmax_kernel(
+    const double* __restrict__ xs, const double* __restrict__ ys, uint64_t n,
+    RootPartial* partials, uint32_t* ticket, RootInfo* root) {
+    const double px = root->px, py = root->py, qx = root->qx, qy = root->qy;
+    // frames of edge a = p->q and edge b = q->p (kernels.hpp:23-25)
+    const double adx = dsub(qx, px), ady = dsub(qy, py);
+    const double bdx = dsub(px, qx), bdy = dsub(py, qy);
+    uint32_t c1 = 0, c2 = 0, bad = 0;
+    Best b1 = best_none(), b2 = best_none();
+    auto visit = [&](uint64_t i, double ux, double uy) {
+        bad |= !(isfinite(ux) && isfinite(uy));
+        const double A = dsub(px, ux), B = dsub(py, uy);
+        const double Cc = dsub(qx, ux), D = dsub(qy, uy);
+        // left of p->q: A*D > B*C ; left of q->p: C*B > D*A (same products)
+        const double t1 = dmul(A, D), t2 = dmul(B, Cc);
+        const bool la = t1 > t2;
+        const bool lb = !la && (t2 > t1);
+        c1 += la;
+        c2 += lb;
+        if (la | lb) {
+            const double off = la ? lat_off(adx, ady, ux, uy) : lat_off(bdx, bdy, ux, uy);
+            if (la) consider(b1, true, off, ux, uy, uint32_t(i));
+            else consider(b2, true, off, ux, uy, uint32_t(i));
+        }
+    };
+    const uint64_t tid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    const bool vec = ((reinterpret_cast<uintptr_t>(xs) | reinterpret_cast<uintptr_t>(ys)) & 15u) == 0;
+    if (vec) {
+        const uint64_t npair = n / 2;
+        const double2* x2 = reinterpret_cast<const double2*>(xs);
+        const double2* y2 = reinterpret_cast<const double2*>(ys);
+        uint64_t j = tid;
+        for (; j + 3 * stride < npair; j += 4 * stride) {
+            double2 vx[4], vy[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                vx[u] = __ldcs(&x2[j + u * stride]);
+                vy[u] = __ldcs(&y2[j + u * stride]);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                visit(2 * (j + u * stride), vx[u].x, vy[u].x);
+                visit(2 * (j + u * stride) + 1, vx[u].y, vy[u].y);
+            }
+        }
+        for (; j < npair; j += stride) {
+            const double2 vx = __ldcs(&x2[j]);
+            const double2 vy = __ldcs(&y2[j]);
+            visit(2 * j, vx.x, vy.x);
+            visit(2 * j + 1, vx.y, vy.y);
+        }
+        if ((n & 1) && tid == 0) visit(n - 1, xs[n - 1], ys[n - 1]);
+    } else {
+        for (uint64_t i = tid; i < n; i += stride) visit(i, xs[i], ys[i]);
+    }
+    // block reduction
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) {
+        c1 += __shfl_xor_sync(kFull, c1, s);
+        c2 += __shfl_xor_sync(kFull, c2, s);
+        bad |= __shfl_xor_sync(kFull, bad, s);
+    }
+    b1 = warp_best(b1);
+    b2 = warp_best(b2);
+    __shared__ RootPartial s_p[8];
+    __shared__ bool s_last;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) {
+        s_p[warp].cnt1 = c1;
+        s_p[warp].cnt2 = c2;
+        s_p[warp].nonfinite = bad;
+        s_p[warp].b1 = b1;
+        s_p[warp].b2 = b2;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        RootPartial r = s_p[0];
+        for (int w = 1; w < int(blockDim.x >> 5); ++w) {
+            r.cnt1 += s_p[w].cnt1;
+            r.cnt2 += s_p[w].cnt2;
+            r.nonfinite |= s_p[w].nonfinite;
+            if (prefer(s_p[w].b1, r.b1)) r.b1 = s_p[w].b1;
+            if (prefer(s_p[w].b2, r.b2)) r.b2 = s_p[w].b2;
+        }
+        partials[blockIdx.x] = r;
+        __threadfence();
+        const uint32_t t = atomicAdd(ticket, 1u);
+        s_last = (t == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    if (warp != 0) return;
+    uint32_t C1 = 0, C2 = 0, BAD = 0;
+    Best B1 = best_none(), B2 = best_none();
+    for (uint32_t b = lane; b < gridDim.x; b += 32) {
+        const RootPartial* p = &partials[b];
+        C1 += __ldcg(&p->cnt1);
+        C2 += __ldcg(&p->cnt2);
+        BAD |= __ldcg(&p->nonfinite);
+        Best x1, x2;
+        x1.off = __ldcg(&p->b1.off); x1.x = __ldcg(&p->b1.x); x1.y = __ldcg(&p->b1.y);
+        x1.idx = __ldcg(&p->b1.idx); x1.valid = __ldcg(&p->b1.valid);
+        x2.off = __ldcg(&p->b2.off); x2.x = __ldcg(&p->b2.x); x2.y = __ldcg(&p->b2.y);
+        x2.idx = __ldcg(&p->b2.idx); x2.valid = __ldcg(&p->b2.valid);
+        if (prefer(x1, B1)) B1 = x1;
+        if (prefer(x2, B2)) B2 = x2;
+    }
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) {
+        C1 += __shfl_xor_sync(kFull, C1, s);
+        C2 += __shfl_xor_sync(kFull, C2, s);
+        BAD |= __shfl_xor_sync(kFull, BAD, s);
+    }
+    B1 = warp_best(B1);
+    B2 = warp_best(B2);
+    if (lane == 0) {
+        root->cnt1 = C1;
+        root->cnt2 = C2;
+        root->nonfinite = BAD;
+        root->r1 = B1;
+        root->r2 = B2;
+        *ticket = 0;
+    }
+}
+
+// ===========================================================================
+// Tile pipeline shared by KB (4 classes) and K2 (2 classes): per-warp ballot
+// ranks, block scan of the per-(item, warp) counts, staging of the survivors
+// in shared memory in input order, look-back for the tile's offsets inside
+// its segment, then coalesced two-sided stores (class c forward from its base
+// or backward from its base, the reference's S1-from-the-left /
+// S2-from-the-right layout, extract.hpp:14-18).
+// ===========================================================================
+template <int NC>
+struct TileSmem {
+    double sx[kTile];
+    double sy[kTile];
+    uint32_t sid[kTile];
+    uint32_t wcnt[NC][kItems * kWarps];
+    uint32_t tot[NC];
+    uint32_t cbase[NC + 1];
+    Best wbest[NC][kWarps];
+    Agg<NC> excl;
+    Agg<NC> local;
+    uint32_t tile;
+    uint32_t ntiles;
+    uint32_t seg;
+    uint32_t last_ticket;
+};
+
+// Ranks + staging + block arg-max.  cls[i] == NC means "no class".
+template <int NC>
+__device__ __forceinline__ void stage_tile(TileSmem<NC>& S, const double (&ux)[kItems],
+                                           const double (&uy)[kItems],
+                                           const uint32_t (&uid)[kItems],
+                                           const int (&cls)[kItems], Best (&best)[NC]) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const unsigned lt = lanemask_lt();
+    uint32_t rk[kItems];
+#pragma unroll
+    for (int i = 0; i < kItems; ++i) {
+        rk[i] = 0;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+            const unsigned bal = __ballot_sync(kFull, cls[i] == c);
+            if (lane == 0) S.wcnt[c][i * kWarps + warp] = __popc(bal);
+            if (cls[i] == c) rk[i] = __popc(bal & lt);
+        }
+    }
+    // block arg-max per class
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        const Best b = warp_best(best[c]);
+        if (lane == 0) S.wbest[c][warp] = b;
+    }
+    __syncthreads();
+    if (warp < NC) {
+        const int c = warp;
+        const uint32_t v0 = S.wcnt[c][2 * lane], v1 = S.wcnt[c][2 * lane + 1];
+        uint32_t s = v0 + v1;
+        uint32_t incl = s;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t o = __shfl_up_sync(kFull, incl, d);
+            if (lane >= d) incl += o;
+        }
+        const uint32_t ex = incl - s;
+        S.wcnt[c][2 * lane] = ex;
+        S.wcnt[c][2 * lane + 1] = ex + v0;
+        if (lane == 31) S.tot[c] = incl;
+        // block best of class c
+        Best b = lane < kWarps ? S.wbest[c][lane] : best_none();
+        b = warp_best(b);
+        if (lane == 0) {
+            S.local.best[c] = b;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t acc = 0;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+            S.cbase[c] = acc;
+            acc += S.tot[c];
+            S.local.cnt[c] = S.tot[c];
+        }
+        S.cbase[NC] = acc;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < kItems; ++i) {
+        const int c = cls[i];
+        if (c < NC) {
+            const uint32_t s = S.cbase[c] + S.wcnt[c][i * kWarps + warp] + rk[i];
+            S.sx[s] = ux[i];
+            S.sy[s] = uy[i];
+            S.sid[s] = uid[i];
+        }
+    }
+}
+
+// After the look-back: stream the staged survivors to their final places.
+// base[c] is the first (fwd) / last (bwd) position of class c in the segment.
+template <int NC>
+__device__ __forceinline__ void flush_tile(const TileSmem<NC>& S, const uint64_t (&base)[NC],
+                                           const bool (&fwd)[NC], double* __restrict__ ox,
+                                           double* __restrict__ oy, uint32_t* __restrict__ oid) {
+    const uint32_t total = S.cbase[NC];
+    for (uint32_t e = threadIdx.x; e < total; e += kThreads) {
+        int c = 0;
+#pragma unroll
+        for (int k = 1; k < NC; ++k) c += (e >= S.cbase[k]);
+        const uint64_t r = uint64_t(S.excl.cnt[c]) + (e - S.cbase[c]);
+        const uint64_t pos = fwd[c] ? base[c] + r : base[c] - r;
+        ox[pos] = S.sx[e];
+        oy[pos] = S.sy[e];
+        oid[pos] = S.sid[e];
+    }
+}
+
+// Claim the next tile (in increasing order — required by the look-back).
+// Returns false when the launch is drained; the last CTA to drain re-arms
+// the counter for the next launch.
+template <int NC>
+__device__ __forceinline__ bool claim_tile(TileSmem<NC>& S, uint32_t* ctr, uint32_t ntiles) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const uint32_t t = atomicAdd(ctr, 1u);
+        S.tile = t;
+        if (t >= ntiles && t == ntiles + gridDim.x - 1) *ctr = 0;
+    }
+    __syncthreads();
+    return S.tile < ntiles;
+}
+
+// ===========================================================================
+// KB: root partition — hull levels 1 and 2 fused (probe P5).
+// Each input point is classified against the bootstrap edges p->q / q->p and
+// then against its side's two child edges, with the reference's
+// mask_b &= ~mask_a rule at both levels (kernels.hpp:91):
+//   class 0: S1 ∧ left(p->r1)        class 1: S1 ∧ ¬0 ∧ left(r1->q)
+//   class 2: S2 ∧ left(q->r2)        class 3: S2 ∧ ¬2 ∧ left(r2->p)
+// These are exactly the sets the reference's second-level extract_subsets
+// calls produce; r11..r22 come out of the same pass (fused arg-max).
+// Output layout: S1's range [0,|S1|) and S2's range [|S1|, |S1|+|S2|) of the
+// destination, each split two-sided like the reference's in-place pass.
+// ===========================================================================
+struct RootArgs {
+    const double* xs;
+    const double* ys;
+    uint64_t n;
+    const RootInfo* root;
+    double* ox;
+    double* oy;
+    uint32_t* oid;
+    uint32_t* flags;
+    Agg<4>* aggs;
+    Agg<4>* incs;
+    uint32_t epoch;
+    uint32_t* ctr;
+    ChildRec* children;  // 4 slots
+    uint32_t ntiles;
+};
+
+__global__ void __launch_bounds__(kThreads, 1) root_partition_kernel(RootArgs a) {
+    __shared__ TileSmem<4> S;
+    const RootInfo& R = *a.root;
+    const double px = R.px, py = R.py, qx = R.qx, qy = R.qy;
+    const double r1x = R.r1.x, r1y = R.r1.y, r2x = R.r2.x, r2y = R.r2.y;
+    const uint32_t n1 = R.cnt1, n2 = R.cnt2;
+    // child frames (kernels.hpp:23-25): 0: p->r1, 1: r1->q, 2: q->r2, 3: r2->p
+    double fdx[4], fdy[4];
+    fdx[0] = dsub(r1x, px); fdy[0] = dsub(r1y, py);
+    fdx[1] = dsub(qx, r1x); fdy[1] = dsub(qy, r1y);
+    fdx[2] = dsub(r2x, qx); fdy[2] = dsub(r2y, qy);
+    fdx[3] = dsub(px, r2x); fdy[3] = dsub(py, r2y);
+    uint64_t base[4];
+    bool fwd[4] = {true, false, true, false};
+    base[0] = 0;
+    base[1] = uint64_t(n1) - 1;  // unused when empty
+    base[2] = n1;
+    base[3] = uint64_t(n1) + n2 - 1;
+
+    while (claim_tile(S, a.ctr, a.ntiles)) {
+        const uint32_t t = S.tile;
+        const uint64_t start = uint64_t(t) * kTile;
+        double ux[kItems], uy[kItems];
+        uint32_t uid[kItems];
+        int cls[kItems];
+        Best best[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) best[c] = best_none();
+#pragma unroll
+        for (int i = 0; i < kItems; ++i) {
+            const uint64_t pos = start + uint64_t(i) * kThreads + threadIdx.x;
+            const bool v = pos < a.n;
+            ux[i] = v ? ld_stream(a.xs + pos) : 0.0;
+            uy[i] = v ? ld_stream(a.ys + pos) : 0.0;
+            uid[i] = uint32_t(pos);
+            cls[i] = v ? 0 : 4;
+        }
+#pragma unroll
+        for (int i = 0; i < kItems; ++i) {
+            const double u = ux[i], w = uy[i];
+            const double A = dsub(px, u), B = dsub(py, w);
+            const double Cc = dsub(qx, u), D = dsub(qy, w);
+            const double t1 = dmul(A, D), t2 = dmul(B, Cc);
+            const bool s1 = t1 > t2;          // left of p->q
+            const bool s2 = !s1 && (t2 > t1); // left of q->p
+            // second level, side-selected operands
+            const double rx = s1 ? r1x : r2x, ry = s1 ? r1y : r2y;
+            const double P1x = s1 ? A : Cc, P1y = s1 ? B : D;
+            const double Q2x = s1 ? Cc : A, Q2y = s1 ? D : B;
+            const double E = dsub(rx, u), F = dsub(ry, w);
+            const bool L = left_diff(P1x, P1y, E, F);       // left of (side start -> r)
+            const bool Rr = !L && left_diff(E, F, Q2x, Q2y); // left of (r -> side end)
+            int c = 4;
+            if (s1) c = L ? 0 : (Rr ? 1 : 4);
+            else if (s2) c = L ? 2 : (Rr ? 3 : 4);
+            if (cls[i] != 0) c = 4;  // out of range
+            cls[i] = c;
+            if (c < 4) {
+                // class frame by select (no dynamically indexed local array)
+                const double edx = c == 0 ? fdx[0] : (c == 1 ? fdx[1] : (c == 2 ? fdx[2] : fdx[3]));
+                const double edy = c == 0 ? fdy[0] : (c == 1 ? fdy[1] : (c == 2 ? fdy[2] : fdy[3]));
+                const double off = lat_off(edx, edy, u, w);
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (k == c) consider(best[k], true, off, u, w, uid[i]);
+            }
+        }
+        stage_tile<4>(S, ux, uy, uid, cls, best);
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            const Agg<4> ex = lookback<Agg<4>>(t, 0u, S.local, a.flags, a.aggs, a.incs, a.epoch);
+            if (threadIdx.x == 0) {
+                S.excl = ex;
+                if (t == a.ntiles - 1) {
+                    Agg<4> inc = ex;
+                    agg_combine(inc, S.local);
+                    // children slots: (p, r11, r1) (r1, r12, q) (q, r21, r2) (r2, r22, p)
+                    const double tri[4][4] = {{px, py, r1x, r1y}, {r1x, r1y, qx, qy},
+                                              {qx, qy, r2x, r2y}, {r2x, r2y, px, py}};
+                    for (int c = 0; c < 4; ++c) {
+                        ChildRec ch;
+                        ch.px = tri[c][0];
+                        ch.py = tri[c][1];
+                        ch.qx = tri[c][2];
+                        ch.qy = tri[c][3];
+                        ch.rx = inc.best[c].x;
+                        ch.ry = inc.best[c].y;
+                        ch.r_idx = inc.best[c].idx;
+                        ch.m = inc.cnt[c];
+                        ch.begin = fwd[c] ? base[c] : base[c] + 1 - inc.cnt[c];
+                        a.children[c] = ch;
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        flush_tile<4>(S, base, fwd, a.ox, a.oy, a.oid);
+    }
+}
+
+// ===========================================================================
+// K2: level kernel — the fused partition (extract_blocks) for every live
+// segment of one recursion level in ONE launch.  Tiles never straddle
+// segments; a segment's tiles are consecutive ids, so the decoupled
+// look-back runs inside the segment and its last tile knows the segment's
+// final counts and arg-maxes and emits the two child nodes.
+// GENERAL = two unrelated edges (the extract_subsets API); otherwise edges
+// p->r and r->q share r, which saves two subtractions per point.
+// ===========================================================================
+struct LevelArgs {
+    const SegRec* segs;
+    const uint32_t* tile_seg;
+    const LevelInfo* info;
+    const double* ix;
+    const double* iy;
+    const uint32_t* iid;
+    double* ox;
+    double* oy;
+    uint32_t* oid;
+    uint32_t* flags;
+    Agg<2>* aggs;
+    Agg<2>* incs;
+    uint32_t epoch;
+    uint32_t* ctr;
+    ChildRec* children;  // 2 per segment
+};
+
+template <bool GENERAL>
+__global__ void __launch_bounds__(kThreads, 1) level_kernel(LevelArgs a) {
+    __shared__ TileSmem<2> S;
+    __shared__ SegRec s_seg;
+    if (threadIdx.x == 0) S.ntiles = a.info->ntiles;
+    __syncthreads();
+    const uint32_t ntiles = S.ntiles;
+    while (claim_tile(S, a.ctr, ntiles)) {
+        const uint32_t t = S.tile;
+        if (threadIdx.x == 0) {
+            S.seg = a.tile_seg[t];
+            s_seg = a.segs[S.seg];
+        }
+        __syncthreads();
+        const SegRec& g = s_seg;
+        const uint32_t j = t - g.tile0;
+        const uint64_t start = g.begin + uint64_t(j) * kTile;
+        const uint32_t cnt = min(uint32_t(kTile), g.m - j * uint32_t(kTile));
+        double ux[kItems], uy[kItems];
+        uint32_t uid[kItems];
+        int cls[kItems];
+        Best best[2] = {best_none(), best_none()};
+#pragma unroll
+        for (int i = 0; i < kItems; ++i) {
+            const uint32_t r = uint32_t(i) * kThreads + threadIdx.x;
+            const bool v = r < cnt;
+            ux[i] = v ? ld_stream(a.ix + start + r) : 0.0;
+            uy[i] = v ? ld_stream(a.iy + start + r) : 0.0;
+            uid[i] = v ? ld_stream(a.iid + start + r) : 0u;
+            cls[i] = v ? 0 : 2;
+        }
+        const double px = g.px, py = g.py, rx = g.rx, ry = g.ry, qx = g.qx, qy = g.qy;
+#pragma unroll
+        for (int i = 0; i < kItems; ++i) {
+            const double u = ux[i], w = uy[i];
+            bool la, lb;
+            if (GENERAL) {
+                la = left_diff(dsub(px, u), dsub(py, w), dsub(rx, u), dsub(ry, w));
+                lb = !la && left_diff(dsub(g.bx, u), dsub(g.by, w), dsub(qx, u), dsub(qy, w));
+            } else {
+                const double A = dsub(px, u), B = dsub(py, w);
+                const double E = dsub(rx, u), F = dsub(ry, w);
+                const double Cc = dsub(qx, u), D = dsub(qy, w);
+                la = left_diff(A, B, E, F);
+                lb = !la && left_diff(E, F, Cc, D);
+            }
+            const int c = (cls[i] != 0) ? 2 : (la ? 0 : (lb ? 1 : 2));
+            cls[i] = c;
+            if (c < 2) {
+                const double off = c == 0 ? lat_off(g.adx, g.ady, u, w) : lat_off(g.bdx, g.bdy, u, w);
+                if (c == 0) consider(best[0], true, off, u, w, uid[i]);
+                else consider(best[1], true, off, u, w, uid[i]);
+            }
+        }
+        stage_tile<2>(S, ux, uy, uid, cls, best);
+        __syncthreads();
+        const uint64_t base[2] = {g.out, g.out + g.m - 1};
+        const bool fwd[2] = {true, false};
+        if (threadIdx.x < 32) {
+            const Agg<2> ex =
+                lookback<Agg<2>>(t, g.tile0, S.local, a.flags, a.aggs, a.incs, a.epoch);
+            if (threadIdx.x == 0) {
+                S.excl = ex;
+                if (j == g.ntiles - 1) {
+                    Agg<2> inc = ex;
+                    agg_combine(inc, S.local);
+                    ChildRec L, Rr;
+                    L.px = px; L.py = py; L.qx = rx; L.qy = ry;
+                    L.rx = inc.best[0].x; L.ry = inc.best[0].y;
+                    L.r_idx = inc.best[0].idx; L.m = inc.cnt[0]; L.begin = g.out;
+                    Rr.px = GENERAL ? g.bx : rx; Rr.py = GENERAL ? g.by : ry; Rr.qx = qx; Rr.qy = qy;
+                    Rr.rx = inc.best[1].x; Rr.ry = inc.best[1].y;
+                    Rr.r_idx = inc.best[1].idx; Rr.m = inc.cnt[1];
+                    Rr.begin = g.out + g.m - inc.cnt[1];
+                    a.children[2 * S.seg] = L;
+                    a.children[2 * S.seg + 1] = Rr;
+                }
+            }
+        }
+        __syncthreads();
+        flush_tile<2>(S, base, fwd, a.ox, a.oy, a.oid);
+    }
+}
+
+// ===========================================================================
+// K3: planner — turns the child slots of a level into the next level's work:
+// internal segments (m > kFinMax, tiled), finisher segments (2..kFinMax),
+// leaves (m == 1: the node's chain is just its apex, hull.cpp:83) and empty
+// slots.  One single-pass scan with decoupled look-back over slot chunks.
+// ===========================================================================
+constexpr int kPlanPer = 4;
+constexpr int kPlanChunk = kThreads * kPlanPer;
+
+struct PlanArgs {
+    const ChildRec* slots;
+    uint32_t nslots;
+    uint32_t nchunks;
+    SegRec* segs;
+    FinRec* fins;
+    uint8_t* kind;
+    uint32_t* link;
+    LevelInfo* info;
+    uint64_t fin_chain_base;  // global offset of this level's finisher chains
+    uint32_t* flags;
+    PlanAgg* aggs;
+    PlanAgg* incs;
+    uint32_t epoch;
+    uint32_t* ctr;
+};
+
+__device__ __forceinline__ uint8_t kind_of(uint32_t m) {
+    return m == 0 ? kEmpty : (m == 1 ? kLeaf : (m <= kFinMax ? kFin : kInternal));
+}
+
+__global__ void __launch_bounds__(kThreads) planner_kernel(PlanArgs a) {
+    __shared__ PlanAgg s_w[kWarps];
+    __shared__ PlanAgg s_excl;
+    __shared__ uint32_t s_chunk;
+    while (true) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const uint32_t c = atomicAdd(a.ctr, 1u);
+            s_chunk = c;
+            if (c >= a.nchunks && c == a.nchunks + gridDim.x - 1) *a.ctr = 0;
+        }
+        __syncthreads();
+        const uint32_t chunk = s_chunk;
+        if (chunk >= a.nchunks) break;
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        // blocked: thread owns kPlanPer consecutive slots
+        const uint64_t s0 = uint64_t(chunk) * kPlanChunk + uint64_t(threadIdx.x) * kPlanPer;
+        uint32_t m[kPlanPer];
+        PlanAgg mine;
+        pl_clear(mine);
+#pragma unroll
+        for (int k = 0; k < kPlanPer; ++k) {
+            const uint64_t s = s0 + k;
+            m[k] = s < a.nslots ? a.slots[s].m : 0u;
+            const uint8_t kd = s < a.nslots ? kind_of(m[k]) : kEmpty;
+            mine.nseg += kd == kInternal;
+            mine.nfin += kd == kFin;
+            mine.leaf += kd == kLeaf;
+            mine.ntiles += kd == kInternal ? (m[k] + kTile - 1) / kTile : 0;
+            mine.out += kd == kInternal ? m[k] : 0;
+            mine.fin += kd == kFin ? m[k] : 0;
+        }
+        // block exclusive scan (warp inclusive scan, then warp totals)
+        PlanAgg incl = mine;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            PlanAgg o;
+            o.nseg = __shfl_up_sync(kFull, incl.nseg, d);
+            o.nfin = __shfl_up_sync(kFull, incl.nfin, d);
+            o.ntiles = __shfl_up_sync(kFull, incl.ntiles, d);
+            o.out = __shfl_up_sync(kFull, incl.out, d);
+            o.fin = __shfl_up_sync(kFull, incl.fin, d);
+            o.leaf = __shfl_up_sync(kFull, incl.leaf, d);
+            if (lane >= d) pl_combine(incl, o);
+        }
+        if (lane == 31) s_w[warp] = incl;
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            PlanAgg tot;
+            pl_clear(tot);
+            for (int w = 0; w < kWarps; ++w) pl_combine(tot, s_w[w]);
+            const PlanAgg ex = lookback<PlanAgg>(chunk, 0u, tot, a.flags, a.aggs, a.incs, a.epoch);
+            if (threadIdx.x == 0) {
+                s_excl = ex;
+                if (chunk == a.nchunks - 1) {
+                    PlanAgg all = ex;
+                    pl_combine(all, tot);
+                    LevelInfo li;
+                    li.nslots = a.nslots;
+                    li.nseg = all.nseg;
+                    li.nfin = all.nfin;
+                    li.ntiles = all.ntiles;
+                    li.out_total = all.out;
+                    li.fin_total = all.fin;
+                    li.nleaf = all.leaf;
+                    li.pad = 0;
+                    *a.info = li;
+                }
+            }
+        }
+        __syncthreads();
+        PlanAgg run = s_excl;
+        for (int w = 0; w < warp; ++w) pl_combine(run, s_w[w]);
+        // exclusive within warp
+        PlanAgg wex = incl;
+        wex.nseg -= mine.nseg; wex.nfin -= mine.nfin; wex.ntiles -= mine.ntiles;
+        wex.out -= mine.out; wex.fin -= mine.fin; wex.leaf -= mine.leaf;
+        pl_combine(run, wex);
+#pragma unroll
+        for (int k = 0; k < kPlanPer; ++k) {
+            const uint64_t s = s0 + k;
+            if (s >= a.nslots) break;
+            const uint8_t kd = kind_of(m[k]);
+            a.kind[s] = kd;
+            if (kd == kInternal) {
+                const ChildRec c = a.slots[s];
+                SegRec g;
+                g.px = c.px; g.py = c.py; g.rx = c.rx; g.ry = c.ry; g.qx = c.qx; g.qy = c.qy;
+                g.bx = c.rx; g.by = c.ry;
+                g.adx = dsub(c.rx, c.px); g.ady = dsub(c.ry, c.py);
+                g.bdx = dsub(c.qx, c.rx); g.bdy = dsub(c.qy, c.ry);
+                g.begin = c.begin;
+                g.out = run.out;
+                g.m = c.m;
+                g.tile0 = run.ntiles;
+                g.ntiles = (c.m + kTile - 1) / kTile;
+                g.slot = uint32_t(s);
+                a.segs[run.nseg] = g;
+                a.link[s] = run.nseg;
+                run.nseg += 1;
+                run.ntiles += g.ntiles;
+                run.out += c.m;
+            } else if (kd == kFin) {
+                FinRec f;
+                f.c = a.slots[s];
+                f.chain_base = a.fin_chain_base + run.fin;
+                f.slot = uint32_t(s);
+                f.pad = 0;
+                a.fins[run.nfin] = f;
+                a.link[s] = run.nfin;
+                run.nfin += 1;
+                run.fin += m[k];
+            } else {
+                a.link[s] = 0;
+                run.leaf += (kd == kLeaf);
+            }
+        }
+    }
+}
+
+// tile -> segment map (binary search over the segments' first tiles)
+__global__ void tilemap_kernel(const SegRec* segs, const LevelInfo* info, uint32_t* tile_seg) {
+    const uint32_t nseg = info->nseg, ntiles = info->ntiles;
+    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < ntiles;
+         t += gridDim.x * blockDim.x) {
+        uint32_t lo = 0, hi = nseg;  // find last k with tile0 <= t
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (segs[mid].tile0 <= t) lo = mid; else hi = mid;
+        }
+        tile_seg[t] = lo;
+    }
+}
+
+// ===========================================================================
+// K3': warp finisher.  One warp solves the whole subtree of a segment with
+// m <= kFinMax points in shared memory, depth-first with an explicit stack
+// (the reference's chain_iterative, hull.cpp:119-190), emitting the chain
+// in order: chain(L) ++ [r] ++ chain(R)  (assemble_chain, hull.cpp:59-73).
+// Points are referenced by local ids; the two working arrays ping-pong per
+// depth so a child's range never overlaps a pending sibling's.
+// ===========================================================================
+constexpr int kFinWarps = 4;
+
+struct FinFrame {
+    uint16_t lo, hi, p, r, q, rcnt, rR, lcnt;
+    uint8_t buf, phase;
+    uint8_t pad[2];
+};
+
+struct FinSmem {
+    double x[kFinMax + 3];
+    double y[kFinMax + 3];
+    uint32_t gid[kFinMax + 3];
+    uint16_t work[2][kFinMax];
+    FinFrame stack[kFinMax + 2];
+};
+
+__global__ void __launch_bounds__(kFinWarps * 32) finisher_kernel(
+    const FinRec* fins, const LevelInfo* info, const double* __restrict__ ix,
+    const double* __restrict__ iy, const uint32_t* __restrict__ iid, uint32_t* chain,
+    uint32_t* chain_count, uint32_t* fin_count_out) {
+    __shared__ FinSmem SM[kFinWarps];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    FinSmem& S = SM[warp];
+    const unsigned lt = lanemask_lt();
+    const uint32_t nfin = info->nfin;
+    for (uint32_t f = blockIdx.x * kFinWarps + warp; f < nfin; f += gridDim.x * kFinWarps) {
+        const FinRec rec = fins[f];
+        const uint32_t m = rec.c.m;
+        for (uint32_t i = lane; i < m; i += 32) {
+            S.x[i] = ix[rec.c.begin + i];
+            S.y[i] = iy[rec.c.begin + i];
+            S.gid[i] = iid[rec.c.begin + i];
+            S.work[0][i] = uint16_t(i);
+        }
+        const uint16_t P0 = uint16_t(m), Q0 = uint16_t(m + 1), R0 = uint16_t(m + 2);
+        if (lane == 0) {
+            S.x[P0] = rec.c.px; S.y[P0] = rec.c.py; S.gid[P0] = 0xffffffffu;
+            S.x[Q0] = rec.c.qx; S.y[Q0] = rec.c.qy; S.gid[Q0] = 0xffffffffu;
+            S.x[R0] = rec.c.rx; S.y[R0] = rec.c.ry; S.gid[R0] = rec.c.r_idx;
+            FinFrame& fr = S.stack[0];
+            fr.lo = 0; fr.hi = uint16_t(m); fr.p = P0; fr.r = R0; fr.q = Q0;
+            fr.buf = 0; fr.phase = 0; fr.rcnt = 0; fr.rR = 0; fr.lcnt = 0;
+        }
+        __syncwarp();
+        int depth = 1;
+        uint32_t emitted = 0;
+        const uint64_t cbase = rec.chain_base;
+        uint32_t guard = 0;
+        while (depth > 0) {
+            if (++guard > 8 * kFinMax + 64) {  // at most ~3 visits per node
+                if (lane == 0) g_vqb_fault = 2u;
+                break;
+            }
+            FinFrame fr = S.stack[depth - 1];
+            if (fr.phase == 0) {
+                const double px = S.x[fr.p], py = S.y[fr.p];
+                const double rx = S.x[fr.r], ry = S.y[fr.r];
+                const double qx = S.x[fr.q], qy = S.y[fr.q];
+                const double adx = dsub(rx, px), ady = dsub(ry, py);
+                const double bdx = dsub(qx, rx), bdy = dsub(qy, ry);
+                const int src = fr.buf, dst = fr.buf ^ 1;
+                uint32_t nL = 0, nR = 0;
+                Best bL = best_none(), bR = best_none();
+                for (uint32_t b0 = fr.lo; b0 < fr.hi; b0 += 32) {
+                    const uint32_t i = b0 + lane;
+                    const bool v = i < fr.hi;
+                    const uint16_t id = v ? S.work[src][i] : 0;
+                    const double u = S.x[id], w = S.y[id];
+                    const double A = dsub(px, u), B = dsub(py, w);
+                    const double E = dsub(rx, u), F = dsub(ry, w);
+                    const double Cc = dsub(qx, u), D = dsub(qy, w);
+                    const bool la = v && left_diff(A, B, E, F);
+                    const bool lb = v && !la && left_diff(E, F, Cc, D);
+                    const unsigned ba = __ballot_sync(kFull, la);
+                    const unsigned bb = __ballot_sync(kFull, lb);
+                    if (la) {
+                        S.work[dst][fr.lo + nL + __popc(ba & lt)] = id;
+                        Best c;
+                        c.off = lat_off(adx, ady, u, w); c.x = u; c.y = w;
+                        c.idx = S.gid[id]; c.valid = uint32_t(id) + 1u;
+                        if (prefer(c, bL)) bL = c;
+                    }
+                    if (lb) {
+                        S.work[dst][fr.hi - 1 - nR - __popc(bb & lt)] = id;
+                        Best c;
+                        c.off = lat_off(bdx, bdy, u, w); c.x = u; c.y = w;
+                        c.idx = S.gid[id]; c.valid = uint32_t(id) + 1u;
+                        if (prefer(c, bR)) bR = c;
+                    }
+                    nL += __popc(ba);
+                    nR += __popc(bb);
+                }
+                bL = warp_best(bL);
+                bR = warp_best(bR);
+                __syncwarp();
+                if (lane == 0) {
+                    FinFrame& cur = S.stack[depth - 1];
+                    cur.phase = 1;
+                    cur.lcnt = uint16_t(nL);
+                    cur.rcnt = uint16_t(nR);
+                    cur.rR = nR ? uint16_t(bR.valid - 1u) : 0;
+                    if (nL) {
+                        FinFrame& ch = S.stack[depth];
+                        ch.lo = fr.lo; ch.hi = uint16_t(fr.lo + nL);
+                        ch.p = fr.p; ch.r = uint16_t(bL.valid - 1u); ch.q = fr.r;
+                        ch.buf = uint8_t(dst); ch.phase = 0; ch.rcnt = 0; ch.rR = 0; ch.lcnt = 0;
+                    }
+                }
+                __syncwarp();
+                if (nL) ++depth;
+            } else if (fr.phase == 1) {
+                if (lane == 0) {
+                    chain[cbase + emitted] = S.gid[fr.r];
+                    FinFrame& cur = S.stack[depth - 1];
+                    if (fr.rcnt) {
+                        // tail call: the frame is replaced by its right child
+                        cur.lo = uint16_t(fr.hi - fr.rcnt);
+                        cur.p = fr.r; cur.r = fr.rR;  // q unchanged
+                        cur.buf = uint8_t(fr.buf ^ 1); cur.phase = 0;
+                        cur.rcnt = 0; cur.rR = 0; cur.lcnt = 0;
+                    } else {
+                        cur.phase = 2;
+                    }
+                }
+                ++emitted;
+                __syncwarp();
+            } else {
+                --depth;
+                // the parent resumes at phase 1 (its left subtree is done)
+            }
+        }
+        if (lane == 0) fin_count_out[f] = emitted;
+        __syncwarp();
+    }
+    (void)chain_count;
+}
+
+// ===========================================================================
+// K4: in-order emission.  Bottom-up chain sizes, then top-down starts;
+// every node writes its apex between its children's chains.
+// Output = [p] ++ chain(S1) ++ [q if q != p] ++ chain(S2)  (hull.cpp:259-266)
+// ===========================================================================
+__global__ void size_kernel(uint32_t nslots, const uint8_t* kind, const uint32_t* link,
+                            const uint32_t* fin_count, const uint32_t* child_size,
+                            uint32_t* size) {
+    for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < nslots;
+         s += gridDim.x * blockDim.x) {
+        const uint8_t k = kind[s];
+        uint32_t v = 0;
+        if (k == kLeaf) v = 1;
+        else if (k == kFin) v = fin_count[link[s]];
+        else if (k == kInternal) v = 1 + child_size[2 * link[s]] + child_size[2 * link[s] + 1];
+        size[s] = v;
+    }
+}
+
+__global__ void emit_kernel(uint32_t nslots, const uint8_t* kind, const uint32_t* link,
+                            const ChildRec* slots, const FinRec* fins, const uint32_t* fin_count,
+                            const uint32_t* chain, const uint32_t* start,
+                            const uint32_t* child_size, uint32_t* child_start, uint32_t* out) {
+    for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < nslots;
+         s += gridDim.x * blockDim.x) {
+        const uint8_t k = kind[s];
+        const uint32_t st = start[s];
+        if (k == kLeaf) {
+            out[st] = slots[s].r_idx;
+        } else if (k == kInternal) {
+            const uint32_t L = link[s];
+            const uint32_t sl = child_size[2 * L];
+            out[st + sl] = slots[s].r_idx;
+            child_start[2 * L] = st;
+            child_start[2 * L + 1] = st + sl + 1;
+        } else if (k == kFin) {
+            const uint32_t f = link[s];
+            const uint32_t c = fin_count[f];
+            const uint64_t b = fins[f].chain_base;
+            for (uint32_t i = 0; i < c; ++i) out[st + i] = chain[b + i];
+        }
+    }
+}
+
+// Level-1 (root) bookkeeping: the two bootstrap sides as slots, then the
+// final frame [p] S1 [q] S2 once their sizes are known.
+__global__ void root_slots_kernel(const RootInfo* root, ChildRec* slots, uint8_t* kind,
+                                  uint32_t* link) {
+    if (threadIdx.x != 0) return;
+    const RootInfo& R = *root;
+    ChildRec a, b;
+    a.px = R.px; a.py = R.py; a.qx = R.qx; a.qy = R.qy;
+    a.rx = R.r1.x; a.ry = R.r1.y; a.r_idx = R.r1.idx; a.m = R.cnt1; a.begin = 0;
+    b.px = R.qx; b.py = R.qy; b.qx = R.px; b.qy = R.py;
+    b.rx = R.r2.x; b.ry = R.r2.y; b.r_idx = R.r2.idx; b.m = R.cnt2; b.begin = R.cnt1;
+    slots[0] = a;
+    slots[1] = b;
+    // both sides are partitioned by the fused root pass whatever their size
+    kind[0] = R.cnt1 ? kInternal : kEmpty;
+    kind[1] = R.cnt2 ? kInternal : kEmpty;
+    link[0] = 0;
+    link[1] = 1;
+}
+
+__global__ void root_frame_kernel(const RootInfo* root, const uint32_t* size1,
+                                  uint32_t* start1, uint32_t* out, uint32_t* h_out) {
+    if (threadIdx.x != 0) return;
+    const RootInfo& R = *root;
+    const bool q_distinct = !(R.qx == R.px && R.qy == R.py);
+    out[0] = R.p_idx;
+    start1[0] = 1;
+    uint32_t pos = 1 + size1[0];
+    if (q_distinct) out[pos++] = R.q_idx;
+    start1[1] = pos;
+    *h_out = pos + size1[1];
+}
+
+// ===========================================================================
+// Host-side launchers (C++ linkage, used by driver.cu)
+// ===========================================================================
+void launch_extremes(const double* xs, const double* ys, uint64_t n, void* partials,
+                     uint32_t* ticket, RootInfo* root, int grid, cudaStream_t st) {
+    extremes_kernel<<<grid, 256, 0, st>>>(xs, ys, n, static_cast<ExtPartial*>(partials), ticket,
+                                          root);
+}
+
+void launch_bootstrap(const double* xs, const double* ys, uint64_t n, void* partials,
+                      uint32_t* ticket, RootInfo* root, int grid, cudaStream_t st) {
+    bootstrap_argmax_kernel<<<grid, 256, 0, st>>>(xs, ys, n, static_cast<RootPartial*>(partials),
+                                                  ticket, root);
+}
+
+size_t partial_bytes(int grid) {
+    return size_t(grid) * (sizeof(RootPartial) > sizeof(ExtPartial) ? sizeof(RootPartial)
+                                                                      : sizeof(ExtPartial));
+}
+
+void launch_root_partition(const double* xs, const double* ys, uint64_t n, const RootInfo* root,
+                           double* ox, double* oy, uint32_t* oid, uint32_t* flags, void* aggs,
+                           void* incs, uint32_t epoch, uint32_t* ctr, ChildRec* children,
+                           int grid, cudaStream_t st) {
+    RootArgs a;
+    a.xs = xs; a.ys = ys; a.n = n; a.root = root;
+    a.ox = ox; a.oy = oy; a.oid = oid;
+    a.flags = flags; a.aggs = static_cast<Agg<4>*>(aggs); a.incs = static_cast<Agg<4>*>(incs);
+    a.epoch = epoch; a.ctr = ctr; a.children = children;
+    a.ntiles = uint32_t((n + kTile - 1) / kTile);
+    root_partition_kernel<<<grid, kThreads, 0, st>>>(a);
+}
+
+void launch_level(const SegRec* segs, const uint32_t* tile_seg, const LevelInfo* info,
+                  const double* ix, const double* iy, const uint32_t* iid, double* ox, double* oy,
+                  uint32_t* oid, uint32_t* flags, void* aggs, void* incs, uint32_t epoch,
+                  uint32_t* ctr, ChildRec* children, bool general, int grid, cudaStream_t st) {
+    LevelArgs a;
+    a.segs = segs; a.tile_seg = tile_seg; a.info = info;
+    a.ix = ix; a.iy = iy; a.iid = iid; a.ox = ox; a.oy = oy; a.oid = oid;
+    a.flags = flags; a.aggs = static_cast<Agg<2>*>(aggs); a.incs = static_cast<Agg<2>*>(incs);
+    a.epoch = epoch; a.ctr = ctr; a.children = children;
+    if (general) level_kernel<true><<<grid, kThreads, 0, st>>>(a);
+    else level_kernel<false><<<grid, kThreads, 0, st>>>(a);
+}
+
+void launch_planner(const ChildRec* slots, uint32_t nslots, SegRec* segs, FinRec* fins,
+                    uint8_t* kind, uint32_t* link, LevelInfo* info, uint64_t fin_chain_base,
+                    uint32_t* flags, void* aggs, void* incs, uint32_t epoch, uint32_t* ctr,
+                    int max_grid, cudaStream_t st) {
+    PlanArgs a;
+    a.slots = slots; a.nslots = nslots;
+    a.nchunks = (nslots + kPlanChunk - 1) / kPlanChunk;
+    a.segs = segs; a.fins = fins; a.kind = kind; a.link = link; a.info = info;
+    a.fin_chain_base = fin_chain_base;
+    a.flags = flags; a.aggs = static_cast<PlanAgg*>(aggs); a.incs = static_cast<PlanAgg*>(incs);
+    a.epoch = epoch; a.ctr = ctr;
+    int grid = int(a.nchunks < uint32_t(max_grid) ? a.nchunks : uint32_t(max_grid));
+    if (grid < 1) grid = 1;
+    planner_kernel<<<grid, kThreads, 0, st>>>(a);
+}
+
+void launch_tilemap(const SegRec* segs, const LevelInfo* info, uint32_t* tile_seg,
+                    uint32_t ntiles_hint, cudaStream_t st) {
+    uint32_t g = (ntiles_hint + 255) / 256;
+    if (g < 1) g = 1;
+    if (g > 1184) g = 1184;
+    tilemap_kernel<<<g, 256, 0, st>>>(segs, info, tile_seg);
+}
+
+void launch_finisher(const FinRec* fins, const LevelInfo* info, const double* ix,
+                     const double* iy, const uint32_t* iid, uint32_t* chain,
+                     uint32_t* fin_count, uint32_t nfin_hint, int max_grid, cudaStream_t st) {
+    uint32_t g = (nfin_hint + kFinWarps - 1) / kFinWarps;
+    if (g < 1) g = 1;
+    if (g > uint32_t(max_grid)) g = uint32_t(max_grid);
+    finisher_kernel<<<g, kFinWarps * 32, 0, st>>>(fins, info, ix, iy, iid, chain, nullptr,
+                                                  fin_count);
+}
+
+void launch_size(uint32_t nslots, const uint8_t* kind, const uint32_t* link,
+                 const uint32_t* fin_count, const uint32_t* child_size, uint32_t* size,
+                 cudaStream_t st) {
+    uint32_t g = (nslots + 255) / 256;
+    if (g < 1) g = 1;
+    if (g > 1184) g = 1184;
+    size_kernel<<<g, 256, 0, st>>>(nslots, kind, link, fin_count, child_size, size);
+}
+
+void launch_emit(uint32_t nslots, const uint8_t* kind, const uint32_t* link,
+                 const ChildRec* slots, const FinRec* fins, const uint32_t* fin_count,
+                 const uint32_t* chain, const uint32_t* start, const uint32_t* child_size,
+                 uint32_t* child_start, uint32_t* out, cudaStream_t st) {
+    uint32_t g = (nslots + 255) / 256;
+    if (g < 1) g = 1;
+    if (g > 1184) g = 1184;
+    emit_kernel<<<g, 256, 0, st>>>(nslots, kind, link, slots, fins, fin_count, chain, start,
+                                   child_size, child_start, out);
+}
+
+void launch_root_slots(const RootInfo* root, ChildRec* slots, uint8_t* kind, uint32_t* link,
+                       cudaStream_t st) {
+    root_slots_kernel<<<1, 32, 0, st>>>(root, slots, kind, link);
+}
+
+void launch_root_frame(const RootInfo* root, const uint32_t* size1, uint32_t* start1,
+                       uint32_t* out, uint32_t* h_out, cudaStream_t st) {
+    root_frame_kernel<<<1, 32, 0, st>>>(root, size1, start1, out, h_out);
+}
+
+size_t agg_bytes(int nc) { return nc == 4 ? sizeof(Agg<4>) : sizeof(Agg<2>); }
+size_t plan_agg_bytes() { return sizeof(PlanAgg); }
+
+int occupancy_root() {
+    int b = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, root_partition_kernel, kThreads, 0);
+    return b;
+}
+int occupancy_level() {
+    int b = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, level_kernel<false>, kThreads, 0);
+    return b;
+}
+int occupancy_finisher() {
+    int b = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, finisher_kernel, kFinWarps * 32, 0);
+    return b;
+}
+
+}  // namespace vqb
+
+namespace vqb {
+uint32_t read_and_clear_fault() {
+    uint32_t v = 0;
+    cudaMemcpyFromSymbol(&v, g_vqb_fault, sizeof v);
+    if (v) {
+        const uint32_t z = 0;
+        cudaMemcpyToSymbol(g_vqb_fault, &z, sizeof z);
+    }
+    return v;
+}
+}  // namespace vqb
