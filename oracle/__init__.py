@@ -136,7 +136,7 @@ class Reference:
             raise FileNotFoundError(path)
         L = self.lib = C.CDLL(path)
         L.ref_convex_hull.argtypes = [_dp, _dp, C.c_size_t, C.c_int, C.c_int, C.c_int,
-                                      C.c_int, _dp, _dp, _sz]
+                                      C.c_int, _dp, _dp, C.c_size_t, _sz]
         L.ref_bench_hull.argtypes = [_dp, _dp, C.c_size_t, C.c_int, C.c_int, _dp, _sz]
         L.ref_find_extremes.argtypes = [_dp, _dp, C.c_size_t, _sz, _sz]
         L.ref_extract_subsets.argtypes = [_dp, _dp, C.c_size_t, _dp, _dp, C.c_int, C.c_int,
@@ -158,17 +158,19 @@ class Reference:
     def hw_threads(self) -> int:
         return int(self.lib.ref_hw_threads())
 
-    def convex_hull(self, xs, ys, workers=1, lanes=8, portable=False, max_depth=512):
+    def convex_hull(self, xs, ys, workers=1, lanes=8, portable=False, max_depth=512,
+                    cap=None):
         xs, px = _f64(xs)
         ys, py = _f64(ys)
         n = len(xs)
-        ox = np.empty(max(n, 1))
-        oy = np.empty(max(n, 1))
+        cap = max(n, 1) if cap is None else cap
+        ox = np.empty(cap)
+        oy = np.empty(cap)
         cnt = C.c_size_t()
         rc = self.lib.ref_convex_hull(px, py, n, workers, lanes, int(portable), max_depth,
-                                      ox.ctypes.data_as(_dp), oy.ctypes.data_as(_dp),
+                                      ox.ctypes.data_as(_dp), oy.ctypes.data_as(_dp), cap,
                                       C.byref(cnt))
-        assert rc == 0
+        assert rc == 0, f"ref_convex_hull rc={rc} (h={cnt.value}, cap={cap})"
         return ox[: cnt.value].copy(), oy[: cnt.value].copy()
 
     def bench_hull(self, xs, ys, workers, reps):

@@ -50,7 +50,7 @@ unsigned ref_hw_threads() { return std::thread::hardware_concurrency(); }
 // Hull coordinates in the reference's output order.  Returns 0 / 1 on error.
 int ref_convex_hull(const double* xs, const double* ys, size_t n, int workers,
                     int lanes, int simd_portable, int max_depth,
-                    double* out_x, double* out_y, size_t* out_count) {
+                    double* out_x, double* out_y, size_t out_cap, size_t* out_count) {
     try {
         PointSet pts = load(xs, ys, n);
         Config cfg;
@@ -59,6 +59,8 @@ int ref_convex_hull(const double* xs, const double* ys, size_t n, int workers,
         cfg.simd = simd_portable ? SimdMode::Portable : SimdMode::Auto;
         cfg.max_depth = max_depth;
         const HullPolygon h = convex_hull(pts, cfg);
+        *out_count = h.size();
+        if (h.size() > out_cap) return 2;
         for (size_t i = 0; i < h.size(); ++i) {
             out_x[i] = h.vertices[i].x;
             out_y[i] = h.vertices[i].y;

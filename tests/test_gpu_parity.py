@@ -1,0 +1,239 @@
+"""GPU parity: the sm_100a path, called through the C ABI, against the golden
+vectors (produced by the reference) and the oracle run live on the same
+seeded inputs.  Bit-exact index lists; integer/index work has no tolerance.
+
+Mirrors proj/tests/test_hull.cpp, test_extract.cpp, test_geometry.cpp and the
+acceptance criteria C1/C4/C8 (acceptance.cpp:63-82, 182-208, 337-371).
+"""
+import numpy as np
+import pytest
+
+import golden_io as G
+
+pytestmark = pytest.mark.gpu
+
+
+def dev(a):
+    import torch
+
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).cuda()
+
+
+def gpu_indices(vq, xs, ys):
+    return vq.hull_device(dev(xs), dev(ys)).cpu().numpy().astype(np.uint64)
+
+
+# --- C ABI (host arrays) on every golden hull case -----------------------------
+@pytest.mark.parametrize("case", G.hull_cases(), ids=lambda c: c[0])
+def test_vqhull_compute_golden(vq, cuda, case):
+    name, xs, ys, idx, hx, hy = case
+    rc, got = vq.vqhull_compute(xs, ys)
+    assert rc == 0
+    assert np.array_equal(got, idx), f"{name}: {got[:10]} vs {idx[:10]}"
+
+
+@pytest.mark.parametrize("case", G.hull_cases()[::3], ids=lambda c: c[0])
+def test_device_hull_golden(vq, cuda, case):
+    name, xs, ys, idx, hx, hy = case
+    got = gpu_indices(vq, xs, ys)
+    assert np.array_equal(got, idx)
+    poly = vq.convex_hull(xs, ys)
+    assert np.array_equal(poly.xs, hx) and np.array_equal(poly.ys, hy)
+
+
+def test_u32_device_output(vq, cuda):
+    xs, ys = vq.generate("disk", 200_000, 9)
+    ref = gpu_indices(vq, xs, ys)
+    got = vq.hull_device(dev(xs), dev(ys), u32=True).cpu().numpy().astype(np.uint64)
+    assert np.array_equal(got, ref)
+
+
+# --- test_hull.cpp:320-345: C ABI semantics and errors ------------------------
+def test_cabi_duplicates_and_errors(vq, cuda):
+    rc, idx = vq.vqhull_compute([0, 4, 4, 0, 2, 0], [0, 0, 4, 4, 2, 0])
+    assert rc == 0 and idx.tolist() == [0, 3, 2, 1]
+    assert vq.vqhull_compute([], [])[0] == 0
+    assert vq.vqhull_compute([0.0, np.nan], [0.0, 1.0])[0] == 1
+    assert vq.vqhull_compute([0.0, 1.0, 2.0], [0.0, -np.inf, 1.0])[0] == 1
+    assert vq.vqhull_compute([0.0, 1.0], [0.0, 1.0], workers=0)[0] == 1
+    # the engine is still healthy after a rejected call
+    rc, idx = vq.vqhull_compute([1, 0, 0.5, 0, 1], [1, 0, 0.5, 1, 0])
+    assert rc == 0 and idx.tolist() == [1, 3, 0, 4]
+
+
+# --- find_extremes (test_geometry.cpp:32-51) -----------------------------------
+def test_find_extremes(vq, cuda, oracle):
+    assert vq.find_extremes(dev([0.0]), dev([0.0])) == (0, 0)
+    assert vq.find_extremes(dev([1, -2, 3]), dev([5, 0, 1])) == (1, 2)
+    assert vq.find_extremes(dev([0, 0, 0]), dev([1, -1, 0])) == (1, 0)
+    with pytest.raises(ValueError):
+        vq.find_extremes(dev([]), dev([]))
+    rng = np.random.default_rng(3)
+    for _ in range(50):
+        n = int(rng.integers(1, 300000))
+        xs = rng.integers(-30, 31, n).astype(float)
+        ys = rng.integers(-30, 31, n).astype(float)
+        assert vq.find_extremes(dev(xs), dev(ys)) == oracle.find_extremes(xs, ys)
+    # misaligned (odd offset) device pointer takes the scalar-load path
+    xs, ys = rng.uniform(-1, 1, 100001), rng.uniform(-1, 1, 100001)
+    X, Y = dev(xs), dev(ys)
+    assert vq.find_extremes(X[1:], Y[1:]) == oracle.find_extremes(xs[1:], ys[1:])
+
+
+# --- extract_subsets (test_extract.cpp:183-299) --------------------------------
+@pytest.mark.parametrize("case", G.extract_cases(), ids=lambda c: c["name"])
+def test_extract_golden(vq, cuda, case):
+    X, Y = dev(case["xs"]), dev(case["ys"])
+    out = vq.extract_subsets(X, Y, case["ea"], case["eb"])
+    assert (out.w_l, out.w_r) == (case["w_l"], case["w_r"])
+    assert out.r1 == case["r1"] and out.r2 == case["r2"]
+    x, y = X.cpu().numpy(), Y.cpu().numpy()
+    assert np.array_equal(G.sorted_pairs(x[:out.w_l], y[:out.w_l]), G.sorted_pairs(*case["s1"].T))
+    assert np.array_equal(G.sorted_pairs(x[out.w_r:], y[out.w_r:]), G.sorted_pairs(*case["s2"].T))
+
+
+def test_extract_large_vs_oracle(vq, cuda, oracle):
+    """Multi-tile segments: the decoupled look-back must give the same sets/r."""
+    rng = np.random.default_rng(17)
+    for n in (4095, 4096, 4097, 100_000, 1_000_003):
+        xs, ys = rng.uniform(-1, 1, n), rng.uniform(-1, 1, n)
+        ea, eb = [-1.0, -0.2, 0.3, 1.4], [0.3, 1.4, 1.0, 0.1]
+        ox, oy, wl, wr, r1, r2 = oracle.extract_subsets(xs, ys, ea, eb)
+        X, Y = dev(xs), dev(ys)
+        out = vq.extract_subsets(X, Y, ea, eb)
+        assert (out.w_l, out.w_r, out.r1, out.r2) == (wl, wr, r1, r2)
+        x, y = X.cpu().numpy(), Y.cpu().numpy()
+        assert np.array_equal(G.sorted_pairs(x[:wl], y[:wl]), G.sorted_pairs(ox[:wl], oy[:wl]))
+        assert np.array_equal(G.sorted_pairs(x[wr:], y[wr:]), G.sorted_pairs(ox[wr:], oy[wr:]))
+
+
+# --- random instances vs the oracle (test_hull.cpp:162-209, acceptance C1) -----
+def random_instance(rng, it):
+    n = int(rng.integers(0, 5000)) if it % 4 else int(rng.integers(0, 60))
+    k = it % 5
+    if k == 0:
+        return rng.integers(-4, 5, n).astype(float), rng.integers(-4, 5, n).astype(float)
+    if k == 1:
+        return rng.uniform(-1, 1, n), rng.uniform(-1, 1, n)
+    if k == 2:
+        t = rng.uniform(0, 2 * np.pi, n)
+        return np.cos(t), np.sin(t)
+    if k == 3:
+        return (rng.integers(-(1 << 24), 1 << 24, n).astype(float),
+                rng.integers(-(1 << 24), 1 << 24, n).astype(float))
+    # duplicates + signed zeros
+    base = rng.integers(-3, 4, (max(n, 1) // 4 + 1, 2)).astype(float)
+    pts = base[rng.integers(0, base.shape[0], n)]
+    xs, ys = pts[:, 0].copy(), pts[:, 1].copy()
+    z = rng.random(n) < 0.3
+    xs[z & (xs == 0)] = -0.0
+    return xs, ys
+
+
+def test_random_vs_oracle(vq, cuda, oracle):
+    rng = np.random.default_rng(2024)
+    for it in range(600):
+        xs, ys = random_instance(rng, it)
+        ref = oracle.hull_indices(xs, ys) if len(xs) else np.zeros(0, np.uint64)
+        got = gpu_indices(vq, xs, ys) if len(xs) else np.zeros(0, np.uint64)
+        assert np.array_equal(got, ref), f"iteration {it}: n={len(xs)}"
+
+
+def test_acceptance_c1_integer_instances(vq, cuda, reference):
+    """acceptance.cpp:63-82: integer instances equal the exact monotone chain."""
+    rng = np.random.default_rng(1)
+    for _ in range(300):
+        n = int(rng.integers(1, 2000))
+        xs = rng.integers(-1000, 1001, n).astype(float)
+        ys = rng.integers(-1000, 1001, n).astype(float)
+        poly = vq.convex_hull(xs, ys)
+        mx, my = reference.monotone_chain(xs, ys)
+        assert np.array_equal(poly.xs, mx) and np.array_equal(poly.ys, my)
+
+
+def test_deep_recursion_pow2_curve(vq, cuda):
+    """test_hull.cpp:220-240: every point on the hull, one peeled per level."""
+    m = 600
+    i = np.arange(m)
+    xs, ys = np.ldexp(1.0, i), np.ldexp(1.0, -i)
+    idx = vq.hull_indices(xs, ys)
+    assert idx.size == m
+    assert idx[0] == 0 and idx[1] == m - 1
+    assert idx[2:].tolist() == list(range(m - 2, 0, -1))
+
+
+# --- BASELINE configs ----------------------------------------------------------
+@pytest.mark.parametrize("name", ["config1_disk_1e6_s1", "config3_circle_1e7_s3",
+                                  "config5_proxy_disk_4e7_s5", "config2_square_1e8_s2"])
+def test_config_golden(vq, cuda, oracle, name):
+    cfg = G.configs()[name]
+    xs, ys = vq.generate(cfg["kind"], cfg["n"], cfg["seed"])
+    got = gpu_indices(vq, xs, ys)
+    assert got.size == cfg["h"]
+    assert f"{oracle.fnv1a64(got):016x}" == cfg["fnv1a64_u64le"]
+    assert got[:8].tolist() == cfg["head"] and got[-8:].tolist() == cfg["tail"]
+    if cfg["n"] <= 10**7:  # the oracle, live on this host, on the same bytes
+        assert np.array_equal(got, oracle.hull_indices(xs, ys))
+    # C ABI with host buffers gives the same list
+    rc, got2 = vq.vqhull_compute(xs, ys)
+    assert rc == 0 and np.array_equal(got2, got)
+
+
+@pytest.mark.slow
+def test_config4_kuzmin_1e9(vq, cuda, oracle):
+    cfg = G.configs().get("config4_kuzmin_1e9_s4")
+    if cfg is None:
+        pytest.skip("config4 golden not generated")
+    import torch
+
+    n = cfg["n"]
+    X = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    Y = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    vq.generate(cfg["kind"], n, cfg["seed"], out=(X, Y))
+    got = vq.hull_device(X.cuda(), Y.cuda()).cpu().numpy().astype(np.uint64)
+    assert got.tolist() == cfg["indices"]
+
+
+# --- size-independent properties at full size ----------------------------------
+def test_permutation_invariance(vq, cuda):
+    """Shuffled input -> the same vertex sequence."""
+    for kind, n in (("disk", 2_000_000), ("circle", 1_000_000), ("square", 3_000_000)):
+        xs, ys = vq.generate(kind, n, 77)
+        idx = gpu_indices(vq, xs, ys).astype(np.int64)
+        perm = np.random.default_rng(5).permutation(n)
+        idx2 = gpu_indices(vq, xs[perm], ys[perm]).astype(np.int64)
+        assert np.array_equal(xs[idx], xs[perm][idx2]) and np.array_equal(ys[idx], ys[perm][idx2])
+
+
+def test_hull_contains_all_points(vq, cuda):
+    """No input point strictly left of any directed hull edge (test_hull.cpp:25-52).
+    Integer coordinates below 2^25 keep the reference predicate exact
+    (SPEC.md:75), so the check is exact; it is evaluated on the GPU in f64."""
+    import torch
+
+    for kind, n in (("disk", 5_000_000), ("kuzmin", 5_000_000), ("circle", 300_000)):
+        xs, ys = vq.generate(kind, n, 3)
+        scale = 2.0**22 / max(np.abs(xs).max(), np.abs(ys).max())
+        xs, ys = np.round(xs * scale), np.round(ys * scale)
+        X, Y = dev(xs), dev(ys)
+        idx = vq.hull_device(X, Y)
+        hx, hy = X[idx], Y[idx]
+        qx, qy = torch.roll(hx, -1), torch.roll(hy, -1)
+        for e in range(0, hx.numel(), 64):  # 64 edges per batch
+            px_, py_ = hx[e:e + 64, None], hy[e:e + 64, None]
+            qx_, qy_ = qx[e:e + 64, None], qy[e:e + 64, None]
+            left = (px_ - X) * (qy_ - Y) > (py_ - Y) * (qx_ - X)
+            assert not bool(left.any())
+
+
+def test_stats_and_timing(vq, cuda):
+    xs, ys = vq.generate("disk", 1_000_000, 1)
+    vq.set_timing(True)
+    try:
+        vq.hull_indices(xs, ys)
+        s = vq.stats()
+    finally:
+        vq.set_timing(False)
+    assert s["n"] == 1_000_000 and s["hull_size"] == 333
+    assert s["timing_valid"] == 1 and s["ms_total"] > 0
+    assert s["launches"] > 5 and s["bytes_moved"] >= 40 * 1_000_000
