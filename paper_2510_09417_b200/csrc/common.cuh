@@ -289,4 +289,88 @@ __device__ T lookback(uint32_t tile, uint32_t first, const T& local, uint32_t* f
     return excl;
 }
 
+// Register-light look-back for the partition payloads: the exclusive prefix
+// accumulates in shared memory (*excl) and the window is reduced one class at
+// a time, so at most one Best is live per lane.  Same protocol as lookback<>.
+template <int NC>
+__device__ void lookback_agg(uint32_t tile, uint32_t first, const Agg<NC>& local, Agg<NC>& excl,
+                             uint32_t* flags, Agg<NC>* aggs, Agg<NC>* incs, uint32_t epoch) {
+    const int lane = threadIdx.x & 31;
+    if (lane == 0) agg_clear(excl);
+    if (tile == first) {
+        if (lane == 0) {
+            agg_store(&incs[tile], local);
+            __threadfence();
+            st_release(&flags[tile], status_word(epoch, kStInc));
+        }
+        __syncwarp();
+        return;
+    }
+    if (lane == 0) {
+        agg_store(&aggs[tile], local);
+        __threadfence();
+        st_release(&flags[tile], status_word(epoch, kStAgg));
+    }
+    __syncwarp();
+    int64_t pred = int64_t(tile) - 1;
+    while (true) {
+        const int64_t t = pred - lane;
+        const bool in_seg = t >= int64_t(first);
+        uint32_t st = 0;
+        if (in_seg) {
+            const uint32_t want_hi = epoch << 2;
+            uint32_t w;
+            uint32_t spins = 0;
+            while (true) {
+                w = ld_acquire(&flags[t]);
+                if ((w & ~3u) == want_hi && (w & 3u) != 0) break;
+                if (++spins > 4) __nanosleep(64);
+                if (spins > (1u << 25)) {
+                    w = kStInc;
+                    g_vqb_fault = 1u;
+                    break;
+                }
+            }
+            st = w & 3u;
+        }
+        const unsigned inc_mask = __ballot_sync(kFull, in_seg && st == kStInc);
+        const int stop = inc_mask ? (__ffs(inc_mask) - 1) : 31;
+        const bool take = in_seg && lane <= stop;
+        const Agg<NC>* src = (st == kStInc) ? &incs[in_seg ? t : 0] : &aggs[in_seg ? t : 0];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+            uint32_t v = take ? __ldcg(&src->cnt[c]) : 0u;
+#pragma unroll
+            for (int s = 16; s > 0; s >>= 1) v += __shfl_xor_sync(kFull, v, s);
+            Best b = best_none();
+            if (take) {
+                b.off = __ldcg(&src->best[c].off);
+                b.x = __ldcg(&src->best[c].x);
+                b.y = __ldcg(&src->best[c].y);
+                b.idx = __ldcg(&src->best[c].idx);
+                b.valid = __ldcg(&src->best[c].valid);
+            }
+            b = warp_best(b);
+            if (lane == 0) {
+                excl.cnt[c] += v;
+                if (prefer(b, excl.best[c])) excl.best[c] = b;
+            }
+        }
+        const unsigned seg_mask = __ballot_sync(kFull, in_seg);
+        if (inc_mask) break;
+        if (seg_mask != kFull) break;
+        pred -= 32;
+    }
+    if (lane == 0) {
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+            incs[tile].cnt[c] = excl.cnt[c] + local.cnt[c];
+            incs[tile].best[c] = prefer(local.best[c], excl.best[c]) ? local.best[c] : excl.best[c];
+        }
+        __threadfence();
+        st_release(&flags[tile], status_word(epoch, kStInc));
+    }
+    __syncwarp();
+}
+
 }  // namespace vqb

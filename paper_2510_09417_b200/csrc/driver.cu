@@ -98,7 +98,7 @@ class Engine {
         occ_root_ = std::max(1, occupancy_root());
         occ_level_ = std::max(1, occupancy_level());
         occ_fin_ = std::max(1, occupancy_finisher());
-        stream_grid_ = sms_ * 4;
+        stream_grid_ = sms_ * std::max(1, std::min(8, occupancy_stream()));  // one full wave
         ck(cudaMalloc(&ctrs_, 64 * sizeof(uint32_t)), "cudaMalloc ctrs");
         ck(cudaMemset(ctrs_, 0, 64 * sizeof(uint32_t)), "memset ctrs");
         ck(cudaMalloc(&root_, sizeof(RootInfo)), "cudaMalloc root");

@@ -13,9 +13,10 @@ namespace vqb {
 // and uses the position as the index).
 
 constexpr int kThreads = 256;               // partition CTA size
-constexpr int kItems = 8;                   // points per thread per tile
+constexpr int kItems = 4;                   // points per thread per tile
 constexpr int kTile = kThreads * kItems;    // points per partition tile
 constexpr int kWarps = kThreads / 32;
+constexpr int kPartMinBlocks = 3;           // resident partition CTAs per SM (register cap)
 constexpr uint32_t kFinMax = 256;           // segments this small go to the warp finisher
 
 // K1 + pass A results, one per hull call (device resident).

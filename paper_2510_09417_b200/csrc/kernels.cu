@@ -324,10 +324,11 @@ __global__ void __launch_bounds__(256) bootstrap_argmax_kernel(
 // ===========================================================================
 // Tile pipeline shared by KB (4 classes) and K2 (2 classes): per-warp ballot
 // ranks, block scan of the per-(item, warp) counts, staging of the survivors
-// in shared memory in input order, look-back for the tile's offsets inside
-// its segment, then coalesced two-sided stores (class c forward from its base
-// or backward from its base, the reference's S1-from-the-left /
-// S2-from-the-right layout, extract.hpp:14-18).
+// in shared memory in input order, block arg-max over the staged survivors
+// (one class at a time, so a thread holds a single candidate), look-back for
+// the tile's offsets inside its segment, then coalesced two-sided stores
+// (class c forward from its base or backward from it: the reference's
+// S1-from-the-left / S2-from-the-right layout, extract.hpp:14-18).
 // ===========================================================================
 template <int NC>
 struct TileSmem {
@@ -335,23 +336,23 @@ struct TileSmem {
     double sy[kTile];
     uint32_t sid[kTile];
     uint32_t wcnt[NC][kItems * kWarps];
-    uint32_t tot[NC];
     uint32_t cbase[NC + 1];
+    double fdx[NC], fdy[NC];  // class frames for the arg-max
     Best wbest[NC][kWarps];
     Agg<NC> excl;
     Agg<NC> local;
     uint32_t tile;
     uint32_t ntiles;
     uint32_t seg;
-    uint32_t last_ticket;
 };
 
-// Ranks + staging + block arg-max.  cls[i] == NC means "no class".
+// cls[i] == NC means "no class".  On return the survivors are staged in
+// input order, class by class, and S.local holds the tile's counts and
+// per-class canonical arg-max (offsets from the class frames S.fdx/S.fdy).
 template <int NC>
 __device__ __forceinline__ void stage_tile(TileSmem<NC>& S, const double (&ux)[kItems],
                                            const double (&uy)[kItems],
-                                           const uint32_t (&uid)[kItems],
-                                           const int (&cls)[kItems], Best (&best)[NC]) {
+                                           const uint32_t (&uid)[kItems], const int (&cls)[kItems]) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const unsigned lt = lanemask_lt();
     uint32_t rk[kItems];
@@ -365,33 +366,19 @@ __device__ __forceinline__ void stage_tile(TileSmem<NC>& S, const double (&ux)[k
             if (cls[i] == c) rk[i] = __popc(bal & lt);
         }
     }
-    // block arg-max per class
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
-        const Best b = warp_best(best[c]);
-        if (lane == 0) S.wbest[c][warp] = b;
-    }
     __syncthreads();
+    static_assert(kItems * kWarps == 32, "one scan entry per lane");
     if (warp < NC) {
         const int c = warp;
-        const uint32_t v0 = S.wcnt[c][2 * lane], v1 = S.wcnt[c][2 * lane + 1];
-        uint32_t s = v0 + v1;
-        uint32_t incl = s;
+        const uint32_t v = S.wcnt[c][lane];
+        uint32_t incl = v;
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
             const uint32_t o = __shfl_up_sync(kFull, incl, d);
             if (lane >= d) incl += o;
         }
-        const uint32_t ex = incl - s;
-        S.wcnt[c][2 * lane] = ex;
-        S.wcnt[c][2 * lane + 1] = ex + v0;
-        if (lane == 31) S.tot[c] = incl;
-        // block best of class c
-        Best b = lane < kWarps ? S.wbest[c][lane] : best_none();
-        b = warp_best(b);
-        if (lane == 0) {
-            S.local.best[c] = b;
-        }
+        S.wcnt[c][lane] = incl - v;
+        if (lane == 31) S.local.cnt[c] = incl;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -399,8 +386,7 @@ __device__ __forceinline__ void stage_tile(TileSmem<NC>& S, const double (&ux)[k
 #pragma unroll
         for (int c = 0; c < NC; ++c) {
             S.cbase[c] = acc;
-            acc += S.tot[c];
-            S.local.cnt[c] = S.tot[c];
+            acc += S.local.cnt[c];
         }
         S.cbase[NC] = acc;
     }
@@ -415,6 +401,26 @@ __device__ __forceinline__ void stage_tile(TileSmem<NC>& S, const double (&ux)[k
             S.sid[s] = uid[i];
         }
     }
+    __syncthreads();
+    // arg-max per class over the staged (contiguous) survivors
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        const double edx = S.fdx[c], edy = S.fdy[c];
+        Best b = best_none();
+        for (uint32_t e = S.cbase[c] + threadIdx.x; e < S.cbase[c + 1]; e += kThreads) {
+            const double u = S.sx[e], w = S.sy[e];
+            consider(b, true, lat_off(edx, edy, u, w), u, w, S.sid[e]);
+        }
+        b = warp_best(b);
+        if (lane == 0) S.wbest[c][warp] = b;
+    }
+    __syncthreads();
+    if (warp < NC) {
+        Best b = lane < kWarps ? S.wbest[warp][lane] : best_none();
+        b = warp_best(b);
+        if (lane == 0) S.local.best[warp] = b;
+    }
+    __syncthreads();
 }
 
 // After the look-back: stream the staged survivors to their final places.
@@ -425,11 +431,21 @@ __device__ __forceinline__ void flush_tile(const TileSmem<NC>& S, const uint64_t
                                            double* __restrict__ oy, uint32_t* __restrict__ oid) {
     const uint32_t total = S.cbase[NC];
     for (uint32_t e = threadIdx.x; e < total; e += kThreads) {
+        // class of staged element e, with base/direction picked by selects
+        // (no dynamically indexed local arrays)
         int c = 0;
+        uint64_t b = base[0];
+        bool f = fwd[0];
 #pragma unroll
-        for (int k = 1; k < NC; ++k) c += (e >= S.cbase[k]);
+        for (int k = 1; k < NC; ++k) {
+            if (e >= S.cbase[k]) {
+                c = k;
+                b = base[k];
+                f = fwd[k];
+            }
+        }
         const uint64_t r = uint64_t(S.excl.cnt[c]) + (e - S.cbase[c]);
-        const uint64_t pos = fwd[c] ? base[c] + r : base[c] - r;
+        const uint64_t pos = f ? b + r : b - r;
         ox[pos] = S.sx[e];
         oy[pos] = S.sy[e];
         oid[pos] = S.sid[e];
@@ -480,20 +496,21 @@ struct RootArgs {
     uint32_t ntiles;
 };
 
-__global__ void __launch_bounds__(kThreads, 1) root_partition_kernel(RootArgs a) {
+__global__ void __launch_bounds__(kThreads, kPartMinBlocks) root_partition_kernel(RootArgs a) {
     __shared__ TileSmem<4> S;
     const RootInfo& R = *a.root;
     const double px = R.px, py = R.py, qx = R.qx, qy = R.qy;
     const double r1x = R.r1.x, r1y = R.r1.y, r2x = R.r2.x, r2y = R.r2.y;
     const uint32_t n1 = R.cnt1, n2 = R.cnt2;
-    // child frames (kernels.hpp:23-25): 0: p->r1, 1: r1->q, 2: q->r2, 3: r2->p
-    double fdx[4], fdy[4];
-    fdx[0] = dsub(r1x, px); fdy[0] = dsub(r1y, py);
-    fdx[1] = dsub(qx, r1x); fdy[1] = dsub(qy, r1y);
-    fdx[2] = dsub(r2x, qx); fdy[2] = dsub(r2y, qy);
-    fdx[3] = dsub(px, r2x); fdy[3] = dsub(py, r2y);
+    if (threadIdx.x == 0) {
+        // child frames (kernels.hpp:23-25): 0: p->r1, 1: r1->q, 2: q->r2, 3: r2->p
+        S.fdx[0] = dsub(r1x, px); S.fdy[0] = dsub(r1y, py);
+        S.fdx[1] = dsub(qx, r1x); S.fdy[1] = dsub(qy, r1y);
+        S.fdx[2] = dsub(r2x, qx); S.fdy[2] = dsub(r2y, qy);
+        S.fdx[3] = dsub(px, r2x); S.fdy[3] = dsub(py, r2y);
+    }
     uint64_t base[4];
-    bool fwd[4] = {true, false, true, false};
+    const bool fwd[4] = {true, false, true, false};
     base[0] = 0;
     base[1] = uint64_t(n1) - 1;  // unused when empty
     base[2] = n1;
@@ -505,9 +522,6 @@ __global__ void __launch_bounds__(kThreads, 1) root_partition_kernel(RootArgs a)
         double ux[kItems], uy[kItems];
         uint32_t uid[kItems];
         int cls[kItems];
-        Best best[4];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) best[c] = best_none();
 #pragma unroll
         for (int i = 0; i < kItems; ++i) {
             const uint64_t pos = start + uint64_t(i) * kThreads + threadIdx.x;
@@ -523,56 +537,40 @@ __global__ void __launch_bounds__(kThreads, 1) root_partition_kernel(RootArgs a)
             const double A = dsub(px, u), B = dsub(py, w);
             const double Cc = dsub(qx, u), D = dsub(qy, w);
             const double t1 = dmul(A, D), t2 = dmul(B, Cc);
-            const bool s1 = t1 > t2;          // left of p->q
-            const bool s2 = !s1 && (t2 > t1); // left of q->p
+            const bool s1 = t1 > t2;           // left of p->q
+            const bool s2 = !s1 && (t2 > t1);  // left of q->p
             // second level, side-selected operands
             const double rx = s1 ? r1x : r2x, ry = s1 ? r1y : r2y;
             const double P1x = s1 ? A : Cc, P1y = s1 ? B : D;
             const double Q2x = s1 ? Cc : A, Q2y = s1 ? D : B;
             const double E = dsub(rx, u), F = dsub(ry, w);
-            const bool L = left_diff(P1x, P1y, E, F);       // left of (side start -> r)
-            const bool Rr = !L && left_diff(E, F, Q2x, Q2y); // left of (r -> side end)
+            const bool L = left_diff(P1x, P1y, E, F);         // left of (side start -> r)
+            const bool Rr = !L && left_diff(E, F, Q2x, Q2y);  // left of (r -> side end)
             int c = 4;
             if (s1) c = L ? 0 : (Rr ? 1 : 4);
             else if (s2) c = L ? 2 : (Rr ? 3 : 4);
-            if (cls[i] != 0) c = 4;  // out of range
-            cls[i] = c;
-            if (c < 4) {
-                // class frame by select (no dynamically indexed local array)
-                const double edx = c == 0 ? fdx[0] : (c == 1 ? fdx[1] : (c == 2 ? fdx[2] : fdx[3]));
-                const double edy = c == 0 ? fdy[0] : (c == 1 ? fdy[1] : (c == 2 ? fdy[2] : fdy[3]));
-                const double off = lat_off(edx, edy, u, w);
-#pragma unroll
-                for (int k = 0; k < 4; ++k)
-                    if (k == c) consider(best[k], true, off, u, w, uid[i]);
-            }
+            cls[i] = (cls[i] != 0) ? 4 : c;  // out of range stays unclassified
         }
-        stage_tile<4>(S, ux, uy, uid, cls, best);
-        __syncthreads();
+        stage_tile<4>(S, ux, uy, uid, cls);
         if (threadIdx.x < 32) {
-            const Agg<4> ex = lookback<Agg<4>>(t, 0u, S.local, a.flags, a.aggs, a.incs, a.epoch);
-            if (threadIdx.x == 0) {
-                S.excl = ex;
-                if (t == a.ntiles - 1) {
-                    Agg<4> inc = ex;
-                    agg_combine(inc, S.local);
-                    // children slots: (p, r11, r1) (r1, r12, q) (q, r21, r2) (r2, r22, p)
-                    const double tri[4][4] = {{px, py, r1x, r1y}, {r1x, r1y, qx, qy},
-                                              {qx, qy, r2x, r2y}, {r2x, r2y, px, py}};
-                    for (int c = 0; c < 4; ++c) {
-                        ChildRec ch;
-                        ch.px = tri[c][0];
-                        ch.py = tri[c][1];
-                        ch.qx = tri[c][2];
-                        ch.qy = tri[c][3];
-                        ch.rx = inc.best[c].x;
-                        ch.ry = inc.best[c].y;
-                        ch.r_idx = inc.best[c].idx;
-                        ch.m = inc.cnt[c];
-                        ch.begin = fwd[c] ? base[c] : base[c] + 1 - inc.cnt[c];
-                        a.children[c] = ch;
-                    }
-                }
+            lookback_agg<4>(t, 0u, S.local, S.excl, a.flags, a.aggs, a.incs, a.epoch);
+            if (threadIdx.x < 4 && t == a.ntiles - 1) {
+                // children slots: (p, r11, r1) (r1, r12, q) (q, r21, r2) (r2, r22, p)
+                const int c = threadIdx.x;
+                const Best b = prefer(S.local.best[c], S.excl.best[c]) ? S.local.best[c] : S.excl.best[c];
+                const uint32_t m = S.excl.cnt[c] + S.local.cnt[c];
+                ChildRec ch;
+                ch.px = c == 0 ? px : (c == 1 ? r1x : (c == 2 ? qx : r2x));
+                ch.py = c == 0 ? py : (c == 1 ? r1y : (c == 2 ? qy : r2y));
+                ch.qx = c == 0 ? r1x : (c == 1 ? qx : (c == 2 ? r2x : px));
+                ch.qy = c == 0 ? r1y : (c == 1 ? qy : (c == 2 ? r2y : py));
+                ch.rx = b.x;
+                ch.ry = b.y;
+                ch.r_idx = b.idx;
+                ch.m = m;
+                ch.begin = (c & 1) ? (c == 1 ? uint64_t(n1) - m : uint64_t(n1) + n2 - m)
+                                   : (c == 0 ? 0 : uint64_t(n1));
+                a.children[c] = ch;
             }
         }
         __syncthreads();
@@ -608,7 +606,7 @@ struct LevelArgs {
 };
 
 template <bool GENERAL>
-__global__ void __launch_bounds__(kThreads, 1) level_kernel(LevelArgs a) {
+__global__ void __launch_bounds__(kThreads, kPartMinBlocks) level_kernel(LevelArgs a) {
     __shared__ TileSmem<2> S;
     __shared__ SegRec s_seg;
     if (threadIdx.x == 0) S.ntiles = a.info->ntiles;
@@ -619,16 +617,16 @@ __global__ void __launch_bounds__(kThreads, 1) level_kernel(LevelArgs a) {
         if (threadIdx.x == 0) {
             S.seg = a.tile_seg[t];
             s_seg = a.segs[S.seg];
+            S.fdx[0] = s_seg.adx; S.fdy[0] = s_seg.ady;
+            S.fdx[1] = s_seg.bdx; S.fdy[1] = s_seg.bdy;
         }
         __syncthreads();
-        const SegRec& g = s_seg;
-        const uint32_t j = t - g.tile0;
-        const uint64_t start = g.begin + uint64_t(j) * kTile;
-        const uint32_t cnt = min(uint32_t(kTile), g.m - j * uint32_t(kTile));
+        const uint32_t j = t - s_seg.tile0;
+        const uint64_t start = s_seg.begin + uint64_t(j) * kTile;
+        const uint32_t cnt = min(uint32_t(kTile), s_seg.m - j * uint32_t(kTile));
         double ux[kItems], uy[kItems];
         uint32_t uid[kItems];
         int cls[kItems];
-        Best best[2] = {best_none(), best_none()};
 #pragma unroll
         for (int i = 0; i < kItems; ++i) {
             const uint32_t r = uint32_t(i) * kThreads + threadIdx.x;
@@ -638,46 +636,42 @@ __global__ void __launch_bounds__(kThreads, 1) level_kernel(LevelArgs a) {
             uid[i] = v ? ld_stream(a.iid + start + r) : 0u;
             cls[i] = v ? 0 : 2;
         }
-        const double px = g.px, py = g.py, rx = g.rx, ry = g.ry, qx = g.qx, qy = g.qy;
+        {
+            const double px = s_seg.px, py = s_seg.py, rx = s_seg.rx, ry = s_seg.ry;
+            const double qx = s_seg.qx, qy = s_seg.qy;
 #pragma unroll
-        for (int i = 0; i < kItems; ++i) {
-            const double u = ux[i], w = uy[i];
-            bool la, lb;
-            if (GENERAL) {
-                la = left_diff(dsub(px, u), dsub(py, w), dsub(rx, u), dsub(ry, w));
-                lb = !la && left_diff(dsub(g.bx, u), dsub(g.by, w), dsub(qx, u), dsub(qy, w));
-            } else {
-                const double A = dsub(px, u), B = dsub(py, w);
-                const double E = dsub(rx, u), F = dsub(ry, w);
-                const double Cc = dsub(qx, u), D = dsub(qy, w);
-                la = left_diff(A, B, E, F);
-                lb = !la && left_diff(E, F, Cc, D);
-            }
-            const int c = (cls[i] != 0) ? 2 : (la ? 0 : (lb ? 1 : 2));
-            cls[i] = c;
-            if (c < 2) {
-                const double off = c == 0 ? lat_off(g.adx, g.ady, u, w) : lat_off(g.bdx, g.bdy, u, w);
-                if (c == 0) consider(best[0], true, off, u, w, uid[i]);
-                else consider(best[1], true, off, u, w, uid[i]);
+            for (int i = 0; i < kItems; ++i) {
+                const double u = ux[i], w = uy[i];
+                bool la, lb;
+                if (GENERAL) {
+                    la = left_diff(dsub(px, u), dsub(py, w), dsub(rx, u), dsub(ry, w));
+                    lb = !la && left_diff(dsub(s_seg.bx, u), dsub(s_seg.by, w), dsub(qx, u), dsub(qy, w));
+                } else {
+                    const double A = dsub(px, u), B = dsub(py, w);
+                    const double E = dsub(rx, u), F = dsub(ry, w);
+                    const double Cc = dsub(qx, u), D = dsub(qy, w);
+                    la = left_diff(A, B, E, F);
+                    lb = !la && left_diff(E, F, Cc, D);
+                }
+                cls[i] = (cls[i] != 0) ? 2 : (la ? 0 : (lb ? 1 : 2));
             }
         }
-        stage_tile<2>(S, ux, uy, uid, cls, best);
-        __syncthreads();
-        const uint64_t base[2] = {g.out, g.out + g.m - 1};
+        stage_tile<2>(S, ux, uy, uid, cls);
+        const uint64_t base[2] = {s_seg.out, s_seg.out + s_seg.m - 1};
         const bool fwd[2] = {true, false};
         if (threadIdx.x < 32) {
-            const Agg<2> ex =
-                lookback<Agg<2>>(t, g.tile0, S.local, a.flags, a.aggs, a.incs, a.epoch);
+            lookback_agg<2>(t, s_seg.tile0, S.local, S.excl, a.flags, a.aggs, a.incs, a.epoch);
             if (threadIdx.x == 0) {
-                S.excl = ex;
-                if (j == g.ntiles - 1) {
-                    Agg<2> inc = ex;
+                if (j == s_seg.ntiles - 1) {
+                    const SegRec& g = s_seg;
+                    Agg<2> inc = S.excl;
                     agg_combine(inc, S.local);
                     ChildRec L, Rr;
-                    L.px = px; L.py = py; L.qx = rx; L.qy = ry;
+                    L.px = g.px; L.py = g.py; L.qx = g.rx; L.qy = g.ry;
                     L.rx = inc.best[0].x; L.ry = inc.best[0].y;
                     L.r_idx = inc.best[0].idx; L.m = inc.cnt[0]; L.begin = g.out;
-                    Rr.px = GENERAL ? g.bx : rx; Rr.py = GENERAL ? g.by : ry; Rr.qx = qx; Rr.qy = qy;
+                    Rr.px = GENERAL ? g.bx : g.rx; Rr.py = GENERAL ? g.by : g.ry;
+                    Rr.qx = g.qx; Rr.qy = g.qy;
                     Rr.rx = inc.best[1].x; Rr.ry = inc.best[1].y;
                     Rr.r_idx = inc.best[1].idx; Rr.m = inc.cnt[1];
                     Rr.begin = g.out + g.m - inc.cnt[1];
@@ -1199,6 +1193,12 @@ int occupancy_level() {
     int b = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, level_kernel<false>, kThreads, 0);
     return b;
+}
+int occupancy_stream() {
+    int a = 0, b = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, extremes_kernel, 256, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, bootstrap_argmax_kernel, 256, 0);
+    return a < b ? a : b;
 }
 int occupancy_finisher() {
     int b = 0;

@@ -47,6 +47,7 @@ size_t plan_agg_bytes();
 int occupancy_root();
 int occupancy_level();
 int occupancy_finisher();
+int occupancy_stream();
 uint32_t read_and_clear_fault();
 
 }  // namespace vqb
