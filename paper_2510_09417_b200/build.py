@@ -15,7 +15,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, "libvqhull_b200.so")
-SOURCES = ["kernels.cu", "driver.cu", "dataset.cpp"]
+SOURCES = ["kernels.cu", "partition.cu", "driver.cu", "dataset.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

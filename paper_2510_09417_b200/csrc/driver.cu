@@ -146,17 +146,19 @@ class Engine {
         // ---- KB: fused levels 1+2 over the input
         bufs_[0].ensure(n, st);
         const uint32_t ntiles_root = uint32_t((n + kTile - 1) / kTile);
-        ensure_lookback(ntiles_root, 4, st);
+        ensure_lookback(2 * ntiles_root, st);
         LevelTables& L2 = level(2);
         L2.slots.ensure(4 * sizeof(ChildRec), st);
         {
             const int grid = std::max(1, std::min<int>(int(ntiles_root), sms_ * occ_root_));
-            const uint32_t ep = next_epoch();
-            tk(2, st, [&] {
-                launch_root_partition(dx, dy, n, root_, bufs_[0].x.as<double>(), bufs_[0].y.as<double>(),
-                                      bufs_[0].id.as<uint32_t>(), flags_.as<uint32_t>(), aggs_.p,
-                                      incs_.p, ep, &ctrs_[0], L2.slots.as<ChildRec>(), grid, st);
-            });
+            part_.ensure(size_t(grid) * 4 * sizeof(Best), st);
+            RootArgs ra;
+            ra.xs = dx; ra.ys = dy; ra.n = n; ra.root = root_;
+            ra.ox = bufs_[0].x.as<double>(); ra.oy = bufs_[0].y.as<double>(); ra.oid = bufs_[0].id.as<uint32_t>();
+            ra.status = status_.as<Status>(); ra.epoch = next_epoch();
+            ra.ctr = &ctrs_[0]; ra.ticket = &ctrs_[4]; ra.cta_part = part_.as<Best>();
+            ra.children = L2.slots.as<ChildRec>(); ra.ntiles = ntiles_root;
+            tk(2, st, [&] { launch_root_partition(ra, grid, st); });
         }
         // finiteness verdict + sizes for the byte accounting
         ck(cudaMemcpyAsync(h_root_, root_, sizeof(RootInfo), cudaMemcpyDeviceToHost, st), "d2h root");
@@ -176,7 +178,8 @@ class Engine {
             T.segs.ensure(size_t(nslots) * sizeof(SegRec), st);
             T.fins.ensure(size_t(nslots) * sizeof(FinRec), st);
             const uint32_t nchunks = (nslots + 1023) / 1024;
-            ensure_lookback(nchunks, 4, st);
+            ensure_lookback(nchunks, st);
+            segaux_.ensure(size_t(nslots) * 8 + 8, st);
             info_.ensure(size_t(lvl + 1) * sizeof(LevelInfo), st, true);
             LevelInfo* dinfo = info_.as<LevelInfo>() + lvl;
             {
@@ -184,7 +187,8 @@ class Engine {
                 tk(5, st, [&] {
                     launch_planner(T.slots.as<ChildRec>(), nslots, T.segs.as<SegRec>(), T.fins.as<FinRec>(),
                                    T.kind.as<uint8_t>(), T.link.as<uint32_t>(), dinfo, fin_base,
-                                   flags_.as<uint32_t>(), aggs_.p, incs_.p, ep, &ctrs_[2], sms_ * 4, st);
+                                   flags_.as<uint32_t>(), aggs_.p, incs_.p, ep, &ctrs_[2],
+                                   segaux_.as<uint32_t>(), segaux_.as<uint32_t>() + nslots, sms_ * 4, st);
                 });
             }
             ck(cudaMemcpyAsync(h_info_, dinfo, sizeof(LevelInfo), cudaMemcpyDeviceToHost, st), "d2h info");
@@ -228,21 +232,23 @@ class Engine {
             const int out = in ^ 1;
             bufs_[out].ensure(std::max<uint64_t>(li.out_total, 1), st);
             tile_seg_.ensure(size_t(li.ntiles) * 4, st);
-            ensure_lookback(li.ntiles, 2, st);
+            ensure_lookback(li.ntiles, st);
+            part_.ensure(size_t(li.ntiles) * 2 * sizeof(Best), st);
             LevelTables& Tn = level(lvl + 1);
             Tn.slots.ensure(size_t(2) * li.nseg * sizeof(ChildRec), st);
-            // re-fetch T: level() may have grown the vector
             LevelTables& Tc = level(lvl);
             tk(5, st, [&] { launch_tilemap(Tc.segs.as<SegRec>(), dinfo, tile_seg_.as<uint32_t>(), li.ntiles, st); });
             {
                 const int grid = std::max(1, std::min<int>(int(li.ntiles), sms_ * occ_level_));
-                const uint32_t ep = next_epoch();
-                tk(3, st, [&] {
-                    launch_level(Tc.segs.as<SegRec>(), tile_seg_.as<uint32_t>(), dinfo, bufs_[in].x.as<double>(),
-                                 bufs_[in].y.as<double>(), bufs_[in].id.as<uint32_t>(), bufs_[out].x.as<double>(),
-                                 bufs_[out].y.as<double>(), bufs_[out].id.as<uint32_t>(), flags_.as<uint32_t>(),
-                                 aggs_.p, incs_.p, ep, &ctrs_[1], Tn.slots.as<ChildRec>(), false, grid, st);
-                });
+                LevelArgs la;
+                la.segs = Tc.segs.as<SegRec>(); la.tile_seg = tile_seg_.as<uint32_t>(); la.info = dinfo;
+                la.ix = bufs_[in].x.as<double>(); la.iy = bufs_[in].y.as<double>(); la.iid = bufs_[in].id.as<uint32_t>();
+                la.ox = bufs_[out].x.as<double>(); la.oy = bufs_[out].y.as<double>(); la.oid = bufs_[out].id.as<uint32_t>();
+                la.status = status_.as<Status>(); la.epoch = next_epoch(); la.ctr = &ctrs_[1];
+                la.tile_part = part_.as<Best>();
+                la.seg_pcnt = segaux_.as<uint32_t>(); la.seg_done = segaux_.as<uint32_t>() + nslots;
+                la.children = Tn.slots.as<ChildRec>();
+                tk(3, st, [&] { launch_level(la, false, grid, st); });
             }
             stats_.segments += li.nseg;
             stats_.level_points += li.out_total;
@@ -345,12 +351,20 @@ class Engine {
         ck(cudaMemcpyAsync(dli, &li, sizeof li, cudaMemcpyHostToDevice, st), "h2d info");
         tile_seg_.ensure(size_t(g.ntiles) * 4, st);
         ck(cudaMemsetAsync(tile_seg_.p, 0, size_t(g.ntiles) * 4, st), "memset tiles");
-        ensure_lookback(g.ntiles, 2, st);
+        ensure_lookback(g.ntiles, st);
+        part_.ensure(size_t(g.ntiles) * 2 * sizeof(Best), st);
+        segaux_.ensure(16, st);
+        ck(cudaMemsetAsync(segaux_.p, 0, 16, st), "memset seg aux");
         const int grid = std::max(1, std::min<int>(int(g.ntiles), sms_ * occ_level_));
-        launch_level(dseg, tile_seg_.as<uint32_t>(), dli, bufs_[0].x.as<double>(), bufs_[0].y.as<double>(),
-                     bufs_[0].id.as<uint32_t>(), bufs_[1].x.as<double>(), bufs_[1].y.as<double>(),
-                     bufs_[1].id.as<uint32_t>(), flags_.as<uint32_t>(), aggs_.p, incs_.p, next_epoch(),
-                     &ctrs_[1], dch, true, grid, st);
+        LevelArgs la;
+        la.segs = dseg; la.tile_seg = tile_seg_.as<uint32_t>(); la.info = dli;
+        la.ix = bufs_[0].x.as<double>(); la.iy = bufs_[0].y.as<double>(); la.iid = bufs_[0].id.as<uint32_t>();
+        la.ox = bufs_[1].x.as<double>(); la.oy = bufs_[1].y.as<double>(); la.oid = bufs_[1].id.as<uint32_t>();
+        la.status = status_.as<Status>(); la.epoch = next_epoch(); la.ctr = &ctrs_[1];
+        la.tile_part = part_.as<Best>();
+        la.seg_pcnt = segaux_.as<uint32_t>(); la.seg_done = segaux_.as<uint32_t>() + 1;
+        la.children = dch;
+        launch_level(la, true, grid, st);
         ChildRec ch[2];
         ck(cudaMemcpyAsync(ch, dch, sizeof ch, cudaMemcpyDeviceToHost, st), "d2h children");
         ck(cudaStreamSynchronize(st), "sync");
@@ -402,16 +416,20 @@ class Engine {
         return epoch_ & 0x3fffffffu;
     }
 
-    void ensure_lookback(uint32_t tiles, int nc, cudaStream_t st) {
+    // status words (partition kernels) and planner look-back arrays; fresh
+    // words must not alias a live epoch, so growth zeroes them
+    void ensure_lookback(uint32_t tiles, cudaStream_t st) {
         const size_t t = std::max<uint32_t>(tiles, 1);
+        if (t * sizeof(Status) > status_.cap) {
+            status_.ensure(t * sizeof(Status), st);
+            ck(cudaMemsetAsync(status_.p, 0, status_.cap, st), "memset status");
+        }
         if (t * 4 > flags_.cap) {
-            // fresh status words must not alias a live epoch: zero them
             flags_.ensure(t * 4, st);
             ck(cudaMemsetAsync(flags_.p, 0, flags_.cap, st), "memset flags");
         }
-        const size_t pb = std::max(agg_bytes(nc), std::max(agg_bytes(4), plan_agg_bytes()));
-        aggs_.ensure(t * pb, st);
-        incs_.ensure(t * pb, st);
+        aggs_.ensure(t * plan_agg_bytes(), st);
+        incs_.ensure(t * plan_agg_bytes(), st);
     }
 
     void iota(uint32_t* d, uint64_t n, cudaStream_t st);
@@ -505,6 +523,7 @@ class Engine {
     RootInfo* h_root_ = nullptr;
     uint32_t* h_word_ = nullptr;
     DevBuf partials_, flags_, aggs_, incs_, tile_seg_, chain_, info_, scratch_, out_;
+    DevBuf status_, part_, segaux_;
     PointBuf bufs_[2];
     PointBuf in_;
     std::deque<LevelTables> levels_;  // deque: references stay valid on growth

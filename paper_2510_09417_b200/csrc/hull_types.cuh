@@ -80,6 +80,49 @@ struct LevelInfo {
     uint32_t pad;
 };
 
+// Look-back status word of the partition kernels: flag (epoch << 2 | state)
+// and two 32-bit class counts in ONE 16-byte word, so a reader never needs a
+// payload that could be stale relative to the flag.
+struct __align__(16) Status {
+    uint32_t flag, c0, c1, pad;
+};
+
+struct RootArgs {
+    const double* xs;
+    const double* ys;
+    uint64_t n;
+    const RootInfo* root;
+    double* ox;
+    double* oy;
+    uint32_t* oid;
+    Status* status;      // 2 per tile (side S1, side S2)
+    uint32_t epoch;
+    uint32_t* ctr;       // tile claim counter
+    uint32_t* ticket;    // CTA exit ticket
+    Best* cta_part;      // 4 per CTA
+    ChildRec* children;  // 4 slots
+    uint32_t ntiles;
+};
+
+struct LevelArgs {
+    const SegRec* segs;
+    const uint32_t* tile_seg;
+    const LevelInfo* info;
+    const double* ix;
+    const double* iy;
+    const uint32_t* iid;
+    double* ox;
+    double* oy;
+    uint32_t* oid;
+    Status* status;      // 1 per tile
+    uint32_t epoch;
+    uint32_t* ctr;
+    Best* tile_part;     // 2 per tile (per-CTA segment partials, indexed tile0 + slot)
+    uint32_t* seg_pcnt;  // per segment: partials published
+    uint32_t* seg_done;  // per segment: tiles finished
+    ChildRec* children;  // 2 per segment
+};
+
 // Look-back payload of the planner scan.
 struct PlanAgg {
     uint32_t nseg, nfin, ntiles, out, fin, leaf;

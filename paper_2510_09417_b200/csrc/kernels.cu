@@ -322,370 +322,6 @@ __global__ void __launch_bounds__(256) bootstrap_argmax_kernel(
 }
 
 // ===========================================================================
-// Tile pipeline shared by KB (4 classes) and K2 (2 classes): per-warp ballot
-// ranks, block scan of the per-(item, warp) counts, staging of the survivors
-// in shared memory in input order, block arg-max over the staged survivors
-// (one class at a time, so a thread holds a single candidate), look-back for
-// the tile's offsets inside its segment, then coalesced two-sided stores
-// (class c forward from its base or backward from it: the reference's
-// S1-from-the-left / S2-from-the-right layout, extract.hpp:14-18).
-// ===========================================================================
-template <int NC>
-struct TileSmem {
-    double sx[kTile];
-    double sy[kTile];
-    uint32_t sid[kTile];
-    uint32_t wcnt[NC][kItems * kWarps];
-    uint32_t cbase[NC + 1];
-    double fdx[NC], fdy[NC];  // class frames for the arg-max
-    Best wbest[NC][kWarps];
-    Agg<NC> excl;
-    Agg<NC> local;
-    uint32_t tile;
-    uint32_t ntiles;
-    uint32_t seg;
-};
-
-// cls[i] == NC means "no class".  On return the survivors are staged in
-// input order, class by class, and S.local holds the tile's counts and
-// per-class canonical arg-max (offsets from the class frames S.fdx/S.fdy).
-template <int NC>
-__device__ __forceinline__ void stage_tile(TileSmem<NC>& S, const double (&ux)[kItems],
-                                           const double (&uy)[kItems],
-                                           const uint32_t (&uid)[kItems], const int (&cls)[kItems]) {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const unsigned lt = lanemask_lt();
-    uint32_t rk[kItems];
-#pragma unroll
-    for (int i = 0; i < kItems; ++i) {
-        rk[i] = 0;
-#pragma unroll
-        for (int c = 0; c < NC; ++c) {
-            const unsigned bal = __ballot_sync(kFull, cls[i] == c);
-            if (lane == 0) S.wcnt[c][i * kWarps + warp] = __popc(bal);
-            if (cls[i] == c) rk[i] = __popc(bal & lt);
-        }
-    }
-    __syncthreads();
-    static_assert(kItems * kWarps == 32, "one scan entry per lane");
-    if (warp < NC) {
-        const int c = warp;
-        const uint32_t v = S.wcnt[c][lane];
-        uint32_t incl = v;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const uint32_t o = __shfl_up_sync(kFull, incl, d);
-            if (lane >= d) incl += o;
-        }
-        S.wcnt[c][lane] = incl - v;
-        if (lane == 31) S.local.cnt[c] = incl;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        uint32_t acc = 0;
-#pragma unroll
-        for (int c = 0; c < NC; ++c) {
-            S.cbase[c] = acc;
-            acc += S.local.cnt[c];
-        }
-        S.cbase[NC] = acc;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int i = 0; i < kItems; ++i) {
-        const int c = cls[i];
-        if (c < NC) {
-            const uint32_t s = S.cbase[c] + S.wcnt[c][i * kWarps + warp] + rk[i];
-            S.sx[s] = ux[i];
-            S.sy[s] = uy[i];
-            S.sid[s] = uid[i];
-        }
-    }
-    __syncthreads();
-    // arg-max per class over the staged (contiguous) survivors
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
-        const double edx = S.fdx[c], edy = S.fdy[c];
-        Best b = best_none();
-        for (uint32_t e = S.cbase[c] + threadIdx.x; e < S.cbase[c + 1]; e += kThreads) {
-            const double u = S.sx[e], w = S.sy[e];
-            consider(b, true, lat_off(edx, edy, u, w), u, w, S.sid[e]);
-        }
-        b = warp_best(b);
-        if (lane == 0) S.wbest[c][warp] = b;
-    }
-    __syncthreads();
-    if (warp < NC) {
-        Best b = lane < kWarps ? S.wbest[warp][lane] : best_none();
-        b = warp_best(b);
-        if (lane == 0) S.local.best[warp] = b;
-    }
-    __syncthreads();
-}
-
-// After the look-back: stream the staged survivors to their final places.
-// base[c] is the first (fwd) / last (bwd) position of class c in the segment.
-template <int NC>
-__device__ __forceinline__ void flush_tile(const TileSmem<NC>& S, const uint64_t (&base)[NC],
-                                           const bool (&fwd)[NC], double* __restrict__ ox,
-                                           double* __restrict__ oy, uint32_t* __restrict__ oid) {
-    const uint32_t total = S.cbase[NC];
-    for (uint32_t e = threadIdx.x; e < total; e += kThreads) {
-        // class of staged element e, with base/direction picked by selects
-        // (no dynamically indexed local arrays)
-        int c = 0;
-        uint64_t b = base[0];
-        bool f = fwd[0];
-#pragma unroll
-        for (int k = 1; k < NC; ++k) {
-            if (e >= S.cbase[k]) {
-                c = k;
-                b = base[k];
-                f = fwd[k];
-            }
-        }
-        const uint64_t r = uint64_t(S.excl.cnt[c]) + (e - S.cbase[c]);
-        const uint64_t pos = f ? b + r : b - r;
-        ox[pos] = S.sx[e];
-        oy[pos] = S.sy[e];
-        oid[pos] = S.sid[e];
-    }
-}
-
-// Claim the next tile (in increasing order — required by the look-back).
-// Returns false when the launch is drained; the last CTA to drain re-arms
-// the counter for the next launch.
-template <int NC>
-__device__ __forceinline__ bool claim_tile(TileSmem<NC>& S, uint32_t* ctr, uint32_t ntiles) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        const uint32_t t = atomicAdd(ctr, 1u);
-        S.tile = t;
-        if (t >= ntiles && t == ntiles + gridDim.x - 1) *ctr = 0;
-    }
-    __syncthreads();
-    return S.tile < ntiles;
-}
-
-// ===========================================================================
-// KB: root partition — hull levels 1 and 2 fused (probe P5).
-// Each input point is classified against the bootstrap edges p->q / q->p and
-// then against its side's two child edges, with the reference's
-// mask_b &= ~mask_a rule at both levels (kernels.hpp:91):
-//   class 0: S1 ∧ left(p->r1)        class 1: S1 ∧ ¬0 ∧ left(r1->q)
-//   class 2: S2 ∧ left(q->r2)        class 3: S2 ∧ ¬2 ∧ left(r2->p)
-// These are exactly the sets the reference's second-level extract_subsets
-// calls produce; r11..r22 come out of the same pass (fused arg-max).
-// Output layout: S1's range [0,|S1|) and S2's range [|S1|, |S1|+|S2|) of the
-// destination, each split two-sided like the reference's in-place pass.
-// ===========================================================================
-struct RootArgs {
-    const double* xs;
-    const double* ys;
-    uint64_t n;
-    const RootInfo* root;
-    double* ox;
-    double* oy;
-    uint32_t* oid;
-    uint32_t* flags;
-    Agg<4>* aggs;
-    Agg<4>* incs;
-    uint32_t epoch;
-    uint32_t* ctr;
-    ChildRec* children;  // 4 slots
-    uint32_t ntiles;
-};
-
-__global__ void __launch_bounds__(kThreads, kPartMinBlocks) root_partition_kernel(RootArgs a) {
-    __shared__ TileSmem<4> S;
-    const RootInfo& R = *a.root;
-    const double px = R.px, py = R.py, qx = R.qx, qy = R.qy;
-    const double r1x = R.r1.x, r1y = R.r1.y, r2x = R.r2.x, r2y = R.r2.y;
-    const uint32_t n1 = R.cnt1, n2 = R.cnt2;
-    if (threadIdx.x == 0) {
-        // child frames (kernels.hpp:23-25): 0: p->r1, 1: r1->q, 2: q->r2, 3: r2->p
-        S.fdx[0] = dsub(r1x, px); S.fdy[0] = dsub(r1y, py);
-        S.fdx[1] = dsub(qx, r1x); S.fdy[1] = dsub(qy, r1y);
-        S.fdx[2] = dsub(r2x, qx); S.fdy[2] = dsub(r2y, qy);
-        S.fdx[3] = dsub(px, r2x); S.fdy[3] = dsub(py, r2y);
-    }
-    uint64_t base[4];
-    const bool fwd[4] = {true, false, true, false};
-    base[0] = 0;
-    base[1] = uint64_t(n1) - 1;  // unused when empty
-    base[2] = n1;
-    base[3] = uint64_t(n1) + n2 - 1;
-
-    while (claim_tile(S, a.ctr, a.ntiles)) {
-        const uint32_t t = S.tile;
-        const uint64_t start = uint64_t(t) * kTile;
-        double ux[kItems], uy[kItems];
-        uint32_t uid[kItems];
-        int cls[kItems];
-#pragma unroll
-        for (int i = 0; i < kItems; ++i) {
-            const uint64_t pos = start + uint64_t(i) * kThreads + threadIdx.x;
-            const bool v = pos < a.n;
-            ux[i] = v ? ld_stream(a.xs + pos) : 0.0;
-            uy[i] = v ? ld_stream(a.ys + pos) : 0.0;
-            uid[i] = uint32_t(pos);
-            cls[i] = v ? 0 : 4;
-        }
-#pragma unroll
-        for (int i = 0; i < kItems; ++i) {
-            const double u = ux[i], w = uy[i];
-            const double A = dsub(px, u), B = dsub(py, w);
-            const double Cc = dsub(qx, u), D = dsub(qy, w);
-            const double t1 = dmul(A, D), t2 = dmul(B, Cc);
-            const bool s1 = t1 > t2;           // left of p->q
-            const bool s2 = !s1 && (t2 > t1);  // left of q->p
-            // second level, side-selected operands
-            const double rx = s1 ? r1x : r2x, ry = s1 ? r1y : r2y;
-            const double P1x = s1 ? A : Cc, P1y = s1 ? B : D;
-            const double Q2x = s1 ? Cc : A, Q2y = s1 ? D : B;
-            const double E = dsub(rx, u), F = dsub(ry, w);
-            const bool L = left_diff(P1x, P1y, E, F);         // left of (side start -> r)
-            const bool Rr = !L && left_diff(E, F, Q2x, Q2y);  // left of (r -> side end)
-            int c = 4;
-            if (s1) c = L ? 0 : (Rr ? 1 : 4);
-            else if (s2) c = L ? 2 : (Rr ? 3 : 4);
-            cls[i] = (cls[i] != 0) ? 4 : c;  // out of range stays unclassified
-        }
-        stage_tile<4>(S, ux, uy, uid, cls);
-        if (threadIdx.x < 32) {
-            lookback_agg<4>(t, 0u, S.local, S.excl, a.flags, a.aggs, a.incs, a.epoch);
-            if (threadIdx.x < 4 && t == a.ntiles - 1) {
-                // children slots: (p, r11, r1) (r1, r12, q) (q, r21, r2) (r2, r22, p)
-                const int c = threadIdx.x;
-                const Best b = prefer(S.local.best[c], S.excl.best[c]) ? S.local.best[c] : S.excl.best[c];
-                const uint32_t m = S.excl.cnt[c] + S.local.cnt[c];
-                ChildRec ch;
-                ch.px = c == 0 ? px : (c == 1 ? r1x : (c == 2 ? qx : r2x));
-                ch.py = c == 0 ? py : (c == 1 ? r1y : (c == 2 ? qy : r2y));
-                ch.qx = c == 0 ? r1x : (c == 1 ? qx : (c == 2 ? r2x : px));
-                ch.qy = c == 0 ? r1y : (c == 1 ? qy : (c == 2 ? r2y : py));
-                ch.rx = b.x;
-                ch.ry = b.y;
-                ch.r_idx = b.idx;
-                ch.m = m;
-                ch.begin = (c & 1) ? (c == 1 ? uint64_t(n1) - m : uint64_t(n1) + n2 - m)
-                                   : (c == 0 ? 0 : uint64_t(n1));
-                a.children[c] = ch;
-            }
-        }
-        __syncthreads();
-        flush_tile<4>(S, base, fwd, a.ox, a.oy, a.oid);
-    }
-}
-
-// ===========================================================================
-// K2: level kernel — the fused partition (extract_blocks) for every live
-// segment of one recursion level in ONE launch.  Tiles never straddle
-// segments; a segment's tiles are consecutive ids, so the decoupled
-// look-back runs inside the segment and its last tile knows the segment's
-// final counts and arg-maxes and emits the two child nodes.
-// GENERAL = two unrelated edges (the extract_subsets API); otherwise edges
-// p->r and r->q share r, which saves two subtractions per point.
-// ===========================================================================
-struct LevelArgs {
-    const SegRec* segs;
-    const uint32_t* tile_seg;
-    const LevelInfo* info;
-    const double* ix;
-    const double* iy;
-    const uint32_t* iid;
-    double* ox;
-    double* oy;
-    uint32_t* oid;
-    uint32_t* flags;
-    Agg<2>* aggs;
-    Agg<2>* incs;
-    uint32_t epoch;
-    uint32_t* ctr;
-    ChildRec* children;  // 2 per segment
-};
-
-template <bool GENERAL>
-__global__ void __launch_bounds__(kThreads, kPartMinBlocks) level_kernel(LevelArgs a) {
-    __shared__ TileSmem<2> S;
-    __shared__ SegRec s_seg;
-    if (threadIdx.x == 0) S.ntiles = a.info->ntiles;
-    __syncthreads();
-    const uint32_t ntiles = S.ntiles;
-    while (claim_tile(S, a.ctr, ntiles)) {
-        const uint32_t t = S.tile;
-        if (threadIdx.x == 0) {
-            S.seg = a.tile_seg[t];
-            s_seg = a.segs[S.seg];
-            S.fdx[0] = s_seg.adx; S.fdy[0] = s_seg.ady;
-            S.fdx[1] = s_seg.bdx; S.fdy[1] = s_seg.bdy;
-        }
-        __syncthreads();
-        const uint32_t j = t - s_seg.tile0;
-        const uint64_t start = s_seg.begin + uint64_t(j) * kTile;
-        const uint32_t cnt = min(uint32_t(kTile), s_seg.m - j * uint32_t(kTile));
-        double ux[kItems], uy[kItems];
-        uint32_t uid[kItems];
-        int cls[kItems];
-#pragma unroll
-        for (int i = 0; i < kItems; ++i) {
-            const uint32_t r = uint32_t(i) * kThreads + threadIdx.x;
-            const bool v = r < cnt;
-            ux[i] = v ? ld_stream(a.ix + start + r) : 0.0;
-            uy[i] = v ? ld_stream(a.iy + start + r) : 0.0;
-            uid[i] = v ? ld_stream(a.iid + start + r) : 0u;
-            cls[i] = v ? 0 : 2;
-        }
-        {
-            const double px = s_seg.px, py = s_seg.py, rx = s_seg.rx, ry = s_seg.ry;
-            const double qx = s_seg.qx, qy = s_seg.qy;
-#pragma unroll
-            for (int i = 0; i < kItems; ++i) {
-                const double u = ux[i], w = uy[i];
-                bool la, lb;
-                if (GENERAL) {
-                    la = left_diff(dsub(px, u), dsub(py, w), dsub(rx, u), dsub(ry, w));
-                    lb = !la && left_diff(dsub(s_seg.bx, u), dsub(s_seg.by, w), dsub(qx, u), dsub(qy, w));
-                } else {
-                    const double A = dsub(px, u), B = dsub(py, w);
-                    const double E = dsub(rx, u), F = dsub(ry, w);
-                    const double Cc = dsub(qx, u), D = dsub(qy, w);
-                    la = left_diff(A, B, E, F);
-                    lb = !la && left_diff(E, F, Cc, D);
-                }
-                cls[i] = (cls[i] != 0) ? 2 : (la ? 0 : (lb ? 1 : 2));
-            }
-        }
-        stage_tile<2>(S, ux, uy, uid, cls);
-        const uint64_t base[2] = {s_seg.out, s_seg.out + s_seg.m - 1};
-        const bool fwd[2] = {true, false};
-        if (threadIdx.x < 32) {
-            lookback_agg<2>(t, s_seg.tile0, S.local, S.excl, a.flags, a.aggs, a.incs, a.epoch);
-            if (threadIdx.x == 0) {
-                if (j == s_seg.ntiles - 1) {
-                    const SegRec& g = s_seg;
-                    Agg<2> inc = S.excl;
-                    agg_combine(inc, S.local);
-                    ChildRec L, Rr;
-                    L.px = g.px; L.py = g.py; L.qx = g.rx; L.qy = g.ry;
-                    L.rx = inc.best[0].x; L.ry = inc.best[0].y;
-                    L.r_idx = inc.best[0].idx; L.m = inc.cnt[0]; L.begin = g.out;
-                    Rr.px = GENERAL ? g.bx : g.rx; Rr.py = GENERAL ? g.by : g.ry;
-                    Rr.qx = g.qx; Rr.qy = g.qy;
-                    Rr.rx = inc.best[1].x; Rr.ry = inc.best[1].y;
-                    Rr.r_idx = inc.best[1].idx; Rr.m = inc.cnt[1];
-                    Rr.begin = g.out + g.m - inc.cnt[1];
-                    a.children[2 * S.seg] = L;
-                    a.children[2 * S.seg + 1] = Rr;
-                }
-            }
-        }
-        __syncthreads();
-        flush_tile<2>(S, base, fwd, a.ox, a.oy, a.oid);
-    }
-}
-
-// ===========================================================================
 // K3: planner — turns the child slots of a level into the next level's work:
 // internal segments (m > kFinMax, tiled), finisher segments (2..kFinMax),
 // leaves (m == 1: the node's chain is just its apex, hull.cpp:83) and empty
@@ -709,6 +345,8 @@ struct PlanArgs {
     PlanAgg* incs;
     uint32_t epoch;
     uint32_t* ctr;
+    uint32_t* seg_pcnt;
+    uint32_t* seg_done;
 };
 
 __device__ __forceinline__ uint8_t kind_of(uint32_t m) {
@@ -813,6 +451,8 @@ __global__ void __launch_bounds__(kThreads) planner_kernel(PlanArgs a) {
                 g.ntiles = (c.m + kTile - 1) / kTile;
                 g.slot = uint32_t(s);
                 a.segs[run.nseg] = g;
+                a.seg_pcnt[run.nseg] = 0;
+                a.seg_done[run.nseg] = 0;
                 a.link[s] = run.nseg;
                 run.nseg += 1;
                 run.ntiles += g.ntiles;
@@ -1091,37 +731,13 @@ size_t partial_bytes(int grid) {
                                                                       : sizeof(ExtPartial));
 }
 
-void launch_root_partition(const double* xs, const double* ys, uint64_t n, const RootInfo* root,
-                           double* ox, double* oy, uint32_t* oid, uint32_t* flags, void* aggs,
-                           void* incs, uint32_t epoch, uint32_t* ctr, ChildRec* children,
-                           int grid, cudaStream_t st) {
-    RootArgs a;
-    a.xs = xs; a.ys = ys; a.n = n; a.root = root;
-    a.ox = ox; a.oy = oy; a.oid = oid;
-    a.flags = flags; a.aggs = static_cast<Agg<4>*>(aggs); a.incs = static_cast<Agg<4>*>(incs);
-    a.epoch = epoch; a.ctr = ctr; a.children = children;
-    a.ntiles = uint32_t((n + kTile - 1) / kTile);
-    root_partition_kernel<<<grid, kThreads, 0, st>>>(a);
-}
-
-void launch_level(const SegRec* segs, const uint32_t* tile_seg, const LevelInfo* info,
-                  const double* ix, const double* iy, const uint32_t* iid, double* ox, double* oy,
-                  uint32_t* oid, uint32_t* flags, void* aggs, void* incs, uint32_t epoch,
-                  uint32_t* ctr, ChildRec* children, bool general, int grid, cudaStream_t st) {
-    LevelArgs a;
-    a.segs = segs; a.tile_seg = tile_seg; a.info = info;
-    a.ix = ix; a.iy = iy; a.iid = iid; a.ox = ox; a.oy = oy; a.oid = oid;
-    a.flags = flags; a.aggs = static_cast<Agg<2>*>(aggs); a.incs = static_cast<Agg<2>*>(incs);
-    a.epoch = epoch; a.ctr = ctr; a.children = children;
-    if (general) level_kernel<true><<<grid, kThreads, 0, st>>>(a);
-    else level_kernel<false><<<grid, kThreads, 0, st>>>(a);
-}
-
 void launch_planner(const ChildRec* slots, uint32_t nslots, SegRec* segs, FinRec* fins,
                     uint8_t* kind, uint32_t* link, LevelInfo* info, uint64_t fin_chain_base,
                     uint32_t* flags, void* aggs, void* incs, uint32_t epoch, uint32_t* ctr,
-                    int max_grid, cudaStream_t st) {
+                    uint32_t* seg_pcnt, uint32_t* seg_done, int max_grid, cudaStream_t st) {
     PlanArgs a;
+    a.seg_pcnt = seg_pcnt;
+    a.seg_done = seg_done;
     a.slots = slots; a.nslots = nslots;
     a.nchunks = (nslots + kPlanChunk - 1) / kPlanChunk;
     a.segs = segs; a.fins = fins; a.kind = kind; a.link = link; a.info = info;
@@ -1181,19 +797,8 @@ void launch_root_frame(const RootInfo* root, const uint32_t* size1, uint32_t* st
     root_frame_kernel<<<1, 32, 0, st>>>(root, size1, start1, out, h_out);
 }
 
-size_t agg_bytes(int nc) { return nc == 4 ? sizeof(Agg<4>) : sizeof(Agg<2>); }
 size_t plan_agg_bytes() { return sizeof(PlanAgg); }
 
-int occupancy_root() {
-    int b = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, root_partition_kernel, kThreads, 0);
-    return b;
-}
-int occupancy_level() {
-    int b = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, level_kernel<false>, kThreads, 0);
-    return b;
-}
 int occupancy_stream() {
     int a = 0, b = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, extremes_kernel, 256, 0);

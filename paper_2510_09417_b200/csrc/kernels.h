@@ -14,18 +14,12 @@ void launch_extremes(const double* xs, const double* ys, uint64_t n, void* parti
 void launch_bootstrap(const double* xs, const double* ys, uint64_t n, void* partials,
                       uint32_t* ticket, RootInfo* root, int grid, cudaStream_t st);
 size_t partial_bytes(int grid);
-void launch_root_partition(const double* xs, const double* ys, uint64_t n, const RootInfo* root,
-                           double* ox, double* oy, uint32_t* oid, uint32_t* flags, void* aggs,
-                           void* incs, uint32_t epoch, uint32_t* ctr, ChildRec* children,
-                           int grid, cudaStream_t st);
-void launch_level(const SegRec* segs, const uint32_t* tile_seg, const LevelInfo* info,
-                  const double* ix, const double* iy, const uint32_t* iid, double* ox, double* oy,
-                  uint32_t* oid, uint32_t* flags, void* aggs, void* incs, uint32_t epoch,
-                  uint32_t* ctr, ChildRec* children, bool general, int grid, cudaStream_t st);
+void launch_root_partition(const RootArgs& a, int grid, cudaStream_t st);
+void launch_level(const LevelArgs& a, bool general, int grid, cudaStream_t st);
 void launch_planner(const ChildRec* slots, uint32_t nslots, SegRec* segs, FinRec* fins,
                     uint8_t* kind, uint32_t* link, LevelInfo* info, uint64_t fin_chain_base,
                     uint32_t* flags, void* aggs, void* incs, uint32_t epoch, uint32_t* ctr,
-                    int max_grid, cudaStream_t st);
+                    uint32_t* seg_pcnt, uint32_t* seg_done, int max_grid, cudaStream_t st);
 void launch_tilemap(const SegRec* segs, const LevelInfo* info, uint32_t* tile_seg,
                     uint32_t ntiles_hint, cudaStream_t st);
 void launch_finisher(const FinRec* fins, const LevelInfo* info, const double* ix,
@@ -42,7 +36,6 @@ void launch_root_slots(const RootInfo* root, ChildRec* slots, uint8_t* kind, uin
                        cudaStream_t st);
 void launch_root_frame(const RootInfo* root, const uint32_t* size1, uint32_t* start1,
                        uint32_t* out, uint32_t* h_out, cudaStream_t st);
-size_t agg_bytes(int nc);
 size_t plan_agg_bytes();
 int occupancy_root();
 int occupancy_level();

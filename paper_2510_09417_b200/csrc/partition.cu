@@ -1,0 +1,566 @@
+// The fused partition kernels of the hot path (sm_100a):
+//
+//   KB  root_partition_kernel  hull levels 1+2 fused over the caller's input
+//   K2  level_kernel           every live segment of one recursion level
+//
+// Both are the reference's extract_blocks (extract_core.hpp:421-515): f64
+// orientation test against two edges with mask_b &= ~mask_a (kernels.hpp:91),
+// order-preserving two-sided compaction (S1 from the left end of the range,
+// S2 from the right end), and the fused farthest-point search in the
+// canonical order (kernels.hpp:36-45).
+//
+// GPU structure (persistent CTAs, tiles claimed in increasing order):
+//   load tile (prefetched during the previous tile's look-back)
+//   -> classify -> warp ballots -> block scan -> stage survivors in smem
+//   -> per-class arg-max over the staged survivors
+//   -> decoupled look-back on ONE self-contained 16-byte status word per tile
+//      (flag + two 32-bit counts; no payload arrays, no fences)
+//   -> coalesced stores of the staged survivors to their final positions.
+// The arg-max does not ride the look-back: each CTA keeps a running best per
+// segment and publishes it once per segment visit; the CTA that completes a
+// segment's tile count reduces those few partials and emits the children.
+#include <cstdint>
+
+#include "common.cuh"
+#include "hull_types.cuh"
+#include "kernels.h"
+
+namespace vqb {
+
+// ---------------------------------------------------------------------------
+// 16-byte status words
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void st_status(Status* p, uint32_t flag, uint32_t c0, uint32_t c1) {
+    asm volatile("st.relaxed.gpu.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(flag),
+                 "r"(c0), "r"(c1), "r"(0u)
+                 : "memory");
+}
+
+__device__ __forceinline__ uint4 ld_status(const Status* p) {
+    uint4 v;
+    asm volatile("ld.relaxed.gpu.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p)
+                 : "memory");
+    return v;
+}
+
+// Decoupled look-back over status words st[t * stride + side]; run by one
+// full warp.  Returns the exclusive prefix (c0, c1) of `tile` within the
+// segment whose first tile is `first`.
+__device__ uint2 lookback16(uint32_t tile, uint32_t first, uint32_t c0, uint32_t c1, Status* st,
+                            uint32_t stride, uint32_t side, uint32_t epoch) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t hi = epoch << 2;
+    if (tile == first) {
+        if (lane == 0) st_status(&st[uint64_t(tile) * stride + side], hi | kStInc, c0, c1);
+        return make_uint2(0u, 0u);
+    }
+    if (lane == 0) st_status(&st[uint64_t(tile) * stride + side], hi | kStAgg, c0, c1);
+    uint32_t acc0 = 0, acc1 = 0;
+    int64_t pred = int64_t(tile) - 1;
+    while (true) {
+        const int64_t t = pred - lane;
+        const bool in_seg = t >= int64_t(first);
+        uint4 w = make_uint4(0u, 0u, 0u, 0u);
+        if (in_seg) {
+            uint32_t spins = 0;
+            while (true) {
+                w = ld_status(&st[uint64_t(t) * stride + side]);
+                if ((w.x & ~3u) == hi && (w.x & 3u) != 0) break;
+                if (++spins > 2) __nanosleep(32);
+                if (spins > (1u << 26)) {  // a bug, never wait forever
+                    g_vqb_fault = 1u;
+                    w.x = hi | kStInc;
+                    w.y = w.z = 0;
+                    break;
+                }
+            }
+        }
+        const unsigned inc_mask = __ballot_sync(kFull, in_seg && (w.x & 3u) == kStInc);
+        const int stop = inc_mask ? (__ffs(inc_mask) - 1) : 31;
+        const bool take = in_seg && lane <= stop;
+        uint32_t v0 = take ? w.y : 0u, v1 = take ? w.z : 0u;
+#pragma unroll
+        for (int s = 16; s > 0; s >>= 1) {
+            v0 += __shfl_xor_sync(kFull, v0, s);
+            v1 += __shfl_xor_sync(kFull, v1, s);
+        }
+        acc0 += v0;
+        acc1 += v1;
+        const unsigned seg_mask = __ballot_sync(kFull, in_seg);
+        if (inc_mask || seg_mask != kFull) break;
+        pred -= 32;
+    }
+    if (lane == 0) st_status(&st[uint64_t(tile) * stride + side], hi | kStInc, acc0 + c0, acc1 + c1);
+    return make_uint2(acc0, acc1);
+}
+
+// ---------------------------------------------------------------------------
+// Tile staging
+// ---------------------------------------------------------------------------
+template <int NC>
+struct TileSmem {
+    double sx[kTile];
+    double sy[kTile];
+    uint32_t sid[kTile];
+    uint32_t wcnt[NC][kItems * kWarps];
+    uint32_t cbase[NC + 1];
+    uint32_t cnt[NC];    // tile counts per class
+    uint32_t excl[NC];   // exclusive prefix inside the segment (look-back)
+    double fdx[NC], fdy[NC];  // class frames for the arg-max
+    Best wbest[NC][kWarps];
+    Best best[NC];       // tile arg-max per class
+    uint32_t tile;
+};
+
+// cls[i] == NC means "no class".  On return the survivors are staged in input
+// order, class by class, and S.cnt / S.best hold the tile's counts and
+// per-class canonical arg-max (offsets from the class frames S.fdx/S.fdy).
+template <int NC>
+__device__ __forceinline__ void stage_tile(TileSmem<NC>& S, const double (&ux)[kItems],
+                                           const double (&uy)[kItems],
+                                           const uint32_t (&uid)[kItems], const int (&cls)[kItems]) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const unsigned lt = lanemask_lt();
+    uint32_t rk[kItems];
+#pragma unroll
+    for (int i = 0; i < kItems; ++i) {
+        rk[i] = 0;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+            const unsigned bal = __ballot_sync(kFull, cls[i] == c);
+            if (lane == 0) S.wcnt[c][i * kWarps + warp] = __popc(bal);
+            if (cls[i] == c) rk[i] = __popc(bal & lt);
+        }
+    }
+    __syncthreads();
+    static_assert(kItems * kWarps == 32, "one scan entry per lane");
+    if (warp < NC) {
+        const int c = warp;
+        const uint32_t v = S.wcnt[c][lane];
+        uint32_t incl = v;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t o = __shfl_up_sync(kFull, incl, d);
+            if (lane >= d) incl += o;
+        }
+        S.wcnt[c][lane] = incl - v;
+        if (lane == 31) S.cnt[c] = incl;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t acc = 0;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+            S.cbase[c] = acc;
+            acc += S.cnt[c];
+        }
+        S.cbase[NC] = acc;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < kItems; ++i) {
+        const int c = cls[i];
+        if (c < NC) {
+            const uint32_t s = S.cbase[c] + S.wcnt[c][i * kWarps + warp] + rk[i];
+            S.sx[s] = ux[i];
+            S.sy[s] = uy[i];
+            S.sid[s] = uid[i];
+        }
+    }
+    __syncthreads();
+    // arg-max per class over the staged (contiguous) survivors
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        const double edx = S.fdx[c], edy = S.fdy[c];
+        Best b = best_none();
+        for (uint32_t e = S.cbase[c] + threadIdx.x; e < S.cbase[c + 1]; e += kThreads) {
+            const double u = S.sx[e], w = S.sy[e];
+            consider(b, true, lat_off(edx, edy, u, w), u, w, S.sid[e]);
+        }
+        b = warp_best(b);
+        if (lane == 0) S.wbest[c][warp] = b;
+    }
+    __syncthreads();
+    if (warp < NC) {
+        Best b = lane < kWarps ? S.wbest[warp][lane] : best_none();
+        b = warp_best(b);
+        if (lane == 0) S.best[warp] = b;
+    }
+    __syncthreads();
+}
+
+// Stream the staged survivors to their final places.  base[c] is the first
+// (fwd) / last (bwd) position of class c in its range.
+template <int NC>
+__device__ __forceinline__ void flush_tile(const TileSmem<NC>& S, const uint64_t (&base)[NC],
+                                           const bool (&fwd)[NC], double* __restrict__ ox,
+                                           double* __restrict__ oy, uint32_t* __restrict__ oid) {
+    const uint32_t total = S.cbase[NC];
+    for (uint32_t e = threadIdx.x; e < total; e += kThreads) {
+        int c = 0;
+        uint64_t b = base[0];
+        bool f = fwd[0];
+#pragma unroll
+        for (int k = 1; k < NC; ++k) {
+            if (e >= S.cbase[k]) {
+                c = k;
+                b = base[k];
+                f = fwd[k];
+            }
+        }
+        const uint64_t r = uint64_t(S.excl[c]) + (e - S.cbase[c]);
+        const uint64_t pos = f ? b + r : b - r;
+        ox[pos] = S.sx[e];
+        oy[pos] = S.sy[e];
+        oid[pos] = S.sid[e];
+    }
+}
+
+// Claim the next tile in increasing order.  The last CTA to drain re-arms
+// the counter for the next launch.
+__device__ __forceinline__ uint32_t claim(uint32_t* s_tile, uint32_t* ctr, uint32_t ntiles) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const uint32_t t = atomicAdd(ctr, 1u);
+        *s_tile = t;
+        if (t >= ntiles && t == ntiles + gridDim.x - 1) *ctr = 0;
+    }
+    __syncthreads();
+    return *s_tile;
+}
+
+__device__ __forceinline__ Best ldcg_best(const Best* p) {
+    Best b;
+    b.off = __ldcg(&p->off);
+    b.x = __ldcg(&p->x);
+    b.y = __ldcg(&p->y);
+    b.idx = __ldcg(&p->idx);
+    b.valid = __ldcg(&p->valid);
+    return b;
+}
+
+// ===========================================================================
+// KB: root partition — hull levels 1 and 2 fused (probe P5).
+// Each input point is classified against the bootstrap edges p->q / q->p and
+// then against its side's two child edges:
+//   class 0: S1 ∧ left(p->r1)        class 1: S1 ∧ ¬0 ∧ left(r1->q)
+//   class 2: S2 ∧ left(q->r2)        class 3: S2 ∧ ¬2 ∧ left(r2->p)
+// exactly the sets of the reference's two second-level extract_subsets calls,
+// with r11..r22 from the same pass.  Output: S1's range [0,|S1|) and S2's
+// range [|S1|, |S1|+|S2|), each split two-sided.  Two status words per tile
+// (side S1: classes 0/1, side S2: classes 2/3), looked back by warps 0 and 1.
+// ===========================================================================
+__global__ void __launch_bounds__(kThreads, kPartMinBlocks) root_partition_kernel(RootArgs a) {
+    __shared__ TileSmem<4> S;
+    __shared__ Best s_run[4];
+    __shared__ bool s_last;
+    const RootInfo& R = *a.root;
+    const double px = R.px, py = R.py, qx = R.qx, qy = R.qy;
+    const double r1x = R.r1.x, r1y = R.r1.y, r2x = R.r2.x, r2y = R.r2.y;
+    const uint32_t n1 = R.cnt1, n2 = R.cnt2;
+    if (threadIdx.x == 0) {
+        // child frames (kernels.hpp:23-25): 0: p->r1, 1: r1->q, 2: q->r2, 3: r2->p
+        S.fdx[0] = dsub(r1x, px); S.fdy[0] = dsub(r1y, py);
+        S.fdx[1] = dsub(qx, r1x); S.fdy[1] = dsub(qy, r1y);
+        S.fdx[2] = dsub(r2x, qx); S.fdy[2] = dsub(r2y, qy);
+        S.fdx[3] = dsub(px, r2x); S.fdy[3] = dsub(py, r2y);
+    }
+    if (threadIdx.x < 4) s_run[threadIdx.x] = best_none();
+    uint64_t base[4];
+    const bool fwd[4] = {true, false, true, false};
+    base[0] = 0;
+    base[1] = uint64_t(n1) - 1;  // unused when empty
+    base[2] = n1;
+    base[3] = uint64_t(n1) + n2 - 1;
+
+    double ux[kItems], uy[kItems];
+    uint32_t uid[kItems];
+    bool inr[kItems];
+    auto load = [&](uint32_t t) {
+        const uint64_t start = uint64_t(t) * kTile;
+#pragma unroll
+        for (int i = 0; i < kItems; ++i) {
+            const uint64_t pos = start + uint64_t(i) * kThreads + threadIdx.x;
+            inr[i] = pos < a.n;
+            ux[i] = inr[i] ? ld_stream(a.xs + pos) : 0.0;
+            uy[i] = inr[i] ? ld_stream(a.ys + pos) : 0.0;
+            uid[i] = uint32_t(pos);
+        }
+    };
+    uint32_t t = claim(&S.tile, a.ctr, a.ntiles);
+    if (t < a.ntiles) load(t);
+    while (t < a.ntiles) {
+        int cls[kItems];
+#pragma unroll
+        for (int i = 0; i < kItems; ++i) {
+            const double u = ux[i], w = uy[i];
+            const double A = dsub(px, u), B = dsub(py, w);
+            const double Cc = dsub(qx, u), D = dsub(qy, w);
+            const double t1 = dmul(A, D), t2 = dmul(B, Cc);
+            const bool s1 = t1 > t2;           // left of p->q
+            const bool s2 = !s1 && (t2 > t1);  // left of q->p
+            // second level, side-selected operands
+            const double rx = s1 ? r1x : r2x, ry = s1 ? r1y : r2y;
+            const double P1x = s1 ? A : Cc, P1y = s1 ? B : D;
+            const double Q2x = s1 ? Cc : A, Q2y = s1 ? D : B;
+            const double E = dsub(rx, u), F = dsub(ry, w);
+            const bool L = left_diff(P1x, P1y, E, F);         // left of (side start -> r)
+            const bool Rr = !L && left_diff(E, F, Q2x, Q2y);  // left of (r -> side end)
+            int c = 4;
+            if (s1) c = L ? 0 : (Rr ? 1 : 4);
+            else if (s2) c = L ? 2 : (Rr ? 3 : 4);
+            cls[i] = inr[i] ? c : 4;
+        }
+        stage_tile<4>(S, ux, uy, uid, cls);
+        if (threadIdx.x < 4 && prefer(S.best[threadIdx.x], s_run[threadIdx.x]))
+            s_run[threadIdx.x] = S.best[threadIdx.x];
+        const uint32_t tn = claim(&S.tile, a.ctr, a.ntiles);
+        if (tn < a.ntiles) load(tn);  // in flight during the look-back and the stores
+        if (threadIdx.x < 64) {
+            const uint32_t side = threadIdx.x >> 5;
+            const uint2 e = lookback16(t, 0u, S.cnt[2 * side], S.cnt[2 * side + 1], a.status, 2u,
+                                       side, a.epoch);
+            if ((threadIdx.x & 31) == 0) {
+                S.excl[2 * side] = e.x;
+                S.excl[2 * side + 1] = e.y;
+            }
+        }
+        __syncthreads();
+        flush_tile<4>(S, base, fwd, a.ox, a.oy, a.oid);
+        t = tn;
+    }
+    // per-CTA arg-max partials; the last CTA out reduces them and emits the
+    // four child nodes (counts from the last tile's inclusive status words)
+    __syncthreads();
+    if (threadIdx.x < 4) a.cta_part[blockIdx.x * 4 + threadIdx.x] = s_run[threadIdx.x];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        s_last = atomicAdd(a.ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp < 4) {
+        const int c = warp;
+        Best b = best_none();
+        for (uint32_t k = lane; k < gridDim.x; k += 32) {
+            const Best o = ldcg_best(&a.cta_part[k * 4 + c]);
+            if (prefer(o, b)) b = o;
+        }
+        b = warp_best(b);
+        if (lane == 0) {
+            uint32_t m = 0;
+            if (a.ntiles) {
+                const uint4 w = ld_status(&a.status[uint64_t(a.ntiles - 1) * 2 + (c >> 1)]);
+                m = (c & 1) ? w.z : w.y;
+            }
+            ChildRec ch;
+            // children: (p, r11, r1) (r1, r12, q) (q, r21, r2) (r2, r22, p)
+            ch.px = c == 0 ? px : (c == 1 ? r1x : (c == 2 ? qx : r2x));
+            ch.py = c == 0 ? py : (c == 1 ? r1y : (c == 2 ? qy : r2y));
+            ch.qx = c == 0 ? r1x : (c == 1 ? qx : (c == 2 ? r2x : px));
+            ch.qy = c == 0 ? r1y : (c == 1 ? qy : (c == 2 ? r2y : py));
+            ch.rx = b.x;
+            ch.ry = b.y;
+            ch.r_idx = b.idx;
+            ch.m = m;
+            ch.begin = (c & 1) ? (c == 1 ? uint64_t(n1) - m : uint64_t(n1) + n2 - m)
+                               : (c == 0 ? 0 : uint64_t(n1));
+            a.children[c] = ch;
+        }
+    }
+    if (threadIdx.x == 0) *a.ticket = 0;
+}
+
+// ===========================================================================
+// K2: level kernel — all live segments of one recursion level in one launch.
+// Tiles never straddle segments; a segment's tiles are consecutive ids.
+// GENERAL = two unrelated edges (the extract_subsets API); otherwise the
+// edges p->r and r->q share r (two subtractions saved per point).
+// ===========================================================================
+template <bool GENERAL>
+__global__ void __launch_bounds__(kThreads, kPartMinBlocks) level_kernel(LevelArgs a) {
+    __shared__ TileSmem<2> S;
+    __shared__ SegRec s_seg[2];
+    __shared__ uint32_t s_k[2];
+    __shared__ SegRec s_cur;  // segment whose arg-max this CTA is accumulating
+    __shared__ uint32_t s_cur_k, s_cur_tiles;
+    __shared__ Best s_run[2];
+    __shared__ bool s_last;
+    __shared__ uint32_t s_ntiles;
+    if (threadIdx.x == 0) {
+        s_ntiles = a.info->ntiles;
+        s_cur_k = 0xffffffffu;
+        s_cur_tiles = 0;
+    }
+    __syncthreads();
+    const uint32_t ntiles = s_ntiles;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    // publish this CTA's running best for s_cur; the CTA completing the
+    // segment's tile count reduces all partials and emits the two children
+    auto finalize = [&]() {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const uint32_t k = s_cur_k;
+            const uint32_t slot = atomicAdd(&a.seg_pcnt[k], 1u);
+            a.tile_part[2 * (uint64_t(s_cur.tile0) + slot)] = s_run[0];
+            a.tile_part[2 * (uint64_t(s_cur.tile0) + slot) + 1] = s_run[1];
+            __threadfence();
+            const uint32_t done = atomicAdd(&a.seg_done[k], s_cur_tiles) + s_cur_tiles;
+            s_last = (done == s_cur.ntiles);
+        }
+        __syncthreads();
+        if (s_last) {
+            __threadfence();
+            if (warp < 2) {
+                const int c = warp;
+                const uint32_t np = __ldcg(&a.seg_pcnt[s_cur_k]);
+                Best b = best_none();
+                for (uint32_t j = lane; j < np; j += 32) {
+                    const Best o = ldcg_best(&a.tile_part[2 * (uint64_t(s_cur.tile0) + j) + c]);
+                    if (prefer(o, b)) b = o;
+                }
+                b = warp_best(b);
+                if (lane == 0) {
+                    const SegRec& g = s_cur;
+                    const uint4 w = ld_status(&a.status[uint64_t(g.tile0) + g.ntiles - 1]);
+                    const uint32_t m = c == 0 ? w.y : w.z;
+                    ChildRec ch;
+                    if (c == 0) {  // left of p->r: triangle (p, rL, r)
+                        ch.px = g.px; ch.py = g.py; ch.qx = g.rx; ch.qy = g.ry;
+                        ch.begin = g.out;
+                    } else {       // left of r->q: triangle (r, rR, q)
+                        ch.px = GENERAL ? g.bx : g.rx; ch.py = GENERAL ? g.by : g.ry;
+                        ch.qx = g.qx; ch.qy = g.qy;
+                        ch.begin = g.out + g.m - m;
+                    }
+                    ch.rx = b.x;
+                    ch.ry = b.y;
+                    ch.r_idx = b.idx;
+                    ch.m = m;
+                    a.children[2 * uint64_t(s_cur_k) + c] = ch;
+                }
+            }
+        }
+        __syncthreads();
+    };
+
+    double ux[kItems], uy[kItems];
+    uint32_t uid[kItems];
+    uint32_t cnt = 0;
+    auto fetch = [&](uint32_t t, int b) {  // segment record of tile t -> s_seg[b], then loads
+        if (threadIdx.x == 0) {
+            const uint32_t k = a.tile_seg[t];
+            s_k[b] = k;
+            s_seg[b] = a.segs[k];
+        }
+        __syncthreads();
+        const SegRec& g = s_seg[b];
+        const uint32_t j = t - g.tile0;
+        const uint64_t start = g.begin + uint64_t(j) * kTile;
+        cnt = min(uint32_t(kTile), g.m - j * uint32_t(kTile));
+#pragma unroll
+        for (int i = 0; i < kItems; ++i) {
+            const uint32_t r = uint32_t(i) * kThreads + threadIdx.x;
+            const bool v = r < cnt;
+            ux[i] = v ? ld_stream(a.ix + start + r) : 0.0;
+            uy[i] = v ? ld_stream(a.iy + start + r) : 0.0;
+            uid[i] = v ? ld_stream(a.iid + start + r) : 0u;
+        }
+    };
+
+    int b = 0;
+    uint32_t t = claim(&S.tile, a.ctr, ntiles);
+    if (t < ntiles) fetch(t, b);
+    while (t < ntiles) {
+        const SegRec& g = s_seg[b];
+        if (threadIdx.x == 0) {
+            S.fdx[0] = g.adx; S.fdy[0] = g.ady;
+            S.fdx[1] = g.bdx; S.fdy[1] = g.bdy;
+        }
+        int cls[kItems];
+        {
+            const double px = g.px, py = g.py, rx = g.rx, ry = g.ry, qx = g.qx, qy = g.qy;
+#pragma unroll
+            for (int i = 0; i < kItems; ++i) {
+                const double u = ux[i], w = uy[i];
+                bool la, lb;
+                if (GENERAL) {
+                    la = left_diff(dsub(px, u), dsub(py, w), dsub(rx, u), dsub(ry, w));
+                    lb = !la && left_diff(dsub(g.bx, u), dsub(g.by, w), dsub(qx, u), dsub(qy, w));
+                } else {
+                    const double A = dsub(px, u), B = dsub(py, w);
+                    const double E = dsub(rx, u), F = dsub(ry, w);
+                    const double Cc = dsub(qx, u), D = dsub(qy, w);
+                    la = left_diff(A, B, E, F);
+                    lb = !la && left_diff(E, F, Cc, D);
+                }
+                const bool v = uint32_t(i) * kThreads + threadIdx.x < cnt;
+                cls[i] = !v ? 2 : (la ? 0 : (lb ? 1 : 2));
+            }
+        }
+        stage_tile<2>(S, ux, uy, uid, cls);
+        const uint64_t base[2] = {g.out, g.out + g.m - 1};
+        const bool fwd[2] = {true, false};
+        const uint32_t tile0 = g.tile0;
+        const uint32_t tn = claim(&S.tile, a.ctr, ntiles);
+        if (tn < ntiles) fetch(tn, b ^ 1);  // in flight during the look-back and the stores
+        if (warp == 0) {
+            const uint2 e = lookback16(t, tile0, S.cnt[0], S.cnt[1], a.status, 1u, 0u, a.epoch);
+            if (lane == 0) {
+                S.excl[0] = e.x;
+                S.excl[1] = e.y;
+            }
+        }
+        __syncthreads();
+        flush_tile<2>(S, base, fwd, a.ox, a.oy, a.oid);
+        // running arg-max of the segment this tile belongs to
+        if (s_k[b] != s_cur_k) {
+            if (s_cur_k != 0xffffffffu) finalize();
+            if (threadIdx.x == 0) {
+                s_cur = s_seg[b];
+                s_cur_k = s_k[b];
+                s_cur_tiles = 0;
+                s_run[0] = best_none();
+                s_run[1] = best_none();
+            }
+            __syncthreads();
+        }
+        if (threadIdx.x < 2 && prefer(S.best[threadIdx.x], s_run[threadIdx.x]))
+            s_run[threadIdx.x] = S.best[threadIdx.x];
+        if (threadIdx.x == 0) ++s_cur_tiles;
+        t = tn;
+        b ^= 1;
+    }
+    if (s_cur_k != 0xffffffffu) finalize();
+}
+
+// ===========================================================================
+// launchers
+// ===========================================================================
+void launch_root_partition(const RootArgs& a, int grid, cudaStream_t st) {
+    root_partition_kernel<<<grid, kThreads, 0, st>>>(a);
+}
+
+void launch_level(const LevelArgs& a, bool general, int grid, cudaStream_t st) {
+    if (general) level_kernel<true><<<grid, kThreads, 0, st>>>(a);
+    else level_kernel<false><<<grid, kThreads, 0, st>>>(a);
+}
+
+int occupancy_root() {
+    int b = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, root_partition_kernel, kThreads, 0);
+    return b;
+}
+int occupancy_level() {
+    int b = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, level_kernel<false>, kThreads, 0);
+    return b;
+}
+
+}  // namespace vqb
