@@ -33,7 +33,9 @@ __all__ = [
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libvqhull_b200.so")
+# VQHULL_LIB selects another build of the same library (e.g. the debug build
+# lib/libvqhull_b200_dbg.so with device bounds checks)
+LIB_PATH = os.environ.get("VQHULL_LIB", os.path.join(HERE, "lib", "libvqhull_b200.so"))
 
 VQHULL_OK, VQHULL_EINVAL, VQHULL_ESIZE, VQHULL_ECUDA = 0, 1, 2, 3
 KINDS = {"kuzmin": 0, "circle": 1, "disk": 2, "square": 3}

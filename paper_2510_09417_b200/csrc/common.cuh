@@ -17,7 +17,26 @@ constexpr unsigned kFull = 0xffffffffu;
 
 // set by a kernel that detected an impossible state (bounded spin expired,
 // runaway loop); the driver checks it after every hull and reports an error
-static __device__ uint32_t g_vqb_fault = 0;  // per-TU; only kernels.cu launches kernels
+static __device__ uint32_t g_vqb_fault = 0;
+// debug builds (-DVQB_DEBUG) record the first failed bounds check here
+static __device__ unsigned long long g_vqb_dbg[4];
+#ifdef VQB_DEBUG
+#define VQB_CHECK(cond, code, a0, a1)                                        \
+    do {                                                                     \
+        if (!(cond)) {                                                       \
+            if (atomicCAS(&g_vqb_fault, 0u, (unsigned)(code)) == 0u) {       \
+                g_vqb_dbg[0] = (unsigned long long)(a0);                     \
+                g_vqb_dbg[1] = (unsigned long long)(a1);                     \
+                g_vqb_dbg[2] = blockIdx.x;                                   \
+                g_vqb_dbg[3] = threadIdx.x;                                  \
+            }                                                                \
+        }                                                                    \
+    } while (0)
+#else
+#define VQB_CHECK(cond, code, a0, a1) \
+    do {                              \
+    } while (0)
+#endif  // per-TU; only kernels.cu launches kernels
 
 // ---------------------------------------------------------------------------
 // Canonical farthest order (kernels.hpp:36-45): the strictly smaller lateral

@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <deque>
 #include <memory>
@@ -36,6 +37,9 @@ struct CudaError {
 inline void ck(cudaError_t e, const char* what) {
     if (e != cudaSuccess) {
         g_last_error = std::string(what) + ": " + cudaGetErrorString(e);
+#ifdef VQB_DEBUG
+        fprintf(stderr, "[vqb debug] %s; device fault word %u\n", g_last_error.c_str(), read_and_clear_fault());
+#endif
         throw CudaError{e};
     }
 }
@@ -155,6 +159,7 @@ class Engine {
             RootArgs ra;
             ra.xs = dx; ra.ys = dy; ra.n = n; ra.root = root_;
             ra.ox = bufs_[0].x.as<double>(); ra.oy = bufs_[0].y.as<double>(); ra.oid = bufs_[0].id.as<uint32_t>();
+            ra.out_cap = bufs_[0].x.cap / 8;
             ra.status = status_.as<Status>(); ra.epoch = next_epoch();
             ra.ctr = &ctrs_[0]; ra.ticket = &ctrs_[4]; ra.cta_part = part_.as<Best>();
             ra.children = L2.slots.as<ChildRec>(); ra.ntiles = ntiles_root;
@@ -244,6 +249,9 @@ class Engine {
                 la.segs = Tc.segs.as<SegRec>(); la.tile_seg = tile_seg_.as<uint32_t>(); la.info = dinfo;
                 la.ix = bufs_[in].x.as<double>(); la.iy = bufs_[in].y.as<double>(); la.iid = bufs_[in].id.as<uint32_t>();
                 la.ox = bufs_[out].x.as<double>(); la.oy = bufs_[out].y.as<double>(); la.oid = bufs_[out].id.as<uint32_t>();
+                la.in_cap = bufs_[in].x.cap / 8; la.out_cap = bufs_[out].x.cap / 8;
+                la.status_cap = status_.cap / sizeof(Status); la.part_cap = part_.cap / sizeof(Best);
+                la.children_cap = Tn.slots.cap / sizeof(ChildRec); la.segs_cap = segaux_.cap / 8;
                 la.status = status_.as<Status>(); la.epoch = next_epoch(); la.ctr = &ctrs_[1];
                 la.tile_part = part_.as<Best>();
                 la.seg_pcnt = segaux_.as<uint32_t>(); la.seg_done = segaux_.as<uint32_t>() + nslots;
@@ -360,6 +368,9 @@ class Engine {
         la.segs = dseg; la.tile_seg = tile_seg_.as<uint32_t>(); la.info = dli;
         la.ix = bufs_[0].x.as<double>(); la.iy = bufs_[0].y.as<double>(); la.iid = bufs_[0].id.as<uint32_t>();
         la.ox = bufs_[1].x.as<double>(); la.oy = bufs_[1].y.as<double>(); la.oid = bufs_[1].id.as<uint32_t>();
+        la.in_cap = bufs_[0].x.cap / 8; la.out_cap = bufs_[1].x.cap / 8;
+        la.status_cap = status_.cap / sizeof(Status); la.part_cap = part_.cap / sizeof(Best);
+        la.children_cap = 2; la.segs_cap = 1;
         la.status = status_.as<Status>(); la.epoch = next_epoch(); la.ctr = &ctrs_[1];
         la.tile_part = part_.as<Best>();
         la.seg_pcnt = segaux_.as<uint32_t>(); la.seg_done = segaux_.as<uint32_t>() + 1;
@@ -459,9 +470,16 @@ class Engine {
             f();
         }
         ++launches_;
-        track_slots();
+        if (sync_each_) {  // VQHULL_SYNC_EACH=1: localize a faulting launch
+            static const char* names[6] = {"extremes", "bootstrap", "root_partition", "level",
+                                           "finisher", "planner/tilemap/emit"};
+            char buf[96];
+            snprintf(buf, sizeof buf, "launch %u (%s)", launches_, names[family]);
+            ck(cudaStreamSynchronize(st), buf);
+            ck(cudaGetLastError(), buf);
+        }
     }
-    void track_slots() {}
+    bool sync_each_ = getenv("VQHULL_SYNC_EACH") != nullptr;
 
     cudaEvent_t event() {
         if (ev_used_ == events_.size()) {

@@ -80,11 +80,12 @@ struct LevelInfo {
     uint32_t pad;
 };
 
-// Look-back status word of the partition kernels: flag (epoch << 2 | state)
-// and two 32-bit class counts in ONE 16-byte word, so a reader never needs a
-// payload that could be stale relative to the flag.
+// Look-back status of one tile (one side) of the partition kernels: two
+// 8-byte words for the aggregate and two for the inclusive prefix, each
+// {tag = epoch << 2 | state, 32-bit count} (see partition.cu).
 struct __align__(16) Status {
-    uint32_t flag, c0, c1, pad;
+    unsigned long long agg[2];
+    unsigned long long inc[2];
 };
 
 struct RootArgs {
@@ -95,6 +96,7 @@ struct RootArgs {
     double* ox;
     double* oy;
     uint32_t* oid;
+    uint64_t out_cap;    // debug bounds
     Status* status;      // 2 per tile (side S1, side S2)
     uint32_t epoch;
     uint32_t* ctr;       // tile claim counter
@@ -114,6 +116,8 @@ struct LevelArgs {
     double* ox;
     double* oy;
     uint32_t* oid;
+    uint64_t in_cap, out_cap;  // debug bounds
+    uint64_t status_cap, part_cap, children_cap, segs_cap;
     Status* status;      // 1 per tile
     uint32_t epoch;
     uint32_t* ctr;

@@ -14,6 +14,7 @@
 //                               (explicit stack)           hull.cpp:119-190
 //   K4  size/emit kernels       in-order chain assembly    hull.cpp:59-73, 259-266
 #include <cfloat>
+#include <cstdio>
 #include <cstdint>
 
 #include "common.cuh"
@@ -525,6 +526,7 @@ __global__ void __launch_bounds__(kFinWarps * 32) finisher_kernel(
     for (uint32_t f = blockIdx.x * kFinWarps + warp; f < nfin; f += gridDim.x * kFinWarps) {
         const FinRec rec = fins[f];
         const uint32_t m = rec.c.m;
+        VQB_CHECK(m >= 2 && m <= kFinMax, 30, m, f);
         for (uint32_t i = lane; i < m; i += 32) {
             S.x[i] = ix[rec.c.begin + i];
             S.y[i] = iy[rec.c.begin + i];
@@ -609,6 +611,7 @@ __global__ void __launch_bounds__(kFinWarps * 32) finisher_kernel(
                 if (nL) ++depth;
             } else if (fr.phase == 1) {
                 if (lane == 0) {
+                    VQB_CHECK(emitted < m, 31, emitted, m);
                     chain[cbase + emitted] = S.gid[fr.r];
                     FinFrame& cur = S.stack[depth - 1];
                     if (fr.rcnt) {
@@ -817,6 +820,13 @@ namespace vqb {
 uint32_t read_and_clear_fault() {
     uint32_t v = 0;
     cudaMemcpyFromSymbol(&v, g_vqb_fault, sizeof v);
+#ifdef VQB_DEBUG
+    if (v) {
+        unsigned long long d[4];
+        cudaMemcpyFromSymbol(d, g_vqb_dbg, sizeof d);
+        fprintf(stderr, "[vqb debug] fault %u: a0=%llu a1=%llu block=%llu thread=%llu\n", v, d[0], d[1], d[2], d[3]);
+    }
+#endif
     if (v) {
         const uint32_t z = 0;
         cudaMemcpyToSymbol(g_vqb_fault, &z, sizeof z);

@@ -28,21 +28,36 @@
 namespace vqb {
 
 // ---------------------------------------------------------------------------
-// 16-byte status words
+// Look-back status words.  Every word is 8 bytes = {tag: epoch<<2 | state,
+// count: 32 bits}, so each one validates itself under PTX's 8-byte
+// single-copy atomicity; aggregate and inclusive values live in separate
+// slots, so a reader can never combine a fresh flag with stale counts.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void st_status(Status* p, uint32_t flag, uint32_t c0, uint32_t c1) {
-    asm volatile("st.relaxed.gpu.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(flag),
-                 "r"(c0), "r"(c1), "r"(0u)
+__device__ __forceinline__ void pub_pair(unsigned long long* p, uint32_t tag, uint32_t c0,
+                                         uint32_t c1) {
+    const unsigned long long w0 = (static_cast<unsigned long long>(tag) << 32) | c0;
+    const unsigned long long w1 = (static_cast<unsigned long long>(tag) << 32) | c1;
+    asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(w0), "l"(w1)
                  : "memory");
 }
 
-__device__ __forceinline__ uint4 ld_status(const Status* p) {
-    uint4 v;
-    asm volatile("ld.relaxed.gpu.global.v4.u32 {%0, %1, %2, %3}, [%4];"
-                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+__device__ __forceinline__ ulonglong2 ld_pair(const unsigned long long* p) {
+    ulonglong2 v;
+    asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];"
+                 : "=l"(v.x), "=l"(v.y)
                  : "l"(p)
                  : "memory");
     return v;
+}
+
+__device__ __forceinline__ uint32_t tag_of(unsigned long long w) { return uint32_t(w >> 32); }
+
+// Inclusive counts of a finished tile (both words carry the inclusive tag).
+__device__ __forceinline__ uint2 inclusive_of(const Status* s, uint32_t epoch) {
+    const ulonglong2 i = ld_pair(s->inc);
+    const uint32_t tagI = (epoch << 2) | kStInc;
+    VQB_CHECK(tag_of(i.x) == tagI && tag_of(i.y) == tagI, 40, tag_of(i.x), tagI);
+    return make_uint2(uint32_t(i.x), uint32_t(i.y));
 }
 
 // Decoupled look-back over status words st[t * stride + side]; run by one
@@ -51,36 +66,50 @@ __device__ __forceinline__ uint4 ld_status(const Status* p) {
 __device__ uint2 lookback16(uint32_t tile, uint32_t first, uint32_t c0, uint32_t c1, Status* st,
                             uint32_t stride, uint32_t side, uint32_t epoch) {
     const int lane = threadIdx.x & 31;
-    const uint32_t hi = epoch << 2;
+    const uint32_t tagA = (epoch << 2) | kStAgg, tagI = (epoch << 2) | kStInc;
+    Status* mine = &st[uint64_t(tile) * stride + side];
     if (tile == first) {
-        if (lane == 0) st_status(&st[uint64_t(tile) * stride + side], hi | kStInc, c0, c1);
+        if (lane == 0) pub_pair(mine->inc, tagI, c0, c1);
         return make_uint2(0u, 0u);
     }
-    if (lane == 0) st_status(&st[uint64_t(tile) * stride + side], hi | kStAgg, c0, c1);
+    if (lane == 0) pub_pair(mine->agg, tagA, c0, c1);
     uint32_t acc0 = 0, acc1 = 0;
     int64_t pred = int64_t(tile) - 1;
     while (true) {
         const int64_t t = pred - lane;
         const bool in_seg = t >= int64_t(first);
-        uint4 w = make_uint4(0u, 0u, 0u, 0u);
+        uint32_t state = 0, v0 = 0, v1 = 0;
         if (in_seg) {
+            const Status* s = &st[uint64_t(t) * stride + side];
             uint32_t spins = 0;
             while (true) {
-                w = ld_status(&st[uint64_t(t) * stride + side]);
-                if ((w.x & ~3u) == hi && (w.x & 3u) != 0) break;
+                const ulonglong2 i = ld_pair(s->inc);
+                if (tag_of(i.x) == tagI && tag_of(i.y) == tagI) {
+                    state = kStInc;
+                    v0 = uint32_t(i.x);
+                    v1 = uint32_t(i.y);
+                    break;
+                }
+                const ulonglong2 g = ld_pair(s->agg);
+                if (tag_of(g.x) == tagA && tag_of(g.y) == tagA) {
+                    state = kStAgg;
+                    v0 = uint32_t(g.x);
+                    v1 = uint32_t(g.y);
+                    break;
+                }
                 if (++spins > 2) __nanosleep(32);
                 if (spins > (1u << 26)) {  // a bug, never wait forever
                     g_vqb_fault = 1u;
-                    w.x = hi | kStInc;
-                    w.y = w.z = 0;
+                    state = kStInc;
                     break;
                 }
             }
         }
-        const unsigned inc_mask = __ballot_sync(kFull, in_seg && (w.x & 3u) == kStInc);
+        const unsigned inc_mask = __ballot_sync(kFull, in_seg && state == kStInc);
         const int stop = inc_mask ? (__ffs(inc_mask) - 1) : 31;
         const bool take = in_seg && lane <= stop;
-        uint32_t v0 = take ? w.y : 0u, v1 = take ? w.z : 0u;
+        v0 = take ? v0 : 0u;
+        v1 = take ? v1 : 0u;
 #pragma unroll
         for (int s = 16; s > 0; s >>= 1) {
             v0 += __shfl_xor_sync(kFull, v0, s);
@@ -92,7 +121,7 @@ __device__ uint2 lookback16(uint32_t tile, uint32_t first, uint32_t c0, uint32_t
         if (inc_mask || seg_mask != kFull) break;
         pred -= 32;
     }
-    if (lane == 0) st_status(&st[uint64_t(tile) * stride + side], hi | kStInc, acc0 + c0, acc1 + c1);
+    if (lane == 0) pub_pair(mine->inc, tagI, acc0 + c0, acc1 + c1);
     return make_uint2(acc0, acc1);
 }
 
@@ -196,7 +225,8 @@ __device__ __forceinline__ void stage_tile(TileSmem<NC>& S, const double (&ux)[k
 template <int NC>
 __device__ __forceinline__ void flush_tile(const TileSmem<NC>& S, const uint64_t (&base)[NC],
                                            const bool (&fwd)[NC], double* __restrict__ ox,
-                                           double* __restrict__ oy, uint32_t* __restrict__ oid) {
+                                           double* __restrict__ oy, uint32_t* __restrict__ oid,
+                                           uint64_t out_cap) {
     const uint32_t total = S.cbase[NC];
     for (uint32_t e = threadIdx.x; e < total; e += kThreads) {
         int c = 0;
@@ -212,6 +242,10 @@ __device__ __forceinline__ void flush_tile(const TileSmem<NC>& S, const uint64_t
         }
         const uint64_t r = uint64_t(S.excl[c]) + (e - S.cbase[c]);
         const uint64_t pos = f ? b + r : b - r;
+        VQB_CHECK(pos < out_cap, 10 + c, pos, out_cap);
+#ifdef VQB_DEBUG
+        if (pos >= out_cap) continue;
+#endif
         ox[pos] = S.sx[e];
         oy[pos] = S.sy[e];
         oid[pos] = S.sid[e];
@@ -328,7 +362,7 @@ __global__ void __launch_bounds__(kThreads, kPartMinBlocks) root_partition_kerne
             }
         }
         __syncthreads();
-        flush_tile<4>(S, base, fwd, a.ox, a.oy, a.oid);
+        flush_tile<4>(S, base, fwd, a.ox, a.oy, a.oid, a.out_cap);
         t = tn;
     }
     // per-CTA arg-max partials; the last CTA out reduces them and emits the
@@ -355,8 +389,8 @@ __global__ void __launch_bounds__(kThreads, kPartMinBlocks) root_partition_kerne
         if (lane == 0) {
             uint32_t m = 0;
             if (a.ntiles) {
-                const uint4 w = ld_status(&a.status[uint64_t(a.ntiles - 1) * 2 + (c >> 1)]);
-                m = (c & 1) ? w.z : w.y;
+                const uint2 w = inclusive_of(&a.status[uint64_t(a.ntiles - 1) * 2 + (c >> 1)], a.epoch);
+                m = (c & 1) ? w.y : w.x;
             }
             ChildRec ch;
             // children: (p, r11, r1) (r1, r12, q) (q, r21, r2) (r2, r22, p)
@@ -407,29 +441,60 @@ __global__ void __launch_bounds__(kThreads, kPartMinBlocks) level_kernel(LevelAr
         __syncthreads();
         if (threadIdx.x == 0) {
             const uint32_t k = s_cur_k;
+            VQB_CHECK(k < a.info->nseg, 52, k, a.info->nseg);
+#ifdef VQB_DEBUG
+            if (k >= a.segs_cap) { s_last = false; goto fin_skip; }
+#endif
+            {
             const uint32_t slot = atomicAdd(&a.seg_pcnt[k], 1u);
+            VQB_CHECK(slot < s_cur.ntiles, 50, slot, s_cur.ntiles);
+            VQB_CHECK(s_cur.tile0 + s_cur.ntiles <= a.info->ntiles, 53, s_cur.tile0, s_cur.ntiles);
+            VQB_CHECK(2 * (uint64_t(s_cur.tile0) + slot) + 1 < a.part_cap, 54, s_cur.tile0, slot);
+#ifdef VQB_DEBUG
+            if (2 * (uint64_t(s_cur.tile0) + slot) + 1 < a.part_cap)
+#endif
+            {
             a.tile_part[2 * (uint64_t(s_cur.tile0) + slot)] = s_run[0];
             a.tile_part[2 * (uint64_t(s_cur.tile0) + slot) + 1] = s_run[1];
+            }
             __threadfence();
             const uint32_t done = atomicAdd(&a.seg_done[k], s_cur_tiles) + s_cur_tiles;
             s_last = (done == s_cur.ntiles);
+            }
+#ifdef VQB_DEBUG
+        fin_skip:;
+#endif
         }
         __syncthreads();
         if (s_last) {
             __threadfence();
             if (warp < 2) {
                 const int c = warp;
-                const uint32_t np = __ldcg(&a.seg_pcnt[s_cur_k]);
+                uint32_t np = __ldcg(&a.seg_pcnt[s_cur_k]);
+                VQB_CHECK(np <= s_cur.ntiles, 51, np, s_cur.ntiles);
+#ifdef VQB_DEBUG
+                if (np > s_cur.ntiles) np = 0;
+#endif
                 Best b = best_none();
                 for (uint32_t j = lane; j < np; j += 32) {
+                    VQB_CHECK(2 * (uint64_t(s_cur.tile0) + j) + c < a.part_cap, 55, s_cur.tile0, j);
+#ifdef VQB_DEBUG
+                    if (2 * (uint64_t(s_cur.tile0) + j) + c >= a.part_cap) break;
+#endif
                     const Best o = ldcg_best(&a.tile_part[2 * (uint64_t(s_cur.tile0) + j) + c]);
                     if (prefer(o, b)) b = o;
                 }
                 b = warp_best(b);
                 if (lane == 0) {
                     const SegRec& g = s_cur;
-                    const uint4 w = ld_status(&a.status[uint64_t(g.tile0) + g.ntiles - 1]);
-                    const uint32_t m = c == 0 ? w.y : w.z;
+                    VQB_CHECK(uint64_t(g.tile0) + g.ntiles - 1 < a.status_cap, 56, g.tile0, g.ntiles);
+#ifdef VQB_DEBUG
+                    const uint2 w = (uint64_t(g.tile0) + g.ntiles - 1 < a.status_cap)
+                        ? inclusive_of(&a.status[uint64_t(g.tile0) + g.ntiles - 1], a.epoch) : make_uint2(0, 0);
+#else
+                    const uint2 w = inclusive_of(&a.status[uint64_t(g.tile0) + g.ntiles - 1], a.epoch);
+#endif
+                    const uint32_t m = c == 0 ? w.x : w.y;
                     ChildRec ch;
                     if (c == 0) {  // left of p->r: triangle (p, rL, r)
                         ch.px = g.px; ch.py = g.py; ch.qx = g.rx; ch.qy = g.ry;
@@ -443,6 +508,10 @@ __global__ void __launch_bounds__(kThreads, kPartMinBlocks) level_kernel(LevelAr
                     ch.ry = b.y;
                     ch.r_idx = b.idx;
                     ch.m = m;
+                    VQB_CHECK(2 * uint64_t(s_cur_k) + c < a.children_cap, 57, s_cur_k, a.children_cap);
+#ifdef VQB_DEBUG
+                    if (2 * uint64_t(s_cur_k) + c < a.children_cap)
+#endif
                     a.children[2 * uint64_t(s_cur_k) + c] = ch;
                 }
             }
@@ -455,15 +524,24 @@ __global__ void __launch_bounds__(kThreads, kPartMinBlocks) level_kernel(LevelAr
     uint32_t cnt = 0;
     auto fetch = [&](uint32_t t, int b) {  // segment record of tile t -> s_seg[b], then loads
         if (threadIdx.x == 0) {
-            const uint32_t k = a.tile_seg[t];
+            uint32_t k = a.tile_seg[t];
+            VQB_CHECK(k < a.info->nseg, 21, k, t);
+#ifdef VQB_DEBUG
+            if (k >= a.info->nseg) k = 0;
+#endif
             s_k[b] = k;
             s_seg[b] = a.segs[k];
+            VQB_CHECK(t >= s_seg[b].tile0 && t < s_seg[b].tile0 + s_seg[b].ntiles, 22, t, s_seg[b].tile0);
         }
         __syncthreads();
         const SegRec& g = s_seg[b];
         const uint32_t j = t - g.tile0;
         const uint64_t start = g.begin + uint64_t(j) * kTile;
         cnt = min(uint32_t(kTile), g.m - j * uint32_t(kTile));
+        VQB_CHECK(j < g.ntiles && start + cnt <= a.in_cap, 20, start + cnt, a.in_cap);
+#ifdef VQB_DEBUG
+        if (!(j < g.ntiles && start + cnt <= a.in_cap)) cnt = 0;
+#endif
 #pragma unroll
         for (int i = 0; i < kItems; ++i) {
             const uint32_t r = uint32_t(i) * kThreads + threadIdx.x;
@@ -508,20 +586,37 @@ __global__ void __launch_bounds__(kThreads, kPartMinBlocks) level_kernel(LevelAr
         const uint64_t base[2] = {g.out, g.out + g.m - 1};
         const bool fwd[2] = {true, false};
         const uint32_t tile0 = g.tile0;
+#ifndef VQB_NO_PREFETCH
         const uint32_t tn = claim(&S.tile, a.ctr, ntiles);
         if (tn < ntiles) fetch(tn, b ^ 1);  // in flight during the look-back and the stores
+#endif
         if (warp == 0) {
+            VQB_CHECK(t < a.status_cap && tile0 <= t, 58, t, tile0);
+#ifdef VQB_DEBUG
+            const uint2 e = (t < a.status_cap && tile0 <= t)
+                ? lookback16(t, tile0, S.cnt[0], S.cnt[1], a.status, 1u, 0u, a.epoch) : make_uint2(0, 0);
+#else
             const uint2 e = lookback16(t, tile0, S.cnt[0], S.cnt[1], a.status, 1u, 0u, a.epoch);
+#endif
             if (lane == 0) {
                 S.excl[0] = e.x;
                 S.excl[1] = e.y;
             }
         }
         __syncthreads();
-        flush_tile<2>(S, base, fwd, a.ox, a.oy, a.oid);
-        // running arg-max of the segment this tile belongs to
-        if (s_k[b] != s_cur_k) {
-            if (s_cur_k != 0xffffffffu) finalize();
+        flush_tile<2>(S, base, fwd, a.ox, a.oy, a.oid, a.out_cap);
+#ifdef VQB_NO_PREFETCH
+        const uint32_t tn = claim(&S.tile, a.ctr, ntiles);
+        if (tn < ntiles) fetch(tn, b ^ 1);
+#endif
+        // running arg-max of the segment this tile belongs to.  The branch
+        // guards barriers, so every thread must decide on the same snapshot
+        // of the shared state: read it, then let thread 0 modify it only
+        // after a barrier.
+        const uint32_t k_now = s_k[b], k_cur = s_cur_k;
+        __syncthreads();
+        if (k_now != k_cur) {
+            if (k_cur != 0xffffffffu) finalize();
             if (threadIdx.x == 0) {
                 s_cur = s_seg[b];
                 s_cur_k = s_k[b];
