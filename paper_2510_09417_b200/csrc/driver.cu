@@ -163,7 +163,7 @@ class Engine {
             ra.status = status_.as<Status>(); ra.epoch = next_epoch();
             ra.ctr = &ctrs_[0]; ra.ticket = &ctrs_[4]; ra.cta_part = part_.as<Best>();
             ra.children = L2.slots.as<ChildRec>(); ra.ntiles = ntiles_root;
-            tk(2, st, [&] { launch_root_partition(ra, grid, st); });
+            tk(2, st, [&] { ck(launch_root_partition(ra, grid, st), "root partition launch"); });
         }
         // finiteness verdict + sizes for the byte accounting
         ck(cudaMemcpyAsync(h_root_, root_, sizeof(RootInfo), cudaMemcpyDeviceToHost, st), "d2h root");
@@ -256,7 +256,7 @@ class Engine {
                 la.tile_part = part_.as<Best>();
                 la.seg_pcnt = segaux_.as<uint32_t>(); la.seg_done = segaux_.as<uint32_t>() + nslots;
                 la.children = Tn.slots.as<ChildRec>();
-                tk(3, st, [&] { launch_level(la, false, grid, st); });
+                tk(3, st, [&] { ck(launch_level(la, false, grid, st), "level launch"); });
             }
             stats_.segments += li.nseg;
             stats_.level_points += li.out_total;
@@ -375,7 +375,7 @@ class Engine {
         la.tile_part = part_.as<Best>();
         la.seg_pcnt = segaux_.as<uint32_t>(); la.seg_done = segaux_.as<uint32_t>() + 1;
         la.children = dch;
-        launch_level(la, true, grid, st);
+        ck(launch_level(la, true, grid, st), "extract launch");
         ChildRec ch[2];
         ck(cudaMemcpyAsync(ch, dch, sizeof ch, cudaMemcpyDeviceToHost, st), "d2h children");
         ck(cudaStreamSynchronize(st), "sync");

@@ -14,8 +14,8 @@ void launch_extremes(const double* xs, const double* ys, uint64_t n, void* parti
 void launch_bootstrap(const double* xs, const double* ys, uint64_t n, void* partials,
                       uint32_t* ticket, RootInfo* root, int grid, cudaStream_t st);
 size_t partial_bytes(int grid);
-void launch_root_partition(const RootArgs& a, int grid, cudaStream_t st);
-void launch_level(const LevelArgs& a, bool general, int grid, cudaStream_t st);
+cudaError_t launch_root_partition(const RootArgs& a, int grid, cudaStream_t st);
+cudaError_t launch_level(const LevelArgs& a, bool general, int grid, cudaStream_t st);
 void launch_planner(const ChildRec* slots, uint32_t nslots, SegRec* segs, FinRec* fins,
                     uint8_t* kind, uint32_t* link, LevelInfo* info, uint64_t fin_chain_base,
                     uint32_t* flags, void* aggs, void* incs, uint32_t epoch, uint32_t* ctr,

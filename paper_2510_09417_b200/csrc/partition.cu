@@ -9,12 +9,11 @@
 // S2 from the right end), and the fused farthest-point search in the
 // canonical order (kernels.hpp:36-45).
 //
-// GPU structure (persistent CTAs, tiles claimed in increasing order):
-//   load tile (prefetched during the previous tile's look-back)
-//   -> classify -> warp ballots -> block scan -> stage survivors in smem
-//   -> per-class arg-max over the staged survivors
-//   -> decoupled look-back on ONE self-contained 16-byte status word per tile
-//      (flag + two 32-bit counts; no payload arrays, no fences)
+// GPU structure (co-resident persistent CTAs, static tile schedule t -> CTA
+// t mod G, next tile prefetched into registers):
+//   classify -> warp ballots -> block scan -> publish the tile's counts
+//   -> stage survivors in smem (input order) -> per-class arg-max
+//   -> decoupled look-back over self-validating 8-byte status words
 //   -> coalesced stores of the staged survivors to their final positions.
 // The arg-max does not ride the look-back: each CTA keeps a running best per
 // segment and publishes it once per segment visit; the CTA that completes a
@@ -55,24 +54,30 @@ __device__ __forceinline__ uint32_t tag_of(unsigned long long w) { return uint32
 // Inclusive counts of a finished tile (both words carry the inclusive tag).
 __device__ __forceinline__ uint2 inclusive_of(const Status* s, uint32_t epoch) {
     const ulonglong2 i = ld_pair(s->inc);
-    const uint32_t tagI = (epoch << 2) | kStInc;
-    VQB_CHECK(tag_of(i.x) == tagI && tag_of(i.y) == tagI, 40, tag_of(i.x), tagI);
+    VQB_CHECK(tag_of(i.x) == ((epoch << 2) | kStInc) && tag_of(i.y) == ((epoch << 2) | kStInc), 40,
+              tag_of(i.x), epoch);
+    (void)epoch;
     return make_uint2(uint32_t(i.x), uint32_t(i.y));
 }
 
+// A tile announces its own counts as early as possible — right after its
+// block scan — so successors rarely wait: INC for the first tile of its
+// segment (nothing precedes it), AGG otherwise.
+__device__ __forceinline__ void publish_counts(Status* s, bool first, uint32_t c0, uint32_t c1,
+                                               uint32_t epoch) {
+    if (first) pub_pair(s->inc, (epoch << 2) | kStInc, c0, c1);
+    else pub_pair(s->agg, (epoch << 2) | kStAgg, c0, c1);
+}
+
 // Decoupled look-back over status words st[t * stride + side]; run by one
-// full warp.  Returns the exclusive prefix (c0, c1) of `tile` within the
-// segment whose first tile is `first`.
+// full warp after the tile's own counts were published.  Returns the
+// exclusive prefix (c0, c1) of `tile` inside the segment whose first tile is
+// `first` and publishes the tile's inclusive counts.
 __device__ uint2 lookback16(uint32_t tile, uint32_t first, uint32_t c0, uint32_t c1, Status* st,
                             uint32_t stride, uint32_t side, uint32_t epoch) {
+    if (tile == first) return make_uint2(0u, 0u);
     const int lane = threadIdx.x & 31;
     const uint32_t tagA = (epoch << 2) | kStAgg, tagI = (epoch << 2) | kStInc;
-    Status* mine = &st[uint64_t(tile) * stride + side];
-    if (tile == first) {
-        if (lane == 0) pub_pair(mine->inc, tagI, c0, c1);
-        return make_uint2(0u, 0u);
-    }
-    if (lane == 0) pub_pair(mine->agg, tagA, c0, c1);
     uint32_t acc0 = 0, acc1 = 0;
     int64_t pred = int64_t(tile) - 1;
     while (true) {
@@ -97,7 +102,7 @@ __device__ uint2 lookback16(uint32_t tile, uint32_t first, uint32_t c0, uint32_t
                     v1 = uint32_t(g.y);
                     break;
                 }
-                if (++spins > 2) __nanosleep(32);
+                if (++spins > 4) __nanosleep(20);
                 if (spins > (1u << 26)) {  // a bug, never wait forever
                     g_vqb_fault = 1u;
                     state = kStInc;
@@ -121,7 +126,8 @@ __device__ uint2 lookback16(uint32_t tile, uint32_t first, uint32_t c0, uint32_t
         if (inc_mask || seg_mask != kFull) break;
         pred -= 32;
     }
-    if (lane == 0) pub_pair(mine->inc, tagI, acc0 + c0, acc1 + c1);
+    if (lane == 0)
+        pub_pair(st[uint64_t(tile) * stride + side].inc, tagI, acc0 + c0, acc1 + c1);
     return make_uint2(acc0, acc1);
 }
 
@@ -140,19 +146,17 @@ struct TileSmem {
     double fdx[NC], fdy[NC];  // class frames for the arg-max
     Best wbest[NC][kWarps];
     Best best[NC];       // tile arg-max per class
-    uint32_t tile;
 };
 
-// cls[i] == NC means "no class".  On return the survivors are staged in input
-// order, class by class, and S.cnt / S.best hold the tile's counts and
-// per-class canonical arg-max (offsets from the class frames S.fdx/S.fdy).
+// Ranks: per-warp ballots then one warp-wide scan per class over the
+// (item, warp) counts.  cls[i] == NC means "no class".  On return S.cnt and
+// S.cbase are final (block-synchronised) and rk[i] holds each item's rank
+// inside its warp and item slot.
 template <int NC>
-__device__ __forceinline__ void stage_tile(TileSmem<NC>& S, const double (&ux)[kItems],
-                                           const double (&uy)[kItems],
-                                           const uint32_t (&uid)[kItems], const int (&cls)[kItems]) {
+__device__ __forceinline__ void scan_tile(TileSmem<NC>& S, const int (&cls)[kItems],
+                                          uint32_t (&rk)[kItems]) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const unsigned lt = lanemask_lt();
-    uint32_t rk[kItems];
 #pragma unroll
     for (int i = 0; i < kItems; ++i) {
         rk[i] = 0;
@@ -178,16 +182,22 @@ __device__ __forceinline__ void stage_tile(TileSmem<NC>& S, const double (&ux)[k
         if (lane == 31) S.cnt[c] = incl;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (threadIdx.x <= NC) {
         uint32_t acc = 0;
-#pragma unroll
-        for (int c = 0; c < NC; ++c) {
-            S.cbase[c] = acc;
-            acc += S.cnt[c];
-        }
-        S.cbase[NC] = acc;
+        for (int c = 0; c < int(threadIdx.x); ++c) acc += S.cnt[c];
+        S.cbase[threadIdx.x] = acc;
     }
     __syncthreads();
+}
+
+// Survivors to the staging area in input order (class by class), then the
+// per-class canonical arg-max over the staged survivors.  Ends synchronised.
+template <int NC>
+__device__ __forceinline__ void stage_tile(TileSmem<NC>& S, const double (&ux)[kItems],
+                                           const double (&uy)[kItems],
+                                           const uint32_t (&uid)[kItems], const int (&cls)[kItems],
+                                           const uint32_t (&rk)[kItems]) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #pragma unroll
     for (int i = 0; i < kItems; ++i) {
         const int c = cls[i];
@@ -199,7 +209,6 @@ __device__ __forceinline__ void stage_tile(TileSmem<NC>& S, const double (&ux)[k
         }
     }
     __syncthreads();
-    // arg-max per class over the staged (contiguous) survivors
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
         const double edx = S.fdx[c], edy = S.fdy[c];
@@ -252,19 +261,6 @@ __device__ __forceinline__ void flush_tile(const TileSmem<NC>& S, const uint64_t
     }
 }
 
-// Claim the next tile in increasing order.  The last CTA to drain re-arms
-// the counter for the next launch.
-__device__ __forceinline__ uint32_t claim(uint32_t* s_tile, uint32_t* ctr, uint32_t ntiles) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        const uint32_t t = atomicAdd(ctr, 1u);
-        *s_tile = t;
-        if (t >= ntiles && t == ntiles + gridDim.x - 1) *ctr = 0;
-    }
-    __syncthreads();
-    return *s_tile;
-}
-
 __device__ __forceinline__ Best ldcg_best(const Best* p) {
     Best b;
     b.off = __ldcg(&p->off);
@@ -274,6 +270,14 @@ __device__ __forceinline__ Best ldcg_best(const Best* p) {
     b.valid = __ldcg(&p->valid);
     return b;
 }
+
+// ===========================================================================
+// Scheduling.  Tile t belongs to CTA t mod G and CTAs visit their tiles in
+// increasing order; all G CTAs are co-resident (cooperative launch), so every
+// look-back waits only on tiles owned by running CTAs that are at most one
+// round behind, and prefetching a CTA's next tile claims nothing another CTA
+// could be waiting for.
+// ===========================================================================
 
 // ===========================================================================
 // KB: root partition — hull levels 1 and 2 fused (probe P5).
@@ -323,7 +327,7 @@ __global__ void __launch_bounds__(kThreads, kPartMinBlocks) root_partition_kerne
             uid[i] = uint32_t(pos);
         }
     };
-    uint32_t t = claim(&S.tile, a.ctr, a.ntiles);
+    uint32_t t = blockIdx.x;
     if (t < a.ntiles) load(t);
     while (t < a.ntiles) {
         int cls[kItems];
@@ -347,10 +351,17 @@ __global__ void __launch_bounds__(kThreads, kPartMinBlocks) root_partition_kerne
             else if (s2) c = L ? 2 : (Rr ? 3 : 4);
             cls[i] = inr[i] ? c : 4;
         }
-        stage_tile<4>(S, ux, uy, uid, cls);
+        uint32_t rk[kItems];
+        scan_tile<4>(S, cls, rk);
+        if (threadIdx.x < 2) {
+            const uint32_t side = threadIdx.x;
+            publish_counts(&a.status[uint64_t(t) * 2 + side], t == 0, S.cnt[2 * side],
+                           S.cnt[2 * side + 1], a.epoch);
+        }
+        stage_tile<4>(S, ux, uy, uid, cls, rk);
         if (threadIdx.x < 4 && prefer(S.best[threadIdx.x], s_run[threadIdx.x]))
             s_run[threadIdx.x] = S.best[threadIdx.x];
-        const uint32_t tn = claim(&S.tile, a.ctr, a.ntiles);
+        const uint32_t tn = t + gridDim.x;
         if (tn < a.ntiles) load(tn);  // in flight during the look-back and the stores
         if (threadIdx.x < 64) {
             const uint32_t side = threadIdx.x >> 5;
@@ -363,6 +374,7 @@ __global__ void __launch_bounds__(kThreads, kPartMinBlocks) root_partition_kerne
         }
         __syncthreads();
         flush_tile<4>(S, base, fwd, a.ox, a.oy, a.oid, a.out_cap);
+        __syncthreads();
         t = tn;
     }
     // per-CTA arg-max partials; the last CTA out reduces them and emits the
@@ -415,6 +427,10 @@ __global__ void __launch_bounds__(kThreads, kPartMinBlocks) root_partition_kerne
 // Tiles never straddle segments; a segment's tiles are consecutive ids.
 // GENERAL = two unrelated edges (the extract_subsets API); otherwise the
 // edges p->r and r->q share r (two subtractions saved per point).
+// The arg-max leaves the look-back: each CTA keeps a running best for the
+// segment it is visiting and publishes it once per visit; the CTA whose
+// finished-tile count completes the segment reduces the partials and emits
+// the two children.
 // ===========================================================================
 template <bool GENERAL>
 __global__ void __launch_bounds__(kThreads, kPartMinBlocks) level_kernel(LevelArgs a) {
@@ -435,65 +451,35 @@ __global__ void __launch_bounds__(kThreads, kPartMinBlocks) level_kernel(LevelAr
     const uint32_t ntiles = s_ntiles;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-    // publish this CTA's running best for s_cur; the CTA completing the
-    // segment's tile count reduces all partials and emits the two children
     auto finalize = [&]() {
         __syncthreads();
         if (threadIdx.x == 0) {
             const uint32_t k = s_cur_k;
-            VQB_CHECK(k < a.info->nseg, 52, k, a.info->nseg);
-#ifdef VQB_DEBUG
-            if (k >= a.segs_cap) { s_last = false; goto fin_skip; }
-#endif
-            {
             const uint32_t slot = atomicAdd(&a.seg_pcnt[k], 1u);
-            VQB_CHECK(slot < s_cur.ntiles, 50, slot, s_cur.ntiles);
-            VQB_CHECK(s_cur.tile0 + s_cur.ntiles <= a.info->ntiles, 53, s_cur.tile0, s_cur.ntiles);
-            VQB_CHECK(2 * (uint64_t(s_cur.tile0) + slot) + 1 < a.part_cap, 54, s_cur.tile0, slot);
-#ifdef VQB_DEBUG
-            if (2 * (uint64_t(s_cur.tile0) + slot) + 1 < a.part_cap)
-#endif
-            {
+            VQB_CHECK(slot < s_cur.ntiles && 2 * (uint64_t(s_cur.tile0) + slot) + 1 < a.part_cap,
+                      50, slot, s_cur.ntiles);
             a.tile_part[2 * (uint64_t(s_cur.tile0) + slot)] = s_run[0];
             a.tile_part[2 * (uint64_t(s_cur.tile0) + slot) + 1] = s_run[1];
-            }
             __threadfence();
             const uint32_t done = atomicAdd(&a.seg_done[k], s_cur_tiles) + s_cur_tiles;
             s_last = (done == s_cur.ntiles);
-            }
-#ifdef VQB_DEBUG
-        fin_skip:;
-#endif
         }
         __syncthreads();
         if (s_last) {
             __threadfence();
             if (warp < 2) {
                 const int c = warp;
-                uint32_t np = __ldcg(&a.seg_pcnt[s_cur_k]);
+                const uint32_t np = __ldcg(&a.seg_pcnt[s_cur_k]);
                 VQB_CHECK(np <= s_cur.ntiles, 51, np, s_cur.ntiles);
-#ifdef VQB_DEBUG
-                if (np > s_cur.ntiles) np = 0;
-#endif
                 Best b = best_none();
                 for (uint32_t j = lane; j < np; j += 32) {
-                    VQB_CHECK(2 * (uint64_t(s_cur.tile0) + j) + c < a.part_cap, 55, s_cur.tile0, j);
-#ifdef VQB_DEBUG
-                    if (2 * (uint64_t(s_cur.tile0) + j) + c >= a.part_cap) break;
-#endif
                     const Best o = ldcg_best(&a.tile_part[2 * (uint64_t(s_cur.tile0) + j) + c]);
                     if (prefer(o, b)) b = o;
                 }
                 b = warp_best(b);
                 if (lane == 0) {
                     const SegRec& g = s_cur;
-                    VQB_CHECK(uint64_t(g.tile0) + g.ntiles - 1 < a.status_cap, 56, g.tile0, g.ntiles);
-#ifdef VQB_DEBUG
-                    const uint2 w = (uint64_t(g.tile0) + g.ntiles - 1 < a.status_cap)
-                        ? inclusive_of(&a.status[uint64_t(g.tile0) + g.ntiles - 1], a.epoch) : make_uint2(0, 0);
-#else
                     const uint2 w = inclusive_of(&a.status[uint64_t(g.tile0) + g.ntiles - 1], a.epoch);
-#endif
                     const uint32_t m = c == 0 ? w.x : w.y;
                     ChildRec ch;
                     if (c == 0) {  // left of p->r: triangle (p, rL, r)
@@ -509,9 +495,6 @@ __global__ void __launch_bounds__(kThreads, kPartMinBlocks) level_kernel(LevelAr
                     ch.r_idx = b.idx;
                     ch.m = m;
                     VQB_CHECK(2 * uint64_t(s_cur_k) + c < a.children_cap, 57, s_cur_k, a.children_cap);
-#ifdef VQB_DEBUG
-                    if (2 * uint64_t(s_cur_k) + c < a.children_cap)
-#endif
                     a.children[2 * uint64_t(s_cur_k) + c] = ch;
                 }
             }
@@ -522,26 +505,19 @@ __global__ void __launch_bounds__(kThreads, kPartMinBlocks) level_kernel(LevelAr
     double ux[kItems], uy[kItems];
     uint32_t uid[kItems];
     uint32_t cnt = 0;
-    auto fetch = [&](uint32_t t, int b) {  // segment record of tile t -> s_seg[b], then loads
+    auto fetch = [&](uint32_t tt, int bb) {  // segment of tile tt -> s_seg[bb], then loads
         if (threadIdx.x == 0) {
-            uint32_t k = a.tile_seg[t];
-            VQB_CHECK(k < a.info->nseg, 21, k, t);
-#ifdef VQB_DEBUG
-            if (k >= a.info->nseg) k = 0;
-#endif
-            s_k[b] = k;
-            s_seg[b] = a.segs[k];
-            VQB_CHECK(t >= s_seg[b].tile0 && t < s_seg[b].tile0 + s_seg[b].ntiles, 22, t, s_seg[b].tile0);
+            const uint32_t k = a.tile_seg[tt];
+            VQB_CHECK(k < a.info->nseg, 21, k, tt);
+            s_k[bb] = k;
+            s_seg[bb] = a.segs[k];
         }
         __syncthreads();
-        const SegRec& g = s_seg[b];
-        const uint32_t j = t - g.tile0;
+        const SegRec& g = s_seg[bb];
+        const uint32_t j = tt - g.tile0;
         const uint64_t start = g.begin + uint64_t(j) * kTile;
         cnt = min(uint32_t(kTile), g.m - j * uint32_t(kTile));
         VQB_CHECK(j < g.ntiles && start + cnt <= a.in_cap, 20, start + cnt, a.in_cap);
-#ifdef VQB_DEBUG
-        if (!(j < g.ntiles && start + cnt <= a.in_cap)) cnt = 0;
-#endif
 #pragma unroll
         for (int i = 0; i < kItems; ++i) {
             const uint32_t r = uint32_t(i) * kThreads + threadIdx.x;
@@ -553,7 +529,7 @@ __global__ void __launch_bounds__(kThreads, kPartMinBlocks) level_kernel(LevelAr
     };
 
     int b = 0;
-    uint32_t t = claim(&S.tile, a.ctr, ntiles);
+    uint32_t t = blockIdx.x;
     if (t < ntiles) fetch(t, b);
     while (t < ntiles) {
         const SegRec& g = s_seg[b];
@@ -582,22 +558,18 @@ __global__ void __launch_bounds__(kThreads, kPartMinBlocks) level_kernel(LevelAr
                 cls[i] = !v ? 2 : (la ? 0 : (lb ? 1 : 2));
             }
         }
-        stage_tile<2>(S, ux, uy, uid, cls);
+        const uint32_t tile0 = g.tile0;
         const uint64_t base[2] = {g.out, g.out + g.m - 1};
         const bool fwd[2] = {true, false};
-        const uint32_t tile0 = g.tile0;
-#ifndef VQB_NO_PREFETCH
-        const uint32_t tn = claim(&S.tile, a.ctr, ntiles);
+        uint32_t rk[kItems];
+        scan_tile<2>(S, cls, rk);
+        if (threadIdx.x == 0)
+            publish_counts(&a.status[t], t == tile0, S.cnt[0], S.cnt[1], a.epoch);
+        stage_tile<2>(S, ux, uy, uid, cls, rk);
+        const uint32_t tn = t + gridDim.x;
         if (tn < ntiles) fetch(tn, b ^ 1);  // in flight during the look-back and the stores
-#endif
         if (warp == 0) {
-            VQB_CHECK(t < a.status_cap && tile0 <= t, 58, t, tile0);
-#ifdef VQB_DEBUG
-            const uint2 e = (t < a.status_cap && tile0 <= t)
-                ? lookback16(t, tile0, S.cnt[0], S.cnt[1], a.status, 1u, 0u, a.epoch) : make_uint2(0, 0);
-#else
             const uint2 e = lookback16(t, tile0, S.cnt[0], S.cnt[1], a.status, 1u, 0u, a.epoch);
-#endif
             if (lane == 0) {
                 S.excl[0] = e.x;
                 S.excl[1] = e.y;
@@ -605,21 +577,16 @@ __global__ void __launch_bounds__(kThreads, kPartMinBlocks) level_kernel(LevelAr
         }
         __syncthreads();
         flush_tile<2>(S, base, fwd, a.ox, a.oy, a.oid, a.out_cap);
-#ifdef VQB_NO_PREFETCH
-        const uint32_t tn = claim(&S.tile, a.ctr, ntiles);
-        if (tn < ntiles) fetch(tn, b ^ 1);
-#endif
         // running arg-max of the segment this tile belongs to.  The branch
-        // guards barriers, so every thread must decide on the same snapshot
-        // of the shared state: read it, then let thread 0 modify it only
-        // after a barrier.
+        // guards barriers, so every thread decides on the same snapshot of
+        // the shared state; thread 0 modifies it only after a barrier.
         const uint32_t k_now = s_k[b], k_cur = s_cur_k;
         __syncthreads();
         if (k_now != k_cur) {
             if (k_cur != 0xffffffffu) finalize();
             if (threadIdx.x == 0) {
                 s_cur = s_seg[b];
-                s_cur_k = s_k[b];
+                s_cur_k = k_now;
                 s_cur_tiles = 0;
                 s_run[0] = best_none();
                 s_run[1] = best_none();
@@ -629,6 +596,7 @@ __global__ void __launch_bounds__(kThreads, kPartMinBlocks) level_kernel(LevelAr
         if (threadIdx.x < 2 && prefer(S.best[threadIdx.x], s_run[threadIdx.x]))
             s_run[threadIdx.x] = S.best[threadIdx.x];
         if (threadIdx.x == 0) ++s_cur_tiles;
+        __syncthreads();
         t = tn;
         b ^= 1;
     }
@@ -636,15 +604,18 @@ __global__ void __launch_bounds__(kThreads, kPartMinBlocks) level_kernel(LevelAr
 }
 
 // ===========================================================================
-// launchers
+// launchers: cooperative, so all CTAs of the static schedule are co-resident
 // ===========================================================================
-void launch_root_partition(const RootArgs& a, int grid, cudaStream_t st) {
-    root_partition_kernel<<<grid, kThreads, 0, st>>>(a);
+cudaError_t launch_root_partition(const RootArgs& a, int grid, cudaStream_t st) {
+    void* args[] = {const_cast<RootArgs*>(&a)};
+    return cudaLaunchCooperativeKernel((const void*)root_partition_kernel, dim3(grid),
+                                       dim3(kThreads), args, 0, st);
 }
 
-void launch_level(const LevelArgs& a, bool general, int grid, cudaStream_t st) {
-    if (general) level_kernel<true><<<grid, kThreads, 0, st>>>(a);
-    else level_kernel<false><<<grid, kThreads, 0, st>>>(a);
+cudaError_t launch_level(const LevelArgs& a, bool general, int grid, cudaStream_t st) {
+    void* args[] = {const_cast<LevelArgs*>(&a)};
+    const void* fn = general ? (const void*)level_kernel<true> : (const void*)level_kernel<false>;
+    return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kThreads), args, 0, st);
 }
 
 int occupancy_root() {
@@ -653,9 +624,10 @@ int occupancy_root() {
     return b;
 }
 int occupancy_level() {
-    int b = 0;
+    int b = 0, c = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, level_kernel<false>, kThreads, 0);
-    return b;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, level_kernel<true>, kThreads, 0);
+    return b < c ? b : c;
 }
 
 }  // namespace vqb
