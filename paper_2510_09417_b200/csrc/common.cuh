@@ -129,6 +129,77 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 }
 
 // ---------------------------------------------------------------------------
+// Register-light running arg-max.  A candidate is (key, idx): key is an
+// order-preserving u64 image of its lateral offset (after +0.0, so -0 and +0
+// map to the same key: they compare equal as doubles), idx its input index.
+// Smaller key = strictly smaller offset = preferred (kernels.hpp:41-45).  Only
+// an exact offset tie needs the coordinates: they are fetched from the input
+// arrays through idx, and the reference's lexicographic (x, y) rule plus the
+// first-occurrence index rule decide.  Equivalent to prefer() on Best.
+// ---------------------------------------------------------------------------
+constexpr unsigned long long kNoKey = ~0ull;
+constexpr uint32_t kNoIdx = 0xffffffffu;
+
+__device__ __forceinline__ unsigned long long key_of(double off) {
+    const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(off + 0.0));
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+// candidate (k, i) strictly preferred over incumbent (kb, ib)?
+__device__ __forceinline__ bool key_better(unsigned long long k, uint32_t i, unsigned long long kb,
+                                           uint32_t ib, const double* __restrict__ xs,
+                                           const double* __restrict__ ys) {
+    if (k != kb) return k < kb;
+    if (i == ib || i == kNoIdx) return false;
+    if (ib == kNoIdx) return true;
+    const double x = xs[i], y = ys[i], xb = xs[ib], yb = ys[ib];
+    if (x != xb) return x < xb;
+    if (y != yb) return y < yb;
+    return i < ib;
+}
+
+__device__ __forceinline__ void key_consider(unsigned long long& kb, uint32_t& ib,
+                                             unsigned long long k, uint32_t i,
+                                             const double* __restrict__ xs,
+                                             const double* __restrict__ ys) {
+    if (k < kb || (k == kb && key_better(k, i, kb, ib, xs, ys))) {
+        kb = k;
+        ib = i;
+    }
+}
+
+// butterfly: every lane ends with the warp's preferred candidate
+__device__ __forceinline__ void warp_key_best(unsigned long long& k, uint32_t& i,
+                                              const double* __restrict__ xs,
+                                              const double* __restrict__ ys) {
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) {
+        const unsigned long long ok = __shfl_xor_sync(kFull, k, s);
+        const uint32_t oi = __shfl_xor_sync(kFull, i, s);
+        if (ok < k || (ok == k && key_better(ok, oi, k, i, xs, ys))) {
+            k = ok;
+            i = oi;
+        }
+    }
+}
+
+// Materialise a (key, idx) candidate as a Best: coordinates from the input,
+// offset recomputed with the same frame (identical rounding).
+__device__ __forceinline__ Best best_from_key(unsigned long long k, uint32_t i, double edx,
+                                              double edy, const double* __restrict__ xs,
+                                              const double* __restrict__ ys) {
+    Best b = best_none();
+    if (i != kNoIdx && k != kNoKey) {
+        b.x = xs[i];
+        b.y = ys[i];
+        b.off = lat_off(edx, edy, b.x, b.y);
+        b.idx = i;
+        b.valid = 1u;
+    }
+    return b;
+}
+
+// ---------------------------------------------------------------------------
 // Memory-ordering primitives for the decoupled look-back.
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {

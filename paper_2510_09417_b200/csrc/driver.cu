@@ -246,6 +246,7 @@ class Engine {
             {
                 const int grid = std::max(1, std::min<int>(int(li.ntiles), sms_ * occ_level_));
                 LevelArgs la;
+                la.gx = dx; la.gy = dy;
                 la.segs = Tc.segs.as<SegRec>(); la.tile_seg = tile_seg_.as<uint32_t>(); la.info = dinfo;
                 la.ix = bufs_[in].x.as<double>(); la.iy = bufs_[in].y.as<double>(); la.iid = bufs_[in].id.as<uint32_t>();
                 la.ox = bufs_[out].x.as<double>(); la.oy = bufs_[out].y.as<double>(); la.oid = bufs_[out].id.as<uint32_t>();
@@ -365,6 +366,7 @@ class Engine {
         ck(cudaMemsetAsync(segaux_.p, 0, 16, st), "memset seg aux");
         const int grid = std::max(1, std::min<int>(int(g.ntiles), sms_ * occ_level_));
         LevelArgs la;
+        la.gx = bufs_[0].x.as<double>(); la.gy = bufs_[0].y.as<double>();
         la.segs = dseg; la.tile_seg = tile_seg_.as<uint32_t>(); la.info = dli;
         la.ix = bufs_[0].x.as<double>(); la.iy = bufs_[0].y.as<double>(); la.iid = bufs_[0].id.as<uint32_t>();
         la.ox = bufs_[1].x.as<double>(); la.oy = bufs_[1].y.as<double>(); la.oid = bufs_[1].id.as<uint32_t>();

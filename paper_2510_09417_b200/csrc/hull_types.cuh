@@ -107,6 +107,8 @@ struct RootArgs {
 };
 
 struct LevelArgs {
+    const double* gx;    // the hull's input arrays (index -> coordinates, arg-max ties)
+    const double* gy;
     const SegRec* segs;
     const uint32_t* tile_seg;
     const LevelInfo* info;

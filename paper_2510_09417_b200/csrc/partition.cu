@@ -143,9 +143,8 @@ struct TileSmem {
     uint32_t cbase[NC + 1];
     uint32_t cnt[NC];    // tile counts per class
     uint32_t excl[NC];   // exclusive prefix inside the segment (look-back)
-    double fdx[NC], fdy[NC];  // class frames for the arg-max
-    Best wbest[NC][kWarps];
-    Best best[NC];       // tile arg-max per class
+    unsigned long long rkey[NC][kWarps];  // block reduction scratch
+    uint32_t ridx[NC][kWarps];
 };
 
 // Ranks: per-warp ballots then one warp-wide scan per class over the
@@ -190,14 +189,13 @@ __device__ __forceinline__ void scan_tile(TileSmem<NC>& S, const int (&cls)[kIte
     __syncthreads();
 }
 
-// Survivors to the staging area in input order (class by class), then the
-// per-class canonical arg-max over the staged survivors.  Ends synchronised.
+// Survivors to the staging area in input order (class by class).
 template <int NC>
 __device__ __forceinline__ void stage_tile(TileSmem<NC>& S, const double (&ux)[kItems],
                                            const double (&uy)[kItems],
                                            const uint32_t (&uid)[kItems], const int (&cls)[kItems],
                                            const uint32_t (&rk)[kItems]) {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
 #pragma unroll
     for (int i = 0; i < kItems; ++i) {
         const int c = cls[i];
@@ -208,23 +206,33 @@ __device__ __forceinline__ void stage_tile(TileSmem<NC>& S, const double (&ux)[k
             S.sid[s] = uid[i];
         }
     }
-    __syncthreads();
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
-        const double edx = S.fdx[c], edy = S.fdy[c];
-        Best b = best_none();
-        for (uint32_t e = S.cbase[c] + threadIdx.x; e < S.cbase[c + 1]; e += kThreads) {
-            const double u = S.sx[e], w = S.sy[e];
-            consider(b, true, lat_off(edx, edy, u, w), u, w, S.sid[e]);
-        }
-        b = warp_best(b);
-        if (lane == 0) S.wbest[c][warp] = b;
+}
+
+// Block-wide reduction of every thread's running (key, idx) candidate of
+// class c; returns the winner to thread 0 only.  Uses S.rkey/S.ridx scratch.
+template <int NC>
+__device__ __forceinline__ void block_key_best(TileSmem<NC>& S, int c, unsigned long long k,
+                                               uint32_t i, const double* __restrict__ xs,
+                                               const double* __restrict__ ys,
+                                               unsigned long long& ko, uint32_t& io) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    warp_key_best(k, i, xs, ys);
+    if (lane == 0) {
+        S.rkey[c][warp] = k;
+        S.ridx[c][warp] = i;
     }
     __syncthreads();
-    if (warp < NC) {
-        Best b = lane < kWarps ? S.wbest[warp][lane] : best_none();
-        b = warp_best(b);
-        if (lane == 0) S.best[warp] = b;
+    if (threadIdx.x == 0) {
+        ko = S.rkey[c][0];
+        io = S.ridx[c][0];
+        for (int w = 1; w < kWarps; ++w) {
+            const unsigned long long kk = S.rkey[c][w];
+            const uint32_t ii = S.ridx[c][w];
+            if (kk < ko || (kk == ko && key_better(kk, ii, ko, io, xs, ys))) {
+                ko = kk;
+                io = ii;
+            }
+        }
     }
     __syncthreads();
 }
@@ -292,26 +300,25 @@ __device__ __forceinline__ Best ldcg_best(const Best* p) {
 // ===========================================================================
 __global__ void __launch_bounds__(kThreads, kPartMinBlocks) root_partition_kernel(RootArgs a) {
     __shared__ TileSmem<4> S;
-    __shared__ Best s_run[4];
     __shared__ bool s_last;
     const RootInfo& R = *a.root;
     const double px = R.px, py = R.py, qx = R.qx, qy = R.qy;
     const double r1x = R.r1.x, r1y = R.r1.y, r2x = R.r2.x, r2y = R.r2.y;
     const uint32_t n1 = R.cnt1, n2 = R.cnt2;
-    if (threadIdx.x == 0) {
-        // child frames (kernels.hpp:23-25): 0: p->r1, 1: r1->q, 2: q->r2, 3: r2->p
-        S.fdx[0] = dsub(r1x, px); S.fdy[0] = dsub(r1y, py);
-        S.fdx[1] = dsub(qx, r1x); S.fdy[1] = dsub(qy, r1y);
-        S.fdx[2] = dsub(r2x, qx); S.fdy[2] = dsub(r2y, qy);
-        S.fdx[3] = dsub(px, r2x); S.fdy[3] = dsub(py, r2y);
-    }
-    if (threadIdx.x < 4) s_run[threadIdx.x] = best_none();
+    // child frames (kernels.hpp:23-25): 0: p->r1, 1: r1->q, 2: q->r2, 3: r2->p
+    const double f0x = dsub(r1x, px), f0y = dsub(r1y, py);
+    const double f1x = dsub(qx, r1x), f1y = dsub(qy, r1y);
+    const double f2x = dsub(r2x, qx), f2y = dsub(r2y, qy);
+    const double f3x = dsub(px, r2x), f3y = dsub(py, r2y);
     uint64_t base[4];
     const bool fwd[4] = {true, false, true, false};
     base[0] = 0;
     base[1] = uint64_t(n1) - 1;  // unused when empty
     base[2] = n1;
     base[3] = uint64_t(n1) + n2 - 1;
+    // per-thread running arg-max of each class over all of this CTA's tiles
+    unsigned long long kb[4] = {kNoKey, kNoKey, kNoKey, kNoKey};
+    uint32_t ib[4] = {kNoIdx, kNoIdx, kNoIdx, kNoIdx};
 
     double ux[kItems], uy[kItems];
     uint32_t uid[kItems];
@@ -349,7 +356,16 @@ __global__ void __launch_bounds__(kThreads, kPartMinBlocks) root_partition_kerne
             int c = 4;
             if (s1) c = L ? 0 : (Rr ? 1 : 4);
             else if (s2) c = L ? 2 : (Rr ? 3 : 4);
-            cls[i] = inr[i] ? c : 4;
+            c = inr[i] ? c : 4;
+            cls[i] = c;
+            if (c < 4) {  // fused farthest-point search (extract_core.hpp:462-463)
+                const double edx = s1 ? (L ? f0x : f1x) : (L ? f2x : f3x);
+                const double edy = s1 ? (L ? f0y : f1y) : (L ? f2y : f3y);
+                const unsigned long long k = key_of(lat_off(edx, edy, u, w));
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if (c == q) key_consider(kb[q], ib[q], k, uid[i], a.xs, a.ys);
+            }
         }
         uint32_t rk[kItems];
         scan_tile<4>(S, cls, rk);
@@ -359,8 +375,6 @@ __global__ void __launch_bounds__(kThreads, kPartMinBlocks) root_partition_kerne
                            S.cnt[2 * side + 1], a.epoch);
         }
         stage_tile<4>(S, ux, uy, uid, cls, rk);
-        if (threadIdx.x < 4 && prefer(S.best[threadIdx.x], s_run[threadIdx.x]))
-            s_run[threadIdx.x] = S.best[threadIdx.x];
         const uint32_t tn = t + gridDim.x;
         if (tn < a.ntiles) load(tn);  // in flight during the look-back and the stores
         if (threadIdx.x < 64) {
@@ -377,11 +391,19 @@ __global__ void __launch_bounds__(kThreads, kPartMinBlocks) root_partition_kerne
         __syncthreads();
         t = tn;
     }
-    // per-CTA arg-max partials; the last CTA out reduces them and emits the
-    // four child nodes (counts from the last tile's inclusive status words)
-    __syncthreads();
-    if (threadIdx.x < 4) a.cta_part[blockIdx.x * 4 + threadIdx.x] = s_run[threadIdx.x];
-    __syncthreads();
+    // CTA arg-max partials; the last CTA out reduces them and emits the four
+    // child nodes (counts from the last tile's inclusive status words)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        unsigned long long ko;
+        uint32_t io;
+        block_key_best<4>(S, q, kb[q], ib[q], a.xs, a.ys, ko, io);
+        if (threadIdx.x == 0) {
+            const double edx = q == 0 ? f0x : (q == 1 ? f1x : (q == 2 ? f2x : f3x));
+            const double edy = q == 0 ? f0y : (q == 1 ? f1y : (q == 2 ? f2y : f3y));
+            a.cta_part[blockIdx.x * 4 + q] = best_from_key(ko, io, edx, edy, a.xs, a.ys);
+        }
+    }
     if (threadIdx.x == 0) {
         __threadfence();
         s_last = atomicAdd(a.ticket, 1u) == gridDim.x - 1;
@@ -427,10 +449,10 @@ __global__ void __launch_bounds__(kThreads, kPartMinBlocks) root_partition_kerne
 // Tiles never straddle segments; a segment's tiles are consecutive ids.
 // GENERAL = two unrelated edges (the extract_subsets API); otherwise the
 // edges p->r and r->q share r (two subtractions saved per point).
-// The arg-max leaves the look-back: each CTA keeps a running best for the
-// segment it is visiting and publishes it once per visit; the CTA whose
-// finished-tile count completes the segment reduces the partials and emits
-// the two children.
+// The arg-max leaves the look-back: each thread keeps a running best for the
+// segment its CTA is visiting; on leaving a segment the CTA reduces them and
+// publishes one partial; the CTA whose finished-tile count completes the
+// segment reduces the partials and emits the two children.
 // ===========================================================================
 template <bool GENERAL>
 __global__ void __launch_bounds__(kThreads, kPartMinBlocks) level_kernel(LevelArgs a) {
@@ -450,9 +472,20 @@ __global__ void __launch_bounds__(kThreads, kPartMinBlocks) level_kernel(LevelAr
     __syncthreads();
     const uint32_t ntiles = s_ntiles;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    unsigned long long kb[2] = {kNoKey, kNoKey};
+    uint32_t ib[2] = {kNoIdx, kNoIdx};
 
+    // leave segment s_cur: reduce this CTA's candidates, publish the partial;
+    // the CTA completing the segment's tile count emits the children
     auto finalize = [&]() {
-        __syncthreads();
+        for (int c = 0; c < 2; ++c) {
+            unsigned long long ko;
+            uint32_t io;
+            block_key_best<2>(S, c, kb[c], ib[c], a.gx, a.gy, ko, io);
+            if (threadIdx.x == 0)
+                s_run[c] = best_from_key(ko, io, c == 0 ? s_cur.adx : s_cur.bdx,
+                                         c == 0 ? s_cur.ady : s_cur.bdy, a.gx, a.gy);
+        }
         if (threadIdx.x == 0) {
             const uint32_t k = s_cur_k;
             const uint32_t slot = atomicAdd(&a.seg_pcnt[k], 1u);
@@ -500,6 +533,8 @@ __global__ void __launch_bounds__(kThreads, kPartMinBlocks) level_kernel(LevelAr
             }
         }
         __syncthreads();
+        kb[0] = kb[1] = kNoKey;
+        ib[0] = ib[1] = kNoIdx;
     };
 
     double ux[kItems], uy[kItems];
@@ -532,14 +567,24 @@ __global__ void __launch_bounds__(kThreads, kPartMinBlocks) level_kernel(LevelAr
     uint32_t t = blockIdx.x;
     if (t < ntiles) fetch(t, b);
     while (t < ntiles) {
-        const SegRec& g = s_seg[b];
-        if (threadIdx.x == 0) {
-            S.fdx[0] = g.adx; S.fdy[0] = g.ady;
-            S.fdx[1] = g.bdx; S.fdy[1] = g.bdy;
+        // entering a new segment?  Every thread decides on the same snapshot
+        // of the shared state (the branch guards barriers).
+        const uint32_t k_now = s_k[b], k_cur = s_cur_k;
+        __syncthreads();
+        if (k_now != k_cur) {
+            if (k_cur != 0xffffffffu) finalize();
+            if (threadIdx.x == 0) {
+                s_cur = s_seg[b];
+                s_cur_k = k_now;
+                s_cur_tiles = 0;
+            }
+            __syncthreads();
         }
+        const SegRec& g = s_seg[b];
         int cls[kItems];
         {
             const double px = g.px, py = g.py, rx = g.rx, ry = g.ry, qx = g.qx, qy = g.qy;
+            const double adx = g.adx, ady = g.ady, bdx = g.bdx, bdy = g.bdy;
 #pragma unroll
             for (int i = 0; i < kItems; ++i) {
                 const double u = ux[i], w = uy[i];
@@ -555,7 +600,14 @@ __global__ void __launch_bounds__(kThreads, kPartMinBlocks) level_kernel(LevelAr
                     lb = !la && left_diff(E, F, Cc, D);
                 }
                 const bool v = uint32_t(i) * kThreads + threadIdx.x < cnt;
-                cls[i] = !v ? 2 : (la ? 0 : (lb ? 1 : 2));
+                const int c = !v ? 2 : (la ? 0 : (lb ? 1 : 2));
+                cls[i] = c;
+                if (c < 2) {  // fused farthest-point search
+                    const unsigned long long k =
+                        key_of(lat_off(c == 0 ? adx : bdx, c == 0 ? ady : bdy, u, w));
+                    if (c == 0) key_consider(kb[0], ib[0], k, uid[i], a.gx, a.gy);
+                    else key_consider(kb[1], ib[1], k, uid[i], a.gx, a.gy);
+                }
             }
         }
         const uint32_t tile0 = g.tile0;
@@ -577,24 +629,6 @@ __global__ void __launch_bounds__(kThreads, kPartMinBlocks) level_kernel(LevelAr
         }
         __syncthreads();
         flush_tile<2>(S, base, fwd, a.ox, a.oy, a.oid, a.out_cap);
-        // running arg-max of the segment this tile belongs to.  The branch
-        // guards barriers, so every thread decides on the same snapshot of
-        // the shared state; thread 0 modifies it only after a barrier.
-        const uint32_t k_now = s_k[b], k_cur = s_cur_k;
-        __syncthreads();
-        if (k_now != k_cur) {
-            if (k_cur != 0xffffffffu) finalize();
-            if (threadIdx.x == 0) {
-                s_cur = s_seg[b];
-                s_cur_k = k_now;
-                s_cur_tiles = 0;
-                s_run[0] = best_none();
-                s_run[1] = best_none();
-            }
-            __syncthreads();
-        }
-        if (threadIdx.x < 2 && prefer(S.best[threadIdx.x], s_run[threadIdx.x]))
-            s_run[threadIdx.x] = S.best[threadIdx.x];
         if (threadIdx.x == 0) ++s_cur_tiles;
         __syncthreads();
         t = tn;
