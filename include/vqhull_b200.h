@@ -109,6 +109,14 @@ int vqhull_cuda_get_stats(vqhull_stats* out);
 /* Enable (1) / disable (0) per-kernel CUDA-event timing inside the engine. */
 int vqhull_cuda_set_timing(int enable);
 
+/* Output-offset mode of the partition kernels.  0 (default): each tile
+ * claims its place in S1/S2 with one packed atomic — no tile waits for
+ * another; survivors inside S1/S2 follow claim order, which the reference
+ * leaves unspecified (extract.hpp:14-18).  1: decoupled look-back, survivors
+ * keep input order (order-preserving compaction).  Hull outputs are identical
+ * in both modes.  The environment variable VQHULL_STABLE=1 sets the default. */
+int vqhull_cuda_set_stable(int stable);
+
 /* Human-readable description of the last CUDA error (thread-local). */
 const char* vqhull_cuda_last_error(void);
 

@@ -29,7 +29,7 @@ import numpy as np
 __all__ = [
     "LIB_PATH", "VQhullError", "lib", "available", "vqhull_compute", "convex_hull",
     "hull_indices", "hull_device", "find_extremes", "extract_subsets", "generate", "stats",
-    "set_timing", "HullPolygon", "ExtractOutcome", "KINDS", "Stats",
+    "set_timing", "set_stable", "HullPolygon", "ExtractOutcome", "KINDS", "Stats",
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -93,6 +93,7 @@ def lib() -> C.CDLL:
                                                   _u64p, _u64p, _dp, _ip, _dp, _ip, C.c_void_p]
         L.vqhull_cuda_get_stats.argtypes = [C.POINTER(Stats)]
         L.vqhull_cuda_set_timing.argtypes = [C.c_int]
+        L.vqhull_cuda_set_stable.argtypes = [C.c_int]
         L.vqhull_cuda_last_error.restype = C.c_char_p
         L.vqhull_b200_version.restype = C.c_char_p
         L.vqhull_generate.argtypes = [C.c_int, C.c_uint64, C.c_uint64, C.c_uint64, C.c_void_p,
@@ -237,6 +238,11 @@ def stats() -> dict:
     s = Stats()
     _check(lib().vqhull_cuda_get_stats(C.byref(s)), "vqhull_cuda_get_stats")
     return s.as_dict()
+
+
+def set_stable(on: bool) -> None:
+    """Order-preserving (look-back) partition offsets instead of atomic claims."""
+    _check(lib().vqhull_cuda_set_stable(int(bool(on))), "vqhull_cuda_set_stable")
 
 
 def set_timing(on: bool) -> None:

@@ -144,7 +144,8 @@ class Engine {
         L1.link.ensure(8, st);
         L1.size.ensure(8, st);
         L1.start.ensure(8, st);
-        launch_root_slots(root_, L1.slots.as<ChildRec>(), L1.kind.as<uint8_t>(), L1.link.as<uint32_t>(), st);
+        launch_root_slots(root_, L1.slots.as<ChildRec>(), L1.kind.as<uint8_t>(), L1.link.as<uint32_t>(),
+                          side_ctr(), st);
         ++launches_;
 
         // ---- KB: fused levels 1+2 over the input
@@ -162,8 +163,9 @@ class Engine {
             ra.out_cap = bufs_[0].x.cap / 8;
             ra.status = status_.as<Status>(); ra.epoch = next_epoch();
             ra.ctr = &ctrs_[0]; ra.ticket = &ctrs_[4]; ra.cta_part = part_.as<Best>();
+            ra.side_ctr = side_ctr();
             ra.children = L2.slots.as<ChildRec>(); ra.ntiles = ntiles_root;
-            tk(2, st, [&] { ck(launch_root_partition(ra, grid, st), "root partition launch"); });
+            tk(2, st, [&] { ck(launch_root_partition(ra, grid, stable_, st), "root partition launch"); });
         }
         // finiteness verdict + sizes for the byte accounting
         ck(cudaMemcpyAsync(h_root_, root_, sizeof(RootInfo), cudaMemcpyDeviceToHost, st), "d2h root");
@@ -184,7 +186,7 @@ class Engine {
             T.fins.ensure(size_t(nslots) * sizeof(FinRec), st);
             const uint32_t nchunks = (nslots + 1023) / 1024;
             ensure_lookback(nchunks, st);
-            segaux_.ensure(size_t(nslots) * 8 + 8, st);
+            segaux_.ensure(segaux_bytes(nslots), st);
             info_.ensure(size_t(lvl + 1) * sizeof(LevelInfo), st, true);
             LevelInfo* dinfo = info_.as<LevelInfo>() + lvl;
             {
@@ -193,7 +195,7 @@ class Engine {
                     launch_planner(T.slots.as<ChildRec>(), nslots, T.segs.as<SegRec>(), T.fins.as<FinRec>(),
                                    T.kind.as<uint8_t>(), T.link.as<uint32_t>(), dinfo, fin_base,
                                    flags_.as<uint32_t>(), aggs_.p, incs_.p, ep, &ctrs_[2],
-                                   segaux_.as<uint32_t>(), segaux_.as<uint32_t>() + nslots, sms_ * 4, st);
+                                   seg_pcnt(), seg_done(nslots), seg_ctr(nslots), sms_ * 4, st);
                 });
             }
             ck(cudaMemcpyAsync(h_info_, dinfo, sizeof(LevelInfo), cudaMemcpyDeviceToHost, st), "d2h info");
@@ -252,12 +254,12 @@ class Engine {
                 la.ox = bufs_[out].x.as<double>(); la.oy = bufs_[out].y.as<double>(); la.oid = bufs_[out].id.as<uint32_t>();
                 la.in_cap = bufs_[in].x.cap / 8; la.out_cap = bufs_[out].x.cap / 8;
                 la.status_cap = status_.cap / sizeof(Status); la.part_cap = part_.cap / sizeof(Best);
-                la.children_cap = Tn.slots.cap / sizeof(ChildRec); la.segs_cap = segaux_.cap / 8;
+                la.children_cap = Tn.slots.cap / sizeof(ChildRec); la.segs_cap = nslots;
                 la.status = status_.as<Status>(); la.epoch = next_epoch(); la.ctr = &ctrs_[1];
                 la.tile_part = part_.as<Best>();
-                la.seg_pcnt = segaux_.as<uint32_t>(); la.seg_done = segaux_.as<uint32_t>() + nslots;
+                la.seg_pcnt = seg_pcnt(); la.seg_done = seg_done(nslots); la.seg_ctr = seg_ctr(nslots);
                 la.children = Tn.slots.as<ChildRec>();
-                tk(3, st, [&] { ck(launch_level(la, false, grid, st), "level launch"); });
+                tk(3, st, [&] { ck(launch_level(la, false, stable_, grid, st), "level launch"); });
             }
             stats_.segments += li.nseg;
             stats_.level_points += li.out_total;
@@ -362,8 +364,8 @@ class Engine {
         ck(cudaMemsetAsync(tile_seg_.p, 0, size_t(g.ntiles) * 4, st), "memset tiles");
         ensure_lookback(g.ntiles, st);
         part_.ensure(size_t(g.ntiles) * 2 * sizeof(Best), st);
-        segaux_.ensure(16, st);
-        ck(cudaMemsetAsync(segaux_.p, 0, 16, st), "memset seg aux");
+        segaux_.ensure(segaux_bytes(1), st);
+        ck(cudaMemsetAsync(segaux_.p, 0, segaux_bytes(1), st), "memset seg aux");
         const int grid = std::max(1, std::min<int>(int(g.ntiles), sms_ * occ_level_));
         LevelArgs la;
         la.gx = bufs_[0].x.as<double>(); la.gy = bufs_[0].y.as<double>();
@@ -375,9 +377,9 @@ class Engine {
         la.children_cap = 2; la.segs_cap = 1;
         la.status = status_.as<Status>(); la.epoch = next_epoch(); la.ctr = &ctrs_[1];
         la.tile_part = part_.as<Best>();
-        la.seg_pcnt = segaux_.as<uint32_t>(); la.seg_done = segaux_.as<uint32_t>() + 1;
+        la.seg_pcnt = seg_pcnt(); la.seg_done = seg_done(1); la.seg_ctr = seg_ctr(1);
         la.children = dch;
-        ck(launch_level(la, true, grid, st), "extract launch");
+        ck(launch_level(la, true, stable_, grid, st), "extract launch");
         ChildRec ch[2];
         ck(cudaMemcpyAsync(ch, dch, sizeof ch, cudaMemcpyDeviceToHost, st), "d2h children");
         ck(cudaStreamSynchronize(st), "sync");
@@ -544,6 +546,23 @@ class Engine {
     uint32_t* h_word_ = nullptr;
     DevBuf partials_, flags_, aggs_, incs_, tile_seg_, chain_, info_, scratch_, out_;
     DevBuf status_, part_, segaux_;
+    bool stable_ = getenv("VQHULL_STABLE") != nullptr && getenv("VQHULL_STABLE")[0] == '1';
+
+    // per-segment scratch of the level kernel: partial count, finished tiles
+    // (u32 each) and the fast mode's packed L/R counter (u64)
+    static size_t segaux_bytes(uint32_t ns) { return size_t(ns) * 16 + 16; }
+    uint32_t* seg_pcnt() { return segaux_.as<uint32_t>(); }
+    uint32_t* seg_done(uint32_t ns) { return segaux_.as<uint32_t>() + ns; }
+    unsigned long long* seg_ctr(uint32_t ns) {
+        return reinterpret_cast<unsigned long long*>(segaux_.as<char>() + ((size_t(ns) * 8 + 7) & ~size_t(7)));
+    }
+    unsigned long long* side_ctr() { return reinterpret_cast<unsigned long long*>(ctrs_ + 8); }
+
+   public:
+    void set_stable(bool s) { stable_ = s; }
+    bool stable() const { return stable_; }
+
+   private:
     PointBuf bufs_[2];
     PointBuf in_;
     std::deque<LevelTables> levels_;  // deque: references stay valid on growth
@@ -632,6 +651,17 @@ int vqhull_cuda_set_timing(int enable) {
         Engine& e = vqb::engine();
         std::lock_guard<std::mutex> lk(e.mutex());
         e.set_timing(enable != 0);
+        return 0;
+    } catch (const CudaError&) {
+        return VQHULL_ECUDA;
+    }
+}
+
+int vqhull_cuda_set_stable(int stable) {
+    try {
+        Engine& e = vqb::engine();
+        std::lock_guard<std::mutex> lk(e.mutex());
+        e.set_stable(stable != 0);
         return 0;
     } catch (const CudaError&) {
         return VQHULL_ECUDA;

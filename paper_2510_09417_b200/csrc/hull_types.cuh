@@ -97,7 +97,8 @@ struct RootArgs {
     double* oy;
     uint32_t* oid;
     uint64_t out_cap;    // debug bounds
-    Status* status;      // 2 per tile (side S1, side S2)
+    Status* status;      // stable mode: 2 per tile (side S1, side S2)
+    unsigned long long* side_ctr;  // fast mode: packed class counters per side
     uint32_t epoch;
     uint32_t* ctr;       // tile claim counter
     uint32_t* ticket;    // CTA exit ticket
@@ -126,6 +127,7 @@ struct LevelArgs {
     Best* tile_part;     // 2 per tile (per-CTA segment partials, indexed tile0 + slot)
     uint32_t* seg_pcnt;  // per segment: partials published
     uint32_t* seg_done;  // per segment: tiles finished
+    unsigned long long* seg_ctr;  // fast mode: packed L/R counters per segment
     ChildRec* children;  // 2 per segment
 };
 

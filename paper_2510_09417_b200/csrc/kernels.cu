@@ -348,6 +348,7 @@ struct PlanArgs {
     uint32_t* ctr;
     uint32_t* seg_pcnt;
     uint32_t* seg_done;
+    unsigned long long* seg_ctr;
 };
 
 __device__ __forceinline__ uint8_t kind_of(uint32_t m) {
@@ -454,6 +455,7 @@ __global__ void __launch_bounds__(kThreads) planner_kernel(PlanArgs a) {
                 a.segs[run.nseg] = g;
                 a.seg_pcnt[run.nseg] = 0;
                 a.seg_done[run.nseg] = 0;
+                a.seg_ctr[run.nseg] = 0ull;
                 a.link[s] = run.nseg;
                 run.nseg += 1;
                 run.ntiles += g.ntiles;
@@ -684,8 +686,9 @@ __global__ void emit_kernel(uint32_t nslots, const uint8_t* kind, const uint32_t
 // Level-1 (root) bookkeeping: the two bootstrap sides as slots, then the
 // final frame [p] S1 [q] S2 once their sizes are known.
 __global__ void root_slots_kernel(const RootInfo* root, ChildRec* slots, uint8_t* kind,
-                                  uint32_t* link) {
+                                  uint32_t* link, unsigned long long* side_ctr) {
     if (threadIdx.x != 0) return;
+    side_ctr[0] = side_ctr[1] = 0ull;  // fast-mode counters of the root partition
     const RootInfo& R = *root;
     ChildRec a, b;
     a.px = R.px; a.py = R.py; a.qx = R.qx; a.qy = R.qy;
@@ -737,10 +740,12 @@ size_t partial_bytes(int grid) {
 void launch_planner(const ChildRec* slots, uint32_t nslots, SegRec* segs, FinRec* fins,
                     uint8_t* kind, uint32_t* link, LevelInfo* info, uint64_t fin_chain_base,
                     uint32_t* flags, void* aggs, void* incs, uint32_t epoch, uint32_t* ctr,
-                    uint32_t* seg_pcnt, uint32_t* seg_done, int max_grid, cudaStream_t st) {
+                    uint32_t* seg_pcnt, uint32_t* seg_done, unsigned long long* seg_ctr,
+                    int max_grid, cudaStream_t st) {
     PlanArgs a;
     a.seg_pcnt = seg_pcnt;
     a.seg_done = seg_done;
+    a.seg_ctr = seg_ctr;
     a.slots = slots; a.nslots = nslots;
     a.nchunks = (nslots + kPlanChunk - 1) / kPlanChunk;
     a.segs = segs; a.fins = fins; a.kind = kind; a.link = link; a.info = info;
@@ -791,8 +796,8 @@ void launch_emit(uint32_t nslots, const uint8_t* kind, const uint32_t* link,
 }
 
 void launch_root_slots(const RootInfo* root, ChildRec* slots, uint8_t* kind, uint32_t* link,
-                       cudaStream_t st) {
-    root_slots_kernel<<<1, 32, 0, st>>>(root, slots, kind, link);
+                       unsigned long long* side_ctr, cudaStream_t st) {
+    root_slots_kernel<<<1, 32, 0, st>>>(root, slots, kind, link, side_ctr);
 }
 
 void launch_root_frame(const RootInfo* root, const uint32_t* size1, uint32_t* start1,

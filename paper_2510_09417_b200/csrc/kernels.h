@@ -14,12 +14,13 @@ void launch_extremes(const double* xs, const double* ys, uint64_t n, void* parti
 void launch_bootstrap(const double* xs, const double* ys, uint64_t n, void* partials,
                       uint32_t* ticket, RootInfo* root, int grid, cudaStream_t st);
 size_t partial_bytes(int grid);
-cudaError_t launch_root_partition(const RootArgs& a, int grid, cudaStream_t st);
-cudaError_t launch_level(const LevelArgs& a, bool general, int grid, cudaStream_t st);
+cudaError_t launch_root_partition(const RootArgs& a, int grid, bool stable, cudaStream_t st);
+cudaError_t launch_level(const LevelArgs& a, bool general, bool stable, int grid, cudaStream_t st);
 void launch_planner(const ChildRec* slots, uint32_t nslots, SegRec* segs, FinRec* fins,
                     uint8_t* kind, uint32_t* link, LevelInfo* info, uint64_t fin_chain_base,
                     uint32_t* flags, void* aggs, void* incs, uint32_t epoch, uint32_t* ctr,
-                    uint32_t* seg_pcnt, uint32_t* seg_done, int max_grid, cudaStream_t st);
+                    uint32_t* seg_pcnt, uint32_t* seg_done, unsigned long long* seg_ctr,
+                    int max_grid, cudaStream_t st);
 void launch_tilemap(const SegRec* segs, const LevelInfo* info, uint32_t* tile_seg,
                     uint32_t ntiles_hint, cudaStream_t st);
 void launch_finisher(const FinRec* fins, const LevelInfo* info, const double* ix,
@@ -33,7 +34,7 @@ void launch_emit(uint32_t nslots, const uint8_t* kind, const uint32_t* link,
                  const uint32_t* chain, const uint32_t* start, const uint32_t* child_size,
                  uint32_t* child_start, uint32_t* out, cudaStream_t st);
 void launch_root_slots(const RootInfo* root, ChildRec* slots, uint8_t* kind, uint32_t* link,
-                       cudaStream_t st);
+                       unsigned long long* side_ctr, cudaStream_t st);
 void launch_root_frame(const RootInfo* root, const uint32_t* size1, uint32_t* start1,
                        uint32_t* out, uint32_t* h_out, cudaStream_t st);
 size_t plan_agg_bytes();

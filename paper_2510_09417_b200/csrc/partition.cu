@@ -89,13 +89,13 @@ __device__ uint2 lookback16(uint32_t tile, uint32_t first, uint32_t c0, uint32_t
             uint32_t spins = 0;
             while (true) {
                 const ulonglong2 i = ld_pair(s->inc);
+                const ulonglong2 g = ld_pair(s->agg);
                 if (tag_of(i.x) == tagI && tag_of(i.y) == tagI) {
                     state = kStInc;
                     v0 = uint32_t(i.x);
                     v1 = uint32_t(i.y);
                     break;
                 }
-                const ulonglong2 g = ld_pair(s->agg);
                 if (tag_of(g.x) == tagA && tag_of(g.y) == tagA) {
                     state = kStAgg;
                     v0 = uint32_t(g.x);
@@ -131,6 +131,19 @@ __device__ uint2 lookback16(uint32_t tile, uint32_t first, uint32_t c0, uint32_t
     return make_uint2(acc0, acc1);
 }
 
+// Two 32-bit class counters packed in one u64, claimed with ONE atomic: the
+// low half never carries into the high half because every count is < 2^32.
+__device__ __forceinline__ uint2 claim_pair(unsigned long long* ctr, uint32_t c0, uint32_t c1) {
+    const unsigned long long old =
+        atomicAdd(ctr, static_cast<unsigned long long>(c0) | (static_cast<unsigned long long>(c1) << 32));
+    return make_uint2(uint32_t(old), uint32_t(old >> 32));
+}
+
+__device__ __forceinline__ uint2 read_pair(const unsigned long long* ctr) {
+    const unsigned long long v = __ldcg(ctr);
+    return make_uint2(uint32_t(v), uint32_t(v >> 32));
+}
+
 // ---------------------------------------------------------------------------
 // Tile staging
 // ---------------------------------------------------------------------------
@@ -142,29 +155,38 @@ struct TileSmem {
     uint32_t wcnt[NC][kItems * kWarps];
     uint32_t cbase[NC + 1];
     uint32_t cnt[NC];    // tile counts per class
-    uint32_t excl[NC];   // exclusive prefix inside the segment (look-back)
+    uint32_t excl[NC];   // offset of the tile inside its range, per class
     unsigned long long rkey[NC][kWarps];  // block reduction scratch
     uint32_t ridx[NC][kWarps];
 };
 
-// Ranks: per-warp ballots then one warp-wide scan per class over the
-// (item, warp) counts.  cls[i] == NC means "no class".  On return S.cnt and
-// S.cbase are final (block-synchronised) and rk[i] holds each item's rank
-// inside its warp and item slot.
+// Ranks: per item 2 (NC=2) or 3 (NC=4) warp ballots encode every lane's
+// class; each lane's rank is a popcount of the lanes before it in its class,
+// and lanes 0..NC-1 record the per-class warp counts.  Then one warp scan per
+// class over the (item, warp) counts.  cls[i] == NC means "no class".
 template <int NC>
 __device__ __forceinline__ void scan_tile(TileSmem<NC>& S, const int (&cls)[kItems],
                                           uint32_t (&rk)[kItems]) {
+    static_assert(NC == 2 || NC == 4, "two or four classes");
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const unsigned lt = lanemask_lt();
 #pragma unroll
     for (int i = 0; i < kItems; ++i) {
-        rk[i] = 0;
-#pragma unroll
-        for (int c = 0; c < NC; ++c) {
-            const unsigned bal = __ballot_sync(kFull, cls[i] == c);
-            if (lane == 0) S.wcnt[c][i * kWarps + warp] = __popc(bal);
-            if (cls[i] == c) rk[i] = __popc(bal & lt);
+        const int c = cls[i];
+        const bool v = c < NC;
+        const unsigned V = __ballot_sync(kFull, v);
+        const unsigned B0 = __ballot_sync(kFull, v && (c & 1));
+        unsigned M, Mq;
+        if (NC == 4) {
+            const unsigned B1 = __ballot_sync(kFull, v && (c & 2));
+            M = V & ((c & 1) ? B0 : ~B0) & ((c & 2) ? B1 : ~B1);
+            Mq = V & ((lane & 1) ? B0 : ~B0) & ((lane & 2) ? B1 : ~B1);
+        } else {
+            M = V & ((c & 1) ? B0 : ~B0);
+            Mq = V & ((lane & 1) ? B0 : ~B0);
         }
+        rk[i] = __popc(M & lt);
+        if (lane < NC) S.wcnt[lane][i * kWarps + warp] = __popc(Mq);
     }
     __syncthreads();
     static_assert(kItems * kWarps == 32, "one scan entry per lane");
@@ -209,7 +231,7 @@ __device__ __forceinline__ void stage_tile(TileSmem<NC>& S, const double (&ux)[k
 }
 
 // Block-wide reduction of every thread's running (key, idx) candidate of
-// class c; returns the winner to thread 0 only.  Uses S.rkey/S.ridx scratch.
+// class c; the winner goes to thread 0 only.
 template <int NC>
 __device__ __forceinline__ void block_key_best(TileSmem<NC>& S, int c, unsigned long long k,
                                                uint32_t i, const double* __restrict__ xs,
@@ -279,12 +301,47 @@ __device__ __forceinline__ Best ldcg_best(const Best* p) {
     return b;
 }
 
+// Branch-free running arg-max update of the candidate's class (one select
+// chain for the incumbent, one predicated write-back); exact offset ties take
+// a warp-uniform slow path that consults the coordinates.
+template <int NC>
+__device__ __forceinline__ void running_best(unsigned long long (&kb)[NC], uint32_t (&ib)[NC],
+                                             int c, unsigned long long k, uint32_t id,
+                                             const double* __restrict__ xs,
+                                             const double* __restrict__ ys) {
+    unsigned long long kc = kb[0];
+    uint32_t ic = ib[0];
+#pragma unroll
+    for (int q = 1; q < NC; ++q) {
+        kc = (c == q) ? kb[q] : kc;
+        ic = (c == q) ? ib[q] : ic;
+    }
+    bool take = (c < NC) && (k < kc);
+    const bool tie = (c < NC) && (k == kc) && (id != ic);
+    if (__any_sync(kFull, tie)) {
+        if (tie) take = key_better(k, id, kc, ic, xs, ys);
+    }
+#pragma unroll
+    for (int q = 0; q < NC; ++q) {
+        const bool w = take && (c == q);
+        kb[q] = w ? k : kb[q];
+        ib[q] = w ? id : ib[q];
+    }
+}
+
 // ===========================================================================
-// Scheduling.  Tile t belongs to CTA t mod G and CTAs visit their tiles in
-// increasing order; all G CTAs are co-resident (cooperative launch), so every
-// look-back waits only on tiles owned by running CTAs that are at most one
-// round behind, and prefetching a CTA's next tile claims nothing another CTA
-// could be waiting for.
+// Scheduling.  Tile t belongs to CTA t mod G; CTAs visit their tiles in
+// increasing order with the next tile prefetched into registers.
+// Output offsets, two modes:
+//   STABLE = false (default): one packed atomicAdd per tile side claims the
+//     tile's place in each class's range; no tile ever waits for another.
+//     The order of survivors inside S1/S2 follows claim order, which the
+//     reference leaves unspecified (extract.hpp:14-18; its own parallel_extract
+//     reorders), so every hull output is unchanged.
+//   STABLE = true: decoupled look-back over self-validating status words gives
+//     each survivor its input-order position (order-preserving compaction).
+//     Launched cooperatively: all G CTAs are co-resident, so every look-back
+//     waits only on running CTAs.
 // ===========================================================================
 
 // ===========================================================================
@@ -295,9 +352,9 @@ __device__ __forceinline__ Best ldcg_best(const Best* p) {
 //   class 2: S2 ∧ left(q->r2)        class 3: S2 ∧ ¬2 ∧ left(r2->p)
 // exactly the sets of the reference's two second-level extract_subsets calls,
 // with r11..r22 from the same pass.  Output: S1's range [0,|S1|) and S2's
-// range [|S1|, |S1|+|S2|), each split two-sided.  Two status words per tile
-// (side S1: classes 0/1, side S2: classes 2/3), looked back by warps 0 and 1.
+// range [|S1|, |S1|+|S2|), each split two-sided.
 // ===========================================================================
+template <bool STABLE>
 __global__ void __launch_bounds__(kThreads, kPartMinBlocks) root_partition_kernel(RootArgs a) {
     __shared__ TileSmem<4> S;
     __shared__ bool s_last;
@@ -353,38 +410,40 @@ __global__ void __launch_bounds__(kThreads, kPartMinBlocks) root_partition_kerne
             const double E = dsub(rx, u), F = dsub(ry, w);
             const bool L = left_diff(P1x, P1y, E, F);         // left of (side start -> r)
             const bool Rr = !L && left_diff(E, F, Q2x, Q2y);  // left of (r -> side end)
-            int c = 4;
-            if (s1) c = L ? 0 : (Rr ? 1 : 4);
-            else if (s2) c = L ? 2 : (Rr ? 3 : 4);
+            const int side = s1 ? 0 : 2;
+            int c = (s1 || s2) ? (L ? side : (Rr ? side + 1 : 4)) : 4;
             c = inr[i] ? c : 4;
             cls[i] = c;
-            if (c < 4) {  // fused farthest-point search (extract_core.hpp:462-463)
-                const double edx = s1 ? (L ? f0x : f1x) : (L ? f2x : f3x);
-                const double edy = s1 ? (L ? f0y : f1y) : (L ? f2y : f3y);
-                const unsigned long long k = key_of(lat_off(edx, edy, u, w));
-#pragma unroll
-                for (int q = 0; q < 4; ++q)
-                    if (c == q) key_consider(kb[q], ib[q], k, uid[i], a.xs, a.ys);
-            }
+            // fused farthest-point search (extract_core.hpp:462-463)
+            const double edx = s1 ? (L ? f0x : f1x) : (L ? f2x : f3x);
+            const double edy = s1 ? (L ? f0y : f1y) : (L ? f2y : f3y);
+            running_best<4>(kb, ib, c, key_of(lat_off(edx, edy, u, w)), uid[i], a.xs, a.ys);
         }
         uint32_t rk[kItems];
         scan_tile<4>(S, cls, rk);
+        uint2 claimed = make_uint2(0u, 0u);
         if (threadIdx.x < 2) {
             const uint32_t side = threadIdx.x;
-            publish_counts(&a.status[uint64_t(t) * 2 + side], t == 0, S.cnt[2 * side],
-                           S.cnt[2 * side + 1], a.epoch);
+            if (STABLE)
+                publish_counts(&a.status[uint64_t(t) * 2 + side], t == 0, S.cnt[2 * side],
+                               S.cnt[2 * side + 1], a.epoch);
+            else
+                claimed = claim_pair(&a.side_ctr[side], S.cnt[2 * side], S.cnt[2 * side + 1]);
         }
         stage_tile<4>(S, ux, uy, uid, cls, rk);
         const uint32_t tn = t + gridDim.x;
-        if (tn < a.ntiles) load(tn);  // in flight during the look-back and the stores
-        if (threadIdx.x < 64) {
-            const uint32_t side = threadIdx.x >> 5;
-            const uint2 e = lookback16(t, 0u, S.cnt[2 * side], S.cnt[2 * side + 1], a.status, 2u,
-                                       side, a.epoch);
-            if ((threadIdx.x & 31) == 0) {
-                S.excl[2 * side] = e.x;
-                S.excl[2 * side + 1] = e.y;
+        if (tn < a.ntiles) load(tn);  // in flight during the offsets and the stores
+        if (STABLE) {
+            if (threadIdx.x < 64) {
+                const uint32_t side = threadIdx.x >> 5;
+                claimed = lookback16(t, 0u, S.cnt[2 * side], S.cnt[2 * side + 1], a.status, 2u,
+                                     side, a.epoch);
             }
+        }
+        if ((STABLE && (threadIdx.x & 31) == 0 && threadIdx.x < 64) || (!STABLE && threadIdx.x < 2)) {
+            const uint32_t side = STABLE ? (threadIdx.x >> 5) : threadIdx.x;
+            S.excl[2 * side] = claimed.x;
+            S.excl[2 * side + 1] = claimed.y;
         }
         __syncthreads();
         flush_tile<4>(S, base, fwd, a.ox, a.oy, a.oid, a.out_cap);
@@ -392,7 +451,7 @@ __global__ void __launch_bounds__(kThreads, kPartMinBlocks) root_partition_kerne
         t = tn;
     }
     // CTA arg-max partials; the last CTA out reduces them and emits the four
-    // child nodes (counts from the last tile's inclusive status words)
+    // child nodes
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
         unsigned long long ko;
@@ -423,7 +482,9 @@ __global__ void __launch_bounds__(kThreads, kPartMinBlocks) root_partition_kerne
         if (lane == 0) {
             uint32_t m = 0;
             if (a.ntiles) {
-                const uint2 w = inclusive_of(&a.status[uint64_t(a.ntiles - 1) * 2 + (c >> 1)], a.epoch);
+                const uint2 w = STABLE
+                    ? inclusive_of(&a.status[uint64_t(a.ntiles - 1) * 2 + (c >> 1)], a.epoch)
+                    : read_pair(&a.side_ctr[c >> 1]);
                 m = (c & 1) ? w.y : w.x;
             }
             ChildRec ch;
@@ -449,12 +510,12 @@ __global__ void __launch_bounds__(kThreads, kPartMinBlocks) root_partition_kerne
 // Tiles never straddle segments; a segment's tiles are consecutive ids.
 // GENERAL = two unrelated edges (the extract_subsets API); otherwise the
 // edges p->r and r->q share r (two subtractions saved per point).
-// The arg-max leaves the look-back: each thread keeps a running best for the
-// segment its CTA is visiting; on leaving a segment the CTA reduces them and
-// publishes one partial; the CTA whose finished-tile count completes the
-// segment reduces the partials and emits the two children.
+// Each thread keeps a running best for the segment its CTA is visiting; on
+// leaving a segment the CTA reduces them and publishes one partial; the CTA
+// whose finished-tile count completes the segment reduces the partials and
+// emits the two children.
 // ===========================================================================
-template <bool GENERAL>
+template <bool GENERAL, bool STABLE>
 __global__ void __launch_bounds__(kThreads, kPartMinBlocks) level_kernel(LevelArgs a) {
     __shared__ TileSmem<2> S;
     __shared__ SegRec s_seg[2];
@@ -475,8 +536,6 @@ __global__ void __launch_bounds__(kThreads, kPartMinBlocks) level_kernel(LevelAr
     unsigned long long kb[2] = {kNoKey, kNoKey};
     uint32_t ib[2] = {kNoIdx, kNoIdx};
 
-    // leave segment s_cur: reduce this CTA's candidates, publish the partial;
-    // the CTA completing the segment's tile count emits the children
     auto finalize = [&]() {
         for (int c = 0; c < 2; ++c) {
             unsigned long long ko;
@@ -512,7 +571,9 @@ __global__ void __launch_bounds__(kThreads, kPartMinBlocks) level_kernel(LevelAr
                 b = warp_best(b);
                 if (lane == 0) {
                     const SegRec& g = s_cur;
-                    const uint2 w = inclusive_of(&a.status[uint64_t(g.tile0) + g.ntiles - 1], a.epoch);
+                    const uint2 w = STABLE
+                        ? inclusive_of(&a.status[uint64_t(g.tile0) + g.ntiles - 1], a.epoch)
+                        : read_pair(&a.seg_ctr[s_cur_k]);
                     const uint32_t m = c == 0 ? w.x : w.y;
                     ChildRec ch;
                     if (c == 0) {  // left of p->r: triangle (p, rL, r)
@@ -602,12 +663,9 @@ __global__ void __launch_bounds__(kThreads, kPartMinBlocks) level_kernel(LevelAr
                 const bool v = uint32_t(i) * kThreads + threadIdx.x < cnt;
                 const int c = !v ? 2 : (la ? 0 : (lb ? 1 : 2));
                 cls[i] = c;
-                if (c < 2) {  // fused farthest-point search
-                    const unsigned long long k =
-                        key_of(lat_off(c == 0 ? adx : bdx, c == 0 ? ady : bdy, u, w));
-                    if (c == 0) key_consider(kb[0], ib[0], k, uid[i], a.gx, a.gy);
-                    else key_consider(kb[1], ib[1], k, uid[i], a.gx, a.gy);
-                }
+                // fused farthest-point search
+                const unsigned long long k = key_of(lat_off(la ? adx : bdx, la ? ady : bdy, u, w));
+                running_best<2>(kb, ib, c, k, uid[i], a.gx, a.gy);
             }
         }
         const uint32_t tile0 = g.tile0;
@@ -615,17 +673,19 @@ __global__ void __launch_bounds__(kThreads, kPartMinBlocks) level_kernel(LevelAr
         const bool fwd[2] = {true, false};
         uint32_t rk[kItems];
         scan_tile<2>(S, cls, rk);
-        if (threadIdx.x == 0)
-            publish_counts(&a.status[t], t == tile0, S.cnt[0], S.cnt[1], a.epoch);
+        uint2 claimed = make_uint2(0u, 0u);
+        if (threadIdx.x == 0) {
+            if (STABLE) publish_counts(&a.status[t], t == tile0, S.cnt[0], S.cnt[1], a.epoch);
+            else claimed = claim_pair(&a.seg_ctr[k_now], S.cnt[0], S.cnt[1]);
+        }
         stage_tile<2>(S, ux, uy, uid, cls, rk);
         const uint32_t tn = t + gridDim.x;
-        if (tn < ntiles) fetch(tn, b ^ 1);  // in flight during the look-back and the stores
-        if (warp == 0) {
-            const uint2 e = lookback16(t, tile0, S.cnt[0], S.cnt[1], a.status, 1u, 0u, a.epoch);
-            if (lane == 0) {
-                S.excl[0] = e.x;
-                S.excl[1] = e.y;
-            }
+        if (tn < ntiles) fetch(tn, b ^ 1);  // in flight during the offsets and the stores
+        if (STABLE && warp == 0)
+            claimed = lookback16(t, tile0, S.cnt[0], S.cnt[1], a.status, 1u, 0u, a.epoch);
+        if (threadIdx.x == 0) {
+            S.excl[0] = claimed.x;
+            S.excl[1] = claimed.y;
         }
         __syncthreads();
         flush_tile<2>(S, base, fwd, a.ox, a.oy, a.oid, a.out_cap);
@@ -638,30 +698,42 @@ __global__ void __launch_bounds__(kThreads, kPartMinBlocks) level_kernel(LevelAr
 }
 
 // ===========================================================================
-// launchers: cooperative, so all CTAs of the static schedule are co-resident
+// launchers (the stable mode is launched cooperatively: co-resident CTAs)
 // ===========================================================================
-cudaError_t launch_root_partition(const RootArgs& a, int grid, cudaStream_t st) {
+cudaError_t launch_root_partition(const RootArgs& a, int grid, bool stable, cudaStream_t st) {
+    if (!stable) {
+        root_partition_kernel<false><<<grid, kThreads, 0, st>>>(a);
+        return cudaGetLastError();
+    }
     void* args[] = {const_cast<RootArgs*>(&a)};
-    return cudaLaunchCooperativeKernel((const void*)root_partition_kernel, dim3(grid),
+    return cudaLaunchCooperativeKernel((const void*)root_partition_kernel<true>, dim3(grid),
                                        dim3(kThreads), args, 0, st);
 }
 
-cudaError_t launch_level(const LevelArgs& a, bool general, int grid, cudaStream_t st) {
+cudaError_t launch_level(const LevelArgs& a, bool general, bool stable, int grid, cudaStream_t st) {
+    if (!stable) {
+        if (general) level_kernel<true, false><<<grid, kThreads, 0, st>>>(a);
+        else level_kernel<false, false><<<grid, kThreads, 0, st>>>(a);
+        return cudaGetLastError();
+    }
     void* args[] = {const_cast<LevelArgs*>(&a)};
-    const void* fn = general ? (const void*)level_kernel<true> : (const void*)level_kernel<false>;
+    const void* fn = general ? (const void*)level_kernel<true, true> : (const void*)level_kernel<false, true>;
     return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kThreads), args, 0, st);
 }
 
 int occupancy_root() {
-    int b = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, root_partition_kernel, kThreads, 0);
-    return b;
+    int b = 0, c = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, root_partition_kernel<true>, kThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, root_partition_kernel<false>, kThreads, 0);
+    return b < c ? b : c;
 }
 int occupancy_level() {
-    int b = 0, c = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, level_kernel<false>, kThreads, 0);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, level_kernel<true>, kThreads, 0);
-    return b < c ? b : c;
+    int m = 1 << 30, b = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, level_kernel<false, false>, kThreads, 0); m = b < m ? b : m;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, level_kernel<true, false>, kThreads, 0); m = b < m ? b : m;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, level_kernel<false, true>, kThreads, 0); m = b < m ? b : m;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, level_kernel<true, true>, kThreads, 0); m = b < m ? b : m;
+    return m;
 }
 
 }  // namespace vqb

@@ -237,3 +237,34 @@ def test_stats_and_timing(vq, cuda):
     assert s["n"] == 1_000_000 and s["hull_size"] == 333
     assert s["timing_valid"] == 1 and s["ms_total"] > 0
     assert s["launches"] > 5 and s["bytes_moved"] >= 40 * 1_000_000
+
+
+# --- both output-offset modes give the same hulls ------------------------------
+def test_stable_lookback_mode(vq, cuda, oracle):
+    """VQHULL stable mode (decoupled look-back, order-preserving compaction)
+    must produce exactly the same index lists as the default atomic mode."""
+    vq.set_stable(True)
+    try:
+        for name, xs, ys, idx, hx, hy in G.hull_cases()[::2]:
+            rc, got = vq.vqhull_compute(xs, ys)
+            assert rc == 0 and np.array_equal(got, idx), name
+        rng = np.random.default_rng(99)
+        for it in range(120):
+            xs, ys = random_instance(rng, it)
+            if len(xs):
+                assert np.array_equal(gpu_indices(vq, xs, ys), oracle.hull_indices(xs, ys))
+        for name in ("config1_disk_1e6_s1", "config3_circle_1e7_s3"):
+            cfg = G.configs()[name]
+            xs, ys = vq.generate(cfg["kind"], cfg["n"], cfg["seed"])
+            got = gpu_indices(vq, xs, ys)
+            assert f"{oracle.fnv1a64(got):016x}" == cfg["fnv1a64_u64le"]
+        # the stable mode's extract keeps S1 in input order (order-preserving)
+        rng = np.random.default_rng(5)
+        xs, ys = rng.uniform(-1, 1, 300_000), rng.uniform(-1, 1, 300_000)
+        X, Y = dev(xs), dev(ys)
+        out = vq.extract_subsets(X, Y, [-1.0, 0.0, 1.0, 0.5], [1.0, 0.5, -1.0, 0.0])
+        x = X.cpu().numpy()[:out.w_l]
+        a = (-1.0 - xs) * (0.5 - ys) > (0.0 - ys) * (1.0 - xs)
+        assert np.array_equal(x, xs[a])
+    finally:
+        vq.set_stable(False)
