@@ -99,7 +99,8 @@ class Engine {
             uint64_t thr = UINT64_MAX;
             cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
         }
-        occ_root_ = std::max(1, occupancy_root());
+        occ_root_ = std::max(1, occupancy_root(false));
+        occ_root_stable_ = std::max(1, occupancy_root(true));
         occ_level_ = std::max(1, occupancy_level());
         occ_fin_ = std::max(1, occupancy_finisher());
         stream_grid_ = sms_ * std::max(1, std::min(8, occupancy_stream()));  // one full wave
@@ -155,7 +156,7 @@ class Engine {
         LevelTables& L2 = level(2);
         L2.slots.ensure(4 * sizeof(ChildRec), st);
         {
-            const int grid = std::max(1, std::min<int>(int(ntiles_root), sms_ * occ_root_));
+            const int grid = std::max(1, std::min<int>(int(ntiles_root), sms_ * (stable_ ? occ_root_stable_ : occ_root_)));
             part_.ensure(size_t(grid) * 4 * sizeof(Best), st);
             RootArgs ra;
             ra.xs = dx; ra.ys = dy; ra.n = n; ra.root = root_;
@@ -536,7 +537,7 @@ class Engine {
    private:
     int dev_ = 0;
     int sms_ = 148;
-    int occ_root_ = 1, occ_level_ = 1, occ_fin_ = 1;
+    int occ_root_ = 1, occ_root_stable_ = 1, occ_level_ = 1, occ_fin_ = 1;
     int stream_grid_ = 592;
     uint32_t* ctrs_ = nullptr;
     RootInfo* root_ = nullptr;

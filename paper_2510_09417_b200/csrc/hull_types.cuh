@@ -17,6 +17,7 @@ constexpr int kItems = 4;                   // points per thread per tile
 constexpr int kTile = kThreads * kItems;    // points per partition tile
 constexpr int kWarps = kThreads / 32;
 constexpr int kPartMinBlocks = 3;           // resident partition CTAs per SM (register cap)
+constexpr int kFastMinBlocks = 4;           // fast-mode kernels (no staging)
 constexpr uint32_t kFinMax = 256;           // segments this small go to the warp finisher
 
 // K1 + pass A results, one per hull call (device resident).

@@ -38,7 +38,7 @@ void launch_root_slots(const RootInfo* root, ChildRec* slots, uint8_t* kind, uin
 void launch_root_frame(const RootInfo* root, const uint32_t* size1, uint32_t* start1,
                        uint32_t* out, uint32_t* h_out, cudaStream_t st);
 size_t plan_agg_bytes();
-int occupancy_root();
+int occupancy_root(bool stable);
 int occupancy_level();
 int occupancy_finisher();
 int occupancy_stream();

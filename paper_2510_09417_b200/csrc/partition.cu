@@ -698,11 +698,260 @@ __global__ void __launch_bounds__(kThreads, kPartMinBlocks) level_kernel(LevelAr
 }
 
 // ===========================================================================
+// Fast mode (default): no staging.  Per item, 2-3 warp ballots give every
+// lane its rank inside its class among the warp's earlier lanes; per-warp
+// running class counts live in lanes 0..NC-1 and are broadcast by shuffle.
+// One tiny block scan over (class, warp) totals and one packed atomic per
+// side claim the tile's place; survivors are then stored straight from
+// registers — each warp store instruction writes one contiguous run per
+// class.  The order inside S1/S2 follows claim order (unspecified in the
+// reference, extract.hpp:14-18).
+// ===========================================================================
+struct FastSmem {
+    uint32_t wtot[4][kWarps];   // per (class, warp) counts of the tile
+    uint32_t wbase[4][kWarps];  // exclusive offsets of each warp inside the tile's class run
+    uint32_t claim[4];          // the tile's offset inside each class range
+    unsigned long long rkey[4][kWarps];
+    uint32_t ridx[4][kWarps];
+};
+
+// running arg-max with double incumbents: a candidate is examined closely
+// only when it is at least as good as its class incumbent, which after the
+// first tiles is rare, so the common path is one compare per point.
+template <int NC>
+__device__ __forceinline__ void running_best_d(double (&bo)[NC], uint32_t (&bi)[NC], int c,
+                                               double off, uint32_t id,
+                                               const double* __restrict__ xs,
+                                               const double* __restrict__ ys) {
+    double inc = bo[0];
+#pragma unroll
+    for (int q = 1; q < NC; ++q) inc = (c == q) ? bo[q] : inc;
+    const bool maybe = (c < NC) && !(off > inc);  // off <= inc (incumbent +inf when empty)
+    if (__any_sync(kFull, maybe)) {
+        if (maybe) {
+            uint32_t ic = bi[0];
+#pragma unroll
+            for (int q = 1; q < NC; ++q) ic = (c == q) ? bi[q] : ic;
+            bool take = off < inc || ic == kNoIdx;
+            if (!take && off == inc && id != ic) {  // exact offset tie: lexicographic, then index
+                const double x = xs[id], y = ys[id], xb = xs[ic], yb = ys[ic];
+                take = (x != xb) ? (x < xb) : ((y != yb) ? (y < yb) : (id < ic));
+            }
+#pragma unroll
+            for (int q = 0; q < NC; ++q) {
+                if (take && c == q) {
+                    bo[q] = off;
+                    bi[q] = id;
+                }
+            }
+        }
+    }
+}
+
+template <int NC>
+__device__ __forceinline__ void block_best_d(FastSmem& S, int c, double off, uint32_t i,
+                                             const double* __restrict__ xs,
+                                             const double* __restrict__ ys,
+                                             double& oo, uint32_t& io) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    unsigned long long k = (i == kNoIdx) ? kNoKey : key_of(off);
+    warp_key_best(k, i, xs, ys);
+    if (lane == 0) {
+        S.rkey[c][warp] = k;
+        S.ridx[c][warp] = i;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long ko = S.rkey[c][0];
+        io = S.ridx[c][0];
+        for (int w = 1; w < kWarps; ++w) {
+            const unsigned long long kk = S.rkey[c][w];
+            const uint32_t ii = S.ridx[c][w];
+            if (kk < ko || (kk == ko && key_better(kk, ii, ko, io, xs, ys))) {
+                ko = kk;
+                io = ii;
+            }
+        }
+        oo = 0.0;
+    }
+    __syncthreads();
+}
+
+// ranks of one item: returns the lane's rank among the warp's lanes of its
+// class so far (earlier items included); wrun (lanes < NC) accumulates counts
+template <int NC>
+__device__ __forceinline__ uint32_t warp_rank(int c, uint32_t& wrun) {
+    const int lane = threadIdx.x & 31;
+    const bool v = c < NC;
+    const unsigned V = __ballot_sync(kFull, v);
+    const unsigned B0 = __ballot_sync(kFull, v && (c & 1));
+    unsigned M, Mq;
+    if (NC == 4) {
+        const unsigned B1 = __ballot_sync(kFull, v && (c & 2));
+        M = V & ((c & 1) ? B0 : ~B0) & ((c & 2) ? B1 : ~B1);
+        Mq = V & ((lane & 1) ? B0 : ~B0) & ((lane & 2) ? B1 : ~B1);
+    } else {
+        M = V & ((c & 1) ? B0 : ~B0);
+        Mq = V & ((lane & 1) ? B0 : ~B0);
+    }
+    const uint32_t before = __shfl_sync(kFull, wrun, c & (NC - 1));
+    wrun += (lane < NC) ? __popc(Mq) : 0u;
+    return before + __popc(M & lanemask_lt());
+}
+
+// tile-level: (class, warp) exclusive offsets + class totals (by warp 0)
+template <int NC>
+__device__ __forceinline__ void tile_scan_fast(FastSmem& S, uint32_t (&tot)[NC]) {
+    const int lane = threadIdx.x & 31;
+    static_assert(NC * kWarps <= 32, "one lane per (class, warp)");
+    const int c = lane / kWarps, w = lane % kWarps;
+    uint32_t v = (lane < NC * kWarps) ? S.wtot[c][w] : 0u;
+    uint32_t incl = v;
+#pragma unroll
+    for (int d = 1; d < kWarps; d <<= 1) {
+        const uint32_t o = __shfl_up_sync(kFull, incl, d, kWarps);
+        if (w >= d) incl += o;
+    }
+    if (lane < NC * kWarps) S.wbase[c][w] = incl - v;
+#pragma unroll
+    for (int q = 0; q < NC; ++q) tot[q] = __shfl_sync(kFull, incl, q * kWarps + kWarps - 1);
+}
+
+__global__ void __launch_bounds__(kThreads, kFastMinBlocks) root_partition_fast(RootArgs a) {
+    __shared__ FastSmem S;
+    __shared__ bool s_last;
+    const RootInfo& R = *a.root;
+    const double px = R.px, py = R.py, qx = R.qx, qy = R.qy;
+    const double r1x = R.r1.x, r1y = R.r1.y, r2x = R.r2.x, r2y = R.r2.y;
+    const uint32_t n1 = R.cnt1, n2 = R.cnt2;
+    const double f0x = dsub(r1x, px), f0y = dsub(r1y, py);
+    const double f1x = dsub(qx, r1x), f1y = dsub(qy, r1y);
+    const double f2x = dsub(r2x, qx), f2y = dsub(r2y, qy);
+    const double f3x = dsub(px, r2x), f3y = dsub(py, r2y);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const double kInf = __longlong_as_double(0x7ff0000000000000ll);
+    double bo[4] = {kInf, kInf, kInf, kInf};
+    uint32_t bi[4] = {kNoIdx, kNoIdx, kNoIdx, kNoIdx};
+
+    for (uint32_t t = blockIdx.x; t < a.ntiles; t += gridDim.x) {
+        const uint64_t start = uint64_t(t) * kTile;
+        double ux[kItems], uy[kItems];
+        int cls[kItems];
+        uint32_t rk[kItems];
+#pragma unroll
+        for (int i = 0; i < kItems; ++i) {
+            const uint64_t pos = start + uint64_t(i) * kThreads + threadIdx.x;
+            const bool in = pos < a.n;
+            ux[i] = in ? ld_stream(a.xs + pos) : 0.0;
+            uy[i] = in ? ld_stream(a.ys + pos) : 0.0;
+        }
+        uint32_t wrun = 0;
+#pragma unroll
+        for (int i = 0; i < kItems; ++i) {
+            const uint64_t pos = start + uint64_t(i) * kThreads + threadIdx.x;
+            const double u = ux[i], w = uy[i];
+            const double A = dsub(px, u), B = dsub(py, w);
+            const double Cc = dsub(qx, u), D = dsub(qy, w);
+            const double t1 = dmul(A, D), t2 = dmul(B, Cc);
+            const bool s1 = t1 > t2;           // left of p->q
+            const bool s2 = !s1 && (t2 > t1);  // left of q->p
+            const double rx = s1 ? r1x : r2x, ry = s1 ? r1y : r2y;
+            const double P1x = s1 ? A : Cc, P1y = s1 ? B : D;
+            const double Q2x = s1 ? Cc : A, Q2y = s1 ? D : B;
+            const double E = dsub(rx, u), F = dsub(ry, w);
+            const bool L = left_diff(P1x, P1y, E, F);
+            const bool Rr = !L && left_diff(E, F, Q2x, Q2y);
+            const int side = s1 ? 0 : 2;
+            int c = (s1 || s2) ? (L ? side : (Rr ? side + 1 : 4)) : 4;
+            c = (pos < a.n) ? c : 4;
+            cls[i] = c;
+            rk[i] = warp_rank<4>(c, wrun);
+            const double edx = s1 ? (L ? f0x : f1x) : (L ? f2x : f3x);
+            const double edy = s1 ? (L ? f0y : f1y) : (L ? f2y : f3y);
+            running_best_d<4>(bo, bi, c, lat_off(edx, edy, u, w), uint32_t(pos), a.xs, a.ys);
+        }
+        if (lane < 4) S.wtot[lane][warp] = wrun;
+        __syncthreads();
+        if (warp == 0) {
+            uint32_t tot[4];
+            tile_scan_fast<4>(S, tot);
+            if (lane < 2) {
+                const uint2 cl = claim_pair(&a.side_ctr[lane], tot[2 * lane], tot[2 * lane + 1]);
+                S.claim[2 * lane] = cl.x;
+                S.claim[2 * lane + 1] = cl.y;
+            }
+        }
+        __syncthreads();
+        // stores straight from registers: base[c] forward / backward
+#pragma unroll
+        for (int i = 0; i < kItems; ++i) {
+            const int c = cls[i];
+            if (c < 4) {
+                const uint64_t r = uint64_t(S.claim[c]) + S.wbase[c][warp] + rk[i];
+                const uint64_t p = (c == 0) ? r
+                                 : (c == 1) ? uint64_t(n1) - 1 - r
+                                 : (c == 2) ? uint64_t(n1) + r
+                                            : uint64_t(n1) + n2 - 1 - r;
+                VQB_CHECK(p < a.out_cap, 12, p, a.out_cap);
+                a.ox[p] = ux[i];
+                a.oy[p] = uy[i];
+                a.oid[p] = uint32_t(start + uint64_t(i) * kThreads + threadIdx.x);
+            }
+        }
+    }
+    // CTA partials -> last CTA emits the four children
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        double oo;
+        uint32_t io;
+        block_best_d<4>(S, q, bo[q], bi[q], a.xs, a.ys, oo, io);
+        if (threadIdx.x == 0) {
+            const double edx = q == 0 ? f0x : (q == 1 ? f1x : (q == 2 ? f2x : f3x));
+            const double edy = q == 0 ? f0y : (q == 1 ? f1y : (q == 2 ? f2y : f3y));
+            a.cta_part[blockIdx.x * 4 + q] = best_from_key(io == kNoIdx ? kNoKey : 0ull, io, edx, edy, a.xs, a.ys);
+        }
+    }
+    if (threadIdx.x == 0) {
+        __threadfence();
+        s_last = atomicAdd(a.ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    if (warp < 4) {
+        const int c = warp;
+        Best b = best_none();
+        for (uint32_t k = lane; k < gridDim.x; k += 32) {
+            const Best o = ldcg_best(&a.cta_part[k * 4 + c]);
+            if (prefer(o, b)) b = o;
+        }
+        b = warp_best(b);
+        if (lane == 0) {
+            const uint2 w = read_pair(&a.side_ctr[c >> 1]);
+            const uint32_t m = (c & 1) ? w.y : w.x;
+            ChildRec ch;
+            ch.px = c == 0 ? px : (c == 1 ? r1x : (c == 2 ? qx : r2x));
+            ch.py = c == 0 ? py : (c == 1 ? r1y : (c == 2 ? qy : r2y));
+            ch.qx = c == 0 ? r1x : (c == 1 ? qx : (c == 2 ? r2x : px));
+            ch.qy = c == 0 ? r1y : (c == 1 ? qy : (c == 2 ? r2y : py));
+            ch.rx = b.x;
+            ch.ry = b.y;
+            ch.r_idx = b.idx;
+            ch.m = m;
+            ch.begin = (c & 1) ? (c == 1 ? uint64_t(n1) - m : uint64_t(n1) + n2 - m)
+                               : (c == 0 ? 0 : uint64_t(n1));
+            a.children[c] = ch;
+        }
+    }
+    if (threadIdx.x == 0) *a.ticket = 0;
+}
+
+// ===========================================================================
 // launchers (the stable mode is launched cooperatively: co-resident CTAs)
 // ===========================================================================
 cudaError_t launch_root_partition(const RootArgs& a, int grid, bool stable, cudaStream_t st) {
     if (!stable) {
-        root_partition_kernel<false><<<grid, kThreads, 0, st>>>(a);
+        root_partition_fast<<<grid, kThreads, 0, st>>>(a);
         return cudaGetLastError();
     }
     void* args[] = {const_cast<RootArgs*>(&a)};
@@ -721,11 +970,11 @@ cudaError_t launch_level(const LevelArgs& a, bool general, bool stable, int grid
     return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kThreads), args, 0, st);
 }
 
-int occupancy_root() {
-    int b = 0, c = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, root_partition_kernel<true>, kThreads, 0);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, root_partition_kernel<false>, kThreads, 0);
-    return b < c ? b : c;
+int occupancy_root(bool stable) {
+    int b = 0;
+    if (stable) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, root_partition_kernel<true>, kThreads, 0);
+    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, root_partition_fast, kThreads, 0);
+    return b;
 }
 int occupancy_level() {
     int m = 1 << 30, b = 0;
