@@ -819,36 +819,48 @@ __device__ __forceinline__ void tile_scan_fast(FastSmem& S, uint32_t (&tot)[NC])
 
 __global__ void __launch_bounds__(kThreads, kFastMinBlocks) root_partition_fast(RootArgs a) {
     __shared__ FastSmem S;
+    __shared__ double2 s_frame[4];   // class frames (edx, edy)
+    __shared__ uint32_t s_org[4][kWarps];  // per (class, warp): store origin of rank 0
     __shared__ bool s_last;
     const RootInfo& R = *a.root;
     const double px = R.px, py = R.py, qx = R.qx, qy = R.qy;
     const double r1x = R.r1.x, r1y = R.r1.y, r2x = R.r2.x, r2y = R.r2.y;
     const uint32_t n1 = R.cnt1, n2 = R.cnt2;
-    const double f0x = dsub(r1x, px), f0y = dsub(r1y, py);
-    const double f1x = dsub(qx, r1x), f1y = dsub(qy, r1y);
-    const double f2x = dsub(r2x, qx), f2y = dsub(r2y, qy);
-    const double f3x = dsub(px, r2x), f3y = dsub(py, r2y);
+    const uint32_t n = uint32_t(a.n);  // < 2^32 (checked by the driver)
+    if (threadIdx.x == 0) {
+        // child frames (kernels.hpp:23-25): 0: p->r1, 1: r1->q, 2: q->r2, 3: r2->p
+        s_frame[0] = make_double2(dsub(r1x, px), dsub(r1y, py));
+        s_frame[1] = make_double2(dsub(qx, r1x), dsub(qy, r1y));
+        s_frame[2] = make_double2(dsub(r2x, qx), dsub(r2y, qy));
+        s_frame[3] = make_double2(dsub(px, r2x), dsub(py, r2y));
+    }
+    __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const double kInf = __longlong_as_double(0x7ff0000000000000ll);
     double bo[4] = {kInf, kInf, kInf, kInf};
     uint32_t bi[4] = {kNoIdx, kNoIdx, kNoIdx, kNoIdx};
 
-    for (uint32_t t = blockIdx.x; t < a.ntiles; t += gridDim.x) {
-        const uint64_t start = uint64_t(t) * kTile;
-        double ux[kItems], uy[kItems];
-        int cls[kItems];
-        uint32_t rk[kItems];
+    double ux[kItems], uy[kItems];
+    auto load = [&](uint32_t t) {
+        const uint32_t start = t * uint32_t(kTile) + threadIdx.x;
 #pragma unroll
         for (int i = 0; i < kItems; ++i) {
-            const uint64_t pos = start + uint64_t(i) * kThreads + threadIdx.x;
-            const bool in = pos < a.n;
+            const uint32_t pos = start + uint32_t(i) * kThreads;
+            const bool in = pos < n;
             ux[i] = in ? ld_stream(a.xs + pos) : 0.0;
             uy[i] = in ? ld_stream(a.ys + pos) : 0.0;
         }
+    };
+    uint32_t t = blockIdx.x;
+    if (t < a.ntiles) load(t);
+    while (t < a.ntiles) {
+        const uint32_t start = t * uint32_t(kTile) + threadIdx.x;
+        int cls[kItems];
+        uint32_t rk[kItems];
         uint32_t wrun = 0;
 #pragma unroll
         for (int i = 0; i < kItems; ++i) {
-            const uint64_t pos = start + uint64_t(i) * kThreads + threadIdx.x;
+            const uint32_t pos = start + uint32_t(i) * kThreads;
             const double u = ux[i], w = uy[i];
             const double A = dsub(px, u), B = dsub(py, w);
             const double Cc = dsub(qx, u), D = dsub(qy, w);
@@ -863,41 +875,51 @@ __global__ void __launch_bounds__(kThreads, kFastMinBlocks) root_partition_fast(
             const bool Rr = !L && left_diff(E, F, Q2x, Q2y);
             const int side = s1 ? 0 : 2;
             int c = (s1 || s2) ? (L ? side : (Rr ? side + 1 : 4)) : 4;
-            c = (pos < a.n) ? c : 4;
+            c = (pos < n) ? c : 4;
             cls[i] = c;
             rk[i] = warp_rank<4>(c, wrun);
-            const double edx = s1 ? (L ? f0x : f1x) : (L ? f2x : f3x);
-            const double edy = s1 ? (L ? f0y : f1y) : (L ? f2y : f3y);
-            running_best_d<4>(bo, bi, c, lat_off(edx, edy, u, w), uint32_t(pos), a.xs, a.ys);
+            const double2 fr = s_frame[c & 3];
+            running_best_d<4>(bo, bi, c, lat_off(fr.x, fr.y, u, w), pos, a.xs, a.ys);
         }
         if (lane < 4) S.wtot[lane][warp] = wrun;
         __syncthreads();
         if (warp == 0) {
             uint32_t tot[4];
             tile_scan_fast<4>(S, tot);
+            uint32_t cl = 0;
             if (lane < 2) {
-                const uint2 cl = claim_pair(&a.side_ctr[lane], tot[2 * lane], tot[2 * lane + 1]);
-                S.claim[2 * lane] = cl.x;
-                S.claim[2 * lane + 1] = cl.y;
+                const uint2 c2 = claim_pair(&a.side_ctr[lane], tot[2 * lane], tot[2 * lane + 1]);
+                S.claim[2 * lane] = c2.x;
+                S.claim[2 * lane + 1] = c2.y;
             }
+            __syncwarp();
+            // store origin of rank 0 of every (class, warp): forward classes
+            // grow from the range start, backward ones shrink from its end
+            if (lane < 4 * kWarps) {
+                const int c = lane / kWarps, w = lane % kWarps;
+                const uint32_t off = S.claim[c] + S.wbase[c][w];
+                const uint32_t org = c == 0 ? 0u : (c == 1 ? n1 - 1u : (c == 2 ? n1 : n1 + n2 - 1u));
+                s_org[c][w] = (c & 1) ? org - off : org + off;
+            }
+            (void)cl;
         }
         __syncthreads();
-        // stores straight from registers: base[c] forward / backward
+        // stores straight from registers
 #pragma unroll
         for (int i = 0; i < kItems; ++i) {
             const int c = cls[i];
             if (c < 4) {
-                const uint64_t r = uint64_t(S.claim[c]) + S.wbase[c][warp] + rk[i];
-                const uint64_t p = (c == 0) ? r
-                                 : (c == 1) ? uint64_t(n1) - 1 - r
-                                 : (c == 2) ? uint64_t(n1) + r
-                                            : uint64_t(n1) + n2 - 1 - r;
+                const uint32_t o = s_org[c][warp];
+                const uint32_t p = (c & 1) ? o - rk[i] : o + rk[i];
                 VQB_CHECK(p < a.out_cap, 12, p, a.out_cap);
                 a.ox[p] = ux[i];
                 a.oy[p] = uy[i];
-                a.oid[p] = uint32_t(start + uint64_t(i) * kThreads + threadIdx.x);
+                a.oid[p] = start + uint32_t(i) * kThreads;
             }
         }
+        const uint32_t tn = t + gridDim.x;
+        if (tn < a.ntiles) load(tn);
+        t = tn;
     }
     // CTA partials -> last CTA emits the four children
 #pragma unroll
@@ -905,11 +927,9 @@ __global__ void __launch_bounds__(kThreads, kFastMinBlocks) root_partition_fast(
         double oo;
         uint32_t io;
         block_best_d<4>(S, q, bo[q], bi[q], a.xs, a.ys, oo, io);
-        if (threadIdx.x == 0) {
-            const double edx = q == 0 ? f0x : (q == 1 ? f1x : (q == 2 ? f2x : f3x));
-            const double edy = q == 0 ? f0y : (q == 1 ? f1y : (q == 2 ? f2y : f3y));
-            a.cta_part[blockIdx.x * 4 + q] = best_from_key(io == kNoIdx ? kNoKey : 0ull, io, edx, edy, a.xs, a.ys);
-        }
+        if (threadIdx.x == 0)
+            a.cta_part[blockIdx.x * 4 + q] =
+                best_from_key(io == kNoIdx ? kNoKey : 0ull, io, s_frame[q].x, s_frame[q].y, a.xs, a.ys);
     }
     if (threadIdx.x == 0) {
         __threadfence();
