@@ -101,7 +101,8 @@ class Engine {
         }
         occ_root_ = std::max(1, occupancy_root(false));
         occ_root_stable_ = std::max(1, occupancy_root(true));
-        occ_level_ = std::max(1, occupancy_level());
+        occ_level_ = std::max(1, occupancy_level(false));
+        occ_level_stable_ = std::max(1, occupancy_level(true));
         occ_fin_ = std::max(1, occupancy_finisher());
         stream_grid_ = sms_ * std::max(1, std::min(8, occupancy_stream()));  // one full wave
         ck(cudaMalloc(&ctrs_, 64 * sizeof(uint32_t)), "cudaMalloc ctrs");
@@ -247,7 +248,7 @@ class Engine {
             LevelTables& Tc = level(lvl);
             tk(5, st, [&] { launch_tilemap(Tc.segs.as<SegRec>(), dinfo, tile_seg_.as<uint32_t>(), li.ntiles, st); });
             {
-                const int grid = std::max(1, std::min<int>(int(li.ntiles), sms_ * occ_level_));
+                const int grid = std::max(1, std::min<int>(int(li.ntiles), sms_ * (stable_ ? occ_level_stable_ : occ_level_)));
                 LevelArgs la;
                 la.gx = dx; la.gy = dy;
                 la.segs = Tc.segs.as<SegRec>(); la.tile_seg = tile_seg_.as<uint32_t>(); la.info = dinfo;
@@ -367,7 +368,7 @@ class Engine {
         part_.ensure(size_t(g.ntiles) * 2 * sizeof(Best), st);
         segaux_.ensure(segaux_bytes(1), st);
         ck(cudaMemsetAsync(segaux_.p, 0, segaux_bytes(1), st), "memset seg aux");
-        const int grid = std::max(1, std::min<int>(int(g.ntiles), sms_ * occ_level_));
+        const int grid = std::max(1, std::min<int>(int(g.ntiles), sms_ * (stable_ ? occ_level_stable_ : occ_level_)));
         LevelArgs la;
         la.gx = bufs_[0].x.as<double>(); la.gy = bufs_[0].y.as<double>();
         la.segs = dseg; la.tile_seg = tile_seg_.as<uint32_t>(); la.info = dli;
@@ -537,7 +538,7 @@ class Engine {
    private:
     int dev_ = 0;
     int sms_ = 148;
-    int occ_root_ = 1, occ_root_stable_ = 1, occ_level_ = 1, occ_fin_ = 1;
+    int occ_root_ = 1, occ_root_stable_ = 1, occ_level_ = 1, occ_level_stable_ = 1, occ_fin_ = 1;
     int stream_grid_ = 592;
     uint32_t* ctrs_ = nullptr;
     RootInfo* root_ = nullptr;

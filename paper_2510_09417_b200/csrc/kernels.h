@@ -39,7 +39,7 @@ void launch_root_frame(const RootInfo* root, const uint32_t* size1, uint32_t* st
                        uint32_t* out, uint32_t* h_out, cudaStream_t st);
 size_t plan_agg_bytes();
 int occupancy_root(bool stable);
-int occupancy_level();
+int occupancy_level(bool stable);
 int occupancy_finisher();
 int occupancy_stream();
 uint32_t read_and_clear_fault();

@@ -19,6 +19,7 @@
 // segment and publishes it once per segment visit; the CTA that completes a
 // segment's tile count reduces those few partials and emits the children.
 #include <cstdint>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "hull_types.cuh"
@@ -817,7 +818,8 @@ __device__ __forceinline__ void tile_scan_fast(FastSmem& S, uint32_t (&tot)[NC])
     for (int q = 0; q < NC; ++q) tot[q] = __shfl_sync(kFull, incl, q * kWarps + kWarps - 1);
 }
 
-__global__ void __launch_bounds__(kThreads, kFastMinBlocks) root_partition_fast(RootArgs a) {
+template <bool PREFETCH>
+__global__ void __launch_bounds__(kThreads, PREFETCH ? 3 : kFastMinBlocks) root_partition_fast(RootArgs a) {
     __shared__ FastSmem S;
     __shared__ double2 s_frame[4];   // class frames (edx, edy)
     __shared__ uint32_t s_org[4][kWarps];  // per (class, warp): store origin of rank 0
@@ -840,21 +842,23 @@ __global__ void __launch_bounds__(kThreads, kFastMinBlocks) root_partition_fast(
     double bo[4] = {kInf, kInf, kInf, kInf};
     uint32_t bi[4] = {kNoIdx, kNoIdx, kNoIdx, kNoIdx};
 
-    double ux[kItems], uy[kItems];
-    auto load = [&](uint32_t t) {
+    double ux[kItems], uy[kItems], nx[kItems], ny[kItems];
+    auto load = [&](uint32_t t, double (&lx)[kItems], double (&ly)[kItems]) {
         const uint32_t start = t * uint32_t(kTile) + threadIdx.x;
 #pragma unroll
         for (int i = 0; i < kItems; ++i) {
             const uint32_t pos = start + uint32_t(i) * kThreads;
             const bool in = pos < n;
-            ux[i] = in ? ld_stream(a.xs + pos) : 0.0;
-            uy[i] = in ? ld_stream(a.ys + pos) : 0.0;
+            lx[i] = in ? ld_stream(a.xs + pos) : 0.0;
+            ly[i] = in ? ld_stream(a.ys + pos) : 0.0;
         }
     };
     uint32_t t = blockIdx.x;
-    if (t < a.ntiles) load(t);
+    if (t < a.ntiles) load(t, ux, uy);
     while (t < a.ntiles) {
         const uint32_t start = t * uint32_t(kTile) + threadIdx.x;
+        const uint32_t tn = t + gridDim.x;
+        if (PREFETCH && tn < a.ntiles) load(tn, nx, ny);  // next tile in flight during this one
         int cls[kItems];
         uint32_t rk[kItems];
         uint32_t wrun = 0;
@@ -917,8 +921,15 @@ __global__ void __launch_bounds__(kThreads, kFastMinBlocks) root_partition_fast(
                 a.oid[p] = start + uint32_t(i) * kThreads;
             }
         }
-        const uint32_t tn = t + gridDim.x;
-        if (tn < a.ntiles) load(tn);
+        if (PREFETCH) {
+#pragma unroll
+            for (int i = 0; i < kItems; ++i) {
+                ux[i] = nx[i];
+                uy[i] = ny[i];
+            }
+        } else if (tn < a.ntiles) {
+            load(tn, ux, uy);
+        }
         t = tn;
     }
     // CTA partials -> last CTA emits the four children
@@ -971,7 +982,8 @@ __global__ void __launch_bounds__(kThreads, kFastMinBlocks) root_partition_fast(
 // ===========================================================================
 cudaError_t launch_root_partition(const RootArgs& a, int grid, bool stable, cudaStream_t st) {
     if (!stable) {
-        root_partition_fast<<<grid, kThreads, 0, st>>>(a);
+        if (getenv("VQB_NO_PREFETCH")) root_partition_fast<false><<<grid, kThreads, 0, st>>>(a);
+        else root_partition_fast<true><<<grid, kThreads, 0, st>>>(a);
         return cudaGetLastError();
     }
     void* args[] = {const_cast<RootArgs*>(&a)};
@@ -993,15 +1005,20 @@ cudaError_t launch_level(const LevelArgs& a, bool general, bool stable, int grid
 int occupancy_root(bool stable) {
     int b = 0;
     if (stable) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, root_partition_kernel<true>, kThreads, 0);
-    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, root_partition_fast, kThreads, 0);
+    else if (getenv("VQB_NO_PREFETCH"))
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, root_partition_fast<false>, kThreads, 0);
+    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, root_partition_fast<true>, kThreads, 0);
     return b;
 }
-int occupancy_level() {
+int occupancy_level(bool stable) {
     int m = 1 << 30, b = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, level_kernel<false, false>, kThreads, 0); m = b < m ? b : m;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, level_kernel<true, false>, kThreads, 0); m = b < m ? b : m;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, level_kernel<false, true>, kThreads, 0); m = b < m ? b : m;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, level_kernel<true, true>, kThreads, 0); m = b < m ? b : m;
+    if (stable) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, level_kernel<false, true>, kThreads, 0); m = b < m ? b : m;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, level_kernel<true, true>, kThreads, 0); m = b < m ? b : m;
+    } else {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, level_kernel<false, false>, kThreads, 0); m = b < m ? b : m;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, level_kernel<true, false>, kThreads, 0); m = b < m ? b : m;
+    }
     return m;
 }
 
