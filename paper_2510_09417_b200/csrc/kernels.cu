@@ -501,11 +501,11 @@ __global__ void tilemap_kernel(const SegRec* segs, const LevelInfo* info, uint32
 // depth so a child's range never overlaps a pending sibling's.
 // ===========================================================================
 constexpr int kFinWarps = 4;
+constexpr uint16_t kNoLid = 0xffffu;
 
 struct FinFrame {
-    uint16_t lo, hi, p, r, q, rcnt, rR, lcnt;
+    uint16_t lo, hi, p, r, q, rcnt, rR;
     uint8_t buf, phase;
-    uint8_t pad[2];
 };
 
 struct FinSmem {
@@ -515,6 +515,33 @@ struct FinSmem {
     uint16_t work[2][kFinMax];
     FinFrame stack[kFinMax + 2];
 };
+
+// canonical order on local ids when the offsets tie exactly: smaller (x, y),
+// then the smaller global (first-occurrence) index
+__device__ __forceinline__ bool fin_tie_better(uint16_t a, uint16_t b, const FinSmem& S) {
+    if (a == kNoLid || a == b) return false;
+    if (b == kNoLid) return true;
+    if (S.x[a] != S.x[b]) return S.x[a] < S.x[b];
+    if (S.y[a] != S.y[b]) return S.y[a] < S.y[b];
+    return S.gid[a] < S.gid[b];
+}
+
+__device__ __forceinline__ void fin_consider(unsigned long long& kb, uint16_t& lb, unsigned long long k,
+                                             uint16_t l, const FinSmem& S) {
+    if (k < kb || (k == kb && fin_tie_better(l, lb, S))) {
+        kb = k;
+        lb = l;
+    }
+}
+
+__device__ __forceinline__ void fin_warp_best(unsigned long long& k, uint16_t& l, const FinSmem& S) {
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) {
+        const unsigned long long ok = __shfl_xor_sync(kFull, k, s);
+        const uint16_t ol = uint16_t(__shfl_xor_sync(kFull, uint32_t(l), s));
+        fin_consider(k, l, ok, ol, S);
+    }
+}
 
 __global__ void __launch_bounds__(kFinWarps * 32) finisher_kernel(
     const FinRec* fins, const LevelInfo* info, const double* __restrict__ ix,
@@ -542,7 +569,7 @@ __global__ void __launch_bounds__(kFinWarps * 32) finisher_kernel(
             S.x[R0] = rec.c.rx; S.y[R0] = rec.c.ry; S.gid[R0] = rec.c.r_idx;
             FinFrame& fr = S.stack[0];
             fr.lo = 0; fr.hi = uint16_t(m); fr.p = P0; fr.r = R0; fr.q = Q0;
-            fr.buf = 0; fr.phase = 0; fr.rcnt = 0; fr.rR = 0; fr.lcnt = 0;
+            fr.buf = 0; fr.phase = 0; fr.rcnt = 0; fr.rR = 0;
         }
         __syncwarp();
         int depth = 1;
@@ -554,8 +581,10 @@ __global__ void __launch_bounds__(kFinWarps * 32) finisher_kernel(
                 if (lane == 0) g_vqb_fault = 2u;
                 break;
             }
-            FinFrame fr = S.stack[depth - 1];
+            const FinFrame fr = S.stack[depth - 1];
             if (fr.phase == 0) {
+                // partition the node's points against (p->r), (r->q) with the
+                // fused farthest search, in the reference's exact predicates
                 const double px = S.x[fr.p], py = S.y[fr.p];
                 const double rx = S.x[fr.r], ry = S.y[fr.r];
                 const double qx = S.x[fr.q], qy = S.y[fr.q];
@@ -563,7 +592,8 @@ __global__ void __launch_bounds__(kFinWarps * 32) finisher_kernel(
                 const double bdx = dsub(qx, rx), bdy = dsub(qy, ry);
                 const int src = fr.buf, dst = fr.buf ^ 1;
                 uint32_t nL = 0, nR = 0;
-                Best bL = best_none(), bR = best_none();
+                unsigned long long kL = kNoKey, kR = kNoKey;
+                uint16_t lL = kNoLid, lR = kNoLid;
                 for (uint32_t b0 = fr.lo; b0 < fr.hi; b0 += 32) {
                     const uint32_t i = b0 + lane;
                     const bool v = i < fr.hi;
@@ -578,59 +608,59 @@ __global__ void __launch_bounds__(kFinWarps * 32) finisher_kernel(
                     const unsigned bb = __ballot_sync(kFull, lb);
                     if (la) {
                         S.work[dst][fr.lo + nL + __popc(ba & lt)] = id;
-                        Best c;
-                        c.off = lat_off(adx, ady, u, w); c.x = u; c.y = w;
-                        c.idx = S.gid[id]; c.valid = uint32_t(id) + 1u;
-                        if (prefer(c, bL)) bL = c;
+                        fin_consider(kL, lL, key_of(lat_off(adx, ady, u, w)), id, S);
                     }
                     if (lb) {
                         S.work[dst][fr.hi - 1 - nR - __popc(bb & lt)] = id;
-                        Best c;
-                        c.off = lat_off(bdx, bdy, u, w); c.x = u; c.y = w;
-                        c.idx = S.gid[id]; c.valid = uint32_t(id) + 1u;
-                        if (prefer(c, bR)) bR = c;
+                        fin_consider(kR, lR, key_of(lat_off(bdx, bdy, u, w)), id, S);
                     }
                     nL += __popc(ba);
                     nR += __popc(bb);
                 }
-                bL = warp_best(bL);
-                bR = warp_best(bR);
+                if (nL) fin_warp_best(kL, lL, S);
+                if (nR) fin_warp_best(kR, lR, S);
                 __syncwarp();
+                // a one-point child is its own chain: emit it in place instead
+                // of visiting it (hull.cpp:83, m <= 1 returns m)
+                if (nL == 1) {
+                    if (lane == 0) chain[cbase + emitted] = S.gid[lL];
+                    ++emitted;
+                }
                 if (lane == 0) {
                     FinFrame& cur = S.stack[depth - 1];
                     cur.phase = 1;
-                    cur.lcnt = uint16_t(nL);
                     cur.rcnt = uint16_t(nR);
-                    cur.rR = nR ? uint16_t(bR.valid - 1u) : 0;
-                    if (nL) {
+                    cur.rR = nR ? lR : 0;
+                    if (nL >= 2) {
                         FinFrame& ch = S.stack[depth];
                         ch.lo = fr.lo; ch.hi = uint16_t(fr.lo + nL);
-                        ch.p = fr.p; ch.r = uint16_t(bL.valid - 1u); ch.q = fr.r;
-                        ch.buf = uint8_t(dst); ch.phase = 0; ch.rcnt = 0; ch.rR = 0; ch.lcnt = 0;
+                        ch.p = fr.p; ch.r = lL; ch.q = fr.r;
+                        ch.buf = uint8_t(dst); ch.phase = 0; ch.rcnt = 0; ch.rR = 0;
                     }
                 }
                 __syncwarp();
-                if (nL) ++depth;
+                if (nL >= 2) ++depth;
             } else if (fr.phase == 1) {
+                // chain(L) is out: emit r, then the right child
                 if (lane == 0) {
                     VQB_CHECK(emitted < m, 31, emitted, m);
                     chain[cbase + emitted] = S.gid[fr.r];
+                    if (fr.rcnt == 1) chain[cbase + emitted + 1] = S.gid[fr.rR];
                     FinFrame& cur = S.stack[depth - 1];
-                    if (fr.rcnt) {
-                        // tail call: the frame is replaced by its right child
+                    if (fr.rcnt >= 2) {
+                        // tail call: the frame becomes its right child
                         cur.lo = uint16_t(fr.hi - fr.rcnt);
                         cur.p = fr.r; cur.r = fr.rR;  // q unchanged
                         cur.buf = uint8_t(fr.buf ^ 1); cur.phase = 0;
-                        cur.rcnt = 0; cur.rR = 0; cur.lcnt = 0;
+                        cur.rcnt = 0; cur.rR = 0;
                     } else {
                         cur.phase = 2;
                     }
                 }
-                ++emitted;
+                emitted += 1 + (fr.rcnt == 1);
                 __syncwarp();
             } else {
-                --depth;
-                // the parent resumes at phase 1 (its left subtree is done)
+                --depth;  // the parent resumes at phase 1 (its left subtree is done)
             }
         }
         if (lane == 0) fin_count_out[f] = emitted;
