@@ -30,6 +30,17 @@ namespace {
 
 thread_local std::string g_last_error;
 
+// VQHULL_TRACE=1: host-side progress trace on stderr (diagnostics)
+const bool g_trace = getenv("VQHULL_TRACE") != nullptr;
+#define VQB_TRACE(...)                          \
+    do {                                        \
+        if (g_trace) {                          \
+            fprintf(stderr, "[vqhull] " __VA_ARGS__); \
+            fputc('\n', stderr);                \
+            fflush(stderr);                     \
+        }                                       \
+    } while (0)
+
 struct CudaError {
     cudaError_t e;
 };
@@ -91,7 +102,9 @@ struct TimedKernel {
 class Engine {
    public:
     explicit Engine(int dev) : dev_(dev) {
+        VQB_TRACE("engine: cudaSetDevice(%d)", dev);
         ck(cudaSetDevice(dev), "cudaSetDevice");
+        VQB_TRACE("engine: context ready");
         ck(cudaDeviceGetAttribute(&sms_, cudaDevAttrMultiProcessorCount, dev), "attr");
         // keep freed pool memory cached: per-call growth then costs nothing
         cudaMemPool_t pool;
@@ -99,12 +112,17 @@ class Engine {
             uint64_t thr = UINT64_MAX;
             cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
         }
+        VQB_TRACE("engine: occupancy queries");
         occ_root_ = std::max(1, occupancy_root(false));
         occ_root_stable_ = std::max(1, occupancy_root(true));
         occ_level_ = std::max(1, occupancy_level(false));
         occ_level_stable_ = std::max(1, occupancy_level(true));
         occ_fin_ = std::max(1, occupancy_finisher());
-        stream_grid_ = sms_ * std::max(1, std::min(8, occupancy_stream()));  // one full wave
+        // one full wave each
+        grid_ext_ = sms_ * std::max(1, std::min(8, occupancy_extremes()));
+        grid_boot_ = sms_ * std::max(1, std::min(8, occupancy_bootstrap()));
+        stream_grid_ = std::max(grid_ext_, grid_boot_);
+        VQB_TRACE("engine: allocations");
         ck(cudaMalloc(&ctrs_, 64 * sizeof(uint32_t)), "cudaMalloc ctrs");
         ck(cudaMemset(ctrs_, 0, 64 * sizeof(uint32_t)), "memset ctrs");
         ck(cudaMalloc(&root_, sizeof(RootInfo)), "cudaMalloc root");
@@ -113,7 +131,9 @@ class Engine {
         ck(cudaMallocHost(&h_root_, sizeof(RootInfo)), "cudaMallocHost");
         ck(cudaMallocHost(&h_word_, 64), "cudaMallocHost");
         partials_.ensure(partial_bytes(stream_grid_), nullptr);
+        VQB_TRACE("engine: synchronize");
         ck(cudaDeviceSynchronize(), "init");
+        VQB_TRACE("engine: ready");
     }
 
     int device() const { return dev_; }
@@ -125,6 +145,7 @@ class Engine {
     // capacity >= n) and returns h through *h.  Returns VQHULL_* code.
     int hull(const double* dx, const double* dy, uint64_t n, uint32_t* d_out, uint64_t* h,
              cudaStream_t st) {
+        VQB_TRACE("hull: n=%llu", (unsigned long long)n);
         reset_stats(n);
         *h = 0;
         if (n == 0) return VQHULL_OK;
@@ -133,9 +154,9 @@ class Engine {
         begin_timing(st);
 
         // ---- K1: extremes
-        tk(0, st, [&] { launch_extremes(dx, dy, n, partials_.p, &ctrs_[3], root_, stream_grid_, st); });
+        tk(0, st, [&] { launch_extremes(dx, dy, n, partials_.p, &ctrs_[3], root_, grid_ext_, st); });
         // ---- KA: bootstrap counts + arg-max + finiteness
-        tk(1, st, [&] { launch_bootstrap(dx, dy, n, partials_.p, &ctrs_[3], root_, stream_grid_, st); });
+        tk(1, st, [&] { launch_bootstrap(dx, dy, n, partials_.p, &ctrs_[3], root_, grid_boot_, st); });
         stats_.bytes_extremes = 8 * n;
         stats_.bytes_bootstrap = 16 * n;
 
@@ -201,7 +222,9 @@ class Engine {
                 });
             }
             ck(cudaMemcpyAsync(h_info_, dinfo, sizeof(LevelInfo), cudaMemcpyDeviceToHost, st), "d2h info");
+            VQB_TRACE("hull: level %d sync", lvl);
             ck(cudaStreamSynchronize(st), "level sync");
+            VQB_TRACE("hull: level %d synced", lvl);
             const LevelInfo li = *h_info_;
             if (lvl == 2 && h_root_->nonfinite) {
                 end_timing(st);
@@ -303,7 +326,9 @@ class Engine {
         }
         ck(cudaMemcpyAsync(h_word_, hword_, 4, cudaMemcpyDeviceToHost, st), "d2h h");
         end_timing(st);
+        VQB_TRACE("hull: final sync");
         ck(cudaStreamSynchronize(st), "final sync");
+        VQB_TRACE("hull: done");
         ck(cudaGetLastError(), "kernel launch");
         if (const uint32_t f = read_and_clear_fault()) {
             g_last_error = "device fault code " + std::to_string(f);
@@ -322,7 +347,7 @@ class Engine {
                       cudaStream_t st) {
         if (n == 0) return VQHULL_EINVAL;
         if (n >= 0xffffffffull) return VQHULL_ESIZE;
-        launch_extremes(dx, dy, n, partials_.p, &ctrs_[3], root_, stream_grid_, st);
+        launch_extremes(dx, dy, n, partials_.p, &ctrs_[3], root_, grid_ext_, st);
         ck(cudaMemcpyAsync(h_root_, root_, sizeof(RootInfo), cudaMemcpyDeviceToHost, st), "d2h root");
         ck(cudaStreamSynchronize(st), "sync");
         ck(cudaGetLastError(), "launch");
@@ -406,6 +431,7 @@ class Engine {
     // host-input path (vqhull_compute)
     int compute_host(const double* xs, const double* ys, uint64_t n, uint32_t* h_out_u32, uint64_t* h,
                      cudaStream_t st) {
+        VQB_TRACE("compute_host: n=%llu", (unsigned long long)n);
         in_.x.ensure(n * 8, st);
         in_.y.ensure(n * 8, st);
         ck(cudaMemcpyAsync(in_.x.p, xs, n * 8, cudaMemcpyHostToDevice, st), "h2d x");
@@ -481,6 +507,7 @@ class Engine {
                                            "finisher", "planner/tilemap/emit"};
             char buf[96];
             snprintf(buf, sizeof buf, "launch %u (%s)", launches_, names[family]);
+            VQB_TRACE("sync after %s", buf);
             ck(cudaStreamSynchronize(st), buf);
             ck(cudaGetLastError(), buf);
         }
@@ -539,7 +566,7 @@ class Engine {
     int dev_ = 0;
     int sms_ = 148;
     int occ_root_ = 1, occ_root_stable_ = 1, occ_level_ = 1, occ_level_stable_ = 1, occ_fin_ = 1;
-    int stream_grid_ = 592;
+    int stream_grid_ = 592, grid_ext_ = 592, grid_boot_ = 592;
     uint32_t* ctrs_ = nullptr;
     RootInfo* root_ = nullptr;
     uint32_t* hword_ = nullptr;
@@ -608,6 +635,7 @@ thread_local bool g_timing = false;
 
 Engine& engine() {
     int dev = 0;
+    VQB_TRACE("engine(): cudaGetDevice");
     ck(cudaGetDevice(&dev), "cudaGetDevice");
     std::lock_guard<std::mutex> lk(g_reg_mu);
     if (g_engines.size() <= size_t(dev)) g_engines.resize(dev + 1);

@@ -26,9 +26,10 @@ namespace vqb {
 
 // ===========================================================================
 // K1: extremes.  lo = lexicographic min of (x, y, index); hi = max x, then
-// max y, then min index.  y is read only on x ties, exactly like the
-// reference scan; the (x, y, index) total order makes the grid reduction
-// independent of the visiting order.
+// max y, then min index.  y is read only on x ties, like the reference scan;
+// the (x, y, index) total order makes the grid reduction independent of the
+// visiting order.  Branch-free per point (compare + select); an exact x tie
+// with the running extreme takes a warp-uniform slow path that reads y.
 // ===========================================================================
 struct ExtKey {
     double x, y;
@@ -63,47 +64,45 @@ struct ExtPartial {
     ExtKey lo, hi;
 };
 
+constexpr int kStreamUnroll = 4;  // double2 loads per array per thread per iteration
+
 __global__ void __launch_bounds__(256) extremes_kernel(const double* __restrict__ xs,
                                                        const double* __restrict__ ys,
                                                        uint64_t n, ExtPartial* partials,
                                                        uint32_t* ticket, RootInfo* root) {
-    // per-thread running extremes; y of the incumbent is fetched lazily
-    double lo_x = 0, hi_x = 0, lo_y = 0, hi_y = 0;
+    const double kInf = __longlong_as_double(0x7ff0000000000000ll);
+    // running extremes (x, index); the first index wins among exact x ties
+    // unless y decides (checked on the slow path)
+    double lo_x = kInf, hi_x = -kInf;
     uint32_t lo_i = 0xffffffffu, hi_i = 0xffffffffu;
-    bool lo_yk = false, hi_yk = false;
-    const uint64_t tid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
-    auto visit = [&](uint64_t i, double x) {
-        if (lo_i == 0xffffffffu || x < lo_x) {
-            lo_x = x;
-            lo_i = uint32_t(i);
-            lo_yk = false;
-        } else if (x == lo_x) {
-            if (!lo_yk) { lo_y = ys[lo_i]; lo_yk = true; }
-            const double y = ys[i];
-            if (y < lo_y) { lo_y = y; lo_i = uint32_t(i); }
+    auto visit = [&](uint32_t i, double x) {
+        const bool lt = x < lo_x, gt = x > hi_x;
+        const bool tie = (x == lo_x) | (x == hi_x);
+        // grid-stride trip counts differ per lane: vote over the lanes that
+        // are actually here (a full-mask vote would be undefined behaviour)
+        if (__any_sync(__activemask(), tie)) {
+            // exact x tie: smaller (larger) y wins; equal y keeps the earlier index
+            if (x == lo_x && lo_i != 0xffffffffu && ys[i] < ys[lo_i]) lo_i = i;
+            if (x == hi_x && hi_i != 0xffffffffu && ys[i] > ys[hi_i]) hi_i = i;
         }
-        if (hi_i == 0xffffffffu || x > hi_x) {
-            hi_x = x;
-            hi_i = uint32_t(i);
-            hi_yk = false;
-        } else if (x == hi_x) {
-            if (!hi_yk) { hi_y = ys[hi_i]; hi_yk = true; }
-            const double y = ys[i];
-            if (y > hi_y) { hi_y = y; hi_i = uint32_t(i); }
-        }
+        lo_i = lt ? i : lo_i;
+        lo_x = lt ? x : lo_x;
+        hi_i = gt ? i : hi_i;
+        hi_x = gt ? x : hi_x;
     };
+    const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t stride = gridDim.x * blockDim.x;
     const bool vec = (reinterpret_cast<uintptr_t>(xs) & 15u) == 0;
     if (vec) {
-        const uint64_t npair = n / 2;
+        const uint32_t npair = uint32_t(n / 2);
         const double2* x2 = reinterpret_cast<const double2*>(xs);
-        uint64_t j = tid;
-        for (; j + 3 * stride < npair; j += 4 * stride) {
-            double2 v[4];
+        uint32_t j = tid;
+        for (; j + (kStreamUnroll - 1) * stride < npair; j += kStreamUnroll * stride) {
+            double2 v[kStreamUnroll];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) v[u] = __ldcs(&x2[j + u * stride]);
+            for (int u = 0; u < kStreamUnroll; ++u) v[u] = __ldcs(&x2[j + u * stride]);
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < kStreamUnroll; ++u) {
                 visit(2 * (j + u * stride), v[u].x);
                 visit(2 * (j + u * stride) + 1, v[u].y);
             }
@@ -113,14 +112,15 @@ __global__ void __launch_bounds__(256) extremes_kernel(const double* __restrict_
             visit(2 * j, v.x);
             visit(2 * j + 1, v.y);
         }
-        if ((n & 1) && tid == 0) visit(n - 1, xs[n - 1]);
+        if ((n & 1) && tid == 0) visit(uint32_t(n - 1), xs[n - 1]);
     } else {
-        for (uint64_t i = tid; i < n; i += stride) visit(i, xs[i]);
+        for (uint32_t i = tid; i < n; i += stride) visit(i, xs[i]);
     }
+    // NaN inputs never win a comparison; they are rejected by KA anyway
     ExtKey lo{lo_x, 0.0, lo_i, lo_i != 0xffffffffu};
     ExtKey hi{hi_x, 0.0, hi_i, hi_i != 0xffffffffu};
-    if (lo.valid) lo.y = lo_yk ? lo_y : ys[lo_i];
-    if (hi.valid) hi.y = hi_yk ? hi_y : ys[hi_i];
+    if (lo.valid) lo.y = ys[lo_i];
+    if (hi.valid) hi.y = ys[hi_i];
 #pragma unroll
     for (int s = 16; s > 0; s >>= 1) {
         ExtKey a = shfl_key(lo, s);
@@ -146,7 +146,6 @@ __global__ void __launch_bounds__(256) extremes_kernel(const double* __restrict_
     }
     __syncthreads();
     if (!s_last) return;
-    // last block: reduce the partials
     __threadfence();
     ExtKey L, H;
     L.valid = H.valid = 0;
@@ -189,54 +188,77 @@ __global__ void __launch_bounds__(256) extremes_kernel(const double* __restrict_
 // point falls on, |S1|, |S2|, and r1/r2 in the canonical order.  No writes:
 // the split itself is recomputed (fused with the next level) by KB.
 // Also folds in vqhull_compute's finiteness check (vqhull_c.cpp:32-34).
+//  * left of p->q is A*D > B*C and left of q->p is C*B > D*A with the same
+//    two products (IEEE products commute), and the second implies "not the
+//    first", so mask_b &= ~mask_a (kernels.hpp:91) holds automatically;
+//  * the q->p frame is the exact negation of the p->q frame, so one offset o
+//    serves both sides: S1 prefers the smallest o, S2 the smallest -o (the
+//    largest o); equal offsets (incl. +-0) go to the slow path's
+//    lexicographic / first-index tie-break.
 // ===========================================================================
 struct RootPartial {
     uint32_t cnt1, cnt2, nonfinite, pad;
     Best b1, b2;
 };
 
+__device__ __forceinline__ bool nonfinite_bits(double v) {
+    return (__double2hiint(v) & 0x7ff00000) == 0x7ff00000;
+}
+
 __global__ void __launch_bounds__(256) bootstrap_argmax_kernel(
     const double* __restrict__ xs, const double* __restrict__ ys, uint64_t n,
     RootPartial* partials, uint32_t* ticket, RootInfo* root) {
     const double px = root->px, py = root->py, qx = root->qx, qy = root->qy;
-    // frames of edge a = p->q and edge b = q->p (kernels.hpp:23-25)
-    const double adx = dsub(qx, px), ady = dsub(qy, py);
-    const double bdx = dsub(px, qx), bdy = dsub(py, qy);
-    uint32_t c1 = 0, c2 = 0, bad = 0;
-    Best b1 = best_none(), b2 = best_none();
-    auto visit = [&](uint64_t i, double ux, double uy) {
-        bad |= !(isfinite(ux) && isfinite(uy));
+    const double adx = dsub(qx, px), ady = dsub(qy, py);  // frame of p->q (kernels.hpp:23-25)
+    const double kInf = __longlong_as_double(0x7ff0000000000000ll);
+    uint32_t c1 = 0, c2 = 0;
+    bool bad = false;
+    double o1 = kInf, o2 = -kInf;  // S1: min o, S2: max o
+    uint32_t i1 = 0xffffffffu, i2 = 0xffffffffu;
+    auto visit = [&](uint32_t i, double ux, double uy) {
+        bad |= nonfinite_bits(ux) | nonfinite_bits(uy);
         const double A = dsub(px, ux), B = dsub(py, uy);
         const double Cc = dsub(qx, ux), D = dsub(qy, uy);
-        // left of p->q: A*D > B*C ; left of q->p: C*B > D*A (same products)
         const double t1 = dmul(A, D), t2 = dmul(B, Cc);
-        const bool la = t1 > t2;
-        const bool lb = !la && (t2 > t1);
+        const bool la = t1 > t2;  // left of p->q
+        const bool lb = t2 > t1;  // left of q->p (and therefore not of p->q)
         c1 += la;
         c2 += lb;
-        if (la | lb) {
-            const double off = la ? lat_off(adx, ady, ux, uy) : lat_off(bdx, bdy, ux, uy);
-            if (la) consider(b1, true, off, ux, uy, uint32_t(i));
-            else consider(b2, true, off, ux, uy, uint32_t(i));
+        const double o = lat_off(adx, ady, ux, uy);
+        const bool maybe = (la && !(o > o1)) || (lb && !(o < o2));
+        if (__any_sync(__activemask(), maybe)) {  // lanes may be in different iterations
+            if (maybe) {
+                const bool s = la;
+                const double ob = s ? o1 : o2;
+                const uint32_t ib = s ? i1 : i2;
+                bool take = s ? (o < ob) : (o > ob);
+                take |= ib == 0xffffffffu;
+                if (!take && o == ob && i != ib) {  // exact tie: smaller (x, y), then index
+                    const double xb = xs[ib], yb = ys[ib];
+                    take = (ux != xb) ? (ux < xb) : ((uy != yb) ? (uy < yb) : (i < ib));
+                }
+                if (take && s) { o1 = o; i1 = i; }
+                if (take && !s) { o2 = o; i2 = i; }
+            }
         }
     };
-    const uint64_t tid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t stride = gridDim.x * blockDim.x;
     const bool vec = ((reinterpret_cast<uintptr_t>(xs) | reinterpret_cast<uintptr_t>(ys)) & 15u) == 0;
     if (vec) {
-        const uint64_t npair = n / 2;
+        const uint32_t npair = uint32_t(n / 2);
         const double2* x2 = reinterpret_cast<const double2*>(xs);
         const double2* y2 = reinterpret_cast<const double2*>(ys);
-        uint64_t j = tid;
-        for (; j + 3 * stride < npair; j += 4 * stride) {
-            double2 vx[4], vy[4];
+        uint32_t j = tid;
+        for (; j + (kStreamUnroll - 1) * stride < npair; j += kStreamUnroll * stride) {
+            double2 vx[kStreamUnroll], vy[kStreamUnroll];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < kStreamUnroll; ++u) {
                 vx[u] = __ldcs(&x2[j + u * stride]);
                 vy[u] = __ldcs(&y2[j + u * stride]);
             }
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < kStreamUnroll; ++u) {
                 visit(2 * (j + u * stride), vx[u].x, vy[u].x);
                 visit(2 * (j + u * stride) + 1, vx[u].y, vy[u].y);
             }
@@ -247,16 +269,20 @@ __global__ void __launch_bounds__(256) bootstrap_argmax_kernel(
             visit(2 * j, vx.x, vy.x);
             visit(2 * j + 1, vx.y, vy.y);
         }
-        if ((n & 1) && tid == 0) visit(n - 1, xs[n - 1], ys[n - 1]);
+        if ((n & 1) && tid == 0) visit(uint32_t(n - 1), xs[n - 1], ys[n - 1]);
     } else {
-        for (uint64_t i = tid; i < n; i += stride) visit(i, xs[i], ys[i]);
+        for (uint32_t i = tid; i < n; i += stride) visit(i, xs[i], ys[i]);
     }
-    // block reduction
+    // thread candidates -> Best (S2's offset in its own frame is -o)
+    Best b1 = best_none(), b2 = best_none();
+    if (i1 != 0xffffffffu) { b1.off = o1; b1.x = xs[i1]; b1.y = ys[i1]; b1.idx = i1; b1.valid = 1; }
+    if (i2 != 0xffffffffu) { b2.off = -o2; b2.x = xs[i2]; b2.y = ys[i2]; b2.idx = i2; b2.valid = 1; }
+    uint32_t ubad = bad ? 1u : 0u;
 #pragma unroll
     for (int s = 16; s > 0; s >>= 1) {
         c1 += __shfl_xor_sync(kFull, c1, s);
         c2 += __shfl_xor_sync(kFull, c2, s);
-        bad |= __shfl_xor_sync(kFull, bad, s);
+        ubad |= __shfl_xor_sync(kFull, ubad, s);
     }
     b1 = warp_best(b1);
     b2 = warp_best(b2);
@@ -266,7 +292,7 @@ __global__ void __launch_bounds__(256) bootstrap_argmax_kernel(
     if (lane == 0) {
         s_p[warp].cnt1 = c1;
         s_p[warp].cnt2 = c2;
-        s_p[warp].nonfinite = bad;
+        s_p[warp].nonfinite = ubad;
         s_p[warp].b1 = b1;
         s_p[warp].b2 = b2;
     }
@@ -837,11 +863,15 @@ void launch_root_frame(const RootInfo* root, const uint32_t* size1, uint32_t* st
 
 size_t plan_agg_bytes() { return sizeof(PlanAgg); }
 
-int occupancy_stream() {
-    int a = 0, b = 0;
+int occupancy_extremes() {
+    int a = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, extremes_kernel, 256, 0);
+    return a;
+}
+int occupancy_bootstrap() {
+    int b = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, bootstrap_argmax_kernel, 256, 0);
-    return a < b ? a : b;
+    return b;
 }
 int occupancy_finisher() {
     int b = 0;

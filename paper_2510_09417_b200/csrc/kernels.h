@@ -41,7 +41,8 @@ size_t plan_agg_bytes();
 int occupancy_root(bool stable);
 int occupancy_level(bool stable);
 int occupancy_finisher();
-int occupancy_stream();
+int occupancy_extremes();
+int occupancy_bootstrap();
 uint32_t read_and_clear_fault();
 
 }  // namespace vqb

@@ -20,6 +20,8 @@ static int failures = 0;
         }                                                                  \
     } while (0)
 
+#define STEP(name) std::fprintf(stderr, "[cpp] %s\n", name)
+
 static PointSet pts(std::initializer_list<Point> l) {
     PointSet p;
     for (const Point& q : l) p.push_back(q);
@@ -28,6 +30,7 @@ static PointSet pts(std::initializer_list<Point> l) {
 
 int main() {
     // test_hull.cpp:71-115 degenerate hulls
+    STEP("degenerate hulls");
     CHECK(convex_hull(PointSet{}).empty());
     {
         const HullPolygon h = convex_hull(pts({{0, 0}}));
@@ -56,6 +59,7 @@ int main() {
         CHECK(h.size() == 2 && h.vertices[0] == (Point{2, -3}) && h.vertices[1] == (Point{2, 3}));
     }
     // test_hull.cpp:117-130 unit square with center
+    STEP("unit square with center");
     {
         const HullPolygon h = convex_hull(pts({{1, 1}, {0, 0}, {0.5, 0.5}, {0, 1}, {1, 0}}));
         CHECK(h.size() == 4);
@@ -63,6 +67,7 @@ int main() {
         CHECK(h.vertices[2] == (Point{1, 1}) && h.vertices[3] == (Point{1, 0}));
     }
     // test_hull.cpp:220-240 deep recursion on a convex power-of-two curve
+    STEP("deep recursion on a convex power-of-two curve");
     {
         const int m = 600;
         PointSet p;
@@ -77,6 +82,7 @@ int main() {
         }
     }
     // test_hull.cpp:320-345 C interface semantics (index 5 duplicates 0)
+    STEP("C interface semantics (index 5 duplicates 0)");
     {
         const double xs[] = {0, 4, 4, 0, 2, 0};
         const double ys[] = {0, 0, 4, 4, 2, 0};
@@ -93,6 +99,7 @@ int main() {
         CHECK(vqhull_compute(bad_x, bad_y, 2, 1, idx, &c) == 1);
     }
     // test_geometry.cpp:32-51 find_extremes tie-breaks
+    STEP("find_extremes tie-breaks");
     {
         CHECK(find_extremes(pts({{0, 0}})) == (std::pair<std::size_t, std::size_t>{0, 0}));
         CHECK(find_extremes(pts({{1, 5}, {-2, 0}, {3, 1}})) == (std::pair<std::size_t, std::size_t>{1, 2}));
@@ -106,6 +113,7 @@ int main() {
         CHECK(threw);
     }
     // test_extract.cpp:183-210 eight points around an edge
+    STEP("eight points around an edge");
     for (bool stable : {false, true}) {
         PointSet p = pts({{1, 1}, {2, -1}, {3, 2}, {1, 0}, {0.5, -3}, {2, 4}, {3, 0}, {2.5, -0.5}});
         Config cfg;

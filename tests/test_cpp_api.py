@@ -28,3 +28,29 @@ def test_cpp_api_runs(tmp_path, cuda):
     out = subprocess.run([build(tmp_path)], capture_output=True, text=True, timeout=300)
     assert out.returncode == 0, out.stderr
     assert "all checks passed" in out.stdout
+
+
+@pytest.mark.gpu
+def test_plain_c_caller_without_torch(tmp_path, cuda):
+    """The drop-in: a C program (no torch, no cudart of its own) calls
+    vqhull_compute on tiny and odd sizes; runs in a fresh process."""
+    src = os.path.join(str(tmp_path), "c_caller.c")
+    with open(src, "w") as f:
+        f.write(r'''
+#include <stdio.h>
+#include "vqhull_b200.h"
+int main(void) {
+    double xs[] = {0, 4, 4, 0, 2, 0}, ys[] = {0, 0, 4, 4, 2, 0};
+    size_t idx[6], cnt = 0;
+    if (vqhull_compute(xs, ys, 6, 1, idx, &cnt) || cnt != 4 || idx[0] != 0 || idx[1] != 3) return 2;
+    for (size_t n = 1; n <= 6; ++n)
+        if (vqhull_compute(xs, ys, n, 1, idx, &cnt)) return 3;
+    puts("c caller ok");
+    return 0;
+}
+''')
+    exe = os.path.join(str(tmp_path), "c_caller")
+    subprocess.run(["gcc", "-O1", "-I", os.path.join(ROOT, "include"), src, "-L", LIBDIR, "-lvqhull_b200",
+                    f"-Wl,-rpath,{LIBDIR}", "-o", exe], check=True)
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0 and "c caller ok" in out.stdout, (out.returncode, out.stderr)
