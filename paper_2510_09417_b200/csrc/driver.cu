@@ -157,6 +157,7 @@ class Engine {
         tk(0, st, [&] { launch_extremes(dx, dy, n, partials_.p, &ctrs_[3], root_, grid_ext_, st); });
         // ---- KA: bootstrap counts + arg-max + finiteness
         tk(1, st, [&] { launch_bootstrap(dx, dy, n, partials_.p, &ctrs_[3], root_, grid_boot_, st); });
+        upload_root_consts(root_, st);  // p, q, r1, r2 -> constant bank for KB
         stats_.bytes_extremes = 8 * n;
         stats_.bytes_bootstrap = 16 * n;
 

@@ -14,6 +14,7 @@ void launch_extremes(const double* xs, const double* ys, uint64_t n, void* parti
 void launch_bootstrap(const double* xs, const double* ys, uint64_t n, void* partials,
                       uint32_t* ticket, RootInfo* root, int grid, cudaStream_t st);
 size_t partial_bytes(int grid);
+void upload_root_consts(const RootInfo* d_root, cudaStream_t st);
 cudaError_t launch_root_partition(const RootArgs& a, int grid, bool stable, cudaStream_t st);
 cudaError_t launch_level(const LevelArgs& a, bool general, bool stable, int grid, cudaStream_t st);
 void launch_planner(const ChildRec* slots, uint32_t nslots, SegRec* segs, FinRec* fins,

@@ -782,18 +782,21 @@ __device__ __forceinline__ void block_best_d(FastSmem& S, int c, double off, uin
 // class so far (earlier items included); wrun (lanes < NC) accumulates counts
 template <int NC>
 __device__ __forceinline__ uint32_t warp_rank(int c, uint32_t& wrun) {
+    // class bits as ballots; a lane's same-class mask is V & ~(B0 ^ m0) &
+    // ~(B1 ^ m1) with m = all-ones where the lane's own bit is set
     const int lane = threadIdx.x & 31;
     const bool v = c < NC;
+    const unsigned b0 = unsigned(c) & 1u, b1 = (unsigned(c) >> 1) & 1u;
     const unsigned V = __ballot_sync(kFull, v);
-    const unsigned B0 = __ballot_sync(kFull, v && (c & 1));
-    unsigned M, Mq;
+    const unsigned B0 = __ballot_sync(kFull, v && b0);
+    const unsigned m0 = 0u - b0, l0 = 0u - (unsigned(lane) & 1u);
+    unsigned M = V & ~(B0 ^ m0);
+    unsigned Mq = V & ~(B0 ^ l0);
     if (NC == 4) {
-        const unsigned B1 = __ballot_sync(kFull, v && (c & 2));
-        M = V & ((c & 1) ? B0 : ~B0) & ((c & 2) ? B1 : ~B1);
-        Mq = V & ((lane & 1) ? B0 : ~B0) & ((lane & 2) ? B1 : ~B1);
-    } else {
-        M = V & ((c & 1) ? B0 : ~B0);
-        Mq = V & ((lane & 1) ? B0 : ~B0);
+        const unsigned B1 = __ballot_sync(kFull, v && b1);
+        const unsigned m1 = 0u - b1, l1 = 0u - ((unsigned(lane) >> 1) & 1u);
+        M &= ~(B1 ^ m1);
+        Mq &= ~(B1 ^ l1);
     }
     const uint32_t before = __shfl_sync(kFull, wrun, c & (NC - 1));
     wrun += (lane < NC) ? __popc(Mq) : 0u;
@@ -818,13 +821,23 @@ __device__ __forceinline__ void tile_scan_fast(FastSmem& S, uint32_t (&tot)[NC])
     for (int q = 0; q < NC; ++q) tot[q] = __shfl_sync(kFull, incl, q * kWarps + kWarps - 1);
 }
 
+// p, q, r1, r2 and the side counts of the current hull, copied device-to-
+// device into the constant bank right after KA (stream-ordered, no host
+// sync): the FP64 instructions read them as constant operands, which keeps
+// 16 registers free for occupancy.
+__constant__ RootInfo c_root;
+
+void upload_root_consts(const RootInfo* d_root, cudaStream_t st) {
+    cudaMemcpyToSymbolAsync(c_root, d_root, sizeof(RootInfo), 0, cudaMemcpyDeviceToDevice, st);
+}
+
 template <bool PREFETCH>
 __global__ void __launch_bounds__(kThreads, PREFETCH ? 3 : kFastMinBlocks) root_partition_fast(RootArgs a) {
     __shared__ FastSmem S;
     __shared__ double2 s_frame[4];   // class frames (edx, edy)
     __shared__ uint32_t s_org[4][kWarps];  // per (class, warp): store origin of rank 0
     __shared__ bool s_last;
-    const RootInfo& R = *a.root;
+    const RootInfo& R = c_root;
     const double px = R.px, py = R.py, qx = R.qx, qy = R.qy;
     const double r1x = R.r1.x, r1y = R.r1.y, r2x = R.r2.x, r2y = R.r2.y;
     const uint32_t n1 = R.cnt1, n2 = R.cnt2;
@@ -882,7 +895,7 @@ __global__ void __launch_bounds__(kThreads, PREFETCH ? 3 : kFastMinBlocks) root_
             c = (pos < n) ? c : 4;
             cls[i] = c;
             rk[i] = warp_rank<4>(c, wrun);
-            const double2 fr = s_frame[c & 3];
+            const double2 fr = s_frame[c & 3];  // fused farthest-point search
             running_best_d<4>(bo, bi, c, lat_off(fr.x, fr.y, u, w), pos, a.xs, a.ys);
         }
         if (lane < 4) S.wtot[lane][warp] = wrun;
@@ -890,7 +903,6 @@ __global__ void __launch_bounds__(kThreads, PREFETCH ? 3 : kFastMinBlocks) root_
         if (warp == 0) {
             uint32_t tot[4];
             tile_scan_fast<4>(S, tot);
-            uint32_t cl = 0;
             if (lane < 2) {
                 const uint2 c2 = claim_pair(&a.side_ctr[lane], tot[2 * lane], tot[2 * lane + 1]);
                 S.claim[2 * lane] = c2.x;
@@ -905,7 +917,6 @@ __global__ void __launch_bounds__(kThreads, PREFETCH ? 3 : kFastMinBlocks) root_
                 const uint32_t org = c == 0 ? 0u : (c == 1 ? n1 - 1u : (c == 2 ? n1 : n1 + n2 - 1u));
                 s_org[c][w] = (c & 1) ? org - off : org + off;
             }
-            (void)cl;
         }
         __syncthreads();
         // stores straight from registers
