@@ -757,7 +757,7 @@ __device__ __forceinline__ void block_best_d(FastSmem& S, int c, double off, uin
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     unsigned long long k = (i == kNoIdx) ? kNoKey : key_of(off);
     warp_key_best(k, i, xs, ys);
-    if (lane == 0) {
+    if (lane == 0 && warp < kWarps) {  // a control warp (no points) does not contribute
         S.rkey[c][warp] = k;
         S.ridx[c][warp] = i;
     }
@@ -989,12 +989,218 @@ __global__ void __launch_bounds__(kThreads, PREFETCH ? 3 : kFastMinBlocks) root_
 }
 
 // ===========================================================================
+// KB with a TMA ring (default fast path when the inputs are 16-byte aligned).
+// One thread streams the CTA's upcoming full tiles (x and y, 8 KB each) into
+// a kRing-deep shared-memory ring with cp.async.bulk, completing on
+// mbarriers; the warps read their items from shared memory.  No per-element
+// load instructions and no prefetch registers; the static tile schedule
+// knows every future tile, so the ring runs kRing tiles ahead.
+// ===========================================================================
+constexpr int kRing = 3;
+
+struct RootRing {
+    double x[kRing][kTile];
+    double y[kRing][kTile];
+    unsigned long long bar[kRing];
+};
+
+// 8 compute warps + 1 control warp (scan, claim, TMA refills): the claim's
+// atomic round trip overlaps the compute warps' arg-max updates.
+constexpr int kCtlThreads = kThreads + 32;
+
+__global__ void __launch_bounds__(kCtlThreads, 3) root_partition_tma(RootArgs a) {
+    extern __shared__ __align__(128) unsigned char dsm[];
+    RootRing& ring = *reinterpret_cast<RootRing*>(dsm);
+    __shared__ FastSmem S;
+    __shared__ double2 s_frame[4];
+    __shared__ uint32_t s_org[4][kWarps];
+    __shared__ bool s_last;
+    const RootInfo& R = c_root;
+    const double px = R.px, py = R.py, qx = R.qx, qy = R.qy;
+    const double r1x = R.r1.x, r1y = R.r1.y, r2x = R.r2.x, r2y = R.r2.y;
+    const uint32_t n1 = R.cnt1, n2 = R.cnt2;
+    const uint32_t n = uint32_t(a.n);
+    const uint32_t G = gridDim.x;
+    const uint32_t nfull = n / kTile;  // tiles streamed by TMA; a partial last tile is loaded directly
+    auto issue = [&](uint32_t k) {     // thread 0: local tile k -> stage k % kRing
+        const uint32_t t = blockIdx.x + k * G;
+        if (t >= nfull) return;
+        const int s = int(k % kRing);
+        mbar_expect_tx(&ring.bar[s], 2u * kTile * 8u);
+        tma_load_1d(ring.x[s], a.xs + uint64_t(t) * kTile, kTile * 8u, &ring.bar[s]);
+        tma_load_1d(ring.y[s], a.ys + uint64_t(t) * kTile, kTile * 8u, &ring.bar[s]);
+    };
+    const bool ctl = threadIdx.x >= kThreads;  // the control warp
+    if (threadIdx.x == kThreads) {
+        s_frame[0] = make_double2(dsub(r1x, px), dsub(r1y, py));
+        s_frame[1] = make_double2(dsub(qx, r1x), dsub(qy, r1y));
+        s_frame[2] = make_double2(dsub(r2x, qx), dsub(r2y, qy));
+        s_frame[3] = make_double2(dsub(px, r2x), dsub(py, r2y));
+        for (int s = 0; s < kRing; ++s) mbar_init(&ring.bar[s], 1);
+        mbar_fence_init();
+        for (uint32_t k = 0; k < kRing; ++k) issue(k);
+    }
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const double kInf = __longlong_as_double(0x7ff0000000000000ll);
+    double bo[4] = {kInf, kInf, kInf, kInf};
+    uint32_t bi[4] = {kNoIdx, kNoIdx, kNoIdx, kNoIdx};
+
+    uint32_t k = 0;
+    for (uint32_t t = blockIdx.x; t < a.ntiles; t += G, ++k) {
+        const uint32_t start = t * uint32_t(kTile) + (threadIdx.x & (kThreads - 1));
+        const int s = int(k % kRing);
+        double ux[kItems], uy[kItems];
+        int cls[kItems];
+        uint32_t rk[kItems];
+        if (!ctl) {
+            if (t < nfull) {
+                mbar_wait(&ring.bar[s], (k / kRing) & 1u);
+#pragma unroll
+                for (int i = 0; i < kItems; ++i) {
+                    ux[i] = ring.x[s][i * kThreads + threadIdx.x];
+                    uy[i] = ring.y[s][i * kThreads + threadIdx.x];
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < kItems; ++i) {
+                    const uint32_t pos = start + uint32_t(i) * kThreads;
+                    ux[i] = pos < n ? a.xs[pos] : 0.0;
+                    uy[i] = pos < n ? a.ys[pos] : 0.0;
+                }
+            }
+            uint32_t wrun = 0;
+#pragma unroll
+            for (int i = 0; i < kItems; ++i) {
+                const uint32_t pos = start + uint32_t(i) * kThreads;
+                const double u = ux[i], w = uy[i];
+                const double A = dsub(px, u), B = dsub(py, w);
+                const double Cc = dsub(qx, u), D = dsub(qy, w);
+                const double t1 = dmul(A, D), t2 = dmul(B, Cc);
+                const bool s1 = t1 > t2;           // left of p->q
+                const bool s2 = !s1 && (t2 > t1);  // left of q->p
+                const double rx = s1 ? r1x : r2x, ry = s1 ? r1y : r2y;
+                const double P1x = s1 ? A : Cc, P1y = s1 ? B : D;
+                const double Q2x = s1 ? Cc : A, Q2y = s1 ? D : B;
+                const double E = dsub(rx, u), F = dsub(ry, w);
+                const bool L = left_diff(P1x, P1y, E, F);
+                const bool Rr = !L && left_diff(E, F, Q2x, Q2y);
+                const int side = s1 ? 0 : 2;
+                int c = (s1 || s2) ? (L ? side : (Rr ? side + 1 : 4)) : 4;
+                c = (pos < n) ? c : 4;
+                cls[i] = c;
+                rk[i] = warp_rank<4>(c, wrun);
+            }
+            if (lane < 4) S.wtot[lane][warp] = wrun;
+        }
+        __syncthreads();  // counts ready; every compute warp is done with stage s
+        if (ctl) {
+            uint32_t tot[4];
+            tile_scan_fast<4>(S, tot);
+            if (lane < 2) {
+                const uint2 c2 = claim_pair(&a.side_ctr[lane], tot[2 * lane], tot[2 * lane + 1]);
+                S.claim[2 * lane] = c2.x;
+                S.claim[2 * lane + 1] = c2.y;
+            }
+            __syncwarp();
+            if (lane < 4 * kWarps) {
+                const int c = lane / kWarps, w = lane % kWarps;
+                const uint32_t off = S.claim[c] + S.wbase[c][w];
+                const uint32_t org = c == 0 ? 0u : (c == 1 ? n1 - 1u : (c == 2 ? n1 : n1 + n2 - 1u));
+                s_org[c][w] = (c & 1) ? org - off : org + off;
+            }
+            if (lane == 0) {
+                fence_proxy_async_smem();
+                issue(k + kRing);  // refill stage s with the tile kRing ahead
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < kItems; ++i) {  // fused farthest-point search, overlapping the claim
+                const int c = cls[i];
+                const double2 fr = s_frame[c & 3];
+                running_best_d<4>(bo, bi, c, lat_off(fr.x, fr.y, ux[i], uy[i]),
+                                  start + uint32_t(i) * kThreads, a.xs, a.ys);
+            }
+        }
+        __syncthreads();
+        if (!ctl) {
+#pragma unroll
+            for (int i = 0; i < kItems; ++i) {
+                const int c = cls[i];
+                if (c < 4) {
+                    const uint32_t o = s_org[c][warp];
+                    const uint32_t p = (c & 1) ? o - rk[i] : o + rk[i];
+                    VQB_CHECK(p < a.out_cap, 12, p, a.out_cap);
+                    a.ox[p] = ux[i];
+                    a.oy[p] = uy[i];
+                    a.oid[p] = start + uint32_t(i) * kThreads;
+                }
+            }
+        }
+    }
+    // CTA partials -> last CTA emits the four children (the control warp's
+    // candidates are empty)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        double oo;
+        uint32_t io;
+        block_best_d<4>(S, q, bo[q], bi[q], a.xs, a.ys, oo, io);
+        if (threadIdx.x == 0)
+            a.cta_part[blockIdx.x * 4 + q] =
+                best_from_key(io == kNoIdx ? kNoKey : 0ull, io, s_frame[q].x, s_frame[q].y, a.xs, a.ys);
+    }
+    if (threadIdx.x == 0) {
+        __threadfence();
+        s_last = atomicAdd(a.ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    if (warp < 4) {
+        const int c = warp;
+        Best b = best_none();
+        for (uint32_t kk = lane; kk < gridDim.x; kk += 32) {
+            const Best o = ldcg_best(&a.cta_part[kk * 4 + c]);
+            if (prefer(o, b)) b = o;
+        }
+        b = warp_best(b);
+        if (lane == 0) {
+            const uint2 w = read_pair(&a.side_ctr[c >> 1]);
+            const uint32_t m = (c & 1) ? w.y : w.x;
+            ChildRec ch;
+            ch.px = c == 0 ? px : (c == 1 ? r1x : (c == 2 ? qx : r2x));
+            ch.py = c == 0 ? py : (c == 1 ? r1y : (c == 2 ? qy : r2y));
+            ch.qx = c == 0 ? r1x : (c == 1 ? qx : (c == 2 ? r2x : px));
+            ch.qy = c == 0 ? r1y : (c == 1 ? qy : (c == 2 ? r2y : py));
+            ch.rx = b.x;
+            ch.ry = b.y;
+            ch.r_idx = b.idx;
+            ch.m = m;
+            ch.begin = (c & 1) ? (c == 1 ? uint64_t(n1) - m : uint64_t(n1) + n2 - m)
+                               : (c == 0 ? 0 : uint64_t(n1));
+            a.children[c] = ch;
+        }
+    }
+    if (threadIdx.x == 0) *a.ticket = 0;
+}
+
+// ===========================================================================
 // launchers (the stable mode is launched cooperatively: co-resident CTAs)
 // ===========================================================================
 cudaError_t launch_root_partition(const RootArgs& a, int grid, bool stable, cudaStream_t st) {
     if (!stable) {
-        if (getenv("VQB_NO_PREFETCH")) root_partition_fast<false><<<grid, kThreads, 0, st>>>(a);
-        else root_partition_fast<true><<<grid, kThreads, 0, st>>>(a);
+        const bool aligned = ((reinterpret_cast<uintptr_t>(a.xs) | reinterpret_cast<uintptr_t>(a.ys)) & 15u) == 0;
+        if (aligned && !getenv("VQB_NO_TMA")) {
+            static bool attr = false;
+            if (!attr) {
+                cudaFuncSetAttribute(root_partition_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(sizeof(RootRing)));
+                attr = true;
+            }
+            root_partition_tma<<<grid, kCtlThreads, sizeof(RootRing), st>>>(a);
+        } else {
+            root_partition_fast<true><<<grid, kThreads, 0, st>>>(a);  // unaligned caller arrays
+        }
         return cudaGetLastError();
     }
     void* args[] = {const_cast<RootArgs*>(&a)};
@@ -1014,12 +1220,15 @@ cudaError_t launch_level(const LevelArgs& a, bool general, bool stable, int grid
 }
 
 int occupancy_root(bool stable) {
-    int b = 0;
-    if (stable) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, root_partition_kernel<true>, kThreads, 0);
-    else if (getenv("VQB_NO_PREFETCH"))
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, root_partition_fast<false>, kThreads, 0);
-    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, root_partition_fast<true>, kThreads, 0);
-    return b;
+    int b = 0, c = 0;
+    if (stable) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, root_partition_kernel<true>, kThreads, 0);
+        return b;
+    }
+    cudaFuncSetAttribute(root_partition_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(RootRing)));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, root_partition_fast<true>, kThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, root_partition_tma, kCtlThreads, sizeof(RootRing));
+    return b < c ? b : c;  // one grid size serves both fast-path kernels
 }
 int occupancy_level(bool stable) {
     int m = 1 << 30, b = 0;
