@@ -81,10 +81,12 @@ struct DevBuf {
 
 struct PointBuf {
     DevBuf x, y, id;
+    // +64 elements: the level kernel's TMA copies round segment ranges out to
+    // 16-byte boundaries and may read a few elements past a segment's end
     void ensure(size_t n, cudaStream_t st) {
-        x.ensure(n * 8, st);
-        y.ensure(n * 8, st);
-        id.ensure(n * 4, st);
+        x.ensure((n + 64) * 8, st);
+        y.ensure((n + 64) * 8, st);
+        id.ensure((n + 64) * 4, st);
     }
 };
 

@@ -1185,6 +1185,240 @@ __global__ void __launch_bounds__(kCtlThreads, 3) root_partition_tma(RootArgs a)
 }
 
 // ===========================================================================
+// K2 fast mode with a TMA ring (8 compute warps + 1 control warp).  The
+// control warp's lane 0 maps each upcoming tile of the CTA to its segment and
+// streams x, y and the indices into a kRing-deep shared-memory ring with
+// cp.async.bulk (segment starts are arbitrary: the copy starts at the
+// 16-byte-aligned element below and the consumer skips the head; buffers
+// carry a small tail pad).  Per tile the control warp scans the warp counts
+// and claims the tile's places in the segment's two child ranges with one
+// packed atomic while the compute warps update the running arg-max.
+// ===========================================================================
+struct LevelRing {
+    double x[kRing][kTile + 2];
+    double y[kRing][kTile + 2];
+    uint32_t id[kRing][kTile + 4];
+    unsigned long long bar[kRing];
+    SegRec seg[kRing];
+    uint32_t k[kRing];
+    uint32_t cnt[kRing];
+    uint32_t dx[kRing];
+    uint32_t di[kRing];
+};
+
+template <bool GENERAL>
+__global__ void __launch_bounds__(kCtlThreads, 3) level_tma(LevelArgs a) {
+    extern __shared__ __align__(128) unsigned char dsm[];
+    LevelRing& ring = *reinterpret_cast<LevelRing*>(dsm);
+    __shared__ FastSmem S;
+    __shared__ SegRec s_cur;
+    __shared__ uint32_t s_cur_k, s_cur_tiles;
+    __shared__ uint32_t s_org[2][kWarps];
+    __shared__ Best s_run[2];
+    __shared__ bool s_last;
+    __shared__ uint32_t s_ntiles;
+    const bool ctl = threadIdx.x >= kThreads;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t G = gridDim.x;
+    auto issue = [&](uint32_t kk) {  // control lane: local tile kk -> stage kk % kRing
+        const uint32_t t = blockIdx.x + kk * G;
+        if (t >= s_ntiles) return;
+        const int s = int(kk % kRing);
+        const uint32_t sk = a.tile_seg[t];
+        const SegRec g = a.segs[sk];
+        const uint32_t j = t - g.tile0;
+        const uint32_t start = uint32_t(g.begin) + j * uint32_t(kTile);
+        const uint32_t cnt = min(uint32_t(kTile), g.m - j * uint32_t(kTile));
+        const uint32_t ax = start & ~1u, dx = start - ax;
+        const uint32_t ai = start & ~3u, di = start - ai;
+        const uint32_t bx = ((cnt + dx + 1u) & ~1u) * 8u;
+        const uint32_t bi = ((cnt + di + 3u) & ~3u) * 4u;
+        VQB_CHECK(uint64_t(ax) * 8 + bx <= a.in_cap * 8 && uint64_t(ai) * 4 + bi <= a.in_cap * 4, 23, start, cnt);
+        ring.seg[s] = g;
+        ring.k[s] = sk;
+        ring.cnt[s] = cnt;
+        ring.dx[s] = dx;
+        ring.di[s] = di;
+        mbar_expect_tx(&ring.bar[s], 2u * bx + bi);
+        tma_load_1d(ring.x[s], a.ix + ax, bx, &ring.bar[s]);
+        tma_load_1d(ring.y[s], a.iy + ax, bx, &ring.bar[s]);
+        tma_load_1d(ring.id[s], a.iid + ai, bi, &ring.bar[s]);
+    };
+    if (threadIdx.x == kThreads) {
+        s_ntiles = a.info->ntiles;
+        s_cur_k = 0xffffffffu;
+        s_cur_tiles = 0;
+        for (int s = 0; s < kRing; ++s) mbar_init(&ring.bar[s], 1);
+        mbar_fence_init();
+        for (uint32_t kk = 0; kk < kRing; ++kk) issue(kk);
+    }
+    __syncthreads();
+    const uint32_t ntiles = s_ntiles;
+    const double kInf = __longlong_as_double(0x7ff0000000000000ll);
+    double bo[2] = {kInf, kInf};
+    uint32_t bi[2] = {kNoIdx, kNoIdx};
+
+    auto finalize = [&]() {
+        for (int c = 0; c < 2; ++c) {
+            double oo;
+            uint32_t io;
+            block_best_d<2>(S, c, bo[c], bi[c], a.gx, a.gy, oo, io);
+            if (threadIdx.x == 0)
+                s_run[c] = best_from_key(io == kNoIdx ? kNoKey : 0ull, io, c == 0 ? s_cur.adx : s_cur.bdx,
+                                         c == 0 ? s_cur.ady : s_cur.bdy, a.gx, a.gy);
+        }
+        if (threadIdx.x == 0) {
+            const uint32_t k = s_cur_k;
+            const uint32_t slot = atomicAdd(&a.seg_pcnt[k], 1u);
+            VQB_CHECK(slot < s_cur.ntiles && 2 * (uint64_t(s_cur.tile0) + slot) + 1 < a.part_cap,
+                      50, slot, s_cur.ntiles);
+            a.tile_part[2 * (uint64_t(s_cur.tile0) + slot)] = s_run[0];
+            a.tile_part[2 * (uint64_t(s_cur.tile0) + slot) + 1] = s_run[1];
+            __threadfence();
+            const uint32_t done = atomicAdd(&a.seg_done[k], s_cur_tiles) + s_cur_tiles;
+            s_last = (done == s_cur.ntiles);
+        }
+        __syncthreads();
+        if (s_last) {
+            __threadfence();
+            if (warp < 2) {
+                const int c = warp;
+                const uint32_t np = __ldcg(&a.seg_pcnt[s_cur_k]);
+                Best b = best_none();
+                for (uint32_t jj = lane; jj < np; jj += 32) {
+                    const Best o = ldcg_best(&a.tile_part[2 * (uint64_t(s_cur.tile0) + jj) + c]);
+                    if (prefer(o, b)) b = o;
+                }
+                b = warp_best(b);
+                if (lane == 0) {
+                    const SegRec& g = s_cur;
+                    const uint2 w = read_pair(&a.seg_ctr[s_cur_k]);
+                    const uint32_t m = c == 0 ? w.x : w.y;
+                    ChildRec ch;
+                    if (c == 0) {  // left of p->r: triangle (p, rL, r)
+                        ch.px = g.px; ch.py = g.py; ch.qx = g.rx; ch.qy = g.ry;
+                        ch.begin = g.out;
+                    } else {       // left of r->q: triangle (r, rR, q)
+                        ch.px = GENERAL ? g.bx : g.rx; ch.py = GENERAL ? g.by : g.ry;
+                        ch.qx = g.qx; ch.qy = g.qy;
+                        ch.begin = g.out + g.m - m;
+                    }
+                    ch.rx = b.x;
+                    ch.ry = b.y;
+                    ch.r_idx = b.idx;
+                    ch.m = m;
+                    VQB_CHECK(2 * uint64_t(s_cur_k) + c < a.children_cap, 57, s_cur_k, a.children_cap);
+                    a.children[2 * uint64_t(s_cur_k) + c] = ch;
+                }
+            }
+        }
+        __syncthreads();
+        bo[0] = bo[1] = kInf;
+        bi[0] = bi[1] = kNoIdx;
+    };
+
+    uint32_t kk = 0;
+    for (uint32_t t = blockIdx.x; t < ntiles; t += G, ++kk) {
+        const int s = int(kk % kRing);
+        // entering a new segment?  all threads decide on one snapshot
+        const uint32_t k_now = ring.k[s], k_cur = s_cur_k;
+        __syncthreads();
+        if (k_now != k_cur) {
+            if (k_cur != 0xffffffffu) finalize();
+            if (threadIdx.x == 0) {
+                s_cur = ring.seg[s];
+                s_cur_k = k_now;
+                s_cur_tiles = 0;
+            }
+            __syncthreads();
+        }
+        double ux[kItems], uy[kItems];
+        uint32_t uid[kItems];
+        int cls[kItems];
+        uint32_t rk[kItems];
+        const uint32_t out = uint32_t(ring.seg[s].out), m = ring.seg[s].m;
+        const double adx = ring.seg[s].adx, ady = ring.seg[s].ady;
+        const double bdx = ring.seg[s].bdx, bdy = ring.seg[s].bdy;
+        if (!ctl) {
+            const SegRec& g = ring.seg[s];
+            const uint32_t cnt = ring.cnt[s], dx = ring.dx[s], di = ring.di[s];
+            mbar_wait(&ring.bar[s], (kk / kRing) & 1u);
+            const double px = g.px, py = g.py, rx = g.rx, ry = g.ry, qx = g.qx, qy = g.qy;
+            uint32_t wrun = 0;
+#pragma unroll
+            for (int i = 0; i < kItems; ++i) {
+                const uint32_t r = uint32_t(i) * kThreads + threadIdx.x;
+                const bool v = r < cnt;
+                const double u = ring.x[s][dx + r], w = ring.y[s][dx + r];
+                ux[i] = u;
+                uy[i] = w;
+                uid[i] = ring.id[s][di + r];
+                bool la, lb;
+                if (GENERAL) {
+                    la = left_diff(dsub(px, u), dsub(py, w), dsub(rx, u), dsub(ry, w));
+                    lb = !la && left_diff(dsub(g.bx, u), dsub(g.by, w), dsub(qx, u), dsub(qy, w));
+                } else {
+                    const double A = dsub(px, u), B = dsub(py, w);
+                    const double E = dsub(rx, u), F = dsub(ry, w);
+                    const double Cc = dsub(qx, u), D = dsub(qy, w);
+                    la = left_diff(A, B, E, F);
+                    lb = !la && left_diff(E, F, Cc, D);
+                }
+                const int c = !v ? 2 : (la ? 0 : (lb ? 1 : 2));
+                cls[i] = c;
+                rk[i] = warp_rank<2>(c, wrun);
+            }
+            if (lane < 2) S.wtot[lane][warp] = wrun;
+        }
+        __syncthreads();  // counts ready; every compute warp is done with stage s
+        if (ctl) {
+            uint32_t tot[2];
+            tile_scan_fast<2>(S, tot);
+            if (lane == 0) {
+                const uint2 c2 = claim_pair(&a.seg_ctr[k_now], tot[0], tot[1]);
+                S.claim[0] = c2.x;
+                S.claim[1] = c2.y;
+            }
+            __syncwarp();
+            if (lane < 2 * kWarps) {
+                const int c = lane / kWarps, w = lane % kWarps;
+                const uint32_t off = S.claim[c] + S.wbase[c][w];
+                const uint32_t org = c == 0 ? out : out + m - 1u;
+                s_org[c][w] = c ? org - off : org + off;
+            }
+            if (lane == 0) {
+                fence_proxy_async_smem();
+                issue(kk + kRing);  // refill stage s
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < kItems; ++i) {  // fused farthest-point search, overlapping the claim
+                const int c = cls[i];
+                running_best_d<2>(bo, bi, c, lat_off(c == 0 ? adx : bdx, c == 0 ? ady : bdy, ux[i], uy[i]),
+                                  uid[i], a.gx, a.gy);
+            }
+        }
+        __syncthreads();
+        if (!ctl) {
+#pragma unroll
+            for (int i = 0; i < kItems; ++i) {
+                const int c = cls[i];
+                if (c < 2) {
+                    const uint32_t o = s_org[c][warp];
+                    const uint32_t p = c ? o - rk[i] : o + rk[i];
+                    VQB_CHECK(p < a.out_cap, 13, p, a.out_cap);
+                    a.ox[p] = ux[i];
+                    a.oy[p] = uy[i];
+                    a.oid[p] = uid[i];
+                }
+            }
+        }
+        if (threadIdx.x == 0) ++s_cur_tiles;
+    }
+    if (s_cur_k != 0xffffffffu) finalize();
+}
+
+// ===========================================================================
 // launchers (the stable mode is launched cooperatively: co-resident CTAs)
 // ===========================================================================
 cudaError_t launch_root_partition(const RootArgs& a, int grid, bool stable, cudaStream_t st) {
@@ -1209,6 +1443,17 @@ cudaError_t launch_root_partition(const RootArgs& a, int grid, bool stable, cuda
 }
 
 cudaError_t launch_level(const LevelArgs& a, bool general, bool stable, int grid, cudaStream_t st) {
+    if (!stable && !getenv("VQB_NO_TMA")) {
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(level_tma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(LevelRing)));
+            cudaFuncSetAttribute(level_tma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(LevelRing)));
+            attr = true;
+        }
+        if (general) level_tma<true><<<grid, kCtlThreads, sizeof(LevelRing), st>>>(a);
+        else level_tma<false><<<grid, kCtlThreads, sizeof(LevelRing), st>>>(a);
+        return cudaGetLastError();
+    }
     if (!stable) {
         if (general) level_kernel<true, false><<<grid, kThreads, 0, st>>>(a);
         else level_kernel<false, false><<<grid, kThreads, 0, st>>>(a);
@@ -1238,6 +1483,10 @@ int occupancy_level(bool stable) {
     } else {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, level_kernel<false, false>, kThreads, 0); m = b < m ? b : m;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, level_kernel<true, false>, kThreads, 0); m = b < m ? b : m;
+        cudaFuncSetAttribute(level_tma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(LevelRing)));
+        cudaFuncSetAttribute(level_tma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(LevelRing)));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, level_tma<false>, kCtlThreads, sizeof(LevelRing)); m = b < m ? b : m;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, level_tma<true>, kCtlThreads, sizeof(LevelRing)); m = b < m ? b : m;
     }
     return m;
 }
