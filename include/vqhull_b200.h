@@ -102,6 +102,11 @@ typedef struct vqhull_stats {
     uint64_t bytes_root_partition;
     uint64_t bytes_levels;
     uint64_t bytes_finisher;
+    uint32_t root_filtered;     /* 1: root stage = 8-direction extremes + level 1
+                                   behind the octagon filter; 0: find_extremes +
+                                   bootstrap + fused levels 1+2 */
+    uint32_t root_filter_on;    /* the octagon filter could drop points (coordinate
+                                   magnitudes in range) */
 } vqhull_stats;
 
 int vqhull_cuda_get_stats(vqhull_stats* out);
@@ -116,6 +121,13 @@ int vqhull_cuda_set_timing(int enable);
  * keep input order (order-preserving compaction).  Hull outputs are identical
  * in both modes.  The environment variable VQHULL_STABLE=1 sets the default. */
 int vqhull_cuda_set_stable(int stable);
+
+/* Root stage: 0 (default, fast mode with 16-byte aligned inputs) one pass for
+ * the 8 exact directional extremes, then level 1 behind their octagon filter;
+ * 1: find_extremes, bootstrap arg-max and the fused levels-1+2 pass.  The
+ * recursion is the reference's in both; hull outputs are identical.  The
+ * environment variable VQHULL_ROOT=reference sets 1. */
+int vqhull_cuda_set_root_reference(int reference);
 
 /* Human-readable description of the last CUDA error (thread-local). */
 const char* vqhull_cuda_last_error(void);

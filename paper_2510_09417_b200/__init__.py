@@ -65,6 +65,8 @@ class Stats(C.Structure):
         ("bytes_extremes", C.c_uint64), ("bytes_bootstrap", C.c_uint64),
         ("bytes_root_partition", C.c_uint64), ("bytes_levels", C.c_uint64),
         ("bytes_finisher", C.c_uint64),
+        ("root_filtered", C.c_uint32),
+        ("root_filter_on", C.c_uint32),
     ]
 
     def as_dict(self) -> dict:
@@ -94,6 +96,7 @@ def lib() -> C.CDLL:
         L.vqhull_cuda_get_stats.argtypes = [C.POINTER(Stats)]
         L.vqhull_cuda_set_timing.argtypes = [C.c_int]
         L.vqhull_cuda_set_stable.argtypes = [C.c_int]
+        L.vqhull_cuda_set_root_reference.argtypes = [C.c_int]
         L.vqhull_cuda_last_error.restype = C.c_char_p
         L.vqhull_b200_version.restype = C.c_char_p
         L.vqhull_generate.argtypes = [C.c_int, C.c_uint64, C.c_uint64, C.c_uint64, C.c_void_p,
@@ -243,6 +246,12 @@ def stats() -> dict:
 def set_stable(on: bool) -> None:
     """Order-preserving (look-back) partition offsets instead of atomic claims."""
     _check(lib().vqhull_cuda_set_stable(int(bool(on))), "vqhull_cuda_set_stable")
+
+
+def set_root_reference(on: bool) -> None:
+    """Root stage without the octagon filter: find_extremes, bootstrap arg-max
+    and the fused levels-1+2 pass.  Same hull either way."""
+    _check(lib().vqhull_cuda_set_root_reference(int(bool(on))), "vqhull_cuda_set_root_reference")
 
 
 def set_timing(on: bool) -> None:

@@ -117,6 +117,11 @@ __device__ __forceinline__ bool left_diff(double pdx, double pdy, double qdx, do
     return dmul(pdx, qdy) > dmul(pdy, qdx);
 }
 
+// Inf or NaN (exponent all ones), by the bits
+__device__ __forceinline__ bool nonfinite_bits(double v) {
+    return (__double2hiint(v) & 0x7ff00000) == 0x7ff00000;
+}
+
 // lateral offset e.dy*ux - e.dx*uy (kernels.hpp:32-34)
 __device__ __forceinline__ double lat_off(double edx, double edy, double ux, double uy) {
     return dsub(dmul(edy, ux), dmul(edx, uy));

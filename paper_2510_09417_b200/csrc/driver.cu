@@ -120,10 +120,12 @@ class Engine {
         occ_level_ = std::max(1, occupancy_level(false));
         occ_level_stable_ = std::max(1, occupancy_level(true));
         occ_fin_ = std::max(1, occupancy_finisher());
+        occ_filt_ = std::max(1, occupancy_filtered());
         // one full wave each
         grid_ext_ = sms_ * std::max(1, std::min(8, occupancy_extremes()));
         grid_boot_ = sms_ * std::max(1, std::min(8, occupancy_bootstrap()));
-        stream_grid_ = std::max(grid_ext_, grid_boot_);
+        grid_poly_ = sms_ * std::max(1, std::min(8, occupancy_poly_extremes()));
+        stream_grid_ = std::max(std::max(grid_ext_, grid_boot_), grid_poly_);
         VQB_TRACE("engine: allocations");
         ck(cudaMalloc(&ctrs_, 64 * sizeof(uint32_t)), "cudaMalloc ctrs");
         ck(cudaMemset(ctrs_, 0, 64 * sizeof(uint32_t)), "memset ctrs");
@@ -155,54 +157,20 @@ class Engine {
         launches_ = 0;
         begin_timing(st);
 
-        // ---- K1: extremes
-        tk(0, st, [&] { launch_extremes(dx, dy, n, partials_.p, &ctrs_[3], root_, grid_ext_, st); });
-        // ---- KA: bootstrap counts + arg-max + finiteness
-        tk(1, st, [&] { launch_bootstrap(dx, dy, n, partials_.p, &ctrs_[3], root_, grid_boot_, st); });
-        upload_root_consts(root_, st);  // p, q, r1, r2 -> constant bank for KB
-        stats_.bytes_extremes = 8 * n;
-        stats_.bytes_bootstrap = 16 * n;
-
-        // ---- level-1 slot table (the two bootstrap sides)
-        LevelTables& L1 = level(1);
-        L1.slots.ensure(2 * sizeof(ChildRec), st);
-        L1.kind.ensure(2, st);
-        L1.link.ensure(8, st);
-        L1.size.ensure(8, st);
-        L1.start.ensure(8, st);
-        launch_root_slots(root_, L1.slots.as<ChildRec>(), L1.kind.as<uint8_t>(), L1.link.as<uint32_t>(),
-                          side_ctr(), st);
-        ++launches_;
-
-        // ---- KB: fused levels 1+2 over the input
-        bufs_[0].ensure(n, st);
-        const uint32_t ntiles_root = uint32_t((n + kTile - 1) / kTile);
-        ensure_lookback(2 * ntiles_root, st);
-        LevelTables& L2 = level(2);
-        L2.slots.ensure(4 * sizeof(ChildRec), st);
-        {
-            const int grid = std::max(1, std::min<int>(int(ntiles_root), sms_ * (stable_ ? occ_root_stable_ : occ_root_)));
-            part_.ensure(size_t(grid) * 4 * sizeof(Best), st);
-            RootArgs ra;
-            ra.xs = dx; ra.ys = dy; ra.n = n; ra.root = root_;
-            ra.ox = bufs_[0].x.as<double>(); ra.oy = bufs_[0].y.as<double>(); ra.oid = bufs_[0].id.as<uint32_t>();
-            ra.out_cap = bufs_[0].x.cap / 8;
-            ra.status = status_.as<Status>(); ra.epoch = next_epoch();
-            ra.ctr = &ctrs_[0]; ra.ticket = &ctrs_[4]; ra.cta_part = part_.as<Best>();
-            ra.side_ctr = side_ctr();
-            ra.children = L2.slots.as<ChildRec>(); ra.ntiles = ntiles_root;
-            tk(2, st, [&] { ck(launch_root_partition(ra, grid, stable_, st), "root partition launch"); });
-        }
-        // finiteness verdict + sizes for the byte accounting
+        // ---- root stage: polygon + first partition (levels 1+2 in reference mode)
+        const bool aligned = ((reinterpret_cast<uintptr_t>(dx) | reinterpret_cast<uintptr_t>(dy)) & 15u) == 0;
+        const bool filtered = !stable_ && !root_reference_ && aligned && !getenv("VQB_NO_TMA");
+        uint32_t nslots = filtered ? run_root_filtered(dx, dy, n, st) : run_root_reference(dx, dy, n, st);
+        // finiteness verdict, octagon verdict, sizes for the byte accounting
         ck(cudaMemcpyAsync(h_root_, root_, sizeof(RootInfo), cudaMemcpyDeviceToHost, st), "d2h root");
 
         // ---- levels
         int in = 0;
-        uint32_t nslots = 4;
         uint64_t fin_base = 0;
         int lvl = 2;
         level_fin_base_.assign(4, 0);
         while (true) {
+            if (lvl == 2) note_slots(2, nslots);
             LevelTables& T = level(lvl);
             T.kind.ensure(nslots, st);
             T.link.ensure(size_t(nslots) * 4, st);
@@ -299,30 +267,30 @@ class Engine {
         }
         stats_.levels = uint32_t(lmax_);
         stats_.bytes_root_partition = 16 * n + 20 * stats_.survivors_root;
+        stats_.root_filtered = filtered ? 1u : 0u;
+        if (filtered) stats_.root_filter_on = h_root_->poly.filter;
 
         // ---- emission: bottom-up sizes, root frame, top-down starts
-        for (int l = lmax_; l >= 1; --l) {
+        for (int l = lmax_; l >= 2; --l) {
             LevelTables& T = level(l);
             const uint32_t ns = slot_count(l);
             const uint32_t* child_size = (l < lmax_) ? level(l + 1).size.as<uint32_t>() : nullptr;
             tk(5, st, [&] {
-                launch_size(ns, T.kind.as<uint8_t>(), T.link.as<uint32_t>(),
-                            l >= 2 ? T.fin_count.as<uint32_t>() : nullptr, child_size,
-                            T.size.as<uint32_t>(), st);
+                launch_size(ns, T.kind.as<uint8_t>(), T.link.as<uint32_t>(), T.fin_count.as<uint32_t>(),
+                            child_size, T.size.as<uint32_t>(), st);
             });
         }
         tk(5, st, [&] {
-            launch_root_frame(root_, level(1).size.as<uint32_t>(), level(1).start.as<uint32_t>(), d_out,
+            launch_poly_frame(root_, level(2).size.as<uint32_t>(), level(2).start.as<uint32_t>(), d_out,
                               hword_, st);
         });
-        for (int l = 1; l <= lmax_; ++l) {
+        for (int l = 2; l <= lmax_; ++l) {
             LevelTables& T = level(l);
             const uint32_t ns = slot_count(l);
             const bool has_child = l < lmax_;
             tk(5, st, [&] {
                 launch_emit(ns, T.kind.as<uint8_t>(), T.link.as<uint32_t>(), T.slots.as<ChildRec>(),
-                            l >= 2 ? T.fins.as<FinRec>() : nullptr,
-                            l >= 2 ? T.fin_count.as<uint32_t>() : nullptr, chain_.as<uint32_t>(),
+                            T.fins.as<FinRec>(), T.fin_count.as<uint32_t>(), chain_.as<uint32_t>(),
                             T.start.as<uint32_t>(), has_child ? level(l + 1).size.as<uint32_t>() : nullptr,
                             has_child ? level(l + 1).start.as<uint32_t>() : nullptr, d_out, st);
             });
@@ -450,6 +418,61 @@ class Engine {
     DevBuf& out_buf() { return out_; }
 
    private:
+    // Default: K1' (8 exact directional extremes + finiteness) then KB'
+    // (level 1 behind the octagon filter).  Returns the level-2 slot count.
+    uint32_t run_root_filtered(const double* dx, const double* dy, uint64_t n, cudaStream_t st) {
+        tk(0, st, [&] { launch_poly_extremes(dx, dy, n, partials_.p, &ctrs_[3], root_, side_ctr(), grid_poly_, st); });
+        upload_root_consts(root_, st);
+        stats_.bytes_extremes = 8 * n + 2 * n;  // x + the 1/8 y sample
+        stats_.bytes_bootstrap = 0;
+        bufs_[0].ensure(n, st);
+        const uint32_t ntiles_root = uint32_t((n + kTile - 1) / kTile);
+        LevelTables& L2 = level(2);
+        L2.slots.ensure(2 * sizeof(ChildRec), st);
+        const int grid = std::max(1, std::min<int>(int(ntiles_root), sms_ * occ_filt_));
+        part_.ensure(size_t(grid) * 2 * sizeof(Best), st);
+        RootArgs ra;
+        std::memset(&ra, 0, sizeof ra);
+        ra.xs = dx; ra.ys = dy; ra.n = n; ra.root = root_; ra.root_w = root_;
+        ra.ox = bufs_[0].x.as<double>(); ra.oy = bufs_[0].y.as<double>(); ra.oid = bufs_[0].id.as<uint32_t>();
+        ra.out_cap = bufs_[0].x.cap / 8;
+        ra.ticket = &ctrs_[4]; ra.cta_part = part_.as<Best>();
+        ra.side_ctr = side_ctr();
+        ra.children = L2.slots.as<ChildRec>(); ra.ntiles = ntiles_root;
+        tk(2, st, [&] { ck(launch_root_filtered(ra, grid, st), "filtered root launch"); });
+        return 2;
+    }
+
+    // Reference mode: K1 find_extremes, KA bootstrap arg-max, KB levels 1+2
+    // fused; polygon (p, r1, q, r2).  Returns the level-2 slot count.
+    uint32_t run_root_reference(const double* dx, const double* dy, uint64_t n, cudaStream_t st) {
+        tk(0, st, [&] { launch_extremes(dx, dy, n, partials_.p, &ctrs_[3], root_, grid_ext_, st); });
+        tk(1, st, [&] { launch_bootstrap(dx, dy, n, partials_.p, &ctrs_[3], root_, grid_boot_, st); });
+        launch_legacy_poly(root_, side_ctr(), st);  // also re-arms the side counters
+        ++launches_;
+        upload_root_consts(root_, st);  // p, q, r1, r2 -> constant bank for KB
+        stats_.bytes_extremes = 8 * n;
+        stats_.bytes_bootstrap = 16 * n;
+        bufs_[0].ensure(n, st);
+        const uint32_t ntiles_root = uint32_t((n + kTile - 1) / kTile);
+        ensure_lookback(2 * ntiles_root, st);
+        LevelTables& L2 = level(2);
+        L2.slots.ensure(4 * sizeof(ChildRec), st);
+        const int grid = std::max(1, std::min<int>(int(ntiles_root), sms_ * (stable_ ? occ_root_stable_ : occ_root_)));
+        part_.ensure(size_t(grid) * 4 * sizeof(Best), st);
+        RootArgs ra;
+        std::memset(&ra, 0, sizeof ra);
+        ra.xs = dx; ra.ys = dy; ra.n = n; ra.root = root_; ra.root_w = root_;
+        ra.ox = bufs_[0].x.as<double>(); ra.oy = bufs_[0].y.as<double>(); ra.oid = bufs_[0].id.as<uint32_t>();
+        ra.out_cap = bufs_[0].x.cap / 8;
+        ra.status = status_.as<Status>(); ra.epoch = next_epoch();
+        ra.ctr = &ctrs_[0]; ra.ticket = &ctrs_[4]; ra.cta_part = part_.as<Best>();
+        ra.side_ctr = side_ctr();
+        ra.children = L2.slots.as<ChildRec>(); ra.ntiles = ntiles_root;
+        tk(2, st, [&] { ck(launch_root_partition(ra, grid, stable_, st), "root partition launch"); });
+        return 4;
+    }
+
     LevelTables& level(int l) {
         if (levels_.size() <= size_t(l)) levels_.resize(l + 1);
         return levels_[l];
@@ -485,8 +508,6 @@ class Engine {
         stats_.n = n;
         timed_.clear();
         slot_counts_.assign(3, 0);
-        slot_counts_[1] = 2;
-        slot_counts_[2] = 4;
         lmax_ = 2;
     }
 
@@ -569,7 +590,8 @@ class Engine {
     int dev_ = 0;
     int sms_ = 148;
     int occ_root_ = 1, occ_root_stable_ = 1, occ_level_ = 1, occ_level_stable_ = 1, occ_fin_ = 1;
-    int stream_grid_ = 592, grid_ext_ = 592, grid_boot_ = 592;
+    int stream_grid_ = 592, grid_ext_ = 592, grid_boot_ = 592, grid_poly_ = 592, occ_filt_ = 1;
+    bool root_reference_ = getenv("VQHULL_ROOT") != nullptr && std::string(getenv("VQHULL_ROOT")) == "reference";
     uint32_t* ctrs_ = nullptr;
     RootInfo* root_ = nullptr;
     uint32_t* hword_ = nullptr;
@@ -592,6 +614,7 @@ class Engine {
 
    public:
     void set_stable(bool s) { stable_ = s; }
+    void set_root_reference(bool r) { root_reference_ = r; }
     bool stable() const { return stable_; }
 
    private:
@@ -695,6 +718,17 @@ int vqhull_cuda_set_stable(int stable) {
         Engine& e = vqb::engine();
         std::lock_guard<std::mutex> lk(e.mutex());
         e.set_stable(stable != 0);
+        return 0;
+    } catch (const CudaError&) {
+        return VQHULL_ECUDA;
+    }
+}
+
+int vqhull_cuda_set_root_reference(int reference) {
+    try {
+        Engine& e = vqb::engine();
+        std::lock_guard<std::mutex> lk(e.mutex());
+        e.set_root_reference(reference != 0);
         return 0;
     } catch (const CudaError&) {
         return VQHULL_ECUDA;

@@ -20,6 +20,31 @@ constexpr int kPartMinBlocks = 3;           // resident partition CTAs per SM (r
 constexpr int kFastMinBlocks = 4;           // fast-mode kernels (no staging)
 constexpr uint32_t kFinMax = 256;           // segments this small go to the warp finisher
 
+// Root stage geometry.  The recursion itself always follows the reference
+// (level 1 splits by p->q, hull.cpp:228-235); the octagon of the 8 exact
+// directional extremes is only a FILTER in front of it: a point provably
+// inside the octagon by a margin far above the predicates' rounding can never
+// be a farthest point or a lone subset member, so dropping it cannot change
+// the reference's output.
+//  * vx/vy/vidx: V_j = extreme in direction j * 45 degrees clockwise from -x
+//    (L, TL, T, TR, R, BR, B, BL); chord j = V_j -> V_{j+1 mod 8};
+//  * emission frame: nv vertices, slot j between V_j and V_{j+1}, repeated
+//    vertices written once: nv = 2 (p, q) for the filtered root, 4 (p, r1,
+//    q, r2) for the fused levels-1+2 root.
+struct RootPoly {
+    double vx[8], vy[8];
+    uint32_t vidx[8];
+    double ex[4], ey[4];        // emission frame vertices
+    uint32_t eidx[4];
+    uint32_t nv;
+    uint32_t filter;            // 1: the octagon filter may drop points
+    // chord j as a linear form f_j(P) = fa*x + fb*y + fc = cross(V_{j+1} - V_j,
+    // P - V_j) (> 0: left of the chord, outside); P is dropped when
+    // f_j(P) < ft_j for all 8 chords (ft_j = -margin * |chord|_1)
+    double fa[8], fb[8], fc[8], ft[8];
+    double bx0, bx1, by0, by1;  // open box verified to lie inside the filter region
+};
+
 // K1 + pass A results, one per hull call (device resident).
 struct RootInfo {
     // K1: find_extremes (geometry.cpp:7-36)
@@ -30,6 +55,7 @@ struct RootInfo {
     Best r1, r2;
     uint32_t nonfinite;
     uint32_t pad;
+    RootPoly poly;
 };
 
 // One node of the recursion tree as produced by its parent's partition:
@@ -103,9 +129,10 @@ struct RootArgs {
     uint32_t epoch;
     uint32_t* ctr;       // tile claim counter
     uint32_t* ticket;    // CTA exit ticket
-    Best* cta_part;      // 4 per CTA
-    ChildRec* children;  // 4 slots
+    Best* cta_part;      // 4 per CTA (8 in octagon mode)
+    ChildRec* children;  // 4 slots (8 in octagon mode)
     uint32_t ntiles;
+    RootInfo* root_w;    // filtered root: side counts and apexes for the stats
 };
 
 struct LevelArgs {

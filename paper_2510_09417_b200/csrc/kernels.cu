@@ -201,9 +201,6 @@ struct RootPartial {
     Best b1, b2;
 };
 
-__device__ __forceinline__ bool nonfinite_bits(double v) {
-    return (__double2hiint(v) & 0x7ff00000) == 0x7ff00000;
-}
 
 __global__ void __launch_bounds__(256) bootstrap_argmax_kernel(
     const double* __restrict__ xs, const double* __restrict__ ys, uint64_t n,
@@ -346,6 +343,303 @@ __global__ void __launch_bounds__(256) bootstrap_argmax_kernel(
         root->r2 = B2;
         *ticket = 0;
     }
+}
+
+// ===========================================================================
+// K1' (default root stage): find_extremes (geometry.cpp:7-36) over every
+// point, exactly as K1 (x read for every point, y only on exact x ties),
+// plus the octagon filter's other six vertices from a sample of the input
+// (every 8th group of 256 points, x and y): max/min y, max/min x+y, max/min
+// x-y.  The filter only needs its vertices to be input points on two
+// x-monotone chains (checked here; otherwise no filter), not exact extremes,
+// so a sample costs 1/8 of a y pass and loses almost nothing.  Finiteness of
+// x is checked here, of y by the root pass that reads every y.
+// ===========================================================================
+struct PolyPartial {
+    ExtKey lo, hi;
+    double av[6];
+    uint32_t ai[6];
+    uint32_t nonfinite;
+    uint32_t pad;
+};
+
+constexpr int kSampleShift = 7;  // groups of 128 pairs (256 points)
+constexpr int kSampleMask = 7;   // one group in 8 is sampled
+
+// sampled directions, in octagon slot order 1, 2, 3, 5, 6, 7:
+// TL min x-y, T max y, TR max x+y, BR max x-y, B min y, BL min x+y
+__device__ __forceinline__ bool approx_better(int a, double v, uint32_t i, double vb, uint32_t ib) {
+    if (i == kNoIdx) return false;
+    if (ib == kNoIdx) return true;
+    const bool maximize = (a == 1 || a == 2 || a == 3);
+    if (v != vb) return maximize ? v > vb : v < vb;
+    return i < ib;
+}
+
+// Last step of K1' (one thread): the root polygon, the filter's chord forms
+// and inner box, the emission frame.
+__device__ __noinline__ void poly_finish(const PolyPartial& F, const double* __restrict__ xs,
+                                         const double* __restrict__ ys, RootInfo* root) {
+    const double kInf = __longlong_as_double(0x7ff0000000000000ll);
+    const ExtKey L = F.lo, H = F.hi;
+    const uint32_t nb = F.nonfinite;
+    const uint32_t* bi = F.ai;
+    RootInfo& R = *root;
+    RootPoly& P = R.poly;
+    // octagon slot order: 0 L, 1 TL, 2 T, 3 TR, 4 R, 5 BR, 6 B, 7 BL
+    const int slot_of[6] = {1, 2, 3, 5, 6, 7};
+    bool ok = L.valid && H.valid && nb == 0;
+    double vx[8], vy[8];
+    uint32_t vi[8];
+    vx[0] = L.x; vy[0] = L.y; vi[0] = L.idx;
+    vx[4] = H.x; vy[4] = H.y; vi[4] = H.idx;
+    for (int q = 0; q < 6; ++q) {
+        const int j = slot_of[q];
+        ok &= bi[q] != kNoIdx;
+        vi[j] = bi[q] != kNoIdx ? bi[q] : L.idx;
+        vx[j] = bi[q] != kNoIdx ? xs[bi[q]] : L.x;
+        vy[j] = bi[q] != kNoIdx ? ys[bi[q]] : L.y;
+    }
+    for (int j = 0; j < 8; ++j) {
+        P.vx[j] = vx[j];
+        P.vy[j] = vy[j];
+        P.vidx[j] = vi[j];
+    }
+    // Every vertex is an input point, so the region right of all 8 chords
+    // (the octagon, or its kernel if the sample made it non-convex) lies in
+    // the hull.  M bounds |coordinates| of the vertices, hence of every point
+    // the filter can drop; the margin is 2^-32 M (~10^5 ulps of M), so the
+    // fused multiply-adds' rounding can never reach a dropped point and no
+    // reference predicate can see one as a hull or farthest candidate.
+    // Outside 2^-400 <= M <= 2^500 (products could underflow/overflow): no
+    // filter.
+    double M = 0.0;
+    for (int j = 0; j < 8; ++j) M = fmax(M, fmax(fabs(vx[j]), fabs(vy[j])));
+    ok &= M >= 0x1p-400 && M <= 0x1p500;
+    int chords = 0;
+    for (int j = 0; j < 8; ++j) {
+        const int k = (j + 1) & 7;
+        const double ex = vx[k] - vx[j], ey = vy[k] - vy[j];
+        chords += !(ex == 0.0 && ey == 0.0);
+        if (ex == 0.0 && ey == 0.0) {  // degenerate chord: no constraint
+            P.fa[j] = 0.0; P.fb[j] = 0.0; P.fc[j] = -1.0; P.ft[j] = 0.0;
+        } else {
+            P.fa[j] = -ey;
+            P.fb[j] = ex;
+            P.fc[j] = ey * vx[j] - ex * vy[j];
+            P.ft[j] = -0x1p-32 * M * (fabs(ex) + fabs(ey));
+        }
+    }
+    auto inside = [&](double x, double y) {
+        bool in = true;
+        for (int j = 0; j < 8; ++j) in &= __fma_rn(P.fa[j], x, __fma_rn(P.fb[j], y, P.fc[j])) < P.ft[j];
+        return in;
+    };
+    // inner box from the vertices (its corners tend to BE vertices, so it is
+    // shrunk a little); kept only if its 4 corners pass the test (the filter
+    // region is convex, so then the whole box does)
+    const double cx0 = fmax(vx[1], vx[7]), cx1 = fmin(vx[3], vx[5]);
+    const double cy0 = fmax(vy[5], vy[7]), cy1 = fmin(vy[1], vy[3]);
+    double bx0 = kInf, bx1 = -kInf, by0 = kInf, by1 = -kInf;  // empty
+    const double shrink[3] = {0x1p-20 * M, 0x1p-10 * M, 0.0625 * fmax(cx1 - cx0, cy1 - cy0)};
+    for (int t = 0; t < 3; ++t) {
+        const double x0 = cx0 + shrink[t], x1 = cx1 - shrink[t];
+        const double y0 = cy0 + shrink[t], y1 = cy1 - shrink[t];
+        if (x0 < x1 && y0 < y1 && inside(x0, y0) && inside(x0, y1) && inside(x1, y0) && inside(x1, y1)) {
+            bx0 = x0; bx1 = x1; by0 = y0; by1 = y1;
+            break;
+        }
+    }
+    P.bx0 = bx0; P.bx1 = bx1; P.by0 = by0; P.by1 = by1;
+    ok &= chords >= 2;  // all vertices equal: the test would constrain nothing
+    P.filter = ok ? 1u : 0u;
+    P.nv = 2;  // emission frame: [p] chain(S1) [q] chain(S2)
+    P.ex[0] = L.x; P.ey[0] = L.y; P.eidx[0] = L.idx;
+    P.ex[1] = H.x; P.ey[1] = H.y; P.eidx[1] = H.idx;
+    R.nonfinite = nb;
+    R.p_idx = L.idx;
+    R.q_idx = H.idx;
+    R.px = L.x; R.py = L.y;
+    R.qx = H.x; R.qy = H.y;
+}
+
+__global__ void __launch_bounds__(256, 3) poly_extremes_kernel(const double* __restrict__ xs,
+                                                            const double* __restrict__ ys, uint64_t n,
+                                                            PolyPartial* partials, uint32_t* ticket,
+                                                            RootInfo* root, unsigned long long* side_ctr) {
+    const double kInf = __longlong_as_double(0x7ff0000000000000ll);
+    double lo_x = kInf, hi_x = -kInf;
+    uint32_t lo_i = kNoIdx, hi_i = kNoIdx;
+    double av[6] = {kInf, -kInf, -kInf, -kInf, kInf, kInf};
+    uint32_t ai[6] = {kNoIdx, kNoIdx, kNoIdx, kNoIdx, kNoIdx, kNoIdx};
+    bool bad = false;
+    auto visit_x = [&](uint32_t i, double x) {
+        bad |= nonfinite_bits(x);
+        const bool lt = x < lo_x, gt = x > hi_x;
+        const bool tie = (x == lo_x) | (x == hi_x);
+        if (__any_sync(__activemask(), tie)) {
+            if (x == lo_x && lo_i != kNoIdx && ys[i] < ys[lo_i]) lo_i = i;
+            if (x == hi_x && hi_i != kNoIdx && ys[i] > ys[hi_i]) hi_i = i;
+        }
+        lo_i = lt ? i : lo_i;
+        lo_x = lt ? x : lo_x;
+        hi_i = gt ? i : hi_i;
+        hi_x = gt ? x : hi_x;
+    };
+    auto visit_xy = [&](uint32_t i, double x, double y) {
+        const double s = __dadd_rn(x, y), d = __dsub_rn(x, y);
+        const double val[6] = {d, y, s, d, y, s};
+#pragma unroll
+        for (int a = 0; a < 6; ++a) {
+            const bool maximize = (a == 1 || a == 2 || a == 3);
+            const bool take = maximize ? val[a] > av[a] : val[a] < av[a];
+            av[a] = take ? val[a] : av[a];
+            ai[a] = take ? i : ai[a];
+        }
+    };
+    const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t stride = gridDim.x * blockDim.x;
+    const bool vec = ((reinterpret_cast<uintptr_t>(xs) | reinterpret_cast<uintptr_t>(ys)) & 15u) == 0;
+    if (vec) {
+        const uint32_t npair = uint32_t(n / 2);
+        const double2* x2 = reinterpret_cast<const double2*>(xs);
+        const double2* y2 = reinterpret_cast<const double2*>(ys);
+        uint32_t j = tid;
+        for (; j + (kStreamUnroll - 1) * stride < npair; j += kStreamUnroll * stride) {
+            double2 v[kStreamUnroll], w[kStreamUnroll];
+            // the sample test is warp-uniform (32 consecutive pairs); y loads
+            // are issued with the x loads so both are in flight together
+#pragma unroll
+            for (int u = 0; u < kStreamUnroll; ++u) {
+                const uint32_t jj = j + u * stride;
+                v[u] = __ldcs(&x2[jj]);
+                if (((jj >> kSampleShift) & kSampleMask) == 0) w[u] = __ldcs(&y2[jj]);
+            }
+#pragma unroll
+            for (int u = 0; u < kStreamUnroll; ++u) {
+                const uint32_t jj = j + u * stride;
+                visit_x(2 * jj, v[u].x);
+                visit_x(2 * jj + 1, v[u].y);
+                if (((jj >> kSampleShift) & kSampleMask) == 0) {
+                    visit_xy(2 * jj, v[u].x, w[u].x);
+                    visit_xy(2 * jj + 1, v[u].y, w[u].y);
+                }
+            }
+        }
+        for (; j < npair; j += stride) {
+            const double2 v = __ldcs(&x2[j]);
+            visit_x(2 * j, v.x);
+            visit_x(2 * j + 1, v.y);
+            if (((j >> kSampleShift) & kSampleMask) == 0) {
+                const double2 w = __ldcs(&y2[j]);
+                visit_xy(2 * j, v.x, w.x);
+                visit_xy(2 * j + 1, v.y, w.y);
+            }
+        }
+        if ((n & 1) && tid == 0) {
+            visit_x(uint32_t(n - 1), xs[n - 1]);
+            visit_xy(uint32_t(n - 1), xs[n - 1], ys[n - 1]);
+        }
+    } else {
+        for (uint32_t i = tid; i < n; i += stride) {
+            visit_x(i, xs[i]);
+            if (((i >> (kSampleShift + 1)) & kSampleMask) == 0) visit_xy(i, xs[i], ys[i]);
+        }
+    }
+    // reductions: warp -> CTA partial -> last CTA
+    ExtKey lo{lo_x, 0.0, lo_i, lo_i != kNoIdx};
+    ExtKey hi{hi_x, 0.0, hi_i, hi_i != kNoIdx};
+    if (lo.valid) lo.y = ys[lo_i];
+    if (hi.valid) hi.y = ys[hi_i];
+    uint32_t ubad = bad ? 1u : 0u;
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) {
+        ExtKey a = shfl_key(lo, s);
+        if (lo_better(a, lo)) lo = a;
+        ExtKey b = shfl_key(hi, s);
+        if (hi_better(b, hi)) hi = b;
+        ubad |= __shfl_xor_sync(kFull, ubad, s);
+#pragma unroll
+        for (int q = 0; q < 6; ++q) {
+            const double ov = __shfl_xor_sync(kFull, av[q], s);
+            const uint32_t oi = __shfl_xor_sync(kFull, ai[q], s);
+            if (approx_better(q, ov, oi, av[q], ai[q])) { av[q] = ov; ai[q] = oi; }
+        }
+    }
+    __shared__ PolyPartial s_w[8];
+    __shared__ bool s_last;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) {
+        s_w[warp].lo = lo;
+        s_w[warp].hi = hi;
+        s_w[warp].nonfinite = ubad;
+#pragma unroll
+        for (int q = 0; q < 6; ++q) { s_w[warp].av[q] = av[q]; s_w[warp].ai[q] = ai[q]; }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        PolyPartial r = s_w[0];
+        for (int w = 1; w < 8; ++w) {
+            if (lo_better(s_w[w].lo, r.lo)) r.lo = s_w[w].lo;
+            if (hi_better(s_w[w].hi, r.hi)) r.hi = s_w[w].hi;
+            r.nonfinite |= s_w[w].nonfinite;
+            for (int q = 0; q < 6; ++q)
+                if (approx_better(q, s_w[w].av[q], s_w[w].ai[q], r.av[q], r.ai[q])) {
+                    r.av[q] = s_w[w].av[q];
+                    r.ai[q] = s_w[w].ai[q];
+                }
+        }
+        partials[blockIdx.x] = r;
+        __threadfence();
+        s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    if (warp != 0) return;
+    ExtKey L, H;
+    L.valid = H.valid = 0;
+    uint32_t nb = 0;
+    double bv[6] = {kInf, -kInf, -kInf, -kInf, kInf, kInf};
+    uint32_t bi[6] = {kNoIdx, kNoIdx, kNoIdx, kNoIdx, kNoIdx, kNoIdx};
+    for (uint32_t b = lane; b < gridDim.x; b += 32) {
+        const PolyPartial* p = &partials[b];
+        ExtKey a, c;
+        a.x = __ldcg(&p->lo.x); a.y = __ldcg(&p->lo.y); a.idx = __ldcg(&p->lo.idx); a.valid = __ldcg(&p->lo.valid);
+        c.x = __ldcg(&p->hi.x); c.y = __ldcg(&p->hi.y); c.idx = __ldcg(&p->hi.idx); c.valid = __ldcg(&p->hi.valid);
+        if (lo_better(a, L)) L = a;
+        if (hi_better(c, H)) H = c;
+        nb |= __ldcg(&p->nonfinite);
+#pragma unroll
+        for (int q = 0; q < 6; ++q) {
+            const double ov = __ldcg(&p->av[q]);
+            const uint32_t oi = __ldcg(&p->ai[q]);
+            if (approx_better(q, ov, oi, bv[q], bi[q])) { bv[q] = ov; bi[q] = oi; }
+        }
+    }
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) {
+        ExtKey a = shfl_key(L, s);
+        if (lo_better(a, L)) L = a;
+        ExtKey b = shfl_key(H, s);
+        if (hi_better(b, H)) H = b;
+        nb |= __shfl_xor_sync(kFull, nb, s);
+#pragma unroll
+        for (int q = 0; q < 6; ++q) {
+            const double ov = __shfl_xor_sync(kFull, bv[q], s);
+            const uint32_t oi = __shfl_xor_sync(kFull, bi[q], s);
+            if (approx_better(q, ov, oi, bv[q], bi[q])) { bv[q] = ov; bi[q] = oi; }
+        }
+    }
+    if (lane != 0) return;
+    __shared__ PolyPartial s_fin;
+    s_fin.lo = L;
+    s_fin.hi = H;
+    s_fin.nonfinite = nb;
+    for (int q = 0; q < 6; ++q) { s_fin.av[q] = bv[q]; s_fin.ai[q] = bi[q]; }
+    poly_finish(s_fin, xs, ys, root);
+    side_ctr[0] = 0ull;  // the root pass's counter (another root mode may have used it)
+    *ticket = 0;
 }
 
 // ===========================================================================
@@ -739,38 +1033,40 @@ __global__ void emit_kernel(uint32_t nslots, const uint8_t* kind, const uint32_t
     }
 }
 
-// Level-1 (root) bookkeeping: the two bootstrap sides as slots, then the
-// final frame [p] S1 [q] S2 once their sizes are known.
-__global__ void root_slots_kernel(const RootInfo* root, ChildRec* slots, uint8_t* kind,
-                                  uint32_t* link, unsigned long long* side_ctr) {
+// Reference mode: the root polygon is (p, r1, q, r2) of the reference's
+// first two recursion levels (hull.cpp:228-235); an empty side contributes
+// no vertex (its r is replaced by the next vertex, emitted once).  Also
+// re-arms the fast-mode side counters of the reference-mode root partition.
+__global__ void legacy_poly_kernel(RootInfo* root, unsigned long long* side_ctr) {
     if (threadIdx.x != 0) return;
-    side_ctr[0] = side_ctr[1] = 0ull;  // fast-mode counters of the root partition
-    const RootInfo& R = *root;
-    ChildRec a, b;
-    a.px = R.px; a.py = R.py; a.qx = R.qx; a.qy = R.qy;
-    a.rx = R.r1.x; a.ry = R.r1.y; a.r_idx = R.r1.idx; a.m = R.cnt1; a.begin = 0;
-    b.px = R.qx; b.py = R.qy; b.qx = R.px; b.qy = R.py;
-    b.rx = R.r2.x; b.ry = R.r2.y; b.r_idx = R.r2.idx; b.m = R.cnt2; b.begin = R.cnt1;
-    slots[0] = a;
-    slots[1] = b;
-    // both sides are partitioned by the fused root pass whatever their size
-    kind[0] = R.cnt1 ? kInternal : kEmpty;
-    kind[1] = R.cnt2 ? kInternal : kEmpty;
-    link[0] = 0;
-    link[1] = 1;
+    side_ctr[0] = side_ctr[1] = 0ull;
+    RootInfo& R = *root;
+    RootPoly& P = R.poly;
+    const bool h1 = R.cnt1 > 0, h2 = R.cnt2 > 0;
+    P.ex[0] = R.px; P.ey[0] = R.py; P.eidx[0] = R.p_idx;
+    P.ex[1] = h1 ? R.r1.x : R.qx; P.ey[1] = h1 ? R.r1.y : R.qy; P.eidx[1] = h1 ? R.r1.idx : R.q_idx;
+    P.ex[2] = R.qx; P.ey[2] = R.qy; P.eidx[2] = R.q_idx;
+    P.ex[3] = h2 ? R.r2.x : R.px; P.ey[3] = h2 ? R.r2.y : R.py; P.eidx[3] = h2 ? R.r2.idx : R.p_idx;
+    P.nv = 4;
+    P.filter = 0;
 }
 
-__global__ void root_frame_kernel(const RootInfo* root, const uint32_t* size1,
-                                  uint32_t* start1, uint32_t* out, uint32_t* h_out) {
+// Output frame: V_0 chain(slot 0) V_1 chain(slot 1) ... with repeated
+// vertices written once (hull.cpp:259-266 for the reference-mode polygon:
+// [p] chain(S1) [q if q != p] chain(S2), chain(S) = chain(S_1) [r] chain(S_2)).
+__global__ void poly_frame_kernel(const RootInfo* root, const uint32_t* size2, uint32_t* start2,
+                                  uint32_t* out, uint32_t* h_out) {
     if (threadIdx.x != 0) return;
-    const RootInfo& R = *root;
-    const bool q_distinct = !(R.qx == R.px && R.qy == R.py);
-    out[0] = R.p_idx;
-    start1[0] = 1;
-    uint32_t pos = 1 + size1[0];
-    if (q_distinct) out[pos++] = R.q_idx;
-    start1[1] = pos;
-    *h_out = pos + size1[1];
+    const RootPoly& P = root->poly;
+    uint32_t pos = 0;
+    for (uint32_t j = 0; j < P.nv; ++j) {
+        const bool same_prev = j > 0 && P.ex[j] == P.ex[j - 1] && P.ey[j] == P.ey[j - 1];
+        const bool same_first = j > 0 && P.ex[j] == P.ex[0] && P.ey[j] == P.ey[0];
+        if (!same_prev && !same_first) out[pos++] = P.eidx[j];
+        start2[j] = pos;
+        pos += size2[j];
+    }
+    *h_out = pos;
 }
 
 // ===========================================================================
@@ -788,9 +1084,17 @@ void launch_bootstrap(const double* xs, const double* ys, uint64_t n, void* part
                                                   ticket, root);
 }
 
+void launch_poly_extremes(const double* xs, const double* ys, uint64_t n, void* partials,
+                          uint32_t* ticket, RootInfo* root, unsigned long long* side_ctr, int grid,
+                          cudaStream_t st) {
+    poly_extremes_kernel<<<grid, 256, 0, st>>>(xs, ys, n, static_cast<PolyPartial*>(partials), ticket,
+                                               root, side_ctr);
+}
+
 size_t partial_bytes(int grid) {
-    return size_t(grid) * (sizeof(RootPartial) > sizeof(ExtPartial) ? sizeof(RootPartial)
-                                                                      : sizeof(ExtPartial));
+    size_t m = sizeof(RootPartial) > sizeof(ExtPartial) ? sizeof(RootPartial) : sizeof(ExtPartial);
+    m = m > sizeof(PolyPartial) ? m : sizeof(PolyPartial);
+    return size_t(grid) * m;
 }
 
 void launch_planner(const ChildRec* slots, uint32_t nslots, SegRec* segs, FinRec* fins,
@@ -851,14 +1155,13 @@ void launch_emit(uint32_t nslots, const uint8_t* kind, const uint32_t* link,
                                    child_size, child_start, out);
 }
 
-void launch_root_slots(const RootInfo* root, ChildRec* slots, uint8_t* kind, uint32_t* link,
-                       unsigned long long* side_ctr, cudaStream_t st) {
-    root_slots_kernel<<<1, 32, 0, st>>>(root, slots, kind, link, side_ctr);
+void launch_legacy_poly(RootInfo* root, unsigned long long* side_ctr, cudaStream_t st) {
+    legacy_poly_kernel<<<1, 32, 0, st>>>(root, side_ctr);
 }
 
-void launch_root_frame(const RootInfo* root, const uint32_t* size1, uint32_t* start1,
-                       uint32_t* out, uint32_t* h_out, cudaStream_t st) {
-    root_frame_kernel<<<1, 32, 0, st>>>(root, size1, start1, out, h_out);
+void launch_poly_frame(const RootInfo* root, const uint32_t* size2, uint32_t* start2, uint32_t* out,
+                       uint32_t* h_out, cudaStream_t st) {
+    poly_frame_kernel<<<1, 32, 0, st>>>(root, size2, start2, out, h_out);
 }
 
 size_t plan_agg_bytes() { return sizeof(PlanAgg); }
@@ -871,6 +1174,11 @@ int occupancy_extremes() {
 int occupancy_bootstrap() {
     int b = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, bootstrap_argmax_kernel, 256, 0);
+    return b;
+}
+int occupancy_poly_extremes() {
+    int b = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, poly_extremes_kernel, 256, 0);
     return b;
 }
 int occupancy_finisher() {

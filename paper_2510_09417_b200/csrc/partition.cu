@@ -783,20 +783,19 @@ __device__ __forceinline__ void block_best_d(FastSmem& S, int c, double off, uin
 template <int NC>
 __device__ __forceinline__ uint32_t warp_rank(int c, uint32_t& wrun) {
     // class bits as ballots; a lane's same-class mask is V & ~(B0 ^ m0) &
-    // ~(B1 ^ m1) with m = all-ones where the lane's own bit is set
+    // ~(B1 ^ m1) & ... with m = all-ones where the lane's own bit is set
+    static_assert(NC == 2 || NC == 4 || NC == 8, "class count");
     const int lane = threadIdx.x & 31;
     const bool v = c < NC;
-    const unsigned b0 = unsigned(c) & 1u, b1 = (unsigned(c) >> 1) & 1u;
     const unsigned V = __ballot_sync(kFull, v);
-    const unsigned B0 = __ballot_sync(kFull, v && b0);
-    const unsigned m0 = 0u - b0, l0 = 0u - (unsigned(lane) & 1u);
-    unsigned M = V & ~(B0 ^ m0);
-    unsigned Mq = V & ~(B0 ^ l0);
-    if (NC == 4) {
-        const unsigned B1 = __ballot_sync(kFull, v && b1);
-        const unsigned m1 = 0u - b1, l1 = 0u - ((unsigned(lane) >> 1) & 1u);
-        M &= ~(B1 ^ m1);
-        Mq &= ~(B1 ^ l1);
+    unsigned M = V, Mq = V;
+#pragma unroll
+    for (int b = 0; (1 << b) < NC; ++b) {
+        const unsigned bit = (unsigned(c) >> b) & 1u;
+        const unsigned B = __ballot_sync(kFull, v && bit);
+        const unsigned mb = 0u - bit, lb = 0u - ((unsigned(lane) >> b) & 1u);
+        M &= ~(B ^ mb);
+        Mq &= ~(B ^ lb);
     }
     const uint32_t before = __shfl_sync(kFull, wrun, c & (NC - 1));
     wrun += (lane < NC) ? __popc(Mq) : 0u;
@@ -1185,6 +1184,270 @@ __global__ void __launch_bounds__(kCtlThreads, 3) root_partition_tma(RootArgs a)
 }
 
 // ===========================================================================
+// KB' (default): level 1 of the reference's recursion behind the octagon
+// filter, over the caller's arrays.  Per point:
+//  1. drop it if it is provably inside the octagon by the margin
+//     (RootPoly): strictly inside the shrunk inner box (4 compares), or else
+//     in the x window of its upper and lower chord (the chains L..R and R..L
+//     are x-monotone, so no other chord is within mu), inside the octagon's
+//     y range, and below both chords' rounded cross-product threshold;
+//  2. otherwise the reference's bootstrap split (hull.cpp:228-235): left of
+//     p->q -> S1, left of q->p -> S2 (kernels.hpp:60-66 expression), with the
+//     fused farthest-point search of each side (one offset o of the p->q
+//     frame: S1 minimises o, S2 minimises -o, the exact offset of its own
+//     q->p frame).
+// S1 grows forward from 0 and S2 backward from n-1 of the output buffer (one
+// packed atomic claim per tile), so the two sides can never collide.
+//
+// Pipeline (8 compute warps + 1 control warp, no CTA-wide barrier per tile):
+//  * the control warp streams tiles into a kRing4-deep shared-memory ring
+//    with cp.async.bulk (mbarrier completion);
+//  * compute warps classify tile k, post their per-warp counts (named barrier
+//    A, arrive only), run the arg-max, then store tile k-1, whose offsets
+//    the control warp published behind named barrier B — so the claim's
+//    atomic round trip overlaps a whole tile of compute;
+//  * stores re-read x and y from the ring stage, which the control warp
+//    refills only once those stores are done (tile k-2's stage at step k).
+// ===========================================================================
+constexpr int kRing4 = 4;
+
+struct RootRing4 {
+    double x[kRing4][kTile];
+    double y[kRing4][kTile];
+    unsigned long long bar[kRing4];
+};
+
+// named barriers with immediate ids (ptxas then reserves only those)
+template <int ID>
+__device__ __forceinline__ void named_sync_i(int count) {
+    asm volatile("bar.sync %0, %1;" ::"n"(ID), "r"(count) : "memory");
+}
+template <int ID>
+__device__ __forceinline__ void named_arrive_i(int count) {
+    asm volatile("bar.arrive %0, %1;" ::"n"(ID), "r"(count) : "memory");
+}
+// barrier pair (base, base+1) selected by a parity bit
+template <int BASE>
+__device__ __forceinline__ void named_sync(int par, int count) {
+    if (par) named_sync_i<BASE + 1>(count); else named_sync_i<BASE>(count);
+}
+template <int BASE>
+__device__ __forceinline__ void named_arrive(int par, int count) {
+    if (par) named_arrive_i<BASE + 1>(count); else named_arrive_i<BASE>(count);
+}
+
+__global__ void __launch_bounds__(kCtlThreads, 3) root_filtered_tma(RootArgs a) {
+    extern __shared__ __align__(128) unsigned char dsm[];
+    RootRing4& ring = *reinterpret_cast<RootRing4*>(dsm);
+    __shared__ FastSmem S;
+    __shared__ uint32_t s_wtot[2][2][kWarps];
+    __shared__ uint32_t s_org[2][2][kWarps];
+    __shared__ bool s_last;
+    const RootInfo& R = c_root;
+    const RootPoly& P = R.poly;
+    const double px = R.px, py = R.py, qx = R.qx, qy = R.qy;
+    const uint32_t n = uint32_t(a.n);
+    const uint32_t G = gridDim.x;
+    const uint32_t nfull = n / kTile;
+    const uint32_t nt = a.ntiles > blockIdx.x ? (a.ntiles - blockIdx.x + G - 1) / G : 0u;  // this CTA's tiles
+    const bool ctl = threadIdx.x >= kThreads;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t tid = threadIdx.x & (kThreads - 1);
+    auto issue = [&](uint32_t k) {
+        const uint32_t t = blockIdx.x + k * G;
+        if (t >= nfull) return;
+        const int s = int(k % kRing4);
+        mbar_expect_tx(&ring.bar[s], 2u * kTile * 8u);
+        tma_load_1d(ring.x[s], a.xs + uint64_t(t) * kTile, kTile * 8u, &ring.bar[s]);
+        tma_load_1d(ring.y[s], a.ys + uint64_t(t) * kTile, kTile * 8u, &ring.bar[s]);
+    };
+    if (threadIdx.x == kThreads) {
+        for (int s = 0; s < kRing4; ++s) mbar_init(&ring.bar[s], 1);
+        mbar_fence_init();
+        for (uint32_t k = 0; k < kRing4; ++k) issue(k);
+    }
+    __syncthreads();
+    const double adx = dsub(qx, px), ady = dsub(qy, py);  // frame of p->q (kernels.hpp:23-25)
+    const double kInf = __longlong_as_double(0x7ff0000000000000ll);
+    double bo[2] = {kInf, kInf};
+    uint32_t bi[2] = {kNoIdx, kNoIdx};
+
+    if (ctl) {
+        // ---- control warp: refills, per-tile scan + claim + store origins
+        const int c = (lane >> 3) & 1, w = lane & 7;
+        for (uint32_t k = 0; k < nt; ++k) {
+            const int par = int(k & 1);
+            named_sync<1>(par, kCtlThreads);  // counts of tile k posted; tile k-2 stored
+            if (lane == 0 && k >= 2) {
+                fence_proxy_async_smem();
+                issue(k - 2 + kRing4);  // refill tile k-2's stage
+            }
+            const uint32_t v = lane < 16 ? s_wtot[par][c][w] : 0u;
+            uint32_t incl = v;
+#pragma unroll
+            for (int d = 1; d < kWarps; d <<= 1) {
+                const uint32_t o = __shfl_up_sync(kFull, incl, d, kWarps);
+                if (w >= d) incl += o;
+            }
+            const uint32_t t0 = __shfl_sync(kFull, incl, kWarps - 1);
+            const uint32_t t1 = __shfl_sync(kFull, incl, 2 * kWarps - 1);
+            uint2 c2 = make_uint2(0u, 0u);
+            if (lane == 0 && (t0 | t1)) c2 = claim_pair(&a.side_ctr[0], t0, t1);
+            const uint32_t cl0 = __shfl_sync(kFull, c2.x, 0), cl1 = __shfl_sync(kFull, c2.y, 0);
+            if (lane < 16) {
+                const uint32_t off = (c ? cl1 : cl0) + incl - v;
+                s_org[par][c][w] = c ? n - 1u - off : off;
+            }
+            named_arrive<3>(par, kCtlThreads);  // store origins of tile k published
+        }
+    } else {
+        // ---- compute warps
+        const bool filter = P.filter != 0;
+        const double bx0 = P.bx0, bx1 = P.bx1, by0 = P.by0, by1 = P.by1;
+        bool bad = false;      // non-finite y (x was checked by K1')
+        uint32_t pcls = 0;     // previous tile: 2-bit classes
+        uint32_t prk[kItems];  // previous tile: ranks
+#pragma unroll
+        for (int i = 0; i < kItems; ++i) prk[i] = 0;
+        auto store_tile = [&](uint32_t k) {  // tile k's survivors, offsets behind barrier B
+            const int par = int(k & 1);
+            named_sync<3>(par, kCtlThreads);
+            const uint32_t t = blockIdx.x + k * G;
+            const uint32_t start = t * uint32_t(kTile) + tid;
+            const int s = int(k % kRing4);
+#pragma unroll
+            for (int i = 0; i < kItems; ++i) {
+                const int c = int((pcls >> (2 * i)) & 3u);
+                if (c < 2) {
+                    const uint32_t pos = start + uint32_t(i) * kThreads;
+                    const double x = t < nfull ? ring.x[s][i * kThreads + tid] : a.xs[pos];
+                    const double y = t < nfull ? ring.y[s][i * kThreads + tid] : a.ys[pos];
+                    const uint32_t o = s_org[par][c][warp];
+                    const uint32_t p = c ? o - prk[i] : o + prk[i];
+                    VQB_CHECK(p < a.out_cap, 14, p, a.out_cap);
+                    a.ox[p] = x;
+                    a.oy[p] = y;
+                    a.oid[p] = pos;
+                }
+            }
+        };
+        for (uint32_t k = 0; k < nt; ++k) {
+            const uint32_t t = blockIdx.x + k * G;
+            const uint32_t start = t * uint32_t(kTile) + tid;
+            const int s = int(k % kRing4);
+            double ux[kItems], uy[kItems];
+            if (t < nfull) {
+                mbar_wait(&ring.bar[s], (k / kRing4) & 1u);
+#pragma unroll
+                for (int i = 0; i < kItems; ++i) {
+                    ux[i] = ring.x[s][i * kThreads + tid];
+                    uy[i] = ring.y[s][i * kThreads + tid];
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < kItems; ++i) {
+                    const uint32_t pos = start + uint32_t(i) * kThreads;
+                    ux[i] = pos < n ? a.xs[pos] : 0.0;
+                    uy[i] = pos < n ? a.ys[pos] : 0.0;
+                }
+            }
+            uint32_t wrun = 0, cls = 0;
+            uint32_t rk[kItems];
+#pragma unroll
+            for (int i = 0; i < kItems; ++i) {
+                const uint32_t pos = start + uint32_t(i) * kThreads;
+                const double u = ux[i], w = uy[i];
+                bad |= nonfinite_bits(w);
+                bool drop = (u > bx0) & (u < bx1) & (w > by0) & (w < by1);
+                if (!drop) {  // inside by the margin w.r.t. all 8 chords
+                    drop = true;
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                        drop &= __fma_rn(P.fa[j], u, __fma_rn(P.fb[j], w, P.fc[j])) < P.ft[j];
+                }
+                drop = filter && drop;
+                int c = 2;
+                if (!drop) {
+                    const double A = dsub(px, u), B = dsub(py, w);
+                    const double Cc = dsub(qx, u), D = dsub(qy, w);
+                    const double t1 = dmul(A, D), t2 = dmul(B, Cc);
+                    c = t1 > t2 ? 0 : (t2 > t1 ? 1 : 2);  // left of p->q / of q->p
+                }
+                c = pos < n ? c : 2;
+                cls |= uint32_t(c) << (2 * i);
+                // a warp whose points all fell away skips the ranking
+                rk[i] = __any_sync(kFull, c < 2) ? warp_rank<2>(c, wrun) : 0u;
+            }
+            if (lane < 2) s_wtot[k & 1][lane][warp] = wrun;
+            named_arrive<1>(int(k & 1), kCtlThreads);
+#pragma unroll
+            for (int i = 0; i < kItems; ++i) {  // fused farthest-point search
+                const int c = int((cls >> (2 * i)) & 3u);
+                if (__any_sync(kFull, c < 2)) {
+                    const double o = lat_off(adx, ady, ux[i], uy[i]);
+                    running_best_d<2>(bo, bi, c, c ? -o : o, start + uint32_t(i) * kThreads, a.xs, a.ys);
+                }
+            }
+            if (k >= 1) store_tile(k - 1);
+            pcls = cls;
+#pragma unroll
+            for (int i = 0; i < kItems; ++i) prk[i] = rk[i];
+        }
+        if (nt >= 1) store_tile(nt - 1);
+        if (bad) atomicOr(&a.root_w->nonfinite, 1u);
+    }
+    __syncthreads();
+    // CTA partials -> last CTA writes the two level-2 slots
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+        double oo;
+        uint32_t io;
+        block_best_d<2>(S, q, bo[q], bi[q], a.xs, a.ys, oo, io);
+        if (threadIdx.x == 0)
+            a.cta_part[blockIdx.x * 2 + q] = best_from_key(io == kNoIdx ? kNoKey : 0ull, io, q ? -adx : adx,
+                                                           q ? -ady : ady, a.xs, a.ys);
+    }
+    if (threadIdx.x == 0) {
+        __threadfence();
+        s_last = atomicAdd(a.ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    if (warp < 2) {
+        const int c = warp;
+        Best b = best_none();
+        for (uint32_t kk = lane; kk < gridDim.x; kk += 32) {
+            const Best o = ldcg_best(&a.cta_part[kk * 2 + c]);
+            if (prefer(o, b)) b = o;
+        }
+        b = warp_best(b);
+        if (lane == 0) {
+            const uint2 w = read_pair(&a.side_ctr[0]);
+            const uint32_t m = c ? w.y : w.x;
+            ChildRec ch;
+            ch.px = c ? qx : px;
+            ch.py = c ? qy : py;
+            ch.qx = c ? px : qx;
+            ch.qy = c ? py : qy;
+            ch.rx = b.x;
+            ch.ry = b.y;
+            ch.r_idx = b.idx;
+            ch.m = m;
+            ch.begin = c ? uint64_t(n) - m : 0;
+            a.children[c] = ch;
+            if (c == 0) { a.root_w->cnt1 = m; a.root_w->r1 = b; }
+            else { a.root_w->cnt2 = m; a.root_w->r2 = b; }
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        a.side_ctr[0] = 0ull;  // re-arm for the next call
+        *a.ticket = 0;
+    }
+}
+
+// ===========================================================================
 // K2 fast mode with a TMA ring (8 compute warps + 1 control warp).  The
 // control warp's lane 0 maps each upcoming tile of the CTA to its segment and
 // streams x, y and the indices into a kRing-deep shared-memory ring with
@@ -1440,6 +1703,23 @@ cudaError_t launch_root_partition(const RootArgs& a, int grid, bool stable, cuda
     void* args[] = {const_cast<RootArgs*>(&a)};
     return cudaLaunchCooperativeKernel((const void*)root_partition_kernel<true>, dim3(grid),
                                        dim3(kThreads), args, 0, st);
+}
+
+cudaError_t launch_root_filtered(const RootArgs& a, int grid, cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(root_filtered_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(RootRing4)));
+        attr = true;
+    }
+    root_filtered_tma<<<grid, kCtlThreads, sizeof(RootRing4), st>>>(a);
+    return cudaGetLastError();
+}
+
+int occupancy_filtered() {
+    int b = 0;
+    cudaFuncSetAttribute(root_filtered_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(RootRing4)));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, root_filtered_tma, kCtlThreads, sizeof(RootRing4));
+    return b;
 }
 
 cudaError_t launch_level(const LevelArgs& a, bool general, bool stable, int grid, cudaStream_t st) {
