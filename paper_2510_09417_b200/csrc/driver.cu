@@ -423,7 +423,7 @@ class Engine {
     uint32_t run_root_filtered(const double* dx, const double* dy, uint64_t n, cudaStream_t st) {
         tk(0, st, [&] { launch_poly_extremes(dx, dy, n, partials_.p, &ctrs_[3], root_, side_ctr(), grid_poly_, st); });
         upload_root_consts(root_, st);
-        stats_.bytes_extremes = 8 * n + 2 * n;  // x + the 1/8 y sample
+        stats_.bytes_extremes = 8 * n + n;  // x, then x and y of the 1/16 sample
         stats_.bytes_bootstrap = 0;
         bufs_[0].ensure(n, st);
         const uint32_t ntiles_root = uint32_t((n + kTile - 1) / kTile);

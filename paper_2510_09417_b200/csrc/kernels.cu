@@ -15,6 +15,7 @@
 //   K4  size/emit kernels       in-order chain assembly    hull.cpp:59-73, 259-266
 #include <cfloat>
 #include <cstdio>
+#include <cstdlib>
 #include <cstdint>
 
 #include "common.cuh"
@@ -349,10 +350,10 @@ __global__ void __launch_bounds__(256) bootstrap_argmax_kernel(
 // K1' (default root stage): find_extremes (geometry.cpp:7-36) over every
 // point, exactly as K1 (x read for every point, y only on exact x ties),
 // plus the octagon filter's other six vertices from a sample of the input
-// (every 8th group of 256 points, x and y): max/min y, max/min x+y, max/min
+// (every 16th group of 256 points, x and y): max/min y, max/min x+y, max/min
 // x-y.  The filter only needs its vertices to be input points on two
 // x-monotone chains (checked here; otherwise no filter), not exact extremes,
-// so a sample costs 1/8 of a y pass and loses almost nothing.  Finiteness of
+// so a sample costs 1/16 of a y pass and loses almost nothing.  Finiteness of
 // x is checked here, of y by the root pass that reads every y.
 // ===========================================================================
 struct PolyPartial {
@@ -364,7 +365,7 @@ struct PolyPartial {
 };
 
 constexpr int kSampleShift = 7;  // groups of 128 pairs (256 points)
-constexpr int kSampleMask = 7;   // one group in 8 is sampled
+constexpr int kSampleMask = 15;  // one group in 16 is sampled
 
 // sampled directions, in octagon slot order 1, 2, 3, 5, 6, 7:
 // TL min x-y, T max y, TR max x+y, BR max x-y, B min y, BL min x+y
@@ -374,6 +375,66 @@ __device__ __forceinline__ bool approx_better(int a, double v, uint32_t i, doubl
     const bool maximize = (a == 1 || a == 2 || a == 3);
     if (v != vb) return maximize ? v > vb : v < vb;
     return i < ib;
+}
+
+__device__ __forceinline__ PolyPartial poly_none() {
+    const double kInf = __longlong_as_double(0x7ff0000000000000ll);
+    PolyPartial p;
+    p.lo = ExtKey{0.0, 0.0, kNoIdx, 0u};
+    p.hi = ExtKey{0.0, 0.0, kNoIdx, 0u};
+    p.nonfinite = 0u;
+    p.pad = 0u;
+    const double init[6] = {kInf, -kInf, -kInf, -kInf, kInf, kInf};
+#pragma unroll
+    for (int q = 0; q < 6; ++q) { p.av[q] = init[q]; p.ai[q] = kNoIdx; }
+    return p;
+}
+
+__device__ __forceinline__ void poly_fold(PolyPartial& a, const PolyPartial& o) {
+    if (lo_better(o.lo, a.lo)) a.lo = o.lo;
+    if (hi_better(o.hi, a.hi)) a.hi = o.hi;
+    a.nonfinite |= o.nonfinite;
+#pragma unroll
+    for (int q = 0; q < 6; ++q)
+        if (approx_better(q, o.av[q], o.ai[q], a.av[q], a.ai[q])) {
+            a.av[q] = o.av[q];
+            a.ai[q] = o.ai[q];
+        }
+}
+
+__device__ __forceinline__ PolyPartial ldcg_poly(const PolyPartial* p) {
+    PolyPartial o;
+    o.lo.x = __ldcg(&p->lo.x); o.lo.y = __ldcg(&p->lo.y); o.lo.idx = __ldcg(&p->lo.idx); o.lo.valid = __ldcg(&p->lo.valid);
+    o.hi.x = __ldcg(&p->hi.x); o.hi.y = __ldcg(&p->hi.y); o.hi.idx = __ldcg(&p->hi.idx); o.hi.valid = __ldcg(&p->hi.valid);
+    o.nonfinite = __ldcg(&p->nonfinite);
+    o.pad = 0u;
+#pragma unroll
+    for (int q = 0; q < 6; ++q) { o.av[q] = __ldcg(&p->av[q]); o.ai[q] = __ldcg(&p->ai[q]); }
+    return o;
+}
+
+// block-wide fold (warp butterflies, then warp 0 over the 8 warp results);
+// the result is valid in thread 0
+__device__ __forceinline__ PolyPartial block_reduce_poly(PolyPartial m, PolyPartial* s_w) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) {
+        PolyPartial o;
+        o.lo = shfl_key(m.lo, s);
+        o.hi = shfl_key(m.hi, s);
+        o.nonfinite = __shfl_xor_sync(kFull, m.nonfinite, s);
+#pragma unroll
+        for (int q = 0; q < 6; ++q) {
+            o.av[q] = __shfl_xor_sync(kFull, m.av[q], s);
+            o.ai[q] = __shfl_xor_sync(kFull, m.ai[q], s);
+        }
+        poly_fold(m, o);
+    }
+    if (lane == 0) s_w[warp] = m;
+    __syncthreads();
+    if (threadIdx.x == 0)
+        for (int w = 1; w < int(blockDim.x >> 5); ++w) poly_fold(m, s_w[w]);
+    return m;
 }
 
 // Last step of K1' (one thread): the root polygon, the filter's chord forms
@@ -393,12 +454,20 @@ __device__ __noinline__ void poly_finish(const PolyPartial& F, const double* __r
     uint32_t vi[8];
     vx[0] = L.x; vy[0] = L.y; vi[0] = L.idx;
     vx[4] = H.x; vy[4] = H.y; vi[4] = H.idx;
+    double gx[6], gy[6];
+#pragma unroll
+    for (int q = 0; q < 6; ++q) {  // independent loads, all in flight together
+        const uint32_t i = bi[q] != kNoIdx ? bi[q] : L.idx;
+        gx[q] = xs[i];
+        gy[q] = ys[i];
+    }
+#pragma unroll
     for (int q = 0; q < 6; ++q) {
         const int j = slot_of[q];
         ok &= bi[q] != kNoIdx;
         vi[j] = bi[q] != kNoIdx ? bi[q] : L.idx;
-        vx[j] = bi[q] != kNoIdx ? xs[bi[q]] : L.x;
-        vy[j] = bi[q] != kNoIdx ? ys[bi[q]] : L.y;
+        vx[j] = gx[q];
+        vy[j] = gy[q];
     }
     for (int j = 0; j < 8; ++j) {
         P.vx[j] = vx[j];
@@ -463,7 +532,7 @@ __device__ __noinline__ void poly_finish(const PolyPartial& F, const double* __r
     R.qx = H.x; R.qy = H.y;
 }
 
-__global__ void __launch_bounds__(256, 3) poly_extremes_kernel(const double* __restrict__ xs,
+__global__ void __launch_bounds__(256, 4) poly_extremes_kernel(const double* __restrict__ xs,
                                                             const double* __restrict__ ys, uint64_t n,
                                                             PolyPartial* partials, uint32_t* ticket,
                                                             RootInfo* root, unsigned long long* side_ctr) {
@@ -504,41 +573,62 @@ __global__ void __launch_bounds__(256, 3) poly_extremes_kernel(const double* __r
         const uint32_t npair = uint32_t(n / 2);
         const double2* x2 = reinterpret_cast<const double2*>(xs);
         const double2* y2 = reinterpret_cast<const double2*>(ys);
+        // phase 1: x of every point (find_extremes); 8 x 16 B in flight per
+        // thread (loaded HBM latency is ~2.5 us at full bandwidth)
+        constexpr int U = 2 * kStreamUnroll;
+        const uint32_t np1 = npair;
         uint32_t j = tid;
-        for (; j + (kStreamUnroll - 1) * stride < npair; j += kStreamUnroll * stride) {
-            double2 v[kStreamUnroll], w[kStreamUnroll];
-            // the sample test is warp-uniform (32 consecutive pairs); y loads
-            // are issued with the x loads so both are in flight together
+        for (; j + (U - 1) * stride < np1; j += U * stride) {
+            double2 v[U];
 #pragma unroll
-            for (int u = 0; u < kStreamUnroll; ++u) {
-                const uint32_t jj = j + u * stride;
-                v[u] = __ldcs(&x2[jj]);
-                if (((jj >> kSampleShift) & kSampleMask) == 0) w[u] = __ldcs(&y2[jj]);
-            }
+            for (int u = 0; u < U; ++u) v[u] = __ldcs(&x2[j + u * stride]);
 #pragma unroll
-            for (int u = 0; u < kStreamUnroll; ++u) {
-                const uint32_t jj = j + u * stride;
-                visit_x(2 * jj, v[u].x);
-                visit_x(2 * jj + 1, v[u].y);
-                if (((jj >> kSampleShift) & kSampleMask) == 0) {
-                    visit_xy(2 * jj, v[u].x, w[u].x);
-                    visit_xy(2 * jj + 1, v[u].y, w[u].y);
-                }
+            for (int u = 0; u < U; ++u) {
+                visit_x(2 * (j + u * stride), v[u].x);
+                visit_x(2 * (j + u * stride) + 1, v[u].y);
             }
         }
-        for (; j < npair; j += stride) {
+        for (; j < np1; j += stride) {
             const double2 v = __ldcs(&x2[j]);
             visit_x(2 * j, v.x);
             visit_x(2 * j + 1, v.y);
-            if (((j >> kSampleShift) & kSampleMask) == 0) {
-                const double2 w = __ldcs(&y2[j]);
-                visit_xy(2 * j, v.x, w.x);
-                visit_xy(2 * j + 1, v.y, w.y);
-            }
         }
         if ((n & 1) && tid == 0) {
             visit_x(uint32_t(n - 1), xs[n - 1]);
             visit_xy(uint32_t(n - 1), xs[n - 1], ys[n - 1]);
+        }
+        // phase 2: x and y of the sampled groups (every 16th run of 128 pairs)
+        const uint32_t ngroups = (npair + (1u << kSampleShift) - 1) >> kSampleShift;
+        const uint32_t nsg = (ngroups + kSampleMask) / (kSampleMask + 1);
+        const uint32_t nsample = nsg << kSampleShift;
+        auto pair_of = [&](uint32_t m) {
+            return ((m >> kSampleShift) * (kSampleMask + 1) << kSampleShift) | (m & ((1u << kSampleShift) - 1));
+        };
+        uint32_t m = tid;
+        for (; m + (kStreamUnroll - 1) * stride < nsample; m += kStreamUnroll * stride) {
+            double2 v[kStreamUnroll], w[kStreamUnroll];
+            uint32_t jj[kStreamUnroll];
+#pragma unroll
+            for (int u = 0; u < kStreamUnroll; ++u) {
+                jj[u] = pair_of(m + u * stride);
+                const uint32_t q = jj[u] < npair ? jj[u] : 0u;
+                v[u] = __ldcs(&x2[q]);
+                w[u] = __ldcs(&y2[q]);
+            }
+#pragma unroll
+            for (int u = 0; u < kStreamUnroll; ++u) {
+                if (jj[u] >= npair) continue;
+                visit_xy(2 * jj[u], v[u].x, w[u].x);
+                visit_xy(2 * jj[u] + 1, v[u].y, w[u].y);
+            }
+        }
+        for (; m < nsample; m += stride) {
+            const uint32_t q = pair_of(m);
+            if (q >= npair) continue;
+            const double2 v = __ldcs(&x2[q]);
+            const double2 w = __ldcs(&y2[q]);
+            visit_xy(2 * q, v.x, w.x);
+            visit_xy(2 * q + 1, v.y, w.y);
         }
     } else {
         for (uint32_t i = tid; i < n; i += stride) {
@@ -546,49 +636,19 @@ __global__ void __launch_bounds__(256, 3) poly_extremes_kernel(const double* __r
             if (((i >> (kSampleShift + 1)) & kSampleMask) == 0) visit_xy(i, xs[i], ys[i]);
         }
     }
-    // reductions: warp -> CTA partial -> last CTA
-    ExtKey lo{lo_x, 0.0, lo_i, lo_i != kNoIdx};
-    ExtKey hi{hi_x, 0.0, hi_i, hi_i != kNoIdx};
-    if (lo.valid) lo.y = ys[lo_i];
-    if (hi.valid) hi.y = ys[hi_i];
-    uint32_t ubad = bad ? 1u : 0u;
+    // reductions: thread -> CTA partial -> (last CTA, all threads) -> final
+    PolyPartial mine;
+    mine.lo = ExtKey{lo_x, 0.0, lo_i, lo_i != kNoIdx};
+    mine.hi = ExtKey{hi_x, 0.0, hi_i, hi_i != kNoIdx};
+    if (mine.lo.valid) mine.lo.y = ys[lo_i];
+    if (mine.hi.valid) mine.hi.y = ys[hi_i];
+    mine.nonfinite = bad ? 1u : 0u;
 #pragma unroll
-    for (int s = 16; s > 0; s >>= 1) {
-        ExtKey a = shfl_key(lo, s);
-        if (lo_better(a, lo)) lo = a;
-        ExtKey b = shfl_key(hi, s);
-        if (hi_better(b, hi)) hi = b;
-        ubad |= __shfl_xor_sync(kFull, ubad, s);
-#pragma unroll
-        for (int q = 0; q < 6; ++q) {
-            const double ov = __shfl_xor_sync(kFull, av[q], s);
-            const uint32_t oi = __shfl_xor_sync(kFull, ai[q], s);
-            if (approx_better(q, ov, oi, av[q], ai[q])) { av[q] = ov; ai[q] = oi; }
-        }
-    }
+    for (int q = 0; q < 6; ++q) { mine.av[q] = av[q]; mine.ai[q] = ai[q]; }
     __shared__ PolyPartial s_w[8];
     __shared__ bool s_last;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (lane == 0) {
-        s_w[warp].lo = lo;
-        s_w[warp].hi = hi;
-        s_w[warp].nonfinite = ubad;
-#pragma unroll
-        for (int q = 0; q < 6; ++q) { s_w[warp].av[q] = av[q]; s_w[warp].ai[q] = ai[q]; }
-    }
-    __syncthreads();
+    PolyPartial r = block_reduce_poly(mine, s_w);
     if (threadIdx.x == 0) {
-        PolyPartial r = s_w[0];
-        for (int w = 1; w < 8; ++w) {
-            if (lo_better(s_w[w].lo, r.lo)) r.lo = s_w[w].lo;
-            if (hi_better(s_w[w].hi, r.hi)) r.hi = s_w[w].hi;
-            r.nonfinite |= s_w[w].nonfinite;
-            for (int q = 0; q < 6; ++q)
-                if (approx_better(q, s_w[w].av[q], s_w[w].ai[q], r.av[q], r.ai[q])) {
-                    r.av[q] = s_w[w].av[q];
-                    r.ai[q] = s_w[w].ai[q];
-                }
-        }
         partials[blockIdx.x] = r;
         __threadfence();
         s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
@@ -596,47 +656,14 @@ __global__ void __launch_bounds__(256, 3) poly_extremes_kernel(const double* __r
     __syncthreads();
     if (!s_last) return;
     __threadfence();
-    if (warp != 0) return;
-    ExtKey L, H;
-    L.valid = H.valid = 0;
-    uint32_t nb = 0;
-    double bv[6] = {kInf, -kInf, -kInf, -kInf, kInf, kInf};
-    uint32_t bi[6] = {kNoIdx, kNoIdx, kNoIdx, kNoIdx, kNoIdx, kNoIdx};
-    for (uint32_t b = lane; b < gridDim.x; b += 32) {
-        const PolyPartial* p = &partials[b];
-        ExtKey a, c;
-        a.x = __ldcg(&p->lo.x); a.y = __ldcg(&p->lo.y); a.idx = __ldcg(&p->lo.idx); a.valid = __ldcg(&p->lo.valid);
-        c.x = __ldcg(&p->hi.x); c.y = __ldcg(&p->hi.y); c.idx = __ldcg(&p->hi.idx); c.valid = __ldcg(&p->hi.valid);
-        if (lo_better(a, L)) L = a;
-        if (hi_better(c, H)) H = c;
-        nb |= __ldcg(&p->nonfinite);
-#pragma unroll
-        for (int q = 0; q < 6; ++q) {
-            const double ov = __ldcg(&p->av[q]);
-            const uint32_t oi = __ldcg(&p->ai[q]);
-            if (approx_better(q, ov, oi, bv[q], bi[q])) { bv[q] = ov; bi[q] = oi; }
-        }
-    }
-#pragma unroll
-    for (int s = 16; s > 0; s >>= 1) {
-        ExtKey a = shfl_key(L, s);
-        if (lo_better(a, L)) L = a;
-        ExtKey b = shfl_key(H, s);
-        if (hi_better(b, H)) H = b;
-        nb |= __shfl_xor_sync(kFull, nb, s);
-#pragma unroll
-        for (int q = 0; q < 6; ++q) {
-            const double ov = __shfl_xor_sync(kFull, bv[q], s);
-            const uint32_t oi = __shfl_xor_sync(kFull, bi[q], s);
-            if (approx_better(q, ov, oi, bv[q], bi[q])) { bv[q] = ov; bi[q] = oi; }
-        }
-    }
-    if (lane != 0) return;
+    // every thread folds its share of the CTA partials (independent loads)
+    PolyPartial acc = poly_none();
+    for (uint32_t c = threadIdx.x; c < gridDim.x; c += blockDim.x) poly_fold(acc, ldcg_poly(&partials[c]));
+    __syncthreads();  // s_w reuse
+    r = block_reduce_poly(acc, s_w);
+    if (threadIdx.x != 0) return;
     __shared__ PolyPartial s_fin;
-    s_fin.lo = L;
-    s_fin.hi = H;
-    s_fin.nonfinite = nb;
-    for (int q = 0; q < 6; ++q) { s_fin.av[q] = bv[q]; s_fin.ai[q] = bi[q]; }
+    s_fin = r;
     poly_finish(s_fin, xs, ys, root);
     side_ctr[0] = 0ull;  // the root pass's counter (another root mode may have used it)
     *ticket = 0;
