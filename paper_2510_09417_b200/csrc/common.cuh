@@ -117,6 +117,14 @@ __device__ __forceinline__ bool left_diff(double pdx, double pdy, double qdx, do
     return dmul(pdx, qdy) > dmul(pdy, qdx);
 }
 
+// Programmatic dependent launch: a kernel waits for its stream predecessor
+// to complete (and its writes to be visible) before touching memory, then at
+// once lets its own successor be launched, so launch latency and CTA
+// placement of the next kernel overlap this one (no-ops without the launch
+// attribute).  Must be the first statement of every kernel launched with
+// pdl_launch.
+#define VQB_PDL() asm volatile("griddepcontrol.wait;\n\tgriddepcontrol.launch_dependents;" ::: "memory")
+
 // Inf or NaN (exponent all ones), by the bits
 __device__ __forceinline__ bool nonfinite_bits(double v) {
     return (__double2hiint(v) & 0x7ff00000) == 0x7ff00000;
@@ -508,3 +516,29 @@ __device__ void lookback_agg(uint32_t tile, uint32_t first, const Agg<NC>& local
 }
 
 }  // namespace vqb
+
+#if defined(__CUDACC__)
+#include <cstdlib>
+namespace vqb {
+inline bool pdl_enabled() {
+    static const bool on = getenv("VQB_NO_PDL") == nullptr;
+    return on;
+}
+// <<<grid, block, smem, st>>> with programmatic stream serialization
+template <typename... KArgs, typename... Args>
+inline cudaError_t pdl_launch(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
+}  // namespace vqb
+#endif

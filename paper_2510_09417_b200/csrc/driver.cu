@@ -164,106 +164,116 @@ class Engine {
         // finiteness verdict, octagon verdict, sizes for the byte accounting
         ck(cudaMemcpyAsync(h_root_, root_, sizeof(RootInfo), cudaMemcpyDeviceToHost, st), "d2h root");
 
-        // ---- levels
+        // ---- levels.  Every kernel of a level reads its counts from the
+        // level's LevelInfo on the device (the planner derives its slot count
+        // and chain base from the previous level's), and every table is sized
+        // by host-side bounds, so the host queues kLevelBatch levels at a time
+        // and synchronizes once per batch to learn whether the recursion has
+        // ended.  Levels queued past the end find zero slots and do nothing.
+        bufs_[0].ensure(n, st);
+        bufs_[1].ensure(n, st);
+        chain_.ensure(n * 4 + 4, st, true);
+        const uint64_t seg_lim = n / (uint64_t(kFinMax) + 1);  // internal segments hold > kFinMax points
+        uint32_t S = nslots;  // slot bound of the level being queued
         int in = 0;
-        uint64_t fin_base = 0;
         int lvl = 2;
-        level_fin_base_.assign(4, 0);
-        while (true) {
-            if (lvl == 2) note_slots(2, nslots);
-            LevelTables& T = level(lvl);
-            T.kind.ensure(nslots, st);
-            T.link.ensure(size_t(nslots) * 4, st);
-            T.size.ensure(size_t(nslots) * 4, st);
-            T.start.ensure(size_t(nslots) * 4, st);
-            T.segs.ensure(size_t(nslots) * sizeof(SegRec), st);
-            T.fins.ensure(size_t(nslots) * sizeof(FinRec), st);
-            const uint32_t nchunks = (nslots + 1023) / 1024;
-            ensure_lookback(nchunks, st);
-            segaux_.ensure(segaux_bytes(nslots), st);
-            info_.ensure(size_t(lvl + 1) * sizeof(LevelInfo), st, true);
-            LevelInfo* dinfo = info_.as<LevelInfo>() + lvl;
-            {
-                const uint32_t ep = next_epoch();
-                tk(5, st, [&] {
-                    launch_planner(T.slots.as<ChildRec>(), nslots, T.segs.as<SegRec>(), T.fins.as<FinRec>(),
-                                   T.kind.as<uint8_t>(), T.link.as<uint32_t>(), dinfo, fin_base,
-                                   flags_.as<uint32_t>(), aggs_.p, incs_.p, ep, &ctrs_[2],
-                                   seg_pcnt(), seg_done(nslots), seg_ctr(nslots), sms_ * 4, st);
+        lmax_ = -1;
+        while (lmax_ < 0) {
+            const int first = lvl;
+            for (int b = 0; b < kLevelBatch; ++b, ++lvl) {
+                const uint32_t nseg_b = uint32_t(std::min<uint64_t>(S, seg_lim));
+                const uint32_t ntiles_b = uint32_t(n / kTile) + nseg_b + 1;
+                const uint32_t S1 = std::max<uint32_t>(S, 1);
+                LevelTables& T = level(lvl);
+                T.kind.ensure(S1, st);
+                T.link.ensure(size_t(S1) * 4, st);
+                T.size.ensure(size_t(S1) * 4, st);
+                T.start.ensure(size_t(S1) * 4, st);
+                T.segs.ensure(size_t(S1) * sizeof(SegRec), st);
+                T.fins.ensure(size_t(S1) * sizeof(FinRec), st);
+                T.fin_count.ensure(size_t(S1) * 4, st);
+                ensure_lookback(std::max<uint32_t>((S1 + 1023) / 1024, ntiles_b), st);
+                segaux_.ensure(segaux_bytes(S1), st);
+                info_.ensure(size_t(lvl + 1) * sizeof(LevelInfo), st, true);
+                LevelInfo* dinfo = info_.as<LevelInfo>() + lvl;
+                const LevelInfo* dprev = lvl == 2 ? nullptr : info_.as<LevelInfo>() + (lvl - 1);
+                {
+                    const uint32_t ep = next_epoch();
+                    tk(5, st, [&] {
+                        launch_planner(T.slots.as<ChildRec>(), S, dprev, S, T.segs.as<SegRec>(), T.fins.as<FinRec>(),
+                                       T.kind.as<uint8_t>(), T.link.as<uint32_t>(), dinfo, flags_.as<uint32_t>(),
+                                       aggs_.p, incs_.p, ep, &ctrs_[2], seg_pcnt(), seg_done(S1), seg_ctr(S1),
+                                       sms_ * 4, st);
+                    });
+                }
+                // finisher: every segment of <= kFinMax points, whole subtrees
+                tk(4, st, [&] {
+                    launch_finisher(T.fins.as<FinRec>(), dinfo, bufs_[in].x.as<double>(), bufs_[in].y.as<double>(),
+                                    bufs_[in].id.as<uint32_t>(), chain_.as<uint32_t>(), T.fin_count.as<uint32_t>(),
+                                    S1, sms_ * occ_fin_, st);
                 });
+                // K2 over all internal segments of this level
+                const int out = in ^ 1;
+                tile_seg_.ensure(size_t(ntiles_b) * 4, st);
+                part_.ensure(size_t(ntiles_b) * 2 * sizeof(Best), st);
+                LevelTables& Tn = level(lvl + 1);
+                Tn.slots.ensure(size_t(2) * std::max<uint32_t>(nseg_b, 1) * sizeof(ChildRec), st);
+                LevelTables& Tc = level(lvl);
+                tk(5, st, [&] { launch_tilemap(Tc.segs.as<SegRec>(), dinfo, tile_seg_.as<uint32_t>(), ntiles_b, st); });
+                {
+                    const int grid = std::max(1, std::min<int>(int(ntiles_b), sms_ * (stable_ ? occ_level_stable_ : occ_level_)));
+                    LevelArgs la;
+                    la.gx = dx; la.gy = dy;
+                    la.segs = Tc.segs.as<SegRec>(); la.tile_seg = tile_seg_.as<uint32_t>(); la.info = dinfo;
+                    la.ix = bufs_[in].x.as<double>(); la.iy = bufs_[in].y.as<double>(); la.iid = bufs_[in].id.as<uint32_t>();
+                    la.ox = bufs_[out].x.as<double>(); la.oy = bufs_[out].y.as<double>(); la.oid = bufs_[out].id.as<uint32_t>();
+                    la.in_cap = bufs_[in].x.cap / 8; la.out_cap = bufs_[out].x.cap / 8;
+                    la.status_cap = status_.cap / sizeof(Status); la.part_cap = part_.cap / sizeof(Best);
+                    la.children_cap = Tn.slots.cap / sizeof(ChildRec); la.segs_cap = S1;
+                    la.status = status_.as<Status>(); la.epoch = next_epoch(); la.ctr = &ctrs_[1];
+                    la.tile_part = part_.as<Best>();
+                    la.seg_pcnt = seg_pcnt(); la.seg_done = seg_done(S1); la.seg_ctr = seg_ctr(S1);
+                    la.children = Tn.slots.as<ChildRec>();
+                    tk(3, st, [&] { ck(launch_level(la, false, stable_, grid, st), "level launch"); });
+                }
+                in = out;
+                S = 2 * nseg_b;
             }
-            ck(cudaMemcpyAsync(h_info_, dinfo, sizeof(LevelInfo), cudaMemcpyDeviceToHost, st), "d2h info");
-            VQB_TRACE("hull: level %d sync", lvl);
+            ck(cudaMemcpyAsync(h_info_, info_.as<LevelInfo>() + (lvl - 1), sizeof(LevelInfo),
+                               cudaMemcpyDeviceToHost, st), "d2h info");
+            VQB_TRACE("hull: levels %d..%d sync", first, lvl - 1);
             ck(cudaStreamSynchronize(st), "level sync");
-            VQB_TRACE("hull: level %d synced", lvl);
-            const LevelInfo li = *h_info_;
-            if (lvl == 2 && h_root_->nonfinite) {
+            if (first == 2 && h_root_->nonfinite) {
                 end_timing(st);
                 ck(cudaStreamSynchronize(st), "sync");
                 return VQHULL_EINVAL;
             }
-            // every point of this level's slots was written (20 B) by the
-            // previous partition (KB for level 2, K2 otherwise)
-            const uint64_t written = uint64_t(li.out_total) + li.fin_total + li.nleaf;
-            if (lvl == 2) stats_.survivors_root = written;
-            else stats_.bytes_levels += 20 * written;
-            // finisher
-            if (level_fin_base_.size() <= size_t(lvl)) level_fin_base_.resize(lvl + 1, 0);
-            level_fin_base_[lvl] = fin_base;
-            T.fin_count.ensure(size_t(std::max<uint32_t>(li.nfin, 1)) * 4, st);
-            if (li.nfin) {
-                chain_.ensure((fin_base + li.fin_total) * 4, st, true);
-                tk(4, st, [&] {
-                    launch_finisher(T.fins.as<FinRec>(), dinfo, bufs_[in].x.as<double>(), bufs_[in].y.as<double>(),
-                                    bufs_[in].id.as<uint32_t>(), chain_.as<uint32_t>(),
-                                    T.fin_count.as<uint32_t>(), li.nfin, sms_ * occ_fin_, st);
-                });
-                stats_.finisher_points += li.fin_total;
-                stats_.finisher_segments += li.nfin;
-                stats_.bytes_finisher += uint64_t(li.fin_total) * 20 + uint64_t(li.fin_total) * 4;
-                fin_base += li.fin_total;
-            }
-            if (li.nseg == 0) {
-                lmax_ = lvl;
-                break;
-            }
-            if (uint64_t(lvl) > n + 8) {  // every level sheds >= 1 point per segment
+            if (h_info_->nseg == 0) {
+                // the recursion ended in this batch: fetch all level infos
+                hinfo_.resize(lvl);
+                ck(cudaMemcpyAsync(hinfo_.data() + 2, info_.as<LevelInfo>() + 2, sizeof(LevelInfo) * (lvl - 2),
+                                   cudaMemcpyDeviceToHost, st), "d2h infos");
+                ck(cudaStreamSynchronize(st), "info sync");
+                for (int l = 2; l < lvl; ++l)
+                    if (hinfo_[l].nseg == 0) { lmax_ = l; break; }
+            } else if (uint64_t(lvl) > n + 8) {  // every level sheds >= 1 point per segment
                 g_last_error = "recursion did not shrink (internal error)";
                 throw CudaError{cudaErrorUnknown};
             }
-            // K2 over all segments of this level
-            const int out = in ^ 1;
-            bufs_[out].ensure(std::max<uint64_t>(li.out_total, 1), st);
-            tile_seg_.ensure(size_t(li.ntiles) * 4, st);
-            ensure_lookback(li.ntiles, st);
-            part_.ensure(size_t(li.ntiles) * 2 * sizeof(Best), st);
-            LevelTables& Tn = level(lvl + 1);
-            Tn.slots.ensure(size_t(2) * li.nseg * sizeof(ChildRec), st);
-            LevelTables& Tc = level(lvl);
-            tk(5, st, [&] { launch_tilemap(Tc.segs.as<SegRec>(), dinfo, tile_seg_.as<uint32_t>(), li.ntiles, st); });
-            {
-                const int grid = std::max(1, std::min<int>(int(li.ntiles), sms_ * (stable_ ? occ_level_stable_ : occ_level_)));
-                LevelArgs la;
-                la.gx = dx; la.gy = dy;
-                la.segs = Tc.segs.as<SegRec>(); la.tile_seg = tile_seg_.as<uint32_t>(); la.info = dinfo;
-                la.ix = bufs_[in].x.as<double>(); la.iy = bufs_[in].y.as<double>(); la.iid = bufs_[in].id.as<uint32_t>();
-                la.ox = bufs_[out].x.as<double>(); la.oy = bufs_[out].y.as<double>(); la.oid = bufs_[out].id.as<uint32_t>();
-                la.in_cap = bufs_[in].x.cap / 8; la.out_cap = bufs_[out].x.cap / 8;
-                la.status_cap = status_.cap / sizeof(Status); la.part_cap = part_.cap / sizeof(Best);
-                la.children_cap = Tn.slots.cap / sizeof(ChildRec); la.segs_cap = nslots;
-                la.status = status_.as<Status>(); la.epoch = next_epoch(); la.ctr = &ctrs_[1];
-                la.tile_part = part_.as<Best>();
-                la.seg_pcnt = seg_pcnt(); la.seg_done = seg_done(nslots); la.seg_ctr = seg_ctr(nslots);
-                la.children = Tn.slots.as<ChildRec>();
-                tk(3, st, [&] { ck(launch_level(la, false, stable_, grid, st), "level launch"); });
-            }
+        }
+        for (int l = 2; l <= lmax_; ++l) {
+            const LevelInfo& li = hinfo_[l];
+            // every point of this level's slots was written (20 B) by the
+            // previous partition (KB for level 2, K2 otherwise)
+            const uint64_t written = uint64_t(li.out_total) + li.fin_total + li.nleaf;
+            if (l == 2) stats_.survivors_root = written;
+            else stats_.bytes_levels += 20 * written;
+            stats_.finisher_points += li.fin_total;
+            stats_.finisher_segments += li.nfin;
+            stats_.bytes_finisher += uint64_t(li.fin_total) * 20 + uint64_t(li.fin_total) * 4;
             stats_.segments += li.nseg;
             stats_.level_points += li.out_total;
             stats_.bytes_levels += uint64_t(li.out_total) * 20;  // reads; writes counted next level
-            nslots = 2 * li.nseg;
-            note_slots(lvl + 1, nslots);
-            in = out;
-            ++lvl;
         }
         stats_.levels = uint32_t(lmax_);
         stats_.bytes_root_partition = 16 * n + 20 * stats_.survivors_root;
@@ -273,7 +283,7 @@ class Engine {
         // ---- emission: bottom-up sizes, root frame, top-down starts
         for (int l = lmax_; l >= 2; --l) {
             LevelTables& T = level(l);
-            const uint32_t ns = slot_count(l);
+            const uint32_t ns = hinfo_[l].nslots;
             const uint32_t* child_size = (l < lmax_) ? level(l + 1).size.as<uint32_t>() : nullptr;
             tk(5, st, [&] {
                 launch_size(ns, T.kind.as<uint8_t>(), T.link.as<uint32_t>(), T.fin_count.as<uint32_t>(),
@@ -286,7 +296,7 @@ class Engine {
         });
         for (int l = 2; l <= lmax_; ++l) {
             LevelTables& T = level(l);
-            const uint32_t ns = slot_count(l);
+            const uint32_t ns = hinfo_[l].nslots;
             const bool has_child = l < lmax_;
             tk(5, st, [&] {
                 launch_emit(ns, T.kind.as<uint8_t>(), T.link.as<uint32_t>(), T.slots.as<ChildRec>(),
@@ -477,7 +487,6 @@ class Engine {
         if (levels_.size() <= size_t(l)) levels_.resize(l + 1);
         return levels_[l];
     }
-    uint32_t slot_count(int l) const { return l < int(slot_counts_.size()) ? slot_counts_[l] : 0; }
 
     uint32_t next_epoch() {
         ++epoch_;
@@ -507,7 +516,6 @@ class Engine {
         std::memset(&stats_, 0, sizeof stats_);
         stats_.n = n;
         timed_.clear();
-        slot_counts_.assign(3, 0);
         lmax_ = 2;
     }
 
@@ -579,13 +587,6 @@ class Engine {
         stats_.timing_valid = 1;
     }
 
-   public:
-    // called by hull() after each level to remember slot counts for emission
-    void note_slots(int l, uint32_t ns) {
-        if (slot_counts_.size() <= size_t(l)) slot_counts_.resize(l + 1, 0);
-        slot_counts_[l] = ns;
-    }
-
    private:
     int dev_ = 0;
     int sms_ = 148;
@@ -621,9 +622,9 @@ class Engine {
     PointBuf bufs_[2];
     PointBuf in_;
     std::deque<LevelTables> levels_;  // deque: references stay valid on growth
-    std::vector<uint32_t> slot_counts_;
-    std::vector<uint64_t> level_fin_base_;
+    std::vector<LevelInfo> hinfo_;  // host copies of the level infos (after the last batch)
     int lmax_ = 2;
+    static constexpr int kLevelBatch = 4;  // levels queued per host synchronization
     uint32_t epoch_ = 0;
     uint32_t launches_ = 0;
     bool timing_ = false;

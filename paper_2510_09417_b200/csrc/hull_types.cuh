@@ -104,7 +104,7 @@ struct LevelInfo {
     uint32_t out_total;   // points handed to the level kernel
     uint32_t fin_total;   // points handed to the finisher
     uint32_t nleaf;
-    uint32_t pad;
+    uint32_t fin_base;    // first chain entry of this level's finisher segments
 };
 
 // Look-back status of one tile (one side) of the partition kernels: two

@@ -71,6 +71,7 @@ __global__ void __launch_bounds__(256) extremes_kernel(const double* __restrict_
                                                        const double* __restrict__ ys,
                                                        uint64_t n, ExtPartial* partials,
                                                        uint32_t* ticket, RootInfo* root) {
+    VQB_PDL();
     const double kInf = __longlong_as_double(0x7ff0000000000000ll);
     // running extremes (x, index); the first index wins among exact x ties
     // unless y decides (checked on the slow path)
@@ -206,6 +207,7 @@ struct RootPartial {
 __global__ void __launch_bounds__(256) bootstrap_argmax_kernel(
     const double* __restrict__ xs, const double* __restrict__ ys, uint64_t n,
     RootPartial* partials, uint32_t* ticket, RootInfo* root) {
+    VQB_PDL();
     const double px = root->px, py = root->py, qx = root->qx, qy = root->qy;
     const double adx = dsub(qx, px), ady = dsub(qy, py);  // frame of p->q (kernels.hpp:23-25)
     const double kInf = __longlong_as_double(0x7ff0000000000000ll);
@@ -536,6 +538,7 @@ __global__ void __launch_bounds__(256, 4) poly_extremes_kernel(const double* __r
                                                             const double* __restrict__ ys, uint64_t n,
                                                             PolyPartial* partials, uint32_t* ticket,
                                                             RootInfo* root, unsigned long long* side_ctr) {
+    VQB_PDL();
     const double kInf = __longlong_as_double(0x7ff0000000000000ll);
     double lo_x = kInf, hi_x = -kInf;
     uint32_t lo_i = kNoIdx, hi_i = kNoIdx;
@@ -680,14 +683,13 @@ constexpr int kPlanChunk = kThreads * kPlanPer;
 
 struct PlanArgs {
     const ChildRec* slots;
-    uint32_t nslots;
-    uint32_t nchunks;
+    uint32_t nslots;      // level 2 only; deeper levels: 2 * prev->nseg
+    const LevelInfo* prev;
     SegRec* segs;
     FinRec* fins;
     uint8_t* kind;
     uint32_t* link;
     LevelInfo* info;
-    uint64_t fin_chain_base;  // global offset of this level's finisher chains
     uint32_t* flags;
     PlanAgg* aggs;
     PlanAgg* incs;
@@ -703,19 +705,32 @@ __device__ __forceinline__ uint8_t kind_of(uint32_t m) {
 }
 
 __global__ void __launch_bounds__(kThreads) planner_kernel(PlanArgs a) {
+    VQB_PDL();
     __shared__ PlanAgg s_w[kWarps];
     __shared__ PlanAgg s_excl;
     __shared__ uint32_t s_chunk;
+    // the level's size comes from the previous level on the device, so the
+    // host can queue several levels without waiting for their counts
+    const uint32_t nslots = a.prev ? 2u * a.prev->nseg : a.nslots;
+    const uint32_t nchunks = (nslots + kPlanChunk - 1) / kPlanChunk;
+    const uint64_t fin_chain_base = a.prev ? uint64_t(a.prev->fin_base) + a.prev->fin_total : 0ull;
+    if (nslots == 0 && blockIdx.x == 0 && threadIdx.x == 0) {
+        LevelInfo li;
+        li.nslots = 0; li.nseg = 0; li.nfin = 0; li.ntiles = 0;
+        li.out_total = 0; li.fin_total = 0; li.nleaf = 0;
+        li.fin_base = uint32_t(fin_chain_base);
+        *a.info = li;
+    }
     while (true) {
         __syncthreads();
         if (threadIdx.x == 0) {
             const uint32_t c = atomicAdd(a.ctr, 1u);
             s_chunk = c;
-            if (c >= a.nchunks && c == a.nchunks + gridDim.x - 1) *a.ctr = 0;
+            if (c >= nchunks && c == nchunks + gridDim.x - 1) *a.ctr = 0;
         }
         __syncthreads();
         const uint32_t chunk = s_chunk;
-        if (chunk >= a.nchunks) break;
+        if (chunk >= nchunks) break;
         const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
         // blocked: thread owns kPlanPer consecutive slots
         const uint64_t s0 = uint64_t(chunk) * kPlanChunk + uint64_t(threadIdx.x) * kPlanPer;
@@ -725,8 +740,8 @@ __global__ void __launch_bounds__(kThreads) planner_kernel(PlanArgs a) {
 #pragma unroll
         for (int k = 0; k < kPlanPer; ++k) {
             const uint64_t s = s0 + k;
-            m[k] = s < a.nslots ? a.slots[s].m : 0u;
-            const uint8_t kd = s < a.nslots ? kind_of(m[k]) : kEmpty;
+            m[k] = s < nslots ? a.slots[s].m : 0u;
+            const uint8_t kd = s < nslots ? kind_of(m[k]) : kEmpty;
             mine.nseg += kd == kInternal;
             mine.nfin += kd == kFin;
             mine.leaf += kd == kLeaf;
@@ -756,18 +771,18 @@ __global__ void __launch_bounds__(kThreads) planner_kernel(PlanArgs a) {
             const PlanAgg ex = lookback<PlanAgg>(chunk, 0u, tot, a.flags, a.aggs, a.incs, a.epoch);
             if (threadIdx.x == 0) {
                 s_excl = ex;
-                if (chunk == a.nchunks - 1) {
+                if (chunk == nchunks - 1) {
                     PlanAgg all = ex;
                     pl_combine(all, tot);
                     LevelInfo li;
-                    li.nslots = a.nslots;
+                    li.nslots = nslots;
                     li.nseg = all.nseg;
                     li.nfin = all.nfin;
                     li.ntiles = all.ntiles;
                     li.out_total = all.out;
                     li.fin_total = all.fin;
                     li.nleaf = all.leaf;
-                    li.pad = 0;
+                    li.fin_base = uint32_t(fin_chain_base);
                     *a.info = li;
                 }
             }
@@ -783,7 +798,7 @@ __global__ void __launch_bounds__(kThreads) planner_kernel(PlanArgs a) {
 #pragma unroll
         for (int k = 0; k < kPlanPer; ++k) {
             const uint64_t s = s0 + k;
-            if (s >= a.nslots) break;
+            if (s >= nslots) break;
             const uint8_t kd = kind_of(m[k]);
             a.kind[s] = kd;
             if (kd == kInternal) {
@@ -810,7 +825,7 @@ __global__ void __launch_bounds__(kThreads) planner_kernel(PlanArgs a) {
             } else if (kd == kFin) {
                 FinRec f;
                 f.c = a.slots[s];
-                f.chain_base = a.fin_chain_base + run.fin;
+                f.chain_base = fin_chain_base + run.fin;
                 f.slot = uint32_t(s);
                 f.pad = 0;
                 a.fins[run.nfin] = f;
@@ -827,6 +842,7 @@ __global__ void __launch_bounds__(kThreads) planner_kernel(PlanArgs a) {
 
 // tile -> segment map (binary search over the segments' first tiles)
 __global__ void tilemap_kernel(const SegRec* segs, const LevelInfo* info, uint32_t* tile_seg) {
+    VQB_PDL();
     const uint32_t nseg = info->nseg, ntiles = info->ntiles;
     for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < ntiles;
          t += gridDim.x * blockDim.x) {
@@ -894,6 +910,7 @@ __global__ void __launch_bounds__(kFinWarps * 32) finisher_kernel(
     const FinRec* fins, const LevelInfo* info, const double* __restrict__ ix,
     const double* __restrict__ iy, const uint32_t* __restrict__ iid, uint32_t* chain,
     uint32_t* chain_count, uint32_t* fin_count_out) {
+    VQB_PDL();
     __shared__ FinSmem SM[kFinWarps];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     FinSmem& S = SM[warp];
@@ -1024,6 +1041,7 @@ __global__ void __launch_bounds__(kFinWarps * 32) finisher_kernel(
 __global__ void size_kernel(uint32_t nslots, const uint8_t* kind, const uint32_t* link,
                             const uint32_t* fin_count, const uint32_t* child_size,
                             uint32_t* size) {
+    VQB_PDL();
     for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < nslots;
          s += gridDim.x * blockDim.x) {
         const uint8_t k = kind[s];
@@ -1039,6 +1057,7 @@ __global__ void emit_kernel(uint32_t nslots, const uint8_t* kind, const uint32_t
                             const ChildRec* slots, const FinRec* fins, const uint32_t* fin_count,
                             const uint32_t* chain, const uint32_t* start,
                             const uint32_t* child_size, uint32_t* child_start, uint32_t* out) {
+    VQB_PDL();
     for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < nslots;
          s += gridDim.x * blockDim.x) {
         const uint8_t k = kind[s];
@@ -1065,6 +1084,7 @@ __global__ void emit_kernel(uint32_t nslots, const uint8_t* kind, const uint32_t
 // no vertex (its r is replaced by the next vertex, emitted once).  Also
 // re-arms the fast-mode side counters of the reference-mode root partition.
 __global__ void legacy_poly_kernel(RootInfo* root, unsigned long long* side_ctr) {
+    VQB_PDL();
     if (threadIdx.x != 0) return;
     side_ctr[0] = side_ctr[1] = 0ull;
     RootInfo& R = *root;
@@ -1083,6 +1103,7 @@ __global__ void legacy_poly_kernel(RootInfo* root, unsigned long long* side_ctr)
 // [p] chain(S1) [q if q != p] chain(S2), chain(S) = chain(S_1) [r] chain(S_2)).
 __global__ void poly_frame_kernel(const RootInfo* root, const uint32_t* size2, uint32_t* start2,
                                   uint32_t* out, uint32_t* h_out) {
+    VQB_PDL();
     if (threadIdx.x != 0) return;
     const RootPoly& P = root->poly;
     uint32_t pos = 0;
@@ -1101,20 +1122,20 @@ __global__ void poly_frame_kernel(const RootInfo* root, const uint32_t* size2, u
 // ===========================================================================
 void launch_extremes(const double* xs, const double* ys, uint64_t n, void* partials,
                      uint32_t* ticket, RootInfo* root, int grid, cudaStream_t st) {
-    extremes_kernel<<<grid, 256, 0, st>>>(xs, ys, n, static_cast<ExtPartial*>(partials), ticket,
+    pdl_launch(extremes_kernel, grid, 256, 0, st, xs, ys, n, static_cast<ExtPartial*>(partials), ticket,
                                           root);
 }
 
 void launch_bootstrap(const double* xs, const double* ys, uint64_t n, void* partials,
                       uint32_t* ticket, RootInfo* root, int grid, cudaStream_t st) {
-    bootstrap_argmax_kernel<<<grid, 256, 0, st>>>(xs, ys, n, static_cast<RootPartial*>(partials),
+    pdl_launch(bootstrap_argmax_kernel, grid, 256, 0, st, xs, ys, n, static_cast<RootPartial*>(partials),
                                                   ticket, root);
 }
 
 void launch_poly_extremes(const double* xs, const double* ys, uint64_t n, void* partials,
                           uint32_t* ticket, RootInfo* root, unsigned long long* side_ctr, int grid,
                           cudaStream_t st) {
-    poly_extremes_kernel<<<grid, 256, 0, st>>>(xs, ys, n, static_cast<PolyPartial*>(partials), ticket,
+    pdl_launch(poly_extremes_kernel, grid, 256, 0, st, xs, ys, n, static_cast<PolyPartial*>(partials), ticket,
                                                root, side_ctr);
 }
 
@@ -1124,8 +1145,8 @@ size_t partial_bytes(int grid) {
     return size_t(grid) * m;
 }
 
-void launch_planner(const ChildRec* slots, uint32_t nslots, SegRec* segs, FinRec* fins,
-                    uint8_t* kind, uint32_t* link, LevelInfo* info, uint64_t fin_chain_base,
+void launch_planner(const ChildRec* slots, uint32_t nslots, const LevelInfo* prev, uint32_t nslots_bound,
+                    SegRec* segs, FinRec* fins, uint8_t* kind, uint32_t* link, LevelInfo* info,
                     uint32_t* flags, void* aggs, void* incs, uint32_t epoch, uint32_t* ctr,
                     uint32_t* seg_pcnt, uint32_t* seg_done, unsigned long long* seg_ctr,
                     int max_grid, cudaStream_t st) {
@@ -1133,15 +1154,14 @@ void launch_planner(const ChildRec* slots, uint32_t nslots, SegRec* segs, FinRec
     a.seg_pcnt = seg_pcnt;
     a.seg_done = seg_done;
     a.seg_ctr = seg_ctr;
-    a.slots = slots; a.nslots = nslots;
-    a.nchunks = (nslots + kPlanChunk - 1) / kPlanChunk;
+    a.slots = slots; a.nslots = nslots; a.prev = prev;
     a.segs = segs; a.fins = fins; a.kind = kind; a.link = link; a.info = info;
-    a.fin_chain_base = fin_chain_base;
     a.flags = flags; a.aggs = static_cast<PlanAgg*>(aggs); a.incs = static_cast<PlanAgg*>(incs);
     a.epoch = epoch; a.ctr = ctr;
-    int grid = int(a.nchunks < uint32_t(max_grid) ? a.nchunks : uint32_t(max_grid));
+    const uint32_t chunks = (nslots_bound + kPlanChunk - 1) / kPlanChunk;
+    int grid = int(chunks < uint32_t(max_grid) ? chunks : uint32_t(max_grid));
     if (grid < 1) grid = 1;
-    planner_kernel<<<grid, kThreads, 0, st>>>(a);
+    pdl_launch(planner_kernel, grid, kThreads, 0, st, a);
 }
 
 void launch_tilemap(const SegRec* segs, const LevelInfo* info, uint32_t* tile_seg,
@@ -1149,7 +1169,7 @@ void launch_tilemap(const SegRec* segs, const LevelInfo* info, uint32_t* tile_se
     uint32_t g = (ntiles_hint + 255) / 256;
     if (g < 1) g = 1;
     if (g > 1184) g = 1184;
-    tilemap_kernel<<<g, 256, 0, st>>>(segs, info, tile_seg);
+    pdl_launch(tilemap_kernel, g, 256, 0, st, segs, info, tile_seg);
 }
 
 void launch_finisher(const FinRec* fins, const LevelInfo* info, const double* ix,
@@ -1158,7 +1178,7 @@ void launch_finisher(const FinRec* fins, const LevelInfo* info, const double* ix
     uint32_t g = (nfin_hint + kFinWarps - 1) / kFinWarps;
     if (g < 1) g = 1;
     if (g > uint32_t(max_grid)) g = uint32_t(max_grid);
-    finisher_kernel<<<g, kFinWarps * 32, 0, st>>>(fins, info, ix, iy, iid, chain, nullptr,
+    pdl_launch(finisher_kernel, g, kFinWarps * 32, 0, st, fins, info, ix, iy, iid, chain, nullptr,
                                                   fin_count);
 }
 
@@ -1168,7 +1188,7 @@ void launch_size(uint32_t nslots, const uint8_t* kind, const uint32_t* link,
     uint32_t g = (nslots + 255) / 256;
     if (g < 1) g = 1;
     if (g > 1184) g = 1184;
-    size_kernel<<<g, 256, 0, st>>>(nslots, kind, link, fin_count, child_size, size);
+    pdl_launch(size_kernel, g, 256, 0, st, nslots, kind, link, fin_count, child_size, size);
 }
 
 void launch_emit(uint32_t nslots, const uint8_t* kind, const uint32_t* link,
@@ -1178,17 +1198,17 @@ void launch_emit(uint32_t nslots, const uint8_t* kind, const uint32_t* link,
     uint32_t g = (nslots + 255) / 256;
     if (g < 1) g = 1;
     if (g > 1184) g = 1184;
-    emit_kernel<<<g, 256, 0, st>>>(nslots, kind, link, slots, fins, fin_count, chain, start,
+    pdl_launch(emit_kernel, g, 256, 0, st, nslots, kind, link, slots, fins, fin_count, chain, start,
                                    child_size, child_start, out);
 }
 
 void launch_legacy_poly(RootInfo* root, unsigned long long* side_ctr, cudaStream_t st) {
-    legacy_poly_kernel<<<1, 32, 0, st>>>(root, side_ctr);
+    pdl_launch(legacy_poly_kernel, 1, 32, 0, st, root, side_ctr);
 }
 
 void launch_poly_frame(const RootInfo* root, const uint32_t* size2, uint32_t* start2, uint32_t* out,
                        uint32_t* h_out, cudaStream_t st) {
-    poly_frame_kernel<<<1, 32, 0, st>>>(root, size2, start2, out, h_out);
+    pdl_launch(poly_frame_kernel, 1, 32, 0, st, root, size2, start2, out, h_out);
 }
 
 size_t plan_agg_bytes() { return sizeof(PlanAgg); }

@@ -17,8 +17,8 @@ size_t partial_bytes(int grid);
 void upload_root_consts(const RootInfo* d_root, cudaStream_t st);
 cudaError_t launch_root_partition(const RootArgs& a, int grid, bool stable, cudaStream_t st);
 cudaError_t launch_level(const LevelArgs& a, bool general, bool stable, int grid, cudaStream_t st);
-void launch_planner(const ChildRec* slots, uint32_t nslots, SegRec* segs, FinRec* fins,
-                    uint8_t* kind, uint32_t* link, LevelInfo* info, uint64_t fin_chain_base,
+void launch_planner(const ChildRec* slots, uint32_t nslots, const LevelInfo* prev, uint32_t nslots_bound,
+                    SegRec* segs, FinRec* fins, uint8_t* kind, uint32_t* link, LevelInfo* info,
                     uint32_t* flags, void* aggs, void* incs, uint32_t epoch, uint32_t* ctr,
                     uint32_t* seg_pcnt, uint32_t* seg_done, unsigned long long* seg_ctr,
                     int max_grid, cudaStream_t st);

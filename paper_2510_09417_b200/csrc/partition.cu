@@ -357,6 +357,7 @@ __device__ __forceinline__ void running_best(unsigned long long (&kb)[NC], uint3
 // ===========================================================================
 template <bool STABLE>
 __global__ void __launch_bounds__(kThreads, kPartMinBlocks) root_partition_kernel(RootArgs a) {
+    VQB_PDL();
     __shared__ TileSmem<4> S;
     __shared__ bool s_last;
     const RootInfo& R = *a.root;
@@ -518,6 +519,7 @@ __global__ void __launch_bounds__(kThreads, kPartMinBlocks) root_partition_kerne
 // ===========================================================================
 template <bool GENERAL, bool STABLE>
 __global__ void __launch_bounds__(kThreads, kPartMinBlocks) level_kernel(LevelArgs a) {
+    VQB_PDL();
     __shared__ TileSmem<2> S;
     __shared__ SegRec s_seg[2];
     __shared__ uint32_t s_k[2];
@@ -832,6 +834,7 @@ void upload_root_consts(const RootInfo* d_root, cudaStream_t st) {
 
 template <bool PREFETCH>
 __global__ void __launch_bounds__(kThreads, PREFETCH ? 3 : kFastMinBlocks) root_partition_fast(RootArgs a) {
+    VQB_PDL();
     __shared__ FastSmem S;
     __shared__ double2 s_frame[4];   // class frames (edx, edy)
     __shared__ uint32_t s_org[4][kWarps];  // per (class, warp): store origin of rank 0
@@ -1008,6 +1011,7 @@ struct RootRing {
 constexpr int kCtlThreads = kThreads + 32;
 
 __global__ void __launch_bounds__(kCtlThreads, 3) root_partition_tma(RootArgs a) {
+    VQB_PDL();
     extern __shared__ __align__(128) unsigned char dsm[];
     RootRing& ring = *reinterpret_cast<RootRing*>(dsm);
     __shared__ FastSmem S;
@@ -1237,6 +1241,7 @@ __device__ __forceinline__ void named_arrive(int par, int count) {
 }
 
 __global__ void __launch_bounds__(kCtlThreads, 3) root_filtered_tma(RootArgs a) {
+    VQB_PDL();
     extern __shared__ __align__(128) unsigned char dsm[];
     RootRing4& ring = *reinterpret_cast<RootRing4*>(dsm);
     __shared__ FastSmem S;
@@ -1471,6 +1476,7 @@ struct LevelRing {
 
 template <bool GENERAL>
 __global__ void __launch_bounds__(kCtlThreads, 3) level_tma(LevelArgs a) {
+    VQB_PDL();
     extern __shared__ __align__(128) unsigned char dsm[];
     LevelRing& ring = *reinterpret_cast<LevelRing*>(dsm);
     __shared__ FastSmem S;
@@ -1694,9 +1700,9 @@ cudaError_t launch_root_partition(const RootArgs& a, int grid, bool stable, cuda
                                      int(sizeof(RootRing)));
                 attr = true;
             }
-            root_partition_tma<<<grid, kCtlThreads, sizeof(RootRing), st>>>(a);
+            pdl_launch(root_partition_tma, grid, kCtlThreads, sizeof(RootRing), st, a);
         } else {
-            root_partition_fast<true><<<grid, kThreads, 0, st>>>(a);  // unaligned caller arrays
+            pdl_launch(root_partition_fast<true>, grid, kThreads, 0, st, a);  // unaligned caller arrays
         }
         return cudaGetLastError();
     }
@@ -1711,7 +1717,7 @@ cudaError_t launch_root_filtered(const RootArgs& a, int grid, cudaStream_t st) {
         cudaFuncSetAttribute(root_filtered_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(RootRing4)));
         attr = true;
     }
-    root_filtered_tma<<<grid, kCtlThreads, sizeof(RootRing4), st>>>(a);
+    pdl_launch(root_filtered_tma, grid, kCtlThreads, sizeof(RootRing4), st, a);
     return cudaGetLastError();
 }
 
@@ -1730,13 +1736,13 @@ cudaError_t launch_level(const LevelArgs& a, bool general, bool stable, int grid
             cudaFuncSetAttribute(level_tma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(LevelRing)));
             attr = true;
         }
-        if (general) level_tma<true><<<grid, kCtlThreads, sizeof(LevelRing), st>>>(a);
-        else level_tma<false><<<grid, kCtlThreads, sizeof(LevelRing), st>>>(a);
+        if (general) pdl_launch(level_tma<true>, grid, kCtlThreads, sizeof(LevelRing), st, a);
+        else pdl_launch(level_tma<false>, grid, kCtlThreads, sizeof(LevelRing), st, a);
         return cudaGetLastError();
     }
     if (!stable) {
-        if (general) level_kernel<true, false><<<grid, kThreads, 0, st>>>(a);
-        else level_kernel<false, false><<<grid, kThreads, 0, st>>>(a);
+        if (general) pdl_launch(level_kernel<true, false>, grid, kThreads, 0, st, a);
+        else pdl_launch(level_kernel<false, false>, grid, kThreads, 0, st, a);
         return cudaGetLastError();
     }
     void* args[] = {const_cast<LevelArgs*>(&a)};
