@@ -120,6 +120,7 @@ class Engine {
         occ_level_ = std::max(1, occupancy_level(false));
         occ_level_stable_ = std::max(1, occupancy_level(true));
         occ_fin_ = std::max(1, occupancy_finisher());
+        occ_fin_cta_ = std::max(1, occupancy_finisher_cta());
         occ_filt_ = std::max(1, occupancy_filtered());
         // one full wave each
         grid_ext_ = sms_ * std::max(1, std::min(8, occupancy_extremes()));
@@ -174,6 +175,7 @@ class Engine {
         bufs_[1].ensure(n, st);
         chain_.ensure(n * 4 + 4, st, true);
         const uint64_t seg_lim = n / (uint64_t(kFinMax) + 1);  // internal segments hold > kFinMax points
+        const uint64_t seg_lim2 = n / (uint64_t(kFinSmall) + 1) + 1;  // CTA-finisher segments hold > kFinSmall
         uint32_t S = nslots;  // slot bound of the level being queued
         int in = 0;
         int lvl = 2;
@@ -206,11 +208,18 @@ class Engine {
                                        sms_ * 4, st);
                     });
                 }
-                // finisher: every segment of <= kFinMax points, whole subtrees
+                // finishers: whole subtrees of every segment of <= kFinMax
+                // points (a warp each up to kFinSmall, a CTA each above)
                 tk(4, st, [&] {
                     launch_finisher(T.fins.as<FinRec>(), dinfo, bufs_[in].x.as<double>(), bufs_[in].y.as<double>(),
                                     bufs_[in].id.as<uint32_t>(), chain_.as<uint32_t>(), T.fin_count.as<uint32_t>(),
                                     S1, sms_ * occ_fin_, st);
+                });
+                tk(4, st, [&] {
+                    launch_finisher_cta(T.fins.as<FinRec>(), dinfo, S1, bufs_[in].x.as<double>(),
+                                        bufs_[in].y.as<double>(), bufs_[in].id.as<uint32_t>(), chain_.as<uint32_t>(),
+                                        T.fin_count.as<uint32_t>(), std::min<uint32_t>(S1, uint32_t(seg_lim2)),
+                                        sms_ * occ_fin_cta_, st);
                 });
                 // K2 over all internal segments of this level
                 const int out = in ^ 1;
@@ -591,7 +600,7 @@ class Engine {
     int dev_ = 0;
     int sms_ = 148;
     int occ_root_ = 1, occ_root_stable_ = 1, occ_level_ = 1, occ_level_stable_ = 1, occ_fin_ = 1;
-    int stream_grid_ = 592, grid_ext_ = 592, grid_boot_ = 592, grid_poly_ = 592, occ_filt_ = 1;
+    int stream_grid_ = 592, grid_ext_ = 592, grid_boot_ = 592, grid_poly_ = 592, occ_filt_ = 1, occ_fin_cta_ = 1;
     bool root_reference_ = getenv("VQHULL_ROOT") != nullptr && std::string(getenv("VQHULL_ROOT")) == "reference";
     uint32_t* ctrs_ = nullptr;
     RootInfo* root_ = nullptr;

@@ -18,7 +18,8 @@ constexpr int kTile = kThreads * kItems;    // points per partition tile
 constexpr int kWarps = kThreads / 32;
 constexpr int kPartMinBlocks = 3;           // resident partition CTAs per SM (register cap)
 constexpr int kFastMinBlocks = 4;           // fast-mode kernels (no staging)
-constexpr uint32_t kFinMax = 256;           // segments this small go to the warp finisher
+constexpr uint32_t kFinSmall = 64;          // segments of 2..64 points: warp finisher
+constexpr uint32_t kFinMax = 1024;          // 65..1024 points: CTA finisher; larger: tiled level kernel
 
 // Root stage geometry.  The recursion itself always follows the reference
 // (level 1 splits by p->q, hull.cpp:228-235); the octagon of the 8 exact
@@ -84,7 +85,7 @@ struct SegRec {
     uint32_t slot;    // this node's slot in the level's slot table
 };
 
-// A node solved entirely by one warp (m <= kFinMax).
+// A node solved entirely by one warp (m <= kFinSmall) or one CTA (m <= kFinMax).
 struct FinRec {
     ChildRec c;
     uint64_t chain_base;  // where its in-order chain is written
@@ -105,6 +106,8 @@ struct LevelInfo {
     uint32_t fin_total;   // points handed to the finisher
     uint32_t nleaf;
     uint32_t fin_base;    // first chain entry of this level's finisher segments
+    uint32_t nfin2;       // CTA-finisher segments (FinRec array from the back)
+    uint32_t pad;
 };
 
 // Look-back status of one tile (one side) of the partition kernels: two
@@ -161,15 +164,16 @@ struct LevelArgs {
 
 // Look-back payload of the planner scan.
 struct PlanAgg {
-    uint32_t nseg, nfin, ntiles, out, fin, leaf;
+    uint32_t nseg, nfin, nfin2, ntiles, out, fin, leaf;
 };
 
 __device__ __forceinline__ void pl_clear(PlanAgg& a) {
-    a.nseg = a.nfin = a.ntiles = a.out = a.fin = a.leaf = 0;
+    a.nseg = a.nfin = a.nfin2 = a.ntiles = a.out = a.fin = a.leaf = 0;
 }
 __device__ __forceinline__ void pl_combine(PlanAgg& a, const PlanAgg& b) {
     a.nseg += b.nseg;
     a.nfin += b.nfin;
+    a.nfin2 += b.nfin2;
     a.ntiles += b.ntiles;
     a.out += b.out;
     a.fin += b.fin;
@@ -180,6 +184,7 @@ __device__ __forceinline__ PlanAgg pl_load(const PlanAgg* s) {
     PlanAgg a;
     a.nseg = __ldcg(&s->nseg);
     a.nfin = __ldcg(&s->nfin);
+    a.nfin2 = __ldcg(&s->nfin2);
     a.ntiles = __ldcg(&s->ntiles);
     a.out = __ldcg(&s->out);
     a.fin = __ldcg(&s->fin);
@@ -190,6 +195,7 @@ __device__ __forceinline__ PlanAgg pl_shfl(const PlanAgg& a, int x) {
     PlanAgg o;
     o.nseg = __shfl_xor_sync(kFull, a.nseg, x);
     o.nfin = __shfl_xor_sync(kFull, a.nfin, x);
+    o.nfin2 = __shfl_xor_sync(kFull, a.nfin2, x);
     o.ntiles = __shfl_xor_sync(kFull, a.ntiles, x);
     o.out = __shfl_xor_sync(kFull, a.out, x);
     o.fin = __shfl_xor_sync(kFull, a.fin, x);

@@ -674,7 +674,8 @@ __global__ void __launch_bounds__(256, 4) poly_extremes_kernel(const double* __r
 
 // ===========================================================================
 // K3: planner — turns the child slots of a level into the next level's work:
-// internal segments (m > kFinMax, tiled), finisher segments (2..kFinMax),
+// internal segments (m > kFinMax, tiled), finisher segments (2..kFinMax: a
+// warp up to kFinSmall, a CTA above),
 // leaves (m == 1: the node's chain is just its apex, hull.cpp:83) and empty
 // slots.  One single-pass scan with decoupled look-back over slot chunks.
 // ===========================================================================
@@ -685,6 +686,7 @@ struct PlanArgs {
     const ChildRec* slots;
     uint32_t nslots;      // level 2 only; deeper levels: 2 * prev->nseg
     const LevelInfo* prev;
+    uint32_t fin_cap;     // FinRec array capacity (CTA-finisher segments fill it from the back)
     SegRec* segs;
     FinRec* fins;
     uint8_t* kind;
@@ -719,6 +721,7 @@ __global__ void __launch_bounds__(kThreads) planner_kernel(PlanArgs a) {
         li.nslots = 0; li.nseg = 0; li.nfin = 0; li.ntiles = 0;
         li.out_total = 0; li.fin_total = 0; li.nleaf = 0;
         li.fin_base = uint32_t(fin_chain_base);
+        li.nfin2 = 0; li.pad = 0;
         *a.info = li;
     }
     while (true) {
@@ -743,7 +746,8 @@ __global__ void __launch_bounds__(kThreads) planner_kernel(PlanArgs a) {
             m[k] = s < nslots ? a.slots[s].m : 0u;
             const uint8_t kd = s < nslots ? kind_of(m[k]) : kEmpty;
             mine.nseg += kd == kInternal;
-            mine.nfin += kd == kFin;
+            mine.nfin += kd == kFin && m[k] <= kFinSmall;
+            mine.nfin2 += kd == kFin && m[k] > kFinSmall;
             mine.leaf += kd == kLeaf;
             mine.ntiles += kd == kInternal ? (m[k] + kTile - 1) / kTile : 0;
             mine.out += kd == kInternal ? m[k] : 0;
@@ -756,6 +760,7 @@ __global__ void __launch_bounds__(kThreads) planner_kernel(PlanArgs a) {
             PlanAgg o;
             o.nseg = __shfl_up_sync(kFull, incl.nseg, d);
             o.nfin = __shfl_up_sync(kFull, incl.nfin, d);
+            o.nfin2 = __shfl_up_sync(kFull, incl.nfin2, d);
             o.ntiles = __shfl_up_sync(kFull, incl.ntiles, d);
             o.out = __shfl_up_sync(kFull, incl.out, d);
             o.fin = __shfl_up_sync(kFull, incl.fin, d);
@@ -783,6 +788,8 @@ __global__ void __launch_bounds__(kThreads) planner_kernel(PlanArgs a) {
                     li.fin_total = all.fin;
                     li.nleaf = all.leaf;
                     li.fin_base = uint32_t(fin_chain_base);
+                    li.nfin2 = all.nfin2;
+                    li.pad = 0;
                     *a.info = li;
                 }
             }
@@ -792,7 +799,7 @@ __global__ void __launch_bounds__(kThreads) planner_kernel(PlanArgs a) {
         for (int w = 0; w < warp; ++w) pl_combine(run, s_w[w]);
         // exclusive within warp
         PlanAgg wex = incl;
-        wex.nseg -= mine.nseg; wex.nfin -= mine.nfin; wex.ntiles -= mine.ntiles;
+        wex.nseg -= mine.nseg; wex.nfin -= mine.nfin; wex.nfin2 -= mine.nfin2; wex.ntiles -= mine.ntiles;
         wex.out -= mine.out; wex.fin -= mine.fin; wex.leaf -= mine.leaf;
         pl_combine(run, wex);
 #pragma unroll
@@ -828,9 +835,13 @@ __global__ void __launch_bounds__(kThreads) planner_kernel(PlanArgs a) {
                 f.chain_base = fin_chain_base + run.fin;
                 f.slot = uint32_t(s);
                 f.pad = 0;
-                a.fins[run.nfin] = f;
-                a.link[s] = run.nfin;
-                run.nfin += 1;
+                // warp-finisher segments from the front of the FinRec array,
+                // CTA-finisher segments from the back
+                const uint32_t fi = m[k] <= kFinSmall ? run.nfin : a.fin_cap - 1u - run.nfin2;
+                a.fins[fi] = f;
+                a.link[s] = fi;
+                run.nfin += m[k] <= kFinSmall;
+                run.nfin2 += m[k] > kFinSmall;
                 run.fin += m[k];
             } else {
                 a.link[s] = 0;
@@ -857,13 +868,13 @@ __global__ void tilemap_kernel(const SegRec* segs, const LevelInfo* info, uint32
 
 // ===========================================================================
 // K3': warp finisher.  One warp solves the whole subtree of a segment with
-// m <= kFinMax points in shared memory, depth-first with an explicit stack
+// m <= kFinSmall points in shared memory, depth-first with an explicit stack
 // (the reference's chain_iterative, hull.cpp:119-190), emitting the chain
 // in order: chain(L) ++ [r] ++ chain(R)  (assemble_chain, hull.cpp:59-73).
 // Points are referenced by local ids; the two working arrays ping-pong per
 // depth so a child's range never overlaps a pending sibling's.
 // ===========================================================================
-constexpr int kFinWarps = 4;
+constexpr int kFinWarps = 8;
 constexpr uint16_t kNoLid = 0xffffu;
 
 struct FinFrame {
@@ -872,11 +883,11 @@ struct FinFrame {
 };
 
 struct FinSmem {
-    double x[kFinMax + 3];
-    double y[kFinMax + 3];
-    uint32_t gid[kFinMax + 3];
-    uint16_t work[2][kFinMax];
-    FinFrame stack[kFinMax + 2];
+    double x[kFinSmall + 3];
+    double y[kFinSmall + 3];
+    uint32_t gid[kFinSmall + 3];
+    uint16_t work[2][kFinSmall];
+    FinFrame stack[kFinSmall + 2];
 };
 
 // canonical order on local ids when the offsets tie exactly: smaller (x, y),
@@ -919,7 +930,7 @@ __global__ void __launch_bounds__(kFinWarps * 32) finisher_kernel(
     for (uint32_t f = blockIdx.x * kFinWarps + warp; f < nfin; f += gridDim.x * kFinWarps) {
         const FinRec rec = fins[f];
         const uint32_t m = rec.c.m;
-        VQB_CHECK(m >= 2 && m <= kFinMax, 30, m, f);
+        VQB_CHECK(m >= 2 && m <= kFinSmall, 30, m, f);
         for (uint32_t i = lane; i < m; i += 32) {
             S.x[i] = ix[rec.c.begin + i];
             S.y[i] = iy[rec.c.begin + i];
@@ -941,7 +952,7 @@ __global__ void __launch_bounds__(kFinWarps * 32) finisher_kernel(
         const uint64_t cbase = rec.chain_base;
         uint32_t guard = 0;
         while (depth > 0) {
-            if (++guard > 8 * kFinMax + 64) {  // at most ~3 visits per node
+            if (++guard > 8 * kFinSmall + 64) {  // at most ~3 visits per node
                 if (lane == 0) g_vqb_fault = 2u;
                 break;
             }
@@ -1031,6 +1042,257 @@ __global__ void __launch_bounds__(kFinWarps * 32) finisher_kernel(
         __syncwarp();
     }
     (void)chain_count;
+}
+
+// ===========================================================================
+// K3'' CTA finisher: one CTA solves the whole subtree of a segment of
+// kFinSmall < m <= kFinMax points in shared memory, LEVEL-SYNCHRONOUSLY:
+// every node of the current depth is partitioned in the same pass (the
+// reference's chain_recursive, hull.cpp:78-115, visited breadth-first), so
+// the serial chain is the tree depth, not the node count (a warp walking the
+// nodes one by one is latency-bound when every point is a hull vertex).
+// Per depth: (1) each point of a live node is classified against the node's
+// (p->r), (r->q) with the reference's expressions and written two-sided into
+// its node's range of the other work array (left child forward, right child
+// backward; shared-memory atomics give the slots, their order is free), and
+// the children's farthest keys are min-reduced with 64-bit shared atomics;
+// (2) points holding the minimal key register as candidates (an exact tie of
+// two candidates is resolved by (x, y, index) on a rare path); (3) children
+// with >= 2 points become the next depth's nodes (block scan), one-point
+// children are leaves.  Finally subtree sizes bottom-up and chain positions
+// top-down give chain(L) ++ [r] ++ chain(R) (assemble_chain, hull.cpp:59-73).
+// ===========================================================================
+constexpr int kFcThreads = 256;
+constexpr int kFcNodes = int(kFinMax / 2);  // nodes of one depth hold >= 2 points each
+constexpr uint16_t kDead = 0xffffu;
+constexpr uint16_t kLinkEmpty = 0, kLinkLeaf = 0x4000, kLinkNode = 0x8000;  // kind | value
+
+struct FinCtaSmem {
+    double x[kFinMax + 3];
+    double y[kFinMax + 3];
+    uint32_t gid[kFinMax + 3];
+    uint16_t work[2][kFinMax];
+    uint16_t wnode[2][kFinMax];
+    uint16_t np[2][kFcNodes], nr[2][kFcNodes], nq[2][kFcNodes];
+    uint16_t nlo[2][kFcNodes], nhi[2][kFcNodes], ntree[2][kFcNodes];
+    unsigned long long ckey[2 * kFcNodes];
+    uint32_t ccnt[2 * kFcNodes];
+    uint32_t cncand[2 * kFcNodes];
+    uint16_t ccand[2 * kFcNodes];
+    uint16_t cmap[2 * kFcNodes];
+    uint16_t tapex[kFinMax + 1];
+    uint16_t tleft[kFinMax + 1], tright[kFinMax + 1];
+    uint16_t tsize[kFinMax + 1], tstart[kFinMax + 1];
+    uint16_t lvl_start[kFinMax + 2];
+    uint32_t wsum[kFcThreads / 32];
+    uint32_t tie;
+    uint32_t nnext;
+};
+
+__device__ __forceinline__ uint32_t fc_link_size(const FinCtaSmem& S, uint16_t l) {
+    return (l & kLinkNode) ? S.tsize[l & 0x3fff] : ((l & kLinkLeaf) ? 1u : 0u);
+}
+
+// the farthest-point key of local point lid in child (node c, side s)
+__device__ __forceinline__ unsigned long long fc_key(const FinCtaSmem& S, int cp, int c, int s, uint16_t lid) {
+    const uint16_t p = S.np[cp][c], r = S.nr[cp][c], q = S.nq[cp][c];
+    const double fx = s ? dsub(S.x[q], S.x[r]) : dsub(S.x[r], S.x[p]);
+    const double fy = s ? dsub(S.y[q], S.y[r]) : dsub(S.y[r], S.y[p]);
+    return key_of(lat_off(fx, fy, S.x[lid], S.y[lid]));
+}
+
+__global__ void __launch_bounds__(kFcThreads) finisher_cta_kernel(const FinRec* fins, const LevelInfo* info,
+                                                                  uint32_t fin_cap,
+                                                                  const double* __restrict__ ix,
+                                                                  const double* __restrict__ iy,
+                                                                  const uint32_t* __restrict__ iid,
+                                                                  uint32_t* chain, uint32_t* fin_count) {
+    VQB_PDL();
+    extern __shared__ __align__(16) unsigned char fc_dsm[];
+    FinCtaSmem& S = *reinterpret_cast<FinCtaSmem*>(fc_dsm);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint32_t nfin2 = info->nfin2;
+    for (uint32_t f = blockIdx.x; f < nfin2; f += gridDim.x) {
+        const uint32_t fi = fin_cap - 1u - f;
+        const FinRec rec = fins[fi];
+        const uint32_t m = rec.c.m;
+        VQB_CHECK(m > kFinSmall && m <= kFinMax, 32, m, f);
+        const uint16_t P0 = uint16_t(m), Q0 = uint16_t(m + 1), R0 = uint16_t(m + 2);
+        for (uint32_t i = tid; i < m; i += kFcThreads) {
+            S.x[i] = ix[rec.c.begin + i];
+            S.y[i] = iy[rec.c.begin + i];
+            S.gid[i] = iid[rec.c.begin + i];
+            S.work[0][i] = uint16_t(i);
+            S.wnode[0][i] = 0;
+            S.wnode[1][i] = kDead;
+        }
+        if (tid == 0) {
+            S.x[P0] = rec.c.px; S.y[P0] = rec.c.py; S.gid[P0] = 0xffffffffu;
+            S.x[Q0] = rec.c.qx; S.y[Q0] = rec.c.qy; S.gid[Q0] = 0xffffffffu;
+            S.x[R0] = rec.c.rx; S.y[R0] = rec.c.ry; S.gid[R0] = rec.c.r_idx;
+            S.np[0][0] = P0; S.nr[0][0] = R0; S.nq[0][0] = Q0;
+            S.nlo[0][0] = 0; S.nhi[0][0] = uint16_t(m); S.ntree[0][0] = 0;
+            S.tapex[0] = R0; S.tleft[0] = kLinkEmpty; S.tright[0] = kLinkEmpty;
+            S.lvl_start[0] = 0; S.lvl_start[1] = 1;
+            S.tie = 0;
+        }
+        if (tid < 2) {
+            S.ckey[tid] = kNoKey; S.ccnt[tid] = 0; S.cncand[tid] = 0;
+        }
+        __syncthreads();
+        uint32_t nnodes = 1, ntree = 1;
+        int cur = 0, depth = 0;
+        while (nnodes > 0) {
+            const int nxt = cur ^ 1;
+            // (1) classify, claim two-sided slots, min-reduce the children's keys
+            for (uint32_t i = tid; i < m; i += kFcThreads) {
+                const uint16_t c = S.wnode[cur][i];
+                if (c == kDead) continue;
+                const uint16_t lid = S.work[cur][i];
+                const uint16_t p = S.np[cur][c], r = S.nr[cur][c], q = S.nq[cur][c];
+                const double u = S.x[lid], w = S.y[lid];
+                const double A = dsub(S.x[p], u), B = dsub(S.y[p], w);
+                const double E = dsub(S.x[r], u), F = dsub(S.y[r], w);
+                const double Cc = dsub(S.x[q], u), D = dsub(S.y[q], w);
+                const bool la = left_diff(A, B, E, F);
+                const bool lb = !la && left_diff(E, F, Cc, D);
+                if (la || lb) {
+                    const int s = la ? 0 : 1;
+                    const uint32_t ch = 2u * c + s;
+                    atomicMin(&S.ckey[ch], fc_key(S, cur, c, s, lid));
+                    const uint32_t pos = atomicAdd(&S.ccnt[ch], 1u);
+                    const uint32_t dest = s ? uint32_t(S.nhi[cur][c]) - 1u - pos : uint32_t(S.nlo[cur][c]) + pos;
+                    S.work[nxt][dest] = lid;
+                    S.wnode[nxt][dest] = uint16_t(ch);
+                }
+            }
+            __syncthreads();
+            // (2) candidates: points holding their child's minimal key
+            for (uint32_t i = tid; i < m; i += kFcThreads) {
+                const uint16_t ch = S.wnode[nxt][i];
+                if (ch == kDead) continue;
+                const uint16_t lid = S.work[nxt][i];
+                if (fc_key(S, cur, ch >> 1, ch & 1, lid) == S.ckey[ch]) {
+                    if (atomicAdd(&S.cncand[ch], 1u) == 0) S.ccand[ch] = lid;
+                    else S.tie = 1;
+                }
+            }
+            __syncthreads();
+            if (S.tie) {  // rare: exact offset ties -> smaller (x, y), then index
+                for (uint32_t ch = tid; ch < 2 * nnodes; ch += kFcThreads) {
+                    if (S.cncand[ch] < 2) continue;
+                    const int c = int(ch >> 1), s = int(ch & 1);
+                    const uint32_t cnt = S.ccnt[ch];
+                    const uint32_t lo = s ? uint32_t(S.nhi[cur][c]) - cnt : S.nlo[cur][c];
+                    uint16_t best = S.ccand[ch];
+                    for (uint32_t j = lo; j < lo + cnt; ++j) {
+                        const uint16_t l = S.work[nxt][j];
+                        if (l == best || fc_key(S, cur, c, s, l) != S.ckey[ch]) continue;
+                        const bool better = S.x[l] != S.x[best] ? S.x[l] < S.x[best]
+                                          : (S.y[l] != S.y[best] ? S.y[l] < S.y[best] : S.gid[l] < S.gid[best]);
+                        if (better) best = l;
+                    }
+                    S.ccand[ch] = best;
+                }
+                __syncthreads();
+                if (tid == 0) S.tie = 0;
+            }
+            // (3) children -> next depth's nodes (block scan over "internal"), links, leaves
+            const uint32_t nch = 2 * nnodes;
+            uint32_t flags = 0, local = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint32_t ch = 4u * tid + k;
+                const bool in = ch < nch && S.ccnt[ch] >= 2;
+                flags |= uint32_t(in) << k;
+                local += in;
+            }
+            uint32_t incl = local;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t o = __shfl_up_sync(kFull, incl, d);
+                if (lane >= d) incl += o;
+            }
+            if (lane == 31) S.wsum[warp] = incl;
+            __syncthreads();
+            uint32_t base = 0;
+            for (int w2 = 0; w2 < warp; ++w2) base += S.wsum[w2];
+            uint32_t id = base + incl - local;  // first next-depth id of this thread's children
+            if (tid == kFcThreads - 1) S.nnext = base + incl;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint32_t ch = 4u * tid + k;
+                if (ch >= nch) break;
+                const int c = int(ch >> 1), s = int(ch & 1);
+                const uint32_t cnt = S.ccnt[ch];
+                const uint16_t t = S.ntree[cur][c];
+                uint16_t link = kLinkEmpty;
+                S.cmap[ch] = kDead;
+                if (cnt == 1) {
+                    link = uint16_t(kLinkLeaf | S.ccand[ch]);
+                } else if (cnt >= 2) {
+                    const uint32_t nid = id++;
+                    const uint16_t tnew = uint16_t(ntree + nid);
+                    link = uint16_t(kLinkNode | tnew);
+                    S.np[nxt][nid] = s ? S.nr[cur][c] : S.np[cur][c];
+                    S.nq[nxt][nid] = s ? S.nq[cur][c] : S.nr[cur][c];
+                    S.nr[nxt][nid] = S.ccand[ch];
+                    S.nlo[nxt][nid] = s ? uint16_t(S.nhi[cur][c] - cnt) : S.nlo[cur][c];
+                    S.nhi[nxt][nid] = s ? S.nhi[cur][c] : uint16_t(S.nlo[cur][c] + cnt);
+                    S.ntree[nxt][nid] = tnew;
+                    S.tapex[tnew] = S.ccand[ch];
+                    S.tleft[tnew] = kLinkEmpty;
+                    S.tright[tnew] = kLinkEmpty;
+                    S.cmap[ch] = uint16_t(nid);
+                }
+                if (s) S.tright[t] = link; else S.tleft[t] = link;
+            }
+            __syncthreads();
+            const uint32_t nn = S.nnext;
+            // remap the next work array to next-depth node ids; reset the
+            // accumulators and the array that becomes the next output
+            for (uint32_t i = tid; i < m; i += kFcThreads) {
+                const uint16_t ch = S.wnode[nxt][i];
+                if (ch != kDead) S.wnode[nxt][i] = S.cmap[ch];
+                S.wnode[cur][i] = kDead;
+            }
+            for (uint32_t ch = tid; ch < 2 * nn; ch += kFcThreads) {
+                S.ckey[ch] = kNoKey;
+                S.ccnt[ch] = 0;
+                S.cncand[ch] = 0;
+            }
+            ntree += nn;
+            ++depth;
+            if (tid == 0) S.lvl_start[depth + 1] = uint16_t(ntree);
+            nnodes = nn;
+            cur = nxt;
+            __syncthreads();
+        }
+        // subtree sizes bottom-up, then chain positions top-down
+        for (int d = depth - 1; d >= 0; --d) {
+            for (uint32_t t = S.lvl_start[d] + tid; t < S.lvl_start[d + 1]; t += kFcThreads)
+                S.tsize[t] = uint16_t(fc_link_size(S, S.tleft[t]) + 1u + fc_link_size(S, S.tright[t]));
+            __syncthreads();
+        }
+        const uint64_t cb = rec.chain_base;
+        if (tid == 0) S.tstart[0] = 0;
+        __syncthreads();
+        for (int d = 0; d < depth; ++d) {
+            for (uint32_t t = S.lvl_start[d] + tid; t < S.lvl_start[d + 1]; t += kFcThreads) {
+                const uint32_t s0 = S.tstart[t];
+                const uint16_t L = S.tleft[t], R = S.tright[t];
+                const uint32_t ap = s0 + fc_link_size(S, L);
+                chain[cb + ap] = S.gid[S.tapex[t]];
+                if (L & kLinkLeaf) chain[cb + s0] = S.gid[L & 0x3fff];
+                else if (L & kLinkNode) S.tstart[L & 0x3fff] = uint16_t(s0);
+                if (R & kLinkLeaf) chain[cb + ap + 1] = S.gid[R & 0x3fff];
+                else if (R & kLinkNode) S.tstart[R & 0x3fff] = uint16_t(ap + 1);
+            }
+            __syncthreads();
+        }
+        if (tid == 0) fin_count[fi] = S.tsize[0];
+        __syncthreads();
+    }
 }
 
 // ===========================================================================
@@ -1154,7 +1416,7 @@ void launch_planner(const ChildRec* slots, uint32_t nslots, const LevelInfo* pre
     a.seg_pcnt = seg_pcnt;
     a.seg_done = seg_done;
     a.seg_ctr = seg_ctr;
-    a.slots = slots; a.nslots = nslots; a.prev = prev;
+    a.slots = slots; a.nslots = nslots; a.prev = prev; a.fin_cap = nslots_bound > 0 ? nslots_bound : 1;
     a.segs = segs; a.fins = fins; a.kind = kind; a.link = link; a.info = info;
     a.flags = flags; a.aggs = static_cast<PlanAgg*>(aggs); a.incs = static_cast<PlanAgg*>(incs);
     a.epoch = epoch; a.ctr = ctr;
@@ -1180,6 +1442,28 @@ void launch_finisher(const FinRec* fins, const LevelInfo* info, const double* ix
     if (g > uint32_t(max_grid)) g = uint32_t(max_grid);
     pdl_launch(finisher_kernel, g, kFinWarps * 32, 0, st, fins, info, ix, iy, iid, chain, nullptr,
                                                   fin_count);
+}
+
+void launch_finisher_cta(const FinRec* fins, const LevelInfo* info, uint32_t fin_cap, const double* ix,
+                         const double* iy, const uint32_t* iid, uint32_t* chain, uint32_t* fin_count,
+                         uint32_t nfin_hint, int max_grid, cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(finisher_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(FinCtaSmem)));
+        attr = true;
+    }
+    uint32_t g = nfin_hint;
+    if (g < 1) g = 1;
+    if (g > uint32_t(max_grid)) g = uint32_t(max_grid);
+    pdl_launch(finisher_cta_kernel, g, kFcThreads, sizeof(FinCtaSmem), st, fins, info, fin_cap, ix, iy, iid, chain,
+               fin_count);
+}
+
+int occupancy_finisher_cta() {
+    int b = 0;
+    cudaFuncSetAttribute(finisher_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(FinCtaSmem)));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, finisher_cta_kernel, kFcThreads, sizeof(FinCtaSmem));
+    return b;
 }
 
 void launch_size(uint32_t nslots, const uint8_t* kind, const uint32_t* link,

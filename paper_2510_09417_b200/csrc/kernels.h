@@ -45,6 +45,10 @@ size_t plan_agg_bytes();
 int occupancy_root(bool stable);
 int occupancy_level(bool stable);
 int occupancy_finisher();
+int occupancy_finisher_cta();
+void launch_finisher_cta(const FinRec* fins, const LevelInfo* info, uint32_t fin_cap, const double* ix,
+                         const double* iy, const uint32_t* iid, uint32_t* chain, uint32_t* fin_count,
+                         uint32_t nfin_hint, int max_grid, cudaStream_t st);
 int occupancy_filtered();
 int occupancy_poly_extremes();
 int occupancy_extremes();
