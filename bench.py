@@ -122,7 +122,9 @@ def cpu_reference_baseline(kind, n, seed, offset_ranks=1, budget_s=20.0, reps=No
     from oracle import Oracle, Reference
 
     threads = os.cpu_count() or 1
-    xs, ys = vq.generate(kind, n * offset_ranks, seed, threads=threads)
+    total = n * offset_ranks
+    m = min(total, 4 * 10**8)  # bounded sample (config 5: 4e9 points would need 128 GB host RAM)
+    xs, ys = vq.generate(kind, m, seed, threads=threads)
     if Reference.available():
         R = Reference()
         secs, h = R.bench_hull(xs, ys, threads, 1)  # first rep calibrates
@@ -130,13 +132,14 @@ def cpu_reference_baseline(kind, n, seed, offset_ranks=1, budget_s=20.0, reps=No
         k = reps or max(1, min(5, int(budget_s / max(t, 1e-3))))
         secs2, h = R.bench_hull(xs, ys, threads, k)
         allsecs = np.concatenate([secs, secs2])
+        what = "full workload" if m == total else f"first {m} of {total} points"
         return {"kind": "reference", "cores": threads, "seconds": allsecs.tolist(),
-                "value": (n * offset_ranks) / float(np.mean(secs2)), "hull": int(h),
-                "sample": f"full workload: {kind} n={n * offset_ranks} seed={seed}, "
+                "value": m / float(np.mean(secs2)), "hull": int(h),
+                "sample": f"{what}: {kind} n={m} seed={seed}, "
                           f"{len(secs2)} timed reps after 1 untimed, convex_hull workers={threads}"}
     # oracle port (single thread): bounded sample
     O = Oracle()
-    m = min(n, 10**7)
+    m = min(m, 10**7)
     t0 = time.perf_counter()
     O.convex_hull(xs[:m], ys[:m])
     dt = time.perf_counter() - t0
@@ -162,7 +165,8 @@ def run_reference(args):
     from oracle import Oracle, Reference
 
     threads = os.cpu_count() or 1
-    total = n * world
+    strong = args.config == 5 and not args.n
+    total = n if strong else n * world
     xs, ys = vq.generate(kind, total, seed, threads=threads)
     if Reference.available():
         R = Reference()
@@ -186,9 +190,10 @@ def run_reference(args):
     emit({
         "metric": METRIC, "value": value, "unit": "points/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": mean * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (reference RNG, seeded)", "impl": "reference",
-        "config": {"workload": f"config{args.config}: {kind} n={n} per GPU seed={seed}",
+        "higher_is_better": True, "scaling": "strong" if strong else "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (reference RNG, seeded)", "impl": "reference",
+        "config": {"workload": (f"config{args.config}: {kind} n={total} total, sharded, seed={seed}" if strong
+                                else f"config{args.config}: {kind} n={n} per GPU seed={seed}"),
                    "points_total": total, "parallelism": f"host threads={cores}"},
         "cpu_baseline": {"value": value, "unit": "points/s", "cores": cores, "kind": kind_s,
                          "sample": sample},
@@ -215,7 +220,15 @@ def run_ours(args):
     kind, n, seed = CONFIGS[args.config]
     if args.n:
         n = args.n
-    offset = rank * n  # weak scaling: each rank owns n points of the global stream
+    # configs 1-4: weak scaling, each rank owns n points of the global stream;
+    # config 5 (BASELINE: 4e9 points sharded evenly over 1/2/4/8 GPUs): strong
+    strong = args.config == 5 and not args.n
+    if strong:
+        total = n
+        n = total // world + (1 if rank < total % world else 0)
+        offset = rank * (total // world) + min(rank, total % world)
+    else:
+        offset = rank * n
 
     # host generation (libm, same bytes as the reference generators) into pinned memory
     Xh = torch.empty(n, dtype=torch.float64, pin_memory=True)
@@ -257,17 +270,20 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
     ms_step = ms / args.steps
-    value = world * n / (ms_step / 1e3)
+    points_total = total if strong else world * n
+    value = points_total / (ms_step / 1e3)
     clocks = clk.summary()
 
     result = {
         "metric": METRIC, "value": value, "unit": "points/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong" if strong else "weak", "vs_baseline": None,
+        "dtype": "f64",
         "data": "synthetic (reference RNG streams, seeded; generated on host with libm)",
-        "config": {"workload": f"config{args.config}: {kind} n={n} per GPU seed={seed}"
+        "config": {"workload": (f"config{args.config}: {kind} n={points_total} total, sharded, seed={seed}"
+                                if strong else f"config{args.config}: {kind} n={n} per GPU seed={seed}")
                                + (" (BASELINE configs[1])" if args.config == 2 else ""),
-                   "points_per_gpu": n, "points_total": world * n, "hull_vertices": h,
+                   "points_per_gpu": n, "points_total": points_total, "hull_vertices": h,
                    "parallelism": f"shard{world}" if world > 1 else "single GPU",
                    "l2": "inputs 16 B/pt x n >> 126 MB L2 (no flush needed)"},
         "clocks": clocks,
@@ -338,7 +354,7 @@ def run_ours(args):
         if world > 1:
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         dt = float(tt.item())
-        result["e2e"] = {"value": world * n / dt, "unit": "points/s",
+        result["e2e"] = {"value": points_total / dt, "unit": "points/s",
                          "h2d_bytes_per_step": 16 * n, "d2h_bytes_per_step": (4 if world == 1 else 8) * hh,
                          "ms_per_step": dt * 1e3,
                          "api": "vqhull_compute (C ABI, pinned host arrays)" if world == 1

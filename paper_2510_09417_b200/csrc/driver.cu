@@ -171,20 +171,26 @@ class Engine {
         // by host-side bounds, so the host queues kLevelBatch levels at a time
         // and synchronizes once per batch to learn whether the recursion has
         // ended.  Levels queued past the end find zero slots and do nothing.
+        // lean mode (very large n): sizes come from the planner's exact
+        // counts, one host sync per level, instead of n-sized bounds
+        const bool lean = n > kLeanN;
         bufs_[0].ensure(n, st);
-        bufs_[1].ensure(n, st);
-        chain_.ensure(n * 4 + 4, st, true);
+        if (!lean) {
+            bufs_[1].ensure(n, st);
+            chain_.ensure(n * 4 + 4, st, true);
+        }
         const uint64_t seg_lim = n / (uint64_t(kFinMax) + 1);  // internal segments hold > kFinMax points
         const uint64_t seg_lim2 = n / (uint64_t(kFinSmall) + 1) + 1;  // CTA-finisher segments hold > kFinSmall
         uint32_t S = nslots;  // slot bound of the level being queued
         int in = 0;
         int lvl = 2;
         lmax_ = -1;
+        const int batch = lean ? 1 : kLevelBatch;
         while (lmax_ < 0) {
             const int first = lvl;
-            for (int b = 0; b < kLevelBatch; ++b, ++lvl) {
-                const uint32_t nseg_b = uint32_t(std::min<uint64_t>(S, seg_lim));
-                const uint32_t ntiles_b = uint32_t(n / kTile) + nseg_b + 1;
+            for (int b = 0; b < batch; ++b, ++lvl) {
+                uint32_t nseg_b = uint32_t(std::min<uint64_t>(S, seg_lim));
+                uint32_t ntiles_b = uint32_t(n / kTile) + nseg_b + 1;
                 const uint32_t S1 = std::max<uint32_t>(S, 1);
                 LevelTables& T = level(lvl);
                 T.kind.ensure(S1, st);
@@ -207,6 +213,20 @@ class Engine {
                                        aggs_.p, incs_.p, ep, &ctrs_[2], seg_pcnt(), seg_done(S1), seg_ctr(S1),
                                        sms_ * 4, st);
                     });
+                }
+                if (lean) {
+                    ck(cudaMemcpyAsync(h_info_, dinfo, sizeof(LevelInfo), cudaMemcpyDeviceToHost, st), "d2h info");
+                    ck(cudaStreamSynchronize(st), "level sync");
+                    if (lvl == 2 && h_root_->nonfinite) {
+                        end_timing(st);
+                        ck(cudaStreamSynchronize(st), "sync");
+                        return VQHULL_EINVAL;
+                    }
+                    const LevelInfo li = *h_info_;
+                    nseg_b = li.nseg;
+                    ntiles_b = li.ntiles;
+                    bufs_[in ^ 1].ensure(std::max<uint32_t>(li.out_total, 1), st);
+                    chain_.ensure((uint64_t(li.fin_base) + li.fin_total) * 4 + 4, st, true);
                 }
                 // finishers: whole subtrees of every segment of <= kFinMax
                 // points (a warp each up to kFinSmall, a CTA each above)
@@ -634,6 +654,7 @@ class Engine {
     std::vector<LevelInfo> hinfo_;  // host copies of the level infos (after the last batch)
     int lmax_ = 2;
     static constexpr int kLevelBatch = 4;  // levels queued per host synchronization
+    static constexpr uint64_t kLeanN = 1ull << 29;  // above: exact per-level sizing (one sync per level)
     uint32_t epoch_ = 0;
     uint32_t launches_ = 0;
     bool timing_ = false;

@@ -1320,23 +1320,28 @@ __global__ void emit_kernel(uint32_t nslots, const uint8_t* kind, const uint32_t
                             const uint32_t* chain, const uint32_t* start,
                             const uint32_t* child_size, uint32_t* child_start, uint32_t* out) {
     VQB_PDL();
-    for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < nslots;
-         s += gridDim.x * blockDim.x) {
+    // one warp per slot: a finisher slot copies its whole chain (up to
+    // kFinMax entries) with the warp's 32 lanes
+    const int lane = threadIdx.x & 31;
+    const uint32_t wpb = blockDim.x >> 5;
+    for (uint32_t s = blockIdx.x * wpb + (threadIdx.x >> 5); s < nslots; s += gridDim.x * wpb) {
         const uint8_t k = kind[s];
         const uint32_t st = start[s];
         if (k == kLeaf) {
-            out[st] = slots[s].r_idx;
+            if (lane == 0) out[st] = slots[s].r_idx;
         } else if (k == kInternal) {
-            const uint32_t L = link[s];
-            const uint32_t sl = child_size[2 * L];
-            out[st + sl] = slots[s].r_idx;
-            child_start[2 * L] = st;
-            child_start[2 * L + 1] = st + sl + 1;
+            if (lane == 0) {
+                const uint32_t L = link[s];
+                const uint32_t sl = child_size[2 * L];
+                out[st + sl] = slots[s].r_idx;
+                child_start[2 * L] = st;
+                child_start[2 * L + 1] = st + sl + 1;
+            }
         } else if (k == kFin) {
             const uint32_t f = link[s];
             const uint32_t c = fin_count[f];
             const uint64_t b = fins[f].chain_base;
-            for (uint32_t i = 0; i < c; ++i) out[st + i] = chain[b + i];
+            for (uint32_t i = lane; i < c; i += 32) out[st + i] = chain[b + i];
         }
     }
 }
@@ -1479,9 +1484,9 @@ void launch_emit(uint32_t nslots, const uint8_t* kind, const uint32_t* link,
                  const ChildRec* slots, const FinRec* fins, const uint32_t* fin_count,
                  const uint32_t* chain, const uint32_t* start, const uint32_t* child_size,
                  uint32_t* child_start, uint32_t* out, cudaStream_t st) {
-    uint32_t g = (nslots + 255) / 256;
+    uint32_t g = (nslots + 7) / 8;  // 8 warps (slots) per block
     if (g < 1) g = 1;
-    if (g > 1184) g = 1184;
+    if (g > 2368) g = 2368;
     pdl_launch(emit_kernel, g, 256, 0, st, nslots, kind, link, slots, fins, fin_count, chain, start,
                                    child_size, child_start, out);
 }
