@@ -330,8 +330,12 @@ def run_ours(args):
     # ---- e2e: public API with HOST buffers (H2D + D2H inside the timed region)
     if not args.no_e2e:
         xs_np, ys_np = Xh.numpy(), Yh.numpy()
-        Xd = torch.empty_like(X)
-        Yd = torch.empty_like(Y)
+        if world == 1:  # the C ABI makes its own device copy: release ours first
+            del X, Y, out_u32
+            torch.cuda.empty_cache()
+        else:
+            Xd = torch.empty_like(X)
+            Yd = torch.empty_like(Y)
 
         def e2e_step():
             if world == 1:

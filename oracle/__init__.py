@@ -239,12 +239,16 @@ class Reference:
                                            oy.ctypes.data_as(_dp), C.byref(cnt)) == 0
         return ox[: cnt.value].copy(), oy[: cnt.value].copy()
 
-    def compute(self, xs, ys, workers=1):
+    def compute(self, xs, ys, workers=1, cap=None):
+        """The reference's own vqhull_compute.  It writes only the h hull
+        indices (vqhull_c.cpp:51-61), so for huge inputs with a known small
+        hull `cap` bounds the output buffer instead of n entries."""
         xs, px = _f64(xs)
         ys, py = _f64(ys)
         n = len(xs)
-        out = np.zeros(max(n, 1), dtype=np.uint64)
+        out = np.zeros(max(min(n, cap) if cap else n, 1), dtype=np.uint64)
         cnt = C.c_size_t()
         rc = self.lib.vqhull_compute(px, py, n, workers,
                                      out.ctypes.data_as(_sz), C.byref(cnt))
+        assert cnt.value <= out.size, "hull larger than the output cap"
         return rc, out[: cnt.value].copy()

@@ -194,6 +194,34 @@ def test_config4_kuzmin_1e9(vq, cuda, oracle):
     assert got.tolist() == cfg["indices"]
 
 
+@pytest.mark.slow
+def test_config5_disk_4e9_one_gpu(vq, cuda, oracle):
+    """BASELINE config 5 (disk, 4e9 points) on ONE device: > 2^31 positions,
+    lean per-level sizing; golden from the reference library
+    (tests/golden/make_config5.py)."""
+    cfg = G.configs().get("config5_disk_4e9_s5")
+    if cfg is None:
+        pytest.skip("config5 golden not generated")
+    import torch
+
+    n = cfg["n"]
+    free, _ = torch.cuda.mem_get_info()
+    if free < 150 * 2**30:
+        pytest.skip("needs ~150 GB of device memory")
+    X = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    Y = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    vq.generate(cfg["kind"], n, cfg["seed"], out=(X, Y))
+    Xd, Yd = X.cuda(), Y.cuda()
+    del X, Y
+    # u32 output (indices < 2^32, torch int32 storage): reinterpret unsigned
+    got = vq.hull_device(Xd, Yd, u32=True).cpu().numpy().view(np.uint32).astype(np.uint64)
+    del Xd, Yd
+    torch.cuda.empty_cache()
+    assert got.size == cfg["h"]
+    assert f"{oracle.fnv1a64(got):016x}" == cfg["fnv1a64_u64le"]
+    assert got.tolist() == cfg["indices"]
+
+
 # --- size-independent properties at full size ----------------------------------
 def test_permutation_invariance(vq, cuda):
     """Shuffled input -> the same vertex sequence."""
