@@ -351,17 +351,17 @@ __global__ void __launch_bounds__(256) bootstrap_argmax_kernel(
 // ===========================================================================
 // K1' (default root stage): find_extremes (geometry.cpp:7-36) over every
 // point, exactly as K1 (x read for every point, y only on exact x ties),
-// plus the octagon filter's other six vertices from a sample of the input
-// (every 16th group of 256 points, x and y): max/min y, max/min x+y, max/min
-// x-y.  The filter only needs its vertices to be input points on two
-// x-monotone chains (checked here; otherwise no filter), not exact extremes,
-// so a sample costs 1/16 of a y pass and loses almost nothing.  Finiteness of
+// plus the octagon filter's 8 vertices from a sample of the input (every
+// 16th group of 256 points, x and y): min/max x, y, x+y, x-y.  The filter
+// only needs its vertices to be input points (see poly_finish), not exact
+// extremes, so a sample costs 1/16 of a y pass and loses almost nothing.  Finiteness of
 // x is checked here, of y by the root pass that reads every y.
 // ===========================================================================
 struct PolyPartial {
     ExtKey lo, hi;
-    double av[6];
-    uint32_t ai[6];
+    double av[8];
+    uint32_t ai[8];
+    double sx, sy, sn;  // sums over the sample (centre of the filter's inner box)
     uint32_t nonfinite;
     uint32_t pad;
 };
@@ -369,12 +369,12 @@ struct PolyPartial {
 constexpr int kSampleShift = 7;  // groups of 128 pairs (256 points)
 constexpr int kSampleMask = 15;  // one group in 16 is sampled
 
-// sampled directions, in octagon slot order 1, 2, 3, 5, 6, 7:
-// TL min x-y, T max y, TR max x+y, BR max x-y, B min y, BL min x+y
+// sampled directions, in octagon slot order: 0 min x, 1 min x-y, 2 max y,
+// 3 max x+y, 4 max x, 5 max x-y, 6 min y, 7 min x+y
 __device__ __forceinline__ bool approx_better(int a, double v, uint32_t i, double vb, uint32_t ib) {
     if (i == kNoIdx) return false;
     if (ib == kNoIdx) return true;
-    const bool maximize = (a == 1 || a == 2 || a == 3);
+    const bool maximize = (a >= 2 && a <= 5);
     if (v != vb) return maximize ? v > vb : v < vb;
     return i < ib;
 }
@@ -386,108 +386,111 @@ __device__ __forceinline__ PolyPartial poly_none() {
     p.hi = ExtKey{0.0, 0.0, kNoIdx, 0u};
     p.nonfinite = 0u;
     p.pad = 0u;
-    const double init[6] = {kInf, -kInf, -kInf, -kInf, kInf, kInf};
+    p.sx = p.sy = p.sn = 0.0;
+    const double init[8] = {kInf, kInf, -kInf, -kInf, -kInf, -kInf, kInf, kInf};
 #pragma unroll
-    for (int q = 0; q < 6; ++q) { p.av[q] = init[q]; p.ai[q] = kNoIdx; }
+    for (int q = 0; q < 8; ++q) { p.av[q] = init[q]; p.ai[q] = kNoIdx; }
     return p;
 }
 
-__device__ __forceinline__ void poly_fold(PolyPartial& a, const PolyPartial& o) {
-    if (lo_better(o.lo, a.lo)) a.lo = o.lo;
-    if (hi_better(o.hi, a.hi)) a.hi = o.hi;
-    a.nonfinite |= o.nonfinite;
-#pragma unroll
-    for (int q = 0; q < 6; ++q)
-        if (approx_better(q, o.av[q], o.ai[q], a.av[q], a.ai[q])) {
-            a.av[q] = o.av[q];
-            a.ai[q] = o.ai[q];
-        }
-}
-
-__device__ __forceinline__ PolyPartial ldcg_poly(const PolyPartial* p) {
-    PolyPartial o;
-    o.lo.x = __ldcg(&p->lo.x); o.lo.y = __ldcg(&p->lo.y); o.lo.idx = __ldcg(&p->lo.idx); o.lo.valid = __ldcg(&p->lo.valid);
-    o.hi.x = __ldcg(&p->hi.x); o.hi.y = __ldcg(&p->hi.y); o.hi.idx = __ldcg(&p->hi.idx); o.hi.valid = __ldcg(&p->hi.valid);
-    o.nonfinite = __ldcg(&p->nonfinite);
-    o.pad = 0u;
-#pragma unroll
-    for (int q = 0; q < 6; ++q) { o.av[q] = __ldcg(&p->av[q]); o.ai[q] = __ldcg(&p->ai[q]); }
-    return o;
-}
-
-// block-wide fold (warp butterflies, then warp 0 over the 8 warp results);
-// the result is valid in thread 0
-__device__ __forceinline__ PolyPartial block_reduce_poly(PolyPartial m, PolyPartial* s_w) {
+// block-wide fold, field group by field group (warp butterflies, then
+// thread 0 over the 8 warp results in shared memory); the result is valid in
+// thread 0.  Reference parameters keep the fields in registers; no struct
+// copies, no spills.
+__device__ __forceinline__ void block_reduce_poly(ExtKey& lo, ExtKey& hi, double (&av)[8], uint32_t (&ai)[8],
+                                                  double& sx, double& sy, double& sn, uint32_t& nb,
+                                                  PolyPartial* s_w) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #pragma unroll
     for (int s = 16; s > 0; s >>= 1) {
-        PolyPartial o;
-        o.lo = shfl_key(m.lo, s);
-        o.hi = shfl_key(m.hi, s);
-        o.nonfinite = __shfl_xor_sync(kFull, m.nonfinite, s);
-#pragma unroll
-        for (int q = 0; q < 6; ++q) {
-            o.av[q] = __shfl_xor_sync(kFull, m.av[q], s);
-            o.ai[q] = __shfl_xor_sync(kFull, m.ai[q], s);
-        }
-        poly_fold(m, o);
+        const ExtKey a = shfl_key(lo, s);
+        if (lo_better(a, lo)) lo = a;
+        const ExtKey b = shfl_key(hi, s);
+        if (hi_better(b, hi)) hi = b;
+        nb |= __shfl_xor_sync(kFull, nb, s);
+        sx += __shfl_xor_sync(kFull, sx, s);
+        sy += __shfl_xor_sync(kFull, sy, s);
+        sn += __shfl_xor_sync(kFull, sn, s);
     }
-    if (lane == 0) s_w[warp] = m;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+#pragma unroll
+        for (int s = 16; s > 0; s >>= 1) {
+            const double ov = __shfl_xor_sync(kFull, av[q], s);
+            const uint32_t oi = __shfl_xor_sync(kFull, ai[q], s);
+            if (approx_better(q, ov, oi, av[q], ai[q])) { av[q] = ov; ai[q] = oi; }
+        }
+    }
+    if (lane == 0) {
+        s_w[warp].lo = lo;
+        s_w[warp].hi = hi;
+        s_w[warp].nonfinite = nb;
+        s_w[warp].sx = sx;
+        s_w[warp].sy = sy;
+        s_w[warp].sn = sn;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) { s_w[warp].av[q] = av[q]; s_w[warp].ai[q] = ai[q]; }
+    }
     __syncthreads();
-    if (threadIdx.x == 0)
-        for (int w = 1; w < int(blockDim.x >> 5); ++w) poly_fold(m, s_w[w]);
-    return m;
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < int(blockDim.x >> 5); ++w) {
+            if (lo_better(s_w[w].lo, lo)) lo = s_w[w].lo;
+            if (hi_better(s_w[w].hi, hi)) hi = s_w[w].hi;
+            nb |= s_w[w].nonfinite;
+            sx += s_w[w].sx;
+            sy += s_w[w].sy;
+            sn += s_w[w].sn;
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                if (approx_better(q, s_w[w].av[q], s_w[w].ai[q], av[q], ai[q])) {
+                    av[q] = s_w[w].av[q];
+                    ai[q] = s_w[w].ai[q];
+                }
+        }
+    }
 }
 
-// Last step of K1' (one thread): the root polygon, the filter's chord forms
-// and inner box, the emission frame.
+// Last step of K1' (one thread): p, q (exact), the octagon filter (the
+// sample's 8 directional extremes: mutually consistent, so in convex
+// position up to rounding ties — exact p, q would not be, e.g. when one far
+// point of a heavy-tailed input dominates), its chord forms and inner box,
+// the emission frame.
 __device__ __noinline__ void poly_finish(const PolyPartial& F, const double* __restrict__ xs,
                                          const double* __restrict__ ys, RootInfo* root) {
     const double kInf = __longlong_as_double(0x7ff0000000000000ll);
     const ExtKey L = F.lo, H = F.hi;
     const uint32_t nb = F.nonfinite;
-    const uint32_t* bi = F.ai;
     RootInfo& R = *root;
     RootPoly& P = R.poly;
-    // octagon slot order: 0 L, 1 TL, 2 T, 3 TR, 4 R, 5 BR, 6 B, 7 BL
-    const int slot_of[6] = {1, 2, 3, 5, 6, 7};
     bool ok = L.valid && H.valid && nb == 0;
     double vx[8], vy[8];
-    uint32_t vi[8];
-    vx[0] = L.x; vy[0] = L.y; vi[0] = L.idx;
-    vx[4] = H.x; vy[4] = H.y; vi[4] = H.idx;
-    double gx[6], gy[6];
 #pragma unroll
-    for (int q = 0; q < 6; ++q) {  // independent loads, all in flight together
-        const uint32_t i = bi[q] != kNoIdx ? bi[q] : L.idx;
-        gx[q] = xs[i];
-        gy[q] = ys[i];
+    for (int j = 0; j < 8; ++j) {  // independent loads, all in flight together
+        const uint32_t i = F.ai[j] != kNoIdx ? F.ai[j] : L.idx;
+        vx[j] = xs[i];
+        vy[j] = ys[i];
     }
 #pragma unroll
-    for (int q = 0; q < 6; ++q) {
-        const int j = slot_of[q];
-        ok &= bi[q] != kNoIdx;
-        vi[j] = bi[q] != kNoIdx ? bi[q] : L.idx;
-        vx[j] = gx[q];
-        vy[j] = gy[q];
-    }
     for (int j = 0; j < 8; ++j) {
+        ok &= F.ai[j] != kNoIdx;
         P.vx[j] = vx[j];
         P.vy[j] = vy[j];
-        P.vidx[j] = vi[j];
+        P.vidx[j] = F.ai[j];
     }
     // Every vertex is an input point, so the region right of all 8 chords
-    // (the octagon, or its kernel if the sample made it non-convex) lies in
-    // the hull.  M bounds |coordinates| of the vertices, hence of every point
-    // the filter can drop; the margin is 2^-32 M (~10^5 ulps of M), so the
-    // fused multiply-adds' rounding can never reach a dropped point and no
-    // reference predicate can see one as a hull or farthest candidate.
+    // (the octagon, or its kernel if rounding ties made it non-convex) lies
+    // in the hull.  M bounds |coordinates| of the vertices, hence of every
+    // point the filter can drop; the margin is 2^-32 M (~10^5 ulps of M), so
+    // the fused multiply-adds' rounding can never reach a dropped point and
+    // no reference predicate can see one as a hull or farthest candidate.
     // Outside 2^-400 <= M <= 2^500 (products could underflow/overflow): no
     // filter.
     double M = 0.0;
+#pragma unroll
     for (int j = 0; j < 8; ++j) M = fmax(M, fmax(fabs(vx[j]), fabs(vy[j])));
     ok &= M >= 0x1p-400 && M <= 0x1p500;
     int chords = 0;
+#pragma unroll
     for (int j = 0; j < 8; ++j) {
         const int k = (j + 1) & 7;
         const double ex = vx[k] - vx[j], ey = vy[k] - vy[j];
@@ -503,12 +506,13 @@ __device__ __noinline__ void poly_finish(const PolyPartial& F, const double* __r
     }
     auto inside = [&](double x, double y) {
         bool in = true;
+#pragma unroll
         for (int j = 0; j < 8; ++j) in &= __fma_rn(P.fa[j], x, __fma_rn(P.fb[j], y, P.fc[j])) < P.ft[j];
         return in;
     };
-    // inner box from the vertices (its corners tend to BE vertices, so it is
-    // shrunk a little); kept only if its 4 corners pass the test (the filter
-    // region is convex, so then the whole box does)
+    // inner box between the diagonal vertices (its corners tend to BE
+    // vertices, so it is shrunk a little); kept only if its 4 corners pass
+    // the test (the filter region is convex, so then the whole box does)
     const double cx0 = fmax(vx[1], vx[7]), cx1 = fmin(vx[3], vx[5]);
     const double cy0 = fmax(vy[5], vy[7]), cy1 = fmin(vy[1], vy[3]);
     double bx0 = kInf, bx1 = -kInf, by0 = kInf, by1 = -kInf;  // empty
@@ -519,6 +523,38 @@ __device__ __noinline__ void poly_finish(const PolyPartial& F, const double* __r
         if (x0 < x1 && y0 < y1 && inside(x0, y0) && inside(x0, y1) && inside(x1, y0) && inside(x1, y1)) {
             bx0 = x0; bx1 = x1; by0 = y0; by1 = y1;
             break;
+        }
+    }
+    // second candidate, for octagons that are not "round" (heavy tails can
+    // collapse the sample's octagon to a triangle): the largest box around
+    // the sample's mean with the octagon's aspect, in closed form per chord
+    // and worst corner, verified like the first; the larger one is kept
+    if (F.sn > 0.0) {
+        const double cx = F.sx / F.sn, cy = F.sy / F.sn;
+        double xmin = vx[0], xmax = vx[0], ymin = vy[0], ymax = vy[0];
+#pragma unroll
+        for (int j = 1; j < 8; ++j) {
+            xmin = fmin(xmin, vx[j]); xmax = fmax(xmax, vx[j]);
+            ymin = fmin(ymin, vy[j]); ymax = fmax(ymax, vy[j]);
+        }
+        const double W = 0.5 * (xmax - xmin), Hh = 0.5 * (ymax - ymin);
+        if (inside(cx, cy) && W > 0.0 && Hh > 0.0) {
+            double t = 1.0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const double f0 = P.fa[j] * cx + P.fb[j] * cy + P.fc[j];
+                const double g = fabs(P.fa[j]) * W + fabs(P.fb[j]) * Hh;
+                if (g > 0.0) t = fmin(t, (P.ft[j] - f0) / g);
+            }
+            for (int tries = 0; tries < 4 && t > 0.0; ++tries, t *= 0.5) {
+                const double x0 = cx - 0.999 * t * W, x1 = cx + 0.999 * t * W;
+                const double y0 = cy - 0.999 * t * Hh, y1 = cy + 0.999 * t * Hh;
+                if (x0 < x1 && y0 < y1 && inside(x0, y0) && inside(x0, y1) && inside(x1, y0) && inside(x1, y1)) {
+                    const double a_old = bx0 < bx1 ? (bx1 - bx0) * (by1 - by0) : 0.0;
+                    if ((x1 - x0) * (y1 - y0) > a_old) { bx0 = x0; bx1 = x1; by0 = y0; by1 = y1; }
+                    break;
+                }
+            }
         }
     }
     P.bx0 = bx0; P.bx1 = bx1; P.by0 = by0; P.by1 = by1;
@@ -534,7 +570,7 @@ __device__ __noinline__ void poly_finish(const PolyPartial& F, const double* __r
     R.qx = H.x; R.qy = H.y;
 }
 
-__global__ void __launch_bounds__(256, 4) poly_extremes_kernel(const double* __restrict__ xs,
+__global__ void __launch_bounds__(256, 3) poly_extremes_kernel(const double* __restrict__ xs,
                                                             const double* __restrict__ ys, uint64_t n,
                                                             PolyPartial* partials, uint32_t* ticket,
                                                             RootInfo* root, unsigned long long* side_ctr) {
@@ -542,9 +578,11 @@ __global__ void __launch_bounds__(256, 4) poly_extremes_kernel(const double* __r
     const double kInf = __longlong_as_double(0x7ff0000000000000ll);
     double lo_x = kInf, hi_x = -kInf;
     uint32_t lo_i = kNoIdx, hi_i = kNoIdx;
-    double av[6] = {kInf, -kInf, -kInf, -kInf, kInf, kInf};
-    uint32_t ai[6] = {kNoIdx, kNoIdx, kNoIdx, kNoIdx, kNoIdx, kNoIdx};
+    double av[8] = {kInf, kInf, -kInf, -kInf, -kInf, -kInf, kInf, kInf};
+    uint32_t ai[8] = {kNoIdx, kNoIdx, kNoIdx, kNoIdx, kNoIdx, kNoIdx, kNoIdx, kNoIdx};
     bool bad = false;
+    double ssx = 0.0, ssy = 0.0;  // sample sums (non-finite input is rejected anyway)
+    uint32_t ssn = 0;
     auto visit_x = [&](uint32_t i, double x) {
         bad |= nonfinite_bits(x);
         const bool lt = x < lo_x, gt = x > hi_x;
@@ -560,10 +598,13 @@ __global__ void __launch_bounds__(256, 4) poly_extremes_kernel(const double* __r
     };
     auto visit_xy = [&](uint32_t i, double x, double y) {
         const double s = __dadd_rn(x, y), d = __dsub_rn(x, y);
-        const double val[6] = {d, y, s, d, y, s};
+        ssx = __dadd_rn(ssx, x);
+        ssy = __dadd_rn(ssy, y);
+        ++ssn;
+        const double val[8] = {x, d, y, s, x, d, y, s};
 #pragma unroll
-        for (int a = 0; a < 6; ++a) {
-            const bool maximize = (a == 1 || a == 2 || a == 3);
+        for (int a = 0; a < 8; ++a) {
+            const bool maximize = (a >= 2 && a <= 5);
             const bool take = maximize ? val[a] > av[a] : val[a] < av[a];
             av[a] = take ? val[a] : av[a];
             ai[a] = take ? i : ai[a];
@@ -640,19 +681,21 @@ __global__ void __launch_bounds__(256, 4) poly_extremes_kernel(const double* __r
         }
     }
     // reductions: thread -> CTA partial -> (last CTA, all threads) -> final
-    PolyPartial mine;
-    mine.lo = ExtKey{lo_x, 0.0, lo_i, lo_i != kNoIdx};
-    mine.hi = ExtKey{hi_x, 0.0, hi_i, hi_i != kNoIdx};
-    if (mine.lo.valid) mine.lo.y = ys[lo_i];
-    if (mine.hi.valid) mine.hi.y = ys[hi_i];
-    mine.nonfinite = bad ? 1u : 0u;
-#pragma unroll
-    for (int q = 0; q < 6; ++q) { mine.av[q] = av[q]; mine.ai[q] = ai[q]; }
+    ExtKey lo{lo_x, 0.0, lo_i, lo_i != kNoIdx};
+    ExtKey hi{hi_x, 0.0, hi_i, hi_i != kNoIdx};
+    if (lo.valid) lo.y = ys[lo_i];
+    if (hi.valid) hi.y = ys[hi_i];
+    uint32_t nb = bad ? 1u : 0u;
+    double sx = ssx, sy = ssy, sn = double(ssn);
     __shared__ PolyPartial s_w[8];
     __shared__ bool s_last;
-    PolyPartial r = block_reduce_poly(mine, s_w);
+    block_reduce_poly(lo, hi, av, ai, sx, sy, sn, nb, s_w);
     if (threadIdx.x == 0) {
-        partials[blockIdx.x] = r;
+        PolyPartial& r = partials[blockIdx.x];
+        r.lo = lo; r.hi = hi; r.nonfinite = nb; r.pad = 0u;
+        r.sx = sx; r.sy = sy; r.sn = sn;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) { r.av[q] = av[q]; r.ai[q] = ai[q]; }
         __threadfence();
         s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
     }
@@ -660,13 +703,38 @@ __global__ void __launch_bounds__(256, 4) poly_extremes_kernel(const double* __r
     if (!s_last) return;
     __threadfence();
     // every thread folds its share of the CTA partials (independent loads)
-    PolyPartial acc = poly_none();
-    for (uint32_t c = threadIdx.x; c < gridDim.x; c += blockDim.x) poly_fold(acc, ldcg_poly(&partials[c]));
+    {
+        PolyPartial acc = poly_none();
+        lo = acc.lo; hi = acc.hi; nb = 0; sx = sy = sn = 0.0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) { av[q] = acc.av[q]; ai[q] = kNoIdx; }
+    }
+    for (uint32_t c = threadIdx.x; c < gridDim.x; c += blockDim.x) {
+        const PolyPartial* p = &partials[c];
+        ExtKey a, h;
+        a.x = __ldcg(&p->lo.x); a.y = __ldcg(&p->lo.y); a.idx = __ldcg(&p->lo.idx); a.valid = __ldcg(&p->lo.valid);
+        h.x = __ldcg(&p->hi.x); h.y = __ldcg(&p->hi.y); h.idx = __ldcg(&p->hi.idx); h.valid = __ldcg(&p->hi.valid);
+        if (lo_better(a, lo)) lo = a;
+        if (hi_better(h, hi)) hi = h;
+        nb |= __ldcg(&p->nonfinite);
+        sx += __ldcg(&p->sx);
+        sy += __ldcg(&p->sy);
+        sn += __ldcg(&p->sn);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const double ov = __ldcg(&p->av[q]);
+            const uint32_t oi = __ldcg(&p->ai[q]);
+            if (approx_better(q, ov, oi, av[q], ai[q])) { av[q] = ov; ai[q] = oi; }
+        }
+    }
     __syncthreads();  // s_w reuse
-    r = block_reduce_poly(acc, s_w);
+    block_reduce_poly(lo, hi, av, ai, sx, sy, sn, nb, s_w);
     if (threadIdx.x != 0) return;
     __shared__ PolyPartial s_fin;
-    s_fin = r;
+    s_fin.lo = lo; s_fin.hi = hi; s_fin.nonfinite = nb; s_fin.pad = 0u;
+    s_fin.sx = sx; s_fin.sy = sy; s_fin.sn = sn;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) { s_fin.av[q] = av[q]; s_fin.ai[q] = ai[q]; }
     poly_finish(s_fin, xs, ys, root);
     side_ctr[0] = 0ull;  // the root pass's counter (another root mode may have used it)
     *ticket = 0;

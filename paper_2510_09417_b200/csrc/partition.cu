@@ -1247,6 +1247,9 @@ __global__ void __launch_bounds__(kCtlThreads, 3) root_filtered_tma(RootArgs a) 
     __shared__ FastSmem S;
     __shared__ uint32_t s_wtot[2][2][kWarps];
     __shared__ uint32_t s_org[2][2][kWarps];
+    __shared__ uint16_t s_q[kWarps][kTile / kWarps];             // a warp's points needing the slow path
+    __shared__ uint16_t s_surv[2][kWarps][kTile / kWarps];       // survivors in rank order: idx | class << 10
+    __shared__ uint32_t s_sn[2][kWarps];
     __shared__ bool s_last;
     const RootInfo& R = c_root;
     const RootPoly& P = R.poly;
@@ -1306,97 +1309,104 @@ __global__ void __launch_bounds__(kCtlThreads, 3) root_filtered_tma(RootArgs a) 
             named_arrive<3>(par, kCtlThreads);  // store origins of tile k published
         }
     } else {
-        // ---- compute warps
+        // ---- compute warps: every warp owns 128 points of a tile (4 per lane)
         const bool filter = P.filter != 0;
-        const double bx0 = P.bx0, bx1 = P.bx1, by0 = P.by0, by1 = P.by1;
-        bool bad = false;      // non-finite y (x was checked by K1')
-        uint32_t pcls = 0;     // previous tile: 2-bit classes
-        uint32_t prk[kItems];  // previous tile: ranks
-#pragma unroll
-        for (int i = 0; i < kItems; ++i) prk[i] = 0;
+        const double bx0 = filter ? P.bx0 : kInf, bx1 = filter ? P.bx1 : -kInf;
+        const double by0 = filter ? P.by0 : kInf, by1 = filter ? P.by1 : -kInf;
+        bool bad = false;  // non-finite y (x was checked by K1'); never inside the box
+        const unsigned lt = lanemask_lt();
         auto store_tile = [&](uint32_t k) {  // tile k's survivors, offsets behind barrier B
             const int par = int(k & 1);
             named_sync<3>(par, kCtlThreads);
             const uint32_t t = blockIdx.x + k * G;
-            const uint32_t start = t * uint32_t(kTile) + tid;
+            const uint32_t tbase = t * uint32_t(kTile);
             const int s = int(k % kRing4);
-#pragma unroll
-            for (int i = 0; i < kItems; ++i) {
-                const int c = int((pcls >> (2 * i)) & 3u);
-                if (c < 2) {
-                    const uint32_t pos = start + uint32_t(i) * kThreads;
-                    const double x = t < nfull ? ring.x[s][i * kThreads + tid] : a.xs[pos];
-                    const double y = t < nfull ? ring.y[s][i * kThreads + tid] : a.ys[pos];
+            const uint32_t sn = s_sn[par][warp];
+            // the list holds each class's survivors in rank order: a
+            // survivor's rank = number of earlier entries of its class
+            uint32_t run0 = 0, run1 = 0;
+            for (uint32_t j0 = 0; j0 < sn; j0 += 32) {
+                const uint32_t j = j0 + lane;
+                const uint32_t e = j < sn ? s_surv[par][warp][j] : 0xffffu;
+                const uint32_t c = (e >> 10) & 1u;
+                const unsigned b1 = __ballot_sync(kFull, j < sn && c == 1u);
+                const unsigned b0 = __ballot_sync(kFull, j < sn) & ~b1;
+                if (j < sn) {
+                    const uint32_t idx = e & (kTile - 1);
+                    const uint32_t rk = c ? run1 + __popc(b1 & lt) : run0 + __popc(b0 & lt);
                     const uint32_t o = s_org[par][c][warp];
-                    const uint32_t p = c ? o - prk[i] : o + prk[i];
+                    const uint32_t p = c ? o - rk : o + rk;
                     VQB_CHECK(p < a.out_cap, 14, p, a.out_cap);
-                    a.ox[p] = x;
-                    a.oy[p] = y;
-                    a.oid[p] = pos;
+                    a.ox[p] = ring.x[s][idx];
+                    a.oy[p] = ring.y[s][idx];
+                    a.oid[p] = tbase + idx;
                 }
+                run0 += __popc(b0);
+                run1 += __popc(b1);
             }
         };
         for (uint32_t k = 0; k < nt; ++k) {
             const uint32_t t = blockIdx.x + k * G;
-            const uint32_t start = t * uint32_t(kTile) + tid;
+            const uint32_t tbase = t * uint32_t(kTile);
             const int s = int(k % kRing4);
-            double ux[kItems], uy[kItems];
+            const int par = int(k & 1);
             if (t < nfull) {
                 mbar_wait(&ring.bar[s], (k / kRing4) & 1u);
+            } else {  // the partial last tile is staged by the warps themselves
 #pragma unroll
                 for (int i = 0; i < kItems; ++i) {
-                    ux[i] = ring.x[s][i * kThreads + tid];
-                    uy[i] = ring.y[s][i * kThreads + tid];
+                    const uint32_t idx = uint32_t(i) * kThreads + tid;
+                    ring.x[s][idx] = tbase + idx < n ? a.xs[tbase + idx] : 0.0;
+                    ring.y[s][idx] = tbase + idx < n ? a.ys[tbase + idx] : 0.0;
                 }
-            } else {
-#pragma unroll
-                for (int i = 0; i < kItems; ++i) {
-                    const uint32_t pos = start + uint32_t(i) * kThreads;
-                    ux[i] = pos < n ? a.xs[pos] : 0.0;
-                    uy[i] = pos < n ? a.ys[pos] : 0.0;
-                }
+                __syncwarp();
             }
-            uint32_t wrun = 0, cls = 0;
-            uint32_t rk[kItems];
+            // phase A: strictly inside the inner box -> dropped at once
+            uint32_t qn = 0;
 #pragma unroll
             for (int i = 0; i < kItems; ++i) {
-                const uint32_t pos = start + uint32_t(i) * kThreads;
-                const double u = ux[i], w = uy[i];
-                bad |= nonfinite_bits(w);
-                bool drop = (u > bx0) & (u < bx1) & (w > by0) & (w < by1);
-                if (!drop) {  // inside by the margin w.r.t. all 8 chords
-                    drop = true;
-#pragma unroll
-                    for (int j = 0; j < 8; ++j)
-                        drop &= __fma_rn(P.fa[j], u, __fma_rn(P.fb[j], w, P.fc[j])) < P.ft[j];
-                }
-                drop = filter && drop;
+                const uint32_t idx = uint32_t(i) * kThreads + tid;
+                const double u = ring.x[s][idx], w = ring.y[s][idx];
+                const bool need = (tbase + idx < n) & !((u > bx0) & (u < bx1) & (w > by0) & (w < by1));
+                const unsigned b = __ballot_sync(kFull, need);
+                if (need) s_q[warp][qn + __popc(b & lt)] = uint16_t(idx);
+                qn += __popc(b);
+            }
+            __syncwarp();
+            // phase C: the rest, densely, 32 at a time
+            uint32_t wrun = 0, sn = 0;
+            for (uint32_t r0 = 0; r0 < qn; r0 += 32) {
+                const uint32_t j = r0 + lane;
+                const bool valid = j < qn;
+                const uint32_t idx = valid ? s_q[warp][j] : 0u;
+                const double u = ring.x[s][idx], w = ring.y[s][idx];
                 int c = 2;
-                if (!drop) {
-                    const double A = dsub(px, u), B = dsub(py, w);
-                    const double Cc = dsub(qx, u), D = dsub(qy, w);
-                    const double t1 = dmul(A, D), t2 = dmul(B, Cc);
-                    c = t1 > t2 ? 0 : (t2 > t1 ? 1 : 2);  // left of p->q / of q->p
-                }
-                c = pos < n ? c : 2;
-                cls |= uint32_t(c) << (2 * i);
-                // a warp whose points all fell away skips the ranking
-                rk[i] = __any_sync(kFull, c < 2) ? warp_rank<2>(c, wrun) : 0u;
-            }
-            if (lane < 2) s_wtot[k & 1][lane][warp] = wrun;
-            named_arrive<1>(int(k & 1), kCtlThreads);
+                if (valid) {
+                    bad |= nonfinite_bits(w);
+                    bool drop = filter;
 #pragma unroll
-            for (int i = 0; i < kItems; ++i) {  // fused farthest-point search
-                const int c = int((cls >> (2 * i)) & 3u);
+                    for (int q = 0; q < 8; ++q)  // inside by the margin w.r.t. all 8 chords
+                        drop &= __fma_rn(P.fa[q], u, __fma_rn(P.fb[q], w, P.fc[q])) < P.ft[q];
+                    if (!drop) {
+                        const double A = dsub(px, u), B = dsub(py, w);
+                        const double Cc = dsub(qx, u), D = dsub(qy, w);
+                        const double t1 = dmul(A, D), t2 = dmul(B, Cc);
+                        c = t1 > t2 ? 0 : (t2 > t1 ? 1 : 2);  // left of p->q / of q->p
+                    }
+                }
                 if (__any_sync(kFull, c < 2)) {
-                    const double o = lat_off(adx, ady, ux[i], uy[i]);
-                    running_best_d<2>(bo, bi, c, c ? -o : o, start + uint32_t(i) * kThreads, a.xs, a.ys);
+                    const double o = lat_off(adx, ady, u, w);  // fused farthest-point search
+                    running_best_d<2>(bo, bi, c, c ? -o : o, tbase + idx, a.xs, a.ys);
+                    (void)warp_rank<2>(c, wrun);  // per-class warp counts
+                    const unsigned b = __ballot_sync(kFull, c < 2);
+                    if (c < 2) s_surv[par][warp][sn + __popc(b & lt)] = uint16_t(idx | (uint32_t(c) << 10));
+                    sn += __popc(b);
                 }
             }
+            if (lane < 2) s_wtot[par][lane][warp] = wrun;
+            if (lane == 0) s_sn[par][warp] = sn;
+            named_arrive<1>(par, kCtlThreads);
             if (k >= 1) store_tile(k - 1);
-            pcls = cls;
-#pragma unroll
-            for (int i = 0; i < kItems; ++i) prk[i] = rk[i];
         }
         if (nt >= 1) store_tile(nt - 1);
         if (bad) atomicOr(&a.root_w->nonfinite, 1u);
