@@ -120,7 +120,6 @@ class Engine {
         occ_level_ = std::max(1, occupancy_level(false));
         occ_level_stable_ = std::max(1, occupancy_level(true));
         occ_fin_ = std::max(1, occupancy_finisher());
-        occ_fin_cta_ = std::max(1, occupancy_finisher_cta());
         occ_filt_ = std::max(1, occupancy_filtered());
         // one full wave each
         grid_ext_ = sms_ * std::max(1, std::min(8, occupancy_extremes()));
@@ -180,7 +179,6 @@ class Engine {
             chain_.ensure(n * 4 + 4, st, true);
         }
         const uint64_t seg_lim = n / (uint64_t(kFinMax) + 1);  // internal segments hold > kFinMax points
-        const uint64_t seg_lim2 = n / (uint64_t(kFinSmall) + 1) + 1;  // CTA-finisher segments hold > kFinSmall
         uint32_t S = nslots;  // slot bound of the level being queued
         int in = 0;
         int lvl = 2;
@@ -231,15 +229,9 @@ class Engine {
                 // finishers: whole subtrees of every segment of <= kFinMax
                 // points (a warp each up to kFinSmall, a CTA each above)
                 tk(4, st, [&] {
-                    launch_finisher(T.fins.as<FinRec>(), dinfo, bufs_[in].x.as<double>(), bufs_[in].y.as<double>(),
-                                    bufs_[in].id.as<uint32_t>(), chain_.as<uint32_t>(), T.fin_count.as<uint32_t>(),
-                                    S1, sms_ * occ_fin_, st);
-                });
-                tk(4, st, [&] {
-                    launch_finisher_cta(T.fins.as<FinRec>(), dinfo, S1, bufs_[in].x.as<double>(),
-                                        bufs_[in].y.as<double>(), bufs_[in].id.as<uint32_t>(), chain_.as<uint32_t>(),
-                                        T.fin_count.as<uint32_t>(), std::min<uint32_t>(S1, uint32_t(seg_lim2)),
-                                        sms_ * occ_fin_cta_, st);
+                    launch_finisher(T.fins.as<FinRec>(), dinfo, S1, bufs_[in].x.as<double>(),
+                                    bufs_[in].y.as<double>(), bufs_[in].id.as<uint32_t>(), chain_.as<uint32_t>(),
+                                    T.fin_count.as<uint32_t>(), S1, sms_ * occ_fin_, st);
                 });
                 // K2 over all internal segments of this level
                 const int out = in ^ 1;
@@ -310,6 +302,23 @@ class Engine {
         if (filtered) stats_.root_filter_on = h_root_->poly.filter;
 
         // ---- emission: bottom-up sizes, root frame, top-down starts
+        uint64_t total_slots = 0;
+        for (int l = 2; l <= lmax_; ++l) total_slots += hinfo_[l].nslots;
+        if (lmax_ - 1 <= kEmitMaxLevels && total_slots <= kEmitSmallSlots) {
+            // small tree: everything in one CTA
+            EmitAll E;
+            std::memset(&E, 0, sizeof E);
+            E.nlev = lmax_ - 1;
+            for (int l = 2; l <= lmax_; ++l) {
+                LevelTables& T = level(l);
+                EmitLevel& el = E.lv[l - 2];
+                el.kind = T.kind.as<uint8_t>(); el.link = T.link.as<uint32_t>(); el.slots = T.slots.as<ChildRec>();
+                el.fins = T.fins.as<FinRec>(); el.fin_count = T.fin_count.as<uint32_t>();
+                el.size = T.size.as<uint32_t>(); el.start = T.start.as<uint32_t>();
+                el.nslots = hinfo_[l].nslots;
+            }
+            tk(5, st, [&] { launch_emit_small(E, root_, chain_.as<uint32_t>(), d_out, hword_, st); });
+        } else {
         for (int l = lmax_; l >= 2; --l) {
             LevelTables& T = level(l);
             const uint32_t ns = hinfo_[l].nslots;
@@ -333,6 +342,7 @@ class Engine {
                             T.start.as<uint32_t>(), has_child ? level(l + 1).size.as<uint32_t>() : nullptr,
                             has_child ? level(l + 1).start.as<uint32_t>() : nullptr, d_out, st);
             });
+        }
         }
         ck(cudaMemcpyAsync(h_word_, hword_, 4, cudaMemcpyDeviceToHost, st), "d2h h");
         end_timing(st);
@@ -620,7 +630,7 @@ class Engine {
     int dev_ = 0;
     int sms_ = 148;
     int occ_root_ = 1, occ_root_stable_ = 1, occ_level_ = 1, occ_level_stable_ = 1, occ_fin_ = 1;
-    int stream_grid_ = 592, grid_ext_ = 592, grid_boot_ = 592, grid_poly_ = 592, occ_filt_ = 1, occ_fin_cta_ = 1;
+    int stream_grid_ = 592, grid_ext_ = 592, grid_boot_ = 592, grid_poly_ = 592, occ_filt_ = 1;
     bool root_reference_ = getenv("VQHULL_ROOT") != nullptr && std::string(getenv("VQHULL_ROOT")) == "reference";
     uint32_t* ctrs_ = nullptr;
     RootInfo* root_ = nullptr;
@@ -654,7 +664,8 @@ class Engine {
     std::vector<LevelInfo> hinfo_;  // host copies of the level infos (after the last batch)
     int lmax_ = 2;
     static constexpr int kLevelBatch = 4;  // levels queued per host synchronization
-    static constexpr uint64_t kLeanN = 1ull << 29;  // above: exact per-level sizing (one sync per level)
+    static constexpr uint64_t kLeanN = 1ull << 29;
+    static constexpr uint64_t kEmitSmallSlots = 1u << 14;  // trees this small: one emission kernel  // above: exact per-level sizing (one sync per level)
     uint32_t epoch_ = 0;
     uint32_t launches_ = 0;
     bool timing_ = false;

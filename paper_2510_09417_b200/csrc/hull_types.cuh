@@ -162,6 +162,25 @@ struct LevelArgs {
     ChildRec* children;  // 2 per segment
 };
 
+// Emission of a small recursion tree in one kernel: per level, the slot
+// tables (levels 2 .. 2 + nlev - 1).
+constexpr int kEmitMaxLevels = 48;
+struct EmitLevel {
+    const uint8_t* kind;
+    const uint32_t* link;
+    const ChildRec* slots;
+    const FinRec* fins;
+    const uint32_t* fin_count;
+    uint32_t* size;
+    uint32_t* start;
+    uint32_t nslots;
+    uint32_t pad;
+};
+struct EmitAll {
+    EmitLevel lv[kEmitMaxLevels];
+    int nlev;
+};
+
 // Look-back payload of the planner scan.
 struct PlanAgg {
     uint32_t nseg, nfin, nfin2, ntiles, out, fin, leaf;

@@ -10,7 +10,8 @@
 //                               level in one launch       extract_core.hpp:421-515
 //   K3  planner_kernel          recursion driver: child -> segment/finisher
 //                               tables, tile offsets       hull.cpp:78-115
-//   K3' finisher_kernel         whole subtrees of small segments, one warp each
+//   K3' finisher_all_kernel     whole subtrees of small segments: a CTA each up to
+//                               kFinMax points, a warp each up to kFinSmall
 //                               (explicit stack)           hull.cpp:119-190
 //   K4  size/emit kernels       in-order chain assembly    hull.cpp:59-73, 259-266
 #include <cfloat>
@@ -942,7 +943,6 @@ __global__ void tilemap_kernel(const SegRec* segs, const LevelInfo* info, uint32
 // Points are referenced by local ids; the two working arrays ping-pong per
 // depth so a child's range never overlaps a pending sibling's.
 // ===========================================================================
-constexpr int kFinWarps = 8;
 constexpr uint16_t kNoLid = 0xffffu;
 
 struct FinFrame {
@@ -985,17 +985,16 @@ __device__ __forceinline__ void fin_warp_best(unsigned long long& k, uint16_t& l
     }
 }
 
-__global__ void __launch_bounds__(kFinWarps * 32) finisher_kernel(
-    const FinRec* fins, const LevelInfo* info, const double* __restrict__ ix,
-    const double* __restrict__ iy, const uint32_t* __restrict__ iid, uint32_t* chain,
-    uint32_t* chain_count, uint32_t* fin_count_out) {
-    VQB_PDL();
-    __shared__ FinSmem SM[kFinWarps];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    FinSmem& S = SM[warp];
+// one warp: segments f = gw, gw + nw, ... of the front (warp) list
+__device__ __forceinline__ void finisher_warp_body(FinSmem& S, uint32_t gw, uint32_t nw, const FinRec* fins,
+                                                   const LevelInfo* info, const double* __restrict__ ix,
+                                                   const double* __restrict__ iy,
+                                                   const uint32_t* __restrict__ iid, uint32_t* chain,
+                                                   uint32_t* fin_count_out) {
+    const int lane = threadIdx.x & 31;
     const unsigned lt = lanemask_lt();
     const uint32_t nfin = info->nfin;
-    for (uint32_t f = blockIdx.x * kFinWarps + warp; f < nfin; f += gridDim.x * kFinWarps) {
+    for (uint32_t f = gw; f < nfin; f += nw) {
         const FinRec rec = fins[f];
         const uint32_t m = rec.c.m;
         VQB_CHECK(m >= 2 && m <= kFinSmall, 30, m, f);
@@ -1109,7 +1108,6 @@ __global__ void __launch_bounds__(kFinWarps * 32) finisher_kernel(
         if (lane == 0) fin_count_out[f] = emitted;
         __syncwarp();
     }
-    (void)chain_count;
 }
 
 // ===========================================================================
@@ -1169,15 +1167,11 @@ __device__ __forceinline__ unsigned long long fc_key(const FinCtaSmem& S, int cp
     return key_of(lat_off(fx, fy, S.x[lid], S.y[lid]));
 }
 
-__global__ void __launch_bounds__(kFcThreads) finisher_cta_kernel(const FinRec* fins, const LevelInfo* info,
-                                                                  uint32_t fin_cap,
-                                                                  const double* __restrict__ ix,
-                                                                  const double* __restrict__ iy,
-                                                                  const uint32_t* __restrict__ iid,
-                                                                  uint32_t* chain, uint32_t* fin_count) {
-    VQB_PDL();
-    extern __shared__ __align__(16) unsigned char fc_dsm[];
-    FinCtaSmem& S = *reinterpret_cast<FinCtaSmem*>(fc_dsm);
+__device__ __forceinline__ void finisher_cta_body(FinCtaSmem& S, const FinRec* fins, const LevelInfo* info,
+                                                  uint32_t fin_cap, const double* __restrict__ ix,
+                                                  const double* __restrict__ iy,
+                                                  const uint32_t* __restrict__ iid, uint32_t* chain,
+                                                  uint32_t* fin_count) {
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint32_t nfin2 = info->nfin2;
     for (uint32_t f = blockIdx.x; f < nfin2; f += gridDim.x) {
@@ -1363,6 +1357,30 @@ __global__ void __launch_bounds__(kFcThreads) finisher_cta_kernel(const FinRec* 
     }
 }
 
+// Both finishers of a level in one launch (kFcThreads per CTA): first the
+// CTA segments (one CTA each), then the warp segments (one warp each), in the
+// same shared memory.
+union FinAllSmem {
+    FinCtaSmem cta;
+    FinSmem warp[kFcThreads / 32];
+};
+
+__global__ void __launch_bounds__(kFcThreads) finisher_all_kernel(const FinRec* fins, const LevelInfo* info,
+                                                                  uint32_t fin_cap,
+                                                                  const double* __restrict__ ix,
+                                                                  const double* __restrict__ iy,
+                                                                  const uint32_t* __restrict__ iid,
+                                                                  uint32_t* chain, uint32_t* fin_count) {
+    VQB_PDL();
+    extern __shared__ __align__(16) unsigned char fc_dsm[];
+    FinAllSmem& U = *reinterpret_cast<FinAllSmem*>(fc_dsm);
+    finisher_cta_body(U.cta, fins, info, fin_cap, ix, iy, iid, chain, fin_count);
+    __syncthreads();
+    const uint32_t wpb = kFcThreads / 32;
+    finisher_warp_body(U.warp[threadIdx.x >> 5], blockIdx.x * wpb + (threadIdx.x >> 5), gridDim.x * wpb, fins,
+                       info, ix, iy, iid, chain, fin_count);
+}
+
 // ===========================================================================
 // K4: in-order emission.  Bottom-up chain sizes, then top-down starts;
 // every node writes its apex between its children's chains.
@@ -1411,6 +1429,67 @@ __global__ void emit_kernel(uint32_t nslots, const uint8_t* kind, const uint32_t
             const uint64_t b = fins[f].chain_base;
             for (uint32_t i = lane; i < c; i += 32) out[st + i] = chain[b + i];
         }
+    }
+}
+
+// Whole emission of a small tree (few slots) in ONE CTA: bottom-up sizes,
+// the root frame, top-down starts and writes — the same steps as
+// size_kernel / poly_frame_kernel / emit_kernel, without one launch each.
+__global__ void __launch_bounds__(1024) emit_small_kernel(EmitAll E, const RootInfo* root, const uint32_t* chain,
+                                                          uint32_t* out, uint32_t* h_out) {
+    VQB_PDL();
+    const int lane = threadIdx.x & 31;
+    for (int l = E.nlev - 1; l >= 0; --l) {
+        const EmitLevel& L = E.lv[l];
+        const uint32_t* child_size = l + 1 < E.nlev ? E.lv[l + 1].size : nullptr;
+        for (uint32_t s = threadIdx.x; s < L.nslots; s += blockDim.x) {
+            const uint8_t k = L.kind[s];
+            uint32_t v = 0;
+            if (k == kLeaf) v = 1;
+            else if (k == kFin) v = L.fin_count[L.link[s]];
+            else if (k == kInternal) v = 1 + child_size[2 * L.link[s]] + child_size[2 * L.link[s] + 1];
+            L.size[s] = v;
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        const RootPoly& P = root->poly;
+        uint32_t pos = 0;
+        for (uint32_t j = 0; j < P.nv; ++j) {
+            const bool same_prev = j > 0 && P.ex[j] == P.ex[j - 1] && P.ey[j] == P.ey[j - 1];
+            const bool same_first = j > 0 && P.ex[j] == P.ex[0] && P.ey[j] == P.ey[0];
+            if (!same_prev && !same_first) out[pos++] = P.eidx[j];
+            E.lv[0].start[j] = pos;
+            pos += E.lv[0].size[j];
+        }
+        *h_out = pos;
+    }
+    __syncthreads();
+    const uint32_t wpb = blockDim.x >> 5;
+    for (int l = 0; l < E.nlev; ++l) {
+        const EmitLevel& L = E.lv[l];
+        const bool has_child = l + 1 < E.nlev;
+        for (uint32_t s = threadIdx.x >> 5; s < L.nslots; s += wpb) {  // one warp per slot
+            const uint8_t k = L.kind[s];
+            const uint32_t st = L.start[s];
+            if (k == kLeaf) {
+                if (lane == 0) out[st] = L.slots[s].r_idx;
+            } else if (k == kInternal && has_child) {
+                if (lane == 0) {
+                    const uint32_t c = L.link[s];
+                    const uint32_t sl = E.lv[l + 1].size[2 * c];
+                    out[st + sl] = L.slots[s].r_idx;
+                    E.lv[l + 1].start[2 * c] = st;
+                    E.lv[l + 1].start[2 * c + 1] = st + sl + 1;
+                }
+            } else if (k == kFin) {
+                const uint32_t f = L.link[s];
+                const uint32_t c = L.fin_count[f];
+                const uint64_t b = L.fins[f].chain_base;
+                for (uint32_t i = lane; i < c; i += 32) out[st + i] = chain[b + i];
+            }
+        }
+        __syncthreads();
     }
 }
 
@@ -1507,35 +1586,25 @@ void launch_tilemap(const SegRec* segs, const LevelInfo* info, uint32_t* tile_se
     pdl_launch(tilemap_kernel, g, 256, 0, st, segs, info, tile_seg);
 }
 
-void launch_finisher(const FinRec* fins, const LevelInfo* info, const double* ix,
-                     const double* iy, const uint32_t* iid, uint32_t* chain,
-                     uint32_t* fin_count, uint32_t nfin_hint, int max_grid, cudaStream_t st) {
-    uint32_t g = (nfin_hint + kFinWarps - 1) / kFinWarps;
-    if (g < 1) g = 1;
-    if (g > uint32_t(max_grid)) g = uint32_t(max_grid);
-    pdl_launch(finisher_kernel, g, kFinWarps * 32, 0, st, fins, info, ix, iy, iid, chain, nullptr,
-                                                  fin_count);
-}
-
-void launch_finisher_cta(const FinRec* fins, const LevelInfo* info, uint32_t fin_cap, const double* ix,
-                         const double* iy, const uint32_t* iid, uint32_t* chain, uint32_t* fin_count,
-                         uint32_t nfin_hint, int max_grid, cudaStream_t st) {
+void launch_finisher(const FinRec* fins, const LevelInfo* info, uint32_t fin_cap, const double* ix,
+                     const double* iy, const uint32_t* iid, uint32_t* chain, uint32_t* fin_count,
+                     uint32_t nfin_hint, int max_grid, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(finisher_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(FinCtaSmem)));
+        cudaFuncSetAttribute(finisher_all_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(FinAllSmem)));
         attr = true;
     }
     uint32_t g = nfin_hint;
     if (g < 1) g = 1;
     if (g > uint32_t(max_grid)) g = uint32_t(max_grid);
-    pdl_launch(finisher_cta_kernel, g, kFcThreads, sizeof(FinCtaSmem), st, fins, info, fin_cap, ix, iy, iid, chain,
+    pdl_launch(finisher_all_kernel, g, kFcThreads, sizeof(FinAllSmem), st, fins, info, fin_cap, ix, iy, iid, chain,
                fin_count);
 }
 
-int occupancy_finisher_cta() {
+int occupancy_finisher() {
     int b = 0;
-    cudaFuncSetAttribute(finisher_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(FinCtaSmem)));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, finisher_cta_kernel, kFcThreads, sizeof(FinCtaSmem));
+    cudaFuncSetAttribute(finisher_all_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(FinAllSmem)));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, finisher_all_kernel, kFcThreads, sizeof(FinAllSmem));
     return b;
 }
 
@@ -1557,6 +1626,11 @@ void launch_emit(uint32_t nslots, const uint8_t* kind, const uint32_t* link,
     if (g > 2368) g = 2368;
     pdl_launch(emit_kernel, g, 256, 0, st, nslots, kind, link, slots, fins, fin_count, chain, start,
                                    child_size, child_start, out);
+}
+
+void launch_emit_small(const EmitAll& e, const RootInfo* root, const uint32_t* chain, uint32_t* out,
+                       uint32_t* h_out, cudaStream_t st) {
+    pdl_launch(emit_small_kernel, 1, 1024, 0, st, e, root, chain, out, h_out);
 }
 
 void launch_legacy_poly(RootInfo* root, unsigned long long* side_ctr, cudaStream_t st) {
@@ -1583,11 +1657,6 @@ int occupancy_bootstrap() {
 int occupancy_poly_extremes() {
     int b = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, poly_extremes_kernel, 256, 0);
-    return b;
-}
-int occupancy_finisher() {
-    int b = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, finisher_kernel, kFinWarps * 32, 0);
     return b;
 }
 

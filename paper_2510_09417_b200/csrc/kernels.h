@@ -24,9 +24,9 @@ void launch_planner(const ChildRec* slots, uint32_t nslots, const LevelInfo* pre
                     int max_grid, cudaStream_t st);
 void launch_tilemap(const SegRec* segs, const LevelInfo* info, uint32_t* tile_seg,
                     uint32_t ntiles_hint, cudaStream_t st);
-void launch_finisher(const FinRec* fins, const LevelInfo* info, const double* ix,
-                     const double* iy, const uint32_t* iid, uint32_t* chain,
-                     uint32_t* fin_count, uint32_t nfin_hint, int max_grid, cudaStream_t st);
+void launch_finisher(const FinRec* fins, const LevelInfo* info, uint32_t fin_cap, const double* ix,
+                     const double* iy, const uint32_t* iid, uint32_t* chain, uint32_t* fin_count,
+                     uint32_t nfin_hint, int max_grid, cudaStream_t st);
 void launch_size(uint32_t nslots, const uint8_t* kind, const uint32_t* link,
                  const uint32_t* fin_count, const uint32_t* child_size, uint32_t* size,
                  cudaStream_t st);
@@ -38,6 +38,8 @@ void launch_poly_extremes(const double* xs, const double* ys, uint64_t n, void* 
                           uint32_t* ticket, RootInfo* root, unsigned long long* side_ctr, int grid,
                           cudaStream_t st);
 cudaError_t launch_root_filtered(const RootArgs& a, int grid, cudaStream_t st);
+void launch_emit_small(const EmitAll& e, const RootInfo* root, const uint32_t* chain, uint32_t* out,
+                       uint32_t* h_out, cudaStream_t st);
 void launch_legacy_poly(RootInfo* root, unsigned long long* side_ctr, cudaStream_t st);
 void launch_poly_frame(const RootInfo* root, const uint32_t* size2, uint32_t* start2, uint32_t* out,
                        uint32_t* h_out, cudaStream_t st);
@@ -45,10 +47,7 @@ size_t plan_agg_bytes();
 int occupancy_root(bool stable);
 int occupancy_level(bool stable);
 int occupancy_finisher();
-int occupancy_finisher_cta();
-void launch_finisher_cta(const FinRec* fins, const LevelInfo* info, uint32_t fin_cap, const double* ix,
-                         const double* iy, const uint32_t* iid, uint32_t* chain, uint32_t* fin_count,
-                         uint32_t nfin_hint, int max_grid, cudaStream_t st);
+
 int occupancy_filtered();
 int occupancy_poly_extremes();
 int occupancy_extremes();
