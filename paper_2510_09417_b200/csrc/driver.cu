@@ -124,7 +124,7 @@ class Engine {
         // one full wave each
         grid_ext_ = sms_ * std::max(1, std::min(8, occupancy_extremes()));
         grid_boot_ = sms_ * std::max(1, std::min(8, occupancy_bootstrap()));
-        grid_poly_ = sms_ * std::max(1, std::min(8, occupancy_poly_extremes()));
+        grid_poly_ = sms_ * std::max(1, std::min(8, occupancy_poly_sample()));
         stream_grid_ = std::max(std::max(grid_ext_, grid_boot_), grid_poly_);
         VQB_TRACE("engine: allocations");
         ck(cudaMalloc(&ctrs_, 64 * sizeof(uint32_t)), "cudaMalloc ctrs");
@@ -470,7 +470,12 @@ class Engine {
     // Default: K1' (8 exact directional extremes + finiteness) then KB'
     // (level 1 behind the octagon filter).  Returns the level-2 slot count.
     uint32_t run_root_filtered(const double* dx, const double* dy, uint64_t n, cudaStream_t st) {
-        tk(0, st, [&] { launch_poly_extremes(dx, dy, n, partials_.p, &ctrs_[3], root_, side_ctr(), grid_poly_, st); });
+        tk(0, st, [&] { launch_extremes(dx, dy, n, partials_.p, &ctrs_[3], root_, grid_ext_, st); });
+        {
+            // the sample is 1/16 of the points: a smaller grid
+            const int g = std::max(1, std::min<int>(grid_poly_, int(n / (16 * 256 * 8)) + 1));
+            tk(0, st, [&] { launch_poly_sample(dx, dy, n, partials_.p, &ctrs_[5], root_, side_ctr(), g, st); });
+        }
         upload_root_consts(root_, st);
         stats_.bytes_extremes = 8 * n + n;  // x, then x and y of the 1/16 sample
         stats_.bytes_bootstrap = 0;

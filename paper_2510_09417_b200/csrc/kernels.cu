@@ -64,6 +64,7 @@ __device__ __forceinline__ ExtKey shfl_key(const ExtKey& k, int x) {
 
 struct ExtPartial {
     ExtKey lo, hi;
+    uint32_t nonfinite, pad;
 };
 
 constexpr int kStreamUnroll = 4;  // double2 loads per array per thread per iteration
@@ -78,7 +79,9 @@ __global__ void __launch_bounds__(256) extremes_kernel(const double* __restrict_
     // unless y decides (checked on the slow path)
     double lo_x = kInf, hi_x = -kInf;
     uint32_t lo_i = 0xffffffffu, hi_i = 0xffffffffu;
+    bool bad = false;  // non-finite x (vqhull_c.cpp:32-34; y is checked by the pass that reads it)
     auto visit = [&](uint32_t i, double x) {
+        bad |= nonfinite_bits(x);
         const bool lt = x < lo_x, gt = x > hi_x;
         const bool tie = (x == lo_x) | (x == hi_x);
         // grid-stride trip counts differ per lane: vote over the lanes that
@@ -133,7 +136,11 @@ __global__ void __launch_bounds__(256) extremes_kernel(const double* __restrict_
     }
     __shared__ ExtKey s_lo[8], s_hi[8];
     __shared__ bool s_last;
+    __shared__ uint32_t s_bad;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) s_bad = 0;
+    __syncthreads();
+    if (bad) atomicOr(&s_bad, 1u);
     if (lane == 0) { s_lo[warp] = lo; s_hi[warp] = hi; }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -143,6 +150,7 @@ __global__ void __launch_bounds__(256) extremes_kernel(const double* __restrict_
         }
         partials[blockIdx.x].lo = lo;
         partials[blockIdx.x].hi = hi;
+        partials[blockIdx.x].nonfinite = s_bad;
         __threadfence();
         const uint32_t t = atomicAdd(ticket, 1u);
         s_last = (t == gridDim.x - 1);
@@ -152,12 +160,14 @@ __global__ void __launch_bounds__(256) extremes_kernel(const double* __restrict_
     __threadfence();
     ExtKey L, H;
     L.valid = H.valid = 0;
+    uint32_t nb = 0;
     for (uint32_t b = threadIdx.x; b < gridDim.x; b += blockDim.x) {
         ExtKey a, c;
         a.x = __ldcg(&partials[b].lo.x); a.y = __ldcg(&partials[b].lo.y);
         a.idx = __ldcg(&partials[b].lo.idx); a.valid = __ldcg(&partials[b].lo.valid);
         c.x = __ldcg(&partials[b].hi.x); c.y = __ldcg(&partials[b].hi.y);
         c.idx = __ldcg(&partials[b].hi.idx); c.valid = __ldcg(&partials[b].hi.valid);
+        nb |= __ldcg(&partials[b].nonfinite);
         if (lo_better(a, L)) L = a;
         if (hi_better(c, H)) H = c;
     }
@@ -167,8 +177,10 @@ __global__ void __launch_bounds__(256) extremes_kernel(const double* __restrict_
         if (lo_better(a, L)) L = a;
         ExtKey b = shfl_key(H, s);
         if (hi_better(b, H)) H = b;
+        nb |= __shfl_xor_sync(kFull, nb, s);
     }
     __syncthreads();
+    if (lane == 0 && nb) atomicOr(&s_bad, 2u);
     if (lane == 0) { s_lo[warp] = L; s_hi[warp] = H; }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -182,6 +194,7 @@ __global__ void __launch_bounds__(256) extremes_kernel(const double* __restrict_
         root->py = L.y;
         root->qx = H.x;
         root->qy = H.y;
+        root->nonfinite = (s_bad & 2u) ? 1u : 0u;
         *ticket = 0;  // re-arm for the next launch
     }
 }
@@ -350,10 +363,12 @@ __global__ void __launch_bounds__(256) bootstrap_argmax_kernel(
 }
 
 // ===========================================================================
-// K1' (default root stage): find_extremes (geometry.cpp:7-36) over every
-// point, exactly as K1 (x read for every point, y only on exact x ties),
-// plus the octagon filter's 8 vertices from a sample of the input (every
-// 16th group of 256 points, x and y): min/max x, y, x+y, x-y.  The filter
+// K1' (default root stage) = K1 (extremes_kernel: find_extremes,
+// geometry.cpp:7-36, over every point; x read for every point, y only on
+// exact x ties; finiteness of x) + this sample kernel: the octagon filter's
+// 8 vertices from a sample of the input (every 16th group of 256 points, x
+// and y): min/max x, y, x+y, x-y.  Two kernels, so the x stream keeps K1's
+// small register footprint (occupancy, loads in flight).  The filter
 // only needs its vertices to be input points (see poly_finish), not exact
 // extremes, so a sample costs 1/16 of a y pass and loses almost nothing.  Finiteness of
 // x is checked here, of y by the root pass that reads every y.
@@ -571,7 +586,7 @@ __device__ __noinline__ void poly_finish(const PolyPartial& F, const double* __r
     R.qx = H.x; R.qy = H.y;
 }
 
-__global__ void __launch_bounds__(256, 3) poly_extremes_kernel(const double* __restrict__ xs,
+__global__ void __launch_bounds__(256, 2) poly_sample_kernel(const double* __restrict__ xs,
                                                             const double* __restrict__ ys, uint64_t n,
                                                             PolyPartial* partials, uint32_t* ticket,
                                                             RootInfo* root, unsigned long long* side_ctr) {
@@ -584,19 +599,6 @@ __global__ void __launch_bounds__(256, 3) poly_extremes_kernel(const double* __r
     bool bad = false;
     double ssx = 0.0, ssy = 0.0;  // sample sums (non-finite input is rejected anyway)
     uint32_t ssn = 0;
-    auto visit_x = [&](uint32_t i, double x) {
-        bad |= nonfinite_bits(x);
-        const bool lt = x < lo_x, gt = x > hi_x;
-        const bool tie = (x == lo_x) | (x == hi_x);
-        if (__any_sync(__activemask(), tie)) {
-            if (x == lo_x && lo_i != kNoIdx && ys[i] < ys[lo_i]) lo_i = i;
-            if (x == hi_x && hi_i != kNoIdx && ys[i] > ys[hi_i]) hi_i = i;
-        }
-        lo_i = lt ? i : lo_i;
-        lo_x = lt ? x : lo_x;
-        hi_i = gt ? i : hi_i;
-        hi_x = gt ? x : hi_x;
-    };
     auto visit_xy = [&](uint32_t i, double x, double y) {
         const double s = __dadd_rn(x, y), d = __dsub_rn(x, y);
         ssx = __dadd_rn(ssx, x);
@@ -618,30 +620,7 @@ __global__ void __launch_bounds__(256, 3) poly_extremes_kernel(const double* __r
         const uint32_t npair = uint32_t(n / 2);
         const double2* x2 = reinterpret_cast<const double2*>(xs);
         const double2* y2 = reinterpret_cast<const double2*>(ys);
-        // phase 1: x of every point (find_extremes); 8 x 16 B in flight per
-        // thread (loaded HBM latency is ~2.5 us at full bandwidth)
-        constexpr int U = 2 * kStreamUnroll;
-        const uint32_t np1 = npair;
-        uint32_t j = tid;
-        for (; j + (U - 1) * stride < np1; j += U * stride) {
-            double2 v[U];
-#pragma unroll
-            for (int u = 0; u < U; ++u) v[u] = __ldcs(&x2[j + u * stride]);
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                visit_x(2 * (j + u * stride), v[u].x);
-                visit_x(2 * (j + u * stride) + 1, v[u].y);
-            }
-        }
-        for (; j < np1; j += stride) {
-            const double2 v = __ldcs(&x2[j]);
-            visit_x(2 * j, v.x);
-            visit_x(2 * j + 1, v.y);
-        }
-        if ((n & 1) && tid == 0) {
-            visit_x(uint32_t(n - 1), xs[n - 1]);
-            visit_xy(uint32_t(n - 1), xs[n - 1], ys[n - 1]);
-        }
+        if ((n & 1) && tid == 0) visit_xy(uint32_t(n - 1), xs[n - 1], ys[n - 1]);
         // phase 2: x and y of the sampled groups (every 16th run of 128 pairs)
         const uint32_t ngroups = (npair + (1u << kSampleShift) - 1) >> kSampleShift;
         const uint32_t nsg = (ngroups + kSampleMask) / (kSampleMask + 1);
@@ -676,10 +655,8 @@ __global__ void __launch_bounds__(256, 3) poly_extremes_kernel(const double* __r
             visit_xy(2 * q + 1, v.y, w.y);
         }
     } else {
-        for (uint32_t i = tid; i < n; i += stride) {
-            visit_x(i, xs[i]);
+        for (uint32_t i = tid; i < n; i += stride)
             if (((i >> (kSampleShift + 1)) & kSampleMask) == 0) visit_xy(i, xs[i], ys[i]);
-        }
     }
     // reductions: thread -> CTA partial -> (last CTA, all threads) -> final
     ExtKey lo{lo_x, 0.0, lo_i, lo_i != kNoIdx};
@@ -732,7 +709,10 @@ __global__ void __launch_bounds__(256, 3) poly_extremes_kernel(const double* __r
     block_reduce_poly(lo, hi, av, ai, sx, sy, sn, nb, s_w);
     if (threadIdx.x != 0) return;
     __shared__ PolyPartial s_fin;
-    s_fin.lo = lo; s_fin.hi = hi; s_fin.nonfinite = nb; s_fin.pad = 0u;
+    // p, q and the finiteness of x come from K1 (extremes_kernel, same stream)
+    s_fin.lo = ExtKey{root->px, root->py, root->p_idx, 1u};
+    s_fin.hi = ExtKey{root->qx, root->qy, root->q_idx, 1u};
+    s_fin.nonfinite = root->nonfinite; s_fin.pad = 0u;
     s_fin.sx = sx; s_fin.sy = sy; s_fin.sn = sn;
 #pragma unroll
     for (int q = 0; q < 8; ++q) { s_fin.av[q] = av[q]; s_fin.ai[q] = ai[q]; }
@@ -1546,10 +1526,10 @@ void launch_bootstrap(const double* xs, const double* ys, uint64_t n, void* part
                                                   ticket, root);
 }
 
-void launch_poly_extremes(const double* xs, const double* ys, uint64_t n, void* partials,
-                          uint32_t* ticket, RootInfo* root, unsigned long long* side_ctr, int grid,
-                          cudaStream_t st) {
-    pdl_launch(poly_extremes_kernel, grid, 256, 0, st, xs, ys, n, static_cast<PolyPartial*>(partials), ticket,
+void launch_poly_sample(const double* xs, const double* ys, uint64_t n, void* partials,
+                        uint32_t* ticket, RootInfo* root, unsigned long long* side_ctr, int grid,
+                        cudaStream_t st) {
+    pdl_launch(poly_sample_kernel, grid, 256, 0, st, xs, ys, n, static_cast<PolyPartial*>(partials), ticket,
                                                root, side_ctr);
 }
 
@@ -1654,9 +1634,9 @@ int occupancy_bootstrap() {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, bootstrap_argmax_kernel, 256, 0);
     return b;
 }
-int occupancy_poly_extremes() {
+int occupancy_poly_sample() {
     int b = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, poly_extremes_kernel, 256, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, poly_sample_kernel, 256, 0);
     return b;
 }
 

@@ -34,9 +34,9 @@ void launch_emit(uint32_t nslots, const uint8_t* kind, const uint32_t* link,
                  const ChildRec* slots, const FinRec* fins, const uint32_t* fin_count,
                  const uint32_t* chain, const uint32_t* start, const uint32_t* child_size,
                  uint32_t* child_start, uint32_t* out, cudaStream_t st);
-void launch_poly_extremes(const double* xs, const double* ys, uint64_t n, void* partials,
-                          uint32_t* ticket, RootInfo* root, unsigned long long* side_ctr, int grid,
-                          cudaStream_t st);
+void launch_poly_sample(const double* xs, const double* ys, uint64_t n, void* partials,
+                        uint32_t* ticket, RootInfo* root, unsigned long long* side_ctr, int grid,
+                        cudaStream_t st);
 cudaError_t launch_root_filtered(const RootArgs& a, int grid, cudaStream_t st);
 void launch_emit_small(const EmitAll& e, const RootInfo* root, const uint32_t* chain, uint32_t* out,
                        uint32_t* h_out, cudaStream_t st);
@@ -49,7 +49,7 @@ int occupancy_level(bool stable);
 int occupancy_finisher();
 
 int occupancy_filtered();
-int occupancy_poly_extremes();
+int occupancy_poly_sample();
 int occupancy_extremes();
 int occupancy_bootstrap();
 uint32_t read_and_clear_fault();
