@@ -102,11 +102,16 @@ typedef struct vqhull_stats {
     uint64_t bytes_root_partition;
     uint64_t bytes_levels;
     uint64_t bytes_finisher;
-    uint32_t root_filtered;     /* 1: root stage = 8-direction extremes + level 1
-                                   behind the octagon filter; 0: find_extremes +
-                                   bootstrap + fused levels 1+2 */
+    uint32_t root_filtered;     /* 2 (default): split root = octagon from a 1/16
+                                   sample, one filter pass over every point (exact
+                                   p, q of the survivors), level 1 over the
+                                   survivors; 1: exact extremes pass + level 1
+                                   behind the octagon filter in one pass;
+                                   0: find_extremes + bootstrap + fused levels 1+2 */
     uint32_t root_filter_on;    /* the octagon filter could drop points (coordinate
                                    magnitudes in range) */
+    uint32_t root_reruns;       /* 1: a split-root survivor lay beyond 2^12 x the
+                                   octagon's scale, the call was rerun unfiltered */
 } vqhull_stats;
 
 int vqhull_cuda_get_stats(vqhull_stats* out);
@@ -128,6 +133,13 @@ int vqhull_cuda_set_stable(int stable);
  * recursion is the reference's in both; hull outputs are identical.  The
  * environment variable VQHULL_ROOT=reference sets 1. */
 int vqhull_cuda_set_root_reference(int reference);
+
+/* Root stage, all three giving identical hulls: 0 (default) split root —
+ * octagon from a 1/16 sample, one filter pass over every point (survivors,
+ * exact p and q), level 1 over the survivors; 1 one-pass octagon root (exact
+ * extremes pass, then level 1 behind the filter); 2 = set_root_reference(1).
+ * Returns 1 for another mode.  VQHULL_ROOT=octagon|reference sets 1|2. */
+int vqhull_cuda_set_root_mode(int mode);
 
 /* Human-readable description of the last CUDA error (thread-local). */
 const char* vqhull_cuda_last_error(void);

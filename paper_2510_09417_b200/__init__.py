@@ -67,6 +67,7 @@ class Stats(C.Structure):
         ("bytes_finisher", C.c_uint64),
         ("root_filtered", C.c_uint32),
         ("root_filter_on", C.c_uint32),
+        ("root_reruns", C.c_uint32),
     ]
 
     def as_dict(self) -> dict:
@@ -97,6 +98,7 @@ def lib() -> C.CDLL:
         L.vqhull_cuda_set_timing.argtypes = [C.c_int]
         L.vqhull_cuda_set_stable.argtypes = [C.c_int]
         L.vqhull_cuda_set_root_reference.argtypes = [C.c_int]
+        L.vqhull_cuda_set_root_mode.argtypes = [C.c_int]
         L.vqhull_cuda_last_error.restype = C.c_char_p
         L.vqhull_b200_version.restype = C.c_char_p
         L.vqhull_generate.argtypes = [C.c_int, C.c_uint64, C.c_uint64, C.c_uint64, C.c_void_p,
@@ -252,6 +254,17 @@ def set_root_reference(on: bool) -> None:
     """Root stage without the octagon filter: find_extremes, bootstrap arg-max
     and the fused levels-1+2 pass.  Same hull either way."""
     _check(lib().vqhull_cuda_set_root_reference(int(bool(on))), "vqhull_cuda_set_root_reference")
+
+
+ROOT_MODES = {"split": 0, "octagon": 1, "reference": 2}
+
+
+def set_root_mode(mode: str) -> None:
+    """Root stage: "split" (default: sampled octagon, filter pass, level 1 over
+    the survivors), "octagon" (exact extremes pass + filtered level 1 in one
+    pass) or "reference" (find_extremes, bootstrap, fused levels 1+2).  Same
+    hull in every mode."""
+    _check(lib().vqhull_cuda_set_root_mode(ROOT_MODES[mode]), "vqhull_cuda_set_root_mode")
 
 
 def set_timing(on: bool) -> None:

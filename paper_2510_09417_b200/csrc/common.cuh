@@ -150,6 +150,37 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 // arrays through idx, and the reference's lexicographic (x, y) rule plus the
 // first-occurrence index rule decide.  Equivalent to prefer() on Best.
 // ---------------------------------------------------------------------------
+// find_extremes key (geometry.cpp:7-36): lo = lexicographic min of (x, y,
+// index); hi = max x, then max y, then min index.
+struct ExtKey {
+    double x, y;
+    uint32_t idx;
+    uint32_t valid;
+};
+
+__device__ __forceinline__ bool lo_better(const ExtKey& a, const ExtKey& b) {
+    if (!a.valid) return false;
+    if (!b.valid) return true;
+    if (a.x != b.x) return a.x < b.x;
+    if (a.y != b.y) return a.y < b.y;
+    return a.idx < b.idx;
+}
+__device__ __forceinline__ bool hi_better(const ExtKey& a, const ExtKey& b) {
+    if (!a.valid) return false;
+    if (!b.valid) return true;
+    if (a.x != b.x) return a.x > b.x;
+    if (a.y != b.y) return a.y > b.y;
+    return a.idx < b.idx;
+}
+__device__ __forceinline__ ExtKey shfl_key(const ExtKey& k, int x) {
+    ExtKey o;
+    o.x = __shfl_xor_sync(kFull, k.x, x);
+    o.y = __shfl_xor_sync(kFull, k.y, x);
+    o.idx = __shfl_xor_sync(kFull, k.idx, x);
+    o.valid = __shfl_xor_sync(kFull, k.valid, x);
+    return o;
+}
+
 constexpr unsigned long long kNoKey = ~0ull;
 constexpr uint32_t kNoIdx = 0xffffffffu;
 

@@ -121,6 +121,8 @@ class Engine {
         occ_level_stable_ = std::max(1, occupancy_level(true));
         occ_fin_ = std::max(1, occupancy_finisher());
         occ_filt_ = std::max(1, occupancy_filtered());
+        occ_filter_ = std::max(1, occupancy_filter());
+        occ_tail_ = std::max(1, std::min(2, occupancy_tail()));
         // one full wave each
         grid_ext_ = sms_ * std::max(1, std::min(8, occupancy_extremes()));
         grid_boot_ = sms_ * std::max(1, std::min(8, occupancy_bootstrap()));
@@ -134,6 +136,7 @@ class Engine {
         ck(cudaMallocHost(&h_info_, sizeof(LevelInfo) * 2), "cudaMallocHost");
         ck(cudaMallocHost(&h_root_, sizeof(RootInfo)), "cudaMallocHost");
         ck(cudaMallocHost(&h_word_, 64), "cudaMallocHost");
+        ck(cudaMallocHost(&h_tail_, 16 + sizeof(LevelInfo) * (kTailLevels + 2)), "cudaMallocHost");
         partials_.ensure(partial_bytes(stream_grid_), nullptr);
         VQB_TRACE("engine: synchronize");
         ck(cudaDeviceSynchronize(), "init");
@@ -159,8 +162,10 @@ class Engine {
 
         // ---- root stage: polygon + first partition (levels 1+2 in reference mode)
         const bool aligned = ((reinterpret_cast<uintptr_t>(dx) | reinterpret_cast<uintptr_t>(dy)) & 15u) == 0;
-        const bool filtered = !stable_ && !root_reference_ && aligned && !getenv("VQB_NO_TMA");
-        uint32_t nslots = filtered ? run_root_filtered(dx, dy, n, st) : run_root_reference(dx, dy, n, st);
+        const bool filtered = !stable_ && !root_reference_ && !force_reference_ && aligned && !getenv("VQB_NO_TMA");
+        const bool split = filtered && !root_octagon_;
+        uint32_t nslots = split ? run_root_split(dx, dy, n, st)
+                                : (filtered ? run_root_filtered(dx, dy, n, st) : run_root_reference(dx, dy, n, st));
         // finiteness verdict, octagon verdict, sizes for the byte accounting
         ck(cudaMemcpyAsync(h_root_, root_, sizeof(RootInfo), cudaMemcpyDeviceToHost, st), "d2h root");
 
@@ -183,6 +188,12 @@ class Engine {
         int in = 0;
         int lvl = 2;
         lmax_ = -1;
+        if (split && !lean && use_tail_) {
+            // KT: every level in one persistent launch while they stay small
+            const int rc = run_tail(dx, dy, n, nslots, st, &lvl, &in, &S);
+            if (rc == VQHULL_EINVAL) return rc;
+            if (rc < 0) return rerun_unfiltered(dx, dy, n, d_out, h, st);
+        }
         const int batch = lean ? 1 : kLevelBatch;
         while (lmax_ < 0) {
             const int first = lvl;
@@ -220,6 +231,7 @@ class Engine {
                         ck(cudaStreamSynchronize(st), "sync");
                         return VQHULL_EINVAL;
                     }
+                    if (lvl == 2 && split && h_root_->unsafe) return rerun_unfiltered(dx, dy, n, d_out, h, st);
                     const LevelInfo li = *h_info_;
                     nseg_b = li.nseg;
                     ntiles_b = li.ntiles;
@@ -269,6 +281,7 @@ class Engine {
                 ck(cudaStreamSynchronize(st), "sync");
                 return VQHULL_EINVAL;
             }
+            if (first == 2 && split && h_root_->unsafe) return rerun_unfiltered(dx, dy, n, d_out, h, st);
             if (h_info_->nseg == 0) {
                 // the recursion ended in this batch: fetch all level infos
                 hinfo_.resize(lvl);
@@ -298,7 +311,7 @@ class Engine {
         }
         stats_.levels = uint32_t(lmax_);
         stats_.bytes_root_partition = 16 * n + 20 * stats_.survivors_root;
-        stats_.root_filtered = filtered ? 1u : 0u;
+        stats_.root_filtered = filtered ? (split ? 2u : 1u) : 0u;
         if (filtered) stats_.root_filter_on = h_root_->poly.filter;
 
         // ---- emission: bottom-up sizes, root frame, top-down starts
@@ -474,7 +487,7 @@ class Engine {
         {
             // the sample is 1/16 of the points: a smaller grid
             const int g = std::max(1, std::min<int>(grid_poly_, int(n / (16 * 256 * 8)) + 1));
-            tk(0, st, [&] { launch_poly_sample(dx, dy, n, partials_.p, &ctrs_[5], root_, side_ctr(), g, st); });
+            tk(0, st, [&] { launch_poly_sample(dx, dy, n, partials_.p, &ctrs_[5], sample_keys(), root_, side_ctr(), g, true, st); });
         }
         upload_root_consts(root_, st);
         stats_.bytes_extremes = 8 * n + n;  // x, then x and y of the 1/16 sample
@@ -495,6 +508,168 @@ class Engine {
         ra.children = L2.slots.as<ChildRec>(); ra.ntiles = ntiles_root;
         tk(2, st, [&] { ck(launch_root_filtered(ra, grid, st), "filtered root launch"); });
         return 2;
+    }
+
+    // KT (tail.cu): levels lvl.. in one cooperative launch.  Returns 0 and sets
+    // lmax_ when the recursion ended inside it; otherwise 0 with (*lvl, *in,
+    // *S) set to the level the host loop resumes at.  VQHULL_EINVAL for
+    // non-finite input, -1 for an `unsafe` split root (caller reruns).
+    int run_tail(const double* dx, const double* dy, uint64_t n, uint32_t nslots, cudaStream_t st, int* lvl,
+                 int* in, uint32_t* S) {
+        const int l0 = *lvl;
+        const int nlev = kTailLevels;
+        for (int li = 0; li < nlev; ++li) {
+            LevelTables& T = level(l0 + li);
+            T.kind.ensure(kTailSlots, st);
+            T.link.ensure(size_t(kTailSlots) * 4, st);
+            T.size.ensure(size_t(kTailSlots) * 4, st);
+            T.start.ensure(size_t(kTailSlots) * 4, st);
+            T.fin_count.ensure(size_t(kTailSlots) * 4, st);
+            T.segs.ensure(size_t(kTailSlots) * sizeof(SegRec), st);
+            T.fins.ensure(size_t(kTailSlots) * sizeof(FinRec), st);
+            T.slots.ensure(size_t(2) * kTailSlots * sizeof(ChildRec), st, li == 0);  // level l0's slots are live
+        }
+        info_.ensure(size_t(l0 + nlev + 1) * sizeof(LevelInfo), st, true);
+        const uint64_t tiles = n / kTile + kTailSlots + 1;
+        ensure_lookback(kTailSlots / 1024 + 1, st);
+        segaux_.ensure(segaux_bytes(kTailSlots), st);
+        tile_seg_.ensure(tiles * 4, st);
+        part_.ensure(tiles * 2 * sizeof(Best), st);
+        bufs_[0].ensure(n, st);
+        bufs_[1].ensure(n, st);
+        chain_.ensure(n * 4 + 4, st, true);
+        TailArgs ta;
+        std::memset(&ta, 0, sizeof ta);
+        for (int li = 0; li < nlev; ++li) {
+            LevelTables& T = level(l0 + li);
+            ta.lv[li].slots = T.slots.as<ChildRec>();
+            ta.lv[li].segs = T.segs.as<SegRec>();
+            ta.lv[li].fins = T.fins.as<FinRec>();
+            ta.lv[li].kind = T.kind.as<uint8_t>();
+            ta.lv[li].link = T.link.as<uint32_t>();
+            ta.lv[li].fin_count = T.fin_count.as<uint32_t>();
+        }
+        ta.info = info_.as<LevelInfo>();
+        ta.prev0 = l0 == 2 ? nullptr : info_.as<LevelInfo>() + (l0 - 1);
+        ta.l0 = l0;
+        ta.nlev = nlev;
+        ta.nslots0 = nslots;
+        ta.max_slots = kTailSlots;
+        for (int b = 0; b < 2; ++b) {
+            ta.bx[b] = bufs_[b].x.as<double>();
+            ta.by[b] = bufs_[b].y.as<double>();
+            ta.bid[b] = bufs_[b].id.as<uint32_t>();
+        }
+        ta.buf_cap = std::min(bufs_[0].x.cap, bufs_[1].x.cap) / 8;
+        ta.gx = dx;
+        ta.gy = dy;
+        ta.flags = flags_.as<uint32_t>();
+        ta.aggs_v = aggs_.p;
+        ta.incs_v = incs_.p;
+        ta.epoch0 = reserve_epochs(nlev);
+        ta.plan_ctr = &ctrs_[2];
+        ta.seg_pcnt = seg_pcnt();
+        ta.seg_done = seg_done(kTailSlots);
+        ta.seg_ctr = seg_ctr(kTailSlots);
+        ta.tile_seg = tile_seg_.as<uint32_t>();
+        ta.tile_part = part_.as<Best>();
+        ta.part_cap = part_.cap / sizeof(Best);
+        ta.chain = chain_.as<uint32_t>();
+        ta.state = &ctrs_[16];
+        if (tail_trace_) {
+            trace_.ensure(8 * (1 + 6 * kTailLevels), st);
+            ck(cudaMemsetAsync(trace_.p, 0, 8 * (1 + 6 * kTailLevels), st), "memset trace");
+            ta.trace = trace_.as<unsigned long long>();
+        }
+        tk(3, st, [&] { ck(launch_tail(ta, sms_ * occ_tail_, st), "tail launch"); });
+        if (tail_trace_) {
+            std::vector<unsigned long long> tr(1 + 6 * kTailLevels);
+            ck(cudaMemcpyAsync(tr.data(), trace_.p, 8 * tr.size(), cudaMemcpyDeviceToHost, st), "d2h trace");
+            ck(cudaStreamSynchronize(st), "trace sync");
+            for (int li = 0; li < kTailLevels && tr[1 + li * 6]; ++li) {
+                fprintf(stderr, "[kt] level %d:", l0 + li);
+                for (int ph = 0; ph < 6; ++ph)
+                    if (tr[1 + li * 6 + ph]) fprintf(stderr, " %.2f", (tr[1 + li * 6 + ph] - tr[0]) * 1e-3);
+                fputc('\n', stderr);
+            }
+        }
+        ck(cudaMemcpyAsync(h_tail_, &ctrs_[16], 8, cudaMemcpyDeviceToHost, st), "d2h tail state");
+        ck(cudaMemcpyAsync(h_tail_ + 2, info_.as<LevelInfo>() + l0, sizeof(LevelInfo) * nlev,
+                           cudaMemcpyDeviceToHost, st), "d2h tail infos");
+        VQB_TRACE("hull: tail sync");
+        ck(cudaStreamSynchronize(st), "tail sync");
+        if (h_root_->nonfinite) return VQHULL_EINVAL;
+        if (h_root_->unsafe) return -1;
+        const uint32_t at = h_tail_[0], how = h_tail_[1];
+        const LevelInfo* li = reinterpret_cast<const LevelInfo*>(h_tail_ + 2);
+        hinfo_.resize(std::max<size_t>(hinfo_.size(), size_t(l0 + nlev)));
+        for (int l = l0; l < int(at) && l < l0 + nlev; ++l) hinfo_[l] = li[l - l0];
+        if (how == 1) {
+            hinfo_[at] = li[at - l0];
+            lmax_ = int(at);
+            VQB_TRACE("hull: tail finished at level %u", at);
+        } else {
+            if (how != 2 || int(at) < l0 || int(at) >= l0 + nlev) {
+                g_last_error = "tail kernel did not report its state (internal error)";
+                throw CudaError{cudaErrorUnknown};
+            }
+            *lvl = int(at);
+            *in = (int(at) - l0) & 1;
+            *S = int(at) == l0 ? nslots : 2u * li[at - 1 - l0].nseg;
+            VQB_TRACE("hull: tail stopped before level %u (%u slots)", at, *S);
+        }
+        return 0;
+    }
+
+    // Split root (default): K_S the octagon from a sample, then K_F the filter
+    // alone over every point (survivors + exact p, q + finiteness); the first
+    // level is the single bootstrap slot (p, q, p) over the survivors, which
+    // the level machinery partitions like any other segment.  Returns 1.
+    uint32_t run_root_split(const double* dx, const double* dy, uint64_t n, cudaStream_t st) {
+        {
+            const int g = std::max(1, std::min<int>(grid_poly_, int(n / (16 * 256 * 8)) + 1));
+            tk(0, st, [&] { launch_poly_sample(dx, dy, n, partials_.p, &ctrs_[5], sample_keys(), root_, side_ctr(), g, false, st); });
+        }
+        if (getenv("VQHULL_SAMPLE_TRACE")) print_sample_trace();
+        upload_root_consts(root_, st);
+        stats_.bytes_extremes = n;  // x and y of the 1/16 sample
+        stats_.bytes_bootstrap = 0;
+        bufs_[0].ensure(n, st);
+        const uint32_t ntiles = uint32_t((n + kTile - 1) / kTile);
+        LevelTables& L2 = level(2);
+        L2.slots.ensure(sizeof(ChildRec), st);
+        const int grid = std::max(1, std::min<int>(int(ntiles), sms_ * occ_filter_));
+        fpart_.ensure(filter_partial_bytes(grid), st);
+        FilterArgs fa;
+        std::memset(&fa, 0, sizeof fa);
+        fa.xs = dx; fa.ys = dy; fa.n = n; fa.ntiles = ntiles;
+        fa.ox = bufs_[0].x.as<double>(); fa.oy = bufs_[0].y.as<double>(); fa.oid = bufs_[0].id.as<uint32_t>();
+        fa.out_cap = bufs_[0].x.cap / 8;
+        fa.ctr = &ctrs_[12]; fa.ticket = &ctrs_[13]; fa.part = fpart_.p;
+        fa.root_w = root_; fa.slot = L2.slots.as<ChildRec>();
+        tk(2, st, [&] { ck(launch_root_filter(fa, grid, st), "root filter launch"); });
+        return 1;
+    }
+
+    // The split root's margin argument needs every survivor within 2^12 of
+    // the octagon's scale; a heavy-tailed input that violates it (the
+    // sample missed a far outlier) is hulled again without the filter.
+    int rerun_unfiltered(const double* dx, const double* dy, uint64_t n, uint32_t* d_out, uint64_t* h,
+                         cudaStream_t st) {
+        VQB_TRACE("hull: survivor beyond 2^12 M, rerun unfiltered");
+        end_timing(st);
+        ck(cudaStreamSynchronize(st), "sync");
+        force_reference_ = true;
+        int rc;
+        try {
+            rc = hull(dx, dy, n, d_out, h, st);
+        } catch (...) {
+            force_reference_ = false;
+            throw;
+        }
+        force_reference_ = false;
+        stats_.root_reruns = 1;
+        return rc;
     }
 
     // Reference mode: K1 find_extremes, KA bootstrap arg-max, KB levels 1+2
@@ -530,6 +705,16 @@ class Engine {
     LevelTables& level(int l) {
         if (levels_.size() <= size_t(l)) levels_.resize(l + 1);
         return levels_[l];
+    }
+
+    uint32_t reserve_epochs(int k) {  // k consecutive epochs (persistent kernel levels)
+        uint32_t e = next_epoch();
+        if (e + uint32_t(k) >= 0x3fffffffu) {
+            epoch_ = 0;
+            e = next_epoch();
+        }
+        epoch_ += uint32_t(k);
+        return e;
     }
 
     uint32_t next_epoch() {
@@ -635,7 +820,17 @@ class Engine {
     int dev_ = 0;
     int sms_ = 148;
     int occ_root_ = 1, occ_root_stable_ = 1, occ_level_ = 1, occ_level_stable_ = 1, occ_fin_ = 1;
-    int stream_grid_ = 592, grid_ext_ = 592, grid_boot_ = 592, grid_poly_ = 592, occ_filt_ = 1;
+    int stream_grid_ = 592, grid_ext_ = 592, grid_boot_ = 592, grid_poly_ = 592, occ_filt_ = 1, occ_filter_ = 1;
+    bool force_reference_ = false;
+    int occ_tail_ = 1;
+    // VQHULL_TAIL=0: levels only through the host-driven kernels
+    bool use_tail_ = !(getenv("VQHULL_TAIL") && getenv("VQHULL_TAIL")[0] == '0');
+    static constexpr uint32_t kTailSlots = 4096;  // slot capacity of the persistent kernel's tables
+    uint32_t* h_tail_ = nullptr;
+    bool tail_trace_ = getenv("VQHULL_TAIL_TRACE") != nullptr;
+    DevBuf trace_;  // set while rerunning an `unsafe` split-root call
+    // VQHULL_ROOT=octagon: the one-pass filtered root (K1' + KB'), kept for comparison
+    bool root_octagon_ = getenv("VQHULL_ROOT") != nullptr && std::string(getenv("VQHULL_ROOT")) == "octagon";
     bool root_reference_ = getenv("VQHULL_ROOT") != nullptr && std::string(getenv("VQHULL_ROOT")) == "reference";
     uint32_t* ctrs_ = nullptr;
     RootInfo* root_ = nullptr;
@@ -644,7 +839,7 @@ class Engine {
     RootInfo* h_root_ = nullptr;
     uint32_t* h_word_ = nullptr;
     DevBuf partials_, flags_, aggs_, incs_, tile_seg_, chain_, info_, scratch_, out_;
-    DevBuf status_, part_, segaux_;
+    DevBuf status_, part_, segaux_, fpart_;
     bool stable_ = getenv("VQHULL_STABLE") != nullptr && getenv("VQHULL_STABLE")[0] == '1';
 
     // per-segment scratch of the level kernel: partial count, finished tiles
@@ -656,10 +851,19 @@ class Engine {
         return reinterpret_cast<unsigned long long*>(segaux_.as<char>() + ((size_t(ns) * 8 + 7) & ~size_t(7)));
     }
     unsigned long long* side_ctr() { return reinterpret_cast<unsigned long long*>(ctrs_ + 8); }
+    // the sample kernel's 8 directional keys (zero between calls)
+    unsigned long long* sample_keys() { return reinterpret_cast<unsigned long long*>(ctrs_ + 32); }
 
    public:
     void set_stable(bool s) { stable_ = s; }
-    void set_root_reference(bool r) { root_reference_ = r; }
+    void set_root_reference(bool r) {
+        root_reference_ = r;
+        root_octagon_ = false;
+    }
+    void set_root_mode(int m) {  // 0 split (default), 1 one-pass octagon, 2 reference
+        root_reference_ = m == 2;
+        root_octagon_ = m == 1;
+    }
     bool stable() const { return stable_; }
 
    private:
@@ -765,6 +969,18 @@ int vqhull_cuda_set_stable(int stable) {
         Engine& e = vqb::engine();
         std::lock_guard<std::mutex> lk(e.mutex());
         e.set_stable(stable != 0);
+        return 0;
+    } catch (const CudaError&) {
+        return VQHULL_ECUDA;
+    }
+}
+
+int vqhull_cuda_set_root_mode(int mode) {
+    if (mode < 0 || mode > 2) return VQHULL_EINVAL;
+    try {
+        Engine& e = vqb::engine();
+        std::lock_guard<std::mutex> lk(e.mutex());
+        e.set_root_mode(mode);
         return 0;
     } catch (const CudaError&) {
         return VQHULL_ECUDA;

@@ -44,6 +44,7 @@ struct RootPoly {
     // f_j(P) < ft_j for all 8 chords (ft_j = -margin * |chord|_1)
     double fa[8], fb[8], fc[8], ft[8];
     double bx0, bx1, by0, by1;  // open box verified to lie inside the filter region
+    double mref;                // M: max |coordinate| of the 8 vertices (the margin is 2^-32 M)
 };
 
 // K1 + pass A results, one per hull call (device resident).
@@ -55,7 +56,7 @@ struct RootInfo {
     uint32_t cnt1, cnt2;
     Best r1, r2;
     uint32_t nonfinite;
-    uint32_t pad;
+    uint32_t unsafe;            // split root: a survivor exceeds 2^12 M (margin argument void) -> rerun unfiltered
     RootPoly poly;
 };
 
@@ -138,6 +139,27 @@ struct RootArgs {
     RootInfo* root_w;    // filtered root: side counts and apexes for the stats
 };
 
+// Split root, pass 1 (root_filter_tma): the octagon filter over the caller's
+// arrays; survivors (x, y, index) are compacted to o*, the exact extremes of
+// the survivors (= find_extremes of the input) give p and q, and the last CTA
+// writes the first level's single slot (p, q, p) — the reference's bootstrap
+// triangle (hull.cpp:228-235).
+struct FilterArgs {
+    const double* xs;
+    const double* ys;
+    uint64_t n;
+    uint32_t ntiles;
+    double* ox;
+    double* oy;
+    uint32_t* oid;
+    uint64_t out_cap;    // debug bounds
+    uint32_t* ctr;       // survivor counter
+    uint32_t* ticket;    // CTA exit ticket
+    void* part;          // per-CTA partials
+    RootInfo* root_w;
+    ChildRec* slot;      // the first level's slot table (1 slot)
+};
+
 struct LevelArgs {
     const double* gx;    // the hull's input arrays (index -> coordinates, arg-max ties)
     const double* gy;
@@ -160,6 +182,46 @@ struct LevelArgs {
     uint32_t* seg_done;  // per segment: tiles finished
     unsigned long long* seg_ctr;  // fast mode: packed L/R counters per segment
     ChildRec* children;  // 2 per segment
+};
+
+// Persistent recursion kernel (tail.cu): per level, the host-allocated tables
+// it fills (the same tables the host-driven level loop uses).
+struct TailLevel {
+    ChildRec* slots;
+    SegRec* segs;
+    FinRec* fins;
+    uint8_t* kind;
+    uint32_t* link;
+    uint32_t* fin_count;
+};
+constexpr int kTailLevels = 40;
+struct TailArgs {
+    TailLevel lv[kTailLevels];
+    LevelInfo* info;          // LevelInfo array indexed by level
+    const LevelInfo* prev0;   // info of level l0 - 1 (nullptr: level l0 has nslots0 slots)
+    int l0, nlev;
+    uint32_t nslots0;
+    uint32_t max_slots;       // table capacity; a level with more slots is left to the host
+    double* bx[2];
+    double* by[2];
+    uint32_t* bid[2];
+    uint64_t buf_cap;
+    const double* gx;
+    const double* gy;
+    uint32_t* flags;          // planner look-back
+    void* aggs_v;
+    void* incs_v;
+    uint32_t epoch0;
+    uint32_t* plan_ctr;
+    uint32_t* seg_pcnt;
+    uint32_t* seg_done;
+    unsigned long long* seg_ctr;
+    uint32_t* tile_seg;
+    Best* tile_part;
+    uint64_t part_cap;
+    uint32_t* chain;
+    uint32_t* state;          // [0] level, [1] 1 = finished at that level, 2 = stopped before it
+    unsigned long long* trace;  // optional (VQHULL_TAIL_TRACE): CTA 0's %globaltimer per level phase
 };
 
 // Emission of a small recursion tree in one kernel: per level, the slot

@@ -33,35 +33,6 @@ namespace vqb {
 // visiting order.  Branch-free per point (compare + select); an exact x tie
 // with the running extreme takes a warp-uniform slow path that reads y.
 // ===========================================================================
-struct ExtKey {
-    double x, y;
-    uint32_t idx;
-    uint32_t valid;
-};
-
-__device__ __forceinline__ bool lo_better(const ExtKey& a, const ExtKey& b) {
-    if (!a.valid) return false;
-    if (!b.valid) return true;
-    if (a.x != b.x) return a.x < b.x;
-    if (a.y != b.y) return a.y < b.y;
-    return a.idx < b.idx;
-}
-__device__ __forceinline__ bool hi_better(const ExtKey& a, const ExtKey& b) {
-    if (!a.valid) return false;
-    if (!b.valid) return true;
-    if (a.x != b.x) return a.x > b.x;
-    if (a.y != b.y) return a.y > b.y;
-    return a.idx < b.idx;
-}
-__device__ __forceinline__ ExtKey shfl_key(const ExtKey& k, int x) {
-    ExtKey o;
-    o.x = __shfl_xor_sync(kFull, k.x, x);
-    o.y = __shfl_xor_sync(kFull, k.y, x);
-    o.idx = __shfl_xor_sync(kFull, k.idx, x);
-    o.valid = __shfl_xor_sync(kFull, k.valid, x);
-    return o;
-}
-
 struct ExtPartial {
     ExtKey lo, hi;
     uint32_t nonfinite, pad;
@@ -366,7 +337,7 @@ __global__ void __launch_bounds__(256) bootstrap_argmax_kernel(
 // K1' (default root stage) = K1 (extremes_kernel: find_extremes,
 // geometry.cpp:7-36, over every point; x read for every point, y only on
 // exact x ties; finiteness of x) + this sample kernel: the octagon filter's
-// 8 vertices from a sample of the input (every 16th group of 256 points, x
+// 8 vertices from a sample of the input (every 16th group of 1024 points, x
 // and y): min/max x, y, x+y, x-y.  Two kernels, so the x stream keeps K1's
 // small register footprint (occupancy, loads in flight).  The filter
 // only needs its vertices to be input points (see poly_finish), not exact
@@ -382,7 +353,26 @@ struct PolyPartial {
     uint32_t pad;
 };
 
-constexpr int kSampleShift = 7;  // groups of 128 pairs (256 points)
+struct SamplePartial {
+    double s[3];  // sample sums of x, y and the count
+};
+
+// monotone u32 key of a double rounded to f32 (larger value -> larger key)
+__device__ __forceinline__ uint32_t f32_order_key(double v) {
+    const uint32_t u = __float_as_uint(__double2float_rn(v));
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+// diagnostics (VQHULL_SAMPLE_TRACE): %globaltimer stamps of the sample kernel
+__device__ unsigned long long g_strace[8];
+__device__ __forceinline__ unsigned long long gtimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+constexpr int kSampleShift = 9;  // groups of 512 pairs (1024 points, 8 KB of x and of y)
+constexpr int kSampleUnroll = 8;  // double2 loads per array per thread in flight
 constexpr int kSampleMask = 15;  // one group in 16 is sampled
 
 // sampled directions, in octagon slot order: 0 min x, 1 min x-y, 2 max y,
@@ -466,106 +456,95 @@ __device__ __forceinline__ void block_reduce_poly(ExtKey& lo, ExtKey& hi, double
     }
 }
 
-// Last step of K1' (one thread): p, q (exact), the octagon filter (the
-// sample's 8 directional extremes: mutually consistent, so in convex
-// position up to rounding ties — exact p, q would not be, e.g. when one far
-// point of a heavy-tailed input dominates), its chord forms and inner box,
-// the emission frame.
-__device__ __noinline__ void poly_finish(const PolyPartial& F, const double* __restrict__ xs,
-                                         const double* __restrict__ ys, RootInfo* root) {
+// Last step of K1' (one warp, poly_finish_warp): p, q (exact, in the
+// one-pass octagon root), the octagon filter (the sample's 8 directional
+// extremes: mutually consistent, so in convex position up to rounding ties —
+// exact p, q would not be, e.g. when one far point of a heavy-tailed input
+// dominates), its chord forms and inner box, the emission frame.
+// Every vertex is an input point, so the region right of all 8 chords (the
+// octagon, or its kernel if rounding ties made it non-convex) lies in the
+// hull.  M bounds |coordinates| of the vertices, hence of every point the
+// filter can drop; the margin is 2^-32 M (~10^5 ulps of M), so the fused
+// multiply-adds' rounding can never reach a dropped point and no reference
+// predicate can see one as a hull or farthest candidate.  Outside
+// 2^-400 <= M <= 2^500 (products could underflow/overflow): no filter.
+// One warp: lane l owns chord
+// j = l & 7 (each chord four times), box corner c = l >> 3 in the 32-lane
+// inside-tests, so a box candidate costs one FMA pair and one vote instead of
+// 32 serial tests.  Every expression is poly_finish's, so the filter is
+// bit-identical.
+__device__ __noinline__ void poly_finish_warp(const PolyPartial& F, const double* __restrict__ xs,
+                                              const double* __restrict__ ys, RootInfo* root, bool with_pq) {
     const double kInf = __longlong_as_double(0x7ff0000000000000ll);
+    const int lane = threadIdx.x & 31, j = lane & 7, corner = lane >> 3;
     const ExtKey L = F.lo, H = F.hi;
     const uint32_t nb = F.nonfinite;
     RootInfo& R = *root;
     RootPoly& P = R.poly;
-    bool ok = L.valid && H.valid && nb == 0;
-    double vx[8], vy[8];
+    bool ok = with_pq ? (L.valid && H.valid && nb == 0) : true;
+    const uint32_t aj = F.ai[j];
+    const uint32_t ij = aj != kNoIdx ? aj : (L.valid ? L.idx : 0u);  // n >= 1
+    const double vxj = xs[ij], vyj = ys[ij];
+    ok &= __all_sync(kFull, aj != kNoIdx);
+    auto VX = [&](int k) { return __shfl_sync(kFull, vxj, k); };
+    auto VY = [&](int k) { return __shfl_sync(kFull, vyj, k); };
+    double M = fmax(fabs(vxj), fabs(vyj));
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {  // independent loads, all in flight together
-        const uint32_t i = F.ai[j] != kNoIdx ? F.ai[j] : L.idx;
-        vx[j] = xs[i];
-        vy[j] = ys[i];
-    }
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-        ok &= F.ai[j] != kNoIdx;
-        P.vx[j] = vx[j];
-        P.vy[j] = vy[j];
-        P.vidx[j] = F.ai[j];
-    }
-    // Every vertex is an input point, so the region right of all 8 chords
-    // (the octagon, or its kernel if rounding ties made it non-convex) lies
-    // in the hull.  M bounds |coordinates| of the vertices, hence of every
-    // point the filter can drop; the margin is 2^-32 M (~10^5 ulps of M), so
-    // the fused multiply-adds' rounding can never reach a dropped point and
-    // no reference predicate can see one as a hull or farthest candidate.
-    // Outside 2^-400 <= M <= 2^500 (products could underflow/overflow): no
-    // filter.
-    double M = 0.0;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) M = fmax(M, fmax(fabs(vx[j]), fabs(vy[j])));
+    for (int s = 16; s > 0; s >>= 1) M = fmax(M, __shfl_xor_sync(kFull, M, s));
     ok &= M >= 0x1p-400 && M <= 0x1p500;
-    int chords = 0;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-        const int k = (j + 1) & 7;
-        const double ex = vx[k] - vx[j], ey = vy[k] - vy[j];
-        chords += !(ex == 0.0 && ey == 0.0);
-        if (ex == 0.0 && ey == 0.0) {  // degenerate chord: no constraint
-            P.fa[j] = 0.0; P.fb[j] = 0.0; P.fc[j] = -1.0; P.ft[j] = 0.0;
-        } else {
-            P.fa[j] = -ey;
-            P.fb[j] = ex;
-            P.fc[j] = ey * vx[j] - ex * vy[j];
-            P.ft[j] = -0x1p-32 * M * (fabs(ex) + fabs(ey));
-        }
-    }
-    auto inside = [&](double x, double y) {
-        bool in = true;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) in &= __fma_rn(P.fa[j], x, __fma_rn(P.fb[j], y, P.fc[j])) < P.ft[j];
-        return in;
+    // chord j = V_j -> V_{j+1}
+    const double nxj = VX((j + 1) & 7), nyj = VY((j + 1) & 7);
+    const double ex = nxj - vxj, ey = nyj - vyj;
+    const bool deg = ex == 0.0 && ey == 0.0;  // degenerate chord: no constraint
+    const double fa = deg ? 0.0 : -ey;
+    const double fb = deg ? 0.0 : ex;
+    const double fc = deg ? -1.0 : ey * vxj - ex * vyj;
+    const double ft = deg ? 0.0 : -0x1p-32 * M * (fabs(ex) + fabs(ey));
+    const int chords = __popc(__ballot_sync(kFull, !deg)) / 4;
+    auto inside_pt = [&](double x, double y) {
+        return __all_sync(kFull, __fma_rn(fa, x, __fma_rn(fb, y, fc)) < ft);
     };
-    // inner box between the diagonal vertices (its corners tend to BE
-    // vertices, so it is shrunk a little); kept only if its 4 corners pass
-    // the test (the filter region is convex, so then the whole box does)
-    const double cx0 = fmax(vx[1], vx[7]), cx1 = fmin(vx[3], vx[5]);
-    const double cy0 = fmax(vy[5], vy[7]), cy1 = fmin(vy[1], vy[3]);
+    auto inside_box = [&](double x0, double x1, double y0, double y1) {
+        const double x = (corner & 1) ? x1 : x0, y = (corner & 2) ? y1 : y0;
+        return __all_sync(kFull, __fma_rn(fa, x, __fma_rn(fb, y, fc)) < ft);
+    };
+    // inner box between the diagonal vertices (shrunk a little), kept only if
+    // its 4 corners pass the test (the filter region is convex)
+    const double cx0 = fmax(VX(1), VX(7)), cx1 = fmin(VX(3), VX(5));
+    const double cy0 = fmax(VY(5), VY(7)), cy1 = fmin(VY(1), VY(3));
     double bx0 = kInf, bx1 = -kInf, by0 = kInf, by1 = -kInf;  // empty
     const double shrink[3] = {0x1p-20 * M, 0x1p-10 * M, 0.0625 * fmax(cx1 - cx0, cy1 - cy0)};
     for (int t = 0; t < 3; ++t) {
         const double x0 = cx0 + shrink[t], x1 = cx1 - shrink[t];
         const double y0 = cy0 + shrink[t], y1 = cy1 - shrink[t];
-        if (x0 < x1 && y0 < y1 && inside(x0, y0) && inside(x0, y1) && inside(x1, y0) && inside(x1, y1)) {
+        if (x0 < x1 && y0 < y1 && inside_box(x0, x1, y0, y1)) {
             bx0 = x0; bx1 = x1; by0 = y0; by1 = y1;
             break;
         }
     }
-    // second candidate, for octagons that are not "round" (heavy tails can
-    // collapse the sample's octagon to a triangle): the largest box around
-    // the sample's mean with the octagon's aspect, in closed form per chord
-    // and worst corner, verified like the first; the larger one is kept
+    // second candidate: the largest box around the sample's mean with the
+    // octagon's aspect (closed form per chord), verified like the first
     if (F.sn > 0.0) {
         const double cx = F.sx / F.sn, cy = F.sy / F.sn;
-        double xmin = vx[0], xmax = vx[0], ymin = vy[0], ymax = vy[0];
+        double xmin = vxj, xmax = vxj, ymin = vyj, ymax = vyj;
 #pragma unroll
-        for (int j = 1; j < 8; ++j) {
-            xmin = fmin(xmin, vx[j]); xmax = fmax(xmax, vx[j]);
-            ymin = fmin(ymin, vy[j]); ymax = fmax(ymax, vy[j]);
+        for (int s = 16; s > 0; s >>= 1) {
+            xmin = fmin(xmin, __shfl_xor_sync(kFull, xmin, s));
+            xmax = fmax(xmax, __shfl_xor_sync(kFull, xmax, s));
+            ymin = fmin(ymin, __shfl_xor_sync(kFull, ymin, s));
+            ymax = fmax(ymax, __shfl_xor_sync(kFull, ymax, s));
         }
         const double W = 0.5 * (xmax - xmin), Hh = 0.5 * (ymax - ymin);
-        if (inside(cx, cy) && W > 0.0 && Hh > 0.0) {
-            double t = 1.0;
+        if (inside_pt(cx, cy) && W > 0.0 && Hh > 0.0) {
+            const double f0 = fa * cx + fb * cy + fc;
+            const double g = fabs(fa) * W + fabs(fb) * Hh;
+            double t = g > 0.0 ? fmin(1.0, (ft - f0) / g) : 1.0;
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                const double f0 = P.fa[j] * cx + P.fb[j] * cy + P.fc[j];
-                const double g = fabs(P.fa[j]) * W + fabs(P.fb[j]) * Hh;
-                if (g > 0.0) t = fmin(t, (P.ft[j] - f0) / g);
-            }
+            for (int s = 16; s > 0; s >>= 1) t = fmin(t, __shfl_xor_sync(kFull, t, s));
             for (int tries = 0; tries < 4 && t > 0.0; ++tries, t *= 0.5) {
                 const double x0 = cx - 0.999 * t * W, x1 = cx + 0.999 * t * W;
                 const double y0 = cy - 0.999 * t * Hh, y1 = cy + 0.999 * t * Hh;
-                if (x0 < x1 && y0 < y1 && inside(x0, y0) && inside(x0, y1) && inside(x1, y0) && inside(x1, y1)) {
+                if (x0 < x1 && y0 < y1 && inside_box(x0, x1, y0, y1)) {
                     const double a_old = bx0 < bx1 ? (bx1 - bx0) * (by1 - by0) : 0.0;
                     if ((x1 - x0) * (y1 - y0) > a_old) { bx0 = x0; bx1 = x1; by0 = y0; by1 = y1; }
                     break;
@@ -573,9 +552,16 @@ __device__ __noinline__ void poly_finish(const PolyPartial& F, const double* __r
             }
         }
     }
-    P.bx0 = bx0; P.bx1 = bx1; P.by0 = by0; P.by1 = by1;
     ok &= chords >= 2;  // all vertices equal: the test would constrain nothing
+    if (lane < 8) {
+        P.vx[j] = vxj; P.vy[j] = vyj; P.vidx[j] = aj;
+        P.fa[j] = fa; P.fb[j] = fb; P.fc[j] = fc; P.ft[j] = ft;
+    }
+    if (lane != 0) return;
+    P.mref = M;
+    P.bx0 = bx0; P.bx1 = bx1; P.by0 = by0; P.by1 = by1;
     P.filter = ok ? 1u : 0u;
+    if (!with_pq) return;
     P.nv = 2;  // emission frame: [p] chain(S1) [q] chain(S2)
     P.ex[0] = L.x; P.ey[0] = L.y; P.eidx[0] = L.idx;
     P.ex[1] = H.x; P.ey[1] = H.y; P.eidx[1] = H.idx;
@@ -588,15 +574,13 @@ __device__ __noinline__ void poly_finish(const PolyPartial& F, const double* __r
 
 __global__ void __launch_bounds__(256, 2) poly_sample_kernel(const double* __restrict__ xs,
                                                             const double* __restrict__ ys, uint64_t n,
-                                                            PolyPartial* partials, uint32_t* ticket,
-                                                            RootInfo* root, unsigned long long* side_ctr) {
+                                                            SamplePartial* partials, uint32_t* ticket,
+                                                            unsigned long long* keys, RootInfo* root,
+                                                            unsigned long long* side_ctr, int with_pq) {
     VQB_PDL();
     const double kInf = __longlong_as_double(0x7ff0000000000000ll);
-    double lo_x = kInf, hi_x = -kInf;
-    uint32_t lo_i = kNoIdx, hi_i = kNoIdx;
     double av[8] = {kInf, kInf, -kInf, -kInf, -kInf, -kInf, kInf, kInf};
     uint32_t ai[8] = {kNoIdx, kNoIdx, kNoIdx, kNoIdx, kNoIdx, kNoIdx, kNoIdx, kNoIdx};
-    bool bad = false;
     double ssx = 0.0, ssy = 0.0;  // sample sums (non-finite input is rejected anyway)
     uint32_t ssn = 0;
     auto visit_xy = [&](uint32_t i, double x, double y) {
@@ -615,13 +599,14 @@ __global__ void __launch_bounds__(256, 2) poly_sample_kernel(const double* __res
     };
     const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
     const uint32_t stride = gridDim.x * blockDim.x;
+    if (tid == 0) g_strace[0] = gtimer_ns();
     const bool vec = ((reinterpret_cast<uintptr_t>(xs) | reinterpret_cast<uintptr_t>(ys)) & 15u) == 0;
     if (vec) {
         const uint32_t npair = uint32_t(n / 2);
         const double2* x2 = reinterpret_cast<const double2*>(xs);
         const double2* y2 = reinterpret_cast<const double2*>(ys);
         if ((n & 1) && tid == 0) visit_xy(uint32_t(n - 1), xs[n - 1], ys[n - 1]);
-        // phase 2: x and y of the sampled groups (every 16th run of 128 pairs)
+        // x and y of the sampled groups (every 16th run of 512 pairs)
         const uint32_t ngroups = (npair + (1u << kSampleShift) - 1) >> kSampleShift;
         const uint32_t nsg = (ngroups + kSampleMask) / (kSampleMask + 1);
         const uint32_t nsample = nsg << kSampleShift;
@@ -629,18 +614,18 @@ __global__ void __launch_bounds__(256, 2) poly_sample_kernel(const double* __res
             return ((m >> kSampleShift) * (kSampleMask + 1) << kSampleShift) | (m & ((1u << kSampleShift) - 1));
         };
         uint32_t m = tid;
-        for (; m + (kStreamUnroll - 1) * stride < nsample; m += kStreamUnroll * stride) {
-            double2 v[kStreamUnroll], w[kStreamUnroll];
-            uint32_t jj[kStreamUnroll];
+        for (; m + (kSampleUnroll - 1) * stride < nsample; m += kSampleUnroll * stride) {
+            double2 v[kSampleUnroll], w[kSampleUnroll];
+            uint32_t jj[kSampleUnroll];
 #pragma unroll
-            for (int u = 0; u < kStreamUnroll; ++u) {
+            for (int u = 0; u < kSampleUnroll; ++u) {
                 jj[u] = pair_of(m + u * stride);
                 const uint32_t q = jj[u] < npair ? jj[u] : 0u;
                 v[u] = __ldcs(&x2[q]);
                 w[u] = __ldcs(&y2[q]);
             }
 #pragma unroll
-            for (int u = 0; u < kStreamUnroll; ++u) {
+            for (int u = 0; u < kSampleUnroll; ++u) {
                 if (jj[u] >= npair) continue;
                 visit_xy(2 * jj[u], v[u].x, w[u].x);
                 visit_xy(2 * jj[u] + 1, v[u].y, w[u].y);
@@ -658,65 +643,105 @@ __global__ void __launch_bounds__(256, 2) poly_sample_kernel(const double* __res
         for (uint32_t i = tid; i < n; i += stride)
             if (((i >> (kSampleShift + 1)) & kSampleMask) == 0) visit_xy(i, xs[i], ys[i]);
     }
-    // reductions: thread -> CTA partial -> (last CTA, all threads) -> final
-    ExtKey lo{lo_x, 0.0, lo_i, lo_i != kNoIdx};
-    ExtKey hi{hi_x, 0.0, hi_i, hi_i != kNoIdx};
-    if (lo.valid) lo.y = ys[lo_i];
-    if (hi.valid) hi.y = ys[hi_i];
-    uint32_t nb = bad ? 1u : 0u;
-    double sx = ssx, sy = ssy, sn = double(ssn);
-    __shared__ PolyPartial s_w[8];
+    if (threadIdx.x == 0) atomicMax(&g_strace[1], gtimer_ns());
+    // Reductions.  A vertex only has to be SOME input point (see
+    // poly_finish_warp), so the CTAs combine their directional extremes with
+    // one 64-bit atomicMax per direction on {order key of the value rounded to
+    // f32, ~index}: order-independent, hence deterministic, and no serial
+    // fold.  The sample sums (box centre) are combined in a fixed order.
+    __shared__ unsigned long long s_key[8][8];
+    __shared__ double s_sum[3][8];
     __shared__ bool s_last;
-    block_reduce_poly(lo, hi, av, ai, sx, sy, sn, nb, s_w);
-    if (threadIdx.x == 0) {
-        PolyPartial& r = partials[blockIdx.x];
-        r.lo = lo; r.hi = hi; r.nonfinite = nb; r.pad = 0u;
-        r.sx = sx; r.sy = sy; r.sn = sn;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    unsigned long long key[8];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) { r.av[q] = av[q]; r.ai[q] = ai[q]; }
+    for (int a = 0; a < 8; ++a) {
+        const bool maximize = (a >= 2 && a <= 5);
+        key[a] = ai[a] == kNoIdx ? 0ull
+                                 : (uint64_t(f32_order_key(maximize ? av[a] : -av[a])) << 32) | uint32_t(~ai[a]);
+    }
+    double sx = ssx, sy = ssy, sn = double(ssn);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+        for (int a = 0; a < 8; ++a) {
+            const unsigned long long k = __shfl_xor_sync(kFull, key[a], o);
+            key[a] = k > key[a] ? k : key[a];
+        }
+        sx += __shfl_xor_sync(kFull, sx, o);
+        sy += __shfl_xor_sync(kFull, sy, o);
+        sn += __shfl_xor_sync(kFull, sn, o);
+    }
+    if (lane == 0) {
+#pragma unroll
+        for (int a = 0; a < 8; ++a) s_key[a][warp] = key[a];
+        s_sum[0][warp] = sx; s_sum[1][warp] = sy; s_sum[2][warp] = sn;
+    }
+    __syncthreads();
+    if (threadIdx.x < 8) {
+        unsigned long long k = s_key[threadIdx.x][0];
+        for (int w = 1; w < 8; ++w) k = s_key[threadIdx.x][w] > k ? s_key[threadIdx.x][w] : k;
+        if (k) atomicMax(&keys[threadIdx.x], k);
+    } else if (threadIdx.x < 11) {
+        const int c = threadIdx.x - 8;
+        double t = 0.0;
+        for (int w = 0; w < 8; ++w) t += s_sum[c][w];
+        partials[blockIdx.x].s[c] = t;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
         __threadfence();
         s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
     }
     __syncthreads();
     if (!s_last) return;
     __threadfence();
-    // every thread folds its share of the CTA partials (independent loads)
-    {
-        PolyPartial acc = poly_none();
-        lo = acc.lo; hi = acc.hi; nb = 0; sx = sy = sn = 0.0;
-#pragma unroll
-        for (int q = 0; q < 8; ++q) { av[q] = acc.av[q]; ai[q] = kNoIdx; }
-    }
+    if (threadIdx.x == 0) g_strace[2] = gtimer_ns();
+    // sums over the CTA partials: strided per thread, then a fixed tree
+    sx = sy = sn = 0.0;
     for (uint32_t c = threadIdx.x; c < gridDim.x; c += blockDim.x) {
-        const PolyPartial* p = &partials[c];
-        ExtKey a, h;
-        a.x = __ldcg(&p->lo.x); a.y = __ldcg(&p->lo.y); a.idx = __ldcg(&p->lo.idx); a.valid = __ldcg(&p->lo.valid);
-        h.x = __ldcg(&p->hi.x); h.y = __ldcg(&p->hi.y); h.idx = __ldcg(&p->hi.idx); h.valid = __ldcg(&p->hi.valid);
-        if (lo_better(a, lo)) lo = a;
-        if (hi_better(h, hi)) hi = h;
-        nb |= __ldcg(&p->nonfinite);
-        sx += __ldcg(&p->sx);
-        sy += __ldcg(&p->sy);
-        sn += __ldcg(&p->sn);
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            const double ov = __ldcg(&p->av[q]);
-            const uint32_t oi = __ldcg(&p->ai[q]);
-            if (approx_better(q, ov, oi, av[q], ai[q])) { av[q] = ov; ai[q] = oi; }
-        }
+        sx += __ldcg(&partials[c].s[0]);
+        sy += __ldcg(&partials[c].s[1]);
+        sn += __ldcg(&partials[c].s[2]);
     }
-    __syncthreads();  // s_w reuse
-    block_reduce_poly(lo, hi, av, ai, sx, sy, sn, nb, s_w);
-    if (threadIdx.x != 0) return;
-    __shared__ PolyPartial s_fin;
-    // p, q and the finiteness of x come from K1 (extremes_kernel, same stream)
-    s_fin.lo = ExtKey{root->px, root->py, root->p_idx, 1u};
-    s_fin.hi = ExtKey{root->qx, root->qy, root->q_idx, 1u};
-    s_fin.nonfinite = root->nonfinite; s_fin.pad = 0u;
-    s_fin.sx = sx; s_fin.sy = sy; s_fin.sn = sn;
 #pragma unroll
-    for (int q = 0; q < 8; ++q) { s_fin.av[q] = av[q]; s_fin.ai[q] = ai[q]; }
-    poly_finish(s_fin, xs, ys, root);
+    for (int o = 16; o > 0; o >>= 1) {
+        sx += __shfl_xor_sync(kFull, sx, o);
+        sy += __shfl_xor_sync(kFull, sy, o);
+        sn += __shfl_xor_sync(kFull, sn, o);
+    }
+    __syncthreads();
+    if (lane == 0) { s_sum[0][warp] = sx; s_sum[1][warp] = sy; s_sum[2][warp] = sn; }
+    __syncthreads();
+    __shared__ PolyPartial s_fin;
+    if (threadIdx.x == 0) {
+        sx = sy = sn = 0.0;
+        for (int w = 0; w < 8; ++w) { sx += s_sum[0][w]; sy += s_sum[1][w]; sn += s_sum[2][w]; }
+        s_fin.sx = sx; s_fin.sy = sy; s_fin.sn = sn;
+        // p, q and the finiteness of x come from K1 (one-pass octagon root)
+        if (with_pq) {
+            s_fin.lo = ExtKey{root->px, root->py, root->p_idx, 1u};
+            s_fin.hi = ExtKey{root->qx, root->qy, root->q_idx, 1u};
+            s_fin.nonfinite = root->nonfinite;
+        } else {
+            s_fin.lo = ExtKey{0.0, 0.0, kNoIdx, 0u};
+            s_fin.hi = s_fin.lo;
+            s_fin.nonfinite = 0u;
+        }
+        s_fin.pad = 0u;
+    }
+    if (threadIdx.x < 8) {
+        const unsigned long long k = __ldcg(&keys[threadIdx.x]);
+        s_fin.ai[threadIdx.x] = k ? ~uint32_t(k) : kNoIdx;
+        s_fin.av[threadIdx.x] = 0.0;  // unused: vertices are re-read by index
+        keys[threadIdx.x] = 0ull;     // re-arm for the next call
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) g_strace[3] = gtimer_ns();
+    if (threadIdx.x >= 32) return;
+    poly_finish_warp(s_fin, xs, ys, root, with_pq != 0);
+    if (threadIdx.x != 0) return;
+    g_strace[4] = gtimer_ns();
     side_ctr[0] = 0ull;  // the root pass's counter (another root mode may have used it)
     *ticket = 0;
 }
@@ -755,8 +780,9 @@ __device__ __forceinline__ uint8_t kind_of(uint32_t m) {
     return m == 0 ? kEmpty : (m == 1 ? kLeaf : (m <= kFinMax ? kFin : kInternal));
 }
 
-__global__ void __launch_bounds__(kThreads) planner_kernel(PlanArgs a) {
-    VQB_PDL();
+// nblocks: CTAs running the planner (they claim slot chunks dynamically);
+// the persistent tail kernel runs it on one CTA.
+__device__ __noinline__ void planner_body(const PlanArgs& a, uint32_t nblocks) {
     __shared__ PlanAgg s_w[kWarps];
     __shared__ PlanAgg s_excl;
     __shared__ uint32_t s_chunk;
@@ -778,7 +804,7 @@ __global__ void __launch_bounds__(kThreads) planner_kernel(PlanArgs a) {
         if (threadIdx.x == 0) {
             const uint32_t c = atomicAdd(a.ctr, 1u);
             s_chunk = c;
-            if (c >= nchunks && c == nchunks + gridDim.x - 1) *a.ctr = 0;
+            if (c >= nchunks && c == nchunks + nblocks - 1) *a.ctr = 0;
         }
         __syncthreads();
         const uint32_t chunk = s_chunk;
@@ -898,6 +924,11 @@ __global__ void __launch_bounds__(kThreads) planner_kernel(PlanArgs a) {
             }
         }
     }
+}
+
+__global__ void __launch_bounds__(kThreads) planner_kernel(PlanArgs a) {
+    VQB_PDL();
+    planner_body(a, gridDim.x);
 }
 
 // tile -> segment map (binary search over the segments' first tiles)
@@ -1345,6 +1376,18 @@ union FinAllSmem {
     FinSmem warp[kFcThreads / 32];
 };
 
+__device__ __forceinline__ void finisher_all_body(FinAllSmem& U, const FinRec* fins, const LevelInfo* info,
+                                                  uint32_t fin_cap, const double* __restrict__ ix,
+                                                  const double* __restrict__ iy,
+                                                  const uint32_t* __restrict__ iid, uint32_t* chain,
+                                                  uint32_t* fin_count) {
+    finisher_cta_body(U.cta, fins, info, fin_cap, ix, iy, iid, chain, fin_count);
+    __syncthreads();
+    const uint32_t wpb = kFcThreads / 32;
+    finisher_warp_body(U.warp[threadIdx.x >> 5], blockIdx.x * wpb + (threadIdx.x >> 5), gridDim.x * wpb, fins,
+                       info, ix, iy, iid, chain, fin_count);
+}
+
 __global__ void __launch_bounds__(kFcThreads) finisher_all_kernel(const FinRec* fins, const LevelInfo* info,
                                                                   uint32_t fin_cap,
                                                                   const double* __restrict__ ix,
@@ -1354,11 +1397,7 @@ __global__ void __launch_bounds__(kFcThreads) finisher_all_kernel(const FinRec* 
     VQB_PDL();
     extern __shared__ __align__(16) unsigned char fc_dsm[];
     FinAllSmem& U = *reinterpret_cast<FinAllSmem*>(fc_dsm);
-    finisher_cta_body(U.cta, fins, info, fin_cap, ix, iy, iid, chain, fin_count);
-    __syncthreads();
-    const uint32_t wpb = kFcThreads / 32;
-    finisher_warp_body(U.warp[threadIdx.x >> 5], blockIdx.x * wpb + (threadIdx.x >> 5), gridDim.x * wpb, fins,
-                       info, ix, iy, iid, chain, fin_count);
+    finisher_all_body(U, fins, info, fin_cap, ix, iy, iid, chain, fin_count);
 }
 
 // ===========================================================================
@@ -1527,10 +1566,20 @@ void launch_bootstrap(const double* xs, const double* ys, uint64_t n, void* part
 }
 
 void launch_poly_sample(const double* xs, const double* ys, uint64_t n, void* partials,
-                        uint32_t* ticket, RootInfo* root, unsigned long long* side_ctr, int grid,
-                        cudaStream_t st) {
-    pdl_launch(poly_sample_kernel, grid, 256, 0, st, xs, ys, n, static_cast<PolyPartial*>(partials), ticket,
-                                               root, side_ctr);
+                        uint32_t* ticket, unsigned long long* keys, RootInfo* root,
+                        unsigned long long* side_ctr, int grid, bool with_pq, cudaStream_t st) {
+    pdl_launch(poly_sample_kernel, grid, 256, 0, st, xs, ys, n, static_cast<SamplePartial*>(partials), ticket,
+               keys, root, side_ctr, int(with_pq));
+}
+
+void print_sample_trace() {
+    unsigned long long t[8];
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(t, g_strace, sizeof t);
+    fprintf(stderr, "[sample] stream end %.2f  fold %.2f  reduce %.2f  finish %.2f us\n", (t[1] - t[0]) * 1e-3,
+            (t[2] - t[0]) * 1e-3, (t[3] - t[0]) * 1e-3, (t[4] - t[0]) * 1e-3);
+    const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    cudaMemcpyToSymbol(g_strace, z, sizeof z);
 }
 
 size_t partial_bytes(int grid) {

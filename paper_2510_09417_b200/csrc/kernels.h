@@ -14,6 +14,7 @@ void launch_extremes(const double* xs, const double* ys, uint64_t n, void* parti
 void launch_bootstrap(const double* xs, const double* ys, uint64_t n, void* partials,
                       uint32_t* ticket, RootInfo* root, int grid, cudaStream_t st);
 size_t partial_bytes(int grid);
+void print_sample_trace();
 void upload_root_consts(const RootInfo* d_root, cudaStream_t st);
 cudaError_t launch_root_partition(const RootArgs& a, int grid, bool stable, cudaStream_t st);
 cudaError_t launch_level(const LevelArgs& a, bool general, bool stable, int grid, cudaStream_t st);
@@ -35,8 +36,8 @@ void launch_emit(uint32_t nslots, const uint8_t* kind, const uint32_t* link,
                  const uint32_t* chain, const uint32_t* start, const uint32_t* child_size,
                  uint32_t* child_start, uint32_t* out, cudaStream_t st);
 void launch_poly_sample(const double* xs, const double* ys, uint64_t n, void* partials,
-                        uint32_t* ticket, RootInfo* root, unsigned long long* side_ctr, int grid,
-                        cudaStream_t st);
+                        uint32_t* ticket, unsigned long long* keys, RootInfo* root,
+                        unsigned long long* side_ctr, int grid, bool with_pq, cudaStream_t st);
 cudaError_t launch_root_filtered(const RootArgs& a, int grid, cudaStream_t st);
 void launch_emit_small(const EmitAll& e, const RootInfo* root, const uint32_t* chain, uint32_t* out,
                        uint32_t* h_out, cudaStream_t st);
@@ -49,9 +50,15 @@ int occupancy_level(bool stable);
 int occupancy_finisher();
 
 int occupancy_filtered();
+cudaError_t launch_root_filter(const FilterArgs& a, int grid, cudaStream_t st);
+int occupancy_filter();
+size_t filter_partial_bytes(int grid);
 int occupancy_poly_sample();
 int occupancy_extremes();
 int occupancy_bootstrap();
 uint32_t read_and_clear_fault();
+size_t tail_smem_bytes();
+int occupancy_tail();
+cudaError_t launch_tail(const TailArgs& a, int grid, cudaStream_t st);
 
 }  // namespace vqb

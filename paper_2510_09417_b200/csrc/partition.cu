@@ -518,8 +518,7 @@ __global__ void __launch_bounds__(kThreads, kPartMinBlocks) root_partition_kerne
 // emits the two children.
 // ===========================================================================
 template <bool GENERAL, bool STABLE>
-__global__ void __launch_bounds__(kThreads, kPartMinBlocks) level_kernel(LevelArgs a) {
-    VQB_PDL();
+__device__ __forceinline__ void level_body(const LevelArgs& a) {
     __shared__ TileSmem<2> S;
     __shared__ SegRec s_seg[2];
     __shared__ uint32_t s_k[2];
@@ -698,6 +697,12 @@ __global__ void __launch_bounds__(kThreads, kPartMinBlocks) level_kernel(LevelAr
         b ^= 1;
     }
     if (s_cur_k != 0xffffffffu) finalize();
+}
+
+template <bool GENERAL, bool STABLE>
+__global__ void __launch_bounds__(kThreads, kPartMinBlocks) level_kernel(LevelArgs a) {
+    VQB_PDL();
+    level_body<GENERAL, STABLE>(a);
 }
 
 // ===========================================================================
@@ -1463,6 +1468,266 @@ __global__ void __launch_bounds__(kCtlThreads, 3) root_filtered_tma(RootArgs a) 
 }
 
 // ===========================================================================
+// KF (default root stage since the split root): pass 1 of the root, the
+// octagon filter ALONE over the caller's arrays.  Per point: dropped when
+// strictly inside the inner box, else when inside all 8 chords by the margin
+// (the same RootPoly test as KB', so the same survivors); every survivor is
+// appended to a dense list (x, y, input index) with one atomic claim per tile.
+// Survivors also carry everything the reference's first level needs:
+//  * find_extremes (geometry.cpp:7-36): a dropped point is strictly inside the
+//    hull, so it can be neither the leftmost nor the rightmost point (nor one
+//    of their exact duplicates) — lo/hi over the survivors ARE the input's
+//    p and q, with the reference's tie-breaks and first-occurrence indices;
+//  * finiteness of x and y (vqhull_c.cpp:32-34): a non-finite point never
+//    passes the box (comparisons with NaN/inf are false) and never passes all
+//    chords (the chord normals span the plane, so one form is +inf or NaN);
+//  * the largest |coordinate| A of any survivor: the margin 2^-32 M is only
+//    proven against rounding of predicates whose operands are <= 2^12 M, so
+//    A > 2^12 M marks the call `unsafe` and the host reruns it unfiltered.
+// The last CTA writes p, q and the first level's single slot: the bootstrap
+// triangle (p, q, p) over all survivors (hull.cpp:228-235 — extract with
+// edges p->q and q->p, then chain_recursive on each side), which the level
+// machinery then partitions like any other segment.  Output frame: [p]
+// chain(slot) where the slot's apex is q (hull.cpp:259-266; p == q means all
+// points are equal: empty slot, output [p]).
+// Bytes: 16 per input point + 20 per survivor; no arg-max, no classes.
+// ===========================================================================
+struct FilterPartial {
+    ExtKey lo, hi;
+    double amax;
+    uint32_t nonfinite;
+    uint32_t pad;
+};
+
+__device__ __forceinline__ void filter_warp_fold(ExtKey& lo, ExtKey& hi, double& amax, uint32_t& bad) {
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) {
+        const ExtKey a = shfl_key(lo, s);
+        if (lo_better(a, lo)) lo = a;
+        const ExtKey b = shfl_key(hi, s);
+        if (hi_better(b, hi)) hi = b;
+        amax = fmax(amax, __shfl_xor_sync(kFull, amax, s));
+        bad |= __shfl_xor_sync(kFull, bad, s);
+    }
+}
+
+__global__ void __launch_bounds__(kCtlThreads, 3) root_filter_tma(FilterArgs a) {
+    VQB_PDL();
+    extern __shared__ __align__(128) unsigned char dsm[];
+    RootRing4& ring = *reinterpret_cast<RootRing4*>(dsm);
+    __shared__ uint32_t s_cnt[2][kWarps];                      // survivors per warp and tile
+    __shared__ uint32_t s_org[2][kWarps];                      // their first output position
+    __shared__ uint16_t s_q[kWarps][kTile / kWarps];           // a warp's points needing the chord test
+    __shared__ uint16_t s_surv[2][kWarps][kTile / kWarps];     // a warp's survivors (tile-local index)
+    __shared__ FilterPartial s_w[kCtlThreads / 32];
+    __shared__ bool s_last;
+    const RootPoly& P = c_root.poly;
+    const uint32_t n = uint32_t(a.n);
+    const uint32_t G = gridDim.x;
+    const uint32_t nfull = n / kTile;
+    const uint32_t nt = a.ntiles > blockIdx.x ? (a.ntiles - blockIdx.x + G - 1) / G : 0u;
+    const bool ctl = threadIdx.x >= kThreads;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t tid = threadIdx.x & (kThreads - 1);
+    auto issue = [&](uint32_t k) {
+        const uint32_t t = blockIdx.x + k * G;
+        if (t >= nfull) return;
+        const int s = int(k % kRing4);
+        mbar_expect_tx(&ring.bar[s], 2u * kTile * 8u);
+        tma_load_1d(ring.x[s], a.xs + uint64_t(t) * kTile, kTile * 8u, &ring.bar[s]);
+        tma_load_1d(ring.y[s], a.ys + uint64_t(t) * kTile, kTile * 8u, &ring.bar[s]);
+    };
+    if (threadIdx.x == kThreads) {
+        for (int s = 0; s < kRing4; ++s) mbar_init(&ring.bar[s], 1);
+        mbar_fence_init();
+        for (uint32_t k = 0; k < kRing4; ++k) issue(k);
+    }
+    __syncthreads();
+    const double kInf = __longlong_as_double(0x7ff0000000000000ll);
+    ExtKey lo{0.0, 0.0, kNoIdx, 0u}, hi{0.0, 0.0, kNoIdx, 0u};
+    double amax = 0.0;
+    uint32_t bad = 0;
+
+    if (ctl) {
+        // ---- control warp: refills, per-tile scan of the warp counts + claim
+        for (uint32_t k = 0; k < nt; ++k) {
+            const int par = int(k & 1);
+            named_sync<1>(par, kCtlThreads);  // counts of tile k posted; tile k-2 stored
+            if (lane == 0 && k >= 2) {
+                fence_proxy_async_smem();
+                issue(k - 2 + kRing4);  // refill tile k-2's stage
+            }
+            const uint32_t v = lane < kWarps ? s_cnt[par][lane] : 0u;
+            uint32_t incl = v;
+#pragma unroll
+            for (int d = 1; d < kWarps; d <<= 1) {
+                const uint32_t o = __shfl_up_sync(kFull, incl, d);
+                if (lane >= d) incl += o;
+            }
+            const uint32_t tot = __shfl_sync(kFull, incl, kWarps - 1);
+            uint32_t base = 0;
+            if (lane == 0 && tot) base = atomicAdd(a.ctr, tot);
+            base = __shfl_sync(kFull, base, 0);
+            if (lane < kWarps) s_org[par][lane] = base + incl - v;
+            named_arrive<3>(par, kCtlThreads);  // store origins of tile k published
+        }
+    } else {
+        // ---- compute warps: every warp owns 128 points of a tile (4 per lane)
+        const bool filter = P.filter != 0;
+        const double bx0 = filter ? P.bx0 : kInf, bx1 = filter ? P.bx1 : -kInf;
+        const double by0 = filter ? P.by0 : kInf, by1 = filter ? P.by1 : -kInf;
+        const unsigned lt = lanemask_lt();
+        auto store_tile = [&](uint32_t k) {  // tile k's survivors, offsets behind barrier B
+            const int par = int(k & 1);
+            named_sync<3>(par, kCtlThreads);
+            const uint32_t tbase = (blockIdx.x + k * G) * uint32_t(kTile);
+            const int s = int(k % kRing4);
+            const uint32_t sn = s_cnt[par][warp];
+            const uint32_t o = s_org[par][warp];
+            for (uint32_t j = lane; j < sn; j += 32) {
+                const uint32_t idx = s_surv[par][warp][j];
+                const uint32_t p = o + j;
+                VQB_CHECK(p < a.out_cap, 15, p, a.out_cap);
+                a.ox[p] = ring.x[s][idx];
+                a.oy[p] = ring.y[s][idx];
+                a.oid[p] = tbase + idx;
+            }
+        };
+        for (uint32_t k = 0; k < nt; ++k) {
+            const uint32_t t = blockIdx.x + k * G;
+            const uint32_t tbase = t * uint32_t(kTile);
+            const int s = int(k % kRing4);
+            const int par = int(k & 1);
+            if (t < nfull) {
+                mbar_wait(&ring.bar[s], (k / kRing4) & 1u);
+            } else {  // the partial last tile is staged by the warps themselves
+#pragma unroll
+                for (int i = 0; i < kItems; ++i) {
+                    const uint32_t idx = uint32_t(i) * kThreads + tid;
+                    ring.x[s][idx] = tbase + idx < n ? a.xs[tbase + idx] : 0.0;
+                    ring.y[s][idx] = tbase + idx < n ? a.ys[tbase + idx] : 0.0;
+                }
+                __syncwarp();
+            }
+            // phase A: strictly inside the inner box -> dropped at once
+            uint32_t qn = 0;
+#pragma unroll
+            for (int i = 0; i < kItems; ++i) {
+                const uint32_t idx = uint32_t(i) * kThreads + tid;
+                const double u = ring.x[s][idx], w = ring.y[s][idx];
+                const bool need = (tbase + idx < n) & !((u > bx0) & (u < bx1) & (w > by0) & (w < by1));
+                const unsigned b = __ballot_sync(kFull, need);
+                if (need) s_q[warp][qn + __popc(b & lt)] = uint16_t(idx);
+                qn += __popc(b);
+            }
+            __syncwarp();
+            // phase C: the chord test for the rest, densely, 32 at a time
+            uint32_t sn = 0;
+            for (uint32_t r0 = 0; r0 < qn; r0 += 32) {
+                const uint32_t j = r0 + lane;
+                const bool valid = j < qn;
+                const uint32_t idx = valid ? s_q[warp][j] : 0u;
+                const double u = ring.x[s][idx], w = ring.y[s][idx];
+                bool keep = false;
+                if (valid) {
+                    bad |= uint32_t(nonfinite_bits(u) | nonfinite_bits(w));
+                    bool drop = filter;
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)  // inside by the margin w.r.t. all 8 chords
+                        drop &= __fma_rn(P.fa[q], u, __fma_rn(P.fb[q], w, P.fc[q])) < P.ft[q];
+                    keep = !drop;
+                }
+                const unsigned b = __ballot_sync(kFull, keep);
+                if (keep) {
+                    s_surv[par][warp][sn + __popc(b & lt)] = uint16_t(idx);
+                    const ExtKey c{u, w, tbase + idx, 1u};
+                    if (lo_better(c, lo)) lo = c;
+                    if (hi_better(c, hi)) hi = c;
+                    amax = fmax(amax, fmax(fabs(u), fabs(w)));
+                }
+                sn += __popc(b);
+            }
+            if (lane == 0) s_cnt[par][warp] = sn;
+            named_arrive<1>(par, kCtlThreads);
+            if (k >= 1) store_tile(k - 1);
+        }
+        if (nt >= 1) store_tile(nt - 1);
+    }
+    // CTA partial -> the last CTA folds them and writes p, q and the slot
+    uint32_t nb = bad;
+    filter_warp_fold(lo, hi, amax, nb);
+    if (lane == 0) {
+        s_w[warp].lo = lo; s_w[warp].hi = hi; s_w[warp].amax = amax; s_w[warp].nonfinite = nb;
+    }
+    __syncthreads();
+    FilterPartial* part = static_cast<FilterPartial*>(a.part);
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < kCtlThreads / 32; ++w) {
+            if (lo_better(s_w[w].lo, lo)) lo = s_w[w].lo;
+            if (hi_better(s_w[w].hi, hi)) hi = s_w[w].hi;
+            amax = fmax(amax, s_w[w].amax);
+            nb |= s_w[w].nonfinite;
+        }
+        part[blockIdx.x].lo = lo; part[blockIdx.x].hi = hi;
+        part[blockIdx.x].amax = amax; part[blockIdx.x].nonfinite = nb;
+        __threadfence();
+        s_last = atomicAdd(a.ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    lo = ExtKey{0.0, 0.0, kNoIdx, 0u};
+    hi = lo;
+    amax = 0.0;
+    nb = 0;
+    for (uint32_t c = threadIdx.x; c < gridDim.x; c += blockDim.x) {
+        const FilterPartial* p = &part[c];
+        ExtKey x, h;
+        x.x = __ldcg(&p->lo.x); x.y = __ldcg(&p->lo.y); x.idx = __ldcg(&p->lo.idx); x.valid = __ldcg(&p->lo.valid);
+        h.x = __ldcg(&p->hi.x); h.y = __ldcg(&p->hi.y); h.idx = __ldcg(&p->hi.idx); h.valid = __ldcg(&p->hi.valid);
+        if (lo_better(x, lo)) lo = x;
+        if (hi_better(h, hi)) hi = h;
+        amax = fmax(amax, __ldcg(&p->amax));
+        nb |= __ldcg(&p->nonfinite);
+    }
+    filter_warp_fold(lo, hi, amax, nb);
+    __syncthreads();  // s_w reuse
+    if (lane == 0) {
+        s_w[warp].lo = lo; s_w[warp].hi = hi; s_w[warp].amax = amax; s_w[warp].nonfinite = nb;
+    }
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    for (int w = 1; w < kCtlThreads / 32; ++w) {
+        if (lo_better(s_w[w].lo, lo)) lo = s_w[w].lo;
+        if (hi_better(s_w[w].hi, hi)) hi = s_w[w].hi;
+        amax = fmax(amax, s_w[w].amax);
+        nb |= s_w[w].nonfinite;
+    }
+    const uint32_t s = *reinterpret_cast<volatile uint32_t*>(a.ctr);
+    RootInfo& R = *a.root_w;
+    RootPoly& Pw = R.poly;
+    const bool unsafe = P.filter != 0 && !(amax <= 0x1p12 * P.mref);
+    R.p_idx = lo.idx; R.px = lo.x; R.py = lo.y;
+    R.q_idx = hi.idx; R.qx = hi.x; R.qy = hi.y;
+    R.cnt1 = s; R.cnt2 = 0;
+    R.nonfinite = nb;
+    R.unsafe = unsafe ? 1u : 0u;
+    Pw.nv = 1;  // output frame: [p] chain(slot 0)
+    Pw.ex[0] = lo.x; Pw.ey[0] = lo.y; Pw.eidx[0] = lo.idx;
+    ChildRec ch;
+    ch.px = lo.x; ch.py = lo.y;
+    ch.rx = hi.x; ch.ry = hi.y;  // apex q
+    ch.qx = lo.x; ch.qy = lo.y;
+    ch.begin = 0;
+    const bool degenerate = !lo.valid || (lo.x == hi.x && lo.y == hi.y);
+    ch.m = (degenerate || nb || unsafe) ? 0u : s;
+    ch.r_idx = hi.idx;
+    a.slot[0] = ch;
+    *a.ctr = 0;  // re-arm for the next call
+    *a.ticket = 0;
+}
+
+// ===========================================================================
 // K2 fast mode with a TMA ring (8 compute warps + 1 control warp).  The
 // control warp's lane 0 maps each upcoming tile of the CTA to its segment and
 // streams x, y and the indices into a kRing-deep shared-memory ring with
@@ -1730,6 +1995,25 @@ cudaError_t launch_root_filtered(const RootArgs& a, int grid, cudaStream_t st) {
     pdl_launch(root_filtered_tma, grid, kCtlThreads, sizeof(RootRing4), st, a);
     return cudaGetLastError();
 }
+
+cudaError_t launch_root_filter(const FilterArgs& a, int grid, cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(root_filter_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(RootRing4)));
+        attr = true;
+    }
+    pdl_launch(root_filter_tma, grid, kCtlThreads, sizeof(RootRing4), st, a);
+    return cudaGetLastError();
+}
+
+int occupancy_filter() {
+    int b = 0;
+    cudaFuncSetAttribute(root_filter_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(RootRing4)));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, root_filter_tma, kCtlThreads, sizeof(RootRing4));
+    return b;
+}
+
+size_t filter_partial_bytes(int grid) { return size_t(grid) * sizeof(FilterPartial); }
 
 int occupancy_filtered() {
     int b = 0;
