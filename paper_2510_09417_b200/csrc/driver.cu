@@ -188,9 +188,10 @@ class Engine {
         int in = 0;
         int lvl = 2;
         lmax_ = -1;
+        tail_emitted_ = false;
         if (split && !lean && use_tail_) {
             // KT: every level in one persistent launch while they stay small
-            const int rc = run_tail(dx, dy, n, nslots, st, &lvl, &in, &S);
+            const int rc = run_tail(dx, dy, n, nslots, d_out, st, &lvl, &in, &S);
             if (rc == VQHULL_EINVAL) return rc;
             if (rc < 0) return rerun_unfiltered(dx, dy, n, d_out, h, st);
         }
@@ -315,9 +316,11 @@ class Engine {
         if (filtered) stats_.root_filter_on = h_root_->poly.filter;
 
         // ---- emission: bottom-up sizes, root frame, top-down starts
+        // (already done inside the persistent tail kernel for small trees)
         uint64_t total_slots = 0;
         for (int l = 2; l <= lmax_; ++l) total_slots += hinfo_[l].nslots;
-        if (lmax_ - 1 <= kEmitMaxLevels && total_slots <= kEmitSmallSlots) {
+        if (tail_emitted_) {
+        } else if (lmax_ - 1 <= kEmitMaxLevels && total_slots <= kEmitSmallSlots) {
             // small tree: everything in one CTA
             EmitAll E;
             std::memset(&E, 0, sizeof E);
@@ -514,8 +517,8 @@ class Engine {
     // lmax_ when the recursion ended inside it; otherwise 0 with (*lvl, *in,
     // *S) set to the level the host loop resumes at.  VQHULL_EINVAL for
     // non-finite input, -1 for an `unsafe` split root (caller reruns).
-    int run_tail(const double* dx, const double* dy, uint64_t n, uint32_t nslots, cudaStream_t st, int* lvl,
-                 int* in, uint32_t* S) {
+    int run_tail(const double* dx, const double* dy, uint64_t n, uint32_t nslots, uint32_t* d_out,
+                 cudaStream_t st, int* lvl, int* in, uint32_t* S) {
         const int l0 = *lvl;
         const int nlev = kTailLevels;
         for (int li = 0; li < nlev; ++li) {
@@ -576,20 +579,23 @@ class Engine {
         ta.part_cap = part_.cap / sizeof(Best);
         ta.chain = chain_.as<uint32_t>();
         ta.state = &ctrs_[16];
+        ta.out = d_out;
+        ta.h_out = hword_;
+        ta.p_idx = &root_->p_idx;
         if (tail_trace_) {
-            trace_.ensure(8 * (1 + 6 * kTailLevels), st);
-            ck(cudaMemsetAsync(trace_.p, 0, 8 * (1 + 6 * kTailLevels), st), "memset trace");
+            trace_.ensure(8 * (1 + 10 * kTailLevels), st);
+            ck(cudaMemsetAsync(trace_.p, 0, 8 * (1 + 10 * kTailLevels), st), "memset trace");
             ta.trace = trace_.as<unsigned long long>();
         }
         tk(3, st, [&] { ck(launch_tail(ta, sms_ * occ_tail_, st), "tail launch"); });
         if (tail_trace_) {
-            std::vector<unsigned long long> tr(1 + 6 * kTailLevels);
+            std::vector<unsigned long long> tr(1 + 10 * kTailLevels);
             ck(cudaMemcpyAsync(tr.data(), trace_.p, 8 * tr.size(), cudaMemcpyDeviceToHost, st), "d2h trace");
             ck(cudaStreamSynchronize(st), "trace sync");
-            for (int li = 0; li < kTailLevels && tr[1 + li * 6]; ++li) {
+            for (int li = 0; li < kTailLevels && tr[1 + li * 10]; ++li) {
                 fprintf(stderr, "[kt] level %d:", l0 + li);
-                for (int ph = 0; ph < 6; ++ph)
-                    if (tr[1 + li * 6 + ph]) fprintf(stderr, " %.2f", (tr[1 + li * 6 + ph] - tr[0]) * 1e-3);
+                for (int ph = 0; ph < 10; ++ph)
+                    if (tr[1 + li * 10 + ph]) fprintf(stderr, " %d:%.2f", ph, (tr[1 + li * 10 + ph] - tr[0]) * 1e-3);
                 fputc('\n', stderr);
             }
         }
@@ -604,9 +610,10 @@ class Engine {
         const LevelInfo* li = reinterpret_cast<const LevelInfo*>(h_tail_ + 2);
         hinfo_.resize(std::max<size_t>(hinfo_.size(), size_t(l0 + nlev)));
         for (int l = l0; l < int(at) && l < l0 + nlev; ++l) hinfo_[l] = li[l - l0];
-        if (how == 1) {
+        if (how == 1 || how == 3) {
             hinfo_[at] = li[at - l0];
             lmax_ = int(at);
+            tail_emitted_ = how == 3;
             VQB_TRACE("hull: tail finished at level %u", at);
         } else {
             if (how != 2 || int(at) < l0 || int(at) >= l0 + nlev) {
@@ -825,8 +832,8 @@ class Engine {
     int occ_tail_ = 1;
     // VQHULL_TAIL=0: levels only through the host-driven kernels
     bool use_tail_ = !(getenv("VQHULL_TAIL") && getenv("VQHULL_TAIL")[0] == '0');
-    static constexpr uint32_t kTailSlots = 4096;  // slot capacity of the persistent kernel's tables
     uint32_t* h_tail_ = nullptr;
+    bool tail_emitted_ = false;
     bool tail_trace_ = getenv("VQHULL_TAIL_TRACE") != nullptr;
     DevBuf trace_;  // set while rerunning an `unsafe` split-root call
     // VQHULL_ROOT=octagon: the one-pass filtered root (K1' + KB'), kept for comparison

@@ -195,6 +195,7 @@ struct TailLevel {
     uint32_t* fin_count;
 };
 constexpr int kTailLevels = 40;
+constexpr uint32_t kTailSlots = 4096;  // slot capacity of the persistent kernel's level tables
 struct TailArgs {
     TailLevel lv[kTailLevels];
     LevelInfo* info;          // LevelInfo array indexed by level
@@ -222,6 +223,9 @@ struct TailArgs {
     uint32_t* chain;
     uint32_t* state;          // [0] level, [1] 1 = finished at that level, 2 = stopped before it
     unsigned long long* trace;  // optional (VQHULL_TAIL_TRACE): CTA 0's %globaltimer per level phase
+    uint32_t* out;            // in-kernel emission: index list (nullptr: the host emits)
+    uint32_t* h_out;          // its length
+    const uint32_t* p_idx;    // &RootInfo::p_idx (the frame vertex)
 };
 
 // Emission of a small recursion tree in one kernel: per level, the slot

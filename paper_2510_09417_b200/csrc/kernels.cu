@@ -926,7 +926,7 @@ __device__ __noinline__ void planner_body(const PlanArgs& a, uint32_t nblocks) {
     }
 }
 
-__global__ void __launch_bounds__(kThreads) planner_kernel(PlanArgs a) {
+__global__ void __launch_bounds__(kThreads) planner_kernel(const __grid_constant__ PlanArgs a) {
     VQB_PDL();
     planner_body(a, gridDim.x);
 }
@@ -1217,24 +1217,42 @@ __device__ __forceinline__ void finisher_cta_body(FinCtaSmem& S, const FinRec* f
         int cur = 0, depth = 0;
         while (nnodes > 0) {
             const int nxt = cur ^ 1;
-            // (1) classify, claim two-sided slots, min-reduce the children's keys
-            for (uint32_t i = tid; i < m; i += kFcThreads) {
-                const uint16_t c = S.wnode[cur][i];
-                if (c == kDead) continue;
-                const uint16_t lid = S.work[cur][i];
-                const uint16_t p = S.np[cur][c], r = S.nr[cur][c], q = S.nq[cur][c];
-                const double u = S.x[lid], w = S.y[lid];
-                const double A = dsub(S.x[p], u), B = dsub(S.y[p], w);
-                const double E = dsub(S.x[r], u), F = dsub(S.y[r], w);
-                const double Cc = dsub(S.x[q], u), D = dsub(S.y[q], w);
-                const bool la = left_diff(A, B, E, F);
-                const bool lb = !la && left_diff(E, F, Cc, D);
-                if (la || lb) {
-                    const int s = la ? 0 : 1;
-                    const uint32_t ch = 2u * c + s;
-                    atomicMin(&S.ckey[ch], fc_key(S, cur, c, s, lid));
-                    const uint32_t pos = atomicAdd(&S.ccnt[ch], 1u);
-                    const uint32_t dest = s ? uint32_t(S.nhi[cur][c]) - 1u - pos : uint32_t(S.nlo[cur][c]) + pos;
+            // (1) classify, claim two-sided slots, min-reduce the children's keys.
+            // Near the top of the subtree most points share one of a few
+            // children, so the slot claims are warp-aggregated (one shared
+            // atomic per child per warp) and a key only attempts the min
+            // when it beats the value already there.
+            for (uint32_t i0 = tid - lane; i0 < m; i0 += kFcThreads) {  // warp-uniform trip count
+                const uint32_t i = i0 + lane;
+                const uint16_t c = i < m ? S.wnode[cur][i] : kDead;
+                uint32_t ch = 0xffffffffu;
+                uint16_t lid = 0;
+                int s = 0;
+                if (c != kDead) {
+                    lid = S.work[cur][i];
+                    const uint16_t p = S.np[cur][c], r = S.nr[cur][c], q = S.nq[cur][c];
+                    const double u = S.x[lid], w = S.y[lid];
+                    const double A = dsub(S.x[p], u), B = dsub(S.y[p], w);
+                    const double E = dsub(S.x[r], u), F = dsub(S.y[r], w);
+                    const double Cc = dsub(S.x[q], u), D = dsub(S.y[q], w);
+                    const bool la = left_diff(A, B, E, F);
+                    const bool lb = !la && left_diff(E, F, Cc, D);
+                    if (la || lb) {
+                        s = la ? 0 : 1;
+                        ch = 2u * c + s;
+                        const unsigned long long k = fc_key(S, cur, c, s, lid);
+                        if (k < S.ckey[ch]) atomicMin(&S.ckey[ch], k);
+                    }
+                }
+                const unsigned grp = __match_any_sync(kFull, ch);
+                const int leader = __ffs(grp) - 1;
+                uint32_t base = 0;
+                if (ch != 0xffffffffu && lane == leader) base = atomicAdd(&S.ccnt[ch], uint32_t(__popc(grp)));
+                base = __shfl_sync(kFull, base, leader);
+                if (ch != 0xffffffffu) {
+                    const uint32_t pos = base + __popc(grp & lanemask_lt());
+                    const uint32_t cc = ch >> 1;
+                    const uint32_t dest = s ? uint32_t(S.nhi[cur][cc]) - 1u - pos : uint32_t(S.nlo[cur][cc]) + pos;
                     S.work[nxt][dest] = lid;
                     S.wnode[nxt][dest] = uint16_t(ch);
                 }

@@ -38,10 +38,226 @@ __device__ __forceinline__ unsigned long long global_ns() {
 #define KT_TRACE(li, ph)                                                      \
     do {                                                                      \
         if (A.trace && blockIdx.x == 0 && threadIdx.x == 0)                   \
-            A.trace[1 + (li) * 6 + (ph)] = global_ns();                      \
+            A.trace[1 + (li) * 10 + (ph)] = global_ns();                      \
     } while (0)
 
-__global__ void __launch_bounds__(kThreads, 2) tail_kernel(TailArgs A) {
+// Single-CTA planner for a level of at most kTailSlots slots: the same
+// tables as planner_body (kinds, links, SegRec / FinRec, LevelInfo, reset
+// per-segment counters) from one block-wide scan — no chunk claims, no
+// look-back — and the tile -> segment map by binary search over the
+// segments' first tiles in shared memory.
+__device__ __noinline__ void tail_plan(const TailArgs& A, const TailLevel& T, uint32_t nslots,
+                                       const LevelInfo* prev, LevelInfo* info, int li) {
+    __shared__ PlanAgg s_w[kWarps];
+    __shared__ PlanAgg s_tot;
+    __shared__ uint32_t s_tile0[kTailSlots];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint64_t fin_chain_base = prev ? uint64_t(prev->fin_base) + prev->fin_total : 0ull;
+    // rounds of kThreads slots (slot k * kThreads + tid), one block scan each:
+    // a small level is one round with at most one slot per thread
+    PlanAgg carry;
+    pl_clear(carry);
+    const uint32_t rounds = (nslots + kThreads - 1) / kThreads;
+    for (uint32_t k = 0; k < rounds; ++k) {
+        const uint32_t s = k * kThreads + uint32_t(tid);
+        ChildRec c;
+        uint32_t m = 0;
+        if (s < nslots) {
+            c = T.slots[s];
+            m = c.m;
+        }
+        const uint8_t kd = s < nslots ? kind_of(m) : kEmpty;
+        PlanAgg mine;
+        pl_clear(mine);
+        mine.nseg = kd == kInternal;
+        mine.nfin = kd == kFin && m <= kFinSmall;
+        mine.nfin2 = kd == kFin && m > kFinSmall;
+        mine.leaf = kd == kLeaf;
+        mine.ntiles = kd == kInternal ? (m + kTile - 1) / kTile : 0;
+        mine.out = kd == kInternal ? m : 0;
+        mine.fin = kd == kFin ? m : 0;
+        PlanAgg incl = mine;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            PlanAgg o;
+            o.nseg = __shfl_up_sync(kFull, incl.nseg, d);
+            o.nfin = __shfl_up_sync(kFull, incl.nfin, d);
+            o.nfin2 = __shfl_up_sync(kFull, incl.nfin2, d);
+            o.ntiles = __shfl_up_sync(kFull, incl.ntiles, d);
+            o.out = __shfl_up_sync(kFull, incl.out, d);
+            o.fin = __shfl_up_sync(kFull, incl.fin, d);
+            o.leaf = __shfl_up_sync(kFull, incl.leaf, d);
+            if (lane >= d) pl_combine(incl, o);
+        }
+        if (lane == 31) s_w[warp] = incl;
+        __syncthreads();
+        PlanAgg run = carry, tot = carry;
+        for (int w = 0; w < kWarps; ++w) {
+            if (w < warp) pl_combine(run, s_w[w]);
+            pl_combine(tot, s_w[w]);
+        }
+        __syncthreads();  // s_w is rewritten by the next round
+        PlanAgg wex = incl;  // exclusive within the warp
+        wex.nseg -= mine.nseg; wex.nfin -= mine.nfin; wex.nfin2 -= mine.nfin2; wex.ntiles -= mine.ntiles;
+        wex.out -= mine.out; wex.fin -= mine.fin; wex.leaf -= mine.leaf;
+        pl_combine(run, wex);
+        carry = tot;
+        if (s >= nslots) continue;
+        T.kind[s] = kd;
+        if (kd == kInternal) {
+            SegRec g;
+            g.px = c.px; g.py = c.py; g.rx = c.rx; g.ry = c.ry; g.qx = c.qx; g.qy = c.qy;
+            g.bx = c.rx; g.by = c.ry;
+            g.adx = dsub(c.rx, c.px); g.ady = dsub(c.ry, c.py);  // EdgeFrame::make (kernels.hpp:23-25)
+            g.bdx = dsub(c.qx, c.rx); g.bdy = dsub(c.qy, c.ry);
+            g.begin = c.begin;
+            g.out = run.out;
+            g.m = c.m;
+            g.tile0 = run.ntiles;
+            g.ntiles = (c.m + kTile - 1) / kTile;
+            g.slot = s;
+            T.segs[run.nseg] = g;
+            s_tile0[run.nseg] = run.ntiles;
+            A.seg_pcnt[run.nseg] = 0;
+            A.seg_done[run.nseg] = 0;
+            A.seg_ctr[run.nseg] = 0ull;
+            T.link[s] = run.nseg;
+        } else if (kd == kFin) {
+            FinRec f;
+            f.c = c;
+            f.chain_base = fin_chain_base + run.fin;
+            f.slot = s;
+            f.pad = 0;
+            // warp-finisher segments from the front, CTA-finisher ones from the back
+            const uint32_t fi = m <= kFinSmall ? run.nfin : kTailSlots - 1u - run.nfin2;
+            T.fins[fi] = f;
+            T.link[s] = fi;
+        } else {
+            T.link[s] = 0;
+        }
+    }
+    KT_TRACE(li, 6);
+    if (tid == 0) {
+        s_tot = carry;
+        LevelInfo lv;
+        lv.nslots = nslots;
+        lv.nseg = carry.nseg;
+        lv.nfin = carry.nfin;
+        lv.ntiles = carry.ntiles;
+        lv.out_total = carry.out;
+        lv.fin_total = carry.fin;
+        lv.nleaf = carry.leaf;
+        lv.fin_base = uint32_t(fin_chain_base);
+        lv.nfin2 = carry.nfin2;
+        lv.pad = 0;
+        *info = lv;
+    }
+    __syncthreads();
+    KT_TRACE(li, 7);
+    const uint32_t nseg = s_tot.nseg, ntiles = s_tot.ntiles;
+    for (uint32_t t = tid; t < ntiles; t += kThreads) {
+        uint32_t lo = 0, hi = nseg;  // last k with tile0 <= t
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (s_tile0[mid] <= t) lo = mid; else hi = mid;
+        }
+        A.tile_seg[t] = lo;
+    }
+}
+
+// In-kernel emission (CTA 0, after the last level): the same in-order chain
+// assembly as size_kernel / poly_frame_kernel / emit_kernel (hull.cpp:59-73,
+// 259-266) with every level's slot sizes and starts in shared memory, for
+// trees of at most kTailEmitSlots slots.  Output = [p] chain(root slot).
+constexpr uint32_t kTailEmitSlots = 4096;
+struct TailEmitSmem {
+    uint32_t sz[kTailEmitSlots];
+    uint32_t st[kTailEmitSlots];
+    uint32_t kl[kTailEmitSlots];  // kind << 30 | link
+    uint32_t off[kTailLevels + 1];
+    uint32_t total;
+};
+static_assert(sizeof(TailEmitSmem) <= sizeof(FinAllSmem), "emission reuses the finisher's shared memory");
+
+// returns false (nothing written) when the tree is too large
+__device__ __noinline__ bool tail_emit(const TailArgs& A, TailEmitSmem& E, int nl) {
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (tid == 0) {
+        uint32_t o = 0;
+        for (int li = 0; li < nl; ++li) {
+            E.off[li] = o;
+            o += A.info[A.l0 + li].nslots;
+        }
+        E.off[nl] = o;
+        E.total = o;
+    }
+    __syncthreads();
+    const uint32_t total = E.total;
+    if (total > kTailEmitSlots || E.off[1] != 1u) return false;  // split root: one root slot
+    for (uint32_t i = tid; i < total; i += kThreads) {
+        int li = 0;
+        while (E.off[li + 1] <= i) ++li;
+        const TailLevel& T = A.lv[li];
+        const uint32_t s = i - E.off[li];
+        const uint32_t k = T.kind[s];
+        const uint32_t ln = T.link[s];
+        E.kl[i] = (k << 30) | ln;
+        E.sz[i] = k == kLeaf ? 1u : (k == kFin ? T.fin_count[ln] : (k == kInternal ? 1u : 0u));
+    }
+    __syncthreads();
+    for (int li = nl - 2; li >= 0; --li) {  // bottom-up subtree sizes (the last level has no internal slot)
+        for (uint32_t i = E.off[li] + tid; i < E.off[li + 1]; i += kThreads) {
+            const uint32_t kl = E.kl[i];
+            if ((kl >> 30) == kInternal) {
+                const uint32_t c = E.off[li + 1] + 2u * (kl & 0x3fffffffu);
+                E.sz[i] += E.sz[c] + E.sz[c + 1];
+            }
+        }
+        __syncthreads();
+    }
+    if (tid == 0) {  // frame: [p] chain(root slot)  (hull.cpp:259-266)
+        A.out[0] = *A.p_idx;
+        E.st[0] = 1;
+        *A.h_out = 1u + E.sz[0];
+    }
+    __syncthreads();
+    for (int li = 0; li + 1 < nl; ++li) {  // top-down starts
+        for (uint32_t i = E.off[li] + tid; i < E.off[li + 1]; i += kThreads) {
+            const uint32_t kl = E.kl[i];
+            if ((kl >> 30) == kInternal) {
+                const uint32_t c = E.off[li + 1] + 2u * (kl & 0x3fffffffu);
+                E.st[c] = E.st[i];
+                E.st[c + 1] = E.st[i] + E.sz[c] + 1u;
+            }
+        }
+        __syncthreads();
+    }
+    // writes: apexes of internal slots and leaves one per thread, finisher
+    // chains one per warp
+    for (uint32_t i = tid; i < total; i += kThreads) {
+        const uint32_t kl = E.kl[i], k = kl >> 30;
+        if (k != kLeaf && k != kInternal) continue;
+        int li = 0;
+        while (E.off[li + 1] <= i) ++li;
+        const uint32_t s = i - E.off[li];
+        uint32_t pos = E.st[i];
+        if (k == kInternal) pos += E.sz[E.off[li + 1] + 2u * (kl & 0x3fffffffu)];
+        A.out[pos] = A.lv[li].slots[s].r_idx;
+    }
+    for (uint32_t i = warp; i < total; i += kWarps) {
+        const uint32_t kl = E.kl[i];
+        if ((kl >> 30) != kFin) continue;
+        int li = 0;
+        while (E.off[li + 1] <= i) ++li;
+        const uint32_t f = kl & 0x3fffffffu;
+        const uint32_t c = E.sz[i];
+        const uint64_t b = A.lv[li].fins[f].chain_base;
+        for (uint32_t j = lane; j < c; j += 32) A.out[E.st[i] + j] = A.chain[b + j];
+    }
+    return true;
+}
+
+__global__ void __launch_bounds__(kThreads, 2) tail_kernel(const __grid_constant__ TailArgs A) {
     VQB_PDL();
     extern __shared__ __align__(16) unsigned char tl_dsm[];
     FinAllSmem& U = *reinterpret_cast<FinAllSmem*>(tl_dsm);
@@ -72,33 +288,7 @@ __global__ void __launch_bounds__(kThreads, 2) tail_kernel(TailArgs A) {
                 }
             }
             __syncthreads();
-            if (!s_flag) {
-                PlanArgs pa;
-                pa.slots = T.slots;
-                pa.nslots = A.nslots0;
-                pa.prev = prev;
-                pa.fin_cap = A.max_slots;
-                pa.segs = T.segs;
-                pa.fins = T.fins;
-                pa.kind = T.kind;
-                pa.link = T.link;
-                pa.info = info;
-                pa.flags = A.flags;
-                pa.aggs = static_cast<PlanAgg*>(A.aggs_v);
-                pa.incs = static_cast<PlanAgg*>(A.incs_v);
-                pa.epoch = A.epoch0 + uint32_t(li);
-                pa.ctr = A.plan_ctr;
-                pa.seg_pcnt = A.seg_pcnt;
-                pa.seg_done = A.seg_done;
-                pa.seg_ctr = A.seg_ctr;
-                planner_body(pa, 1u);
-                __syncthreads();
-                const uint32_t nseg = info->nseg;
-                for (uint32_t k = threadIdx.x; k < nseg; k += blockDim.x) {
-                    const uint32_t t0 = T.segs[k].tile0, nt = T.segs[k].ntiles;
-                    for (uint32_t t = 0; t < nt; ++t) A.tile_seg[t0 + t] = k;
-                }
-            }
+            if (!s_flag) tail_plan(A, T, prev ? 2u * prev->nseg : A.nslots0, prev, info, li);
         }
         KT_TRACE(li, 1);
         grid.sync();
@@ -141,9 +331,11 @@ __global__ void __launch_bounds__(kThreads, 2) tail_kernel(TailArgs A) {
         grid.sync();
         KT_TRACE(li, 5);
         if (info->nseg == 0) {  // no internal segment: the recursion ended at this level
-            if (blockIdx.x == 0 && threadIdx.x == 0) {
+            if (blockIdx.x != 0) return;
+            const bool emitted = A.out && tail_emit(A, *reinterpret_cast<TailEmitSmem*>(tl_dsm), li + 1);
+            if (threadIdx.x == 0) {
                 A.state[0] = uint32_t(l);
-                A.state[1] = 1u;
+                A.state[1] = emitted ? 3u : 1u;
             }
             return;
         }
