@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -29,6 +30,9 @@ namespace vqb {
 namespace {
 
 thread_local std::string g_last_error;
+// bumped whenever an engine buffer is (re)allocated: a captured hull graph
+// is valid only while every pointer baked into it is
+std::atomic<uint64_t> g_alloc_gen{0};
 
 // VQHULL_TRACE=1: host-side progress trace on stderr (diagnostics)
 const bool g_trace = getenv("VQHULL_TRACE") != nullptr;
@@ -67,6 +71,7 @@ struct DevBuf {
         ncap = (ncap + 255) & ~size_t(255);
         void* np = nullptr;
         ck(cudaMallocAsync(&np, ncap, st), "cudaMallocAsync");
+        g_alloc_gen.fetch_add(1);
         if (keep && p && cap) ck(cudaMemcpyAsync(np, p, cap, cudaMemcpyDeviceToDevice, st), "grow copy");
         if (p) ck(cudaFreeAsync(p, st), "cudaFreeAsync");
         p = np;
@@ -136,7 +141,7 @@ class Engine {
         ck(cudaMallocHost(&h_info_, sizeof(LevelInfo) * 2), "cudaMallocHost");
         ck(cudaMallocHost(&h_root_, sizeof(RootInfo)), "cudaMallocHost");
         ck(cudaMallocHost(&h_word_, 64), "cudaMallocHost");
-        ck(cudaMallocHost(&h_tail_, 16 + sizeof(LevelInfo) * (kTailLevels + 2)), "cudaMallocHost");
+        ck(cudaMallocHost(&h_tail_, report_bytes(kTailLevels)), "cudaMallocHost");
         partials_.ensure(partial_bytes(stream_grid_), nullptr);
         VQB_TRACE("engine: synchronize");
         ck(cudaDeviceSynchronize(), "init");
@@ -153,6 +158,9 @@ class Engine {
     int hull(const double* dx, const double* dy, uint64_t n, uint32_t* d_out, uint64_t* h,
              cudaStream_t st) {
         VQB_TRACE("hull: n=%llu", (unsigned long long)n);
+        // the legacy default stream cannot be captured into a graph: use the
+        // engine's own blocking stream, which orders with it both ways
+        if (st == nullptr) st = own_stream();
         reset_stats(n);
         *h = 0;
         if (n == 0) return VQHULL_OK;
@@ -164,10 +172,18 @@ class Engine {
         const bool aligned = ((reinterpret_cast<uintptr_t>(dx) | reinterpret_cast<uintptr_t>(dy)) & 15u) == 0;
         const bool filtered = !stable_ && !root_reference_ && !force_reference_ && aligned && !getenv("VQB_NO_TMA");
         const bool split = filtered && !root_octagon_;
-        uint32_t nslots = split ? run_root_split(dx, dy, n, st)
+        // the common small-recursion case (split root + KT) replays one
+        // captured CUDA graph: sample, filter, KT and the report copy
+        graph_run_ = split && n <= kLeanN && use_tail_ && use_graph_ && !timing_ && !tail_trace_ && !sample_trace_ && !sync_each_ &&
+                     run_graph(dx, dy, n, d_out, st);
+        uint32_t nslots = graph_run_ ? 1u
+                        : split ? run_root_split(dx, dy, n, st)
                                 : (filtered ? run_root_filtered(dx, dy, n, st) : run_root_reference(dx, dy, n, st));
         // finiteness verdict, octagon verdict, sizes for the byte accounting
-        ck(cudaMemcpyAsync(h_root_, root_, sizeof(RootInfo), cudaMemcpyDeviceToHost, st), "d2h root");
+        const bool lean = n > kLeanN;
+        const bool tail = split && !lean && use_tail_;
+        if (!tail)  // (the tail kernel reports the root's verdicts with its own state)
+            ck(cudaMemcpyAsync(h_root_, root_, sizeof(RootInfo), cudaMemcpyDeviceToHost, st), "d2h root");
 
         // ---- levels.  Every kernel of a level reads its counts from the
         // level's LevelInfo on the device (the planner derives its slot count
@@ -177,7 +193,6 @@ class Engine {
         // ended.  Levels queued past the end find zero slots and do nothing.
         // lean mode (very large n): sizes come from the planner's exact
         // counts, one host sync per level, instead of n-sized bounds
-        const bool lean = n > kLeanN;
         bufs_[0].ensure(n, st);
         if (!lean) {
             bufs_[1].ensure(n, st);
@@ -189,9 +204,10 @@ class Engine {
         int lvl = 2;
         lmax_ = -1;
         tail_emitted_ = false;
-        if (split && !lean && use_tail_) {
+        if (tail) {
             // KT: every level in one persistent launch while they stay small
-            const int rc = run_tail(dx, dy, n, nslots, d_out, st, &lvl, &in, &S);
+            const int rc = graph_run_ ? finish_tail(graph_ta_, st, &lvl, &in, &S)
+                                      : run_tail(dx, dy, n, nslots, d_out, st, &lvl, &in, &S);
             if (rc == VQHULL_EINVAL) return rc;
             if (rc < 0) return rerun_unfiltered(dx, dy, n, d_out, h, st);
         }
@@ -360,10 +376,12 @@ class Engine {
             });
         }
         }
-        ck(cudaMemcpyAsync(h_word_, hword_, 4, cudaMemcpyDeviceToHost, st), "d2h h");
-        end_timing(st);
-        VQB_TRACE("hull: final sync");
-        ck(cudaStreamSynchronize(st), "final sync");
+        if (!tail_emitted_) {  // (the tail kernel's h came with its state)
+            ck(cudaMemcpyAsync(h_word_, hword_, 4, cudaMemcpyDeviceToHost, st), "d2h h");
+            end_timing(st);
+            VQB_TRACE("hull: final sync");
+            ck(cudaStreamSynchronize(st), "final sync");
+        }
         VQB_TRACE("hull: done");
         ck(cudaGetLastError(), "kernel launch");
         if (const uint32_t f = read_and_clear_fault()) {
@@ -519,7 +537,14 @@ class Engine {
     // non-finite input, -1 for an `unsafe` split root (caller reruns).
     int run_tail(const double* dx, const double* dy, uint64_t n, uint32_t nslots, uint32_t* d_out,
                  cudaStream_t st, int* lvl, int* in, uint32_t* S) {
-        const int l0 = *lvl;
+        const TailArgs ta = tail_args(dx, dy, n, nslots, d_out, *lvl, st);
+        launch_tail_report(ta, st);
+        return finish_tail(ta, st, lvl, in, S);
+    }
+
+    // KT's arguments (and every table it writes, allocated here)
+    TailArgs tail_args(const double* dx, const double* dy, uint64_t n, uint32_t nslots, uint32_t* d_out, int l0,
+                       cudaStream_t st) {
         const int nlev = kTailLevels;
         for (int li = 0; li < nlev; ++li) {
             LevelTables& T = level(l0 + li);
@@ -582,11 +607,20 @@ class Engine {
         ta.out = d_out;
         ta.h_out = hword_;
         ta.p_idx = &root_->p_idx;
+        ta.root = root_;
+        report_.ensure(report_bytes(nlev), st);
+        ta.report = report_.as<uint32_t>();
         if (tail_trace_) {
             trace_.ensure(8 * (1 + 10 * kTailLevels), st);
-            ck(cudaMemsetAsync(trace_.p, 0, 8 * (1 + 10 * kTailLevels), st), "memset trace");
             ta.trace = trace_.as<unsigned long long>();
         }
+        return ta;
+    }
+
+    // KT's launch and the one copy of its report (stream-ordered, capturable)
+    void launch_tail_report(const TailArgs& ta, cudaStream_t st) {
+        const int l0 = ta.l0;
+        if (ta.trace) ck(cudaMemsetAsync(ta.trace, 0, 8 * (1 + 10 * kTailLevels), st), "memset trace");
         tk(3, st, [&] { ck(launch_tail(ta, sms_ * occ_tail_, st), "tail launch"); });
         if (tail_trace_) {
             std::vector<unsigned long long> tr(1 + 10 * kTailLevels);
@@ -599,15 +633,27 @@ class Engine {
                 fputc('\n', stderr);
             }
         }
-        ck(cudaMemcpyAsync(h_tail_, &ctrs_[16], 8, cudaMemcpyDeviceToHost, st), "d2h tail state");
-        ck(cudaMemcpyAsync(h_tail_ + 2, info_.as<LevelInfo>() + l0, sizeof(LevelInfo) * nlev,
-                           cudaMemcpyDeviceToHost, st), "d2h tail infos");
+        ck(cudaMemcpyAsync(h_tail_, ta.report, report_bytes(ta.nlev), cudaMemcpyDeviceToHost, st),
+           "d2h tail report");
+        end_timing(st);  // (re-recorded later if the host emits)
+    }
+
+    // after KT: one sync, then the report decides — finished (lmax_ set,
+    // perhaps emitted) or the level the host loop resumes at
+    int finish_tail(const TailArgs& ta, cudaStream_t st, int* lvl, int* in, uint32_t* S) {
+        const int l0 = ta.l0, nlev = ta.nlev;
+        const uint32_t nslots = ta.nslots0;
         VQB_TRACE("hull: tail sync");
         ck(cudaStreamSynchronize(st), "tail sync");
+        const uint32_t at = h_tail_[0], how = h_tail_[1];
+        *h_word_ = h_tail_[2];
+        h_root_->nonfinite = h_tail_[3];
+        h_root_->unsafe = h_tail_[4];
+        h_root_->poly.filter = h_tail_[5];
+        h_root_->cnt1 = h_tail_[6];
         if (h_root_->nonfinite) return VQHULL_EINVAL;
         if (h_root_->unsafe) return -1;
-        const uint32_t at = h_tail_[0], how = h_tail_[1];
-        const LevelInfo* li = reinterpret_cast<const LevelInfo*>(h_tail_ + 2);
+        const LevelInfo* li = reinterpret_cast<const LevelInfo*>(h_tail_ + 8) - 0;
         hinfo_.resize(std::max<size_t>(hinfo_.size(), size_t(l0 + nlev)));
         for (int l = l0; l < int(at) && l < l0 + nlev; ++l) hinfo_[l] = li[l - l0];
         if (how == 1 || how == 3) {
@@ -628,6 +674,80 @@ class Engine {
         return 0;
     }
 
+    // Captures (once per input / buffer set) and launches the graph of the
+    // split root + KT + report copy.  Returns false when capture fails (the
+    // caller then launches the same work directly).
+    bool run_graph(const double* dx, const double* dy, uint64_t n, uint32_t* d_out, cudaStream_t st) {
+        // allocate everything first: nothing may allocate inside the capture
+        prepare_split(n, st);
+        graph_ta_ = tail_args(dx, dy, n, 1u, d_out, 2, st);
+        const uint64_t gen = g_alloc_gen.load();
+        if (!(graph_exec_ && graph_dx_ == dx && graph_dy_ == dy && graph_n_ == n && graph_out_ == d_out &&
+              graph_st_ == st && graph_gen_ == gen)) {
+            if (graph_exec_) {
+                cudaGraphExecDestroy(graph_exec_);
+                graph_exec_ = nullptr;
+            }
+            cudaGraph_t g = nullptr;
+            VQB_TRACE("hull: capturing the split-root graph");
+            if (cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+                VQB_TRACE("hull: capture refused: %s", cudaGetErrorString(cudaGetLastError()));
+                use_graph_ = false;
+                return false;
+            }
+            const uint32_t saved = launches_;
+            try {
+                run_root_split(dx, dy, n, st);
+                launch_tail_report(graph_ta_, st);
+            } catch (...) {
+                VQB_TRACE("hull: capture threw: %s", g_last_error.c_str());
+                cudaStreamEndCapture(st, &g);
+                if (g) cudaGraphDestroy(g);
+                (void)cudaGetLastError();
+                use_graph_ = false;
+                launches_ = saved;
+                return false;
+            }
+            graph_launches_ = launches_ - saved;
+            launches_ = saved;
+            const cudaError_t e = cudaStreamEndCapture(st, &g);
+            if (e != cudaSuccess || !g || cudaGraphInstantiate(&graph_exec_, g, 0) != cudaSuccess) {
+                if (g) cudaGraphDestroy(g);
+                VQB_TRACE("hull: capture failed: %s", cudaGetErrorString(cudaGetLastError()));
+                graph_exec_ = nullptr;
+                use_graph_ = false;
+                return false;
+            }
+            cudaGraphDestroy(g);
+            if (g_alloc_gen.load() != gen) {  // something allocated during the capture: do not trust it
+                cudaGraphExecDestroy(graph_exec_);
+                graph_exec_ = nullptr;
+                use_graph_ = false;
+                return false;
+            }
+            graph_dx_ = dx; graph_dy_ = dy; graph_n_ = n; graph_out_ = d_out; graph_st_ = st; graph_gen_ = gen;
+        }
+        VQB_TRACE("hull: graph launch");
+        ck(cudaGraphLaunch(graph_exec_, st), "graph launch");
+        launches_ += graph_launches_;
+        stats_.bytes_extremes = n;
+        stats_.bytes_bootstrap = 0;
+        return true;
+    }
+
+    cudaStream_t own_stream() {
+        if (!own_st_) ck(cudaStreamCreate(&own_st_), "cudaStreamCreate");
+        return own_st_;
+    }
+
+    void prepare_split(uint64_t n, cudaStream_t st) {
+        bufs_[0].ensure(n, st);
+        level(2).slots.ensure(sizeof(ChildRec), st);
+        const uint32_t ntiles = uint32_t((n + kTile - 1) / kTile);
+        const int grid = std::max(1, std::min<int>(int(ntiles), sms_ * occ_filter_));
+        fpart_.ensure(filter_partial_bytes(grid), st);
+    }
+
     // Split root (default): K_S the octagon from a sample, then K_F the filter
     // alone over every point (survivors + exact p, q + finiteness); the first
     // level is the single bootstrap slot (p, q, p) over the survivors, which
@@ -637,8 +757,8 @@ class Engine {
             const int g = std::max(1, std::min<int>(grid_poly_, int(n / (16 * 256 * 8)) + 1));
             tk(0, st, [&] { launch_poly_sample(dx, dy, n, partials_.p, &ctrs_[5], sample_keys(), root_, side_ctr(), g, false, st); });
         }
-        if (getenv("VQHULL_SAMPLE_TRACE")) print_sample_trace();
-        upload_root_consts(root_, st);
+        if (sample_trace_) print_sample_trace();
+        upload_root_consts(root_, st);  // the filter's geometry -> constant bank (FP64 operands)
         stats_.bytes_extremes = n;  // x and y of the 1/16 sample
         stats_.bytes_bootstrap = 0;
         bufs_[0].ensure(n, st);
@@ -834,6 +954,22 @@ class Engine {
     bool use_tail_ = !(getenv("VQHULL_TAIL") && getenv("VQHULL_TAIL")[0] == '0');
     uint32_t* h_tail_ = nullptr;
     bool tail_emitted_ = false;
+    // captured split-root + KT graph (VQHULL_GRAPH=0 disables)
+    bool use_graph_ = !(getenv("VQHULL_GRAPH") && getenv("VQHULL_GRAPH")[0] == '0');
+    bool graph_run_ = false;
+    cudaStream_t own_st_ = nullptr;
+    bool sample_trace_ = getenv("VQHULL_SAMPLE_TRACE") != nullptr;
+    cudaGraphExec_t graph_exec_ = nullptr;
+    const double* graph_dx_ = nullptr;
+    const double* graph_dy_ = nullptr;
+    uint64_t graph_n_ = 0;
+    uint32_t* graph_out_ = nullptr;
+    cudaStream_t graph_st_ = nullptr;
+    uint64_t graph_gen_ = 0;
+    uint32_t graph_launches_ = 0;
+    TailArgs graph_ta_;
+    DevBuf report_;
+    static size_t report_bytes(int nlev) { return 32 + sizeof(LevelInfo) * size_t(nlev); }
     bool tail_trace_ = getenv("VQHULL_TAIL_TRACE") != nullptr;
     DevBuf trace_;  // set while rerunning an `unsafe` split-root call
     // VQHULL_ROOT=octagon: the one-pass filtered root (K1' + KB'), kept for comparison

@@ -226,6 +226,8 @@ struct TailArgs {
     uint32_t* out;            // in-kernel emission: index list (nullptr: the host emits)
     uint32_t* h_out;          // its length
     const uint32_t* p_idx;    // &RootInfo::p_idx (the frame vertex)
+    const RootInfo* root;
+    uint32_t* report;         // [8 words: state, h, nonfinite, unsafe, filter, survivors, 0] + level infos
 };
 
 // Emission of a small recursion tree in one kernel: per level, the slot

@@ -257,6 +257,26 @@ __device__ __noinline__ bool tail_emit(const TailArgs& A, TailEmitSmem& E, int n
     return true;
 }
 
+// CTA 0 at exit: everything the host needs in ONE contiguous copy — state,
+// h, the root verdicts and every processed level's LevelInfo.
+__device__ __noinline__ void tail_report(const TailArgs& A, int nl) {
+    uint32_t* r = A.report;
+    if (threadIdx.x == 0) {
+        const RootInfo* R = A.root;
+        r[0] = A.state[0];
+        r[1] = A.state[1];
+        r[2] = *A.h_out;
+        r[3] = R->nonfinite;
+        r[4] = R->unsafe;
+        r[5] = R->poly.filter;
+        r[6] = R->cnt1;
+        r[7] = 0;
+    }
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(A.info + A.l0);
+    const uint32_t words = uint32_t(nl) * uint32_t(sizeof(LevelInfo) / 4);
+    for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) r[8 + i] = src[i];
+}
+
 __global__ void __launch_bounds__(kThreads, 2) tail_kernel(const __grid_constant__ TailArgs A) {
     VQB_PDL();
     extern __shared__ __align__(16) unsigned char tl_dsm[];
@@ -295,7 +315,10 @@ __global__ void __launch_bounds__(kThreads, 2) tail_kernel(const __grid_constant
         KT_TRACE(li, 2);
         if (threadIdx.x == 0) s_flag = *reinterpret_cast<volatile uint32_t*>(&A.state[1]);
         __syncthreads();
-        if (s_flag == 2u) return;
+        if (s_flag == 2u) {
+            if (blockIdx.x == 0) tail_report(A, li);
+            return;
+        }
         // ---- work: K2 tiles, then the finisher segments
         LevelArgs la;
         la.gx = A.gx;
@@ -337,6 +360,8 @@ __global__ void __launch_bounds__(kThreads, 2) tail_kernel(const __grid_constant
                 A.state[0] = uint32_t(l);
                 A.state[1] = emitted ? 3u : 1u;
             }
+            __syncthreads();
+            tail_report(A, li + 1);
             return;
         }
         in ^= 1;
@@ -357,6 +382,28 @@ cudaError_t launch_tail(const TailArgs& a, int grid, cudaStream_t st) {
     if (!attr) {
         cudaFuncSetAttribute(tail_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(FinAllSmem)));
         attr = true;
+    }
+    // cooperative (grid barriers) and, where the driver accepts the pair,
+    // programmatic stream serialization so the launch overlaps the filter
+    // pass's tail (the kernel's griddepcontrol.wait orders the data)
+    static int pdl_ok = pdl_enabled() ? 1 : 0;
+    if (pdl_ok) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(grid);
+        cfg.blockDim = dim3(kThreads);
+        cfg.dynamicSmemBytes = sizeof(FinAllSmem);
+        cfg.stream = st;
+        cudaLaunchAttribute at[2];
+        at[0].id = cudaLaunchAttributeCooperative;
+        at[0].val.cooperative = 1;
+        at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[1].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 2;
+        const cudaError_t e = cudaLaunchKernelEx(&cfg, tail_kernel, a);
+        if (e == cudaSuccess) return e;
+        (void)cudaGetLastError();
+        pdl_ok = 0;
     }
     void* args[] = {const_cast<TailArgs*>(&a)};
     return cudaLaunchCooperativeKernel((const void*)tail_kernel, dim3(grid), dim3(kThreads), args,
