@@ -249,7 +249,10 @@ def run_ours(args):
             dist.barrier()
         torch.cuda.synchronize()
 
+    res = None
     for _ in range(max(args.warmup, 0)):
+        res = step()
+    if res is None:  # --warmup 0: one untimed call still gives h and the launch count
         res = step()
     barrier()
     h = int(res.numel())
@@ -316,8 +319,12 @@ def run_ours(args):
             traffic = json.load(f).get(f"config{args.config}", {}).get(dom)
     except Exception:
         pass
+    kname = {"root_partition": ("root_filter_tma (split root pass 1: octagon filter over every point)"
+                                if st.get("root_filtered") == 2 else "root pass"),
+             "levels": "tail_kernel (persistent recursion)" if st.get("root_filtered") == 2 else "level kernels",
+             "extremes": "poly_sample_kernel" if st.get("root_filtered") == 2 else "extremes"}.get(dom, dom)
     result["roofline"] = {
-        "bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+        "bound": "hbm", "kernel": kname, "family": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
         "frac": achieved / peak, "peak_source": peak_src, "traffic": traffic,
         "bytes_per_launch": fam[dom][1] / args.steps,
         "ms_per_launch": fam[dom][0] / args.steps,
