@@ -1139,6 +1139,10 @@ __device__ __forceinline__ void finisher_warp_body(FinSmem& S, uint32_t gw, uint
 // children are leaves.  Finally subtree sizes bottom-up and chain positions
 // top-down give chain(L) ++ [r] ++ chain(R) (assemble_chain, hull.cpp:59-73).
 // ===========================================================================
+// diagnostics (VQHULL_FIN_TRACE): block 0's CTA-finisher per-depth timestamps
+__device__ unsigned long long g_ftrace[64];
+__device__ uint32_t g_ftrace_on;
+
 constexpr int kFcThreads = 256;
 constexpr int kFcNodes = int(kFinMax / 2);  // nodes of one depth hold >= 2 points each
 constexpr uint16_t kDead = 0xffffu;
@@ -1215,7 +1219,10 @@ __device__ __forceinline__ void finisher_cta_body(FinCtaSmem& S, const FinRec* f
         __syncthreads();
         uint32_t nnodes = 1, ntree = 1;
         int cur = 0, depth = 0;
+        const bool ftr = g_ftrace_on && blockIdx.x == 0 && tid == 0;
+        if (ftr) { g_ftrace[0] = m; g_ftrace[1] = gtimer_ns(); }
         while (nnodes > 0) {
+            if (ftr && depth < 38) g_ftrace[2 + depth] = gtimer_ns();
             const int nxt = cur ^ 1;
             // (1) classify, claim two-sided slots, min-reduce the children's keys.
             // Near the top of the subtree most points share one of a few
@@ -1258,6 +1265,7 @@ __device__ __forceinline__ void finisher_cta_body(FinCtaSmem& S, const FinRec* f
                 }
             }
             __syncthreads();
+            if (ftr && depth == 0) g_ftrace[40] = gtimer_ns();
             // (2) candidates: points holding their child's minimal key
             for (uint32_t i = tid; i < m; i += kFcThreads) {
                 const uint16_t ch = S.wnode[nxt][i];
@@ -1269,6 +1277,7 @@ __device__ __forceinline__ void finisher_cta_body(FinCtaSmem& S, const FinRec* f
                 }
             }
             __syncthreads();
+            if (ftr && depth == 0) g_ftrace[41] = gtimer_ns();
             if (S.tie) {  // rare: exact offset ties -> smaller (x, y), then index
                 for (uint32_t ch = tid; ch < 2 * nnodes; ch += kFcThreads) {
                     if (S.cncand[ch] < 2) continue;
@@ -1306,6 +1315,7 @@ __device__ __forceinline__ void finisher_cta_body(FinCtaSmem& S, const FinRec* f
             }
             if (lane == 31) S.wsum[warp] = incl;
             __syncthreads();
+            if (ftr && depth == 0) g_ftrace[42] = gtimer_ns();
             uint32_t base = 0;
             for (int w2 = 0; w2 < warp; ++w2) base += S.wsum[w2];
             uint32_t id = base + incl - local;  // first next-depth id of this thread's children
@@ -1339,6 +1349,7 @@ __device__ __forceinline__ void finisher_cta_body(FinCtaSmem& S, const FinRec* f
                 if (s) S.tright[t] = link; else S.tleft[t] = link;
             }
             __syncthreads();
+            if (ftr && depth == 0) g_ftrace[43] = gtimer_ns();
             const uint32_t nn = S.nnext;
             // remap the next work array to next-depth node ids; reset the
             // accumulators and the array that becomes the next output
@@ -1359,6 +1370,7 @@ __device__ __forceinline__ void finisher_cta_body(FinCtaSmem& S, const FinRec* f
             cur = nxt;
             __syncthreads();
         }
+        if (ftr) { g_ftrace[62] = depth; g_ftrace[63] = gtimer_ns(); }
         // subtree sizes bottom-up, then chain positions top-down
         for (int d = depth - 1; d >= 0; --d) {
             for (uint32_t t = S.lvl_start[d] + tid; t < S.lvl_start[d + 1]; t += kFcThreads)
@@ -1588,6 +1600,24 @@ void launch_poly_sample(const double* xs, const double* ys, uint64_t n, void* pa
                         unsigned long long* side_ctr, int grid, bool with_pq, cudaStream_t st) {
     pdl_launch(poly_sample_kernel, grid, 256, 0, st, xs, ys, n, static_cast<SamplePartial*>(partials), ticket,
                keys, root, side_ctr, int(with_pq));
+}
+
+void fin_trace(bool on) {
+    const uint32_t v = on ? 1u : 0u;
+    cudaMemcpyToSymbol(g_ftrace_on, &v, 4);
+}
+void print_fin_trace() {
+    unsigned long long t[64];
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(t, g_ftrace, sizeof t);
+    if (!t[1]) return;
+    fprintf(stderr, "[fin] m=%llu depth=%llu total %.2f us:", t[0], t[62], (t[63] - t[1]) * 1e-3);
+    for (int d = 0; d < 38 && d < int(t[62]); ++d) fprintf(stderr, " %.2f", (t[2 + d] - t[1]) * 1e-3);
+    fprintf(stderr, " | depth0 phases:");
+    for (int k = 40; k < 44; ++k) fprintf(stderr, " %.2f", (t[k] - t[1]) * 1e-3);
+    fputc('\n', stderr);
+    const unsigned long long z[64] = {};
+    cudaMemcpyToSymbol(g_ftrace, z, sizeof z);
 }
 
 void print_sample_trace() {

@@ -1534,8 +1534,9 @@ __global__ void __launch_bounds__(kCtlThreads, 3) root_filter_tma(FilterArgs a) 
         if (t >= nfull) return;
         const int s = int(k % kRing4);
         mbar_expect_tx(&ring.bar[s], 2u * kTile * 8u);
-        tma_load_1d(ring.x[s], a.xs + uint64_t(t) * kTile, kTile * 8u, &ring.bar[s]);
-        tma_load_1d(ring.y[s], a.ys + uint64_t(t) * kTile, kTile * 8u, &ring.bar[s]);
+        const unsigned long long pol = l2_evict_first_policy();
+        tma_load_1d_stream(ring.x[s], a.xs + uint64_t(t) * kTile, kTile * 8u, &ring.bar[s], pol);
+        tma_load_1d_stream(ring.y[s], a.ys + uint64_t(t) * kTile, kTile * 8u, &ring.bar[s], pol);
     };
     if (threadIdx.x == kThreads) {
         for (int s = 0; s < kRing4; ++s) mbar_init(&ring.bar[s], 1);
