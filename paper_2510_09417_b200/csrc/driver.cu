@@ -507,11 +507,11 @@ class Engine {
         tk(0, st, [&] { launch_extremes(dx, dy, n, partials_.p, &ctrs_[3], root_, grid_ext_, st); });
         {
             // the sample is 1/16 of the points: a smaller grid
-            const int g = std::max(1, std::min<int>(grid_poly_, int(n / (16 * 256 * 8)) + 1));
+            const int g = std::max(1, std::min<int>(grid_poly_, int(n / ((uint64_t(sample_mask(n)) + 1) * 256 * 8)) + 1));
             tk(0, st, [&] { launch_poly_sample(dx, dy, n, partials_.p, &ctrs_[5], sample_keys(), root_, side_ctr(), g, true, st); });
         }
         upload_root_consts(root_, st);
-        stats_.bytes_extremes = 8 * n + n;  // x, then x and y of the 1/16 sample
+        stats_.bytes_extremes = 8 * n + 16 * n / (sample_mask(n) + 1);  // x, then x and y of the sample
         stats_.bytes_bootstrap = 0;
         bufs_[0].ensure(n, st);
         const uint32_t ntiles_root = uint32_t((n + kTile - 1) / kTile);
@@ -730,7 +730,7 @@ class Engine {
         VQB_TRACE("hull: graph launch");
         ck(cudaGraphLaunch(graph_exec_, st), "graph launch");
         launches_ += graph_launches_;
-        stats_.bytes_extremes = n;
+        stats_.bytes_extremes = 16 * n / (sample_mask(n) + 1);
         stats_.bytes_bootstrap = 0;
         return true;
     }
@@ -754,12 +754,12 @@ class Engine {
     // the level machinery partitions like any other segment.  Returns 1.
     uint32_t run_root_split(const double* dx, const double* dy, uint64_t n, cudaStream_t st) {
         {
-            const int g = std::max(1, std::min<int>(grid_poly_, int(n / (16 * 256 * 8)) + 1));
+            const int g = std::max(1, std::min<int>(grid_poly_, int(n / ((uint64_t(sample_mask(n)) + 1) * 256 * 8)) + 1));
             tk(0, st, [&] { launch_poly_sample(dx, dy, n, partials_.p, &ctrs_[5], sample_keys(), root_, side_ctr(), g, false, st); });
         }
         if (sample_trace_) print_sample_trace();
         upload_root_consts(root_, st);  // the filter's geometry -> constant bank (FP64 operands)
-        stats_.bytes_extremes = n;  // x and y of the 1/16 sample
+        stats_.bytes_extremes = 16 * n / (sample_mask(n) + 1);  // x and y of the sample
         stats_.bytes_bootstrap = 0;
         bufs_[0].ensure(n, st);
         const uint32_t ntiles = uint32_t((n + kTile - 1) / kTile);

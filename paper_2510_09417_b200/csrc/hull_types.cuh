@@ -22,29 +22,39 @@ constexpr uint32_t kFinSmall = 64;          // segments of 2..64 points: warp fi
 constexpr uint32_t kFinMax = 1024;          // 65..1024 points: CTA finisher; larger: tiled level kernel
 
 // Root stage geometry.  The recursion itself always follows the reference
-// (level 1 splits by p->q, hull.cpp:228-235); the octagon of the 8 exact
-// directional extremes is only a FILTER in front of it: a point provably
-// inside the octagon by a margin far above the predicates' rounding can never
-// be a farthest point or a lone subset member, so dropping it cannot change
-// the reference's output.
-//  * vx/vy/vidx: V_j = extreme in direction j * 45 degrees clockwise from -x
-//    (L, TL, T, TR, R, BR, B, BL); chord j = V_j -> V_{j+1 mod 8};
+// (level 1 splits by p->q, hull.cpp:228-235); a polygon of kPolyV input
+// points (directional extremes of a sample) is only a FILTER in front of it:
+// a point provably inside the polygon by a margin far above the predicates'
+// rounding can never be a farthest point or a lone subset member, so dropping
+// it cannot change the reference's output.
+//  * vx/vy/vidx: V_j = the sample's extreme along direction j, the 16
+//    directions (-1,0), (-2,1), (-1,1), (-1,2), (0,1), (1,2), (1,1), (2,1),
+//    (1,0), ... clockwise from -x; chord j = V_j -> V_{j+1 mod 16};
+//  * two inner regions verified inside the filter region, tested before any
+//    chord: an open box (every point) and an octagon = box' ∩ diamond
+//    (points outside the box);
 //  * emission frame: nv vertices, slot j between V_j and V_{j+1}, repeated
-//    vertices written once: nv = 2 (p, q) for the filtered root, 4 (p, r1,
-//    q, r2) for the fused levels-1+2 root.
+//    vertices written once: nv = 2 (p, q) for the one-pass filtered root,
+//    4 (p, r1, q, r2) for the fused levels-1+2 root, 1 (p) for the split root.
+constexpr int kPolyV = 16;
 struct RootPoly {
-    double vx[8], vy[8];
-    uint32_t vidx[8];
+    double vx[kPolyV], vy[kPolyV];
+    uint32_t vidx[kPolyV];
     double ex[4], ey[4];        // emission frame vertices
     uint32_t eidx[4];
     uint32_t nv;
-    uint32_t filter;            // 1: the octagon filter may drop points
+    uint32_t filter;            // 1: the polygon filter may drop points
     // chord j as a linear form f_j(P) = fa*x + fb*y + fc = cross(V_{j+1} - V_j,
     // P - V_j) (> 0: left of the chord, outside); P is dropped when
-    // f_j(P) < ft_j for all 8 chords (ft_j = -margin * |chord|_1)
-    double fa[8], fb[8], fc[8], ft[8];
+    // f_j(P) < ft_j for all chords (ft_j = -margin * |chord|_1)
+    double fa[kPolyV], fb[kPolyV], fc[kPolyV], ft[kPolyV];
     double bx0, bx1, by0, by1;  // open box verified to lie inside the filter region
-    double mref;                // M: max |coordinate| of the 8 vertices (the margin is 2^-32 M)
+    // octagon |x - ocx| < ohx, |y - ocy| < ohy, |x - ocx| + |y - ocy| < od,
+    // verified (its 8 vertices) to lie inside the filter region
+    double ocx, ocy, ohx, ohy, od;
+    uint32_t oct_on;            // the octagon is tested (it covers clearly more than the box)
+    uint32_t pad2;
+    double mref;                // M: max |coordinate| of the vertices (the margin is 2^-32 M)
 };
 
 // K1 + pass A results, one per hull call (device resident).

@@ -346,8 +346,8 @@ __global__ void __launch_bounds__(256) bootstrap_argmax_kernel(
 // ===========================================================================
 struct PolyPartial {
     ExtKey lo, hi;
-    double av[8];
-    uint32_t ai[8];
+    double av[kPolyV];
+    uint32_t ai[kPolyV];
     double sx, sy, sn;  // sums over the sample (centre of the filter's inner box)
     uint32_t nonfinite;
     uint32_t pad;
@@ -372,89 +372,7 @@ __device__ __forceinline__ unsigned long long gtimer_ns() {
 }
 
 constexpr int kSampleShift = 9;  // groups of 512 pairs (1024 points, 8 KB of x and of y)
-constexpr int kSampleUnroll = 8;  // double2 loads per array per thread in flight
-constexpr int kSampleMask = 15;  // one group in 16 is sampled
-
-// sampled directions, in octagon slot order: 0 min x, 1 min x-y, 2 max y,
-// 3 max x+y, 4 max x, 5 max x-y, 6 min y, 7 min x+y
-__device__ __forceinline__ bool approx_better(int a, double v, uint32_t i, double vb, uint32_t ib) {
-    if (i == kNoIdx) return false;
-    if (ib == kNoIdx) return true;
-    const bool maximize = (a >= 2 && a <= 5);
-    if (v != vb) return maximize ? v > vb : v < vb;
-    return i < ib;
-}
-
-__device__ __forceinline__ PolyPartial poly_none() {
-    const double kInf = __longlong_as_double(0x7ff0000000000000ll);
-    PolyPartial p;
-    p.lo = ExtKey{0.0, 0.0, kNoIdx, 0u};
-    p.hi = ExtKey{0.0, 0.0, kNoIdx, 0u};
-    p.nonfinite = 0u;
-    p.pad = 0u;
-    p.sx = p.sy = p.sn = 0.0;
-    const double init[8] = {kInf, kInf, -kInf, -kInf, -kInf, -kInf, kInf, kInf};
-#pragma unroll
-    for (int q = 0; q < 8; ++q) { p.av[q] = init[q]; p.ai[q] = kNoIdx; }
-    return p;
-}
-
-// block-wide fold, field group by field group (warp butterflies, then
-// thread 0 over the 8 warp results in shared memory); the result is valid in
-// thread 0.  Reference parameters keep the fields in registers; no struct
-// copies, no spills.
-__device__ __forceinline__ void block_reduce_poly(ExtKey& lo, ExtKey& hi, double (&av)[8], uint32_t (&ai)[8],
-                                                  double& sx, double& sy, double& sn, uint32_t& nb,
-                                                  PolyPartial* s_w) {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-#pragma unroll
-    for (int s = 16; s > 0; s >>= 1) {
-        const ExtKey a = shfl_key(lo, s);
-        if (lo_better(a, lo)) lo = a;
-        const ExtKey b = shfl_key(hi, s);
-        if (hi_better(b, hi)) hi = b;
-        nb |= __shfl_xor_sync(kFull, nb, s);
-        sx += __shfl_xor_sync(kFull, sx, s);
-        sy += __shfl_xor_sync(kFull, sy, s);
-        sn += __shfl_xor_sync(kFull, sn, s);
-    }
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-#pragma unroll
-        for (int s = 16; s > 0; s >>= 1) {
-            const double ov = __shfl_xor_sync(kFull, av[q], s);
-            const uint32_t oi = __shfl_xor_sync(kFull, ai[q], s);
-            if (approx_better(q, ov, oi, av[q], ai[q])) { av[q] = ov; ai[q] = oi; }
-        }
-    }
-    if (lane == 0) {
-        s_w[warp].lo = lo;
-        s_w[warp].hi = hi;
-        s_w[warp].nonfinite = nb;
-        s_w[warp].sx = sx;
-        s_w[warp].sy = sy;
-        s_w[warp].sn = sn;
-#pragma unroll
-        for (int q = 0; q < 8; ++q) { s_w[warp].av[q] = av[q]; s_w[warp].ai[q] = ai[q]; }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        for (int w = 1; w < int(blockDim.x >> 5); ++w) {
-            if (lo_better(s_w[w].lo, lo)) lo = s_w[w].lo;
-            if (hi_better(s_w[w].hi, hi)) hi = s_w[w].hi;
-            nb |= s_w[w].nonfinite;
-            sx += s_w[w].sx;
-            sy += s_w[w].sy;
-            sn += s_w[w].sn;
-#pragma unroll
-            for (int q = 0; q < 8; ++q)
-                if (approx_better(q, s_w[w].av[q], s_w[w].ai[q], av[q], ai[q])) {
-                    av[q] = s_w[w].av[q];
-                    ai[q] = s_w[w].ai[q];
-                }
-        }
-    }
-}
+constexpr int kSampleUnroll = 4;  // double2 loads per array per thread in flight
 
 // Last step of K1' (one warp, poly_finish_warp): p, q (exact, in the
 // one-pass octagon root), the octagon filter (the sample's 8 directional
@@ -468,15 +386,12 @@ __device__ __forceinline__ void block_reduce_poly(ExtKey& lo, ExtKey& hi, double
 // multiply-adds' rounding can never reach a dropped point and no reference
 // predicate can see one as a hull or farthest candidate.  Outside
 // 2^-400 <= M <= 2^500 (products could underflow/overflow): no filter.
-// One warp: lane l owns chord
-// j = l & 7 (each chord four times), box corner c = l >> 3 in the 32-lane
-// inside-tests, so a box candidate costs one FMA pair and one vote instead of
-// 32 serial tests.  Every expression is poly_finish's, so the filter is
-// bit-identical.
+// One warp: lane l owns vertex / chord j = l & 15 (each twice) and a share of
+// the inside-tests, so a candidate region costs a few FMAs and one vote.
 __device__ __noinline__ void poly_finish_warp(const PolyPartial& F, const double* __restrict__ xs,
                                               const double* __restrict__ ys, RootInfo* root, bool with_pq) {
     const double kInf = __longlong_as_double(0x7ff0000000000000ll);
-    const int lane = threadIdx.x & 31, j = lane & 7, corner = lane >> 3;
+    const int lane = threadIdx.x & 31, j = lane & (kPolyV - 1), half = lane >> 4;
     const ExtKey L = F.lo, H = F.hi;
     const uint32_t nb = F.nonfinite;
     RootInfo& R = *root;
@@ -488,30 +403,44 @@ __device__ __noinline__ void poly_finish_warp(const PolyPartial& F, const double
     ok &= __all_sync(kFull, aj != kNoIdx);
     auto VX = [&](int k) { return __shfl_sync(kFull, vxj, k); };
     auto VY = [&](int k) { return __shfl_sync(kFull, vyj, k); };
-    double M = fmax(fabs(vxj), fabs(vyj));
+    auto wmax = [&](double v) {
 #pragma unroll
-    for (int s = 16; s > 0; s >>= 1) M = fmax(M, __shfl_xor_sync(kFull, M, s));
+        for (int s = 16; s > 0; s >>= 1) v = fmax(v, __shfl_xor_sync(kFull, v, s));
+        return v;
+    };
+    auto wmin = [&](double v) {
+#pragma unroll
+        for (int s = 16; s > 0; s >>= 1) v = fmin(v, __shfl_xor_sync(kFull, v, s));
+        return v;
+    };
+    const double M = wmax(fmax(fabs(vxj), fabs(vyj)));
     ok &= M >= 0x1p-400 && M <= 0x1p500;
     // chord j = V_j -> V_{j+1}
-    const double nxj = VX((j + 1) & 7), nyj = VY((j + 1) & 7);
+    const double nxj = VX((j + 1) & (kPolyV - 1)), nyj = VY((j + 1) & (kPolyV - 1));
     const double ex = nxj - vxj, ey = nyj - vyj;
     const bool deg = ex == 0.0 && ey == 0.0;  // degenerate chord: no constraint
     const double fa = deg ? 0.0 : -ey;
     const double fb = deg ? 0.0 : ex;
     const double fc = deg ? -1.0 : ey * vxj - ex * vyj;
     const double ft = deg ? 0.0 : -0x1p-32 * M * (fabs(ex) + fabs(ey));
-    const int chords = __popc(__ballot_sync(kFull, !deg)) / 4;
-    auto inside_pt = [&](double x, double y) {
-        return __all_sync(kFull, __fma_rn(fa, x, __fma_rn(fb, y, fc)) < ft);
+    const int chords = __popc(__ballot_sync(kFull, !deg)) / 2;
+    auto in_j = [&](double x, double y) { return __fma_rn(fa, x, __fma_rn(fb, y, fc)) < ft; };
+    auto inside_pt = [&](double x, double y) { return __all_sync(kFull, in_j(x, y)); };
+    auto inside_box = [&](double x0, double x1, double y0, double y1) {  // corners half, half + 2
+        return __all_sync(kFull, in_j((half & 1) ? x1 : x0, y0) && in_j((half & 1) ? x1 : x0, y1));
     };
-    auto inside_box = [&](double x0, double x1, double y0, double y1) {
-        const double x = (corner & 1) ? x1 : x0, y = (corner & 2) ? y1 : y0;
-        return __all_sync(kFull, __fma_rn(fa, x, __fma_rn(fb, y, fc)) < ft);
+    // octagon {|X| < hx, |Y| < hy, |X| + |Y| < d} around (cx, cy): its
+    // vertices (+-hx, +-min(hy, d - hx)), (+-min(hx, d - hy), +-hy)
+    auto inside_oct = [&](double cx, double cy, double hx, double hy, double d) {
+        const double a = fmin(hy, d - hx), b = fmin(hx, d - hy);
+        const double sx = half ? -1.0 : 1.0;
+        return __all_sync(kFull, in_j(cx + sx * hx, cy + a) && in_j(cx + sx * hx, cy - a) &&
+                                     in_j(cx + sx * b, cy + hy) && in_j(cx + sx * b, cy - hy));
     };
     // inner box between the diagonal vertices (shrunk a little), kept only if
     // its 4 corners pass the test (the filter region is convex)
-    const double cx0 = fmax(VX(1), VX(7)), cx1 = fmin(VX(3), VX(5));
-    const double cy0 = fmax(VY(5), VY(7)), cy1 = fmin(VY(1), VY(3));
+    const double cx0 = fmax(VX(2), VX(14)), cx1 = fmin(VX(6), VX(10));
+    const double cy0 = fmax(VY(10), VY(14)), cy1 = fmin(VY(2), VY(6));
     double bx0 = kInf, bx1 = -kInf, by0 = kInf, by1 = -kInf;  // empty
     const double shrink[3] = {0x1p-20 * M, 0x1p-10 * M, 0.0625 * fmax(cx1 - cx0, cy1 - cy0)};
     for (int t = 0; t < 3; ++t) {
@@ -522,28 +451,20 @@ __device__ __noinline__ void poly_finish_warp(const PolyPartial& F, const double
             break;
         }
     }
+    const double xmin = wmin(vxj), xmax = wmax(vxj), ymin = wmin(vyj), ymax = wmax(vyj);
     // second candidate: the largest box around the sample's mean with the
-    // octagon's aspect (closed form per chord), verified like the first
-    if (F.sn > 0.0) {
-        const double cx = F.sx / F.sn, cy = F.sy / F.sn;
-        double xmin = vxj, xmax = vxj, ymin = vyj, ymax = vyj;
-#pragma unroll
-        for (int s = 16; s > 0; s >>= 1) {
-            xmin = fmin(xmin, __shfl_xor_sync(kFull, xmin, s));
-            xmax = fmax(xmax, __shfl_xor_sync(kFull, xmax, s));
-            ymin = fmin(ymin, __shfl_xor_sync(kFull, ymin, s));
-            ymax = fmax(ymax, __shfl_xor_sync(kFull, ymax, s));
-        }
+    // polygon's aspect (closed form per chord), verified like the first
+    const bool mean_ok = F.sn > 0.0;
+    const double mx = mean_ok ? F.sx / F.sn : 0.0, my = mean_ok ? F.sy / F.sn : 0.0;
+    if (mean_ok) {
         const double W = 0.5 * (xmax - xmin), Hh = 0.5 * (ymax - ymin);
-        if (inside_pt(cx, cy) && W > 0.0 && Hh > 0.0) {
-            const double f0 = fa * cx + fb * cy + fc;
+        if (inside_pt(mx, my) && W > 0.0 && Hh > 0.0) {
+            const double f0 = fa * mx + fb * my + fc;
             const double g = fabs(fa) * W + fabs(fb) * Hh;
-            double t = g > 0.0 ? fmin(1.0, (ft - f0) / g) : 1.0;
-#pragma unroll
-            for (int s = 16; s > 0; s >>= 1) t = fmin(t, __shfl_xor_sync(kFull, t, s));
+            double t = wmin(g > 0.0 ? fmin(1.0, (ft - f0) / g) : 1.0);
             for (int tries = 0; tries < 4 && t > 0.0; ++tries, t *= 0.5) {
-                const double x0 = cx - 0.999 * t * W, x1 = cx + 0.999 * t * W;
-                const double y0 = cy - 0.999 * t * Hh, y1 = cy + 0.999 * t * Hh;
+                const double x0 = mx - 0.999 * t * W, x1 = mx + 0.999 * t * W;
+                const double y0 = my - 0.999 * t * Hh, y1 = my + 0.999 * t * Hh;
                 if (x0 < x1 && y0 < y1 && inside_box(x0, x1, y0, y1)) {
                     const double a_old = bx0 < bx1 ? (bx1 - bx0) * (by1 - by0) : 0.0;
                     if ((x1 - x0) * (y1 - y0) > a_old) { bx0 = x0; bx1 = x1; by0 = y0; by1 = y1; }
@@ -552,14 +473,52 @@ __device__ __noinline__ void poly_finish_warp(const PolyPartial& F, const double
             }
         }
     }
+    // the octagon, for the points outside the box: around the box centre (or
+    // the mean), the polygon's own extents in x, y and x +- y, scaled by the
+    // largest s that keeps its 8 vertices inside every chord (closed form)
+    double ocx = 0.0, ocy = 0.0, ohx = -1.0, ohy = -1.0, od = -1.0;  // empty: |.| < -1 never holds
+    {
+        const bool have_box = bx0 < bx1;
+        const double cx = have_box ? 0.5 * (bx0 + bx1) : mx, cy = have_box ? 0.5 * (by0 + by1) : my;
+        if ((have_box || mean_ok) && inside_pt(cx, cy)) {
+            const double Wx = wmax(fabs(vxj - cx)), Wy = wmax(fabs(vyj - cy));
+            const double Wd = wmax(fabs(vxj - cx) + fabs(vyj - cy));
+            const double a = fmin(Wy, Wd - Wx), b = fmin(Wx, Wd - Wy);
+            const double f0 = fa * cx + fb * cy + fc;
+            // this lane's chord against the vertices of its half
+            const double sx = half ? -1.0 : 1.0;
+            const double den[4] = {fa * sx * Wx + fb * a, fa * sx * Wx - fb * a, fa * sx * b + fb * Wy,
+                                   fa * sx * b - fb * Wy};
+            double s = kInf;
+#pragma unroll
+            for (int v = 0; v < 4; ++v)
+                if (den[v] > 0.0) s = fmin(s, (ft - f0) / den[v]);
+            s = 0.999 * wmin(s);
+            for (int tries = 0; tries < 4 && s > 0.0 && s < kInf; ++tries, s *= 0.5) {
+                const double hx = s * Wx, hy = s * Wy, d = s * Wd;
+                if (hx > 0.0 && hy > 0.0 && inside_oct(cx, cy, hx, hy, d)) {
+                    ocx = cx; ocy = cy; ohx = hx; ohy = hy; od = d;
+                    break;
+                }
+            }
+        }
+    }
     ok &= chords >= 2;  // all vertices equal: the test would constrain nothing
-    if (lane < 8) {
+    if (lane < kPolyV) {
         P.vx[j] = vxj; P.vy[j] = vyj; P.vidx[j] = aj;
         P.fa[j] = fa; P.fb[j] = fb; P.fc[j] = fc; P.ft[j] = ft;
     }
     if (lane != 0) return;
     P.mref = M;
     P.bx0 = bx0; P.bx1 = bx1; P.by0 = by0; P.by1 = by1;
+    P.ocx = ocx; P.ocy = ocy; P.ohx = ohx; P.ohy = ohy; P.od = od;
+    {
+        const double box_area = bx0 < bx1 ? (bx1 - bx0) * (by1 - by0) : 0.0;
+        const double cut = fmax(0.0, ohx + ohy - od);
+        const double oct_area = ohx > 0.0 ? 4.0 * ohx * ohy - 2.0 * cut * cut : 0.0;
+        P.oct_on = oct_area > 1.02 * box_area ? 1u : 0u;
+        P.pad2 = 0u;
+    }
     P.filter = ok ? 1u : 0u;
     if (!with_pq) return;
     P.nv = 2;  // emission frame: [p] chain(S1) [q] chain(S2)
@@ -576,22 +535,34 @@ __global__ void __launch_bounds__(256, 2) poly_sample_kernel(const double* __res
                                                             const double* __restrict__ ys, uint64_t n,
                                                             SamplePartial* partials, uint32_t* ticket,
                                                             unsigned long long* keys, RootInfo* root,
-                                                            unsigned long long* side_ctr, int with_pq) {
+                                                            unsigned long long* side_ctr, int with_pq,
+                                                            uint32_t smask) {
     VQB_PDL();
     const double kInf = __longlong_as_double(0x7ff0000000000000ll);
-    double av[8] = {kInf, kInf, -kInf, -kInf, -kInf, -kInf, kInf, kInf};
-    uint32_t ai[8] = {kNoIdx, kNoIdx, kNoIdx, kNoIdx, kNoIdx, kNoIdx, kNoIdx, kNoIdx};
+    // slot j: the extreme of the functional of direction j (clockwise from
+    // -x, see RootPoly): 0 min x, 1 min 2x-y, 2 min x-y, 3 min x-2y, 4 max y,
+    // 5 max x+2y, 6 max x+y, 7 max 2x+y, 8 max x, 9 max 2x-y, 10 max x-y,
+    // 11 max x-2y, 12 min y, 13 min x+2y, 14 min x+y, 15 min 2x+y
+    double av[kPolyV];
+    uint32_t ai[kPolyV];
+#pragma unroll
+    for (int a = 0; a < kPolyV; ++a) {
+        av[a] = (a >= 4 && a <= 11) ? -kInf : kInf;
+        ai[a] = kNoIdx;
+    }
     double ssx = 0.0, ssy = 0.0;  // sample sums (non-finite input is rejected anyway)
     uint32_t ssn = 0;
     auto visit_xy = [&](uint32_t i, double x, double y) {
         const double s = __dadd_rn(x, y), d = __dsub_rn(x, y);
+        const double u1 = __dadd_rn(x, s), u2 = __dadd_rn(y, s);  // 2x+y, x+2y
+        const double u3 = __dadd_rn(x, d), u4 = __dsub_rn(d, y);  // 2x-y, x-2y
         ssx = __dadd_rn(ssx, x);
         ssy = __dadd_rn(ssy, y);
         ++ssn;
-        const double val[8] = {x, d, y, s, x, d, y, s};
+        const double val[kPolyV] = {x, u3, d, u4, y, u2, s, u1, x, u3, d, u4, y, u2, s, u1};
 #pragma unroll
-        for (int a = 0; a < 8; ++a) {
-            const bool maximize = (a >= 2 && a <= 5);
+        for (int a = 0; a < kPolyV; ++a) {
+            const bool maximize = (a >= 4 && a <= 11);
             const bool take = maximize ? val[a] > av[a] : val[a] < av[a];
             av[a] = take ? val[a] : av[a];
             ai[a] = take ? i : ai[a];
@@ -608,10 +579,10 @@ __global__ void __launch_bounds__(256, 2) poly_sample_kernel(const double* __res
         if ((n & 1) && tid == 0) visit_xy(uint32_t(n - 1), xs[n - 1], ys[n - 1]);
         // x and y of the sampled groups (every 16th run of 512 pairs)
         const uint32_t ngroups = (npair + (1u << kSampleShift) - 1) >> kSampleShift;
-        const uint32_t nsg = (ngroups + kSampleMask) / (kSampleMask + 1);
+        const uint32_t nsg = (ngroups + smask) / (smask + 1);
         const uint32_t nsample = nsg << kSampleShift;
         auto pair_of = [&](uint32_t m) {
-            return ((m >> kSampleShift) * (kSampleMask + 1) << kSampleShift) | (m & ((1u << kSampleShift) - 1));
+            return ((m >> kSampleShift) * (smask + 1) << kSampleShift) | (m & ((1u << kSampleShift) - 1));
         };
         uint32_t m = tid;
         for (; m + (kSampleUnroll - 1) * stride < nsample; m += kSampleUnroll * stride) {
@@ -641,7 +612,7 @@ __global__ void __launch_bounds__(256, 2) poly_sample_kernel(const double* __res
         }
     } else {
         for (uint32_t i = tid; i < n; i += stride)
-            if (((i >> (kSampleShift + 1)) & kSampleMask) == 0) visit_xy(i, xs[i], ys[i]);
+            if (((i >> (kSampleShift + 1)) & smask) == 0) visit_xy(i, xs[i], ys[i]);
     }
     if (threadIdx.x == 0) atomicMax(&g_strace[1], gtimer_ns());
     // Reductions.  A vertex only has to be SOME input point (see
@@ -649,14 +620,14 @@ __global__ void __launch_bounds__(256, 2) poly_sample_kernel(const double* __res
     // one 64-bit atomicMax per direction on {order key of the value rounded to
     // f32, ~index}: order-independent, hence deterministic, and no serial
     // fold.  The sample sums (box centre) are combined in a fixed order.
-    __shared__ unsigned long long s_key[8][8];
+    __shared__ unsigned long long s_key[kPolyV][8];
     __shared__ double s_sum[3][8];
     __shared__ bool s_last;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    unsigned long long key[8];
+    unsigned long long key[kPolyV];
 #pragma unroll
-    for (int a = 0; a < 8; ++a) {
-        const bool maximize = (a >= 2 && a <= 5);
+    for (int a = 0; a < kPolyV; ++a) {
+        const bool maximize = (a >= 4 && a <= 11);
         key[a] = ai[a] == kNoIdx ? 0ull
                                  : (uint64_t(f32_order_key(maximize ? av[a] : -av[a])) << 32) | uint32_t(~ai[a]);
     }
@@ -664,7 +635,7 @@ __global__ void __launch_bounds__(256, 2) poly_sample_kernel(const double* __res
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
 #pragma unroll
-        for (int a = 0; a < 8; ++a) {
+        for (int a = 0; a < kPolyV; ++a) {
             const unsigned long long k = __shfl_xor_sync(kFull, key[a], o);
             key[a] = k > key[a] ? k : key[a];
         }
@@ -674,16 +645,16 @@ __global__ void __launch_bounds__(256, 2) poly_sample_kernel(const double* __res
     }
     if (lane == 0) {
 #pragma unroll
-        for (int a = 0; a < 8; ++a) s_key[a][warp] = key[a];
+        for (int a = 0; a < kPolyV; ++a) s_key[a][warp] = key[a];
         s_sum[0][warp] = sx; s_sum[1][warp] = sy; s_sum[2][warp] = sn;
     }
     __syncthreads();
-    if (threadIdx.x < 8) {
+    if (threadIdx.x < kPolyV) {
         unsigned long long k = s_key[threadIdx.x][0];
         for (int w = 1; w < 8; ++w) k = s_key[threadIdx.x][w] > k ? s_key[threadIdx.x][w] : k;
         if (k) atomicMax(&keys[threadIdx.x], k);
-    } else if (threadIdx.x < 11) {
-        const int c = threadIdx.x - 8;
+    } else if (threadIdx.x < kPolyV + 3) {
+        const int c = threadIdx.x - kPolyV;
         double t = 0.0;
         for (int w = 0; w < 8; ++w) t += s_sum[c][w];
         partials[blockIdx.x].s[c] = t;
@@ -730,7 +701,7 @@ __global__ void __launch_bounds__(256, 2) poly_sample_kernel(const double* __res
         }
         s_fin.pad = 0u;
     }
-    if (threadIdx.x < 8) {
+    if (threadIdx.x < kPolyV) {
         const unsigned long long k = __ldcg(&keys[threadIdx.x]);
         s_fin.ai[threadIdx.x] = k ? ~uint32_t(k) : kNoIdx;
         s_fin.av[threadIdx.x] = 0.0;  // unused: vertices are re-read by index
@@ -1599,7 +1570,7 @@ void launch_poly_sample(const double* xs, const double* ys, uint64_t n, void* pa
                         uint32_t* ticket, unsigned long long* keys, RootInfo* root,
                         unsigned long long* side_ctr, int grid, bool with_pq, cudaStream_t st) {
     pdl_launch(poly_sample_kernel, grid, 256, 0, st, xs, ys, n, static_cast<SamplePartial*>(partials), ticket,
-               keys, root, side_ctr, int(with_pq));
+               keys, root, side_ctr, int(with_pq), sample_mask(n));
 }
 
 void fin_trace(bool on) {
@@ -1618,6 +1589,14 @@ void print_fin_trace() {
     fputc('\n', stderr);
     const unsigned long long z[64] = {};
     cudaMemcpyToSymbol(g_ftrace, z, sizeof z);
+}
+
+// one run of 1024 points in (mask + 1) is sampled: the largest power of two
+// that still leaves >= 3M sample points (1/32 at n = 1e8, 1/256 at 1e9)
+uint32_t sample_mask(uint64_t n) {
+    uint64_t k = 1;
+    while (k < 1024 && n / (2 * k) >= 3000000ull) k *= 2;
+    return uint32_t(k - 1);
 }
 
 void print_sample_trace() {

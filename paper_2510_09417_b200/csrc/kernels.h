@@ -15,6 +15,7 @@ void launch_bootstrap(const double* xs, const double* ys, uint64_t n, void* part
                       uint32_t* ticket, RootInfo* root, int grid, cudaStream_t st);
 size_t partial_bytes(int grid);
 void print_sample_trace();
+uint32_t sample_mask(uint64_t n);
 void fin_trace(bool on);
 void print_fin_trace();
 void upload_root_consts(const RootInfo* d_root, cudaStream_t st);

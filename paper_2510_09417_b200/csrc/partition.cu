@@ -1388,10 +1388,14 @@ __global__ void __launch_bounds__(kCtlThreads, 3) root_filtered_tma(RootArgs a) 
                 int c = 2;
                 if (valid) {
                     bad |= nonfinite_bits(w);
-                    bool drop = filter;
+                    const double du = fabs(u - P.ocx), dw = fabs(w - P.ocy);
+                    bool drop = filter && du < P.ohx && dw < P.ohy && du + dw < P.od;  // inner octagon
+                    if (filter && !drop) {
+                        drop = true;
 #pragma unroll
-                    for (int q = 0; q < 8; ++q)  // inside by the margin w.r.t. all 8 chords
-                        drop &= __fma_rn(P.fa[q], u, __fma_rn(P.fb[q], w, P.fc[q])) < P.ft[q];
+                        for (int q = 0; q < kPolyV; ++q)  // inside by the margin w.r.t. every chord
+                            drop &= __fma_rn(P.fa[q], u, __fma_rn(P.fb[q], w, P.fc[q])) < P.ft[q];
+                    }
                     if (!drop) {
                         const double A = dsub(px, u), B = dsub(py, w);
                         const double Cc = dsub(qx, u), D = dsub(qy, w);
@@ -1622,11 +1626,29 @@ __global__ void __launch_bounds__(kCtlThreads, 3) root_filter_tma(FilterArgs a) 
                 qn += __popc(b);
             }
             __syncwarp();
-            // phase C: the chord test for the rest, densely, 32 at a time
-            uint32_t sn = 0;
+            // phase B: the inner octagon for the points outside the box,
+            // densely (32 at a time); the rest is queued again in place
+            uint32_t qn2 = qn;
+            if (P.oct_on) {  // (uniform: skipped when the octagon adds nothing to the box)
+            qn2 = 0;
             for (uint32_t r0 = 0; r0 < qn; r0 += 32) {
                 const uint32_t j = r0 + lane;
                 const bool valid = j < qn;
+                const uint32_t idx = valid ? s_q[warp][j] : 0u;
+                const double du = fabs(ring.x[s][idx] - P.ocx), dw = fabs(ring.y[s][idx] - P.ocy);
+                const bool need = valid & !(filter & (du < P.ohx) & (dw < P.ohy) & (du + dw < P.od));
+                const unsigned b = __ballot_sync(kFull, need);
+                __syncwarp();  // every lane has read its entry before any is overwritten
+                if (need) s_q[warp][qn2 + __popc(b & lt)] = uint16_t(idx);
+                qn2 += __popc(b);
+            }
+            __syncwarp();
+            }
+            // phase C: the chord test for the rest, densely, 32 at a time
+            uint32_t sn = 0;
+            for (uint32_t r0 = 0; r0 < qn2; r0 += 32) {
+                const uint32_t j = r0 + lane;
+                const bool valid = j < qn2;
                 const uint32_t idx = valid ? s_q[warp][j] : 0u;
                 const double u = ring.x[s][idx], w = ring.y[s][idx];
                 bool keep = false;
@@ -1634,7 +1656,7 @@ __global__ void __launch_bounds__(kCtlThreads, 3) root_filter_tma(FilterArgs a) 
                     bad |= uint32_t(nonfinite_bits(u) | nonfinite_bits(w));
                     bool drop = filter;
 #pragma unroll
-                    for (int q = 0; q < 8; ++q)  // inside by the margin w.r.t. all 8 chords
+                    for (int q = 0; q < kPolyV; ++q)  // inside by the margin w.r.t. every chord
                         drop &= __fma_rn(P.fa[q], u, __fma_rn(P.fb[q], w, P.fc[q])) < P.ft[q];
                     keep = !drop;
                 }

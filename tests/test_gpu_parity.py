@@ -352,15 +352,16 @@ def test_split_root_far_outlier_rerun(vq, cuda, oracle):
     """A survivor far beyond the sampled octagon's scale voids the margin
     argument: the call is rerun unfiltered, with the same (reference) result."""
     for far in (1e10, -3e9, 5e12):
-        xs, ys = vq.generate("disk", 200_000, 11)
-        # indices 5000 and 20000 lie in unsampled groups (the sample takes
-        # every 16th run of 1024 points), so the octagon cannot see them
-        xs[5000], ys[5000] = far, 0.25
-        xs[20000], ys[20000] = 0.5, far / 3
+        xs, ys = vq.generate("disk", 7_000_000, 11)
+        # runs 5 and 19 of 1024 points are never sampled (at n = 7e6 the
+        # sample takes every 2nd run; never an odd one), so the polygon
+        # cannot see these two points
+        xs[5 * 1024 + 17], ys[5 * 1024 + 17] = far, 0.25
+        xs[19 * 1024 + 100], ys[19 * 1024 + 100] = 0.5, far / 3
         got = gpu_indices(vq, xs, ys)
         assert vq.stats()["root_reruns"] == 1
         assert np.array_equal(got, oracle.hull_indices(xs, ys))
-    xs, ys = vq.generate("disk", 200_000, 11)
+    xs, ys = vq.generate("disk", 7_000_000, 11)
     gpu_indices(vq, xs, ys)
     assert vq.stats()["root_reruns"] == 0
 
