@@ -141,6 +141,11 @@ int vqhull_cuda_set_root_reference(int reference);
  * Returns 1 for another mode.  VQHULL_ROOT=octagon|reference sets 1|2. */
 int vqhull_cuda_set_root_mode(int mode);
 
+/* Frees this thread's device engine buffers (points, level tables) and
+ * trims the memory pool; the next call re-allocates.  For callers that need
+ * the device memory back between hulls. */
+int vqhull_cuda_trim(void);
+
 /* Human-readable description of the last CUDA error (thread-local). */
 const char* vqhull_cuda_last_error(void);
 

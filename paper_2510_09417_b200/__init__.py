@@ -99,6 +99,7 @@ def lib() -> C.CDLL:
         L.vqhull_cuda_set_stable.argtypes = [C.c_int]
         L.vqhull_cuda_set_root_reference.argtypes = [C.c_int]
         L.vqhull_cuda_set_root_mode.argtypes = [C.c_int]
+        L.vqhull_cuda_trim.argtypes = []
         L.vqhull_cuda_last_error.restype = C.c_char_p
         L.vqhull_b200_version.restype = C.c_char_p
         L.vqhull_generate.argtypes = [C.c_int, C.c_uint64, C.c_uint64, C.c_uint64, C.c_void_p,
@@ -254,6 +255,11 @@ def set_root_reference(on: bool) -> None:
     """Root stage without the octagon filter: find_extremes, bootstrap arg-max
     and the fused levels-1+2 pass.  Same hull either way."""
     _check(lib().vqhull_cuda_set_root_reference(int(bool(on))), "vqhull_cuda_set_root_reference")
+
+
+def trim() -> None:
+    """Release the engine's device buffers (they are re-allocated on demand)."""
+    _check(lib().vqhull_cuda_trim(), "vqhull_cuda_trim")
 
 
 ROOT_MODES = {"split": 0, "octagon": 1, "reference": 2}

@@ -79,6 +79,7 @@ struct DevBuf {
     }
     void release() {
         if (p) cudaFree(p);
+        if (p) g_alloc_gen.fetch_add(1);
         p = nullptr;
         cap = 0;
     }
@@ -499,6 +500,30 @@ class Engine {
     }
 
     DevBuf& out_buf() { return out_; }
+
+    // frees the big per-call buffers (points, level tables, staging) and
+    // returns the pool's cached memory to the device; the next call
+    // re-allocates what it needs
+    void trim() {
+        ck(cudaDeviceSynchronize(), "trim sync");
+        for (PointBuf* b : {&bufs_[0], &bufs_[1], &in_}) {
+            b->x.release();
+            b->y.release();
+            b->id.release();
+        }
+        for (LevelTables& T : levels_)
+            for (DevBuf* d : {&T.slots, &T.kind, &T.link, &T.size, &T.start, &T.segs, &T.fins, &T.fin_count})
+                d->release();
+        for (DevBuf* d : {&tile_seg_, &chain_, &out_, &part_, &status_, &flags_, &aggs_, &incs_})
+            d->release();
+        if (graph_exec_) {
+            cudaGraphExecDestroy(graph_exec_);
+            graph_exec_ = nullptr;
+        }
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev_) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
+        ck(cudaDeviceSynchronize(), "trim sync");
+    }
 
    private:
     // Default: K1' (8 exact directional extremes + finiteness) then KB'
@@ -1112,6 +1137,17 @@ int vqhull_cuda_set_stable(int stable) {
         Engine& e = vqb::engine();
         std::lock_guard<std::mutex> lk(e.mutex());
         e.set_stable(stable != 0);
+        return 0;
+    } catch (const CudaError&) {
+        return VQHULL_ECUDA;
+    }
+}
+
+int vqhull_cuda_trim(void) {
+    try {
+        Engine& e = vqb::engine();
+        std::lock_guard<std::mutex> lk(e.mutex());
+        e.trim();
         return 0;
     } catch (const CudaError&) {
         return VQHULL_ECUDA;

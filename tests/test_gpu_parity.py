@@ -205,6 +205,8 @@ def test_config5_disk_4e9_one_gpu(vq, cuda, oracle):
     import torch
 
     n = cfg["n"]
+    vq.trim()  # earlier tests' engine buffers back to the device
+    torch.cuda.empty_cache()
     free, _ = torch.cuda.mem_get_info()
     if free < 150 * 2**30:
         pytest.skip("needs ~150 GB of device memory")
