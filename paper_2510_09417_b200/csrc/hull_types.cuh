@@ -48,6 +48,9 @@ struct RootPoly {
     // P - V_j) (> 0: left of the chord, outside); P is dropped when
     // f_j(P) < ft_j for all chords (ft_j = -margin * |chord|_1)
     double fa[kPolyV], fb[kPolyV], fc[kPolyV], ft[kPolyV];
+    // the pass kernels' form of the test: fma(fa, x, fb * y) < fg = ft - fc
+    // (two constant operands per chord, error <= ~6 eps |e| M << margin)
+    double fg[kPolyV];
     double bx0, bx1, by0, by1;  // open box verified to lie inside the filter region
     // octagon |x - ocx| < ohx, |y - ocy| < ohy, |x - ocx| + |y - ocy| < od,
     // verified (its 8 vertices) to lie inside the filter region

@@ -507,6 +507,7 @@ __device__ __noinline__ void poly_finish_warp(const PolyPartial& F, const double
     if (lane < kPolyV) {
         P.vx[j] = vxj; P.vy[j] = vyj; P.vidx[j] = aj;
         P.fa[j] = fa; P.fb[j] = fb; P.fc[j] = fc; P.ft[j] = ft;
+        P.fg[j] = ft - fc;
     }
     if (lane != 0) return;
     P.mref = M;

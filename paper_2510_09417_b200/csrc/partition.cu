@@ -1394,7 +1394,7 @@ __global__ void __launch_bounds__(kCtlThreads, 3) root_filtered_tma(RootArgs a) 
                         drop = true;
 #pragma unroll
                         for (int q = 0; q < kPolyV; ++q)  // inside by the margin w.r.t. every chord
-                            drop &= __fma_rn(P.fa[q], u, __fma_rn(P.fb[q], w, P.fc[q])) < P.ft[q];
+                            drop &= __fma_rn(P.fa[q], u, __dmul_rn(P.fb[q], w)) < P.fg[q];
                     }
                     if (!drop) {
                         const double A = dsub(px, u), B = dsub(py, w);
@@ -1578,6 +1578,7 @@ __global__ void __launch_bounds__(kCtlThreads, 3) root_filter_tma(FilterArgs a) 
         }
     } else {
         // ---- compute warps: every warp owns 128 points of a tile (4 per lane)
+        const bool oct = P.filter != 0 && P.oct_on != 0;
         const bool filter = P.filter != 0;
         const double bx0 = filter ? P.bx0 : kInf, bx1 = filter ? P.bx1 : -kInf;
         const double by0 = filter ? P.by0 : kInf, by1 = filter ? P.by1 : -kInf;
@@ -1614,36 +1615,35 @@ __global__ void __launch_bounds__(kCtlThreads, 3) root_filter_tma(FilterArgs a) 
                 }
                 __syncwarp();
             }
-            // phase A: strictly inside the inner box -> dropped at once
+            // phase A: strictly inside the inner box, or (when it adds
+            // coverage, a uniform choice) inside the inner octagon -> dropped
             uint32_t qn = 0;
+            if (oct) {
 #pragma unroll
-            for (int i = 0; i < kItems; ++i) {
-                const uint32_t idx = uint32_t(i) * kThreads + tid;
-                const double u = ring.x[s][idx], w = ring.y[s][idx];
-                const bool need = (tbase + idx < n) & !((u > bx0) & (u < bx1) & (w > by0) & (w < by1));
-                const unsigned b = __ballot_sync(kFull, need);
-                if (need) s_q[warp][qn + __popc(b & lt)] = uint16_t(idx);
-                qn += __popc(b);
+                for (int i = 0; i < kItems; ++i) {
+                    const uint32_t idx = uint32_t(i) * kThreads + tid;
+                    const double u = ring.x[s][idx], w = ring.y[s][idx];
+                    const double du = fabs(u - P.ocx), dw = fabs(w - P.ocy);
+                    const bool in = ((u > bx0) & (u < bx1) & (w > by0) & (w < by1)) |
+                                    ((du < P.ohx) & (dw < P.ohy) & (du + dw < P.od));
+                    const bool need = (tbase + idx < n) & !in;
+                    const unsigned b = __ballot_sync(kFull, need);
+                    if (need) s_q[warp][qn + __popc(b & lt)] = uint16_t(idx);
+                    qn += __popc(b);
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < kItems; ++i) {
+                    const uint32_t idx = uint32_t(i) * kThreads + tid;
+                    const double u = ring.x[s][idx], w = ring.y[s][idx];
+                    const bool need = (tbase + idx < n) & !((u > bx0) & (u < bx1) & (w > by0) & (w < by1));
+                    const unsigned b = __ballot_sync(kFull, need);
+                    if (need) s_q[warp][qn + __popc(b & lt)] = uint16_t(idx);
+                    qn += __popc(b);
+                }
             }
             __syncwarp();
-            // phase B: the inner octagon for the points outside the box,
-            // densely (32 at a time); the rest is queued again in place
-            uint32_t qn2 = qn;
-            if (P.oct_on) {  // (uniform: skipped when the octagon adds nothing to the box)
-            qn2 = 0;
-            for (uint32_t r0 = 0; r0 < qn; r0 += 32) {
-                const uint32_t j = r0 + lane;
-                const bool valid = j < qn;
-                const uint32_t idx = valid ? s_q[warp][j] : 0u;
-                const double du = fabs(ring.x[s][idx] - P.ocx), dw = fabs(ring.y[s][idx] - P.ocy);
-                const bool need = valid & !(filter & (du < P.ohx) & (dw < P.ohy) & (du + dw < P.od));
-                const unsigned b = __ballot_sync(kFull, need);
-                __syncwarp();  // every lane has read its entry before any is overwritten
-                if (need) s_q[warp][qn2 + __popc(b & lt)] = uint16_t(idx);
-                qn2 += __popc(b);
-            }
-            __syncwarp();
-            }
+            const uint32_t qn2 = qn;
             // phase C: the chord test for the rest, densely, 32 at a time
             uint32_t sn = 0;
             for (uint32_t r0 = 0; r0 < qn2; r0 += 32) {
@@ -1657,7 +1657,7 @@ __global__ void __launch_bounds__(kCtlThreads, 3) root_filter_tma(FilterArgs a) 
                     bool drop = filter;
 #pragma unroll
                     for (int q = 0; q < kPolyV; ++q)  // inside by the margin w.r.t. every chord
-                        drop &= __fma_rn(P.fa[q], u, __fma_rn(P.fb[q], w, P.fc[q])) < P.ft[q];
+                        drop &= __fma_rn(P.fa[q], u, __dmul_rn(P.fb[q], w)) < P.fg[q];
                     keep = !drop;
                 }
                 const unsigned b = __ballot_sync(kFull, keep);
