@@ -1593,10 +1593,14 @@ void print_fin_trace() {
 }
 
 // one run of 1024 points in (mask + 1) is sampled: the largest power of two
-// that still leaves >= 3M sample points (1/32 at n = 1e8, 1/256 at 1e9)
+// that still leaves >= kSampleMin sample points
+#ifndef VQB_SAMPLE_MIN
+#define VQB_SAMPLE_MIN 1500000ull
+#endif
+constexpr uint64_t kSampleMin = VQB_SAMPLE_MIN;
 uint32_t sample_mask(uint64_t n) {
     uint64_t k = 1;
-    while (k < 1024 && n / (2 * k) >= 3000000ull) k *= 2;
+    while (k < 1024 && n / (2 * k) >= kSampleMin) k *= 2;
     return uint32_t(k - 1);
 }
 
