@@ -300,6 +300,23 @@ class Engine {
                 return VQHULL_EINVAL;
             }
             if (first == 2 && split && h_root_->unsafe) return rerun_unfiltered(dx, dy, n, d_out, h, st);
+            if (h_info_->nseg != 0 && tail && 2u * h_info_->nseg <= kTailSlots &&
+                h_info_->out_total <= uint64_t(kTailTilesPerCta) * sms_ * occ_tail_ * kTile / 2) {
+                // the recursion narrowed again: the rest in one persistent launch
+                uint32_t S2 = 2u * h_info_->nseg;
+                int lvl2 = lvl, in2 = in;
+                hinfo_.resize(std::max<size_t>(hinfo_.size(), size_t(lvl + kTailLevels)));
+                const int rc = run_tail(dx, dy, n, S2, d_out, st, &lvl2, &in2, &S2);
+                if (rc) {
+                    g_last_error = "tail kernel after host levels failed (internal error)";
+                    throw CudaError{cudaErrorUnknown};
+                }
+                if (lmax_ >= 0) break;
+                lvl = lvl2;
+                in = in2;
+                S = S2;
+                continue;
+            }
             if (h_info_->nseg == 0) {
                 // the recursion ended in this batch: fetch all level infos
                 hinfo_.resize(lvl);
@@ -562,14 +579,14 @@ class Engine {
     // non-finite input, -1 for an `unsafe` split root (caller reruns).
     int run_tail(const double* dx, const double* dy, uint64_t n, uint32_t nslots, uint32_t* d_out,
                  cudaStream_t st, int* lvl, int* in, uint32_t* S) {
-        const TailArgs ta = tail_args(dx, dy, n, nslots, d_out, *lvl, st);
+        const TailArgs ta = tail_args(dx, dy, n, nslots, d_out, *lvl, st, *in);
         launch_tail_report(ta, st);
         return finish_tail(ta, st, lvl, in, S);
     }
 
     // KT's arguments (and every table it writes, allocated here)
     TailArgs tail_args(const double* dx, const double* dy, uint64_t n, uint32_t nslots, uint32_t* d_out, int l0,
-                       cudaStream_t st) {
+                       cudaStream_t st, int in0 = 0) {
         const int nlev = kTailLevels;
         for (int li = 0; li < nlev; ++li) {
             LevelTables& T = level(l0 + li);
@@ -608,6 +625,8 @@ class Engine {
         ta.nlev = nlev;
         ta.nslots0 = nslots;
         ta.max_slots = kTailSlots;
+        ta.max_tiles = uint32_t(kTailTilesPerCta * sms_ * occ_tail_);
+        ta.in0 = in0;
         for (int b = 0; b < 2; ++b) {
             ta.bx[b] = bufs_[b].x.as<double>();
             ta.by[b] = bufs_[b].y.as<double>();
@@ -629,7 +648,7 @@ class Engine {
         ta.part_cap = part_.cap / sizeof(Best);
         ta.chain = chain_.as<uint32_t>();
         ta.state = &ctrs_[16];
-        ta.out = d_out;
+        ta.out = l0 == 2 ? d_out : nullptr;  // (in-kernel emission needs the whole tree)
         ta.h_out = hword_;
         ta.p_idx = &root_->p_idx;
         ta.root = root_;
@@ -683,6 +702,11 @@ class Engine {
         for (int l = l0; l < int(at) && l < l0 + nlev; ++l) hinfo_[l] = li[l - l0];
         if (how == 1 || how == 3) {
             hinfo_[at] = li[at - l0];
+            if (l0 > 2) {  // the host-driven levels before this launch
+                ck(cudaMemcpyAsync(hinfo_.data() + 2, info_.as<LevelInfo>() + 2, sizeof(LevelInfo) * (l0 - 2),
+                                   cudaMemcpyDeviceToHost, st), "d2h infos");
+                ck(cudaStreamSynchronize(st), "info sync");
+            }
             lmax_ = int(at);
             tail_emitted_ = how == 3;
             VQB_TRACE("hull: tail finished at level %u", at);
@@ -979,6 +1003,7 @@ class Engine {
     bool use_tail_ = !(getenv("VQHULL_TAIL") && getenv("VQHULL_TAIL")[0] == '0');
     uint32_t* h_tail_ = nullptr;
     bool tail_emitted_ = false;
+    static constexpr uint32_t kTailTilesPerCta = 2;  // KT takes levels of at most this many tiles per CTA
     // captured split-root + KT graph (VQHULL_GRAPH=0 disables)
     bool use_graph_ = !(getenv("VQHULL_GRAPH") && getenv("VQHULL_GRAPH")[0] == '0');
     bool graph_run_ = false;

@@ -216,6 +216,8 @@ struct TailArgs {
     int l0, nlev;
     uint32_t nslots0;
     uint32_t max_slots;       // table capacity; a level with more slots is left to the host
+    uint32_t max_tiles;       // a level with more tiles is left to the host's TMA-ring kernel
+    int in0;                  // buffer read by level l0
     double* bx[2];
     double* by[2];
     uint32_t* bid[2];

@@ -288,7 +288,7 @@ __global__ void __launch_bounds__(kThreads, 2) tail_kernel(const __grid_constant
         A.state[1] = 0u;
         if (A.trace) A.trace[0] = global_ns();
     }
-    int in = 0;  // level l0 reads buffer 0 (the root's output)
+    int in = A.in0;  // the buffer level l0 reads
     for (int li = 0;; ++li) {
         const int l = A.l0 + li;
         const TailLevel& T = A.lv[li];
@@ -308,7 +308,15 @@ __global__ void __launch_bounds__(kThreads, 2) tail_kernel(const __grid_constant
                 }
             }
             __syncthreads();
-            if (!s_flag) tail_plan(A, T, prev ? 2u * prev->nseg : A.nslots0, prev, info, li);
+            if (!s_flag) {
+                tail_plan(A, T, prev ? 2u * prev->nseg : A.nslots0, prev, info, li);
+                // a level with many points runs better through the host-driven
+                // TMA-ring kernel: hand it over (the host re-plans it)
+                if (threadIdx.x == 0 && info->ntiles > A.max_tiles) {
+                    A.state[0] = uint32_t(l);
+                    A.state[1] = 2u;
+                }
+            }
         }
         KT_TRACE(li, 1);
         grid.sync();
