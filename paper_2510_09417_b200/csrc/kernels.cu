@@ -1117,6 +1117,7 @@ __device__ uint32_t g_ftrace_on;
 
 constexpr int kFcThreads = 256;
 constexpr int kFcNodes = int(kFinMax / 2);  // nodes of one depth hold >= 2 points each
+constexpr int kFcItems = int(kFinMax) / kFcThreads;  // points per thread
 constexpr uint16_t kDead = 0xffffu;
 constexpr uint16_t kLinkEmpty = 0, kLinkLeaf = 0x4000, kLinkNode = 0x8000;  // kind | value
 
@@ -1201,14 +1202,19 @@ __device__ __forceinline__ void finisher_cta_body(FinCtaSmem& S, const FinRec* f
             // children, so the slot claims are warp-aggregated (one shared
             // atomic per child per warp) and a key only attempts the min
             // when it beats the value already there.
-            for (uint32_t i0 = tid - lane; i0 < m; i0 += kFcThreads) {  // warp-uniform trip count
-                const uint32_t i = i0 + lane;
+            // all of a thread's points first (independent f64 chains overlap),
+            // then the warp-aggregated claims
+            uint32_t chv[kFcItems];
+            uint16_t lidv[kFcItems];
+#pragma unroll
+            for (int k = 0; k < kFcItems; ++k) {
+                const uint32_t i = uint32_t(k) * kFcThreads + tid;
                 const uint16_t c = i < m ? S.wnode[cur][i] : kDead;
-                uint32_t ch = 0xffffffffu;
-                uint16_t lid = 0;
-                int s = 0;
+                chv[k] = 0xffffffffu;
+                lidv[k] = 0;
                 if (c != kDead) {
-                    lid = S.work[cur][i];
+                    const uint16_t lid = S.work[cur][i];
+                    lidv[k] = lid;
                     const uint16_t p = S.np[cur][c], r = S.nr[cur][c], q = S.nq[cur][c];
                     const double u = S.x[lid], w = S.y[lid];
                     const double A = dsub(S.x[p], u), B = dsub(S.y[p], w);
@@ -1217,12 +1223,17 @@ __device__ __forceinline__ void finisher_cta_body(FinCtaSmem& S, const FinRec* f
                     const bool la = left_diff(A, B, E, F);
                     const bool lb = !la && left_diff(E, F, Cc, D);
                     if (la || lb) {
-                        s = la ? 0 : 1;
-                        ch = 2u * c + s;
-                        const unsigned long long k = fc_key(S, cur, c, s, lid);
-                        if (k < S.ckey[ch]) atomicMin(&S.ckey[ch], k);
+                        const int sd = la ? 0 : 1;
+                        const uint32_t ch = 2u * c + sd;
+                        chv[k] = ch;
+                        const unsigned long long key = fc_key(S, cur, c, sd, lid);
+                        if (key < S.ckey[ch]) atomicMin(&S.ckey[ch], key);
                     }
                 }
+            }
+#pragma unroll
+            for (int k = 0; k < kFcItems; ++k) {
+                const uint32_t ch = chv[k];
                 const unsigned grp = __match_any_sync(kFull, ch);
                 const int leader = __ffs(grp) - 1;
                 uint32_t base = 0;
@@ -1231,16 +1242,18 @@ __device__ __forceinline__ void finisher_cta_body(FinCtaSmem& S, const FinRec* f
                 if (ch != 0xffffffffu) {
                     const uint32_t pos = base + __popc(grp & lanemask_lt());
                     const uint32_t cc = ch >> 1;
-                    const uint32_t dest = s ? uint32_t(S.nhi[cur][cc]) - 1u - pos : uint32_t(S.nlo[cur][cc]) + pos;
-                    S.work[nxt][dest] = lid;
+                    const uint32_t dest = (ch & 1u) ? uint32_t(S.nhi[cur][cc]) - 1u - pos : uint32_t(S.nlo[cur][cc]) + pos;
+                    S.work[nxt][dest] = lidv[k];
                     S.wnode[nxt][dest] = uint16_t(ch);
                 }
             }
             __syncthreads();
             if (ftr && depth == 0) g_ftrace[40] = gtimer_ns();
             // (2) candidates: points holding their child's minimal key
-            for (uint32_t i = tid; i < m; i += kFcThreads) {
-                const uint16_t ch = S.wnode[nxt][i];
+#pragma unroll
+            for (int k = 0; k < kFcItems; ++k) {
+                const uint32_t i = uint32_t(k) * kFcThreads + tid;
+                const uint16_t ch = i < m ? S.wnode[nxt][i] : kDead;
                 if (ch == kDead) continue;
                 const uint16_t lid = S.work[nxt][i];
                 if (fc_key(S, cur, ch >> 1, ch & 1, lid) == S.ckey[ch]) {
