@@ -111,7 +111,9 @@ typedef struct vqhull_stats {
     uint32_t root_filter_on;    /* the octagon filter could drop points (coordinate
                                    magnitudes in range) */
     uint32_t root_reruns;       /* 1: a split-root survivor lay beyond 2^12 x the
-                                   octagon's scale, the call was rerun unfiltered */
+                                   polygon's scale, the call was rerun unfiltered */
+    uint32_t tail_launches;     /* launches of the persistent recursion kernel */
+    uint32_t tail_levels;       /* levels it processed */
 } vqhull_stats;
 
 int vqhull_cuda_get_stats(vqhull_stats* out);

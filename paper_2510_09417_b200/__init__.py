@@ -68,6 +68,8 @@ class Stats(C.Structure):
         ("root_filtered", C.c_uint32),
         ("root_filter_on", C.c_uint32),
         ("root_reruns", C.c_uint32),
+        ("tail_launches", C.c_uint32),
+        ("tail_levels", C.c_uint32),
     ]
 
     def as_dict(self) -> dict:

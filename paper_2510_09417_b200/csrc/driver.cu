@@ -175,7 +175,7 @@ class Engine {
         const bool split = filtered && !root_octagon_;
         // the common small-recursion case (split root + KT) replays one
         // captured CUDA graph: sample, filter, KT and the report copy
-        graph_run_ = split && n <= kLeanN && use_tail_ && use_graph_ && !timing_ && !tail_trace_ && !sample_trace_ && !sync_each_ &&
+        graph_run_ = split && n <= kLeanN && use_tail_ && use_graph_ && !timing_ && !tail_trace_ && !sync_each_ &&
                      run_graph(dx, dy, n, d_out, st);
         uint32_t nslots = graph_run_ ? 1u
                         : split ? run_root_split(dx, dy, n, st)
@@ -212,7 +212,9 @@ class Engine {
             if (rc == VQHULL_EINVAL) return rc;
             if (rc < 0) return rerun_unfiltered(dx, dy, n, d_out, h, st);
         }
-        const int batch = lean ? 1 : kLevelBatch;
+        // (VQHULL_LEVEL_BATCH overrides the batch: tests of the re-entry path)
+        const int batch = lean ? 1 : (getenv("VQHULL_LEVEL_BATCH") ? std::max(1, atoi(getenv("VQHULL_LEVEL_BATCH")))
+                                                                   : kLevelBatch);
         while (lmax_ < 0) {
             const int first = lvl;
             for (int b = 0; b < batch; ++b, ++lvl) {
@@ -300,23 +302,8 @@ class Engine {
                 return VQHULL_EINVAL;
             }
             if (first == 2 && split && h_root_->unsafe) return rerun_unfiltered(dx, dy, n, d_out, h, st);
-            if (h_info_->nseg != 0 && tail && 2u * h_info_->nseg <= kTailSlots &&
-                h_info_->out_total <= uint64_t(kTailTilesPerCta) * sms_ * occ_tail_ * kTile / 2) {
-                // the recursion narrowed again: the rest in one persistent launch
-                uint32_t S2 = 2u * h_info_->nseg;
-                int lvl2 = lvl, in2 = in;
-                hinfo_.resize(std::max<size_t>(hinfo_.size(), size_t(lvl + kTailLevels)));
-                const int rc = run_tail(dx, dy, n, S2, d_out, st, &lvl2, &in2, &S2);
-                if (rc) {
-                    g_last_error = "tail kernel after host levels failed (internal error)";
-                    throw CudaError{cudaErrorUnknown};
-                }
-                if (lmax_ >= 0) break;
-                lvl = lvl2;
-                in = in2;
-                S = S2;
-                continue;
-            }
+            VQB_TRACE("hull: after level %d: nslots %u nseg %u out_total %u fin_total %u", lvl - 1, h_info_->nslots,
+                      h_info_->nseg, h_info_->out_total, h_info_->fin_total);
             if (h_info_->nseg == 0) {
                 // the recursion ended in this batch: fetch all level infos
                 hinfo_.resize(lvl);
@@ -407,6 +394,8 @@ class Engine {
             throw CudaError{cudaErrorUnknown};
         }
         *h = *h_word_;
+        if (sample_trace_) print_sample_trace();
+        if (fin_trace_) print_fin_trace();
         stats_.hull_size = *h;
         stats_.launches = launches_;
         stats_.bytes_moved = stats_.bytes_extremes + stats_.bytes_bootstrap + stats_.bytes_root_partition +
@@ -625,7 +614,7 @@ class Engine {
         ta.nlev = nlev;
         ta.nslots0 = nslots;
         ta.max_slots = kTailSlots;
-        ta.max_tiles = uint32_t(kTailTilesPerCta * sms_ * occ_tail_);
+        ta.max_tiles = tail_max_tiles();
         ta.in0 = in0;
         for (int b = 0; b < 2; ++b) {
             ta.bx[b] = bufs_[b].x.as<double>();
@@ -690,6 +679,8 @@ class Engine {
         VQB_TRACE("hull: tail sync");
         ck(cudaStreamSynchronize(st), "tail sync");
         const uint32_t at = h_tail_[0], how = h_tail_[1];
+        stats_.tail_launches += 1;
+        stats_.tail_levels += (how == 2 ? at : at + 1) - uint32_t(l0);
         *h_word_ = h_tail_[2];
         h_root_->nonfinite = h_tail_[3];
         h_root_->unsafe = h_tail_[4];
@@ -806,7 +797,6 @@ class Engine {
             const int g = std::max(1, std::min<int>(grid_poly_, int(n / ((uint64_t(sample_mask(n)) + 1) * 256 * 8)) + 1));
             tk(0, st, [&] { launch_poly_sample(dx, dy, n, partials_.p, &ctrs_[5], sample_keys(), root_, side_ctr(), g, false, st); });
         }
-        if (sample_trace_) print_sample_trace();
         upload_root_consts(root_, st);  // the filter's geometry -> constant bank (FP64 operands)
         stats_.bytes_extremes = 16 * n / (sample_mask(n) + 1);  // x and y of the sample
         stats_.bytes_bootstrap = 0;
@@ -1004,11 +994,17 @@ class Engine {
     uint32_t* h_tail_ = nullptr;
     bool tail_emitted_ = false;
     static constexpr uint32_t kTailTilesPerCta = 2;  // KT takes levels of at most this many tiles per CTA
+    // (VQHULL_TAIL_MAXTILES overrides the tile bound: tests of the hand-over paths)
+    uint32_t tail_max_tiles() const {
+        const char* e = getenv("VQHULL_TAIL_MAXTILES");
+        return e ? uint32_t(atoi(e)) : uint32_t(kTailTilesPerCta * sms_ * occ_tail_);
+    }
     // captured split-root + KT graph (VQHULL_GRAPH=0 disables)
     bool use_graph_ = !(getenv("VQHULL_GRAPH") && getenv("VQHULL_GRAPH")[0] == '0');
     bool graph_run_ = false;
     cudaStream_t own_st_ = nullptr;
     bool sample_trace_ = getenv("VQHULL_SAMPLE_TRACE") != nullptr;
+    bool fin_trace_ = getenv("VQHULL_FIN_TRACE") != nullptr && (fin_trace(true), true);
     cudaGraphExec_t graph_exec_ = nullptr;
     const double* graph_dx_ = nullptr;
     const double* graph_dy_ = nullptr;

@@ -1621,9 +1621,11 @@ void print_sample_trace() {
     unsigned long long t[8];
     cudaDeviceSynchronize();
     cudaMemcpyFromSymbol(t, g_strace, sizeof t);
-    fprintf(stderr, "[sample] stream end %.2f  fold %.2f  reduce %.2f  finish %.2f us\n", (t[1] - t[0]) * 1e-3,
-            (t[2] - t[0]) * 1e-3, (t[3] - t[0]) * 1e-3, (t[4] - t[0]) * 1e-3);
-    const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    fprintf(stderr, "[sample] stream end %.2f  fold %.2f  reduce %.2f  finish %.2f | filter start %.2f end %.2f | tail start %.2f us\n",
+            (t[1] - t[0]) * 1e-3, (t[2] - t[0]) * 1e-3, (t[3] - t[0]) * 1e-3, (t[4] - t[0]) * 1e-3,
+            (double(t[5]) - double(t[0])) * 1e-3, (double(t[6]) - double(t[0])) * 1e-3,
+            (double(t[7]) - double(t[0])) * 1e-3);
+    const unsigned long long z[8] = {0, 0, 0, 0, 0, ~0ull, 0, 0};
     cudaMemcpyToSymbol(g_strace, z, sizeof z);
 }
 

@@ -1517,6 +1517,7 @@ __device__ __forceinline__ void filter_warp_fold(ExtKey& lo, ExtKey& hi, double&
 
 __global__ void __launch_bounds__(kCtlThreads, 3) root_filter_tma(FilterArgs a) {
     VQB_PDL();
+    if (threadIdx.x == 0) atomicMin(&g_strace[5], gtimer_ns());
     extern __shared__ __align__(128) unsigned char dsm[];
     RootRing4& ring = *reinterpret_cast<RootRing4*>(dsm);
     __shared__ uint32_t s_cnt[2][kWarps];                      // survivors per warp and tile
@@ -1748,6 +1749,7 @@ __global__ void __launch_bounds__(kCtlThreads, 3) root_filter_tma(FilterArgs a) 
     a.slot[0] = ch;
     *a.ctr = 0;  // re-arm for the next call
     *a.ticket = 0;
+    g_strace[6] = gtimer_ns();
 }
 
 // ===========================================================================

@@ -350,6 +350,29 @@ def test_root_mode_selection(vq, cuda):
         vq.set_stable(False)
 
 
+def test_tail_kernel_paths(vq, cuda, oracle, monkeypatch):
+    """The persistent recursion kernel: the whole recursion in one launch
+    (small survivor sets); a level wider than its tile bound handed to the
+    host-driven kernels, which finish the recursion (forced here with small
+    bounds), including circle-like inputs."""
+    xs, ys = vq.generate("square", 2_000_000, 2)
+    got = gpu_indices(vq, xs, ys)
+    s = vq.stats()
+    assert s["tail_launches"] == 1 and s["tail_levels"] == s["levels"] - 1
+    assert np.array_equal(got, oracle.hull_indices(xs, ys))
+    handed_over = 0
+    for bound in ("2", "8", "40"):
+        monkeypatch.setenv("VQHULL_TAIL_MAXTILES", bound)
+        for kind, n, seed in (("square", 8_000_000, 2), ("disk", 4_000_000, 5), ("circle", 400_000, 3)):
+            xs, ys = vq.generate(kind, n, seed)
+            got = gpu_indices(vq, xs, ys)
+            s = vq.stats()
+            handed_over += s["tail_levels"] < s["levels"] - 1
+            assert np.array_equal(got, oracle.hull_indices(xs, ys)), (bound, kind)
+    monkeypatch.delenv("VQHULL_TAIL_MAXTILES")
+    assert handed_over >= 3
+
+
 def test_split_root_far_outlier_rerun(vq, cuda, oracle):
     """A survivor far beyond the sampled octagon's scale voids the margin
     argument: the call is rerun unfiltered, with the same (reference) result."""
