@@ -34,28 +34,49 @@ def _default_local_hull(x: torch.Tensor, y: torch.Tensor) -> torch.Tensor:
     return hull_device(x, y)
 
 
+# candidates a rank sends in the one-collective fast path (local hulls are a
+# few dozen to a few thousand vertices; larger ones take a second round)
+GATHER_CAP = 8192
+
+
 def gather_candidates(cx: torch.Tensor, cy: torch.Tensor, cg: torch.Tensor,
-                      group: Optional[dist.ProcessGroup] = None):
+                      group: Optional[dist.ProcessGroup] = None, cap: Optional[int] = None):
     """All-gather variable-length (x, y, global index) candidate lists.
 
     Packs each candidate as three 64-bit words (the index bit-cast into f64
-    storage) so one collective moves everything; counts go first so the
-    payload can be padded to the largest shard.
+    storage) behind a header row holding the count, padded to `cap` rows, so
+    ONE collective moves counts and payload.  If any rank has more than `cap`
+    candidates (every rank sees that in the headers), a second all-gather
+    padded to the largest count follows.
     """
     dev = cx.device
-    k = torch.tensor([cx.numel()], dtype=torch.int64, device=dev)
+    k = cx.numel()
     world = dist.get_world_size(group)
-    counts = [torch.zeros_like(k) for _ in range(world)]
-    dist.all_gather(counts, k, group=group)
-    counts = [int(c.item()) for c in counts]
-    kmax = max(max(counts), 1)
-    pack = torch.zeros((kmax, 3), dtype=torch.float64, device=dev)
-    pack[: cx.numel(), 0] = cx
-    pack[: cx.numel(), 1] = cy
-    pack[: cx.numel(), 2] = cg.to(torch.int64).view(torch.float64)
-    bufs = [torch.empty_like(pack) for _ in range(world)]
-    dist.all_gather(bufs, pack, group=group)
-    parts = [b[:c] for b, c in zip(bufs, counts)]
+    cap = GATHER_CAP if cap is None else cap
+
+    def packed(rows: int, with_header: bool) -> torch.Tensor:
+        h = 1 if with_header else 0
+        pack = torch.zeros((rows + h, 3), dtype=torch.float64, device=dev)
+        if with_header:
+            pack[0, 0] = float(k)
+        m = min(k, rows)
+        pack[h:h + m, 0] = cx[:m]
+        pack[h:h + m, 1] = cy[:m]
+        pack[h:h + m, 2] = cg[:m].to(torch.int64).view(torch.float64)
+        return pack
+
+    first = packed(cap, True)
+    bufs = [torch.empty_like(first) for _ in range(world)]
+    dist.all_gather(bufs, first, group=group)
+    counts = [int(c) for c in torch.stack([b[0, 0] for b in bufs]).cpu().tolist()]
+    if max(counts) <= cap:
+        parts = [b[1:1 + c] for b, c in zip(bufs, counts)]
+    else:  # rare: a local hull larger than the fast path's capacity
+        kmax = max(counts)
+        full = packed(kmax, False)
+        bufs = [torch.empty_like(full) for _ in range(world)]
+        dist.all_gather(bufs, full, group=group)
+        parts = [b[:c] for b, c in zip(bufs, counts)]
     allp = torch.cat(parts, dim=0)
     gidx = allp[:, 2].contiguous().view(torch.int64)
     return allp[:, 0].contiguous(), allp[:, 1].contiguous(), gidx

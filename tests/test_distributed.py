@@ -26,12 +26,16 @@ def _oracle_local_hull(x: torch.Tensor, y: torch.Tensor) -> torch.Tensor:
     return torch.from_numpy(idx.astype(np.int64))
 
 
-def _worker(rank, world, port, kind, n, seed, dup, q):
+def _worker(rank, world, port, kind, n, seed, dup, q, cap=None):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
+        from paper_2510_09417_b200 import distributed as D
         from paper_2510_09417_b200 import generate
         from paper_2510_09417_b200.distributed import shard_range, sharded_hull
+
+        if cap is not None:  # force the two-round gather
+            D.GATHER_CAP = cap
 
         xs, ys = generate(kind, n, seed, threads=2)
         if dup:  # copies of points of shard 0 placed in the last shard
@@ -45,11 +49,11 @@ def _worker(rank, world, port, kind, n, seed, dup, q):
         dist.destroy_process_group()
 
 
-def run_world(world, kind, n, seed, dup=0):
+def run_world(world, kind, n, seed, dup=0, cap=None):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, kind, n, seed, dup, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, kind, n, seed, dup, q, cap)) for r in range(world)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=300) for _ in procs)
@@ -68,6 +72,18 @@ def test_sharded_hull_world2_equals_global(oracle, kind, n, seed, dup):
     xs, ys = generate(kind, n, seed, threads=2)
     if dup:
         xs[-dup:], ys[-dup:] = xs[:dup], ys[:dup]
+    ref = oracle.hull_indices(xs, ys).astype(np.int64)
+    for r in (0, 1):
+        assert np.array_equal(res[r], ref)
+
+
+def test_sharded_hull_two_round_gather(oracle):
+    """A local hull larger than the one-collective capacity (forced to 8
+    candidates) takes the second, count-padded all-gather."""
+    from paper_2510_09417_b200 import generate
+
+    res = run_world(2, "disk", 100_000, 3, cap=8)
+    xs, ys = generate("disk", 100_000, 3, threads=2)
     ref = oracle.hull_indices(xs, ys).astype(np.int64)
     for r in (0, 1):
         assert np.array_equal(res[r], ref)
