@@ -128,7 +128,7 @@ class Engine {
         occ_fin_ = std::max(1, occupancy_finisher());
         occ_filt_ = std::max(1, occupancy_filtered());
         occ_filter_ = std::max(1, occupancy_filter());
-        occ_tail_ = std::max(1, std::min(2, occupancy_tail()));
+        occ_tail_ = std::max(1, std::min(getenv("VQHULL_TAIL_OCC") ? atoi(getenv("VQHULL_TAIL_OCC")) : 1, occupancy_tail()));
         // one full wave each
         grid_ext_ = sms_ * std::max(1, std::min(8, occupancy_extremes()));
         grid_boot_ = sms_ * std::max(1, std::min(8, occupancy_bootstrap()));
