@@ -615,6 +615,8 @@ class Engine {
         ta.nslots0 = nslots;
         ta.max_slots = kTailSlots;
         ta.max_tiles = tail_max_tiles();
+        ta.fin_max = getenv("VQHULL_TAIL_FINMAX") ? std::min<uint32_t>(kTailFinMax, std::max(65, atoi(getenv("VQHULL_TAIL_FINMAX"))))
+                                                  : kTailFinMax;
         ta.in0 = in0;
         for (int b = 0; b < 2; ++b) {
             ta.bx[b] = bufs_[b].x.as<double>();

@@ -20,6 +20,7 @@ constexpr int kPartMinBlocks = 3;           // resident partition CTAs per SM (r
 constexpr int kFastMinBlocks = 4;           // fast-mode kernels (no staging)
 constexpr uint32_t kFinSmall = 64;          // segments of 2..64 points: warp finisher
 constexpr uint32_t kFinMax = 1024;          // 65..1024 points: CTA finisher; larger: tiled level kernel
+constexpr uint32_t kTailFinMax = 1024;      // inside the persistent tail kernel (2048 measured: faster on disk 1e6, slower on square 1e8 and disk 1e7)
 
 // Root stage geometry.  The recursion itself always follows the reference
 // (level 1 splits by p->q, hull.cpp:228-235); a polygon of kPolyV input
@@ -217,6 +218,7 @@ struct TailArgs {
     uint32_t nslots0;
     uint32_t max_slots;       // table capacity; a level with more slots is left to the host
     uint32_t max_tiles;       // a level with more tiles is left to the host's TMA-ring kernel
+    uint32_t fin_max;         // segments up to this size go to the finishers (<= kTailFinMax)
     int in0;                  // buffer read by level l0
     double* bx[2];
     double* by[2];

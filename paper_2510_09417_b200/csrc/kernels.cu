@@ -751,6 +751,9 @@ struct PlanArgs {
 __device__ __forceinline__ uint8_t kind_of(uint32_t m) {
     return m == 0 ? kEmpty : (m == 1 ? kLeaf : (m <= kFinMax ? kFin : kInternal));
 }
+__device__ __forceinline__ uint8_t kind_of_cap(uint32_t m, uint32_t fin_max) {
+    return m == 0 ? kEmpty : (m == 1 ? kLeaf : (m <= fin_max ? kFin : kInternal));
+}
 
 // nblocks: CTAs running the planner (they claim slot chunks dynamically);
 // the persistent tail kernel runs it on one CTA.
@@ -1116,46 +1119,53 @@ __device__ unsigned long long g_ftrace[64];
 __device__ uint32_t g_ftrace_on;
 
 constexpr int kFcThreads = 256;
-constexpr int kFcNodes = int(kFinMax / 2);  // nodes of one depth hold >= 2 points each
-constexpr int kFcItems = int(kFinMax) / kFcThreads;  // points per thread
 constexpr uint16_t kDead = 0xffffu;
 constexpr uint16_t kLinkEmpty = 0, kLinkLeaf = 0x4000, kLinkNode = 0x8000;  // kind | value
 
-struct FinCtaSmem {
-    double x[kFinMax + 3];
-    double y[kFinMax + 3];
-    uint32_t gid[kFinMax + 3];
-    uint16_t work[2][kFinMax];
-    uint16_t wnode[2][kFinMax];
-    uint16_t np[2][kFcNodes], nr[2][kFcNodes], nq[2][kFcNodes];
-    uint16_t nlo[2][kFcNodes], nhi[2][kFcNodes], ntree[2][kFcNodes];
-    unsigned long long ckey[2 * kFcNodes];
-    uint32_t ccnt[2 * kFcNodes];
-    uint32_t cncand[2 * kFcNodes];
-    uint16_t ccand[2 * kFcNodes];
-    uint16_t cmap[2 * kFcNodes];
-    uint16_t tapex[kFinMax + 1];
-    uint16_t tleft[kFinMax + 1], tright[kFinMax + 1];
-    uint16_t tsize[kFinMax + 1], tstart[kFinMax + 1];
-    uint16_t lvl_start[kFinMax + 2];
+// shared memory of the CTA finisher for segments of at most CAP points
+// (kFinMax for the host-driven finisher kernel, kTailFinMax inside KT)
+template <int CAP>
+struct FinCtaSmemT {
+    static constexpr int kCap = CAP;
+    static constexpr int kNodes = CAP / 2;  // nodes of one depth hold >= 2 points each
+    double x[CAP + 3];
+    double y[CAP + 3];
+    uint32_t gid[CAP + 3];
+    uint16_t work[2][CAP];
+    uint16_t wnode[2][CAP];
+    uint16_t np[2][kNodes], nr[2][kNodes], nq[2][kNodes];
+    uint16_t nlo[2][kNodes], nhi[2][kNodes], ntree[2][kNodes];
+    unsigned long long ckey[2 * kNodes];
+    uint32_t ccnt[2 * kNodes];
+    uint32_t cncand[2 * kNodes];
+    uint16_t ccand[2 * kNodes];
+    uint16_t cmap[2 * kNodes];
+    uint16_t tapex[CAP + 1];
+    uint16_t tleft[CAP + 1], tright[CAP + 1];
+    uint16_t tsize[CAP + 1], tstart[CAP + 1];
+    uint16_t lvl_start[CAP + 2];
     uint32_t wsum[kFcThreads / 32];
     uint32_t tie;
     uint32_t nnext;
 };
+using FinCtaSmem = FinCtaSmemT<int(kFinMax)>;
 
-__device__ __forceinline__ uint32_t fc_link_size(const FinCtaSmem& S, uint16_t l) {
+template <class SM>
+__device__ __forceinline__ uint32_t fc_link_size(const SM& S, uint16_t l) {
     return (l & kLinkNode) ? S.tsize[l & 0x3fff] : ((l & kLinkLeaf) ? 1u : 0u);
 }
 
 // the farthest-point key of local point lid in child (node c, side s)
-__device__ __forceinline__ unsigned long long fc_key(const FinCtaSmem& S, int cp, int c, int s, uint16_t lid) {
+template <class SM>
+__device__ __forceinline__ unsigned long long fc_key(const SM& S, int cp, int c, int s, uint16_t lid) {
     const uint16_t p = S.np[cp][c], r = S.nr[cp][c], q = S.nq[cp][c];
     const double fx = s ? dsub(S.x[q], S.x[r]) : dsub(S.x[r], S.x[p]);
     const double fy = s ? dsub(S.y[q], S.y[r]) : dsub(S.y[r], S.y[p]);
     return key_of(lat_off(fx, fy, S.x[lid], S.y[lid]));
 }
 
-__device__ __forceinline__ void finisher_cta_body(FinCtaSmem& S, const FinRec* fins, const LevelInfo* info,
+template <int CAP>
+__device__ __forceinline__ void finisher_cta_body(FinCtaSmemT<CAP>& S, const FinRec* fins, const LevelInfo* info,
                                                   uint32_t fin_cap, const double* __restrict__ ix,
                                                   const double* __restrict__ iy,
                                                   const uint32_t* __restrict__ iid, uint32_t* chain,
@@ -1166,7 +1176,7 @@ __device__ __forceinline__ void finisher_cta_body(FinCtaSmem& S, const FinRec* f
         const uint32_t fi = fin_cap - 1u - f;
         const FinRec rec = fins[fi];
         const uint32_t m = rec.c.m;
-        VQB_CHECK(m > kFinSmall && m <= kFinMax, 32, m, f);
+        VQB_CHECK(m > kFinSmall && m <= uint32_t(CAP), 32, m, f);
         const uint16_t P0 = uint16_t(m), Q0 = uint16_t(m + 1), R0 = uint16_t(m + 2);
         for (uint32_t i = tid; i < m; i += kFcThreads) {
             S.x[i] = ix[rec.c.begin + i];
@@ -1204,17 +1214,21 @@ __device__ __forceinline__ void finisher_cta_body(FinCtaSmem& S, const FinRec* f
             // when it beats the value already there.
             // all of a thread's points first (independent f64 chains overlap),
             // then the warp-aggregated claims
-            uint32_t chv[kFcItems];
-            uint16_t lidv[kFcItems];
+            constexpr int kFcItems = CAP / kFcThreads;  // points per thread
+            constexpr int kFcChunk = kFcItems < 4 ? kFcItems : 4;  // in registers at a time
+            for (int k0 = 0; k0 < kFcItems; k0 += kFcChunk) {
+            uint32_t chv[kFcChunk];
+            uint16_t lidv[kFcChunk];
 #pragma unroll
-            for (int k = 0; k < kFcItems; ++k) {
+            for (int kk = 0; kk < kFcChunk; ++kk) {
+                const int k = k0 + kk;
                 const uint32_t i = uint32_t(k) * kFcThreads + tid;
                 const uint16_t c = i < m ? S.wnode[cur][i] : kDead;
-                chv[k] = 0xffffffffu;
-                lidv[k] = 0;
+                chv[kk] = 0xffffffffu;
+                lidv[kk] = 0;
                 if (c != kDead) {
                     const uint16_t lid = S.work[cur][i];
-                    lidv[k] = lid;
+                    lidv[kk] = lid;
                     const uint16_t p = S.np[cur][c], r = S.nr[cur][c], q = S.nq[cur][c];
                     const double u = S.x[lid], w = S.y[lid];
                     const double A = dsub(S.x[p], u), B = dsub(S.y[p], w);
@@ -1225,15 +1239,15 @@ __device__ __forceinline__ void finisher_cta_body(FinCtaSmem& S, const FinRec* f
                     if (la || lb) {
                         const int sd = la ? 0 : 1;
                         const uint32_t ch = 2u * c + sd;
-                        chv[k] = ch;
+                        chv[kk] = ch;
                         const unsigned long long key = fc_key(S, cur, c, sd, lid);
                         if (key < S.ckey[ch]) atomicMin(&S.ckey[ch], key);
                     }
                 }
             }
 #pragma unroll
-            for (int k = 0; k < kFcItems; ++k) {
-                const uint32_t ch = chv[k];
+            for (int kk = 0; kk < kFcChunk; ++kk) {
+                const uint32_t ch = chv[kk];
                 const unsigned grp = __match_any_sync(kFull, ch);
                 const int leader = __ffs(grp) - 1;
                 uint32_t base = 0;
@@ -1243,9 +1257,10 @@ __device__ __forceinline__ void finisher_cta_body(FinCtaSmem& S, const FinRec* f
                     const uint32_t pos = base + __popc(grp & lanemask_lt());
                     const uint32_t cc = ch >> 1;
                     const uint32_t dest = (ch & 1u) ? uint32_t(S.nhi[cur][cc]) - 1u - pos : uint32_t(S.nlo[cur][cc]) + pos;
-                    S.work[nxt][dest] = lidv[k];
+                    S.work[nxt][dest] = lidv[kk];
                     S.wnode[nxt][dest] = uint16_t(ch);
                 }
+            }
             }
             __syncthreads();
             if (ftr && depth == 0) g_ftrace[40] = gtimer_ns();
@@ -1386,12 +1401,15 @@ __device__ __forceinline__ void finisher_cta_body(FinCtaSmem& S, const FinRec* f
 // Both finishers of a level in one launch (kFcThreads per CTA): first the
 // CTA segments (one CTA each), then the warp segments (one warp each), in the
 // same shared memory.
-union FinAllSmem {
-    FinCtaSmem cta;
+template <int CAP>
+union FinAllSmemT {
+    FinCtaSmemT<CAP> cta;
     FinSmem warp[kFcThreads / 32];
 };
+using FinAllSmem = FinAllSmemT<int(kFinMax)>;
 
-__device__ __forceinline__ void finisher_all_body(FinAllSmem& U, const FinRec* fins, const LevelInfo* info,
+template <int CAP>
+__device__ __forceinline__ void finisher_all_body(FinAllSmemT<CAP>& U, const FinRec* fins, const LevelInfo* info,
                                                   uint32_t fin_cap, const double* __restrict__ ix,
                                                   const double* __restrict__ iy,
                                                   const uint32_t* __restrict__ iid, uint32_t* chain,

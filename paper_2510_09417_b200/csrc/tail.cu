@@ -66,7 +66,7 @@ __device__ __noinline__ void tail_plan(const TailArgs& A, const TailLevel& T, ui
             c = T.slots[s];
             m = c.m;
         }
-        const uint8_t kd = s < nslots ? kind_of(m) : kEmpty;
+        const uint8_t kd = s < nslots ? kind_of_cap(m, A.fin_max) : kEmpty;
         PlanAgg mine;
         pl_clear(mine);
         mine.nseg = kd == kInternal;
@@ -177,7 +177,7 @@ struct TailEmitSmem {
     uint32_t off[kTailLevels + 1];
     uint32_t total;
 };
-static_assert(sizeof(TailEmitSmem) <= sizeof(FinAllSmem), "emission reuses the finisher's shared memory");
+static_assert(sizeof(TailEmitSmem) <= sizeof(FinAllSmemT<kTailFinMax>), "emission reuses the finisher's shared memory");
 
 // returns false (nothing written) when the tree is too large
 __device__ __noinline__ bool tail_emit(const TailArgs& A, TailEmitSmem& E, int nl) {
@@ -280,7 +280,7 @@ __device__ __noinline__ void tail_report(const TailArgs& A, int nl) {
 __global__ void __launch_bounds__(kThreads, 2) tail_kernel(const __grid_constant__ TailArgs A) {
     VQB_PDL();
     extern __shared__ __align__(16) unsigned char tl_dsm[];
-    FinAllSmem& U = *reinterpret_cast<FinAllSmem*>(tl_dsm);
+    FinAllSmemT<kTailFinMax>& U = *reinterpret_cast<FinAllSmemT<kTailFinMax>*>(tl_dsm);
     __shared__ uint32_t s_flag;
     cg::grid_group grid = cg::this_grid();
     if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -377,19 +377,19 @@ __global__ void __launch_bounds__(kThreads, 2) tail_kernel(const __grid_constant
     }
 }
 
-size_t tail_smem_bytes() { return sizeof(FinAllSmem); }
+size_t tail_smem_bytes() { return sizeof(FinAllSmemT<kTailFinMax>); }
 
 int occupancy_tail() {
     int b = 0;
-    cudaFuncSetAttribute(tail_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(FinAllSmem)));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, tail_kernel, kThreads, sizeof(FinAllSmem));
+    cudaFuncSetAttribute(tail_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(FinAllSmemT<kTailFinMax>)));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, tail_kernel, kThreads, sizeof(FinAllSmemT<kTailFinMax>));
     return b;
 }
 
 cudaError_t launch_tail(const TailArgs& a, int grid, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(tail_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(FinAllSmem)));
+        cudaFuncSetAttribute(tail_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(FinAllSmemT<kTailFinMax>)));
         attr = true;
     }
     // cooperative (grid barriers) and, where the driver accepts the pair,
@@ -400,7 +400,7 @@ cudaError_t launch_tail(const TailArgs& a, int grid, cudaStream_t st) {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(grid);
         cfg.blockDim = dim3(kThreads);
-        cfg.dynamicSmemBytes = sizeof(FinAllSmem);
+        cfg.dynamicSmemBytes = sizeof(FinAllSmemT<kTailFinMax>);
         cfg.stream = st;
         cudaLaunchAttribute at[2];
         at[0].id = cudaLaunchAttributeCooperative;
@@ -416,7 +416,7 @@ cudaError_t launch_tail(const TailArgs& a, int grid, cudaStream_t st) {
     }
     void* args[] = {const_cast<TailArgs*>(&a)};
     return cudaLaunchCooperativeKernel((const void*)tail_kernel, dim3(grid), dim3(kThreads), args,
-                                       sizeof(FinAllSmem), st);
+                                       sizeof(FinAllSmemT<kTailFinMax>), st);
 }
 
 }  // namespace vqb
