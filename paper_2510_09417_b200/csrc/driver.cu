@@ -522,10 +522,11 @@ class Engine {
                 d->release();
         for (DevBuf* d : {&tile_seg_, &chain_, &out_, &part_, &status_, &flags_, &aggs_, &incs_})
             d->release();
-        if (graph_exec_) {
-            cudaGraphExecDestroy(graph_exec_);
-            graph_exec_ = nullptr;
-        }
+        for (GraphEntry& e : graphs_)
+            if (e.exec) {
+                cudaGraphExecDestroy(e.exec);
+                e.exec = nullptr;
+            }
         cudaMemPool_t pool;
         if (cudaDeviceGetDefaultMemPool(&pool, dev_) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
         ck(cudaDeviceSynchronize(), "trim sync");
@@ -723,12 +724,24 @@ class Engine {
         // allocate everything first: nothing may allocate inside the capture
         prepare_split(n, st);
         graph_ta_ = tail_args(dx, dy, n, 1u, d_out, 2, st);
-        const uint64_t gen = g_alloc_gen.load();
-        if (!(graph_exec_ && graph_dx_ == dx && graph_dy_ == dy && graph_n_ == n && graph_out_ == d_out &&
-              graph_st_ == st && graph_gen_ == gen)) {
-            if (graph_exec_) {
-                cudaGraphExecDestroy(graph_exec_);
-                graph_exec_ = nullptr;
+        const GraphKey key{dx, dy, n, d_out, st, g_alloc_gen.load()};
+        GraphEntry* hit = nullptr;
+        for (GraphEntry& e : graphs_)
+            if (e.exec && e.key == key) hit = &e;
+        if (!hit) {
+            // capture only an input seen twice in a row (one-off inputs, e.g.
+            // the candidates of a sharded hull, run direct: a capture costs
+            // more than it saves once)
+            if (!(pending_ == key)) {
+                pending_ = key;
+                return false;
+            }
+            GraphEntry* slot = &graphs_[0];  // least recently used
+            for (GraphEntry& e : graphs_)
+                if (!e.exec || e.used < slot->used) slot = &e;
+            if (slot->exec) {
+                cudaGraphExecDestroy(slot->exec);
+                slot->exec = nullptr;
             }
             cudaGraph_t g = nullptr;
             VQB_TRACE("hull: capturing the split-root graph");
@@ -750,28 +763,30 @@ class Engine {
                 launches_ = saved;
                 return false;
             }
-            graph_launches_ = launches_ - saved;
+            slot->launches = launches_ - saved;
             launches_ = saved;
             const cudaError_t e = cudaStreamEndCapture(st, &g);
-            if (e != cudaSuccess || !g || cudaGraphInstantiate(&graph_exec_, g, 0) != cudaSuccess) {
+            if (e != cudaSuccess || !g || cudaGraphInstantiate(&slot->exec, g, 0) != cudaSuccess) {
                 if (g) cudaGraphDestroy(g);
                 VQB_TRACE("hull: capture failed: %s", cudaGetErrorString(cudaGetLastError()));
-                graph_exec_ = nullptr;
+                slot->exec = nullptr;
                 use_graph_ = false;
                 return false;
             }
             cudaGraphDestroy(g);
-            if (g_alloc_gen.load() != gen) {  // something allocated during the capture: do not trust it
-                cudaGraphExecDestroy(graph_exec_);
-                graph_exec_ = nullptr;
+            if (g_alloc_gen.load() != key.gen) {  // something allocated during the capture: do not trust it
+                cudaGraphExecDestroy(slot->exec);
+                slot->exec = nullptr;
                 use_graph_ = false;
                 return false;
             }
-            graph_dx_ = dx; graph_dy_ = dy; graph_n_ = n; graph_out_ = d_out; graph_st_ = st; graph_gen_ = gen;
+            slot->key = key;
+            hit = slot;
         }
+        hit->used = ++graph_clock_;
         VQB_TRACE("hull: graph launch");
-        ck(cudaGraphLaunch(graph_exec_, st), "graph launch");
-        launches_ += graph_launches_;
+        ck(cudaGraphLaunch(hit->exec, st), "graph launch");
+        launches_ += hit->launches;
         stats_.bytes_extremes = 16 * n / (sample_mask(n) + 1);
         stats_.bytes_bootstrap = 0;
         return true;
@@ -1007,14 +1022,26 @@ class Engine {
     cudaStream_t own_st_ = nullptr;
     bool sample_trace_ = getenv("VQHULL_SAMPLE_TRACE") != nullptr;
     bool fin_trace_ = getenv("VQHULL_FIN_TRACE") != nullptr && (fin_trace(true), true);
-    cudaGraphExec_t graph_exec_ = nullptr;
-    const double* graph_dx_ = nullptr;
-    const double* graph_dy_ = nullptr;
-    uint64_t graph_n_ = 0;
-    uint32_t* graph_out_ = nullptr;
-    cudaStream_t graph_st_ = nullptr;
-    uint64_t graph_gen_ = 0;
-    uint32_t graph_launches_ = 0;
+    struct GraphKey {
+        const double* dx = nullptr;
+        const double* dy = nullptr;
+        uint64_t n = 0;
+        uint32_t* out = nullptr;
+        cudaStream_t st = nullptr;
+        uint64_t gen = ~0ull;
+        bool operator==(const GraphKey& o) const {
+            return dx == o.dx && dy == o.dy && n == o.n && out == o.out && st == o.st && gen == o.gen;
+        }
+    };
+    struct GraphEntry {
+        GraphKey key;
+        cudaGraphExec_t exec = nullptr;
+        uint32_t launches = 0;
+        uint64_t used = 0;
+    };
+    GraphEntry graphs_[4];  // small LRU cache of captured hulls (all share the engine's buffers)
+    GraphKey pending_;
+    uint64_t graph_clock_ = 0;
     TailArgs graph_ta_;
     DevBuf report_;
     static size_t report_bytes(int nlev) { return 32 + sizeof(LevelInfo) * size_t(nlev); }

@@ -373,6 +373,29 @@ def test_tail_kernel_paths(vq, cuda, oracle, monkeypatch):
     assert handed_over >= 3
 
 
+def test_graph_cache_alternating_inputs(vq, cuda, oracle):
+    """Replayed hull graphs are keyed by the caller's buffers: alternating
+    between two inputs (as a sharded hull alternates shard and candidates)
+    replays the right graph every time, also after the data changed."""
+    import torch
+
+    bufs = []
+    for kind, n, seed in (("square", 3_000_000, 2), ("disk", 2_000_000, 1)):
+        xs, ys = vq.generate(kind, n, seed)
+        bufs.append((torch.from_numpy(xs).cuda(), torch.from_numpy(ys).cuda(), oracle.hull_indices(xs, ys)))
+    for rep in range(6):
+        X, Y, ref = bufs[rep % 2]
+        got = vq.hull_device(X, Y).cpu().numpy().astype(np.uint64)
+        assert np.array_equal(got, ref), rep
+    # same buffers, new contents: the replay reads the new points
+    X, Y, _ = bufs[0]
+    xs, ys = vq.generate("disk", X.numel(), 9)
+    X.copy_(torch.from_numpy(xs))
+    Y.copy_(torch.from_numpy(ys))
+    got = vq.hull_device(X, Y).cpu().numpy().astype(np.uint64)
+    assert np.array_equal(got, oracle.hull_indices(xs, ys))
+
+
 def test_split_root_far_outlier_rerun(vq, cuda, oracle):
     """A survivor far beyond the sampled octagon's scale voids the margin
     argument: the call is rerun unfiltered, with the same (reference) result."""
