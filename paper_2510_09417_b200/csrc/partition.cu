@@ -1550,7 +1550,7 @@ __global__ void __launch_bounds__(kCtlThreads, 3) root_filter_tma(FilterArgs a) 
     }
     __syncthreads();
     const double kInf = __longlong_as_double(0x7ff0000000000000ll);
-    ExtKey lo{0.0, 0.0, kNoIdx, 0u}, hi{0.0, 0.0, kNoIdx, 0u};
+    ExtKey lo{kInf, 0.0, kNoIdx, 0u}, hi{-kInf, 0.0, kNoIdx, 0u};
     double amax = 0.0;
     uint32_t bad = 0;
 
@@ -1664,9 +1664,16 @@ __global__ void __launch_bounds__(kCtlThreads, 3) root_filter_tma(FilterArgs a) 
                 const unsigned b = __ballot_sync(kFull, keep);
                 if (keep) {
                     s_surv[par][warp][sn + __popc(b & lt)] = uint16_t(idx);
-                    const ExtKey c{u, w, tbase + idx, 1u};
-                    if (lo_better(c, lo)) lo = c;
-                    if (hi_better(c, hi)) hi = c;
+                    // the full (x, y, index) order only for a possible new extreme
+                    // (lo/hi start at x = +-inf, so the first survivor enters)
+                    if (u <= lo.x) {
+                        const ExtKey c{u, w, tbase + idx, 1u};
+                        if (lo_better(c, lo)) lo = c;
+                    }
+                    if (u >= hi.x) {
+                        const ExtKey c{u, w, tbase + idx, 1u};
+                        if (hi_better(c, hi)) hi = c;
+                    }
                     amax = fmax(amax, fmax(fabs(u), fabs(w)));
                 }
                 sn += __popc(b);
