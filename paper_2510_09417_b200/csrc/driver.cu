@@ -657,7 +657,7 @@ class Engine {
     void launch_tail_report(const TailArgs& ta, cudaStream_t st) {
         const int l0 = ta.l0;
         if (ta.trace) ck(cudaMemsetAsync(ta.trace, 0, 8 * (1 + 10 * kTailLevels), st), "memset trace");
-        tk(3, st, [&] { ck(launch_tail(ta, sms_ * occ_tail_, st), "tail launch"); });
+        tk(3, st, [&] { ck(launch_tail(ta, tail_grid(), st), "tail launch"); });
         if (tail_trace_) {
             std::vector<unsigned long long> tr(1 + 10 * kTailLevels);
             ck(cudaMemcpyAsync(tr.data(), trace_.p, 8 * tr.size(), cudaMemcpyDeviceToHost, st), "d2h trace");
@@ -1012,6 +1012,10 @@ class Engine {
     bool tail_emitted_ = false;
     static constexpr uint32_t kTailTilesPerCta = 2;  // KT takes levels of at most this many tiles per CTA
     // (VQHULL_TAIL_MAXTILES overrides the tile bound: tests of the hand-over paths)
+    int tail_grid() const {  // (VQHULL_TAIL_GRID overrides: experiments)
+        const char* e = getenv("VQHULL_TAIL_GRID");
+        return e ? std::max(1, std::min(atoi(e), sms_ * occ_tail_)) : sms_ * occ_tail_;
+    }
     uint32_t tail_max_tiles() const {
         const char* e = getenv("VQHULL_TAIL_MAXTILES");
         return e ? uint32_t(atoi(e)) : uint32_t(kTailTilesPerCta * sms_ * occ_tail_);
