@@ -1835,13 +1835,26 @@ __global__ void __launch_bounds__(kCtlThreads, 3) level_tma(LevelArgs a) {
     uint32_t bi[2] = {kNoIdx, kNoIdx};
 
     auto finalize = [&]() {
-        for (int c = 0; c < 2; ++c) {
-            double oo;
-            uint32_t io;
-            block_best_d<2>(S, c, bo[c], bi[c], a.gx, a.gy, oo, io);
-            if (threadIdx.x == 0)
-                s_run[c] = best_from_key(io == kNoIdx ? kNoKey : 0ull, io, c == 0 ? s_cur.adx : s_cur.bdx,
-                                         c == 0 ? s_cur.ady : s_cur.bdy, a.gx, a.gy);
+        // both classes' winners first, then their coordinates in one round
+        // trip (they are random accesses to the input)
+        double oo;
+        uint32_t io0, io1;
+        block_best_d<2>(S, 0, bo[0], bi[0], a.gx, a.gy, oo, io0);
+        block_best_d<2>(S, 1, bo[1], bi[1], a.gx, a.gy, oo, io1);
+        if (threadIdx.x == 0) {
+            const double x0 = io0 != kNoIdx ? a.gx[io0] : 0.0, y0 = io0 != kNoIdx ? a.gy[io0] : 0.0;
+            const double x1 = io1 != kNoIdx ? a.gx[io1] : 0.0, y1 = io1 != kNoIdx ? a.gy[io1] : 0.0;
+            Best b0 = best_none(), b1 = best_none();
+            if (io0 != kNoIdx) {
+                b0.x = x0; b0.y = y0; b0.idx = io0; b0.valid = 1u;
+                b0.off = lat_off(s_cur.adx, s_cur.ady, x0, y0);
+            }
+            if (io1 != kNoIdx) {
+                b1.x = x1; b1.y = y1; b1.idx = io1; b1.valid = 1u;
+                b1.off = lat_off(s_cur.bdx, s_cur.bdy, x1, y1);
+            }
+            s_run[0] = b0;
+            s_run[1] = b1;
         }
         if (threadIdx.x == 0) {
             const uint32_t k = s_cur_k;
