@@ -142,6 +142,7 @@ class Engine {
         ck(cudaMallocHost(&h_info_, sizeof(LevelInfo) * 2), "cudaMallocHost");
         ck(cudaMallocHost(&h_root_, sizeof(RootInfo)), "cudaMallocHost");
         ck(cudaMallocHost(&h_word_, 64), "cudaMallocHost");
+        fault_dev_ = fault_word_ptr();
         ck(cudaMallocHost(&h_tail_, report_bytes(kTailLevels)), "cudaMallocHost");
         partials_.ensure(partial_bytes(stream_grid_), nullptr);
         VQB_TRACE("engine: synchronize");
@@ -168,6 +169,8 @@ class Engine {
         if (n >= 0xffffffffull) return VQHULL_ESIZE;
         launches_ = 0;
         begin_timing(st);
+        if (n <= kFinMax && !stable_ && !root_reference_ && !root_octagon_ && !force_reference_ && use_tiny_)
+            return run_tiny(dx, dy, n, d_out, h, st);
 
         // ---- root stage: polygon + first partition (levels 1+2 in reference mode)
         const bool aligned = ((reinterpret_cast<uintptr_t>(dx) | reinterpret_cast<uintptr_t>(dy)) & 15u) == 0;
@@ -383,16 +386,14 @@ class Engine {
         }
         if (!tail_emitted_) {  // (the tail kernel's h came with its state)
             ck(cudaMemcpyAsync(h_word_, hword_, 4, cudaMemcpyDeviceToHost, st), "d2h h");
+            ck(cudaMemcpyAsync(h_word_ + 1, fault_dev_, 4, cudaMemcpyDeviceToHost, st), "d2h fault");
             end_timing(st);
             VQB_TRACE("hull: final sync");
             ck(cudaStreamSynchronize(st), "final sync");
         }
         VQB_TRACE("hull: done");
         ck(cudaGetLastError(), "kernel launch");
-        if (const uint32_t f = read_and_clear_fault()) {
-            g_last_error = "device fault code " + std::to_string(f);
-            throw CudaError{cudaErrorUnknown};
-        }
+        check_fault();
         *h = *h_word_;
         if (sample_trace_) print_sample_trace();
         if (fin_trace_) print_fin_trace();
@@ -671,6 +672,7 @@ class Engine {
         }
         ck(cudaMemcpyAsync(h_tail_, ta.report, report_bytes(ta.nlev), cudaMemcpyDeviceToHost, st),
            "d2h tail report");
+        ck(cudaMemcpyAsync(h_word_ + 1, fault_dev_, 4, cudaMemcpyDeviceToHost, st), "d2h fault");
         end_timing(st);  // (re-recorded later if the host emits)
     }
 
@@ -790,6 +792,51 @@ class Engine {
         stats_.bytes_extremes = 16 * n / (sample_mask(n) + 1);
         stats_.bytes_bootstrap = 0;
         return true;
+    }
+
+    // n <= kFinMax: the whole hull in one CTA (tiny_hull_kernel), one launch
+    // and one synchronization
+    int run_tiny(const double* dx, const double* dy, uint64_t n, uint32_t* d_out, uint64_t* h, cudaStream_t st) {
+        tiny_.ensure(kFinMax * 8 + sizeof(FinRec) + sizeof(LevelInfo) + 64, st);
+        char* p = tiny_.as<char>();
+        TinyArgs ta;
+        ta.xs = dx;
+        ta.ys = dy;
+        ta.n = uint32_t(n);
+        ta.iid = reinterpret_cast<uint32_t*>(p);
+        ta.chain = reinterpret_cast<uint32_t*>(p + kFinMax * 4);
+        ta.fin = reinterpret_cast<FinRec*>(p + kFinMax * 8);
+        ta.info = reinterpret_cast<LevelInfo*>(p + kFinMax * 8 + sizeof(FinRec));
+        ta.fin_count = reinterpret_cast<uint32_t*>(p + kFinMax * 8 + sizeof(FinRec) + sizeof(LevelInfo));
+        ta.report = ta.fin_count + 4;
+        ta.out = d_out;
+        tk(4, st, [&] { launch_tiny(ta, st); ck(cudaGetLastError(), "tiny launch"); });
+        ck(cudaMemcpyAsync(h_tail_, ta.report, 8, cudaMemcpyDeviceToHost, st), "d2h tiny report");
+        ck(cudaMemcpyAsync(h_word_ + 1, fault_dev_, 4, cudaMemcpyDeviceToHost, st), "d2h fault");
+        end_timing(st);
+        ck(cudaStreamSynchronize(st), "tiny sync");
+        check_fault();
+        if (h_tail_[1]) return VQHULL_EINVAL;
+        *h = h_tail_[0];
+        stats_.hull_size = *h;
+        stats_.launches = launches_;
+        stats_.levels = 1;
+        stats_.survivors_root = n;
+        stats_.bytes_root_partition = 16 * n;
+        stats_.bytes_moved = 16 * n + 4 * *h;
+        collect_timing();
+        return VQHULL_OK;
+    }
+
+    // the device fault word (finisher guard, debug bounds checks) arrives with
+    // each call's last host copy: no extra synchronous read per hull
+    void check_fault() {
+        if (const uint32_t f = h_word_[1]) {
+            h_word_[1] = 0;
+            (void)read_and_clear_fault();
+            g_last_error = "device fault code " + std::to_string(f);
+            throw CudaError{cudaErrorUnknown};
+        }
     }
 
     cudaStream_t own_stream() {
@@ -1010,6 +1057,10 @@ class Engine {
     bool use_tail_ = !(getenv("VQHULL_TAIL") && getenv("VQHULL_TAIL")[0] == '0');
     uint32_t* h_tail_ = nullptr;
     bool tail_emitted_ = false;
+    DevBuf tiny_;  // the one-CTA path's scratch
+    uint32_t* fault_dev_ = nullptr;
+    // VQHULL_TINY=0: tiny inputs through the general pipeline (tests)
+    bool use_tiny_ = !(getenv("VQHULL_TINY") && getenv("VQHULL_TINY")[0] == '0');
     static constexpr uint32_t kTailTilesPerCta = 2;  // KT takes levels of at most this many tiles per CTA
     // (VQHULL_TAIL_MAXTILES overrides the tile bound: tests of the hand-over paths)
     int tail_grid() const {  // (VQHULL_TAIL_GRID overrides: experiments)

@@ -247,6 +247,20 @@ struct TailArgs {
     uint32_t* report;         // [8 words: state, h, nonfinite, unsafe, filter, survivors, 0] + level infos
 };
 
+// One-CTA hull of a tiny input (kernels.cu, tiny_hull_kernel).
+struct TinyArgs {
+    const double* xs;
+    const double* ys;
+    uint32_t n;
+    uint32_t* iid;        // scratch: positions 0..n-1 (the segment's carried indices)
+    FinRec* fin;          // one FinRec
+    LevelInfo* info;      // its counts (warp or CTA list)
+    uint32_t* chain;
+    uint32_t* fin_count;
+    uint32_t* out;        // index list (device)
+    uint32_t* report;     // [0] h, [1] non-finite
+};
+
 // Emission of a small recursion tree in one kernel: per level, the slot
 // tables (levels 2 .. 2 + nlev - 1).
 constexpr int kEmitMaxLevels = 48;

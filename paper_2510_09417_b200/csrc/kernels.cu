@@ -1584,6 +1584,103 @@ __global__ void poly_frame_kernel(const RootInfo* root, const uint32_t* size2, u
 }
 
 // ===========================================================================
+// K0: a whole hull of n <= kFinMax points in ONE CTA (tiny inputs, the
+// candidates of a sharded hull): find_extremes (geometry.cpp:7-36) as a block
+// reduction, then the bootstrap triangle (p, q, p) (hull.cpp:228-235) as one
+// finisher segment — the finisher's chain of that segment is chain(S1) [q]
+// chain(S2) — and the output [p] chain (hull.cpp:259-266).  No filter, no
+// levels: one launch instead of sample + filter + recursion kernel.
+// ===========================================================================
+
+__global__ void __launch_bounds__(kFcThreads) tiny_hull_kernel(const __grid_constant__ TinyArgs A) {
+    VQB_PDL();
+    extern __shared__ __align__(16) unsigned char tn_dsm[];
+    FinAllSmem& U = *reinterpret_cast<FinAllSmem*>(tn_dsm);
+    __shared__ ExtKey s_lo[kFcThreads / 32], s_hi[kFcThreads / 32];
+    __shared__ uint32_t s_bad[kFcThreads / 32];
+    __shared__ uint32_t s_go;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint32_t n = A.n;
+    ExtKey lo{0.0, 0.0, kNoIdx, 0u}, hi{0.0, 0.0, kNoIdx, 0u};
+    uint32_t bad = 0;
+    for (uint32_t i = tid; i < n; i += kFcThreads) {
+        const double x = A.xs[i], y = A.ys[i];
+        A.iid[i] = i;
+        bad |= uint32_t(nonfinite_bits(x) | nonfinite_bits(y));
+        const ExtKey c{x, y, i, 1u};
+        if (lo_better(c, lo)) lo = c;
+        if (hi_better(c, hi)) hi = c;
+    }
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) {
+        const ExtKey a = shfl_key(lo, s);
+        if (lo_better(a, lo)) lo = a;
+        const ExtKey b = shfl_key(hi, s);
+        if (hi_better(b, hi)) hi = b;
+        bad |= __shfl_xor_sync(kFull, bad, s);
+    }
+    if (lane == 0) {
+        s_lo[warp] = lo;
+        s_hi[warp] = hi;
+        s_bad[warp] = bad;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        for (int w = 1; w < kFcThreads / 32; ++w) {
+            if (lo_better(s_lo[w], lo)) lo = s_lo[w];
+            if (hi_better(s_hi[w], hi)) hi = s_hi[w];
+            bad |= s_bad[w];
+        }
+        A.report[1] = bad;
+        s_go = 0u;
+        if (!bad && lo.valid) {
+            A.out[0] = lo.idx;
+            if (lo.x == hi.x && lo.y == hi.y) {
+                A.report[0] = 1u;  // all points equal: [p]
+            } else {
+                FinRec f;
+                f.c.px = lo.x; f.c.py = lo.y;
+                f.c.rx = hi.x; f.c.ry = hi.y;  // apex q
+                f.c.qx = lo.x; f.c.qy = lo.y;
+                f.c.begin = 0;
+                f.c.m = n;
+                f.c.r_idx = hi.idx;
+                f.chain_base = 0;
+                f.slot = 0;
+                f.pad = 0;
+                *A.fin = f;
+                LevelInfo li;
+                li.nslots = 1; li.nseg = 0; li.ntiles = 0; li.out_total = 0;
+                li.fin_total = n; li.nleaf = 0; li.fin_base = 0; li.pad = 0;
+                li.nfin = n <= kFinSmall ? 1u : 0u;  // warp list (front) or CTA list (back, fin_cap 1)
+                li.nfin2 = n <= kFinSmall ? 0u : 1u;
+                *A.info = li;
+                s_go = 1u;
+            }
+        } else {
+            A.report[0] = 0u;
+        }
+        __threadfence_block();
+    }
+    __syncthreads();
+    if (!s_go) return;
+    finisher_all_body(U, A.fin, A.info, 1u, A.xs, A.ys, A.iid, A.chain, A.fin_count);
+    __syncthreads();
+    const uint32_t c = *reinterpret_cast<volatile uint32_t*>(A.fin_count);
+    for (uint32_t i = tid; i < c; i += kFcThreads) A.out[1 + i] = A.chain[i];
+    if (tid == 0) A.report[0] = 1u + c;
+}
+
+void launch_tiny(const TinyArgs& a, cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(tiny_hull_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(FinAllSmem)));
+        attr = true;
+    }
+    pdl_launch(tiny_hull_kernel, 1, kFcThreads, sizeof(FinAllSmem), st, a);
+}
+
+// ===========================================================================
 // Host-side launchers (C++ linkage, used by driver.cu)
 // ===========================================================================
 void launch_extremes(const double* xs, const double* ys, uint64_t n, void* partials,
@@ -1757,6 +1854,12 @@ int occupancy_poly_sample() {
 }  // namespace vqb
 
 namespace vqb {
+uint32_t* fault_word_ptr() {
+    void* p = nullptr;
+    cudaGetSymbolAddress(&p, g_vqb_fault);
+    return static_cast<uint32_t*>(p);
+}
+
 uint32_t read_and_clear_fault() {
     uint32_t v = 0;
     cudaMemcpyFromSymbol(&v, g_vqb_fault, sizeof v);

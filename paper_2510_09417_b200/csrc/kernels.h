@@ -60,6 +60,8 @@ int occupancy_poly_sample();
 int occupancy_extremes();
 int occupancy_bootstrap();
 uint32_t read_and_clear_fault();
+uint32_t* fault_word_ptr();  // device address of the fault word (async copies)
+void launch_tiny(const TinyArgs& a, cudaStream_t st);
 size_t tail_smem_bytes();
 int occupancy_tail();
 cudaError_t launch_tail(const TailArgs& a, int grid, cudaStream_t st);
