@@ -672,7 +672,6 @@ class Engine {
         }
         ck(cudaMemcpyAsync(h_tail_, ta.report, report_bytes(ta.nlev), cudaMemcpyDeviceToHost, st),
            "d2h tail report");
-        ck(cudaMemcpyAsync(h_word_ + 1, fault_dev_, 4, cudaMemcpyDeviceToHost, st), "d2h fault");
         end_timing(st);  // (re-recorded later if the host emits)
     }
 
@@ -684,6 +683,7 @@ class Engine {
         VQB_TRACE("hull: tail sync");
         ck(cudaStreamSynchronize(st), "tail sync");
         const uint32_t at = h_tail_[0], how = h_tail_[1];
+        h_word_[1] = h_tail_[7];  // the device fault word, copied by the kernel into its report
         stats_.tail_launches += 1;
         stats_.tail_levels += (how == 2 ? at : at + 1) - uint32_t(l0);
         *h_word_ = h_tail_[2];
@@ -811,10 +811,10 @@ class Engine {
         ta.report = ta.fin_count + 4;
         ta.out = d_out;
         tk(4, st, [&] { launch_tiny(ta, st); ck(cudaGetLastError(), "tiny launch"); });
-        ck(cudaMemcpyAsync(h_tail_, ta.report, 8, cudaMemcpyDeviceToHost, st), "d2h tiny report");
-        ck(cudaMemcpyAsync(h_word_ + 1, fault_dev_, 4, cudaMemcpyDeviceToHost, st), "d2h fault");
+        ck(cudaMemcpyAsync(h_tail_, ta.report, 12, cudaMemcpyDeviceToHost, st), "d2h tiny report");
         end_timing(st);
         ck(cudaStreamSynchronize(st), "tiny sync");
+        h_word_[1] = h_tail_[2];  // the device fault word (copied by the kernel)
         check_fault();
         if (h_tail_[1]) return VQHULL_EINVAL;
         *h = h_tail_[0];

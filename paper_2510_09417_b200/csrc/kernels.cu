@@ -1632,6 +1632,7 @@ __global__ void __launch_bounds__(kFcThreads) tiny_hull_kernel(const __grid_cons
             bad |= s_bad[w];
         }
         A.report[1] = bad;
+        A.report[2] = 0u;
         s_go = 0u;
         if (!bad && lo.valid) {
             A.out[0] = lo.idx;
@@ -1668,7 +1669,10 @@ __global__ void __launch_bounds__(kFcThreads) tiny_hull_kernel(const __grid_cons
     __syncthreads();
     const uint32_t c = *reinterpret_cast<volatile uint32_t*>(A.fin_count);
     for (uint32_t i = tid; i < c; i += kFcThreads) A.out[1 + i] = A.chain[i];
-    if (tid == 0) A.report[0] = 1u + c;
+    if (tid == 0) {
+        A.report[0] = 1u + c;
+        A.report[2] = *reinterpret_cast<volatile uint32_t*>(&g_vqb_fault);
+    }
 }
 
 void launch_tiny(const TinyArgs& a, cudaStream_t st) {

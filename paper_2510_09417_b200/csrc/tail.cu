@@ -270,7 +270,7 @@ __device__ __noinline__ void tail_report(const TailArgs& A, int nl) {
         r[4] = R->unsafe;
         r[5] = R->poly.filter;
         r[6] = R->cnt1;
-        r[7] = 0;
+        r[7] = *reinterpret_cast<volatile uint32_t*>(&g_vqb_fault);  // (its own copy would cost a memcpy)
     }
     const uint32_t* src = reinterpret_cast<const uint32_t*>(A.info + A.l0);
     const uint32_t words = uint32_t(nl) * uint32_t(sizeof(LevelInfo) / 4);
