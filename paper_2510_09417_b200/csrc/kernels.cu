@@ -1731,8 +1731,9 @@ void print_fin_trace() {
 #endif
 constexpr uint64_t kSampleMin = VQB_SAMPLE_MIN;
 uint32_t sample_mask(uint64_t n) {
+    static const uint64_t smin = getenv("VQHULL_SAMPLE_MIN") ? uint64_t(atoll(getenv("VQHULL_SAMPLE_MIN"))) : kSampleMin;
     uint64_t k = 1;
-    while (k < 1024 && n / (2 * k) >= kSampleMin) k *= 2;
+    while (k < 1024 && n / (2 * k) >= smin) k *= 2;
     return uint32_t(k - 1);
 }
 
