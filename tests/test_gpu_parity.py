@@ -466,3 +466,30 @@ def test_filter_off_for_extreme_magnitudes(vq, cuda, oracle):
         got = gpu_indices(vq, xs, ys)
         assert vq.stats()["root_filter_on"] == 0
         assert np.array_equal(got, oracle.hull_indices(xs, ys))
+
+
+def test_sharded_hull_nccl_world1(vq, cuda, oracle):
+    """The multi-GPU path end to end on the device with NCCL (world size 1
+    here: one GPU in this pool): local hull, the header-row candidate
+    all-gather over NCCL, the candidates' one-CTA hull, global indices."""
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2510_09417_b200.distributed import sharded_hull
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        for kind, n, seed in (("square", 2_000_000, 2), ("disk", 1_000_000, 1)):
+            xs, ys = vq.generate(kind, n, seed)
+            X, Y = torch.from_numpy(xs).cuda(), torch.from_numpy(ys).cuda()
+            got = sharded_hull(X, Y, 0).cpu().numpy().astype(np.uint64)
+            assert np.array_equal(got, oracle.hull_indices(xs, ys)), kind
+    finally:
+        dist.destroy_process_group()
