@@ -1,12 +1,16 @@
 // Host-side recursion driver and C ABI of the B200 VQhull hot path.
 //
-// One Engine per device owns the HBM workspace (ping-pong point buffers,
-// look-back status words, per-level node tables) and runs a hull as:
-//   K1 extremes -> KA bootstrap arg-max -> KB fused levels 1+2 ->
-//   { planner -> finisher -> tile map -> K2 } per level -> size/emit.
+// One Engine per device owns the HBM workspace (point buffers, level tables,
+// look-back words) and runs a hull as:
+//   n <= kFinMax:  K0 one-CTA hull;
+//   default:       K_S sample polygon -> K_F filter pass -> KT persistent
+//                  recursion (+ emission) — captured once per input as a CUDA
+//                  graph and replayed; wide levels continue host-driven:
+//                  { planner -> finisher -> tile map -> K2 } per level -> emit;
+//   other modes:   K1 extremes -> KA bootstrap -> KB fused levels 1+2 -> levels.
 // The reference's equivalent is convex_hull (hull.cpp:207-267) driving
 // chain_recursive/chain_iterative (hull.cpp:78-190), one call per segment;
-// here every level is one launch over all of its segments.
+// here a level is one launch (or one phase of KT) over all of its segments.
 #include <cuda_runtime.h>
 
 #include <algorithm>

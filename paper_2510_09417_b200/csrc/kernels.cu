@@ -1,11 +1,17 @@
 // sm_100a kernels of the VQhull hot path (see DESIGN.md for the roofline of
 // each one).  Reference behaviour each kernel reproduces is cited inline.
 //
+// Default pipeline (split root):
+//   K_S poly_sample_kernel      16-gon filter polygon from a sample of the input
+//   K_F root_filter_tma         (partition.cu) filter + survivors + find_extremes
+//   KT  tail_kernel             (tail.cu) every recursion level in one launch
+//   K0  tiny_hull_kernel        the whole hull of n <= kFinMax points in one CTA
+// Kernels shared with the other root modes and the host-driven levels:
 //   K1  extremes_kernel         find_extremes            geometry.cpp:7-36
 //   KA  bootstrap_argmax_kernel bootstrap pass p,q,p     hull.cpp:228-235 (+ finiteness check vqhull_c.cpp:32-34)
 //   KB  root_partition_kernel   levels 1+2 fused: the bootstrap split AND the
 //                               two child partitions in ONE pass over the input
-//   K2  level_kernel            extract_blocks (fused classify + two-sided
+//   K2  level_kernel / level_tma  extract_blocks (fused classify + two-sided
 //                               compaction + arg-max), all live segments of a
 //                               level in one launch       extract_core.hpp:421-515
 //   K3  planner_kernel          recursion driver: child -> segment/finisher

@@ -1,7 +1,9 @@
-// The fused partition kernels of the hot path (sm_100a):
+// The partition kernels of the hot path (sm_100a):
 //
+//   K_F root_filter_tma        the default root: polygon filter over every point
+//   KB' root_filtered_tma      one-pass octagon root (level 1 behind the filter)
 //   KB  root_partition_kernel  hull levels 1+2 fused over the caller's input
-//   K2  level_kernel           every live segment of one recursion level
+//   K2  level_kernel / level_tma  every live segment of one recursion level
 //
 // Both are the reference's extract_blocks (extract_core.hpp:421-515): f64
 // orientation test against two edges with mask_b &= ~mask_a (kernels.hpp:91),
