@@ -1762,6 +1762,146 @@ __global__ void __launch_bounds__(kCtlThreads, 3) root_filter_tma(FilterArgs a) 
 }
 
 // ===========================================================================
+// K2 for levels of many small segments (deep levels of circle-like inputs:
+// thousands of segments of a few tiles each): one CTA owns whole segments.
+// With no other CTA on the segment there is nothing to claim, publish or
+// reduce across CTAs: output places are running per-class counts (class 0
+// forward from the range start, class 1 backward from its end — the
+// two-sided layout), the farthest point of each class is the CTA's own
+// running best, and the CTA writes the two children itself
+// (hull.cpp:95-112).  Classification and order exactly as level_tma.
+// ===========================================================================
+constexpr uint32_t kSegCtaTiles = 16;
+
+struct SegCtaSmem {
+    uint32_t wc[2][kWarps];
+    uint32_t wex[2][kWarps];
+    uint32_t tot[2];
+    unsigned long long rkey[2][kWarps];
+    uint32_t ridx[2][kWarps];
+};
+
+template <bool GENERAL>
+__device__ __forceinline__ void level_segcta_body(const LevelArgs& a, uint32_t nseg, SegCtaSmem& S) {
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    for (uint32_t k = blockIdx.x; k < nseg; k += gridDim.x) {
+        const SegRec g = a.segs[k];
+        const double px = g.px, py = g.py, rx = g.rx, ry = g.ry, qx = g.qx, qy = g.qy;
+        const double adx = g.adx, ady = g.ady, bdx = g.bdx, bdy = g.bdy;
+        unsigned long long kb[2] = {kNoKey, kNoKey};
+        uint32_t ib[2] = {kNoIdx, kNoIdx};
+        uint32_t run0 = 0, run1 = 0;  // CTA-uniform running class counts
+        for (uint32_t j = 0; j < g.ntiles; ++j) {
+            const uint64_t start = g.begin + uint64_t(j) * kTile;
+            const uint32_t cnt = min(uint32_t(kTile), g.m - j * uint32_t(kTile));
+            int cls[kItems];
+            double ux[kItems], uy[kItems];
+            uint32_t uid[kItems], rk[kItems];
+            uint32_t wrun = 0;
+#pragma unroll
+            for (int i = 0; i < kItems; ++i) {
+                const uint32_t r = uint32_t(i) * kThreads + tid;
+                const bool v = r < cnt;
+                const double u = v ? __ldcs(a.ix + start + r) : 0.0;
+                const double w = v ? __ldcs(a.iy + start + r) : 0.0;
+                ux[i] = u;
+                uy[i] = w;
+                uid[i] = v ? __ldcs(a.iid + start + r) : 0u;
+                bool la, lb;
+                if (GENERAL) {
+                    la = left_diff(dsub(px, u), dsub(py, w), dsub(rx, u), dsub(ry, w));
+                    lb = !la && left_diff(dsub(g.bx, u), dsub(g.by, w), dsub(qx, u), dsub(qy, w));
+                } else {
+                    const double A = dsub(px, u), B = dsub(py, w);
+                    const double E = dsub(rx, u), F = dsub(ry, w);
+                    const double Cc = dsub(qx, u), D = dsub(qy, w);
+                    la = left_diff(A, B, E, F);
+                    lb = !la && left_diff(E, F, Cc, D);
+                }
+                const int c = !v ? 2 : (la ? 0 : (lb ? 1 : 2));
+                cls[i] = c;
+                rk[i] = warp_rank<2>(c, wrun);
+                const unsigned long long key = key_of(lat_off(c == 0 ? adx : bdx, c == 0 ? ady : bdy, u, w));
+                running_best<2>(kb, ib, c, key, uid[i], a.gx, a.gy);
+            }
+            if (lane < 2) S.wc[lane][warp] = wrun;
+            __syncthreads();
+            if (warp == 0) {  // per-class exclusive scan over the warps
+                const int c = (lane >> 3) & 1, w8 = lane & 7;
+                const uint32_t v = lane < 16 ? S.wc[c][w8] : 0u;
+                uint32_t incl = v;
+#pragma unroll
+                for (int d = 1; d < kWarps; d <<= 1) {
+                    const uint32_t o = __shfl_up_sync(kFull, incl, d, kWarps);
+                    if (w8 >= d) incl += o;
+                }
+                if (lane < 16) S.wex[c][w8] = incl - v;
+                if (lane == 7) S.tot[0] = incl;
+                if (lane == 15) S.tot[1] = incl;
+            }
+            __syncthreads();
+#pragma unroll
+            for (int i = 0; i < kItems; ++i) {
+                const int c = cls[i];
+                if (c < 2) {
+                    const uint32_t off = (c ? run1 : run0) + S.wex[c][warp] + rk[i];
+                    const uint64_t pos = c ? g.out + g.m - 1u - off : g.out + off;
+                    VQB_CHECK(pos < a.out_cap, 16, pos, a.out_cap);
+                    a.ox[pos] = ux[i];
+                    a.oy[pos] = uy[i];
+                    a.oid[pos] = uid[i];
+                }
+            }
+            run0 += S.tot[0];
+            run1 += S.tot[1];
+            __syncthreads();  // S reused by the next tile
+        }
+        // the segment's two children (farthest point: block reduction)
+        for (int c = 0; c < 2; ++c) {
+            unsigned long long kk = kb[c];
+            uint32_t ii = ib[c];
+            warp_key_best(kk, ii, a.gx, a.gy);
+            if (lane == 0) {
+                S.rkey[c][warp] = kk;
+                S.ridx[c][warp] = ii;
+            }
+        }
+        __syncthreads();
+        if (tid < 2) {
+            const int c = tid;
+            unsigned long long ko = S.rkey[c][0];
+            uint32_t io = S.ridx[c][0];
+            for (int w = 1; w < kWarps; ++w) {
+                const unsigned long long kk = S.rkey[c][w];
+                const uint32_t ii = S.ridx[c][w];
+                if (kk < ko || (kk == ko && key_better(kk, ii, ko, io, a.gx, a.gy))) {
+                    ko = kk;
+                    io = ii;
+                }
+            }
+            const Best b = best_from_key(ko, io, c == 0 ? adx : bdx, c == 0 ? ady : bdy, a.gx, a.gy);
+            const uint32_t m = c == 0 ? run0 : run1;
+            ChildRec ch;
+            if (c == 0) {  // left of p->r: triangle (p, rL, r)
+                ch.px = g.px; ch.py = g.py; ch.qx = g.rx; ch.qy = g.ry;
+                ch.begin = g.out;
+            } else {       // left of r->q: triangle (r, rR, q)
+                ch.px = GENERAL ? g.bx : g.rx; ch.py = GENERAL ? g.by : g.ry;
+                ch.qx = g.qx; ch.qy = g.qy;
+                ch.begin = g.out + g.m - m;
+            }
+            ch.rx = b.x;
+            ch.ry = b.y;
+            ch.r_idx = b.idx;
+            ch.m = m;
+            VQB_CHECK(2 * uint64_t(k) + c < a.children_cap, 58, k, a.children_cap);
+            a.children[2 * uint64_t(k) + c] = ch;
+        }
+        __syncthreads();  // S reused by the next segment
+    }
+}
+
+// ===========================================================================
 // K2 fast mode with a TMA ring (8 compute warps + 1 control warp).  The
 // control warp's lane 0 maps each upcoming tile of the CTA to its segment and
 // streams x, y and the indices into a kRing-deep shared-memory ring with
@@ -1786,6 +1926,16 @@ struct LevelRing {
 template <bool GENERAL>
 __global__ void __launch_bounds__(kCtlThreads, 3) level_tma(LevelArgs a) {
     VQB_PDL();
+    {
+        // many small segments (at most kSegCtaTiles tiles on average): one
+        // CTA per segment, no cross-CTA claims or partials (uniform branch)
+        const uint32_t nseg = a.info->nseg, nt = a.info->ntiles;
+        if (nseg >= gridDim.x && nt <= kSegCtaTiles * nseg) {
+            __shared__ SegCtaSmem SC;
+            if (threadIdx.x < kThreads) level_segcta_body<GENERAL>(a, nseg, SC);
+            return;
+        }
+    }
     extern __shared__ __align__(128) unsigned char dsm[];
     LevelRing& ring = *reinterpret_cast<LevelRing*>(dsm);
     __shared__ FastSmem S;
