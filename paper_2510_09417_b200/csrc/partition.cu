@@ -1949,8 +1949,11 @@ __global__ void __launch_bounds__(kCtlThreads, 3) level_tma(LevelArgs a) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t G = gridDim.x;
     auto issue = [&](uint32_t kk) {  // control lane: local tile kk -> stage kk % kRing
-        const uint32_t t = blockIdx.x + kk * G;
-        if (t >= s_ntiles) return;
+        // contiguous chunks of tiles per CTA: consecutive tiles of a CTA
+        // mostly share a segment (one partial per segment visit, not per tile)
+        const uint32_t chunk = (s_ntiles + G - 1) / G;
+        const uint32_t t = blockIdx.x * chunk + kk;
+        if (t >= s_ntiles || kk >= chunk) return;
         const int s = int(kk % kRing);
         const uint32_t sk = a.tile_seg[t];
         const SegRec g = a.segs[sk];
@@ -2059,7 +2062,9 @@ __global__ void __launch_bounds__(kCtlThreads, 3) level_tma(LevelArgs a) {
     };
 
     uint32_t kk = 0;
-    for (uint32_t t = blockIdx.x; t < ntiles; t += G, ++kk) {
+    const uint32_t chunk = (ntiles + G - 1) / G;
+    const uint32_t t_end = min(ntiles, (blockIdx.x + 1) * chunk);
+    for (uint32_t t = blockIdx.x * chunk; t < t_end; ++t, ++kk) {
         const int s = int(kk % kRing);
         // entering a new segment?  all threads decide on one snapshot
         const uint32_t k_now = ring.k[s], k_cur = s_cur_k;
