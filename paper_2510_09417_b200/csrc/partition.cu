@@ -1771,7 +1771,7 @@ __global__ void __launch_bounds__(kCtlThreads, 3) root_filter_tma(FilterArgs a) 
 // running best, and the CTA writes the two children itself
 // (hull.cpp:95-112).  Classification and order exactly as level_tma.
 // ===========================================================================
-constexpr uint32_t kSegCtaTiles = 16;
+constexpr uint32_t kSegCtaTiles = 4;
 
 struct SegCtaSmem {
     uint32_t wc[2][kWarps];
