@@ -56,7 +56,10 @@ struct RootPoly {
     // octagon |x - ocx| < ohx, |y - ocy| < ohy, |x - ocx| + |y - ocy| < od,
     // verified (its 8 vertices) to lie inside the filter region
     double ocx, ocy, ohx, ohy, od;
-    uint32_t oct_on;            // the octagon is tested (it covers clearly more than the box)
+    // disk |P - (dcx, dcy)|^2 < dr2 (radius: the distance to the nearest chord
+    // line, shrunk), by construction inside every chord's margin
+    double dcx, dcy, dr2;
+    uint32_t oct_on;            // K_F's fast inner test: 0 box, 1 box | octagon, 2 box | disk (the largest area)
     uint32_t pad2;
     double mref;                // M: max |coordinate| of the vertices (the margin is 2^-32 M)
 };

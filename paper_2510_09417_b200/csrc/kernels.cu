@@ -483,6 +483,7 @@ __device__ __noinline__ void poly_finish_warp(const PolyPartial& F, const double
     // the mean), the polygon's own extents in x, y and x +- y, scaled by the
     // largest s that keeps its 8 vertices inside every chord (closed form)
     double ocx = 0.0, ocy = 0.0, ohx = -1.0, ohy = -1.0, od = -1.0;  // empty: |.| < -1 never holds
+    double dcx = 0.0, dcy = 0.0, dr2 = -1.0;                           // empty disk
     {
         const bool have_box = bx0 < bx1;
         const double cx = have_box ? 0.5 * (bx0 + bx1) : mx, cy = have_box ? 0.5 * (by0 + by1) : my;
@@ -507,6 +508,35 @@ __device__ __noinline__ void poly_finish_warp(const PolyPartial& F, const double
                     break;
                 }
             }
+            // the disk around (cx, cy): radius = 0.999 x the distance to the
+            // nearest chord line, ft - f0 being the chord's slack at the centre.
+            // A slack within 2^-40 of the operands' scale (rounding of f0) voids
+            // it.  For |P - C| < r: f_j(P) <= f_j(C) + |n_j| r < ft_j exactly,
+            // so the disk lies inside every chord's margin; the pass kernel
+            // tests fma(du, du, dw dw) < r^2 (1 - 2^-30), which bounds the true
+            // distance below r through its three roundings.
+            const double nrm = sqrt(fa * fa + fb * fb);
+            const double slack = ft - f0;
+            const double scale = fabs(fa * cx) + fabs(fb * cy) + fabs(fc);
+            const double rj = deg ? kInf : (nrm > 0.0 && slack > 0x1p-40 * scale ? slack / nrm : -1.0);
+            const double r = 0.999 * wmin(rj);
+            if (r > 0.0 && r < kInf) {
+                // belt and braces: 64 points of the circle (two per lane) pass
+                // every chord
+                bool circ = true;
+                for (int h2 = 0; h2 < 2; ++h2) {
+                    double sn, cs;
+                    sincospi(double(lane + 32 * h2) / 32.0, &sn, &cs);
+                    const double x = cx + r * cs, y = cy + r * sn;
+#pragma unroll 4
+                    for (int q = 0; q < kPolyV; ++q) {
+                        const double a = __shfl_sync(kFull, fa, q), b = __shfl_sync(kFull, fb, q);
+                        const double c = __shfl_sync(kFull, fc, q), t = __shfl_sync(kFull, ft, q);
+                        circ &= __fma_rn(a, x, __fma_rn(b, y, c)) < t;
+                    }
+                }
+                if (__all_sync(kFull, circ)) { dcx = cx; dcy = cy; dr2 = r * r * (1.0 - 0x1p-30); }
+            }
         }
     }
     ok &= chords >= 2;  // all vertices equal: the test would constrain nothing
@@ -519,11 +549,14 @@ __device__ __noinline__ void poly_finish_warp(const PolyPartial& F, const double
     P.mref = M;
     P.bx0 = bx0; P.bx1 = bx1; P.by0 = by0; P.by1 = by1;
     P.ocx = ocx; P.ocy = ocy; P.ohx = ohx; P.ohy = ohy; P.od = od;
+    P.dcx = dcx; P.dcy = dcy; P.dr2 = dr2;
     {
         const double box_area = bx0 < bx1 ? (bx1 - bx0) * (by1 - by0) : 0.0;
         const double cut = fmax(0.0, ohx + ohy - od);
         const double oct_area = ohx > 0.0 ? 4.0 * ohx * ohy - 2.0 * cut * cut : 0.0;
-        P.oct_on = oct_area > 1.02 * box_area ? 1u : 0u;
+        const double disk_area = dr2 > 0.0 ? 3.14159 * dr2 : 0.0;
+        // the inner test that adds the most area (a uniform choice per call)
+        P.oct_on = disk_area > 1.02 * fmax(oct_area, box_area) ? 2u : (oct_area > 1.02 * box_area ? 1u : 0u);
         P.pad2 = 0u;
     }
     P.filter = ok ? 1u : 0u;

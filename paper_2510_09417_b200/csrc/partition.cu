@@ -1581,7 +1581,7 @@ __global__ void __launch_bounds__(kCtlThreads, 3) root_filter_tma(FilterArgs a) 
         }
     } else {
         // ---- compute warps: every warp owns 128 points of a tile (4 per lane)
-        const bool oct = P.filter != 0 && P.oct_on != 0;
+        const uint32_t mode = P.filter != 0 ? P.oct_on : 0u;
         const bool filter = P.filter != 0;
         const double bx0 = filter ? P.bx0 : kInf, bx1 = filter ? P.bx1 : -kInf;
         const double by0 = filter ? P.by0 : kInf, by1 = filter ? P.by1 : -kInf;
@@ -1618,41 +1618,37 @@ __global__ void __launch_bounds__(kCtlThreads, 3) root_filter_tma(FilterArgs a) 
                 }
                 __syncwarp();
             }
-            // phase A: strictly inside the inner box, or (when it adds
-            // coverage, a uniform choice) inside the inner octagon -> dropped
+            // phase A: strictly inside the inner box, or (a uniform choice,
+            // when it adds coverage) inside the inner octagon or disk -> dropped
             uint32_t qn = 0;
-            if (oct) {
+            auto phase_a = [&](auto inner) {
 #pragma unroll
                 for (int i = 0; i < kItems; ++i) {
                     const uint32_t idx = uint32_t(i) * kThreads + tid;
                     const double u = ring.x[s][idx], w = ring.y[s][idx];
-                    const double du = fabs(u - P.ocx), dw = fabs(w - P.ocy);
-                    const bool in = ((u > bx0) & (u < bx1) & (w > by0) & (w < by1)) |
-                                    ((du < P.ohx) & (dw < P.ohy) & (du + dw < P.od));
+                    const bool in = ((u > bx0) & (u < bx1) & (w > by0) & (w < by1)) | inner(u, w);
                     const bool need = (tbase + idx < n) & !in;
                     const unsigned b = __ballot_sync(kFull, need);
                     if (need) s_q[warp][qn + __popc(b & lt)] = uint16_t(idx);
                     qn += __popc(b);
                 }
+            };
+            if (mode >= 2u) {
+                phase_a([&](double u, double w) {
+                    const double du = u - P.dcx, dw = w - P.dcy;
+                    return __fma_rn(du, du, __dmul_rn(dw, dw)) < P.dr2;
+                });
+            } else if (mode == 1u) {
+                phase_a([&](double u, double w) {
+                    const double du = fabs(u - P.ocx), dw = fabs(w - P.ocy);
+                    return (du < P.ohx) & (dw < P.ohy) & (du + dw < P.od);
+                });
             } else {
-#pragma unroll
-                for (int i = 0; i < kItems; ++i) {
-                    const uint32_t idx = uint32_t(i) * kThreads + tid;
-                    const double u = ring.x[s][idx], w = ring.y[s][idx];
-                    const bool need = (tbase + idx < n) & !((u > bx0) & (u < bx1) & (w > by0) & (w < by1));
-                    const unsigned b = __ballot_sync(kFull, need);
-                    if (need) s_q[warp][qn + __popc(b & lt)] = uint16_t(idx);
-                    qn += __popc(b);
-                }
+                phase_a([](double, double) { return false; });
             }
-            __syncwarp();
-            const uint32_t qn2 = qn;
-            // phase C: the chord test for the rest, densely, 32 at a time
+            // phase C: the chord test for the rest, 32 at a time
             uint32_t sn = 0;
-            for (uint32_t r0 = 0; r0 < qn2; r0 += 32) {
-                const uint32_t j = r0 + lane;
-                const bool valid = j < qn2;
-                const uint32_t idx = valid ? s_q[warp][j] : 0u;
+            auto chord_round = [&](uint32_t idx, bool valid) {
                 const double u = ring.x[s][idx], w = ring.y[s][idx];
                 bool keep = false;
                 if (valid) {
@@ -1679,6 +1675,11 @@ __global__ void __launch_bounds__(kCtlThreads, 3) root_filter_tma(FilterArgs a) 
                     amax = fmax(amax, fmax(fabs(u), fabs(w)));
                 }
                 sn += __popc(b);
+            };
+            __syncwarp();
+            for (uint32_t r0 = 0; r0 < qn; r0 += 32) {
+                const uint32_t j = r0 + lane;
+                chord_round(j < qn ? s_q[warp][j] : 0u, j < qn);
             }
             if (lane == 0) s_cnt[par][warp] = sn;
             named_arrive<1>(par, kCtlThreads);
