@@ -1582,6 +1582,7 @@ __global__ void __launch_bounds__(kCtlThreads, 3) root_filter_tma(FilterArgs a) 
     } else {
         // ---- compute warps: every warp owns 128 points of a tile (4 per lane)
         const uint32_t mode = P.filter != 0 ? P.oct_on : 0u;
+        const double alim = 0x1p12 * P.mref;
         const bool filter = P.filter != 0;
         const double bx0 = filter ? P.bx0 : kInf, bx1 = filter ? P.bx1 : -kInf;
         const double by0 = filter ? P.by0 : kInf, by1 = filter ? P.by1 : -kInf;
@@ -1672,7 +1673,8 @@ __global__ void __launch_bounds__(kCtlThreads, 3) root_filter_tma(FilterArgs a) 
                         const ExtKey c{u, w, tbase + idx, 1u};
                         if (hi_better(c, hi)) hi = c;
                     }
-                    amax = fmax(amax, fmax(fabs(u), fabs(w)));
+                    // only whether it exceeds 2^12 M matters (the unsafe flag)
+                    if ((fabs(u) > alim) | (fabs(w) > alim)) amax = kInf;
                 }
                 sn += __popc(b);
             };
