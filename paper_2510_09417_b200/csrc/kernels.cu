@@ -521,21 +521,7 @@ __device__ __noinline__ void poly_finish_warp(const PolyPartial& F, const double
             const double rj = deg ? kInf : (nrm > 0.0 && slack > 0x1p-40 * scale ? slack / nrm : -1.0);
             const double r = 0.999 * wmin(rj);
             if (r > 0.0 && r < kInf) {
-                // belt and braces: 64 points of the circle (two per lane) pass
-                // every chord
-                bool circ = true;
-                for (int h2 = 0; h2 < 2; ++h2) {
-                    double sn, cs;
-                    sincospi(double(lane + 32 * h2) / 32.0, &sn, &cs);
-                    const double x = cx + r * cs, y = cy + r * sn;
-#pragma unroll 4
-                    for (int q = 0; q < kPolyV; ++q) {
-                        const double a = __shfl_sync(kFull, fa, q), b = __shfl_sync(kFull, fb, q);
-                        const double c = __shfl_sync(kFull, fc, q), t = __shfl_sync(kFull, ft, q);
-                        circ &= __fma_rn(a, x, __fma_rn(b, y, c)) < t;
-                    }
-                }
-                if (__all_sync(kFull, circ)) { dcx = cx; dcy = cy; dr2 = r * r * (1.0 - 0x1p-30); }
+                dcx = cx; dcy = cy; dr2 = r * r * (1.0 - 0x1p-30);
             }
         }
     }
