@@ -143,6 +143,14 @@ int vqhull_cuda_set_root_reference(int reference);
  * Returns 1 for another mode.  VQHULL_ROOT=octagon|reference sets 1|2. */
 int vqhull_cuda_set_root_mode(int mode);
 
+/* The filter pass's fast inner test (a drop region verified inside the
+ * filter polygon, tested before the chord test): -1 = automatic (the sample
+ * pass picks the region of largest area, default), 0 = the box only,
+ * 1 = box | octagon, 2 = box | disk (a forced region that does not exist for
+ * the input falls back to the automatic choice).  The hull never depends on
+ * it; tests use it to show that.  Returns VQHULL_EINVAL outside -1..2. */
+int vqhull_cuda_set_filter_inner(int mode);
+
 /* Frees this thread's device engine buffers (points, level tables) and
  * trims the memory pool; the next call re-allocates.  For callers that need
  * the device memory back between hulls. */

@@ -101,6 +101,7 @@ def lib() -> C.CDLL:
         L.vqhull_cuda_set_stable.argtypes = [C.c_int]
         L.vqhull_cuda_set_root_reference.argtypes = [C.c_int]
         L.vqhull_cuda_set_root_mode.argtypes = [C.c_int]
+        L.vqhull_cuda_set_filter_inner.argtypes = [C.c_int]
         L.vqhull_cuda_trim.argtypes = []
         L.vqhull_cuda_last_error.restype = C.c_char_p
         L.vqhull_b200_version.restype = C.c_char_p
@@ -273,6 +274,16 @@ def set_root_mode(mode: str) -> None:
     pass) or "reference" (find_extremes, bootstrap, fused levels 1+2).  Same
     hull in every mode."""
     _check(lib().vqhull_cuda_set_root_mode(ROOT_MODES[mode]), "vqhull_cuda_set_root_mode")
+
+
+FILTER_INNER = {"auto": -1, "box": 0, "octagon": 1, "disk": 2}
+
+
+def set_filter_inner(mode: str) -> None:
+    """The filter pass's fast inner test: "auto" (default: the sample pass
+    picks the largest region), or force "box", "octagon" or "disk".  Same
+    hull (and, on ordinary inputs, the same survivors) in every mode."""
+    _check(lib().vqhull_cuda_set_filter_inner(FILTER_INNER[mode]), "vqhull_cuda_set_filter_inner")
 
 
 def set_timing(on: bool) -> None:

@@ -1275,6 +1275,18 @@ int vqhull_cuda_set_root_mode(int mode) {
     }
 }
 
+int vqhull_cuda_set_filter_inner(int mode) {
+    if (mode < -1 || mode > 2) return VQHULL_EINVAL;
+    try {
+        Engine& e = vqb::engine();
+        std::lock_guard<std::mutex> lk(e.mutex());
+        vqb::set_filter_inner(mode);
+        return 0;
+    } catch (const CudaError&) {
+        return VQHULL_ECUDA;
+    }
+}
+
 int vqhull_cuda_set_root_reference(int reference) {
     try {
         Engine& e = vqb::engine();

@@ -394,6 +394,8 @@ constexpr int kSampleUnroll = 4;  // double2 loads per array per thread in fligh
 // 2^-400 <= M <= 2^500 (products could underflow/overflow): no filter.
 // One warp: lane l owns vertex / chord j = l & 15 (each twice) and a share of
 // the inside-tests, so a candidate region costs a few FMAs and one vote.
+__device__ int g_inner_force = -1;  // set_filter_inner
+
 __device__ __noinline__ void poly_finish_warp(const PolyPartial& F, const double* __restrict__ xs,
                                               const double* __restrict__ ys, RootInfo* root, bool with_pq) {
     const double kInf = __longlong_as_double(0x7ff0000000000000ll);
@@ -543,6 +545,8 @@ __device__ __noinline__ void poly_finish_warp(const PolyPartial& F, const double
         const double disk_area = dr2 > 0.0 ? 3.14159 * dr2 : 0.0;
         // the inner test that adds the most area (a uniform choice per call)
         P.oct_on = disk_area > 1.02 * fmax(oct_area, box_area) ? 2u : (oct_area > 1.02 * box_area ? 1u : 0u);
+        const int f = g_inner_force;  // test knob: a forced choice, when that region exists
+        if (f == 0 || (f == 1 && ohx > 0.0) || (f == 2 && dr2 > 0.0)) P.oct_on = uint32_t(f);
         P.pad2 = 0u;
     }
     P.filter = ok ? 1u : 0u;
@@ -1906,4 +1910,6 @@ uint32_t read_and_clear_fault() {
     }
     return v;
 }
+void set_filter_inner(int mode) { cudaMemcpyToSymbol(g_inner_force, &mode, sizeof mode); }
+
 }  // namespace vqb

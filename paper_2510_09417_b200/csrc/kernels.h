@@ -61,6 +61,7 @@ int occupancy_extremes();
 int occupancy_bootstrap();
 uint32_t read_and_clear_fault();
 uint32_t* fault_word_ptr();  // device address of the fault word (async copies)
+void set_filter_inner(int mode);  // -1 auto (K_S picks), else force 0 box / 1 octagon / 2 disk when valid
 void launch_tiny(const TinyArgs& a, cudaStream_t st);
 size_t tail_smem_bytes();
 int occupancy_tail();

@@ -324,6 +324,28 @@ def test_root_modes_agree(vq, cuda, oracle):
             assert np.array_equal(a, b), f"case {i}: n={len(xs)} mode={mode}"
 
 
+def test_filter_inner_modes_agree(vq, cuda):
+    """The filter pass's fast inner region (box, octagon or disk — normally
+    the sample pass picks the largest) only decides which points reach the
+    chord test: every forced choice gives the same survivors and the same
+    hull.  The disk is the one derived in closed form."""
+    for kind, n, seed in (("disk", 2_000_000, 5), ("square", 2_000_000, 2), ("kuzmin", 2_000_000, 4),
+                          ("disk", 10_000_000, 1), ("circle", 2_000_000, 3)):
+        xs, ys = vq.generate(kind, n, seed)
+        a = gpu_indices(vq, xs, ys)
+        s0 = vq.stats()
+        assert s0["root_filtered"] == 2
+        for mode in ("box", "octagon", "disk"):
+            vq.set_filter_inner(mode)
+            try:
+                b = gpu_indices(vq, xs, ys)
+                s1 = vq.stats()
+            finally:
+                vq.set_filter_inner("auto")
+            assert np.array_equal(a, b), f"{kind} n={n}: inner={mode}"
+            assert s1["survivors_root"] == s0["survivors_root"], f"{kind} n={n}: inner={mode}"
+
+
 def test_root_mode_selection(vq, cuda):
     xs, ys = vq.generate("square", 1_000_000, 2)
     vq.hull_indices(xs, ys)
