@@ -1149,7 +1149,7 @@ class Engine {
     std::deque<LevelTables> levels_;  // deque: references stay valid on growth
     std::vector<LevelInfo> hinfo_;  // host copies of the level infos (after the last batch)
     int lmax_ = 2;
-    static constexpr int kLevelBatch = 4;  // levels queued per host synchronization
+    static constexpr int kLevelBatch = 8;  // levels queued per host synchronization (4: disk 1e8 +2 %, 16: +6 %)
     static constexpr uint64_t kLeanN = 1ull << 29;
     static constexpr uint64_t kEmitSmallSlots = 1u << 14;  // trees this small: one emission kernel  // above: exact per-level sizing (one sync per level)
     uint32_t epoch_ = 0;
