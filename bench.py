@@ -55,6 +55,8 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--profile", action="store_true", help="minimal run for ncu (no extras)")
+    p.add_argument("--csv", default="", help="also write one row per timed step in the reference's "
+                   "CSV schema (bench.cpp:156-160) to this path (rank 0)")
     return p.parse_args()
 
 
@@ -302,9 +304,11 @@ def run_ours(args):
     fam = {"extremes": [0.0, 0], "bootstrap": [0.0, 0], "root_partition": [0.0, 0],
            "levels": [0.0, 0], "finisher": [0.0, 0]}
     st = {}
+    rep_rows = []  # (seconds, bytes_moved) per step, for --csv
     for _ in range(args.steps):
         step()
         st = vq.stats()
+        rep_rows.append((st["ms_total"] / 1e3, int(st["bytes_moved"])))
         for k in fam:
             fam[k][0] += st[f"ms_{k}"]
             fam[k][1] += st[f"bytes_{k}"]
@@ -380,11 +384,42 @@ def run_ours(args):
         except Exception as e:  # never lose the GPU line over the baseline
             result["cpu_baseline"] = {"value": None, "unit": "points/s", "cores": None,
                                       "kind": "reference", "sample": f"failed: {e}"}
+    if rank == 0 and args.csv:
+        write_csv(args.csv, kind, points_total, seed, world, rep_rows, h, peak)
     if rank == 0:
         emit(result)
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+CSV_HEADER = ("kind,n,seed,workers,block_size,lanes,simd,write_combining,reps,"
+              "rep,seconds,mean_seconds,stddev_seconds,model_bytes,"
+              "bandwidth_gbps,baseline_gbps,hull_vertices,joules")
+
+
+def write_csv(path, kind, n, seed, workers, rep_rows, h, peak_gbs):
+    """The reference's bench CSV (header: bench.cpp:156-160, rows: :162-199),
+    one row per timed step.  Column meaning on the GPU: workers = GPUs,
+    block_size = points per tile, lanes = threads per warp, simd = sm_100a,
+    seconds = the hull's device time (CUDA events in the library),
+    model_bytes = the device byte model (vqhull_stats.bytes_moved, DESIGN.md
+    §9 — the algorithmic bytes of OUR kernels, not the reference's traced
+    extraction bytes), baseline_gbps = the measured HBM copy peak standing in
+    for the STREAM Scale baseline, joules left empty as in the reference."""
+    import statistics
+    secs = [r[0] for r in rep_rows]
+    mean = statistics.fmean(secs) if secs else 0.0
+    # shortest round-trip numbers, as append_number's std::to_chars (bench.cpp:91-95);
+    # the reference's stddev_of is the sample deviation (n - 1), 0 for one rep
+    sd = statistics.stdev(secs) if len(secs) > 1 else 0.0
+    mb = rep_rows[-1][1] if rep_rows else 0
+    bw = mb / mean / 1e9 if mean > 0 else 0.0
+    with open(path, "w") as f:
+        f.write(CSV_HEADER + "\n")
+        for i, (sec, _) in enumerate(rep_rows):
+            f.write(f"{kind},{n},{seed},{workers},1024,32,sm_100a,0,{len(rep_rows)},{i + 1},"
+                    f"{sec!r},{mean!r},{sd!r},{mb},{bw!r},{float(peak_gbs)!r},{h},\n")
 
 
 def main():
