@@ -12,15 +12,23 @@ format (``pbbs_sequencePoint2d``) is out of scope.
 from __future__ import annotations
 
 import os
+import re
 import struct
 from typing import Tuple
 
 import numpy as np
 
 MAGIC = b"VQH1"
+TEXT_HEADER = "pbbs_sequencePoint2d"
 HEADER_BYTES = 12
 
-__all__ = ["LoadError", "MAGIC", "save_vqh1", "load_vqh1", "load_vqh1_device"]
+__all__ = ["LoadError", "MAGIC", "TEXT_HEADER", "save_vqh1", "load_vqh1", "load_vqh1_device",
+           "format_for_path", "read_points", "write_points", "to_chars"]
+
+
+# what std::from_chars(double) accepts (general format): no leading '+', no
+# hex; inf / nan spellings parse and are then rejected by the finiteness check
+_NUM = re.compile(r"-?(?:(?:\d+\.?\d*|\.\d+)(?:[eE][+-]?\d+)?|(?i:inf(?:inity)?|nan(?:\([0-9A-Za-z_]*\))?))")
 
 
 class LoadError(ValueError):
@@ -116,3 +124,95 @@ def load_vqh1_device(path: str, device="cuda", stream=None):
     finally:
         s.synchronize()
     return X, Y
+
+
+# ---- text format and format dispatch ------------------------------------
+
+def to_chars(v: float) -> str:
+    """``std::to_chars(double)`` without a format: the shortest round-trip
+    digits (Python's ``repr`` finds the same ones), printed fixed or
+    scientific (``e±dd``) whichever is shorter, fixed on a tie; an integral
+    value in fixed form prints exactly.  Pinned by tests/golden/to_chars.txt
+    (libstdc++'s own output, tests/golden/make_to_chars.cpp)."""
+    from decimal import Decimal
+
+    v = float(v)
+    neg = v < 0 or (v == 0 and str(v).startswith("-"))
+    if v == 0:
+        return "-0" if neg else "0"
+    _, dig, exp = Decimal(repr(abs(v))).as_tuple()
+    ds = "".join(map(str, dig)).lstrip("0")
+    t = len(ds) - len(ds.rstrip("0"))
+    ds, exp = ds[:len(ds) - t], exp + t
+    k = len(ds)
+    x = exp + k - 1  # value = d.ddd x 10^x
+    sci = ds[0] + ("." + ds[1:] if k > 1 else "") + ("e-" if x < 0 else "e+") + f"{abs(x):02d}"
+    if x >= k - 1:  # an integer: fixed form prints its exact digits, as printf("%.0f")
+        fix = str(int(abs(v)))
+    elif x >= 0:
+        fix = ds[:x + 1] + "." + ds[x + 1:]
+    else:
+        fix = "0." + "0" * (-x - 1) + ds
+    out = fix if len(fix) <= len(sci) else sci
+    return "-" + out if neg else out
+
+
+def format_for_path(path: str) -> str:
+    """``"text"`` for ``.txt`` / ``.pbbs``, else ``"binary"`` (``io.cpp:91-98``)."""
+    dot = path.rfind(".")
+    return "text" if dot >= 0 and path[dot:] in (".txt", ".pbbs") else "binary"
+
+
+def _read_text(path: str) -> Tuple[np.ndarray, np.ndarray]:
+    with _open(path, "rb") as f:
+        lines = f.read().decode("latin-1").split("\n")
+    if not lines or (len(lines) == 1 and lines[0] == ""):
+        raise LoadError(f"{path}: empty file")
+    head = lines[0][:-1] if lines[0].endswith("\r") else lines[0]
+    if head != TEXT_HEADER:
+        raise LoadError(f'{path}: unrecognized header "{head}"')
+    xs, ys = [], []
+    if lines[-1] == "":
+        lines.pop()
+    for lineno, line in enumerate(lines[1:], start=2):
+        if line.endswith("\r"):
+            line = line[:-1]
+        if not line:
+            continue
+        vals, cur = [], 0
+        for _ in range(2):  # from_chars after skipping spaces/tabs; the rest of the line is ignored
+            while cur < len(line) and line[cur] in " \t":
+                cur += 1
+            m = _NUM.match(line, cur)
+            if not m:
+                raise LoadError(f"{path}: malformed coordinate on line {lineno}")
+            vals.append(float(m.group(0)))
+            cur = m.end()
+        xs.append(vals[0])
+        ys.append(vals[1])
+    xs = np.array(xs, dtype=np.float64)
+    ys = np.array(ys, dtype=np.float64)
+    _check_finite(path, xs, ys)
+    return xs, ys
+
+
+def read_points(path: str) -> Tuple[np.ndarray, np.ndarray]:
+    """The reference's ``read_points``: VQH1 if the file starts with the
+    magic, else the text format (``io.cpp:134-144``)."""
+    with _open(path, "rb") as f:
+        binary = f.read(4) == MAGIC
+    return load_vqh1(path) if binary else _read_text(path)
+
+
+def write_points(path: str, xs, ys, fmt: str = "") -> None:
+    """The reference's ``write_points``; ``fmt`` defaults to
+    :func:`format_for_path`."""
+    fmt = fmt or format_for_path(path)
+    if fmt != "text":
+        save_vqh1(path, xs, ys)
+        return
+    xs = np.asarray(xs, dtype=np.float64)
+    ys = np.asarray(ys, dtype=np.float64)
+    body = "".join(f"{to_chars(a)} {to_chars(b)}\n" for a, b in zip(xs.tolist(), ys.tolist()))
+    with _open(path, "wb") as f:
+        f.write((TEXT_HEADER + "\n" + body).encode("ascii"))

@@ -73,3 +73,78 @@ def test_device_load_then_hull(tmp_path):
     save_vqh1(str(p), xs, ys)
     with pytest.raises(LoadError, match="point 3"):
         load_vqh1_device(str(p))
+
+
+# ---- text format (io.cpp:26-65, 100-121; test_dataset_io.cpp:122-206) ----
+
+from paper_2510_09417_b200.io import format_for_path, read_points, to_chars, write_points  # noqa: E402
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "to_chars.txt")
+
+
+def test_to_chars_matches_libstdcxx_golden():
+    n = 0
+    with open(GOLDEN) as f:
+        for line in f:
+            h, want = line.split()
+            v = struct.unpack("<d", bytes.fromhex(h)[::-1])[0]
+            assert to_chars(v) == want, (h, want)
+            n += 1
+    assert n > 5000
+
+
+@pytest.mark.parametrize("ext", [".txt", ".pbbs", ".bin"])
+def test_text_and_binary_round_trips_byte_identical(tmp_path, ext):
+    xs, ys = _pts(500, 3)
+    xs[:4] = [0.0, -0.0, 1e22, 123456.0]
+    a, b = tmp_path / ("a" + ext), tmp_path / ("b" + ext)
+    write_points(str(a), xs, ys)
+    x2, y2 = read_points(str(a))
+    assert np.array_equal(x2, xs) and np.array_equal(y2, ys)
+    write_points(str(b), x2, y2)
+    assert a.read_bytes() == b.read_bytes()
+    if ext != ".bin":
+        assert a.read_bytes().startswith(b"pbbs_sequencePoint2d\n")
+
+
+def test_text_and_binary_loads_equal(tmp_path):
+    xs, ys = _pts(300, 4)
+    write_points(str(tmp_path / "x.txt"), xs, ys)
+    write_points(str(tmp_path / "x.bin"), xs, ys)
+    t = read_points(str(tmp_path / "x.txt"))
+    b = read_points(str(tmp_path / "x.bin"))
+    assert np.array_equal(t[0], b[0]) and np.array_equal(t[1], b[1])
+
+
+def test_text_empty_set_and_crlf(tmp_path):
+    p = tmp_path / "e.txt"
+    write_points(str(p), np.empty(0), np.empty(0))
+    assert p.read_bytes() == b"pbbs_sequencePoint2d\n"
+    assert read_points(str(p))[0].size == 0
+    p.write_bytes(b"pbbs_sequencePoint2d\r\n1 2\r\n\r\n\t-3.5   4e-1\r\n")
+    xs, ys = read_points(str(p))
+    assert xs.tolist() == [1.0, -3.5] and ys.tolist() == [2.0, 0.4]
+
+
+def test_text_malformed(tmp_path):
+    p = tmp_path / "m.txt"
+    p.write_bytes(b"")
+    with pytest.raises(LoadError, match="empty file"):
+        read_points(str(p))
+    p.write_bytes(b"not_a_header\n1 2\n")
+    with pytest.raises(LoadError, match='unrecognized header "not_a_header"'):
+        read_points(str(p))
+    p.write_bytes(b"pbbs_sequencePoint2d\n1 2\n3 x\n")
+    with pytest.raises(LoadError, match="malformed coordinate on line 3"):
+        read_points(str(p))
+    p.write_bytes(b"pbbs_sequencePoint2d\n1 2\n3 inf\n")
+    with pytest.raises(LoadError, match="non-finite coordinate at point 1"):
+        read_points(str(p))
+
+
+def test_format_for_path():
+    assert format_for_path("points.txt") == "text"
+    assert format_for_path("points.pbbs") == "text"
+    assert format_for_path("points.bin") == "binary"
+    assert format_for_path("points") == "binary"
+    assert format_for_path("dir.txt/points") == "binary"
