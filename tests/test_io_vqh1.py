@@ -148,3 +148,17 @@ def test_format_for_path():
     assert format_for_path("points.bin") == "binary"
     assert format_for_path("points") == "binary"
     assert format_for_path("dir.txt/points") == "binary"
+
+
+def test_text_writer_matches_reference_library(tmp_path):
+    """ref_points.txt was written by the reference's own write_points
+    (tests/golden/make_ref_text.py) from ref_points.bin."""
+    g = os.path.dirname(GOLDEN)
+    xs, ys = read_points(os.path.join(g, "ref_points.bin"))
+    out = tmp_path / "ours.txt"
+    write_points(str(out), xs, ys)
+    with open(os.path.join(g, "ref_points.txt"), "rb") as f:
+        assert out.read_bytes() == f.read()
+    t = read_points(os.path.join(g, "ref_points.txt"))
+    assert np.array_equal(t[0], xs) and np.array_equal(t[1], ys)
+    assert np.array_equal(np.signbit(t[0]), np.signbit(xs))
