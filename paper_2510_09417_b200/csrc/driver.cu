@@ -137,6 +137,8 @@ class Engine {
         grid_ext_ = sms_ * std::max(1, std::min(8, occupancy_extremes()));
         grid_boot_ = sms_ * std::max(1, std::min(8, occupancy_bootstrap()));
         grid_poly_ = sms_ * std::max(1, std::min(8, occupancy_poly_sample()));
+        if (const char* e = getenv("VQHULL_POLY_OCC"))  // experiments: K_S CTAs per SM
+            grid_poly_ = sms_ * std::max(1, std::min(atoi(e), occupancy_poly_sample()));
         stream_grid_ = std::max(std::max(grid_ext_, grid_boot_), grid_poly_);
         VQB_TRACE("engine: allocations");
         ck(cudaMalloc(&ctrs_, 64 * sizeof(uint32_t)), "cudaMalloc ctrs");
