@@ -1,31 +1,45 @@
 #!/usr/bin/env python
 """bench.py — VQhull hot path on B200 (driver contract).
 
-Workload (BASELINE.json configs[1]): N = 1e8 float64 points uniform in the
-square [-1, 1]^2, seed 2; one "step" = one full hull (extremes, fused
-partition + arg-max levels, recursion, clockwise first-occurrence index
-list) over one batch.  With --gpus N (torchrun, one process per GPU) every
-rank hulls its own 1e8-point contiguous shard of the global seed-2 stream
-(weak scaling) and the ranks merge through one NCCL all-gather of the
-candidate vertices (paper_2510_09417_b200/distributed.py).
+One "step" = one full hull (sample polygon, filter pass, fused partition +
+arg-max levels, recursion, clockwise first-occurrence index list) over one
+batch of the workload.  Workloads (BASELINE.json configs):
 
-  value : whole-job points/s with inputs resident in HBM (device-timed, CUDA
-          events, max over ranks; inputs 1.6 GB/GPU >> 126 MB L2, so no flush)
-  e2e   : points/s through the public API with HOST buffers (pinned), i.e.
-          vqhull_compute's H2D of the coordinates and D2H of the index list
-          inside the timed region
+  --gpus 1 (default)  config 2: 1e8 f64 points uniform in [-1, 1]^2, seed 2
+                      (BASELINE configs[1], "single B200").
+  --gpus N > 1        config 5: 4e9 f64 points uniform in the unit disk,
+                      seed 5, sharded evenly over the N GPUs (strong
+                      scaling): per rank the local hull and its certified
+                      candidates, one NCCL all-gather, the merge hull
+                      (paper_2510_09417_b200/distributed.py).
+  --config K          any BASELINE config (1-4 weak-scaled per GPU at N > 1).
+
+With --gpus N > 1 and no torchrun environment, bench.py relaunches itself
+through torch.distributed.run (one process per GPU, 127.0.0.1); it refuses to
+run when fewer than N GPUs are visible.
+
+  value    : whole-job points/s, inputs resident in HBM (CUDA events on the
+             launching stream, max over ranks)
+  e2e      : points/s through the public API with HOST buffers: the C ABI
+             vqhull_compute at N = 1 (pinned arrays; the pageable case is
+             reported beside it), per-rank H2D + sharded hull + D2H at N > 1
   roofline : the dominant kernel's algorithmic bytes / its CUDA-event time
   cpu_baseline : the reference library (oracle/_ref, compiled from the
-          reference sources) on this host's cores, same workload
+             reference sources) on this host's cores, bounded sample of the
+             same workload, workers = 1 and workers = nproc, plus the
+             reference's Scale baseline
 
 `--impl reference` times the reference's own CPU implementation of the path
-(convex_hull, all host threads) on the same config and prints the same line.
+(convex_hull, all host threads) on the same workload and prints the same
+line; it generates its inputs with the reference's own generators and never
+loads this repository's library.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import subprocess
 import sys
 import threading
@@ -43,22 +57,66 @@ CONFIGS = {
 }
 L2_BYTES = 126 * 2**20
 METRIC = "points/sec per hull (f64 2D) and achieved HBM GB/s vs peak"
+# the reference arm's bounded sample (host RAM and minutes): the first
+# REF_SAMPLE points of the workload's stream
+REF_SAMPLE = 4 * 10**8
 
 
-def parse():
+def parse(argv=None):
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    p.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
-    p.add_argument("--n", type=int, default=0, help="override points per rank")
+    p.add_argument("--config", type=int, default=0, choices=[0, *sorted(CONFIGS)],
+                   help="BASELINE config (default: 2 on one GPU, 5 sharded on N > 1)")
+    p.add_argument("--n", type=int, default=0, help="override the workload's point count")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--profile", action="store_true", help="minimal run for ncu (no extras)")
     p.add_argument("--csv", default="", help="also write one row per timed step in the reference's "
                    "CSV schema (bench.cpp:156-160) to this path (rank 0)")
-    return p.parse_args()
+    return p.parse_args(argv)
+
+
+class Workload:
+    """The one description both arms print (identical `config` objects)."""
+
+    def __init__(self, args, world: int):
+        cfg = args.config or (5 if world > 1 else 2)
+        kind, n, seed = CONFIGS[cfg]
+        if args.n:
+            n = args.n
+        self.cfg, self.kind, self.seed, self.world = cfg, kind, seed, world
+        # config 5 is defined sharded (strong scaling); configs 1-4 are
+        # single-GPU workloads, weak-scaled (n per GPU) when N > 1
+        self.strong = cfg == 5
+        self.total = n if self.strong else n * world
+        self.n_arg = n
+
+    def shard(self, rank: int):
+        """(offset, count) of this rank's contiguous shard."""
+        if self.strong:
+            base, rem = divmod(self.total, self.world)
+            return rank * base + min(rank, rem), base + (1 if rank < rem else 0)
+        return rank * self.n_arg, self.n_arg
+
+    @property
+    def name(self) -> str:
+        w = f"config{self.cfg}: {self.kind} seed={self.seed}, "
+        if self.strong:
+            w += f"n={self.total} total, sharded evenly over {self.world} GPU(s)"
+        elif self.world > 1:
+            w += f"n={self.n_arg} per GPU x {self.world} GPUs (contiguous ranges of one stream)"
+        else:
+            w += f"n={self.n_arg}"
+        if self.cfg == 2 and self.world == 1 and not self.strong:
+            w += " (BASELINE configs[1])"
+        return w
+
+    def config(self) -> dict:
+        return {"workload": self.name, "points_total": self.total, "n_gpus": self.world,
+                "parallelism": f"shard{self.world}" if self.world > 1 else "single GPU"}
 
 
 def peaks():
@@ -68,6 +126,17 @@ def peaks():
         return float(d["hbm_gbs"]), "measured"
     except Exception:
         return 6650.0, "fallback"
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 class Clocks:
@@ -116,97 +185,135 @@ class Clocks:
                 "samples": len(self.samples)}
 
 
-def cpu_reference_baseline(kind, n, seed, offset_ranks=1, budget_s=20.0, reps=None):
-    """The reference library (oracle/_ref) on this host: convex_hull with all
-    host threads, run_bench_points semantics (fresh copy per rep, hull timed)."""
-    import numpy as np
-
-    import paper_2510_09417_b200 as vq
-    from oracle import Oracle, Reference
-
-    threads = os.cpu_count() or 1
-    total = n * offset_ranks
-    m = min(total, 4 * 10**8)  # bounded sample (config 5: 4e9 points would need 128 GB host RAM)
-    xs, ys = vq.generate(kind, m, seed, threads=threads)
-    if Reference.available():
-        R = Reference()
-        secs, h = R.bench_hull(xs, ys, threads, 1)  # first rep calibrates
-        t = float(secs[0])
-        k = reps or max(1, min(5, int(budget_s / max(t, 1e-3))))
-        secs2, h = R.bench_hull(xs, ys, threads, k)
-        allsecs = np.concatenate([secs, secs2])
-        what = "full workload" if m == total else f"first {m} of {total} points"
-        return {"kind": "reference", "cores": threads, "seconds": allsecs.tolist(),
-                "value": m / float(np.mean(secs2)), "hull": int(h),
-                "sample": f"{what}: {kind} n={m} seed={seed}, "
-                          f"{len(secs2)} timed reps after 1 untimed, convex_hull workers={threads}"}
-    # oracle port (single thread): bounded sample
-    O = Oracle()
-    m = min(m, 10**7)
-    t0 = time.perf_counter()
-    O.convex_hull(xs[:m], ys[:m])
-    dt = time.perf_counter() - t0
-    return {"kind": "port", "cores": 1, "value": m / dt, "seconds": [dt],
-            "sample": f"first {m} points of {kind} seed={seed}, oracle convex_hull, 1 thread"}
-
-
 def emit(obj):
     print(json.dumps(obj), flush=True)
 
 
-def run_reference(args):
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    if rank != 0:
-        return 0
-    kind, n, seed = CONFIGS[args.config]
-    if args.n:
-        n = args.n
+def free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def relaunch(args) -> int:
+    """--gpus N > 1 outside torchrun: check the GPUs, then one process per GPU."""
+    import torch
+
+    have = torch.cuda.device_count() if torch.cuda.is_available() else 0
+    if have < args.gpus:
+        print(f"bench.py --gpus {args.gpus}: only {have} CUDA device(s) visible; refusing to run "
+              f"(a {args.gpus}-GPU line measured on {have} GPU(s) would be wrong)", file=sys.stderr)
+        return 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(free_port()), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.run(cmd).returncode
+
+
+# ---------------------------------------------------------------------------
+# reference arm and CPU baseline: the reference library only (oracle/_ref)
+# ---------------------------------------------------------------------------
+def _ref_inputs(R, wl: Workload, m: int, threads: int):
+    """The first m points of the workload's stream, from the reference's own
+    generators (dataset.cpp:58-75; square: its rng::uniform01)."""
+    if wl.kind == "square":
+        return R.generate_square(m, wl.seed, 0, threads)
+    return R.generate(wl.kind, m, wl.seed, threads)
+
+
+def reference_runs(wl: Workload, steps: int, warmup: int, workers: int, R=None, m=None):
     import numpy as np
 
-    import paper_2510_09417_b200 as vq
-    from oracle import Oracle, Reference
+    from oracle import Reference
 
+    R = R or Reference()
     threads = os.cpu_count() or 1
-    strong = args.config == 5 and not args.n
-    total = n if strong else n * world
-    xs, ys = vq.generate(kind, total, seed, threads=threads)
-    if Reference.available():
-        R = Reference()
-        R.bench_hull(xs, ys, threads, max(args.warmup, 0)) if args.warmup else None
-        secs, h = R.bench_hull(xs, ys, threads, args.steps)
-        kind_s, cores = "reference", threads
-        sample = (f"{kind} n={total} seed={seed}: {args.steps} timed convex_hull reps "
-                  f"(fresh copy each, hull timed), workers={threads}")
-    else:
-        O = Oracle()
-        secs = []
-        for _ in range(args.steps):
-            t0 = time.perf_counter()
-            O.convex_hull(xs, ys)
-            secs.append(time.perf_counter() - t0)
-        secs = np.array(secs)
-        kind_s, cores = "port", 1
-        sample = f"{kind} n={total} seed={seed}: oracle port, 1 thread"
-    mean = float(np.mean(secs))
-    value = total / mean
+    m = min(wl.total, REF_SAMPLE) if m is None else m
+    xs, ys = _ref_inputs(R, wl, m, threads)
+    if warmup:
+        R.bench_hull(xs, ys, workers, warmup)
+    secs, h = R.bench_hull(xs, ys, workers, steps)
+    what = "the full workload" if m == wl.total else f"the first {m} of {wl.total} points"
+    return np.asarray(secs), int(h), m, what
+
+
+def run_reference(args) -> int:
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    if rank != 0:
+        return 0
+    wl = Workload(args, world)
+    from oracle import Reference
+
+    if not Reference.available():
+        emit({"impl": "reference", "unavailable": "oracle/_ref/libvqhull_ref.so was not built"})
+        return 0
+    threads = os.cpu_count() or 1
+    secs, h, m, what = reference_runs(wl, args.steps, max(args.warmup, 0), threads)
+    mean = float(secs.mean())
+    value = m / mean
     emit({
         "metric": METRIC, "value": value, "unit": "points/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": mean * 1e3,
-        "higher_is_better": True, "scaling": "strong" if strong else "weak", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic (reference RNG, seeded)", "impl": "reference",
-        "config": {"workload": (f"config{args.config}: {kind} n={total} total, sharded, seed={seed}" if strong
-                                else f"config{args.config}: {kind} n={n} per GPU seed={seed}"),
-                   "points_total": total, "parallelism": f"host threads={cores}"},
-        "cpu_baseline": {"value": value, "unit": "points/s", "cores": cores, "kind": kind_s,
-                         "sample": sample},
-        "e2e": {"value": value, "unit": "points/s", "h2d_bytes_per_step": 0,
-                "d2h_bytes_per_step": 0},
+        "higher_is_better": True, "scaling": "strong" if wl.strong else "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (reference generators, seeded)", "impl": "reference",
+        "config": wl.config(),
+        "cpu_baseline": {"value": value, "unit": "points/s", "cores": threads, "kind": "reference",
+                         "cpu_model": cpu_model(),
+                         "sample": f"{what} ({wl.kind}, seed {wl.seed}): {args.steps} timed "
+                                   f"convex_hull reps after {args.warmup} untimed, fresh copy each, "
+                                   f"hull timed (run_bench_points), workers={threads}",
+                         "seconds": secs.tolist(), "hull_vertices_of_sample": h},
+        "e2e": {"value": value, "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     })
     return 0
 
 
-def run_ours(args):
+def cpu_reference_baseline(wl: Workload, budget_s: float = 20.0) -> dict:
+    """BASELINE.md §3 on this host: convex_hull at workers = nproc and
+    workers = 1 on a bounded sample of the workload, plus the Scale baseline."""
+    import numpy as np
+
+    from oracle import Oracle, Reference
+
+    threads = os.cpu_count() or 1
+    if not Reference.available():  # the oracle port, one thread, bounded sample
+        import paper_2510_09417_b200 as vq
+
+        m = min(wl.total, 10**7)
+        xs, ys = vq.generate(wl.kind, m, wl.seed)
+        t0 = time.perf_counter()
+        Oracle().convex_hull(xs, ys)
+        dt = time.perf_counter() - t0
+        return {"kind": "port", "cores": 1, "value": m / dt, "unit": "points/s",
+                "cpu_model": cpu_model(),
+                "sample": f"first {m} points of {wl.kind} seed {wl.seed}, oracle convex_hull, 1 thread"}
+    R = Reference()
+    m = min(wl.total, REF_SAMPLE)
+    xs, ys = _ref_inputs(R, wl, m, threads)
+    out = {"kind": "reference", "cores": threads, "unit": "points/s", "cpu_model": cpu_model()}
+    for workers, key in ((threads, "nproc"), (1, "one")):
+        s0, _ = R.bench_hull(xs, ys, workers, 1)  # calibration rep (untimed)
+        k = max(1, min(10, int(budget_s / 2 / max(float(s0[0]), 1e-3))))
+        secs, h = R.bench_hull(xs, ys, workers, k)
+        out[f"workers_{key}"] = {"workers": workers, "reps": k, "mean_s": float(np.mean(secs)),
+                                 "stddev_s": float(np.std(secs, ddof=1)) if k > 1 else 0.0,
+                                 "best_s": float(np.min(secs)), "points_per_s": m / float(np.mean(secs))}
+    out["value"] = out["workers_nproc"]["points_per_s"]
+    out["scale_baseline_gbps"] = R.scale_baseline(threads, 5)
+    what = "the full workload" if m == wl.total else f"the first {m} of {wl.total} points"
+    out["sample"] = (f"{what} ({wl.kind}, seed {wl.seed}), reference generators; convex_hull "
+                     f"(run_bench_points: fresh copy per rep, hull timed) at workers={threads} "
+                     f"and workers=1; Scale baseline (bench.cpp:33-74) at workers={threads}")
+    return out
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def run_ours(args) -> int:
     import numpy as np
     import torch
     import torch.distributed as dist
@@ -217,29 +324,25 @@ def run_ours(args):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        return 2
+    if not torch.cuda.is_available():
+        print("bench.py: no CUDA device visible", file=sys.stderr)
+        return 2
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    kind, n, seed = CONFIGS[args.config]
-    if args.n:
-        n = args.n
-    # configs 1-4: weak scaling, each rank owns n points of the global stream;
-    # config 5 (BASELINE: 4e9 points sharded evenly over 1/2/4/8 GPUs): strong
-    strong = args.config == 5 and not args.n
-    if strong:
-        total = n
-        n = total // world + (1 if rank < total % world else 0)
-        offset = rank * (total // world) + min(rank, total % world)
-    else:
-        offset = rank * n
+    wl = Workload(args, world)
+    offset, n = wl.shard(rank)
 
-    # host generation (libm, same bytes as the reference generators) into pinned memory
+    # host generation (libm, the reference generators' bytes) into pinned memory
     Xh = torch.empty(n, dtype=torch.float64, pin_memory=True)
     Yh = torch.empty(n, dtype=torch.float64, pin_memory=True)
-    vq.generate(kind, n, seed, first=offset, out=(Xh, Yh))
+    vq.generate(wl.kind, n, wl.seed, first=offset, out=(Xh, Yh))
     X = Xh.cuda(non_blocking=False)
     Y = Yh.cuda(non_blocking=False)
-    out_u32 = torch.empty(n, dtype=torch.int32, device="cuda")
+    out_u32 = torch.empty(n, dtype=torch.int32, device="cuda") if world == 1 else None
     stream = torch.cuda.current_stream()
 
     def step():
@@ -259,11 +362,12 @@ def run_ours(args):
         res = step()
     barrier()
     h = int(res.numel())
-    launches_per_step = int(vq.stats()["launches"]) * (2 if world > 1 else 1)
+    from paper_2510_09417_b200 import distributed as D
+    launches_per_step = int(vq.stats()["launches"]) if world == 1 else D.last_launches()
 
-    # ---- timed region: device resident inputs
-    # inputs (16 B/pt) that fit in L2 twice over are timed step by step with
-    # an L2 flush (a 512 MB write) between steps, outside the events
+    # ---- timed region: device-resident inputs.  Inputs (16 B/pt) that fit in
+    # L2 twice over are timed step by step with an L2 flush (a 512 MB write)
+    # between steps, outside the events
     flush = None
     if 16 * n < 2 * L2_BYTES:
         flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
@@ -292,47 +396,50 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
     ms_step = ms / args.steps
-    points_total = total if strong else world * n
-    value = points_total / (ms_step / 1e3)
+    value = wl.total / (ms_step / 1e3)
     clocks = clk.summary()
 
     result = {
         "metric": METRIC, "value": value, "unit": "points/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-        "higher_is_better": True, "scaling": "strong" if strong else "weak", "vs_baseline": None,
+        "higher_is_better": True, "scaling": "strong" if wl.strong else "weak", "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (reference RNG streams, seeded; generated on host with libm)",
-        "config": {"workload": (f"config{args.config}: {kind} n={points_total} total, sharded, seed={seed}"
-                                if strong else f"config{args.config}: {kind} n={n} per GPU seed={seed}")
-                               + (" (BASELINE configs[1])" if args.config == 2 else ""),
-                   "points_per_gpu": n, "points_total": points_total, "hull_vertices": h,
-                   "parallelism": f"shard{world}" if world > 1 else "single GPU",
-                   "l2": ("inputs 16 B/pt x n >> 126 MB L2 (no flush needed)" if flush is None else
-                          "L2 flushed (512 MB write) before every timed step; per-step CUDA events summed")},
+        "config": wl.config(),
+        "details": {"points_per_gpu": n, "hull_vertices": h,
+                    "l2": ("inputs 16 B/pt x n >> 126 MB L2 (no flush needed)" if flush is None else
+                           "L2 flushed (512 MB write) before every timed step; per-step CUDA events summed")},
         "clocks": clocks,
         "gpu_launches": launches_per_step * args.steps,
     }
+    if world > 1:
+        result["details"]["merge"] = D.last_info()
     if args.profile:
         if rank == 0:
             emit(result)
+        if world > 1:
+            dist.destroy_process_group()
         return 0
 
-    # ---- roofline: per-kernel CUDA-event times inside the library (same stream)
+    # ---- roofline: per-kernel CUDA-event times inside the library (same
+    # stream) for this rank's hull (at N > 1: the local hull of its shard)
     vq.set_timing(True)
     fam = {"extremes": [0.0, 0], "bootstrap": [0.0, 0], "root_partition": [0.0, 0],
            "levels": [0.0, 0], "finisher": [0.0, 0]}
     st = {}
     rep_rows = []  # (seconds, bytes_moved) per step, for --csv
+    tmp_out = out_u32 if out_u32 is not None else torch.empty(n, dtype=torch.int32, device="cuda")
     for _ in range(args.steps):
         if flush is not None:
             flush.fill_(1)
-        step()
+        vq.hull_device(X, Y, stream=stream, out=tmp_out, u32=True)
         st = vq.stats()
         rep_rows.append((st["ms_total"] / 1e3, int(st["bytes_moved"])))
         for k in fam:
             fam[k][0] += st[f"ms_{k}"]
             fam[k][1] += st[f"bytes_{k}"]
     vq.set_timing(False)
+    del tmp_out
     barrier()
     dom = max(fam, key=lambda k: fam[k][0])
     peak, peak_src = peaks()
@@ -340,12 +447,12 @@ def run_ours(args):
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            traffic = json.load(f).get(f"config{args.config}", {}).get(dom)
+            traffic = json.load(f).get(f"config{wl.cfg}", {}).get(dom)
     except Exception:
         pass
-    kname = {"root_partition": ("root_filter_tma (split root pass 1: octagon filter over every point)"
+    kname = {"root_partition": ("root_filter_tma (split root pass 1: polygon filter over every point)"
                                 if st.get("root_filtered") == 2 else "root pass"),
-             "levels": "tail_kernel (persistent recursion)" if st.get("root_filtered") == 2 else "level kernels",
+             "levels": "tail_kernel / level kernels (recursion)",
              "extremes": "poly_sample_kernel" if st.get("root_filtered") == 2 else "extremes"}.get(dom, dom)
     result["roofline"] = {
         "bound": "hbm", "kernel": kname, "family": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -356,6 +463,7 @@ def run_ours(args):
         "families_gbs": {k: (v[1] / 1e9) / (v[0] / 1e3) if v[0] else None for k, v in fam.items()},
         "hull_ms_events": st.get("ms_total"), "bytes_moved_per_step": st.get("bytes_moved"),
         "lower_bound_16n_frac": (16 * n / 1e9) / (ms_step / 1e3) / peak,
+        "scope": "rank 0's local hull of its shard" if world > 1 else "the whole hull",
     }
 
     # ---- e2e: public API with HOST buffers (H2D + D2H inside the timed region)
@@ -368,9 +476,10 @@ def run_ours(args):
             Xd = torch.empty_like(X)
             Yd = torch.empty_like(Y)
 
-        def e2e_step():
+        def e2e_step(pinned=True):
             if world == 1:
-                rc, idx = vq.vqhull_compute(xs_np, ys_np)
+                a, b = (xs_np, ys_np) if pinned else (xs_pg, ys_pg)
+                rc, idx = vq.vqhull_compute(a, b)
                 assert rc == 0
                 return idx.size
             Xd.copy_(Xh, non_blocking=True)
@@ -378,34 +487,41 @@ def run_ours(args):
             g = sharded_hull(Xd, Yd, offset)
             return g.cpu().numel()
 
-        e2e_step()
-        barrier()
-        t0 = time.perf_counter()
-        for _ in range(args.steps):
-            hh = e2e_step()
-        barrier()
-        dt = (time.perf_counter() - t0) / args.steps
-        tt = torch.tensor([dt], dtype=torch.float64, device="cuda")
-        if world > 1:
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        dt = float(tt.item())
-        result["e2e"] = {"value": points_total / dt, "unit": "points/s",
-                         "h2d_bytes_per_step": 16 * n, "d2h_bytes_per_step": (4 if world == 1 else 8) * hh,
+        def timed(fn, steps):
+            fn()
+            barrier()
+            t0 = time.perf_counter()
+            for _ in range(steps):
+                hh = fn()
+            barrier()
+            dt = (time.perf_counter() - t0) / steps
+            tt = torch.tensor([dt], dtype=torch.float64, device="cuda")
+            if world > 1:
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            return float(tt.item()), hh
+
+        dt, hh = timed(e2e_step, args.steps)
+        result["e2e"] = {"value": wl.total / dt, "unit": "points/s",
+                         "h2d_bytes_per_step": 16 * n, "d2h_bytes_per_step": (8 if world > 1 else 8) * hh,
                          "ms_per_step": dt * 1e3,
                          "api": "vqhull_compute (C ABI, pinned host arrays)" if world == 1
-                         else "H2D + sharded_hull + D2H"}
+                         else "per rank: H2D of its shard + sharded_hull + D2H of the index list"}
+        if world == 1:  # a drop-in C caller passes pageable memory: measured beside it
+            xs_pg, ys_pg = np.array(xs_np), np.array(ys_np)
+            dtp, _ = timed(lambda: e2e_step(False), max(1, min(args.steps, 5)))
+            result["e2e"]["pageable"] = {"value": wl.total / dtp, "unit": "points/s",
+                                         "ms_per_step": dtp * 1e3}
+            del xs_pg, ys_pg
 
     # ---- CPU baseline (rank 0, N=1 only)
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
-            cb = cpu_reference_baseline(kind, n, seed)
-            result["cpu_baseline"] = {"value": cb["value"], "unit": "points/s", "cores": cb["cores"],
-                                      "kind": cb["kind"], "sample": cb["sample"]}
+            result["cpu_baseline"] = cpu_reference_baseline(wl)
         except Exception as e:  # never lose the GPU line over the baseline
             result["cpu_baseline"] = {"value": None, "unit": "points/s", "cores": None,
                                       "kind": "reference", "sample": f"failed: {e}"}
     if rank == 0 and args.csv:
-        write_csv(args.csv, kind, points_total, seed, world, rep_rows, h, peak)
+        write_csv(args.csv, wl.kind, wl.total, wl.seed, world, rep_rows, h, peak)
     if rank == 0:
         emit(result)
     if world > 1:
@@ -444,8 +560,13 @@ def write_csv(path, kind, n, seed, workers, rep_rows, h, peak_gbs):
 
 def main():
     args = parse()
+    if args.gpus < 1:
+        print("bench.py: --gpus must be >= 1", file=sys.stderr)
+        return 2
     if args.impl == "reference":
         return run_reference(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch(args)
     return run_ours(args)
 
 

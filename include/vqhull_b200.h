@@ -19,7 +19,8 @@
  * Return codes: 0 success; 1 invalid arguments (exactly the reference's
  * conditions: out_count NULL, workers < 1, NULL arrays with n > 0, a
  * non-finite coordinate); 2 unsupported size (n >= 2^32 - 1 points per
- * device); 3 CUDA error (see vqhull_cuda_last_error()).
+ * device); 3 CUDA error (see vqhull_cuda_last_error()); 4 (sharded merge
+ * only) retry the shards with a margin floor.
  */
 #ifndef VQHULL_B200_H
 #define VQHULL_B200_H
@@ -35,6 +36,7 @@ extern "C" {
 #define VQHULL_EINVAL 1
 #define VQHULL_ESIZE 2
 #define VQHULL_ECUDA 3
+#define VQHULL_ERETRY 4  /* sharded merge: recompute the shards with a margin floor */
 
 /* Replaces vqhull_compute (vqhull_c.h:23-24, vqhull_c.cpp:26-64).
  * xs, ys: n host coordinates (pageable or pinned).  out_indices: host array
@@ -114,6 +116,10 @@ typedef struct vqhull_stats {
                                    polygon's scale, the call was rerun unfiltered */
     uint32_t tail_launches;     /* launches of the persistent recursion kernel */
     uint32_t tail_levels;       /* levels it processed */
+    uint64_t shard_tested;      /* last vqhull_cuda_shard_candidates: points certified */
+    uint64_t shard_candidates;  /* ... and the candidates it kept */
+    uint32_t shard_cert_vertices; /* vertices of the certificate polygon (0: none) */
+    uint32_t pad0;
 } vqhull_stats;
 
 int vqhull_cuda_get_stats(vqhull_stats* out);
@@ -161,6 +167,43 @@ const char* vqhull_cuda_last_error(void);
 
 /* 1 when a CUDA device is usable from this library. */
 int vqhull_cuda_available(void);
+
+/* ---- sharded hull ----------------------------
+ * Exact by construction: each shard sends every point it cannot prove to be
+ * deep inside its own local hull (a margin argument), and the
+ * merge runs the ordinary recursion over the union; the result equals the
+ * reference's global recursion over all points.
+ *
+ * Local stage on this device: hull of the shard d_xs/d_ys[0, n) (global
+ * indices offset + i), then its candidates, sorted by global index and packed
+ * as 3-double rows: row 0 = {count, M_eff, A} (count = -1: the shard holds a
+ * non-finite coordinate), rows 1.. = {x, y, global index as uint64 bits}.
+ * d_pack: device buffer of cap_rows + 1 rows (NULL: only *count); the first
+ * min(count, cap_rows) candidates are written.  margin_floor: 0, or the value
+ * a merge returned with VQHULL_ERETRY. */
+int vqhull_cuda_shard_candidates(const double* d_xs, const double* d_ys, uint64_t n, uint64_t offset,
+                                 double margin_floor, double* d_pack, uint64_t cap_rows,
+                                 uint64_t* count, void* stream);
+
+/* The last vqhull_cuda_shard_candidates' pack again, with room for cap_rows
+ * candidates (after a first pack that was too small). */
+int vqhull_cuda_shard_repack(double* d_pack, uint64_t cap_rows, void* stream);
+
+/* Merge on this device: nranks packs in offset order, pack r at
+ * d_packs + 3 * r * stride_rows.  out_indices (host or device, room for all
+ * candidates) receives the global clockwise first-occurrence list.
+ * VQHULL_ERETRY: recompute every shard with *margin_floor and merge again. */
+int vqhull_cuda_merge_candidates(const double* d_packs, uint32_t nranks, uint64_t stride_rows,
+                                 uint64_t* out_indices, uint64_t* out_count, double* margin_floor,
+                                 void* stream);
+
+/* Single-process multi-GPU hull of HOST arrays: num_shards contiguous shards,
+ * shard s on device s mod (device count), each with its own H2D, local hull
+ * and candidates; peer copies to device 0, merge there.  64-bit indices: n
+ * may exceed 2^32 - 1 when every shard stays below it.  vqhull_compute uses
+ * this path when VQHULL_GPUS is set (its value = shards) or n needs it. */
+int vqhull_cuda_hull_multi(const double* xs, const double* ys, uint64_t n, int num_shards,
+                           uint64_t* out_indices, uint64_t* out_count);
 
 /* Library version string. */
 const char* vqhull_b200_version(void);

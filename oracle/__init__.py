@@ -142,6 +142,9 @@ class Reference:
         L.ref_extract_subsets.argtypes = [_dp, _dp, C.c_size_t, _dp, _dp, C.c_int, C.c_int,
                                           _sz, _sz, _dp, _ip, _dp, _ip]
         L.ref_generate.argtypes = [C.c_int, C.c_uint64, C.c_uint64, C.c_int, _dp, _dp]
+        L.ref_generate_square.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, C.c_int, _dp, _dp]
+        L.ref_scale_baseline.argtypes = [C.c_uint64, C.c_int, C.c_int]
+        L.ref_scale_baseline.restype = C.c_double
         L.ref_rng_at.argtypes = [C.c_uint64, C.c_uint64]
         L.ref_rng_at.restype = C.c_uint64
         L.ref_uniform01.argtypes = [C.c_uint64, C.c_uint64]
@@ -212,6 +215,26 @@ class Reference:
         assert self.lib.ref_generate(KIND[kind], n, seed, workers, xs.ctypes.data_as(_dp),
                                      ys.ctypes.data_as(_dp)) == 0
         return xs, ys
+
+    def generate_square(self, n: int, seed: int, first: int = 0, workers: int = 8):
+        """BASELINE config 2's square from the reference's own RNG
+        (rng::uniform01, dataset.cpp:32-50): x = 2U(2k)-1, y = 2U(2k+1)-1."""
+        xs = np.empty(n)
+        ys = np.empty(n)
+        assert self.lib.ref_generate_square(seed, first, n, workers, xs.ctypes.data_as(_dp),
+                                            ys.ctypes.data_as(_dp)) == 0
+        return xs, ys
+
+    def generate_any(self, kind: str, n: int, seed: int, workers: int = 8):
+        """Points [0, n) of any BASELINE kind, generated by the reference."""
+        if kind == "square":
+            return self.generate_square(n, seed, 0, workers)
+        return self.generate(kind, n, seed, workers)
+
+    def scale_baseline(self, workers: int, reps: int = 5, buffer_bytes: int = 0) -> float:
+        """stream_scale_baseline (bench.cpp:33-74): in-place a[i] = s*a[i],
+        best-of-reps GB/s at 16 B per element; default buffer 4x the LLC."""
+        return float(self.lib.ref_scale_baseline(buffer_bytes, reps, workers))
 
     def rng_at(self, seed, index) -> int:
         return int(self.lib.ref_rng_at(seed, index))

@@ -12,9 +12,14 @@
 //   ref_find_extremes    -> vqhull::find_extremes        (geometry.hpp:135-138)
 //   ref_extract_subsets  -> vqhull::extract_subsets      (extract.hpp:79-82)
 //   ref_generate         -> vqhull::generate             (dataset.hpp:50)
+//   ref_generate_square  -> rng::uniform01 (dataset.hpp:30) for BASELINE
+//                           config 2's harness-defined square, x = 2U(2i)-1,
+//                           y = 2U(2i+1)-1 (the reference has no square kind)
+//   ref_scale_baseline   -> stream_scale_baseline        (bench.hpp:32, bench.cpp:33-74)
 //   ref_trace_hull       -> HullTrace + bytes_model      (hull.hpp:26-36, bench.cpp:16-21)
 //   ref_monotone_chain   -> monotone_chain_hull          (bench.hpp:87)
 //   vqhull_compute       is exported by the reference itself (vqhull_c.h:23)
+#include <algorithm>
 #include <chrono>
 #include <cstring>
 #include <cstdint>
@@ -144,6 +149,43 @@ int ref_generate(int kind, uint64_t n, uint64_t seed, int workers, double* xs,
         return 0;
     } catch (...) {
         return 1;
+    }
+}
+
+// points [first, first + n) of the square stream; the fill is split over
+// `workers` threads like generate() (the bytes do not depend on the split)
+int ref_generate_square(uint64_t seed, uint64_t first, uint64_t n, int workers, double* xs,
+                        double* ys) {
+    try {
+        if (workers < 1) workers = 1;
+        auto fill = [&](uint64_t b, uint64_t e) {
+            for (uint64_t i = b; i < e; ++i) {
+                const uint64_t k = first + i;
+                xs[i] = 2.0 * rng::uniform01(seed, 2 * k) - 1.0;
+                ys[i] = 2.0 * rng::uniform01(seed, 2 * k + 1) - 1.0;
+            }
+        };
+        std::vector<std::thread> th;
+        const uint64_t chunk = (n + uint64_t(workers) - 1) / uint64_t(workers);
+        for (int t = 1; t < workers; ++t) {
+            const uint64_t b = chunk * uint64_t(t);
+            if (b >= n) break;
+            th.emplace_back(fill, b, std::min(n, b + chunk));
+        }
+        fill(0, std::min(n, chunk));
+        for (auto& t : th) t.join();
+        return 0;
+    } catch (...) {
+        return 1;
+    }
+}
+
+// the reference's STREAM-Scale ceiling (best-of-reps GB/s, 16 B per element)
+double ref_scale_baseline(uint64_t buffer_bytes, int reps, int workers) {
+    try {
+        return stream_scale_baseline(buffer_bytes ? buffer_bytes : default_scale_bytes(), reps, workers).gbps;
+    } catch (...) {
+        return -1.0;
     }
 }
 

@@ -30,6 +30,7 @@ __all__ = [
     "LIB_PATH", "VQhullError", "lib", "available", "vqhull_compute", "convex_hull",
     "hull_indices", "hull_device", "find_extremes", "extract_subsets", "generate", "stats",
     "set_timing", "set_stable", "HullPolygon", "ExtractOutcome", "KINDS", "Stats",
+    "shard_candidates", "shard_repack", "merge_candidates", "hull_multi", "RetryWithFloor",
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -37,7 +38,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 # lib/libvqhull_b200_dbg.so with device bounds checks)
 LIB_PATH = os.environ.get("VQHULL_LIB", os.path.join(HERE, "lib", "libvqhull_b200.so"))
 
-VQHULL_OK, VQHULL_EINVAL, VQHULL_ESIZE, VQHULL_ECUDA = 0, 1, 2, 3
+VQHULL_OK, VQHULL_EINVAL, VQHULL_ESIZE, VQHULL_ECUDA, VQHULL_ERETRY = 0, 1, 2, 3, 4
 KINDS = {"kuzmin": 0, "circle": 1, "disk": 2, "square": 3}
 
 _dp = C.POINTER(C.c_double)
@@ -70,6 +71,10 @@ class Stats(C.Structure):
         ("root_reruns", C.c_uint32),
         ("tail_launches", C.c_uint32),
         ("tail_levels", C.c_uint32),
+        ("shard_tested", C.c_uint64),
+        ("shard_candidates", C.c_uint64),
+        ("shard_cert_vertices", C.c_uint32),
+        ("pad0", C.c_uint32),
     ]
 
     def as_dict(self) -> dict:
@@ -107,6 +112,13 @@ def lib() -> C.CDLL:
         L.vqhull_b200_version.restype = C.c_char_p
         L.vqhull_generate.argtypes = [C.c_int, C.c_uint64, C.c_uint64, C.c_uint64, C.c_void_p,
                                       C.c_void_p, C.c_int]
+        L.vqhull_cuda_shard_candidates.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64,
+                                                   C.c_double, C.c_void_p, C.c_uint64, _u64p,
+                                                   C.c_void_p]
+        L.vqhull_cuda_shard_repack.argtypes = [C.c_void_p, C.c_uint64, C.c_void_p]
+        L.vqhull_cuda_merge_candidates.argtypes = [C.c_void_p, C.c_uint32, C.c_uint64, C.c_void_p,
+                                                   _u64p, _dp, C.c_void_p]
+        L.vqhull_cuda_hull_multi.argtypes = [_dp, _dp, C.c_uint64, C.c_int, _u64p, _u64p]
         _LIB = L
     return _LIB
 
@@ -176,43 +188,141 @@ def convex_hull(xs, ys) -> HullPolygon:
 # ---------------------------------------------------------------------------
 # device-array API (torch tensors as HBM handles)
 # ---------------------------------------------------------------------------
-def _stream_ptr(stream) -> Optional[int]:
+def _stream_ptr(stream, device=None) -> Optional[int]:
     if stream is None:
         import torch
-        return torch.cuda.current_stream().cuda_stream
+        return torch.cuda.current_stream(device).cuda_stream
     return getattr(stream, "cuda_stream", stream)
+
+
+def _check_pair(x, y, what: str, writable: bool = False) -> None:
+    """Both coordinate arrays: float64 CUDA tensors of one length on one
+    device (the kernels index y by x's positions and launch on x's device)."""
+    import torch
+    for t in (x, y):
+        if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float64):
+            raise TypeError(f"{what}: coordinates must be float64 CUDA tensors")
+        if writable and not t.is_contiguous():
+            raise ValueError(f"{what}: in-place call needs contiguous tensors")
+    if x.numel() != y.numel():
+        raise ValueError(f"{what}: x has {x.numel()} points, y has {y.numel()}")
+    if x.device != y.device:
+        raise ValueError(f"{what}: x is on {x.device}, y on {y.device}")
 
 
 def hull_device(x, y, stream=None, out=None, u32: bool = False):
     """Hull of device-resident points (torch float64 CUDA tensors).
 
     Returns a CUDA tensor of indices (int64 view of the uint64 list, or int32
-    when ``u32``) — clockwise, first occurrence.
+    when ``u32``) — clockwise, first occurrence.  Runs on x's device (its
+    current stream unless ``stream`` is given).
     """
     import torch
-    assert x.is_cuda and y.is_cuda and x.dtype == torch.float64 and y.dtype == torch.float64
+    _check_pair(x, y, "hull_device")
     x, y = x.contiguous(), y.contiguous()
     n = x.numel()
+    want = torch.int32 if u32 else torch.int64
+    if out is None:
+        out = torch.empty(max(n, 1), dtype=want, device=x.device)
+    elif out.dtype != want or out.device != x.device or out.numel() < n or not out.is_contiguous():
+        raise ValueError(f"hull_device: out must be a contiguous {want} tensor on {x.device} "
+                         f"with room for {n} indices")
     cnt = C.c_uint64(0)
-    if u32:
-        if out is None:
-            out = torch.empty(max(n, 1), dtype=torch.int32, device=x.device)
-        rc = lib().vqhull_cuda_hull_u32(x.data_ptr(), y.data_ptr(), n, out.data_ptr(),
-                                        C.byref(cnt), _stream_ptr(stream))
-    else:
-        if out is None:
-            out = torch.empty(max(n, 1), dtype=torch.int64, device=x.device)
-        rc = lib().vqhull_cuda_hull(x.data_ptr(), y.data_ptr(), n, out.data_ptr(),
-                                    C.byref(cnt), _stream_ptr(stream))
+    with torch.cuda.device(x.device):
+        st = _stream_ptr(stream, x.device)
+        if u32:
+            rc = lib().vqhull_cuda_hull_u32(x.data_ptr(), y.data_ptr(), n, out.data_ptr(),
+                                            C.byref(cnt), st)
+        else:
+            rc = lib().vqhull_cuda_hull(x.data_ptr(), y.data_ptr(), n, out.data_ptr(),
+                                        C.byref(cnt), st)
     _check(rc, "vqhull_cuda_hull")
     return out[: cnt.value]
 
 
+# ---------------------------------------------------------------------------
+# sharded hull building blocks (SURVEY §8e; distributed.py drives them)
+# ---------------------------------------------------------------------------
+class RetryWithFloor(Exception):
+    """The merge found a shard whose margin scale is too small for the largest
+    coordinate in play: recompute every shard with ``floor``."""
+
+    def __init__(self, floor: float):
+        super().__init__(f"recompute the shards with margin floor {floor!r}")
+        self.floor = floor
+
+
+def shard_candidates(x, y, offset: int, cap: int, floor: float = 0.0, stream=None):
+    """Local stage of the sharded hull on x's device: returns (pack, count),
+    pack a float64 tensor of cap + 1 rows x 3 (header {count, M_eff, A}, then
+    the first min(count, cap) candidates {x, y, global index bits}).  A
+    count above cap: call :func:`shard_repack` with a larger buffer."""
+    import torch
+    _check_pair(x, y, "shard_candidates")
+    x, y = x.contiguous(), y.contiguous()
+    pack = torch.empty((cap + 1, 3), dtype=torch.float64, device=x.device)
+    cnt = C.c_uint64(0)
+    with torch.cuda.device(x.device):
+        rc = lib().vqhull_cuda_shard_candidates(x.data_ptr(), y.data_ptr(), x.numel(), int(offset),
+                                                float(floor), pack.data_ptr(), cap, C.byref(cnt),
+                                                _stream_ptr(stream, x.device))
+    _check(rc, "vqhull_cuda_shard_candidates")
+    return pack, int(cnt.value)
+
+
+def shard_repack(pack, stream=None) -> None:
+    """The last shard_candidates' rows again into ``pack`` (rows - 1 of room)."""
+    import torch
+    with torch.cuda.device(pack.device):
+        rc = lib().vqhull_cuda_shard_repack(pack.data_ptr(), pack.shape[0] - 1,
+                                           _stream_ptr(stream, pack.device))
+    _check(rc, "vqhull_cuda_shard_repack")
+
+
+def merge_candidates(packs, stream=None):
+    """Merge on packs' device: ``packs`` (nranks, rows, 3) float64 in offset
+    order.  Returns the global clockwise index list (int64 CUDA tensor);
+    raises :class:`RetryWithFloor` when the shards must be recomputed."""
+    import torch
+    packs = packs.contiguous()
+    nranks, rows = packs.shape[0], packs.shape[1]
+    out = torch.empty(max(nranks * (rows - 1), 1), dtype=torch.int64, device=packs.device)
+    cnt = C.c_uint64(0)
+    fl = C.c_double(0.0)
+    with torch.cuda.device(packs.device):
+        rc = lib().vqhull_cuda_merge_candidates(packs.data_ptr(), nranks, rows, out.data_ptr(),
+                                                C.byref(cnt), C.byref(fl),
+                                                _stream_ptr(stream, packs.device))
+    if rc == VQHULL_ERETRY:
+        raise RetryWithFloor(fl.value)
+    _check(rc, "vqhull_cuda_merge_candidates")
+    return out[: cnt.value]
+
+
+def hull_multi(xs, ys, shards: int) -> np.ndarray:
+    """Single-process multi-GPU hull of host arrays (vqhull_cuda_hull_multi):
+    ``shards`` contiguous shards over the visible devices, merged on device 0."""
+    xs, ys = _f64(xs), _f64(ys)
+    if xs.shape != ys.shape:
+        raise ValueError("xs and ys differ in length")
+    n = xs.size
+    out = np.zeros(max(n, 1), dtype=np.uint64)
+    cnt = C.c_uint64(0)
+    rc = lib().vqhull_cuda_hull_multi(xs.ctypes.data_as(_dp), ys.ctypes.data_as(_dp), n, shards,
+                                      out.ctypes.data_as(_u64p), C.byref(cnt))
+    _check(rc, "vqhull_cuda_hull_multi")
+    return out[: cnt.value].copy()
+
+
 def find_extremes(x, y, stream=None) -> Tuple[int, int]:
     """find_extremes on device tensors -> (lo, hi).  Raises on empty input."""
+    import torch
+    _check_pair(x, y, "find_extremes")
+    x, y = x.contiguous(), y.contiguous()
     lo, hi = C.c_uint64(), C.c_uint64()
-    rc = lib().vqhull_cuda_find_extremes(x.data_ptr(), y.data_ptr(), x.numel(), C.byref(lo),
-                                         C.byref(hi), _stream_ptr(stream))
+    with torch.cuda.device(x.device):
+        rc = lib().vqhull_cuda_find_extremes(x.data_ptr(), y.data_ptr(), x.numel(), C.byref(lo),
+                                             C.byref(hi), _stream_ptr(stream, x.device))
     if rc == VQHULL_EINVAL and x.numel() == 0:
         raise ValueError("find_extremes: empty input")
     _check(rc, "vqhull_cuda_find_extremes")
@@ -230,14 +340,17 @@ class ExtractOutcome:
 
 def extract_subsets(x, y, edge_a, edge_b, stream=None) -> ExtractOutcome:
     """In-place fused partition + arg-max on device tensors (extract_subsets)."""
+    import torch
+    _check_pair(x, y, "extract_subsets", writable=True)
     ea = (C.c_double * 4)(*[float(v) for v in edge_a])
     eb = (C.c_double * 4)(*[float(v) for v in edge_b])
     wl, wr = C.c_uint64(), C.c_uint64()
     r1, r2 = (C.c_double * 2)(), (C.c_double * 2)()
     h1, h2 = C.c_int(), C.c_int()
-    rc = lib().vqhull_cuda_extract_subsets(x.data_ptr(), y.data_ptr(), x.numel(), ea, eb,
-                                           C.byref(wl), C.byref(wr), r1, C.byref(h1), r2,
-                                           C.byref(h2), _stream_ptr(stream))
+    with torch.cuda.device(x.device):
+        rc = lib().vqhull_cuda_extract_subsets(x.data_ptr(), y.data_ptr(), x.numel(), ea, eb,
+                                               C.byref(wl), C.byref(wr), r1, C.byref(h1), r2,
+                                               C.byref(h2), _stream_ptr(stream, x.device))
     _check(rc, "vqhull_cuda_extract_subsets")
     return ExtractOutcome(wl.value, wr.value, (r1[0], r1[1]) if h1.value else None,
                           (r2[0], r2[1]) if h2.value else None)

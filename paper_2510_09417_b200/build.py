@@ -16,7 +16,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, "libvqhull_b200.so")
 LIB_DBG = os.path.join(LIBDIR, "libvqhull_b200_dbg.so")
-SOURCES = ["device.cu", "driver.cu", "dataset.cpp"]  # device.cu includes kernels.cu, partition.cu, tail.cu
+SOURCES = ["device.cu", "shard.cu", "driver.cu", "dataset.cpp"]  # device.cu includes kernels.cu, partition.cu, tail.cu
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

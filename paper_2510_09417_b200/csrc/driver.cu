@@ -23,6 +23,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/vqhull_b200.h"
@@ -148,6 +149,7 @@ class Engine {
         ck(cudaMallocHost(&h_info_, sizeof(LevelInfo) * 2), "cudaMallocHost");
         ck(cudaMallocHost(&h_root_, sizeof(RootInfo)), "cudaMallocHost");
         ck(cudaMallocHost(&h_word_, 64), "cudaMallocHost");
+        ck(cudaMallocHost(&h_dbl_, 8 * 32), "cudaMallocHost");
         fault_dev_ = fault_word_ptr();
         ck(cudaMallocHost(&h_tail_, report_bytes(kTailLevels)), "cudaMallocHost");
         partials_.ensure(partial_bytes(stream_grid_), nullptr);
@@ -171,6 +173,7 @@ class Engine {
         if (st == nullptr) st = own_stream();
         reset_stats(n);
         *h = 0;
+        keep_valid_ = false;
         if (n == 0) return VQHULL_OK;
         if (n >= 0xffffffffull) return VQHULL_ESIZE;
         launches_ = 0;
@@ -185,6 +188,7 @@ class Engine {
         // the common small-recursion case (split root + KT) replays one
         // captured CUDA graph: sample, filter, KT and the report copy
         graph_run_ = split && n <= kLeanN && use_tail_ && use_graph_ && !timing_ && !tail_trace_ && !sync_each_ &&
+                     !keep_req_ &&
                      run_graph(dx, dy, n, d_out, st);
         uint32_t nslots = graph_run_ ? 1u
                         : split ? run_root_split(dx, dy, n, st)
@@ -500,6 +504,7 @@ class Engine {
     int compute_host(const double* xs, const double* ys, uint64_t n, uint32_t* h_out_u32, uint64_t* h,
                      cudaStream_t st) {
         VQB_TRACE("compute_host: n=%llu", (unsigned long long)n);
+        if (n >= 0xffffffffull) return VQHULL_ESIZE;  // before any allocation or copy
         in_.x.ensure(n * 8, st);
         in_.y.ensure(n * 8, st);
         ck(cudaMemcpyAsync(in_.x.p, xs, n * 8, cudaMemcpyHostToDevice, st), "h2d x");
@@ -512,6 +517,202 @@ class Engine {
         return VQHULL_OK;
     }
 
+    // ---- sharded hull (shard.cu) --------------------------------
+    // Local stage of one shard: its hull, then the certificate, then the
+    // candidates (every point not proven deep inside the local hull) sorted
+    // by index, packed as rows {x, y, bits(offset + index)} behind a header
+    // row {count, M_eff, A} (count -1: invalid input).  d_pack (device, room
+    // for cap + 1 rows) may be null: the candidates stay in the engine for
+    // repack().  floor_m > 0 (a merge's retry): no filter-pass shortcut, the
+    // whole shard is tested with the margin scale max(M, floor_m).
+    int shard(const double* dx, const double* dy, uint64_t n, uint64_t offset, double floor_m, double* d_pack,
+              uint64_t cap, uint64_t* count, cudaStream_t st) {
+        if (st == nullptr) st = own_stream();
+        *count = 0;
+        const double kInf = HUGE_VAL;
+        shard_hdr_[0] = 0.0; shard_hdr_[1] = kInf; shard_hdr_[2] = 0.0;
+        shard_k_ = 0;
+        shard_offset_ = offset;
+        if (n >= 0xffffffffull) return VQHULL_ESIZE;
+        if (n == 0) return write_header(d_pack, st);
+        out_.ensure(n * 4, st);
+        uint64_t h = 0;
+        keep_req_ = floor_m == 0.0;
+        int rc;
+        try {
+            rc = hull(dx, dy, n, out_.as<uint32_t>(), &h, st);
+        } catch (...) {
+            keep_req_ = false;
+            throw;
+        }
+        keep_req_ = false;
+        if (rc == VQHULL_EINVAL) {  // non-finite input: every rank learns it from the merge
+            shard_hdr_[0] = -1.0;
+            return write_header(d_pack, st);
+        }
+        if (rc) return rc;
+        const bool kept = floor_m == 0.0 && keep_valid_ && stats_.root_filtered == 2 && !stats_.root_reruns &&
+                          stats_.root_filter_on;
+        // the tested set: the filter pass's survivors, or the whole shard
+        uint64_t m = n;
+        ck(cudaMemcpyAsync(h_word_ + 4, &root_->cnt1, 4, cudaMemcpyDeviceToHost, st), "d2h survivors");
+        ck(cudaMemcpyAsync(h_dbl_, &root_->poly.mref, 8, cudaMemcpyDeviceToHost, st), "d2h M");
+        ck(cudaStreamSynchronize(st), "sync");
+        if (kept) m = h_word_[4];
+        const double m_kf = h_dbl_[0];
+        cert_head_.ensure(sizeof(CertHead), st);
+        cert_rec_.ensure(size_t(kCertMax) * sizeof(CertRec), st);
+        cert_asc_.ensure(size_t(2 * kCertMax) * 4, st);
+        cert_tab_.ensure(size_t(kCertBuckets) * 4, st);
+        resid_.ensure(std::max<uint64_t>(m, 1), st);
+        ck(cudaMemsetAsync(ctrs_ + 20, 0, 12, st), "memset cert counters");  // count + amax bits
+        tk(5, st, [&] {
+            launch_cert_build(out_.as<uint32_t>(), uint32_t(h), dx, dy, floor_m, cert_head_.as<CertHead>(),
+                              cert_rec_.as<CertRec>(), cert_asc_.as<float>(), cert_tab_.as<uint32_t>(), st);
+        });
+        tk(5, st, [&] {
+            launch_certify(kept ? keep_.x.as<double>() : dx, kept ? keep_.y.as<double>() : dy,
+                           kept ? keep_.id.as<uint32_t>() : nullptr, m, nullptr, cert_head_.as<CertHead>(),
+                           cert_rec_.as<CertRec>(), cert_asc_.as<float>(), cert_tab_.as<uint32_t>(),
+                           resid_.x.as<double>(), resid_.y.as<double>(), resid_.id.as<uint32_t>(), ctrs_ + 20,
+                           reinterpret_cast<unsigned long long*>(ctrs_ + 22), sms_ * 8, st);
+        });
+        CertHead ch;
+        ck(cudaMemcpyAsync(h_word_ + 4, ctrs_ + 20, 12, cudaMemcpyDeviceToHost, st), "d2h cert counters");
+        ck(cudaMemcpyAsync(h_dbl_ + 1, cert_head_.p, sizeof(CertHead), cudaMemcpyDeviceToHost, st), "d2h cert");
+        ck(cudaStreamSynchronize(st), "sync");
+        std::memcpy(&ch, h_dbl_ + 1, sizeof ch);
+        const uint32_t k = h_word_[4];
+        double amax;
+        {
+            uint64_t bits = uint64_t(h_word_[5]) | (uint64_t(h_word_[6]) << 32);
+            std::memcpy(&amax, &bits, 8);
+        }
+        double m_eff = kInf;
+        if (kept) m_eff = std::min(m_eff, m_kf);
+        if (ch.valid) m_eff = std::min(m_eff, ch.Me);
+        shard_hdr_[0] = double(k);
+        shard_hdr_[1] = m_eff;
+        shard_hdr_[2] = kept ? std::max(amax, m_kf) : amax;
+        shard_k_ = k;
+        stats_.shard_tested = m;
+        stats_.shard_candidates = k;
+        stats_.shard_cert_vertices = ch.K;
+        // sort the candidates by index (first occurrence = smallest global index)
+        if (k) {
+            sorted_.ensure(size_t(k) * 12, st);  // sorted ids | permutation | iota
+            const size_t tb = sort_temp_bytes(k);
+            sort_tmp_.ensure(tb, st);
+            int end_bit = 1;
+            while (end_bit < 32 && (uint64_t(1) << end_bit) < n) ++end_bit;
+            tk(5, st, [&] {
+                ck(launch_sort_ids(sort_tmp_.p, tb, resid_.id.as<uint32_t>(), sorted_.as<uint32_t>(),
+                                   sorted_.as<uint32_t>() + 2 * size_t(k), sorted_.as<uint32_t>() + k, k, end_bit, st),
+                   "sort candidates");
+            });
+            launches_ += 2 + uint32_t((end_bit + 7) / 8);  // cub onesweep: histogram, scan, one pass per 8 bits (+ our iota)
+        }
+        stats_.launches = launches_;
+        *count = k;
+        return d_pack ? repack(d_pack, cap, st) : VQHULL_OK;
+    }
+
+    // the last shard()'s header and first min(count, cap) rows into d_pack
+    int repack(double* d_pack, uint64_t cap, cudaStream_t st) {
+        if (st == nullptr) st = own_stream();
+        if (!d_pack) return VQHULL_EINVAL;
+        const uint32_t c = uint32_t(std::min<uint64_t>(cap, 0xffffffffull));
+        if (shard_k_)
+            tk(5, st, [&] {
+                launch_pack(resid_.x.as<double>(), resid_.y.as<double>(), sorted_.as<uint32_t>(),
+                            sorted_.as<uint32_t>() + shard_k_, shard_k_, c, shard_offset_, d_pack, st);
+            });
+        return write_header(d_pack, st);
+    }
+
+    // Merge: nranks packs at a stride of stride_rows rows (header + rows, in
+    // offset order).  Writes the global clockwise index list (host or device
+    // out) or returns VQHULL_ERETRY with *floor_out: recompute every shard
+    // with that margin floor (a shard's scale was too small for the largest
+    // coordinate in play).
+    int merge(const double* d_packs, uint32_t nranks, uint64_t stride_rows, uint64_t* out, uint64_t* count,
+              double* floor_out, cudaStream_t st) {
+        if (st == nullptr) st = own_stream();
+        *count = 0;
+        if (floor_out) *floor_out = 0.0;
+        if (nranks == 0 || stride_rows == 0) return VQHULL_EINVAL;
+        std::vector<double> hdr(size_t(nranks) * 3);
+        ck(cudaMemcpy2DAsync(hdr.data(), 24, d_packs, stride_rows * 24, 24, nranks, cudaMemcpyDeviceToHost, st),
+           "d2h headers");
+        ck(cudaStreamSynchronize(st), "sync");
+        double A = 0.0, Mmin = HUGE_VAL;
+        std::vector<uint64_t> starts(nranks + 1, 0);
+        for (uint32_t r = 0; r < nranks; ++r) {
+            const double c = hdr[3 * r];
+            if (!(c >= 0.0)) return VQHULL_EINVAL;  // a shard held a non-finite point (or garbage)
+            if (c > double(stride_rows - 1)) {
+                g_last_error = "merge: a shard's candidates exceed the pack stride (repack them)";
+                return VQHULL_EINVAL;
+            }
+            starts[r + 1] = starts[r] + uint64_t(c);
+            A = std::max(A, hdr[3 * r + 2]);
+            Mmin = std::min(Mmin, hdr[3 * r + 1]);
+        }
+        if (!(A <= 0x1p12 * Mmin)) {  // the margins' rounding bound needs A <= 2^12 M on every shard
+            if (floor_out) *floor_out = A * 0x1p-12;
+            return VQHULL_ERETRY;
+        }
+        const uint64_t total = starts[nranks];
+        stats_merge_ = total;
+        if (total == 0) return VQHULL_OK;
+        if (total >= 0xffffffffull) return VQHULL_ESIZE;
+        mbuf_.ensure(total, st);
+        mg_.ensure(total * 8, st);
+        mstarts_.ensure(size_t(nranks + 1) * 8, st);
+        ck(cudaMemcpyAsync(mstarts_.p, starts.data(), size_t(nranks + 1) * 8, cudaMemcpyHostToDevice, st),
+           "h2d starts");
+        ck(cudaStreamSynchronize(st), "sync");  // (starts is a host vector)
+        ck(cudaMemsetAsync(ctrs_ + 24, 0, 4, st), "memset flag");
+        launch_merge_gather(d_packs, stride_rows, mstarts_.as<uint64_t>(), nranks, total, mbuf_.x.as<double>(),
+                            mbuf_.y.as<double>(), mg_.as<uint64_t>(), ctrs_ + 24, st);
+        ck(cudaMemcpyAsync(h_word_ + 8, ctrs_ + 24, 4, cudaMemcpyDeviceToHost, st), "d2h flag");
+        ck(cudaStreamSynchronize(st), "sync");
+        if (h_word_[8]) {
+            g_last_error = "merge: candidates are not in increasing global-index order (shards out of offset order)";
+            return VQHULL_EINVAL;
+        }
+        out_.ensure(total * 4, st);
+        uint64_t h = 0;
+        const int rc = hull(mbuf_.x.as<double>(), mbuf_.y.as<double>(), total, out_.as<uint32_t>(), &h, st);
+        if (rc) return rc;
+        const bool dev = is_device_ptr_(out);
+        uint64_t* dst = out;
+        if (!dev) {
+            mout_.ensure(std::max<uint64_t>(h, 1) * 8, st);
+            dst = mout_.as<uint64_t>();
+        }
+        launch_map_gidx(out_.as<uint32_t>(), h, mg_.as<uint64_t>(), dst, st);
+        stats_.launches += 2;  // gather + map
+        if (!dev && h) ck(cudaMemcpyAsync(out, dst, h * 8, cudaMemcpyDeviceToHost, st), "d2h indices");
+        ck(cudaStreamSynchronize(st), "sync");
+        ck(cudaGetLastError(), "merge");
+        *count = h;
+        return VQHULL_OK;
+    }
+
+    uint64_t merged_candidates() const { return stats_merge_; }
+
+    // a copy of host points [0, n) into the engine's input pair (multi-device driver)
+    void load_host(const double* xs, const double* ys, uint64_t n, cudaStream_t st) {
+        in_.x.ensure(n * 8, st);
+        in_.y.ensure(n * 8, st);
+        ck(cudaMemcpyAsync(in_.x.p, xs, n * 8, cudaMemcpyHostToDevice, st), "h2d x");
+        ck(cudaMemcpyAsync(in_.y.p, ys, n * 8, cudaMemcpyHostToDevice, st), "h2d y");
+    }
+    const double* in_x() const { return in_.x.as<double>(); }
+    const double* in_y() const { return in_.y.as<double>(); }
+    cudaStream_t stream() { return own_stream(); }
+
     DevBuf& out_buf() { return out_; }
 
     // frees the big per-call buffers (points, level tables, staging) and
@@ -519,7 +720,7 @@ class Engine {
     // re-allocates what it needs
     void trim() {
         ck(cudaDeviceSynchronize(), "trim sync");
-        for (PointBuf* b : {&bufs_[0], &bufs_[1], &in_}) {
+        for (PointBuf* b : {&bufs_[0], &bufs_[1], &in_, &keep_, &resid_, &mbuf_}) {
             b->x.release();
             b->y.release();
             b->id.release();
@@ -527,7 +728,8 @@ class Engine {
         for (LevelTables& T : levels_)
             for (DevBuf* d : {&T.slots, &T.kind, &T.link, &T.size, &T.start, &T.segs, &T.fins, &T.fin_count})
                 d->release();
-        for (DevBuf* d : {&tile_seg_, &chain_, &out_, &part_, &status_, &flags_, &aggs_, &incs_})
+        for (DevBuf* d : {&tile_seg_, &chain_, &out_, &part_, &status_, &flags_, &aggs_, &incs_, &cert_head_,
+                          &cert_rec_, &cert_asc_, &cert_tab_, &sorted_, &sort_tmp_, &mg_, &mstarts_, &mout_})
             d->release();
         for (GraphEntry& e : graphs_)
             if (e.exec) {
@@ -885,6 +1087,11 @@ class Engine {
         fa.out_cap = bufs_[0].x.cap / 8;
         fa.ctr = &ctrs_[12]; fa.ticket = &ctrs_[13]; fa.part = fpart_.p;
         fa.root_w = root_; fa.slot = L2.slots.as<ChildRec>();
+        if (keep_req_) {  // sharded hull: the filter pass also keeps its survivors for the certificate
+            keep_.ensure(n, st);
+            fa.kx = keep_.x.as<double>(); fa.ky = keep_.y.as<double>(); fa.kid = keep_.id.as<uint32_t>();
+            keep_valid_ = true;
+        }
         tk(2, st, [&] { ck(launch_root_filter(fa, grid, st), "root filter launch"); });
         return 1;
     }
@@ -1150,6 +1357,30 @@ class Engine {
    private:
     PointBuf bufs_[2];
     PointBuf in_;
+    // sharded hull: the filter pass's survivor copy, the candidates, the merge
+    PointBuf keep_, resid_, mbuf_;
+    DevBuf cert_head_, cert_rec_, cert_asc_, cert_tab_, sorted_, sort_tmp_, mg_, mstarts_, mout_;
+    bool keep_req_ = false, keep_valid_ = false;
+    double shard_hdr_[3] = {0.0, 0.0, 0.0};
+    uint32_t shard_k_ = 0;
+    uint64_t shard_offset_ = 0;
+    uint64_t stats_merge_ = 0;
+    double* h_dbl_ = nullptr;  // pinned scratch (8 + CertHead)
+    int write_header(double* d_pack, cudaStream_t st) {
+        if (!d_pack) return VQHULL_OK;
+        std::memcpy(h_dbl_ + 16, shard_hdr_, 24);
+        ck(cudaMemcpyAsync(d_pack, h_dbl_ + 16, 24, cudaMemcpyHostToDevice, st), "h2d header");
+        ck(cudaStreamSynchronize(st), "sync");
+        return VQHULL_OK;
+    }
+    static bool is_device_ptr_(const void* p) {
+        cudaPointerAttributes a;
+        if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+            cudaGetLastError();
+            return false;
+        }
+        return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+    }
     std::deque<LevelTables> levels_;  // deque: references stay valid on growth
     std::vector<LevelInfo> hinfo_;  // host copies of the level infos (after the last batch)
     int lmax_ = 2;
@@ -1191,14 +1422,147 @@ std::mutex g_reg_mu;
 std::vector<std::unique_ptr<Engine>> g_engines;
 thread_local bool g_timing = false;
 
-Engine& engine() {
-    int dev = 0;
-    VQB_TRACE("engine(): cudaGetDevice");
-    ck(cudaGetDevice(&dev), "cudaGetDevice");
+Engine& engine_for(int dev) {
     std::lock_guard<std::mutex> lk(g_reg_mu);
     if (g_engines.size() <= size_t(dev)) g_engines.resize(dev + 1);
     if (!g_engines[dev]) g_engines[dev].reset(new Engine(dev));
     return *g_engines[dev];
+}
+
+Engine& engine() {
+    int dev = 0;
+    VQB_TRACE("engine(): cudaGetDevice");
+    ck(cudaGetDevice(&dev), "cudaGetDevice");
+    return engine_for(dev);
+}
+
+// ---------------------------------------------------------------------------
+// Single-process multi-GPU hull of host arrays: the
+// points are cut into `shards` contiguous ranges, shard s runs on device
+// s mod ndev (one host thread per device: its own H2D over its own PCIe link,
+// its local hull and certificate, Engine::shard); the packed candidates are
+// copied peer-to-peer to device 0, which merges them (Engine::merge).  Global
+// indices are 64-bit, so n may exceed 2^32 - 1 as long as every shard stays
+// below it.  More shards than devices run one after another per device
+// (tests of the sharded path on one GPU).
+// ---------------------------------------------------------------------------
+int hull_multi(const double* xs, const double* ys, uint64_t n, int shards, uint64_t* out, uint64_t* count) {
+    *count = 0;
+    if (shards < 1) return VQHULL_EINVAL;
+    if (n == 0) return VQHULL_OK;
+    int ndev = 0;
+    ck(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+    if (ndev < 1) return VQHULL_ECUDA;
+    const uint64_t S = uint64_t(shards);
+    const uint64_t base = n / S, rem = n % S;
+    if (base + (rem ? 1 : 0) >= 0xffffffffull) return VQHULL_ESIZE;
+    std::vector<uint64_t> off(S), cnt(S), k(S, 0);
+    for (uint64_t s = 0; s < S; ++s) {
+        off[s] = s * base + std::min(s, rem);
+        cnt[s] = base + (s < rem ? 1 : 0);
+    }
+    const int nd = int(std::min<uint64_t>(uint64_t(ndev), S));
+    std::vector<void*> packs(S, nullptr);
+    auto free_packs = [&] {
+        for (uint64_t s = 0; s < S; ++s)
+            if (packs[s]) {
+                cudaSetDevice(int(s % uint64_t(nd)));
+                cudaFree(packs[s]);
+                packs[s] = nullptr;
+            }
+    };
+    double floor_m = 0.0;
+    int rc = VQHULL_OK;
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        std::vector<int> rcs(nd, VQHULL_OK);
+        std::vector<std::string> errs(nd);
+        auto work = [&](int d) {
+            try {
+                ck(cudaSetDevice(d), "cudaSetDevice");
+                Engine& e = engine_for(d);
+                std::lock_guard<std::mutex> lk(e.mutex());
+                cudaStream_t st = e.stream();
+                for (uint64_t s = uint64_t(d); s < S; s += uint64_t(nd)) {
+                    e.load_host(xs + off[s], ys + off[s], cnt[s], st);
+                    int r = e.shard(e.in_x(), e.in_y(), cnt[s], off[s], floor_m, nullptr, 0, &k[s], st);
+                    if (r) {
+                        rcs[d] = r;
+                        return;
+                    }
+                    if (packs[s]) cudaFree(packs[s]);
+                    packs[s] = nullptr;
+                    ck(cudaMalloc(&packs[s], (k[s] + 1) * 24), "cudaMalloc pack");
+                    r = e.repack(static_cast<double*>(packs[s]), k[s], st);
+                    if (r) {
+                        rcs[d] = r;
+                        return;
+                    }
+                    ck(cudaStreamSynchronize(st), "sync");
+                }
+            } catch (const CudaError&) {
+                rcs[d] = VQHULL_ECUDA;
+                errs[d] = g_last_error;
+            }
+        };
+        std::vector<std::thread> th;
+        for (int d = 1; d < nd; ++d) th.emplace_back(work, d);
+        work(0);
+        for (auto& t : th) t.join();
+        for (int d = 0; d < nd; ++d)
+            if (rcs[d]) {
+                if (!errs[d].empty()) g_last_error = errs[d];
+                free_packs();
+                return rcs[d];
+            }
+        uint64_t kmax = 0;
+        for (uint64_t s = 0; s < S; ++s) kmax = std::max(kmax, k[s]);
+        const uint64_t stride = kmax + 1;
+        ck(cudaSetDevice(0), "cudaSetDevice");
+        Engine& e0 = engine_for(0);
+        {
+            std::lock_guard<std::mutex> lk(e0.mutex());
+            cudaStream_t st = e0.stream();
+            void* area = nullptr;
+            ck(cudaMallocAsync(&area, S * stride * 24, st), "cudaMallocAsync merge area");
+            for (uint64_t s = 0; s < S; ++s)
+                ck(cudaMemcpyPeerAsync(static_cast<char*>(area) + s * stride * 24, 0, packs[s],
+                                       int(s % uint64_t(nd)), (k[s] + 1) * 24, st),
+                   "peer copy candidates");
+            double fl = 0.0;
+            try {
+                rc = e0.merge(static_cast<const double*>(area), uint32_t(S), stride, out, count, &fl, st);
+            } catch (...) {
+                cudaFreeAsync(area, st);
+                free_packs();
+                throw;
+            }
+            ck(cudaFreeAsync(area, st), "cudaFreeAsync");
+            ck(cudaStreamSynchronize(st), "sync");
+            if (rc == VQHULL_ERETRY && attempt == 0) {
+                floor_m = fl;
+                continue;
+            }
+        }
+        break;
+    }
+    free_packs();
+    return rc;
+}
+
+// devices the drop-in entry point uses: VQHULL_GPUS, else 1 (or as many as
+// the 32-bit per-device limit needs)
+int compute_shards(uint64_t n) {
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess) {
+        cudaGetLastError();
+        ndev = 0;
+    }
+    if (const char* e = getenv("VQHULL_GPUS")) {
+        const int g = atoi(e);
+        if (g >= 1) return g;
+    }
+    const uint64_t need = (n + 0xfffffffdull) / 0xfffffffeull;  // shards below 2^32 - 1 points
+    return int(std::max<uint64_t>(1, need));
 }
 
 bool is_device_ptr(const void* p) {
@@ -1323,6 +1687,16 @@ int vqhull_compute(const double* xs, const double* ys, size_t n, int workers, si
     if (n == 0) return VQHULL_OK;
     if (!xs || !ys || !out_indices) return VQHULL_EINVAL;
     try {
+        // several GPUs (VQHULL_GPUS, or n beyond one device's 32-bit range)
+        const int shards = vqb::compute_shards(n);
+        if (shards > 1 || getenv("VQHULL_GPUS")) {
+            static_assert(sizeof(size_t) == sizeof(uint64_t), "size_t is 64-bit");
+            uint64_t h = 0;
+            const int rc = vqb::hull_multi(xs, ys, n, shards, reinterpret_cast<uint64_t*>(out_indices), &h);
+            if (rc) return rc;
+            *out_count = size_t(h);
+            return VQHULL_OK;
+        }
         Engine& e = vqb::engine();
         std::lock_guard<std::mutex> lk(e.mutex());
         std::vector<uint32_t> tmp;
@@ -1413,6 +1787,61 @@ int vqhull_cuda_extract_subsets(double* d_xs, double* d_ys, uint64_t n, const do
         std::lock_guard<std::mutex> lk(e.mutex());
         return e.extract(d_xs, d_ys, n, edge_a, edge_b, w_l, w_r, r1, has_r1, r2, has_r2,
                          static_cast<cudaStream_t>(stream));
+    } catch (const CudaError&) {
+        return VQHULL_ECUDA;
+    }
+}
+
+int vqhull_cuda_hull_multi(const double* xs, const double* ys, uint64_t n, int num_shards,
+                           uint64_t* out_indices, uint64_t* out_count) {
+    if (!out_count) return VQHULL_EINVAL;
+    *out_count = 0;
+    if (n == 0) return VQHULL_OK;
+    if (!xs || !ys || !out_indices || num_shards < 1) return VQHULL_EINVAL;
+    try {
+        return vqb::hull_multi(xs, ys, n, num_shards, out_indices, out_count);
+    } catch (const CudaError&) {
+        return VQHULL_ECUDA;
+    }
+}
+
+int vqhull_cuda_shard_candidates(const double* d_xs, const double* d_ys, uint64_t n, uint64_t offset,
+                                 double margin_floor, double* d_pack, uint64_t cap_rows, uint64_t* count,
+                                 void* stream) {
+    if (!count) return VQHULL_EINVAL;
+    *count = 0;
+    if (n > 0 && (!d_xs || !d_ys)) return VQHULL_EINVAL;
+    if (!(margin_floor >= 0.0)) return VQHULL_EINVAL;
+    try {
+        Engine& e = vqb::engine();
+        std::lock_guard<std::mutex> lk(e.mutex());
+        return e.shard(d_xs, d_ys, n, offset, margin_floor, d_pack, cap_rows, count,
+                       static_cast<cudaStream_t>(stream));
+    } catch (const CudaError&) {
+        return VQHULL_ECUDA;
+    }
+}
+
+int vqhull_cuda_shard_repack(double* d_pack, uint64_t cap_rows, void* stream) {
+    try {
+        Engine& e = vqb::engine();
+        std::lock_guard<std::mutex> lk(e.mutex());
+        return e.repack(d_pack, cap_rows, static_cast<cudaStream_t>(stream));
+    } catch (const CudaError&) {
+        return VQHULL_ECUDA;
+    }
+}
+
+int vqhull_cuda_merge_candidates(const double* d_packs, uint32_t nranks, uint64_t stride_rows,
+                                 uint64_t* out_indices, uint64_t* out_count, double* margin_floor,
+                                 void* stream) {
+    if (!out_count || !d_packs || !out_indices) return VQHULL_EINVAL;
+    *out_count = 0;
+    try {
+        Engine& e = vqb::engine();
+        std::lock_guard<std::mutex> lk(e.mutex());
+        return e.merge(d_packs, nranks, stride_rows, out_indices, out_count, margin_floor,
+                       static_cast<cudaStream_t>(stream));
     } catch (const CudaError&) {
         return VQHULL_ECUDA;
     }

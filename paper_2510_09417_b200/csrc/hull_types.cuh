@@ -175,6 +175,9 @@ struct FilterArgs {
     void* part;          // per-CTA partials
     RootInfo* root_w;
     ChildRec* slot;      // the first level's slot table (1 slot)
+    double* kx;          // sharded hull: a second copy of the survivors (nullptr: none)
+    double* ky;
+    uint32_t* kid;
 };
 
 struct LevelArgs {
@@ -248,6 +251,25 @@ struct TailArgs {
     const uint32_t* p_idx;    // &RootInfo::p_idx (the frame vertex)
     const RootInfo* root;
     uint32_t* report;         // [8 words: state, h, nonfinite, unsafe, filter, survivors, 0] + level infos
+};
+
+// Sharded hull certificate (shard.cu): polygon of at most kCertMax vertices
+// of the local hull, the three chord forms per vertex, the wedge table.
+constexpr uint32_t kCertMax = 16384;
+constexpr uint32_t kCertBuckets = 16384;
+struct CertHead {
+    uint32_t K;        // vertices (0: no certificate)
+    uint32_t j0;       // vertex of the smallest angle around c
+    uint32_t valid;
+    uint32_t pad;
+    double cx, cy;     // centre, verified inside conv(Q)
+    double M;          // max |coordinate| of the vertices and c
+    double Me;         // margin scale max(M, floor): margin 2^-32 Me
+};
+struct CertRec {
+    double ra, rb, rg;  // chord c -> v_j        (drop side: fma(a, x, b*y) < g)
+    double ba, bb, bg;  // chord v_j -> c
+    double ea, eb, eg;  // chord v_j -> v_{j+1}
 };
 
 // One-CTA hull of a tiny input (kernels.cu, tiny_hull_kernel).

@@ -369,8 +369,14 @@ __device__ __forceinline__ uint32_t f32_order_key(double v) {
     return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
 }
 
-// diagnostics (VQHULL_SAMPLE_TRACE): %globaltimer stamps of the sample kernel
+// diagnostics (VQHULL_SAMPLE_TRACE, build with -DVQB_STAMPS): %globaltimer
+// stamps of the sample, filter and tail kernels; compiled out otherwise
 __device__ unsigned long long g_strace[8];
+#ifdef VQB_STAMPS
+#define VQB_STAMP(...) __VA_ARGS__
+#else
+#define VQB_STAMP(...)
+#endif
 __device__ __forceinline__ unsigned long long gtimer_ns() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -600,7 +606,7 @@ __global__ void __launch_bounds__(256, 2) poly_sample_kernel(const double* __res
     };
     const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
     const uint32_t stride = gridDim.x * blockDim.x;
-    if (tid == 0) g_strace[0] = gtimer_ns();
+    VQB_STAMP(if (tid == 0) g_strace[0] = gtimer_ns();)
     const bool vec = ((reinterpret_cast<uintptr_t>(xs) | reinterpret_cast<uintptr_t>(ys)) & 15u) == 0;
     if (vec) {
         const uint32_t npair = uint32_t(n / 2);
@@ -644,7 +650,7 @@ __global__ void __launch_bounds__(256, 2) poly_sample_kernel(const double* __res
         for (uint32_t i = tid; i < n; i += stride)
             if (((i >> (kSampleShift + 1)) & smask) == 0) visit_xy(i, xs[i], ys[i]);
     }
-    if (threadIdx.x == 0) atomicMax(&g_strace[1], gtimer_ns());
+    VQB_STAMP(if (threadIdx.x == 0) atomicMax(&g_strace[1], gtimer_ns());)
     // Reductions.  A vertex only has to be SOME input point (see
     // poly_finish_warp), so the CTAs combine their directional extremes with
     // one 64-bit atomicMax per direction on {order key of the value rounded to
@@ -697,7 +703,7 @@ __global__ void __launch_bounds__(256, 2) poly_sample_kernel(const double* __res
     __syncthreads();
     if (!s_last) return;
     __threadfence();
-    if (threadIdx.x == 0) g_strace[2] = gtimer_ns();
+    VQB_STAMP(if (threadIdx.x == 0) g_strace[2] = gtimer_ns();)
     // sums over the CTA partials: strided per thread, then a fixed tree
     sx = sy = sn = 0.0;
     for (uint32_t c = threadIdx.x; c < gridDim.x; c += blockDim.x) {
@@ -738,11 +744,11 @@ __global__ void __launch_bounds__(256, 2) poly_sample_kernel(const double* __res
         keys[threadIdx.x] = 0ull;     // re-arm for the next call
     }
     __syncthreads();
-    if (threadIdx.x == 0) g_strace[3] = gtimer_ns();
+    VQB_STAMP(if (threadIdx.x == 0) g_strace[3] = gtimer_ns();)
     if (threadIdx.x >= 32) return;
     poly_finish_warp(s_fin, xs, ys, root, with_pq != 0);
     if (threadIdx.x != 0) return;
-    g_strace[4] = gtimer_ns();
+    VQB_STAMP(g_strace[4] = gtimer_ns();)
     side_ctr[0] = 0ull;  // the root pass's counter (another root mode may have used it)
     *ticket = 0;
 }

@@ -67,4 +67,21 @@ size_t tail_smem_bytes();
 int occupancy_tail();
 cudaError_t launch_tail(const TailArgs& a, int grid, cudaStream_t st);
 
+// sharded hull (shard.cu)
+void launch_cert_build(const uint32_t* hull, uint32_t h, const double* xs, const double* ys, double floor_m,
+                       CertHead* head, CertRec* rec, float* asc, uint32_t* tab, cudaStream_t st);
+void launch_certify(const double* xs, const double* ys, const uint32_t* ids, uint64_t n_host,
+                    const uint32_t* n_dev, const CertHead* head, const CertRec* rec, const float* asc,
+                    const uint32_t* tab, double* rx, double* ry, uint32_t* rid, uint32_t* rcount,
+                    unsigned long long* amax_bits, int grid, cudaStream_t st);
+size_t sort_temp_bytes(uint32_t n);
+cudaError_t launch_sort_ids(void* temp, size_t temp_bytes, const uint32_t* keys_in, uint32_t* keys_out,
+                            uint32_t* vals_in, uint32_t* vals_out, uint32_t n, int end_bit, cudaStream_t st);
+void launch_pack(const double* rx, const double* ry, const uint32_t* sorted_id, const uint32_t* perm,
+                 uint32_t count, uint32_t cap, uint64_t offset, double* pack, cudaStream_t st);
+void launch_merge_gather(const double* packs, uint64_t stride_rows, const uint64_t* starts, uint32_t nranks,
+                         uint64_t total, double* mx, double* my, uint64_t* mg, uint32_t* unsorted,
+                         cudaStream_t st);
+void launch_map_gidx(const uint32_t* pos, uint64_t h, const uint64_t* mg, uint64_t* out, cudaStream_t st);
+
 }  // namespace vqb

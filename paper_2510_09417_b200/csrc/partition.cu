@@ -1519,7 +1519,7 @@ __device__ __forceinline__ void filter_warp_fold(ExtKey& lo, ExtKey& hi, double&
 
 __global__ void __launch_bounds__(kCtlThreads, 3) root_filter_tma(FilterArgs a) {
     VQB_PDL();
-    if (threadIdx.x == 0) atomicMin(&g_strace[5], gtimer_ns());
+    VQB_STAMP(if (threadIdx.x == 0) atomicMin(&g_strace[5], gtimer_ns());)
     extern __shared__ __align__(128) unsigned char dsm[];
     RootRing4& ring = *reinterpret_cast<RootRing4*>(dsm);
     __shared__ uint32_t s_cnt[2][kWarps];                      // survivors per warp and tile
@@ -1598,9 +1598,15 @@ __global__ void __launch_bounds__(kCtlThreads, 3) root_filter_tma(FilterArgs a) 
                 const uint32_t idx = s_surv[par][warp][j];
                 const uint32_t p = o + j;
                 VQB_CHECK(p < a.out_cap, 15, p, a.out_cap);
-                a.ox[p] = ring.x[s][idx];
-                a.oy[p] = ring.y[s][idx];
+                const double u = ring.x[s][idx], w = ring.y[s][idx];
+                a.ox[p] = u;
+                a.oy[p] = w;
                 a.oid[p] = tbase + idx;
+                if (a.kx) {  // sharded hull: the certificate's copy (shard.cu)
+                    a.kx[p] = u;
+                    a.ky[p] = w;
+                    a.kid[p] = tbase + idx;
+                }
             }
         };
         for (uint32_t k = 0; k < nt; ++k) {
@@ -1761,7 +1767,7 @@ __global__ void __launch_bounds__(kCtlThreads, 3) root_filter_tma(FilterArgs a) 
     a.slot[0] = ch;
     *a.ctr = 0;  // re-arm for the next call
     *a.ticket = 0;
-    g_strace[6] = gtimer_ns();
+    VQB_STAMP(g_strace[6] = gtimer_ns();)
 }
 
 // ===========================================================================

@@ -287,7 +287,7 @@ __global__ void __launch_bounds__(kThreads, 2) tail_kernel(const __grid_constant
         A.state[0] = uint32_t(A.l0);
         A.state[1] = 0u;
         if (A.trace) A.trace[0] = global_ns();
-        g_strace[7] = global_ns();
+        VQB_STAMP(g_strace[7] = global_ns();)
     }
     int in = A.in0;  // the buffer level l0 reads
     for (int li = 0;; ++li) {

@@ -1,102 +1,135 @@
 """Multi-GPU sharded hull: one process per GPU, torch.distributed for plumbing.
 
-Scheme (BASELINE north star): rank r owns a contiguous shard
-[offset_r, offset_r + n_r) of the global point sequence and computes its local
-hull with the sm_100a path.  The local hull vertices — a few thousand
-(x, y, global index) candidates — are exchanged with ONE all-gather (NCCL over
-NVLink on GPUs; gloo in the CPU tests), and every rank computes the hull of
-the candidates (the same sm_100a path) and maps it back to global indices.
+Scheme (BASELINE north star), exact by construction:
 
-Exactness: conv(∪ local hulls) = conv(all points), and each local hull carries
-first-occurrence indices within its shard; candidates are ordered by global
-index before the final hull, so a vertex present in several shards resolves
-to its smallest global index — the reference's first-occurrence rule
-(vqhull_c.cpp:51-61).  Under the reference's non-robust f64 predicates the
-merged result can differ from a single global pass on near-degenerate inputs
-(probe P3: circle); tests gate each distribution on the oracle.
+1. rank r owns a contiguous shard [offset_r, offset_r + n_r) of the global
+   point sequence and runs the local stage on its GPU
+   (``vqhull_cuda_shard_candidates``): its local hull with the sm_100a path,
+   then a certificate that keeps every point it cannot PROVE to lie deep
+   inside that local hull (the split root's margin argument),
+   sorted by global index and packed behind a header row {count, M_eff, A};
+2. ONE all-gather of the packs (NCCL over NVLink on GPUs; gloo in the CPU
+   tests); a second, count-padded round only when a rank has more than
+   ``GATHER_CAP`` candidates;
+3. every rank merges (``vqhull_cuda_merge_candidates``): the ordinary hull
+   over the union of the candidates, in global-index order so that equal
+   coordinates resolve to their first occurrence (vqhull_c.cpp:51-61), mapped
+   back to global indices.
 
-There is no data-path collective other than this candidate all-gather: the
-partition work itself is embarrassingly parallel across shards.
+Why not just the hull of the local hulls: the reference's f64 predicates are
+not robust, so a global recursion can keep near-collinear points a shard's
+recursion dropped (circle 1e7, 9,994,016 vs 9,994,044 vertices).
+Only points that provably cannot affect any decision of the global recursion
+are left behind, so the merge IS the reference's global recursion.  The
+margin's rounding bound needs the largest coordinate in play within 2^12 of
+every shard's scale; the merge checks it and, if a shard's scale is too
+small (wildly different shards), every rank recomputes its candidates with a
+margin floor (``RetryWithFloor``) — one more round, then it always holds.
+
+There is no data-path collective other than this candidate all-gather.
 """
 from __future__ import annotations
 
-from typing import Callable, Optional
+from typing import Callable, Optional, Tuple
 
 import torch
 import torch.distributed as dist
 
-LocalHull = Callable[[torch.Tensor, torch.Tensor], torch.Tensor]
-
-
-def _default_local_hull(x: torch.Tensor, y: torch.Tensor) -> torch.Tensor:
-    from . import hull_device
-
-    return hull_device(x, y)
-
-
-# candidates a rank sends in the one-collective fast path (local hulls are a
-# few dozen to a few thousand vertices; larger ones take a second round)
+# candidates a rank sends in the one-collective fast path (disk 4e9 over 8
+# GPUs: ~3k per rank); larger candidate sets take a second round
 GATHER_CAP = 8192
 
+LocalStage = Callable[..., Tuple[torch.Tensor, int]]
 
-def gather_candidates(cx: torch.Tensor, cy: torch.Tensor, cg: torch.Tensor,
-                      group: Optional[dist.ProcessGroup] = None, cap: Optional[int] = None):
-    """All-gather variable-length (x, y, global index) candidate lists.
+_LAST = {"launches": 0, "info": {}}
 
-    Packs each candidate as three 64-bit words (the index bit-cast into f64
-    storage) behind a header row holding the count, padded to `cap` rows, so
-    ONE collective moves counts and payload.  If any rank has more than `cap`
-    candidates (every rank sees that in the headers), a second all-gather
-    padded to the largest count follows.
-    """
-    dev = cx.device
-    k = cx.numel()
+
+def last_launches() -> int:
+    """Kernels the last sharded_hull launched on this rank (local + merge)."""
+    return int(_LAST["launches"])
+
+
+def last_info() -> dict:
+    """Candidate counts, rounds and retries of the last sharded_hull."""
+    return dict(_LAST["info"])
+
+
+class DeviceStages:
+    """The sm_100a local stage and merge (the product path)."""
+
+    def __init__(self):
+        from . import lib
+
+        lib()  # fail loudly without the native library
+
+    def local(self, x, y, offset: int, cap: int, floor: float):
+        from . import shard_candidates, stats
+
+        pack, k = shard_candidates(x, y, offset, cap, floor)
+        return pack, k, int(stats()["launches"])
+
+    def repack(self, pack):
+        from . import shard_repack
+
+        shard_repack(pack)
+
+    def merge(self, packs):
+        from . import merge_candidates, stats
+
+        out = merge_candidates(packs)
+        return out, int(stats()["launches"])
+
+
+def _gather(pack: torch.Tensor, stages, group) -> Tuple[torch.Tensor, list, int]:
     world = dist.get_world_size(group)
-    cap = GATHER_CAP if cap is None else cap
+    # gloo moves host tensors: device packs are staged through host memory
+    # (the single-GPU test of the multi-rank path); NCCL gathers in HBM
+    host = pack.is_cuda and dist.get_backend(group) == "gloo"
 
-    def packed(rows: int, with_header: bool) -> torch.Tensor:
-        h = 1 if with_header else 0
-        pack = torch.zeros((rows + h, 3), dtype=torch.float64, device=dev)
-        if with_header:
-            pack[0, 0] = float(k)
-        m = min(k, rows)
-        pack[h:h + m, 0] = cx[:m]
-        pack[h:h + m, 1] = cy[:m]
-        pack[h:h + m, 2] = cg[:m].to(torch.int64).view(torch.float64)
-        return pack
+    def all_gather(t):
+        src = t.cpu() if host else t
+        bufs = [torch.empty_like(src) for _ in range(world)]
+        dist.all_gather(bufs, src, group=group)
+        out = torch.stack(bufs)
+        return out.to(t.device) if host else out
 
-    first = packed(cap, True)
-    bufs = [torch.empty_like(first) for _ in range(world)]
-    dist.all_gather(bufs, first, group=group)
-    counts = [int(c) for c in torch.stack([b[0, 0] for b in bufs]).cpu().tolist()]
-    if max(counts) <= cap:
-        parts = [b[1:1 + c] for b, c in zip(bufs, counts)]
-    else:  # rare: a local hull larger than the fast path's capacity
-        kmax = max(counts)
-        full = packed(kmax, False)
-        bufs = [torch.empty_like(full) for _ in range(world)]
-        dist.all_gather(bufs, full, group=group)
-        parts = [b[:c] for b, c in zip(bufs, counts)]
-    allp = torch.cat(parts, dim=0)
-    gidx = allp[:, 2].contiguous().view(torch.int64)
-    return allp[:, 0].contiguous(), allp[:, 1].contiguous(), gidx
+    packs = all_gather(pack)
+    counts = [int(c) for c in packs[:, 0, 0].cpu().tolist()]
+    rounds = 1
+    kmax = max(counts)
+    if kmax > pack.shape[0] - 1:  # rare: more candidates than the fast path's room
+        big = torch.empty((kmax + 1, 3), dtype=pack.dtype, device=pack.device)
+        stages.repack(big)
+        packs = all_gather(big)
+        rounds = 2
+    return packs, counts, rounds
 
 
 def sharded_hull(x: torch.Tensor, y: torch.Tensor, offset: int,
-                 group: Optional[dist.ProcessGroup] = None,
-                 local_hull: Optional[LocalHull] = None) -> torch.Tensor:
+                 group: Optional[dist.ProcessGroup] = None, stages=None,
+                 cap: Optional[int] = None) -> torch.Tensor:
     """Global clockwise hull indices (int64, on x's device) of the union of
-    every rank's shard.  Called by every rank of `group` with its own shard."""
-    hull = local_hull or _default_local_hull
-    li = hull(x, y).to(torch.int64)
-    cx, cy = x[li], y[li]
-    cg = li + int(offset)
-    ax, ay, ag = gather_candidates(cx, cy, cg, group)
-    # first occurrence == smallest global index: order candidates by it
-    order = torch.argsort(ag)
-    ax, ay, ag = ax[order].contiguous(), ay[order].contiguous(), ag[order]
-    fi = hull(ax, ay).to(torch.int64)
-    return ag[fi]
+    every rank's shard.  Called by every rank of `group` with its own shard;
+    ranks must hold contiguous shards in rank (= offset) order."""
+    stages = stages or DeviceStages()
+    cap = GATHER_CAP if cap is None else cap
+    floor = 0.0
+    retries = 0
+    while True:
+        pack, k, l_local = stages.local(x, y, int(offset), cap, floor)
+        packs, counts, rounds = _gather(pack, stages, group)
+        try:
+            out, l_merge = stages.merge(packs)
+            break
+        except Exception as e:  # RetryWithFloor: every rank sees the same headers
+            if getattr(e, "floor", None) is None or retries:
+                raise
+            floor = e.floor
+            retries += 1
+    _LAST["launches"] = l_local + l_merge
+    _LAST["info"] = {"candidates_per_rank": counts, "candidates_total": int(sum(counts)),
+                     "gather_rounds": rounds, "margin_retries": retries, "hull": int(out.numel())}
+    return out
 
 
 def shard_range(n_total: int, rank: int, world: int):

@@ -1,0 +1,225 @@
+"""GPU: the sharded hull with the sm_100a local stage and merge.
+
+* the single-process multi-device C ABI (vqhull_cuda_hull_multi, and
+  vqhull_compute with VQHULL_GPUS) with several shards — on this one-GPU pool
+  the shards of a device run one after another, the merge is the same;
+* the torch.distributed path (paper_2510_09417_b200.distributed) at world
+  size 2: two processes on cuda:0, candidates exchanged over gloo through
+  host memory (no rank's kernels wait on another's);
+* against the reference's golden lists and the oracle, circle included:
+  there the hull of the local hulls is NOT the reference's answer, the
+  certified candidates are.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import golden_io as G
+
+pytestmark = pytest.mark.gpu
+
+
+def _golden(name):
+    return G.configs()[name]
+
+
+def _check_golden(oracle, got, cfg):
+    assert got.size == cfg["h"]
+    assert f"{oracle.fnv1a64(got):016x}" == cfg["fnv1a64_u64le"]
+
+
+@pytest.mark.parametrize("shards", [1, 2, 3, 8])
+def test_hull_multi_config5_proxy(vq, cuda, oracle, shards):
+    cfg = _golden("config5_proxy_disk_4e7_s5")
+    xs, ys = vq.generate(cfg["kind"], cfg["n"], cfg["seed"])
+    got = vq.hull_multi(xs, ys, shards)
+    _check_golden(oracle, got, cfg)
+    s = vq.stats()
+    assert s["hull_size"] == cfg["h"]
+
+
+@pytest.mark.parametrize("kind,n,seed,shards", [("disk", 1_000_000, 1, 4), ("square", 3_000_000, 2, 2),
+                                                ("kuzmin", 2_000_000, 4, 5), ("circle", 1_000_000, 3, 2),
+                                                ("circle", 2_000_000, 7, 8), ("disk", 10_000, 2, 16)])
+def test_hull_multi_vs_oracle(vq, cuda, oracle, kind, n, seed, shards):
+    xs, ys = vq.generate(kind, n, seed)
+    got = vq.hull_multi(xs, ys, shards)
+    assert np.array_equal(got, oracle.hull_indices(xs, ys))
+
+
+def test_hull_multi_config3_circle_and_naive_merge_differs(vq, cuda, oracle):
+    """Config 3 (every point on the circle) in 4 shards equals the reference
+    golden; the hull of the 4 local hulls does not."""
+    import torch
+
+    cfg = _golden("config3_circle_1e7_s3")
+    xs, ys = vq.generate(cfg["kind"], cfg["n"], cfg["seed"])
+    got = vq.hull_multi(xs, ys, 4)
+    _check_golden(oracle, got, cfg)
+    # the naive scheme: hull of the union of local hulls
+    cand = []
+    n = xs.size
+    for r in range(4):
+        a, b = r * n // 4, (r + 1) * n // 4
+        X, Y = torch.from_numpy(xs[a:b]).cuda(), torch.from_numpy(ys[a:b]).cuda()
+        cand.append(vq.hull_device(X, Y).cpu().numpy() + a)
+    cand = np.sort(np.concatenate(cand))
+    naive = cand[vq.hull_indices(xs[cand], ys[cand]).astype(np.int64)]
+    assert not np.array_equal(naive.astype(np.uint64), got)
+
+
+def test_hull_multi_duplicates_across_shards(vq, cuda, oracle):
+    xs, ys = vq.generate("disk", 400_000, 8)
+    xs[-5000:], ys[-5000:] = xs[:5000], ys[:5000]  # copies in the last shard
+    got = vq.hull_multi(xs, ys, 4)
+    ref = oracle.hull_indices(xs, ys)
+    assert np.array_equal(got, ref)
+    assert got.max() < 400_000 - 5000  # first occurrences win
+
+
+def test_hull_multi_margin_retry(vq, cuda, oracle):
+    """Shards of wildly different scale: the merge's scale check asks for the
+    candidates again with a margin floor."""
+    xs, ys = vq.generate("disk", 200_000, 11)
+    xs[:100_000] *= 1e-7
+    ys[:100_000] *= 1e-7
+    xs[100_000:] *= 1e3
+    ys[100_000:] *= 1e3
+    got = vq.hull_multi(xs, ys, 2)
+    assert np.array_equal(got, oracle.hull_indices(xs, ys))
+
+
+def test_hull_multi_errors(vq, cuda):
+    xs, ys = vq.generate("disk", 50_000, 1)
+    xs[40_000] = np.nan
+    with pytest.raises(vq.VQhullError) as e:
+        vq.hull_multi(xs, ys, 3)
+    assert e.value.rc == 1
+    assert vq.hull_multi(np.zeros(0), np.zeros(0), 2).size == 0
+    # the engines are healthy after the rejected call
+    xs, ys = vq.generate("square", 20_000, 2)
+    assert vq.hull_multi(xs, ys, 2).size > 0
+
+
+def test_vqhull_compute_through_shards(vq, cuda, oracle, monkeypatch):
+    """The drop-in entry point with VQHULL_GPUS set takes the sharded path."""
+    cfg = _golden("config1_disk_1e6_s1")
+    xs, ys = vq.generate(cfg["kind"], cfg["n"], cfg["seed"])
+    for g in ("1", "3"):
+        monkeypatch.setenv("VQHULL_GPUS", g)
+        rc, got = vq.vqhull_compute(xs, ys)
+        assert rc == 0
+        _check_golden(oracle, got, cfg)
+    monkeypatch.delenv("VQHULL_GPUS")
+
+
+def test_shard_candidates_pack_layout(vq, cuda, oracle):
+    """The local stage's pack: header {count, M_eff, A}, candidates sorted by
+    global index, every local hull vertex among them."""
+    import torch
+
+    xs, ys = vq.generate("disk", 2_000_000, 3)
+    X, Y = torch.from_numpy(xs).cuda(), torch.from_numpy(ys).cuda()
+    off = 123_456_789_012
+    pack, k = vq.shard_candidates(X, Y, off, cap=1 << 16)
+    P = pack.cpu().numpy()
+    assert P[0, 0] == k and 0 < k < 20_000
+    assert 0.9 < P[0, 1] <= 1.0 and P[0, 2] <= 1.0
+    g = P[1:1 + k, 2].copy().view(np.int64)
+    assert np.all(np.diff(g) > 0) and g.min() >= off
+    loc = g - off
+    assert np.array_equal(P[1:1 + k, 0], xs[loc]) and np.array_equal(P[1:1 + k, 1], ys[loc])
+    h = oracle.hull_indices(xs, ys).astype(np.int64)
+    assert np.isin(h, loc).all()
+    s = vq.stats()
+    assert s["shard_candidates"] == k and s["shard_cert_vertices"] == h.size
+    assert s["shard_tested"] < 0.05 * xs.size  # the filter pass's survivors only
+    # a second, smaller pack then the repack
+    small, k2 = vq.shard_candidates(X, Y, off, cap=4)
+    assert k2 == k and small[0, 0].item() == k
+    big = torch.empty((k + 1, 3), dtype=torch.float64, device="cuda")
+    vq.shard_repack(big)
+    assert np.array_equal(big.cpu().numpy()[: k + 1], P[: k + 1])
+
+
+# --- torch.distributed at world size 2 on one GPU (gloo, host staging) -------
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, kind, n, seed, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2510_09417_b200 as vq
+        from paper_2510_09417_b200 import distributed as D
+
+        xs, ys = vq.generate(kind, n, seed)
+        off, cnt = D.shard_range(n, rank, world)
+        X = torch.from_numpy(xs[off:off + cnt].copy()).cuda()
+        Y = torch.from_numpy(ys[off:off + cnt].copy()).cuda()
+        g = D.sharded_hull(X, Y, off)
+        q.put((rank, g.cpu().numpy(), D.last_info()))
+    except Exception as e:  # noqa: BLE001
+        q.put((rank, repr(e), None))
+    finally:
+        dist.destroy_process_group()
+
+
+def _run_world(kind, n, seed, world=2):
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, kind, n, seed, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in procs:
+        r, g, info = q.get(timeout=600)
+        res[r] = (g, info)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    return res
+
+
+def test_world2_config5_proxy(vq, cuda, oracle):
+    cfg = _golden("config5_proxy_disk_4e7_s5")
+    res = _run_world(cfg["kind"], cfg["n"], cfg["seed"])
+    for r in (0, 1):
+        g, info = res[r]
+        assert isinstance(g, np.ndarray), g
+        _check_golden(oracle, g.astype(np.uint64), cfg)
+        assert info["gather_rounds"] == 1
+
+
+@pytest.mark.parametrize("kind,n,seed", [("square", 4_000_000, 2), ("kuzmin", 4_000_000, 4),
+                                         ("circle", 1_000_000, 3)])
+def test_world2_vs_oracle(vq, cuda, oracle, kind, n, seed):
+    res = _run_world(kind, n, seed)
+    xs, ys = vq.generate(kind, n, seed)
+    ref = oracle.hull_indices(xs, ys)
+    for r in (0, 1):
+        g, _ = res[r]
+        assert isinstance(g, np.ndarray), g
+        assert np.array_equal(g.astype(np.uint64), ref)
+
+
+@pytest.mark.slow
+def test_world2_config3_circle(vq, cuda, oracle):
+    cfg = _golden("config3_circle_1e7_s3")
+    res = _run_world(cfg["kind"], cfg["n"], cfg["seed"])
+    for r in (0, 1):
+        _check_golden(oracle, res[r][0].astype(np.uint64), cfg)
