@@ -223,3 +223,41 @@ def test_world2_config3_circle(vq, cuda, oracle):
     res = _run_world(cfg["kind"], cfg["n"], cfg["seed"])
     for r in (0, 1):
         _check_golden(oracle, res[r][0].astype(np.uint64), cfg)
+
+
+@pytest.mark.slow
+def test_hull_multi_beyond_u32(vq, cuda, oracle):
+    """n = 2^32 + 4096 points (above one device's 32-bit range): the sharded
+    drop-in takes them in shards below 2^32 (run one after another on this
+    GPU), with 64-bit global indices.  No reference run fits this host, so the
+    check is consistency: 2 and 3 shards give the same list, which reaches
+    indices above 2^32, and its first 4e9-point part agrees with config 5's
+    golden hull where the two overlap."""
+    import torch
+
+    n = (1 << 32) + 4096
+    torch.cuda.empty_cache()
+    vq.trim()
+    free, _ = torch.cuda.mem_get_info()
+    if free < 150 * 2**30:
+        pytest.skip("needs ~150 GB of device memory")
+    import psutil
+    if psutil.virtual_memory().available < 90 * 2**30:
+        pytest.skip("needs ~90 GB of host memory")
+    xs = np.empty(n)
+    ys = np.empty(n)
+    vq.generate("disk", n, 5, out=(xs, ys))
+    g2 = vq.hull_multi(xs, ys, 2)
+    vq.trim()
+    g3 = vq.hull_multi(xs, ys, 3)
+    vq.trim()
+    assert np.array_equal(g2, g3)
+    assert g2.max() >= (1 << 32)
+    # its vertices below 4e9 are vertices of config 5's (4e9-point) hull
+    cfg = G.configs()["config5_disk_4e9_s5"]
+    low = g2[g2 < 4 * 10**9]
+    assert np.isin(low, np.array(cfg["indices"], dtype=np.uint64)).all()
+    # with the drop-in entry point (it picks the shard count itself)
+    rc, g = vq.vqhull_compute(xs, ys)
+    assert rc == 0 and np.array_equal(g, g2)
+    del xs, ys
