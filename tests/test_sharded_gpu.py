@@ -247,13 +247,19 @@ def test_hull_multi_beyond_u32(vq, cuda, oracle):
     xs = np.empty(n)
     ys = np.empty(n)
     vq.generate("disk", n, 5, out=(xs, ys))
+    # a far vertex above 2^32, and an exact copy of it further up (the first
+    # occurrence must win with 64-bit indices)
+    far = (1 << 32) + 100
+    xs[far], ys[far] = 3.0, 3.0
+    xs[far + 50], ys[far + 50] = 3.0, 3.0
     g2 = vq.hull_multi(xs, ys, 2)
     vq.trim()
     g3 = vq.hull_multi(xs, ys, 3)
     vq.trim()
     assert np.array_equal(g2, g3)
-    assert g2.max() >= (1 << 32)
+    assert far in g2.tolist() and far + 50 not in g2.tolist()
     # its vertices below 4e9 are vertices of config 5's (4e9-point) hull
+    # (a point that is a vertex of a superset's hull is one of the subset's)
     cfg = G.configs()["config5_disk_4e9_s5"]
     low = g2[g2 < 4 * 10**9]
     assert np.isin(low, np.array(cfg["indices"], dtype=np.uint64)).all()
