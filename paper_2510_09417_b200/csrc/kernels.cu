@@ -1133,29 +1133,42 @@ __device__ __forceinline__ void finisher_warp_body(FinSmem& S, uint32_t gw, uint
 
 // ===========================================================================
 // K3'' CTA finisher: one CTA solves the whole subtree of a segment of
-// kFinSmall < m <= kFinMax points in shared memory, LEVEL-SYNCHRONOUSLY:
-// every node of the current depth is partitioned in the same pass (the
-// reference's chain_recursive, hull.cpp:78-115, visited breadth-first), so
-// the serial chain is the tree depth, not the node count (a warp walking the
-// nodes one by one is latency-bound when every point is a hull vertex).
-// Per depth: (1) each point of a live node is classified against the node's
-// (p->r), (r->q) with the reference's expressions and written two-sided into
-// its node's range of the other work array (left child forward, right child
-// backward; shared-memory atomics give the slots, their order is free), and
-// the children's farthest keys are min-reduced with 64-bit shared atomics;
-// (2) points holding the minimal key register as candidates (an exact tie of
-// two candidates is resolved by (x, y, index) on a rare path); (3) children
-// with >= 2 points become the next depth's nodes (block scan), one-point
-// children are leaves.  Finally subtree sizes bottom-up and chain positions
-// top-down give chain(L) ++ [r] ++ chain(R) (assemble_chain, hull.cpp:59-73).
+// kFinSmall < m <= CAP points in shared memory, LEVEL-SYNCHRONOUSLY: every
+// node of the current depth is partitioned in the same pass (the reference's
+// chain_recursive, hull.cpp:78-115, visited breadth-first), so the serial
+// chain is the tree depth, not the node count (a warp walking the nodes one
+// by one is latency-bound when every point is a hull vertex).  Points never
+// move: each carries its node id, which becomes its child's id, then the
+// child's next-depth node id.  Per depth:
+//   (1) every live point is classified against its node's (p->r), (r->q)
+//       with the reference's exact predicates (left_diff, kernels.hpp:28-30;
+//       mask_b &= ~mask_a, :91) and its farthest key (the canonical order of
+//       kernels.hpp:41-45 as an order-preserving u64) stays in a register; the
+//       child's point count (warp-aggregated) and minimal key (shared atomic,
+//       warp-reduced first when the whole warp shares one child — the top of
+//       the subtree) are accumulated;
+//   (2) the points holding their child's minimal key register as its apex; an
+//       exact tie (real on circle-like inputs: ~2 children per segment) lists
+//       the extra candidates, resolved by smaller (x, y), then smaller index
+//       (first occurrence) on one thread;
+//   (3) children with >= 2 points become the next depth's nodes (block scan),
+//       one-point children are leaves (hull.cpp:83); the subtree's links;
+//   (4) fresh accumulators for the next depth.
+// Finally subtree sizes bottom-up and chain positions top-down give
+// chain(L) ++ [r] ++ chain(R) (assemble_chain, hull.cpp:59-73).
+// (An earlier version moved every point to its child's range each depth and
+// recomputed the keys: ~2x the instructions; a one-warp-per-segment variant
+// was latency-bound: profiles/r02_finisher_warp_bfs.md.)
 // ===========================================================================
-// diagnostics (VQHULL_FIN_TRACE): block 0's CTA-finisher per-depth timestamps
+// diagnostics (VQHULL_FIN_TRACE, build with -DVQB_STAMPS): block 0's
+// CTA-finisher per-depth timestamps
 __device__ unsigned long long g_ftrace[64];
 __device__ uint32_t g_ftrace_on;
 
 constexpr int kFcThreads = 256;
 constexpr uint16_t kDead = 0xffffu;
 constexpr uint16_t kLinkEmpty = 0, kLinkLeaf = 0x4000, kLinkNode = 0x8000;  // kind | value
+constexpr uint32_t kFcNoChild = 0xffffffffu;
 
 // shared memory of the CTA finisher for segments of at most CAP points
 // (kFinMax for the host-driven finisher kernel, kTailFinMax inside KT)
@@ -1166,37 +1179,30 @@ struct FinCtaSmemT {
     double x[CAP + 3];
     double y[CAP + 3];
     uint32_t gid[CAP + 3];
-    uint16_t work[2][CAP];
-    uint16_t wnode[2][CAP];
-    uint16_t np[2][kNodes], nr[2][kNodes], nq[2][kNodes];
-    uint16_t nlo[2][kNodes], nhi[2][kNodes], ntree[2][kNodes];
-    unsigned long long ckey[2 * kNodes];
-    uint32_t ccnt[2 * kNodes];
-    uint32_t cncand[2 * kNodes];
-    uint16_t ccand[2 * kNodes];
-    uint16_t cmap[2 * kNodes];
-    uint16_t tapex[CAP + 1];
-    uint16_t tleft[CAP + 1], tright[CAP + 1];
-    uint16_t tsize[CAP + 1], tstart[CAP + 1];
+    uint32_t ccnt[CAP];             // per child: points | candidates << 16
+    uint16_t pnode[CAP];            // per point: child id of the last depth (kDead: done)
+    uint16_t np[2][kNodes], nr[2][kNodes], nq[2][kNodes], ntree[2][kNodes];
+    uint16_t ccand[CAP];            // per child: its apex
+    uint16_t cmap[CAP];             // per child: next-depth node id (kDead: none)
+    uint16_t tlist[CAP];            // extra candidates of tied children
+    uint16_t tapex[CAP + 1], tleft[CAP + 1], tright[CAP + 1];
     uint16_t lvl_start[CAP + 2];
+    union {
+        unsigned long long ckey[CAP];  // per child: minimal key (during the BFS)
+        struct {
+            uint16_t tsize[CAP + 1];
+            uint16_t tstart[CAP + 1];
+        } t;                           // subtree sizes / chain positions (emission)
+    } u;
     uint32_t wsum[kFcThreads / 32];
-    uint32_t tie;
+    uint32_t ntie;
     uint32_t nnext;
 };
 using FinCtaSmem = FinCtaSmemT<int(kFinMax)>;
 
 template <class SM>
 __device__ __forceinline__ uint32_t fc_link_size(const SM& S, uint16_t l) {
-    return (l & kLinkNode) ? S.tsize[l & 0x3fff] : ((l & kLinkLeaf) ? 1u : 0u);
-}
-
-// the farthest-point key of local point lid in child (node c, side s)
-template <class SM>
-__device__ __forceinline__ unsigned long long fc_key(const SM& S, int cp, int c, int s, uint16_t lid) {
-    const uint16_t p = S.np[cp][c], r = S.nr[cp][c], q = S.nq[cp][c];
-    const double fx = s ? dsub(S.x[q], S.x[r]) : dsub(S.x[r], S.x[p]);
-    const double fy = s ? dsub(S.y[q], S.y[r]) : dsub(S.y[r], S.y[p]);
-    return key_of(lat_off(fx, fy, S.x[lid], S.y[lid]));
+    return (l & kLinkNode) ? S.u.t.tsize[l & 0x3fff] : ((l & kLinkLeaf) ? 1u : 0u);
 }
 
 template <int CAP>
@@ -1206,6 +1212,7 @@ __device__ __forceinline__ void finisher_cta_body(FinCtaSmemT<CAP>& S, const Fin
                                                   const uint32_t* __restrict__ iid, uint32_t* chain,
                                                   uint32_t* fin_count) {
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    constexpr int kFcItems = (CAP + kFcThreads - 1) / kFcThreads;  // points per thread
     const uint32_t nfin2 = info->nfin2;
     for (uint32_t f = blockIdx.x; f < nfin2; f += gridDim.x) {
         const uint32_t fi = fin_cap - 1u - f;
@@ -1217,120 +1224,116 @@ __device__ __forceinline__ void finisher_cta_body(FinCtaSmemT<CAP>& S, const Fin
             S.x[i] = ix[rec.c.begin + i];
             S.y[i] = iy[rec.c.begin + i];
             S.gid[i] = iid[rec.c.begin + i];
-            S.work[0][i] = uint16_t(i);
-            S.wnode[0][i] = 0;
-            S.wnode[1][i] = kDead;
         }
         if (tid == 0) {
             S.x[P0] = rec.c.px; S.y[P0] = rec.c.py; S.gid[P0] = 0xffffffffu;
             S.x[Q0] = rec.c.qx; S.y[Q0] = rec.c.qy; S.gid[Q0] = 0xffffffffu;
             S.x[R0] = rec.c.rx; S.y[R0] = rec.c.ry; S.gid[R0] = rec.c.r_idx;
-            S.np[0][0] = P0; S.nr[0][0] = R0; S.nq[0][0] = Q0;
-            S.nlo[0][0] = 0; S.nhi[0][0] = uint16_t(m); S.ntree[0][0] = 0;
+            S.np[0][0] = P0; S.nr[0][0] = R0; S.nq[0][0] = Q0; S.ntree[0][0] = 0;
             S.tapex[0] = R0; S.tleft[0] = kLinkEmpty; S.tright[0] = kLinkEmpty;
             S.lvl_start[0] = 0; S.lvl_start[1] = 1;
-            S.tie = 0;
+            S.ntie = 0;
+            S.cmap[0] = 0;  // depth 0: every point's "child" 0 maps to node 0
         }
         if (tid < 2) {
-            S.ckey[tid] = kNoKey; S.ccnt[tid] = 0; S.cncand[tid] = 0;
+            S.u.ckey[tid] = kNoKey;
+            S.ccnt[tid] = 0;
         }
         __syncthreads();
         uint32_t nnodes = 1, ntree = 1;
         int cur = 0, depth = 0;
-        const bool ftr = g_ftrace_on && blockIdx.x == 0 && tid == 0;
-        if (ftr) { g_ftrace[0] = m; g_ftrace[1] = gtimer_ns(); }
+        VQB_STAMP(const bool ftr = g_ftrace_on && blockIdx.x == 0 && tid == 0;
+                  if (ftr) { g_ftrace[0] = m; g_ftrace[1] = gtimer_ns(); })
         while (nnodes > 0) {
-            if (ftr && depth < 38) g_ftrace[2 + depth] = gtimer_ns();
+            VQB_STAMP(if (ftr && depth < 38) g_ftrace[2 + depth] = gtimer_ns();)
+            if (depth > CAP + 2) {  // every depth consumes >= 1 apex
+                if (tid == 0) g_vqb_fault = 5u;
+                break;
+            }
             const int nxt = cur ^ 1;
-            // (1) classify, claim two-sided slots, min-reduce the children's keys.
-            // Near the top of the subtree most points share one of a few
-            // children, so the slot claims are warp-aggregated (one shared
-            // atomic per child per warp) and a key only attempts the min
-            // when it beats the value already there.
-            // all of a thread's points first (independent f64 chains overlap),
-            // then the warp-aggregated claims
-            constexpr int kFcItems = CAP / kFcThreads;  // points per thread
-            constexpr int kFcChunk = kFcItems < 4 ? kFcItems : 4;  // in registers at a time
-            for (int k0 = 0; k0 < kFcItems; k0 += kFcChunk) {
-            uint32_t chv[kFcChunk];
-            uint16_t lidv[kFcChunk];
-#pragma unroll
-            for (int kk = 0; kk < kFcChunk; ++kk) {
-                const int k = k0 + kk;
-                const uint32_t i = uint32_t(k) * kFcThreads + tid;
-                const uint16_t c = i < m ? S.wnode[cur][i] : kDead;
-                chv[kk] = 0xffffffffu;
-                lidv[kk] = 0;
-                if (c != kDead) {
-                    const uint16_t lid = S.work[cur][i];
-                    lidv[kk] = lid;
-                    const uint16_t p = S.np[cur][c], r = S.nr[cur][c], q = S.nq[cur][c];
-                    const double u = S.x[lid], w = S.y[lid];
-                    const double A = dsub(S.x[p], u), B = dsub(S.y[p], w);
-                    const double E = dsub(S.x[r], u), F = dsub(S.y[r], w);
-                    const double Cc = dsub(S.x[q], u), D = dsub(S.y[q], w);
-                    const bool la = left_diff(A, B, E, F);
-                    const bool lb = !la && left_diff(E, F, Cc, D);
-                    if (la || lb) {
-                        const int sd = la ? 0 : 1;
-                        const uint32_t ch = 2u * c + sd;
-                        chv[kk] = ch;
-                        const unsigned long long key = fc_key(S, cur, c, sd, lid);
-                        if (key < S.ckey[ch]) atomicMin(&S.ckey[ch], key);
-                    }
-                }
-            }
-#pragma unroll
-            for (int kk = 0; kk < kFcChunk; ++kk) {
-                const uint32_t ch = chv[kk];
-                const unsigned grp = __match_any_sync(kFull, ch);
-                const int leader = __ffs(grp) - 1;
-                uint32_t base = 0;
-                if (ch != 0xffffffffu && lane == leader) base = atomicAdd(&S.ccnt[ch], uint32_t(__popc(grp)));
-                base = __shfl_sync(kFull, base, leader);
-                if (ch != 0xffffffffu) {
-                    const uint32_t pos = base + __popc(grp & lanemask_lt());
-                    const uint32_t cc = ch >> 1;
-                    const uint32_t dest = (ch & 1u) ? uint32_t(S.nhi[cur][cc]) - 1u - pos : uint32_t(S.nlo[cur][cc]) + pos;
-                    S.work[nxt][dest] = lidv[kk];
-                    S.wnode[nxt][dest] = uint16_t(ch);
-                }
-            }
-            }
-            __syncthreads();
-            if (ftr && depth == 0) g_ftrace[40] = gtimer_ns();
-            // (2) candidates: points holding their child's minimal key
+            // (1) classify in place; child counts and minimal keys
+            uint32_t chv[kFcItems];
+            unsigned long long keyv[kFcItems];
 #pragma unroll
             for (int k = 0; k < kFcItems; ++k) {
                 const uint32_t i = uint32_t(k) * kFcThreads + tid;
-                const uint16_t ch = i < m ? S.wnode[nxt][i] : kDead;
-                if (ch == kDead) continue;
-                const uint16_t lid = S.work[nxt][i];
-                if (fc_key(S, cur, ch >> 1, ch & 1, lid) == S.ckey[ch]) {
-                    if (atomicAdd(&S.cncand[ch], 1u) == 0) S.ccand[ch] = lid;
-                    else S.tie = 1;
+                chv[k] = kFcNoChild;
+                keyv[k] = kNoKey;
+                if (i >= m) continue;
+                const uint16_t pc = depth == 0 ? uint16_t(0) : S.pnode[i];
+                const uint16_t c = pc == kDead ? kDead : S.cmap[pc];
+                if (c == kDead) {
+                    if (depth > 0) S.pnode[i] = kDead;
+                    continue;
+                }
+                const uint16_t p = S.np[cur][c], r = S.nr[cur][c], q = S.nq[cur][c];
+                const double u = S.x[i], w = S.y[i];
+                const double px = S.x[p], py = S.y[p], rx = S.x[r], ry = S.y[r];
+                const double qx = S.x[q], qy = S.y[q];
+                const double A = dsub(px, u), B = dsub(py, w);
+                const double E = dsub(rx, u), F = dsub(ry, w);
+                const double Cc = dsub(qx, u), D = dsub(qy, w);
+                const bool la = left_diff(A, B, E, F);
+                const bool lb = !la && left_diff(E, F, Cc, D);
+                if (la || lb) {
+                    const uint32_t ch = 2u * c + (lb ? 1u : 0u);
+                    const double fx = lb ? dsub(qx, rx) : dsub(rx, px);
+                    const double fy = lb ? dsub(qy, ry) : dsub(ry, py);
+                    const unsigned long long key = key_of(lat_off(fx, fy, u, w));
+                    chv[k] = ch;
+                    keyv[k] = key;
+                    S.pnode[i] = uint16_t(ch);
+                } else {
+                    S.pnode[i] = kDead;
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < kFcItems; ++k) {
+                const uint32_t ch = chv[k];
+                const unsigned grp = __match_any_sync(kFull, ch);
+                if (grp == kFull) {  // the whole warp in one child (or none)
+                    unsigned long long key = keyv[k];
+#pragma unroll
+                    for (int s = 16; s > 0; s >>= 1) {
+                        const unsigned long long o = __shfl_xor_sync(kFull, key, s);
+                        key = o < key ? o : key;
+                    }
+                    if (ch != kFcNoChild && lane == 0) {
+                        atomicAdd(&S.ccnt[ch], 32u);
+                        if (key < S.u.ckey[ch]) atomicMin(&S.u.ckey[ch], key);
+                    }
+                } else if (ch != kFcNoChild) {
+                    if (lane == __ffs(grp) - 1) atomicAdd(&S.ccnt[ch], uint32_t(__popc(grp)));
+                    if (keyv[k] < S.u.ckey[ch]) atomicMin(&S.u.ckey[ch], keyv[k]);
                 }
             }
             __syncthreads();
-            if (ftr && depth == 0) g_ftrace[41] = gtimer_ns();
-            if (S.tie) {  // rare: exact offset ties -> smaller (x, y), then index
-                for (uint32_t ch = tid; ch < 2 * nnodes; ch += kFcThreads) {
-                    if (S.cncand[ch] < 2) continue;
-                    const int c = int(ch >> 1), s = int(ch & 1);
-                    const uint32_t cnt = S.ccnt[ch];
-                    const uint32_t lo = s ? uint32_t(S.nhi[cur][c]) - cnt : S.nlo[cur][c];
-                    uint16_t best = S.ccand[ch];
-                    for (uint32_t j = lo; j < lo + cnt; ++j) {
-                        const uint16_t l = S.work[nxt][j];
-                        if (l == best || fc_key(S, cur, c, s, l) != S.ckey[ch]) continue;
-                        const bool better = S.x[l] != S.x[best] ? S.x[l] < S.x[best]
-                                          : (S.y[l] != S.y[best] ? S.y[l] < S.y[best] : S.gid[l] < S.gid[best]);
-                        if (better) best = l;
+            VQB_STAMP(if (ftr && depth == 0) g_ftrace[40] = gtimer_ns();)
+            // (2) apexes: the points holding their child's minimal key
+#pragma unroll
+            for (int k = 0; k < kFcItems; ++k) {
+                const uint32_t ch = chv[k];
+                if (ch == kFcNoChild || keyv[k] != S.u.ckey[ch]) continue;
+                const uint32_t i = uint32_t(k) * kFcThreads + tid;
+                if ((atomicAdd(&S.ccnt[ch], 0x10000u) >> 16) == 0) S.ccand[ch] = uint16_t(i);
+                else S.tlist[atomicAdd(&S.ntie, 1u)] = uint16_t(i);
+            }
+            __syncthreads();
+            VQB_STAMP(if (ftr && depth == 0) g_ftrace[41] = gtimer_ns();)
+            if (S.ntie) {  // exact offset ties: smaller (x, y), then first index
+                if (tid == 0) {
+                    const uint32_t nt = S.ntie;
+                    for (uint32_t t = 0; t < nt; ++t) {
+                        const uint16_t i = S.tlist[t];
+                        const uint16_t ch = S.pnode[i];
+                        const uint16_t b = S.ccand[ch];
+                        const bool better = S.x[i] != S.x[b] ? S.x[i] < S.x[b]
+                                          : (S.y[i] != S.y[b] ? S.y[i] < S.y[b] : S.gid[i] < S.gid[b]);
+                        if (better) S.ccand[ch] = i;
                     }
-                    S.ccand[ch] = best;
+                    S.ntie = 0;
                 }
                 __syncthreads();
-                if (tid == 0) S.tie = 0;
             }
             // (3) children -> next depth's nodes (block scan over "internal"), links, leaves
             const uint32_t nch = 2 * nnodes;
@@ -1338,7 +1341,7 @@ __device__ __forceinline__ void finisher_cta_body(FinCtaSmemT<CAP>& S, const Fin
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 const uint32_t ch = 4u * tid + k;
-                const bool in = ch < nch && S.ccnt[ch] >= 2;
+                const bool in = ch < nch && (S.ccnt[ch] & 0xffffu) >= 2;
                 flags |= uint32_t(in) << k;
                 local += in;
             }
@@ -1350,7 +1353,7 @@ __device__ __forceinline__ void finisher_cta_body(FinCtaSmemT<CAP>& S, const Fin
             }
             if (lane == 31) S.wsum[warp] = incl;
             __syncthreads();
-            if (ftr && depth == 0) g_ftrace[42] = gtimer_ns();
+            VQB_STAMP(if (ftr && depth == 0) g_ftrace[42] = gtimer_ns();)
             uint32_t base = 0;
             for (int w2 = 0; w2 < warp; ++w2) base += S.wsum[w2];
             uint32_t id = base + incl - local;  // first next-depth id of this thread's children
@@ -1360,10 +1363,10 @@ __device__ __forceinline__ void finisher_cta_body(FinCtaSmemT<CAP>& S, const Fin
                 const uint32_t ch = 4u * tid + k;
                 if (ch >= nch) break;
                 const int c = int(ch >> 1), s = int(ch & 1);
-                const uint32_t cnt = S.ccnt[ch];
+                const uint32_t cnt = S.ccnt[ch] & 0xffffu;
                 const uint16_t t = S.ntree[cur][c];
                 uint16_t link = kLinkEmpty;
-                S.cmap[ch] = kDead;
+                uint16_t map = kDead;
                 if (cnt == 1) {
                     link = uint16_t(kLinkLeaf | S.ccand[ch]);
                 } else if (cnt >= 2) {
@@ -1373,30 +1376,23 @@ __device__ __forceinline__ void finisher_cta_body(FinCtaSmemT<CAP>& S, const Fin
                     S.np[nxt][nid] = s ? S.nr[cur][c] : S.np[cur][c];
                     S.nq[nxt][nid] = s ? S.nq[cur][c] : S.nr[cur][c];
                     S.nr[nxt][nid] = S.ccand[ch];
-                    S.nlo[nxt][nid] = s ? uint16_t(S.nhi[cur][c] - cnt) : S.nlo[cur][c];
-                    S.nhi[nxt][nid] = s ? S.nhi[cur][c] : uint16_t(S.nlo[cur][c] + cnt);
                     S.ntree[nxt][nid] = tnew;
                     S.tapex[tnew] = S.ccand[ch];
                     S.tleft[tnew] = kLinkEmpty;
                     S.tright[tnew] = kLinkEmpty;
-                    S.cmap[ch] = uint16_t(nid);
+                    map = uint16_t(nid);
                 }
+                S.cmap[ch] = map;
                 if (s) S.tright[t] = link; else S.tleft[t] = link;
             }
             __syncthreads();
-            if (ftr && depth == 0) g_ftrace[43] = gtimer_ns();
+            VQB_STAMP(if (ftr && depth == 0) g_ftrace[43] = gtimer_ns();)
             const uint32_t nn = S.nnext;
-            // remap the next work array to next-depth node ids; reset the
-            // accumulators and the array that becomes the next output
-            for (uint32_t i = tid; i < m; i += kFcThreads) {
-                const uint16_t ch = S.wnode[nxt][i];
-                if (ch != kDead) S.wnode[nxt][i] = S.cmap[ch];
-                S.wnode[cur][i] = kDead;
-            }
+            // (4) fresh accumulators for the next depth's children (points
+            // read their next node id through cmap in the next phase 1)
             for (uint32_t ch = tid; ch < 2 * nn; ch += kFcThreads) {
-                S.ckey[ch] = kNoKey;
+                S.u.ckey[ch] = kNoKey;
                 S.ccnt[ch] = 0;
-                S.cncand[ch] = 0;
             }
             ntree += nn;
             ++depth;
@@ -1405,30 +1401,30 @@ __device__ __forceinline__ void finisher_cta_body(FinCtaSmemT<CAP>& S, const Fin
             cur = nxt;
             __syncthreads();
         }
-        if (ftr) { g_ftrace[62] = depth; g_ftrace[63] = gtimer_ns(); }
+        VQB_STAMP(if (ftr) { g_ftrace[62] = depth; g_ftrace[63] = gtimer_ns(); })
         // subtree sizes bottom-up, then chain positions top-down
         for (int d = depth - 1; d >= 0; --d) {
             for (uint32_t t = S.lvl_start[d] + tid; t < S.lvl_start[d + 1]; t += kFcThreads)
-                S.tsize[t] = uint16_t(fc_link_size(S, S.tleft[t]) + 1u + fc_link_size(S, S.tright[t]));
+                S.u.t.tsize[t] = uint16_t(fc_link_size(S, S.tleft[t]) + 1u + fc_link_size(S, S.tright[t]));
             __syncthreads();
         }
         const uint64_t cb = rec.chain_base;
-        if (tid == 0) S.tstart[0] = 0;
+        if (tid == 0) S.u.t.tstart[0] = 0;
         __syncthreads();
         for (int d = 0; d < depth; ++d) {
             for (uint32_t t = S.lvl_start[d] + tid; t < S.lvl_start[d + 1]; t += kFcThreads) {
-                const uint32_t s0 = S.tstart[t];
+                const uint32_t s0 = S.u.t.tstart[t];
                 const uint16_t L = S.tleft[t], R = S.tright[t];
                 const uint32_t ap = s0 + fc_link_size(S, L);
                 chain[cb + ap] = S.gid[S.tapex[t]];
                 if (L & kLinkLeaf) chain[cb + s0] = S.gid[L & 0x3fff];
-                else if (L & kLinkNode) S.tstart[L & 0x3fff] = uint16_t(s0);
+                else if (L & kLinkNode) S.u.t.tstart[L & 0x3fff] = uint16_t(s0);
                 if (R & kLinkLeaf) chain[cb + ap + 1] = S.gid[R & 0x3fff];
-                else if (R & kLinkNode) S.tstart[R & 0x3fff] = uint16_t(ap + 1);
+                else if (R & kLinkNode) S.u.t.tstart[R & 0x3fff] = uint16_t(ap + 1);
             }
             __syncthreads();
         }
-        if (tid == 0) fin_count[fi] = S.tsize[0];
+        if (tid == 0) fin_count[fi] = S.u.t.tsize[0];
         __syncthreads();
     }
 }
