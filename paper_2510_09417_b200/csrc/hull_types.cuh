@@ -19,7 +19,10 @@ constexpr int kWarps = kThreads / 32;
 constexpr int kPartMinBlocks = 3;           // resident partition CTAs per SM (register cap)
 constexpr int kFastMinBlocks = 4;           // fast-mode kernels (no staging)
 constexpr uint32_t kFinSmall = 64;          // segments of 2..64 points: warp finisher
-constexpr uint32_t kFinMax = 768;           // 65..768 points: CTA finisher (4 per SM; 1024: 3 per SM, 8 % slower on circle 1e7); larger: tiled level kernel
+#ifndef VQB_FIN_MAX
+#define VQB_FIN_MAX 768
+#endif
+constexpr uint32_t kFinMax = VQB_FIN_MAX;           // 65..768 points: CTA finisher (4 per SM; 1024: 3 per SM, 8 % slower on circle 1e7); larger: tiled level kernel
 constexpr uint32_t kTailFinMax = 1024;      // inside the persistent tail kernel (2048 measured: faster on disk 1e6, slower on square 1e8 and disk 1e7)
 
 // Root stage geometry.  The recursion itself always follows the reference

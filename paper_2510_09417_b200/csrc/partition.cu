@@ -2070,11 +2070,37 @@ __global__ void __launch_bounds__(kCtlThreads, 3) level_tma(LevelArgs a) {
         bi[0] = bi[1] = kNoIdx;
     };
 
+    // Lagged stores (as in the filter pass): tile k is classified while the
+    // control warp claims its output ranges, and tile k-1 — classes and ranks
+    // kept in shared memory, coordinates still in its ring stage — is stored
+    // in the same interval, so the claim's L2 round trip never stalls the
+    // compute warps; the stage is refilled once its stores are done.
+    __shared__ uint16_t s_cr[2][kTile];          // class << 8 | rank in the (class, warp) run
+    __shared__ uint32_t s_og[2][2][kWarps];      // output origins per (tile parity, class, warp)
+    auto store_tile = [&](uint32_t kt) {         // compute warps: tile kt's points to their places
+        const int st = int(kt % kRing), par = int(kt & 1);
+        const uint32_t dx = ring.dx[st], di = ring.di[st];
+        const int warp_ = threadIdx.x >> 5;
+#pragma unroll
+        for (int i = 0; i < kItems; ++i) {
+            const uint32_t r = uint32_t(i) * kThreads + threadIdx.x;
+            const uint32_t v = s_cr[par][r];
+            const uint32_t c = v >> 8, rk = v & 0xffu;
+            if (c < 2) {
+                const uint32_t o = s_og[par][c][warp_];
+                const uint32_t p = c ? o - rk : o + rk;
+                VQB_CHECK(p < a.out_cap, 13, p, a.out_cap);
+                a.ox[p] = ring.x[st][dx + r];
+                a.oy[p] = ring.y[st][dx + r];
+                a.oid[p] = ring.id[st][di + r];
+            }
+        }
+    };
     uint32_t kk = 0;
     const uint32_t chunk = (ntiles + G - 1) / G;
     const uint32_t t_end = min(ntiles, (blockIdx.x + 1) * chunk);
     for (uint32_t t = blockIdx.x * chunk; t < t_end; ++t, ++kk) {
-        const int s = int(kk % kRing);
+        const int s = int(kk % kRing), par = int(kk & 1);
         // entering a new segment?  all threads decide on one snapshot
         const uint32_t k_now = ring.k[s], k_cur = s_cur_k;
         __syncthreads();
@@ -2087,16 +2113,10 @@ __global__ void __launch_bounds__(kCtlThreads, 3) level_tma(LevelArgs a) {
             }
             __syncthreads();
         }
-        double ux[kItems], uy[kItems];
-        uint32_t uid[kItems];
-        int cls[kItems];
-        uint32_t rk[kItems];
-        const uint32_t out = uint32_t(ring.seg[s].out), m = ring.seg[s].m;
-        const double adx = ring.seg[s].adx, ady = ring.seg[s].ady;
-        const double bdx = ring.seg[s].bdx, bdy = ring.seg[s].bdy;
         if (!ctl) {
             const SegRec& g = ring.seg[s];
             const uint32_t cnt = ring.cnt[s], dx = ring.dx[s], di = ring.di[s];
+            const double adx = g.adx, ady = g.ady, bdx = g.bdx, bdy = g.bdy;
             mbar_wait(&ring.bar[s], (kk / kRing) & 1u);
             const double px = g.px, py = g.py, rx = g.rx, ry = g.ry, qx = g.qx, qy = g.qy;
             uint32_t wrun = 0;
@@ -2105,9 +2125,6 @@ __global__ void __launch_bounds__(kCtlThreads, 3) level_tma(LevelArgs a) {
                 const uint32_t r = uint32_t(i) * kThreads + threadIdx.x;
                 const bool v = r < cnt;
                 const double u = ring.x[s][dx + r], w = ring.y[s][dx + r];
-                ux[i] = u;
-                uy[i] = w;
-                uid[i] = ring.id[s][di + r];
                 bool la, lb;
                 if (GENERAL) {
                     la = left_diff(dsub(px, u), dsub(py, w), dsub(rx, u), dsub(ry, w));
@@ -2120,12 +2137,15 @@ __global__ void __launch_bounds__(kCtlThreads, 3) level_tma(LevelArgs a) {
                     lb = !la && left_diff(E, F, Cc, D);
                 }
                 const int c = !v ? 2 : (la ? 0 : (lb ? 1 : 2));
-                cls[i] = c;
-                rk[i] = warp_rank<2>(c, wrun);
+                const uint32_t rk = warp_rank<2>(c, wrun);
+                s_cr[par][r] = uint16_t((uint32_t(c) << 8) | rk);
+                // fused farthest-point search (kernels.hpp:41-45)
+                running_best_d<2>(bo, bi, c, lat_off(c == 0 ? adx : bdx, c == 0 ? ady : bdy, u, w),
+                                  ring.id[s][di + r], a.gx, a.gy);
             }
             if (lane < 2) S.wtot[lane][warp] = wrun;
         }
-        __syncthreads();  // counts ready; every compute warp is done with stage s
+        __syncthreads();  // A: tile kk's counts and ranks posted
         if (ctl) {
             uint32_t tot[2];
             tile_scan_fast<2>(S, tot);
@@ -2137,39 +2157,22 @@ __global__ void __launch_bounds__(kCtlThreads, 3) level_tma(LevelArgs a) {
             __syncwarp();
             if (lane < 2 * kWarps) {
                 const int c = lane / kWarps, w = lane % kWarps;
+                const uint32_t out = uint32_t(ring.seg[s].out), m = ring.seg[s].m;
                 const uint32_t off = S.claim[c] + S.wbase[c][w];
                 const uint32_t org = c == 0 ? out : out + m - 1u;
-                s_org[c][w] = c ? org - off : org + off;
+                s_og[par][c][w] = c ? org - off : org + off;
             }
-            if (lane == 0) {
-                fence_proxy_async_smem();
-                issue(kk + kRing);  // refill stage s
-            }
-        } else {
-#pragma unroll
-            for (int i = 0; i < kItems; ++i) {  // fused farthest-point search, overlapping the claim
-                const int c = cls[i];
-                running_best_d<2>(bo, bi, c, lat_off(c == 0 ? adx : bdx, c == 0 ? ady : bdy, ux[i], uy[i]),
-                                  uid[i], a.gx, a.gy);
-            }
+        } else if (kk >= 1) {
+            store_tile(kk - 1);  // overlaps the claim of tile kk
         }
-        __syncthreads();
-        if (!ctl) {
-#pragma unroll
-            for (int i = 0; i < kItems; ++i) {
-                const int c = cls[i];
-                if (c < 2) {
-                    const uint32_t o = s_org[c][warp];
-                    const uint32_t p = c ? o - rk[i] : o + rk[i];
-                    VQB_CHECK(p < a.out_cap, 13, p, a.out_cap);
-                    a.ox[p] = ux[i];
-                    a.oy[p] = uy[i];
-                    a.oid[p] = uid[i];
-                }
-            }
+        __syncthreads();  // B: tile kk's origins published; tile kk-1 stored
+        if (ctl && lane == 0 && kk >= 1) {
+            fence_proxy_async_smem();
+            issue(kk - 1 + kRing);  // refill tile kk-1's stage
         }
         if (threadIdx.x == 0) ++s_cur_tiles;
     }
+    if (kk >= 1 && !ctl) store_tile(kk - 1);
     if (s_cur_k != 0xffffffffu) finalize();
 }
 
