@@ -1790,52 +1790,121 @@ struct SegCtaSmem {
     uint32_t ridx[2][kWarps];
 };
 
+// ===========================================================================
+// K2 fast mode with a TMA ring (8 compute warps + 1 control warp).  The
+// control warp's lane 0 maps each upcoming tile of the CTA to its segment and
+// streams x, y and the indices into a kRing-deep shared-memory ring with
+// cp.async.bulk (segment starts are arbitrary: the copy starts at the
+// 16-byte-aligned element below and the consumer skips the head; buffers
+// carry a small tail pad).  Per tile the control warp scans the warp counts
+// and claims the tile's places in the segment's two child ranges with one
+// packed atomic while the compute warps update the running arg-max.
+// ===========================================================================
+struct LevelRing {
+    double x[kRing][kTile + 2];
+    double y[kRing][kTile + 2];
+    uint32_t id[kRing][kTile + 4];
+    unsigned long long bar[kRing];
+    SegRec seg[kRing];
+    uint32_t k[kRing];
+    uint32_t cnt[kRing];
+    uint32_t dx[kRing];
+    uint32_t di[kRing];
+};
+
+// Segment-per-CTA levels, fed by the TMA ring: the control warp walks the
+// CTA's segments (k = blockIdx.x, + gridDim.x, ...) tile by tile and keeps
+// kRing tiles in flight, so the next segment's points are already in shared
+// memory when the current one ends (a CTA owns 2-4 tiles per segment on
+// these levels; unprefetched, every tile exposed a full load latency).
 template <bool GENERAL>
-__device__ __forceinline__ void level_segcta_body(const LevelArgs& a, uint32_t nseg, SegCtaSmem& S) {
+__device__ __forceinline__ void level_segcta_tma(const LevelArgs& a, uint32_t nseg, LevelRing& ring,
+                                                 SegCtaSmem& S) {
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    for (uint32_t k = blockIdx.x; k < nseg; k += gridDim.x) {
+    const bool ctl = tid >= kThreads;
+    const uint32_t G = gridDim.x;
+    uint32_t it_k = blockIdx.x, it_j = 0;  // control lane: next (segment, tile) to load
+    auto issue_next = [&](uint32_t n) {     // CTA-local tile n -> stage n % kRing
+        if (it_k >= nseg) return;
+        const int st = int(n % kRing);
+        const SegRec& g = a.segs[it_k];
+        const uint32_t m = g.m, ntl = g.ntiles;
+        const uint32_t start = uint32_t(g.begin) + it_j * uint32_t(kTile);
+        const uint32_t cnt = min(uint32_t(kTile), m - it_j * uint32_t(kTile));
+        const uint32_t ax = start & ~1u, dx = start - ax;
+        const uint32_t ai = start & ~3u, di = start - ai;
+        const uint32_t bx = ((cnt + dx + 1u) & ~1u) * 8u;
+        const uint32_t bi = ((cnt + di + 3u) & ~3u) * 4u;
+        VQB_CHECK(uint64_t(ax) * 8 + bx <= a.in_cap * 8 && uint64_t(ai) * 4 + bi <= a.in_cap * 4, 24, start, cnt);
+        ring.cnt[st] = cnt;
+        ring.dx[st] = dx;
+        ring.di[st] = di;
+        mbar_expect_tx(&ring.bar[st], 2u * bx + bi);
+        tma_load_1d(ring.x[st], a.ix + ax, bx, &ring.bar[st]);
+        tma_load_1d(ring.y[st], a.iy + ax, bx, &ring.bar[st]);
+        tma_load_1d(ring.id[st], a.iid + ai, bi, &ring.bar[st]);
+        if (++it_j == ntl) {
+            it_j = 0;
+            it_k += G;
+        }
+    };
+    if (tid == kThreads) {
+        for (int st = 0; st < kRing; ++st) mbar_init(&ring.bar[st], 1);
+        mbar_fence_init();
+        for (uint32_t n = 0; n < uint32_t(kRing); ++n) issue_next(n);
+    }
+    __syncthreads();
+    uint32_t n = 0;  // CTA-local tile counter (every thread)
+    for (uint32_t k = blockIdx.x; k < nseg; k += G) {
         const SegRec g = a.segs[k];
         const double px = g.px, py = g.py, rx = g.rx, ry = g.ry, qx = g.qx, qy = g.qy;
         const double adx = g.adx, ady = g.ady, bdx = g.bdx, bdy = g.bdy;
         unsigned long long kb[2] = {kNoKey, kNoKey};
         uint32_t ib[2] = {kNoIdx, kNoIdx};
         uint32_t run0 = 0, run1 = 0;  // CTA-uniform running class counts
-        for (uint32_t j = 0; j < g.ntiles; ++j) {
-            const uint64_t start = g.begin + uint64_t(j) * kTile;
-            const uint32_t cnt = min(uint32_t(kTile), g.m - j * uint32_t(kTile));
+        for (uint32_t j = 0; j < g.ntiles; ++j, ++n) {
+            const int st = int(n % kRing);
             int cls[kItems];
             double ux[kItems], uy[kItems];
             uint32_t uid[kItems], rk[kItems];
-            uint32_t wrun = 0;
+            if (!ctl) {
+                const uint32_t cnt = ring.cnt[st], dx = ring.dx[st], di = ring.di[st];
+                mbar_wait(&ring.bar[st], (n / kRing) & 1u);
+                uint32_t wrun = 0;
 #pragma unroll
-            for (int i = 0; i < kItems; ++i) {
-                const uint32_t r = uint32_t(i) * kThreads + tid;
-                const bool v = r < cnt;
-                const double u = v ? __ldcs(a.ix + start + r) : 0.0;
-                const double w = v ? __ldcs(a.iy + start + r) : 0.0;
-                ux[i] = u;
-                uy[i] = w;
-                uid[i] = v ? __ldcs(a.iid + start + r) : 0u;
-                bool la, lb;
-                if (GENERAL) {
-                    la = left_diff(dsub(px, u), dsub(py, w), dsub(rx, u), dsub(ry, w));
-                    lb = !la && left_diff(dsub(g.bx, u), dsub(g.by, w), dsub(qx, u), dsub(qy, w));
-                } else {
-                    const double A = dsub(px, u), B = dsub(py, w);
-                    const double E = dsub(rx, u), F = dsub(ry, w);
-                    const double Cc = dsub(qx, u), D = dsub(qy, w);
-                    la = left_diff(A, B, E, F);
-                    lb = !la && left_diff(E, F, Cc, D);
+                for (int i = 0; i < kItems; ++i) {
+                    const uint32_t r = uint32_t(i) * kThreads + tid;
+                    const bool v = r < cnt;
+                    const double u = ring.x[st][dx + r], w = ring.y[st][dx + r];
+                    ux[i] = u;
+                    uy[i] = w;
+                    uid[i] = ring.id[st][di + r];
+                    bool la, lb;
+                    if (GENERAL) {
+                        la = left_diff(dsub(px, u), dsub(py, w), dsub(rx, u), dsub(ry, w));
+                        lb = !la && left_diff(dsub(g.bx, u), dsub(g.by, w), dsub(qx, u), dsub(qy, w));
+                    } else {
+                        const double A = dsub(px, u), B = dsub(py, w);
+                        const double E = dsub(rx, u), F = dsub(ry, w);
+                        const double Cc = dsub(qx, u), D = dsub(qy, w);
+                        la = left_diff(A, B, E, F);
+                        lb = !la && left_diff(E, F, Cc, D);
+                    }
+                    const int c = !v ? 2 : (la ? 0 : (lb ? 1 : 2));
+                    cls[i] = c;
+                    rk[i] = warp_rank<2>(c, wrun);
+                    const unsigned long long key = key_of(lat_off(c == 0 ? adx : bdx, c == 0 ? ady : bdy, u, w));
+                    running_best<2>(kb, ib, c, key, uid[i], a.gx, a.gy);
                 }
-                const int c = !v ? 2 : (la ? 0 : (lb ? 1 : 2));
-                cls[i] = c;
-                rk[i] = warp_rank<2>(c, wrun);
-                const unsigned long long key = key_of(lat_off(c == 0 ? adx : bdx, c == 0 ? ady : bdy, u, w));
-                running_best<2>(kb, ib, c, key, uid[i], a.gx, a.gy);
+                if (lane < 2) S.wc[lane][warp] = wrun;
             }
-            if (lane < 2) S.wc[lane][warp] = wrun;
-            __syncthreads();
-            if (warp == 0) {  // per-class exclusive scan over the warps
+            __syncthreads();  // A: counts posted; the stage's points are in registers
+            if (ctl) {
+                if (lane == 0) {
+                    fence_proxy_async_smem();
+                    issue_next(n + kRing);  // refill this stage
+                }
+            } else if (warp == 0) {  // per-class exclusive scan over the warps
                 const int c = (lane >> 3) & 1, w8 = lane & 7;
                 const uint32_t v = lane < 16 ? S.wc[c][w8] : 0u;
                 uint32_t incl = v;
@@ -1848,34 +1917,35 @@ __device__ __forceinline__ void level_segcta_body(const LevelArgs& a, uint32_t n
                 if (lane == 7) S.tot[0] = incl;
                 if (lane == 15) S.tot[1] = incl;
             }
-            __syncthreads();
+            __syncthreads();  // B: offsets ready
+            if (!ctl) {
 #pragma unroll
-            for (int i = 0; i < kItems; ++i) {
-                const int c = cls[i];
-                if (c < 2) {
-                    const uint32_t off = (c ? run1 : run0) + S.wex[c][warp] + rk[i];
-                    const uint64_t pos = c ? g.out + g.m - 1u - off : g.out + off;
-                    VQB_CHECK(pos < a.out_cap, 16, pos, a.out_cap);
-                    a.ox[pos] = ux[i];
-                    a.oy[pos] = uy[i];
-                    a.oid[pos] = uid[i];
+                for (int i = 0; i < kItems; ++i) {
+                    const int c = cls[i];
+                    if (c < 2) {
+                        const uint32_t off = (c ? run1 : run0) + S.wex[c][warp] + rk[i];
+                        const uint64_t pos = c ? g.out + g.m - 1u - off : g.out + off;
+                        VQB_CHECK(pos < a.out_cap, 16, pos, a.out_cap);
+                        a.ox[pos] = ux[i];
+                        a.oy[pos] = uy[i];
+                        a.oid[pos] = uid[i];
+                    }
                 }
             }
             run0 += S.tot[0];
             run1 += S.tot[1];
-            __syncthreads();  // S reused by the next tile
         }
         // the segment's two children (farthest point: block reduction)
         for (int c = 0; c < 2; ++c) {
             unsigned long long kk = kb[c];
             uint32_t ii = ib[c];
-            warp_key_best(kk, ii, a.gx, a.gy);
-            if (lane == 0) {
+            if (!ctl) warp_key_best(kk, ii, a.gx, a.gy);
+            if (lane == 0 && !ctl) {
                 S.rkey[c][warp] = kk;
                 S.ridx[c][warp] = ii;
             }
         }
-        __syncthreads();
+        __syncthreads();  // (also: every thread has read S.tot of the last tile)
         if (tid < 2) {
             const int c = tid;
             unsigned long long ko = S.rkey[c][0];
@@ -1910,28 +1980,6 @@ __device__ __forceinline__ void level_segcta_body(const LevelArgs& a, uint32_t n
     }
 }
 
-// ===========================================================================
-// K2 fast mode with a TMA ring (8 compute warps + 1 control warp).  The
-// control warp's lane 0 maps each upcoming tile of the CTA to its segment and
-// streams x, y and the indices into a kRing-deep shared-memory ring with
-// cp.async.bulk (segment starts are arbitrary: the copy starts at the
-// 16-byte-aligned element below and the consumer skips the head; buffers
-// carry a small tail pad).  Per tile the control warp scans the warp counts
-// and claims the tile's places in the segment's two child ranges with one
-// packed atomic while the compute warps update the running arg-max.
-// ===========================================================================
-struct LevelRing {
-    double x[kRing][kTile + 2];
-    double y[kRing][kTile + 2];
-    uint32_t id[kRing][kTile + 4];
-    unsigned long long bar[kRing];
-    SegRec seg[kRing];
-    uint32_t k[kRing];
-    uint32_t cnt[kRing];
-    uint32_t dx[kRing];
-    uint32_t di[kRing];
-};
-
 template <bool GENERAL>
 __global__ void __launch_bounds__(kCtlThreads, 3) level_tma(LevelArgs a) {
     VQB_PDL();
@@ -1941,7 +1989,8 @@ __global__ void __launch_bounds__(kCtlThreads, 3) level_tma(LevelArgs a) {
         const uint32_t nseg = a.info->nseg, nt = a.info->ntiles;
         if (nseg >= gridDim.x && nt <= kSegCtaTiles * nseg) {
             __shared__ SegCtaSmem SC;
-            if (threadIdx.x < kThreads) level_segcta_body<GENERAL>(a, nseg, SC);
+            extern __shared__ __align__(128) unsigned char dsm_sc[];
+            level_segcta_tma<GENERAL>(a, nseg, *reinterpret_cast<LevelRing*>(dsm_sc), SC);
             return;
         }
     }
