@@ -3,3 +3,4 @@
 #include "kernels.cu"
 #include "partition.cu"
 #include "tail.cu"
+#include "cluster_tail.cu"

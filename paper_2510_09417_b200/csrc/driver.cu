@@ -134,6 +134,8 @@ class Engine {
         occ_filt_ = std::max(1, occupancy_filtered());
         occ_filter_ = std::max(1, occupancy_filter());
         occ_tail_ = std::max(1, std::min(getenv("VQHULL_TAIL_OCC") ? atoi(getenv("VQHULL_TAIL_OCC")) : 1, occupancy_tail()));
+        // VQHULL_KC=0: no cluster recursion (KT does every small recursion)
+        use_kc_ = !(getenv("VQHULL_KC") && getenv("VQHULL_KC")[0] == '0') && kc_prepare() > 0;
         // one full wave each
         grid_ext_ = sms_ * std::max(1, std::min(8, occupancy_extremes()));
         grid_boot_ = sms_ * std::max(1, std::min(8, occupancy_bootstrap()));
@@ -857,6 +859,8 @@ class Engine {
         ta.root = root_;
         report_.ensure(report_bytes(nlev), st);
         ta.report = report_.as<uint32_t>();
+        // the cluster recursion first (it hands the call to KT when it cannot take it)
+        ta.kc_done = (use_kc_ && l0 == 2 && ta.out) ? ctrs_ + 25 : nullptr;
         if (tail_trace_) {
             trace_.ensure(8 * (1 + 10 * kTailLevels), st);
             ta.trace = trace_.as<unsigned long long>();
@@ -868,6 +872,7 @@ class Engine {
     void launch_tail_report(const TailArgs& ta, cudaStream_t st) {
         const int l0 = ta.l0;
         if (ta.trace) ck(cudaMemsetAsync(ta.trace, 0, 8 * (1 + 10 * kTailLevels), st), "memset trace");
+        if (ta.kc_done) tk(3, st, [&] { ck(launch_cluster_tail(ta, st), "cluster recursion launch"); });
         tk(3, st, [&] { ck(launch_tail(ta, tail_grid(), st), "tail launch"); });
         if (tail_trace_) {
             std::vector<unsigned long long> tr(1 + 10 * kTailLevels);
@@ -1272,6 +1277,7 @@ class Engine {
     bool use_tail_ = !(getenv("VQHULL_TAIL") && getenv("VQHULL_TAIL")[0] == '0');
     uint32_t* h_tail_ = nullptr;
     bool tail_emitted_ = false;
+    bool use_kc_ = false;
     DevBuf tiny_;  // the one-CTA path's scratch
     uint32_t* fault_dev_ = nullptr;
     // VQHULL_TINY=0: tiny inputs through the general pipeline (tests)

@@ -254,6 +254,7 @@ struct TailArgs {
     const uint32_t* p_idx;    // &RootInfo::p_idx (the frame vertex)
     const RootInfo* root;
     uint32_t* report;         // [8 words: state, h, nonfinite, unsafe, filter, survivors, 0] + level infos
+    uint32_t* kc_done;        // set to 1 by the cluster recursion (KC) when it did the whole call
 };
 
 // Sharded hull certificate (shard.cu): polygon of at most kCertMax vertices

@@ -66,6 +66,8 @@ void launch_tiny(const TinyArgs& a, cudaStream_t st);
 size_t tail_smem_bytes();
 int occupancy_tail();
 cudaError_t launch_tail(const TailArgs& a, int grid, cudaStream_t st);
+int kc_prepare();  // clusters of the cluster recursion the device can host (0: none)
+cudaError_t launch_cluster_tail(const TailArgs& a, cudaStream_t st);
 
 // sharded hull (shard.cu)
 void launch_cert_build(const uint32_t* hull, uint32_t h, const double* xs, const double* ys, double floor_m,
