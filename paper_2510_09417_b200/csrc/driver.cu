@@ -230,6 +230,14 @@ class Engine {
         // (VQHULL_LEVEL_BATCH overrides the batch: tests of the re-entry path)
         const int batch = lean ? 1 : (getenv("VQHULL_LEVEL_BATCH") ? std::max(1, atoi(getenv("VQHULL_LEVEL_BATCH")))
                                                                    : kLevelBatch);
+        // planner-free levels (fast mode): each level kernel plans the next one
+        // (plan_child, partition.cu); only the first host level runs the
+        // planner and tile-map kernels.  The tile map and the per-segment
+        // counters alternate between two sets (the level reads one, plans
+        // into the other).
+        const bool pfree = !stable_ && use_pf_;
+        int par = 0;
+        bool planned = false;
         while (lmax_ < 0) {
             const int first = lvl;
             for (int b = 0; b < batch; ++b, ++lvl) {
@@ -237,27 +245,23 @@ class Engine {
                 uint32_t ntiles_b = uint32_t(n / kTile) + nseg_b + 1;
                 const uint32_t S1 = std::max<uint32_t>(S, 1);
                 LevelTables& T = level(lvl);
-                T.kind.ensure(S1, st);
-                T.link.ensure(size_t(S1) * 4, st);
-                T.size.ensure(size_t(S1) * 4, st);
-                T.start.ensure(size_t(S1) * 4, st);
-                T.segs.ensure(size_t(S1) * sizeof(SegRec), st);
-                T.fins.ensure(size_t(S1) * sizeof(FinRec), st);
-                T.fin_count.ensure(size_t(S1) * 4, st);
+                ensure_tables(T, S1, st);
                 ensure_lookback(std::max<uint32_t>((S1 + 1023) / 1024, ntiles_b), st);
-                segaux_.ensure(segaux_bytes(S1), st);
-                info_.ensure(size_t(lvl + 1) * sizeof(LevelInfo), st, true);
+                DevBuf& SA = par ? segaux2_ : segaux_;
+                SA.ensure(segaux_bytes(S1), st);
+                info_.ensure(size_t(lvl + 3) * sizeof(LevelInfo), st, true);
                 LevelInfo* dinfo = info_.as<LevelInfo>() + lvl;
                 const LevelInfo* dprev = lvl == 2 ? nullptr : info_.as<LevelInfo>() + (lvl - 1);
-                {
+                if (!planned) {
                     const uint32_t ep = next_epoch();
                     tk(5, st, [&] {
                         launch_planner(T.slots.as<ChildRec>(), S, dprev, S, T.segs.as<SegRec>(), T.fins.as<FinRec>(),
                                        T.kind.as<uint8_t>(), T.link.as<uint32_t>(), dinfo, flags_.as<uint32_t>(),
-                                       aggs_.p, incs_.p, ep, &ctrs_[2], seg_pcnt(), seg_done(S1), seg_ctr(S1),
-                                       sms_ * 4, st);
+                                       aggs_.p, incs_.p, ep, &ctrs_[2], seg_pcnt(SA), seg_done(SA, S1),
+                                       seg_ctr(SA, S1), sms_ * 4, st, pfree ? dinfo + 1 : nullptr);
                     });
                 }
+                uint64_t out_bound = n;  // points of the next level
                 if (lean) {
                     ck(cudaMemcpyAsync(h_info_, dinfo, sizeof(LevelInfo), cudaMemcpyDeviceToHost, st), "d2h info");
                     ck(cudaStreamSynchronize(st), "level sync");
@@ -270,6 +274,7 @@ class Engine {
                     const LevelInfo li = *h_info_;
                     nseg_b = li.nseg;
                     ntiles_b = li.ntiles;
+                    out_bound = li.out_total;
                     bufs_[in ^ 1].ensure(std::max<uint32_t>(li.out_total, 1), st);
                     chain_.ensure((uint64_t(li.fin_base) + li.fin_total) * 4 + 4, st, true);
                 }
@@ -282,17 +287,19 @@ class Engine {
                 });
                 // K2 over all internal segments of this level
                 const int out = in ^ 1;
-                tile_seg_.ensure(size_t(ntiles_b) * 4, st);
+                DevBuf& TS = par ? tile_seg2_ : tile_seg_;
+                TS.ensure(size_t(ntiles_b) * 4, st);
                 part_.ensure(size_t(ntiles_b) * 2 * sizeof(Best), st);
                 LevelTables& Tn = level(lvl + 1);
                 Tn.slots.ensure(size_t(2) * std::max<uint32_t>(nseg_b, 1) * sizeof(ChildRec), st);
                 LevelTables& Tc = level(lvl);
-                tk(5, st, [&] { launch_tilemap(Tc.segs.as<SegRec>(), dinfo, tile_seg_.as<uint32_t>(), ntiles_b, st); });
+                if (!planned)
+                    tk(5, st, [&] { launch_tilemap(Tc.segs.as<SegRec>(), dinfo, TS.as<uint32_t>(), ntiles_b, st); });
                 {
                     const int grid = std::max(1, std::min<int>(int(ntiles_b), sms_ * (stable_ ? occ_level_stable_ : occ_level_)));
-                    LevelArgs la;
+                    LevelArgs la = {};
                     la.gx = dx; la.gy = dy;
-                    la.segs = Tc.segs.as<SegRec>(); la.tile_seg = tile_seg_.as<uint32_t>(); la.info = dinfo;
+                    la.segs = Tc.segs.as<SegRec>(); la.tile_seg = TS.as<uint32_t>(); la.info = dinfo;
                     la.ix = bufs_[in].x.as<double>(); la.iy = bufs_[in].y.as<double>(); la.iid = bufs_[in].id.as<uint32_t>();
                     la.ox = bufs_[out].x.as<double>(); la.oy = bufs_[out].y.as<double>(); la.oid = bufs_[out].id.as<uint32_t>();
                     la.in_cap = bufs_[in].x.cap / 8; la.out_cap = bufs_[out].x.cap / 8;
@@ -300,12 +307,28 @@ class Engine {
                     la.children_cap = Tn.slots.cap / sizeof(ChildRec); la.segs_cap = S1;
                     la.status = status_.as<Status>(); la.epoch = next_epoch(); la.ctr = &ctrs_[1];
                     la.tile_part = part_.as<Best>();
-                    la.seg_pcnt = seg_pcnt(); la.seg_done = seg_done(S1); la.seg_ctr = seg_ctr(S1);
+                    la.seg_pcnt = seg_pcnt(SA); la.seg_done = seg_done(SA, S1); la.seg_ctr = seg_ctr(SA, S1);
                     la.children = Tn.slots.as<ChildRec>();
+                    if (pfree) {  // plan level lvl + 1 inside this launch
+                        const uint32_t S1n = std::max<uint32_t>(2 * nseg_b, 1);
+                        const uint64_t nseg_n = std::min<uint64_t>(S1n, seg_lim);
+                        ensure_tables(Tn, S1n, st);
+                        DevBuf& SAn = par ? segaux_ : segaux2_;
+                        SAn.ensure(segaux_bytes(S1n), st);
+                        DevBuf& TSn = par ? tile_seg_ : tile_seg2_;
+                        TSn.ensure(size_t(out_bound / kTile + nseg_n + 1) * 4, st);
+                        la.n_kind = Tn.kind.as<uint8_t>(); la.n_link = Tn.link.as<uint32_t>();
+                        la.n_segs = Tn.segs.as<SegRec>(); la.n_fins = Tn.fins.as<FinRec>(); la.n_fin_cap = S1n;
+                        la.n_info = dinfo + 1; la.nn_info = dinfo + 2;
+                        la.n_tile_seg = TSn.as<uint32_t>();
+                        la.n_seg_pcnt = seg_pcnt(SAn); la.n_seg_done = seg_done(SAn, S1n); la.n_seg_ctr = seg_ctr(SAn, S1n);
+                    }
                     tk(3, st, [&] { ck(launch_level(la, false, stable_, grid, st), "level launch"); });
                 }
                 in = out;
                 S = 2 * nseg_b;
+                if (pfree) par ^= 1;
+                planned = pfree;
             }
             ck(cudaMemcpyAsync(h_info_, info_.as<LevelInfo>() + (lvl - 1), sizeof(LevelInfo),
                                cudaMemcpyDeviceToHost, st), "d2h info");
@@ -468,7 +491,7 @@ class Engine {
         segaux_.ensure(segaux_bytes(1), st);
         ck(cudaMemsetAsync(segaux_.p, 0, segaux_bytes(1), st), "memset seg aux");
         const int grid = std::max(1, std::min<int>(int(g.ntiles), sms_ * (stable_ ? occ_level_stable_ : occ_level_)));
-        LevelArgs la;
+        LevelArgs la = {};
         la.gx = bufs_[0].x.as<double>(); la.gy = bufs_[0].y.as<double>();
         la.segs = dseg; la.tile_seg = tile_seg_.as<uint32_t>(); la.info = dli;
         la.ix = bufs_[0].x.as<double>(); la.iy = bufs_[0].y.as<double>(); la.iid = bufs_[0].id.as<uint32_t>();
@@ -730,7 +753,7 @@ class Engine {
         for (LevelTables& T : levels_)
             for (DevBuf* d : {&T.slots, &T.kind, &T.link, &T.size, &T.start, &T.segs, &T.fins, &T.fin_count})
                 d->release();
-        for (DevBuf* d : {&tile_seg_, &chain_, &out_, &part_, &status_, &flags_, &aggs_, &incs_, &cert_head_,
+        for (DevBuf* d : {&tile_seg_, &tile_seg2_, &segaux2_, &chain_, &out_, &part_, &status_, &flags_, &aggs_, &incs_, &cert_head_,
                           &cert_rec_, &cert_asc_, &cert_tab_, &sorted_, &sort_tmp_, &mg_, &mstarts_, &mout_})
             d->release();
         for (GraphEntry& e : graphs_)
@@ -1339,6 +1362,23 @@ class Engine {
     // per-segment scratch of the level kernel: partial count, finished tiles
     // (u32 each) and the fast mode's packed L/R counter (u64)
     static size_t segaux_bytes(uint32_t ns) { return size_t(ns) * 16 + 16; }
+    static uint32_t* seg_pcnt(DevBuf& b) { return b.as<uint32_t>(); }
+    static uint32_t* seg_done(DevBuf& b, uint32_t ns) { return b.as<uint32_t>() + ns; }
+    static unsigned long long* seg_ctr(DevBuf& b, uint32_t ns) {
+        return reinterpret_cast<unsigned long long*>(b.as<char>() + ((size_t(ns) * 8 + 7) & ~size_t(7)));
+    }
+    void ensure_tables(LevelTables& T, uint32_t S1, cudaStream_t st) {
+        T.kind.ensure(S1, st);
+        T.link.ensure(size_t(S1) * 4, st);
+        T.size.ensure(size_t(S1) * 4, st);
+        T.start.ensure(size_t(S1) * 4, st);
+        T.segs.ensure(size_t(S1) * sizeof(SegRec), st);
+        T.fins.ensure(size_t(S1) * sizeof(FinRec), st);
+        T.fin_count.ensure(size_t(S1) * 4, st);
+    }
+    DevBuf tile_seg2_, segaux2_;  // the second tile-map / segment-counter set (planner-free levels)
+    // VQHULL_PLANNER=1: the planner and tile-map kernels before every host level
+    bool use_pf_ = !(getenv("VQHULL_PLANNER") && getenv("VQHULL_PLANNER")[0] == '1');
     uint32_t* seg_pcnt() { return segaux_.as<uint32_t>(); }
     uint32_t* seg_done(uint32_t ns) { return segaux_.as<uint32_t>() + ns; }
     unsigned long long* seg_ctr(uint32_t ns) {

@@ -205,6 +205,22 @@ struct LevelArgs {
     uint32_t* seg_done;  // per segment: tiles finished
     unsigned long long* seg_ctr;  // fast mode: packed L/R counters per segment
     ChildRec* children;  // 2 per segment
+    // the next level's plan, written by the level kernel as each segment
+    // finishes (planner-free host levels; n_kind == nullptr: the host runs the
+    // planner kernel instead): kinds, links, SegRec / FinRec tables, the tile
+    // -> segment map, zeroed per-segment counters, and LevelInfo counters
+    // (atomics); nn_info (the level after) is zeroed for the next launch
+    uint8_t* n_kind;
+    uint32_t* n_link;
+    SegRec* n_segs;
+    FinRec* n_fins;
+    uint32_t n_fin_cap;
+    LevelInfo* n_info;
+    LevelInfo* nn_info;
+    uint32_t* n_tile_seg;
+    uint32_t* n_seg_pcnt;
+    uint32_t* n_seg_done;
+    unsigned long long* n_seg_ctr;
 };
 
 // Persistent recursion kernel (tail.cu): per level, the host-allocated tables

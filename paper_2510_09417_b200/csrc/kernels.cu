@@ -781,6 +781,7 @@ struct PlanArgs {
     uint32_t* seg_pcnt;
     uint32_t* seg_done;
     unsigned long long* seg_ctr;
+    LevelInfo* next_info;  // zeroed here: the planner-free level kernel accumulates into it
 };
 
 __device__ __forceinline__ uint8_t kind_of(uint32_t m) {
@@ -801,6 +802,8 @@ __device__ __noinline__ void planner_body(const PlanArgs& a, uint32_t nblocks) {
     const uint32_t nslots = a.prev ? 2u * a.prev->nseg : a.nslots;
     const uint32_t nchunks = (nslots + kPlanChunk - 1) / kPlanChunk;
     const uint64_t fin_chain_base = a.prev ? uint64_t(a.prev->fin_base) + a.prev->fin_total : 0ull;
+    if (a.next_info && blockIdx.x == 0 && threadIdx.x < sizeof(LevelInfo) / 4)
+        reinterpret_cast<uint32_t*>(a.next_info)[threadIdx.x] = 0u;
     if (nslots == 0 && blockIdx.x == 0 && threadIdx.x == 0) {
         LevelInfo li;
         li.nslots = 0; li.nseg = 0; li.nfin = 0; li.ntiles = 0;
@@ -1790,8 +1793,9 @@ void launch_planner(const ChildRec* slots, uint32_t nslots, const LevelInfo* pre
                     SegRec* segs, FinRec* fins, uint8_t* kind, uint32_t* link, LevelInfo* info,
                     uint32_t* flags, void* aggs, void* incs, uint32_t epoch, uint32_t* ctr,
                     uint32_t* seg_pcnt, uint32_t* seg_done, unsigned long long* seg_ctr,
-                    int max_grid, cudaStream_t st) {
+                    int max_grid, cudaStream_t st, LevelInfo* next_info) {
     PlanArgs a;
+    a.next_info = next_info;
     a.seg_pcnt = seg_pcnt;
     a.seg_done = seg_done;
     a.seg_ctr = seg_ctr;

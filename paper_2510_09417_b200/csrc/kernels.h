@@ -25,7 +25,7 @@ void launch_planner(const ChildRec* slots, uint32_t nslots, const LevelInfo* pre
                     SegRec* segs, FinRec* fins, uint8_t* kind, uint32_t* link, LevelInfo* info,
                     uint32_t* flags, void* aggs, void* incs, uint32_t epoch, uint32_t* ctr,
                     uint32_t* seg_pcnt, uint32_t* seg_done, unsigned long long* seg_ctr,
-                    int max_grid, cudaStream_t st);
+                    int max_grid, cudaStream_t st, LevelInfo* next_info = nullptr);
 void launch_tilemap(const SegRec* segs, const LevelInfo* info, uint32_t* tile_seg,
                     uint32_t ntiles_hint, cudaStream_t st);
 void launch_finisher(const FinRec* fins, const LevelInfo* info, uint32_t fin_cap, const double* ix,

@@ -1812,6 +1812,75 @@ struct LevelRing {
     uint32_t di[kRing];
 };
 
+// Planner-free host levels: the warp that writes a finished segment's child
+// slot s also plans it for the next level (what planner_body does for a whole
+// level, kernels.cu): its kind; an internal child gets a SegRec, fresh
+// per-segment counters and its entries of the tile -> segment map, a finisher
+// child a FinRec with its chain position, a leaf is counted.  Places in the
+// next level's tables come from atomics on its LevelInfo (their order is free:
+// the output ranges of internal segments are disjoint either way), so the
+// host launches no planner and no tile-map kernel between levels.  Lane 0
+// holds ch; every lane of the warp calls.
+__device__ __forceinline__ void plan_child(const LevelArgs& a, uint64_t s, const ChildRec& ch) {
+    const int lane = threadIdx.x & 31;
+    uint32_t j = 0, t0 = 0, ntl = 0;
+    if (lane == 0) {
+        const uint32_t m = ch.m;
+        const uint8_t kd = kind_of(m);
+        a.n_kind[s] = kd;
+        if (kd == kInternal) {
+            ntl = (m + kTile - 1) / kTile;
+            j = atomicAdd(&a.n_info->nseg, 1u);
+            t0 = atomicAdd(&a.n_info->ntiles, ntl);
+            const uint32_t out = atomicAdd(&a.n_info->out_total, m);
+            SegRec g;
+            g.px = ch.px; g.py = ch.py; g.rx = ch.rx; g.ry = ch.ry; g.qx = ch.qx; g.qy = ch.qy;
+            g.bx = ch.rx; g.by = ch.ry;
+            g.adx = dsub(ch.rx, ch.px); g.ady = dsub(ch.ry, ch.py);  // EdgeFrame::make (kernels.hpp:23-25)
+            g.bdx = dsub(ch.qx, ch.rx); g.bdy = dsub(ch.qy, ch.ry);
+            g.begin = ch.begin;
+            g.out = out;
+            g.m = m;
+            g.tile0 = t0;
+            g.ntiles = ntl;
+            g.slot = uint32_t(s);
+            a.n_segs[j] = g;
+            a.n_seg_pcnt[j] = 0;
+            a.n_seg_done[j] = 0;
+            a.n_seg_ctr[j] = 0ull;
+            a.n_link[s] = j;
+        } else if (kd == kFin) {
+            const uint32_t f = m <= kFinSmall ? atomicAdd(&a.n_info->nfin, 1u)
+                                              : a.n_fin_cap - 1u - atomicAdd(&a.n_info->nfin2, 1u);
+            FinRec fr;
+            fr.c = ch;
+            fr.chain_base = uint64_t(a.info->fin_base) + a.info->fin_total + atomicAdd(&a.n_info->fin_total, m);
+            fr.slot = uint32_t(s);
+            fr.pad = 0;
+            a.n_fins[f] = fr;
+            a.n_link[s] = f;
+        } else {
+            if (kd == kLeaf) atomicAdd(&a.n_info->nleaf, 1u);
+            a.n_link[s] = 0;
+        }
+    }
+    j = __shfl_sync(kFull, j, 0);
+    t0 = __shfl_sync(kFull, t0, 0);
+    ntl = __shfl_sync(kFull, ntl, 0);
+    for (uint32_t t = lane; t < ntl; t += 32) a.n_tile_seg[t0 + t] = j;
+}
+
+// block 0 at the start of a planner-free level: the next level's slot count
+// and chain base; the level after it starts from zero counters
+__device__ __forceinline__ void plan_level_start(const LevelArgs& a) {
+    if (!a.n_kind || blockIdx.x != 0) return;
+    if (threadIdx.x < sizeof(LevelInfo) / 4) reinterpret_cast<uint32_t*>(a.nn_info)[threadIdx.x] = 0u;
+    if (threadIdx.x == 0) {
+        a.n_info->nslots = 2u * a.info->nseg;
+        a.n_info->fin_base = a.info->fin_base + a.info->fin_total;
+    }
+}
+
 // Segment-per-CTA levels, fed by the TMA ring: the control warp walks the
 // CTA's segments (k = blockIdx.x, + gridDim.x, ...) tile by tile and keeps
 // kRing tiles in flight, so the next segment's points are already in shared
@@ -1946,35 +2015,38 @@ __device__ __forceinline__ void level_segcta_tma(const LevelArgs& a, uint32_t ns
             }
         }
         __syncthreads();  // (also: every thread has read S.tot of the last tile)
-        if (tid < 2) {
-            const int c = tid;
-            unsigned long long ko = S.rkey[c][0];
-            uint32_t io = S.ridx[c][0];
-            for (int w = 1; w < kWarps; ++w) {
-                const unsigned long long kk = S.rkey[c][w];
-                const uint32_t ii = S.ridx[c][w];
-                if (kk < ko || (kk == ko && key_better(kk, ii, ko, io, a.gx, a.gy))) {
-                    ko = kk;
-                    io = ii;
-                }
-            }
-            const Best b = best_from_key(ko, io, c == 0 ? adx : bdx, c == 0 ? ady : bdy, a.gx, a.gy);
-            const uint32_t m = c == 0 ? run0 : run1;
+        if (warp < 2) {
+            const int c = warp;
             ChildRec ch;
-            if (c == 0) {  // left of p->r: triangle (p, rL, r)
-                ch.px = g.px; ch.py = g.py; ch.qx = g.rx; ch.qy = g.ry;
-                ch.begin = g.out;
-            } else {       // left of r->q: triangle (r, rR, q)
-                ch.px = GENERAL ? g.bx : g.rx; ch.py = GENERAL ? g.by : g.ry;
-                ch.qx = g.qx; ch.qy = g.qy;
-                ch.begin = g.out + g.m - m;
+            if (lane == 0) {
+                unsigned long long ko = S.rkey[c][0];
+                uint32_t io = S.ridx[c][0];
+                for (int w = 1; w < kWarps; ++w) {
+                    const unsigned long long kk = S.rkey[c][w];
+                    const uint32_t ii = S.ridx[c][w];
+                    if (kk < ko || (kk == ko && key_better(kk, ii, ko, io, a.gx, a.gy))) {
+                        ko = kk;
+                        io = ii;
+                    }
+                }
+                const Best b = best_from_key(ko, io, c == 0 ? adx : bdx, c == 0 ? ady : bdy, a.gx, a.gy);
+                const uint32_t m = c == 0 ? run0 : run1;
+                if (c == 0) {  // left of p->r: triangle (p, rL, r)
+                    ch.px = g.px; ch.py = g.py; ch.qx = g.rx; ch.qy = g.ry;
+                    ch.begin = g.out;
+                } else {       // left of r->q: triangle (r, rR, q)
+                    ch.px = GENERAL ? g.bx : g.rx; ch.py = GENERAL ? g.by : g.ry;
+                    ch.qx = g.qx; ch.qy = g.qy;
+                    ch.begin = g.out + g.m - m;
+                }
+                ch.rx = b.x;
+                ch.ry = b.y;
+                ch.r_idx = b.idx;
+                ch.m = m;
+                VQB_CHECK(2 * uint64_t(k) + c < a.children_cap, 58, k, a.children_cap);
+                a.children[2 * uint64_t(k) + c] = ch;
             }
-            ch.rx = b.x;
-            ch.ry = b.y;
-            ch.r_idx = b.idx;
-            ch.m = m;
-            VQB_CHECK(2 * uint64_t(k) + c < a.children_cap, 58, k, a.children_cap);
-            a.children[2 * uint64_t(k) + c] = ch;
+            if (a.n_kind) plan_child(a, 2 * uint64_t(k) + c, ch);
         }
         __syncthreads();  // S reused by the next segment
     }
@@ -1983,6 +2055,7 @@ __device__ __forceinline__ void level_segcta_tma(const LevelArgs& a, uint32_t ns
 template <bool GENERAL>
 __global__ void __launch_bounds__(kCtlThreads, 3) level_tma(LevelArgs a) {
     VQB_PDL();
+    plan_level_start(a);
     {
         // many small segments (at most kSegCtaTiles tiles on average): one
         // CTA per segment, no cross-CTA claims or partials (uniform branch)
@@ -2092,11 +2165,11 @@ __global__ void __launch_bounds__(kCtlThreads, 3) level_tma(LevelArgs a) {
                     if (prefer(o, b)) b = o;
                 }
                 b = warp_best(b);
+                ChildRec ch;
                 if (lane == 0) {
                     const SegRec& g = s_cur;
                     const uint2 w = read_pair(&a.seg_ctr[s_cur_k]);
                     const uint32_t m = c == 0 ? w.x : w.y;
-                    ChildRec ch;
                     if (c == 0) {  // left of p->r: triangle (p, rL, r)
                         ch.px = g.px; ch.py = g.py; ch.qx = g.rx; ch.qy = g.ry;
                         ch.begin = g.out;
@@ -2112,6 +2185,7 @@ __global__ void __launch_bounds__(kCtlThreads, 3) level_tma(LevelArgs a) {
                     VQB_CHECK(2 * uint64_t(s_cur_k) + c < a.children_cap, 57, s_cur_k, a.children_cap);
                     a.children[2 * uint64_t(s_cur_k) + c] = ch;
                 }
+                if (a.n_kind) plan_child(a, 2 * uint64_t(s_cur_k) + c, ch);
             }
         }
         __syncthreads();

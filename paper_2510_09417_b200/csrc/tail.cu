@@ -331,7 +331,7 @@ __global__ void __launch_bounds__(kThreads, 2) tail_kernel(const __grid_constant
             return;
         }
         // ---- work: K2 tiles, then the finisher segments
-        LevelArgs la;
+        LevelArgs la = {};
         la.gx = A.gx;
         la.gy = A.gy;
         la.segs = T.segs;
