@@ -228,14 +228,12 @@ def hull_device(x, y, stream=None, out=None, u32: bool = False):
         raise ValueError(f"hull_device: out must be a contiguous {want} tensor on {x.device} "
                          f"with room for {n} indices")
     cnt = C.c_uint64(0)
-    with torch.cuda.device(x.device):
-        st = _stream_ptr(stream, x.device)
-        if u32:
-            rc = lib().vqhull_cuda_hull_u32(x.data_ptr(), y.data_ptr(), n, out.data_ptr(),
-                                            C.byref(cnt), st)
-        else:
-            rc = lib().vqhull_cuda_hull(x.data_ptr(), y.data_ptr(), n, out.data_ptr(),
-                                        C.byref(cnt), st)
+    fn = lib().vqhull_cuda_hull_u32 if u32 else lib().vqhull_cuda_hull
+    if x.device.index == torch.cuda.current_device():  # (the common case: no device switch)
+        rc = fn(x.data_ptr(), y.data_ptr(), n, out.data_ptr(), C.byref(cnt), _stream_ptr(stream, x.device))
+    else:
+        with torch.cuda.device(x.device):
+            rc = fn(x.data_ptr(), y.data_ptr(), n, out.data_ptr(), C.byref(cnt), _stream_ptr(stream, x.device))
     _check(rc, "vqhull_cuda_hull")
     return out[: cnt.value]
 
