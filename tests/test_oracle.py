@@ -5,6 +5,8 @@ itself and (b) the reference library run live (oracle/_ref) when present.
 Mirrors proj/tests/test_geometry.cpp, test_extract.cpp, test_hull.cpp,
 test_dataset_io.cpp and test_bench.cpp.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -121,3 +123,20 @@ def test_oracle_config_golden(oracle, vq, name):
     assert f"{oracle.fnv1a64(idx):016x}" == cfg["fnv1a64_u64le"]
     if "indices" in cfg:
         assert idx.tolist() == cfg["indices"]
+
+
+def test_config5_global_golden_index_mapping(oracle, reference):
+    """tests/golden/make_config5_global.py maps the reference's hull
+    coordinates to first input indices by a scan; on a small input with
+    duplicates it equals the reference mapping (vqhull_c.cpp:46-61)."""
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden"))
+    from make_config5_global import first_occurrence
+
+    xs, ys = reference.generate("disk", 50_000, 5, 4)
+    xs[-50:], ys[-50:] = xs[:50], ys[:50]
+    xs[7], ys[7] = -0.0 * xs[7], ys[7]  # (a signed zero never matters here; the scan uses ==)
+    hx, hy = reference.convex_hull(xs, ys, workers=2)
+    got = first_occurrence(xs, ys, hx, hy, chunk=1 << 12)
+    rc, ref = reference.compute(xs, ys)
+    assert rc == 0 and np.array_equal(got, ref)
