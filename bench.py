@@ -335,9 +335,17 @@ def run_ours(args) -> int:
     if not torch.cuda.is_available():
         print("bench.py: no CUDA device visible", file=sys.stderr)
         return 2
+    # test hook (tests/test_sharded_gpu.py): every rank on cuda:0 over gloo, so
+    # the N > 1 code path runs on a one-GPU box; never used for a bench line
+    share = os.environ.get("VQHULL_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     wl = Workload(args, world)
     offset, n = wl.shard(rank)
 

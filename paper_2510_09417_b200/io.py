@@ -6,8 +6,10 @@ Follows the reference's binary format and its checks
 as f64 — exactly the SoA layout the device path keeps in HBM, so a file is
 two reads into pinned buffers and two H2D copies, no reshuffle.  Errors
 raise :class:`LoadError` with the reference's messages (bad magic, truncated
-header, truncated payload, non-finite coordinate at point i).  The text
-format (``pbbs_sequencePoint2d``) is out of scope.
+header, truncated payload, non-finite coordinate at point i).  The reference's
+text format (``pbbs_sequencePoint2d``, ``io.cpp:100-160``) is read and written
+too (:func:`read_points`, :func:`write_points`); it is kept as written in
+round 1 and not developed further.
 """
 from __future__ import annotations
 
@@ -137,6 +139,10 @@ def to_chars(v: float) -> str:
     from decimal import Decimal
 
     v = float(v)
+    if v != v:  # libstdc++ prints the sign of a NaN
+        return "-nan" if str(v).startswith("-") or np.signbit(v) else "nan"
+    if v in (float("inf"), float("-inf")):
+        return "-inf" if v < 0 else "inf"
     neg = v < 0 or (v == 0 and str(v).startswith("-"))
     if v == 0:
         return "-0" if neg else "0"
@@ -186,7 +192,19 @@ def _read_text(path: str) -> Tuple[np.ndarray, np.ndarray]:
             m = _NUM.match(line, cur)
             if not m:
                 raise LoadError(f"{path}: malformed coordinate on line {lineno}")
-            vals.append(float(m.group(0)))
+            lit = m.group(0)
+            try:
+                v = float(lit)
+            except ValueError:  # e.g. nan(...) payloads float() does not take
+                raise LoadError(f"{path}: malformed coordinate on line {lineno}") from None
+            # std::from_chars reports result_out_of_range (the reference:
+            # malformed) for a finite literal that overflows, or a nonzero one
+            # that underflows to zero
+            mant = lit.lower().split("e")[0]
+            if (v == 0.0 and any(c in mant for c in "123456789")) or \
+                    (v in (float("inf"), float("-inf")) and "inf" not in lit.lower()):
+                raise LoadError(f"{path}: malformed coordinate on line {lineno}")
+            vals.append(v)
             cur = m.end()
         xs.append(vals[0])
         ys.append(vals[1])

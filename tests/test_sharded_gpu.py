@@ -267,3 +267,28 @@ def test_hull_multi_beyond_u32(vq, cuda, oracle):
     rc, g = vq.vqhull_compute(xs, ys)
     assert rc == 0 and np.array_equal(g, g2)
     del xs, ys
+
+
+def test_bench_multi_gpu_path_on_one_gpu(cuda, tmp_path):
+    """bench.py's N > 1 flow (torchrun, sharded config 5 with a reduced n,
+    timing, max over ranks, e2e) end to end, both ranks on this one GPU over
+    gloo (VQHULL_BENCH_SHARE_GPU, a test hook): the JSON line it prints."""
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, VQHULL_BENCH_SHARE_GPU="1")
+    env.pop("WORLD_SIZE", None)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+           os.path.join(root, "bench.py"), "--gpus", "2", "--n", "4000000", "--steps", "2", "--warmup", "1",
+           "--no-cpu"]
+    p = subprocess.run(cmd, capture_output=True, text=True, env=env, timeout=900, cwd=root)
+    assert p.returncode == 0, p.stderr[-3000:]
+    line = [l for l in p.stdout.splitlines() if l.startswith("{")][-1]
+    d = json.loads(line)
+    assert d["n_gpus"] == 2 and d["scaling"] == "strong"
+    assert d["config"]["workload"].startswith("config5: disk seed=5, n=4000000 total, sharded evenly over 2 GPU(s)")
+    assert d["details"]["merge"]["margin_retries"] == 0 and d["details"]["merge"]["hull"] > 100
+    assert d["value"] > 0 and d["e2e"]["value"] > 0 and d["gpu_launches"] > 0
