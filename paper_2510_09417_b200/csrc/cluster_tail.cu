@@ -43,6 +43,9 @@ constexpr int kKcChildren = 2 * kKcNodes;
 constexpr int kKcTree = 2048;       // internal tree nodes (hull vertices from internal nodes)
 constexpr int kKcLeaves = 2048;
 constexpr int kKcLevels = kTailLevels - 1;
+constexpr int kKcWarps = kKcThreads / 32;
+constexpr int kKcWarpPts = kKcPts / kKcWarps;  // points a warp owns (256)
+constexpr int kKcRounds = kKcWarpPts / 32;     // its rounds of 32 (8)
 constexpr uint32_t kKcNone = 0xffffffffu;
 constexpr uint16_t kKcDead = 0xffffu;
 
@@ -54,6 +57,7 @@ struct KcSmem {
     double x[kKcPts];
     double y[kKcPts];
     uint16_t pn[kKcPts];                    // node id (between levels) / child id (in a level) / dead
+    uint16_t lst[kKcThreads / 32][kKcPts / (kKcThreads / 32)];  // each warp's live points
     // per child, double-buffered by level parity (read remotely over DSMEM)
     uint32_t lcnt[2][kKcChildren];
     unsigned long long lkey[2][kKcChildren];
@@ -111,6 +115,10 @@ __global__ void __launch_bounds__(kKcThreads, 1) cluster_tail_kernel(const __gri
         S.y[i] = gy[lo + i];
         S.pn[i] = 0;
     }
+    // warp w owns points [w * P, (w + 1) * P) and walks only its live ones
+    const uint32_t P = (np + kKcWarps - 1) / kKcWarps;
+    uint32_t wn = warp * P < np ? min(P, np - warp * P) : 0u;  // (warp-uniform)
+    for (uint32_t j = lane; j < wn; j += 32) S.lst[warp][j] = uint16_t(warp * P + j);
     for (uint32_t c = tid; c < 2u * kKcChildren; c += kKcThreads) {
         const uint32_t b = c / kKcChildren, k = c % kKcChildren;
         S.lcnt[b][k] = 0;
@@ -139,32 +147,40 @@ __global__ void __launch_bounds__(kKcThreads, 1) cluster_tail_kernel(const __gri
     bool ok = true;
     while (true) {
         const int b = depth & 1, nxt = cur ^ 1;
-        // (1) classify this CTA's points; per-child counts and minimal keys
-        for (uint32_t i0 = 0; i0 < np; i0 += kKcThreads) {
-            const uint32_t i = i0 + tid;
+        // (1) classify this CTA's live points; per-child counts and minimal
+        // keys (each lane's keys stay in registers for the candidate pass)
+        uint32_t chv[kKcRounds];
+        unsigned long long keyv[kKcRounds];
+#pragma unroll
+        for (int k = 0; k < kKcRounds; ++k) {
+            chv[k] = kKcNone;
+            keyv[k] = kNoKey;
+            if (uint32_t(k) * 32 >= wn) continue;  // (warp-uniform)
+            const uint32_t j = uint32_t(k) * 32 + lane;
             uint32_t ch = kKcNone;
             unsigned long long key = kNoKey;
-            if (i < np) {
+            if (j < wn) {
+                const uint32_t i = S.lst[warp][j];
                 const uint16_t c = S.pn[i];
-                if (c != kKcDead) {
-                    const KcNode& nd = S.node[cur][c];
-                    const double u = S.x[i], w = S.y[i];
-                    const double Aa = dsub(nd.px, u), B = dsub(nd.py, w);
-                    const double E = dsub(nd.rx, u), F = dsub(nd.ry, w);
-                    const double Cc = dsub(nd.qx, u), D = dsub(nd.qy, w);
-                    const bool la = left_diff(Aa, B, E, F);
-                    const bool lb = !la && left_diff(E, F, Cc, D);
-                    if (la || lb) {
-                        ch = 2u * c + (lb ? 1u : 0u);
-                        const double fx = lb ? dsub(nd.qx, nd.rx) : dsub(nd.rx, nd.px);
-                        const double fy = lb ? dsub(nd.qy, nd.ry) : dsub(nd.ry, nd.py);
-                        key = key_of(lat_off(fx, fy, u, w));
-                        S.pn[i] = uint16_t(ch);
-                    } else {
-                        S.pn[i] = kKcDead;
-                    }
+                const KcNode& nd = S.node[cur][c];
+                const double u = S.x[i], w = S.y[i];
+                const double Aa = dsub(nd.px, u), B = dsub(nd.py, w);
+                const double E = dsub(nd.rx, u), F = dsub(nd.ry, w);
+                const double Cc = dsub(nd.qx, u), D = dsub(nd.qy, w);
+                const bool la = left_diff(Aa, B, E, F);
+                const bool lb = !la && left_diff(E, F, Cc, D);
+                if (la || lb) {
+                    ch = 2u * c + (lb ? 1u : 0u);
+                    const double fx = lb ? dsub(nd.qx, nd.rx) : dsub(nd.rx, nd.px);
+                    const double fy = lb ? dsub(nd.qy, nd.ry) : dsub(nd.ry, nd.py);
+                    key = key_of(lat_off(fx, fy, u, w));
+                    S.pn[i] = uint16_t(ch);
+                } else {
+                    S.pn[i] = kKcDead;
                 }
             }
+            chv[k] = ch;
+            keyv[k] = key;
             const unsigned grp = __match_any_sync(kFull, ch);
             if (grp == kFull) {  // the whole warp in one child (or none)
 #pragma unroll
@@ -205,14 +221,11 @@ __global__ void __launch_bounds__(kKcThreads, 1) cluster_tail_kernel(const __gri
         }
         __syncthreads();
         // this CTA's candidates: its points holding their child's minimal key
-        for (uint32_t i = tid; i < np; i += kKcThreads) {
-            const uint16_t ch = S.pn[i];
-            if (ch == kKcDead) continue;
-            const KcNode& nd = S.node[cur][ch >> 1];
-            const bool side = ch & 1;
-            const double fx = side ? dsub(nd.qx, nd.rx) : dsub(nd.rx, nd.px);
-            const double fy = side ? dsub(nd.qy, nd.ry) : dsub(nd.ry, nd.py);
-            if (key_of(lat_off(fx, fy, S.x[i], S.y[i])) != S.gkey[ch]) continue;
+#pragma unroll
+        for (int k = 0; k < kKcRounds; ++k) {
+            const uint32_t ch = chv[k];
+            if (ch == kKcNone || keyv[k] != S.gkey[ch]) continue;
+            const uint32_t i = S.lst[warp][uint32_t(k) * 32 + lane];
             if (atomicAdd(&S.lncand[b][ch], 1u) == 0) S.lcand[b][ch] = i;
             else S.tlist[atomicAdd(&S.ntie, 1u)] = uint16_t(i);
         }
@@ -243,17 +256,19 @@ __global__ void __launch_bounds__(kKcThreads, 1) cluster_tail_kernel(const __gri
             double bx = 0.0, by = 0.0;
             uint32_t bref = kKcNone;
             int ncand = 0, r1 = 0;
+            uint32_t l1 = 0;
 #pragma unroll
             for (int r = 0; r < kKcCtas; ++r)
                 if (lv[r] != kKcNone) {
                     ++ncand;
                     r1 = r;
+                    l1 = lv[r];
                 }
             if (ncand == 1) {
                 const KcSmem* R = cluster.map_shared_rank(&S, r1);
-                bx = R->x[lv[r1]];
-                by = R->y[lv[r1]];
-                bref = (uint32_t(r1) << 16) | lv[r1];
+                bx = R->x[l1];
+                by = R->y[l1];
+                bref = (uint32_t(r1) << 16) | l1;
             } else if (ncand > 1) {  // an exact key tie across CTAs: smaller (x, y), then index
                 uint32_t bg = kKcNone;
                 for (int r = 0; r < kKcCtas; ++r) {
@@ -350,9 +365,25 @@ __global__ void __launch_bounds__(kKcThreads, 1) cluster_tail_kernel(const __gri
             S.lcand[b ^ 1][c] = kKcNone;
         }
         __syncthreads();  // cmap complete
-        for (uint32_t i = tid; i < np; i += kKcThreads) {
-            const uint16_t ch = S.pn[i];
-            if (ch != kKcDead) S.pn[i] = S.cmap[ch];
+        {  // points follow their child to its next node id; the warp's live list shrinks in place
+            uint32_t w2 = 0;
+            for (uint32_t j0 = 0; j0 < wn; j0 += 32) {
+                const uint32_t j = j0 + lane;
+                uint32_t i = 0;
+                bool alive = false;
+                if (j < wn) {
+                    i = S.lst[warp][j];
+                    const uint16_t ch = S.pn[i];
+                    const uint16_t nd = ch == kKcDead ? kKcDead : S.cmap[ch];
+                    S.pn[i] = nd;
+                    alive = nd != kKcDead;
+                }
+                const unsigned bal = __ballot_sync(kFull, alive);
+                __syncwarp();  // every lane has read its entry before any is overwritten
+                if (alive) S.lst[warp][w2 + __popc(bal & lt)] = uint16_t(i);
+                w2 += __popc(bal);
+            }
+            wn = w2;
         }
         ntree += nnext;
         nleaf += nlv;
