@@ -39,6 +39,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import re
 import socket
 import subprocess
 import sys
@@ -69,7 +70,7 @@ def parse(argv=None):
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--config", type=int, default=0, choices=[0, *sorted(CONFIGS)],
                    help="BASELINE config (default: 2 on one GPU, 5 sharded on N > 1)")
-    p.add_argument("--n", type=int, default=0, help="override the workload's point count")
+    p.add_argument("--points", "--n", dest="n", type=int, default=0, help="override the workload's point count")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--profile", action="store_true", help="minimal run for ncu (no extras)")
@@ -213,7 +214,9 @@ def relaunch(args) -> int:
         return 2
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
            f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
-           "--master-port", str(free_port()), os.path.abspath(__file__), *sys.argv[1:]]
+           "--master-port", str(free_port()), os.path.abspath(__file__),
+           # (torchrun's own parser reads "--n" as an ambiguous abbreviation)
+           *[re.sub(r"^--n(?==|$)", "--points", a) for a in sys.argv[1:]]]
     return subprocess.run(cmd).returncode
 
 

@@ -282,7 +282,7 @@ def test_bench_multi_gpu_path_on_one_gpu(cuda, tmp_path):
     env.pop("WORLD_SIZE", None)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
-           os.path.join(root, "bench.py"), "--gpus", "2", "--n", "4000000", "--steps", "2", "--warmup", "1",
+           os.path.join(root, "bench.py"), "--gpus", "2", "--points", "4000000", "--steps", "2", "--warmup", "1",
            "--no-cpu"]
     p = subprocess.run(cmd, capture_output=True, text=True, env=env, timeout=900, cwd=root)
     assert p.returncode == 0, p.stderr[-3000:]

@@ -9,4 +9,4 @@ timeout 1200 python -m pytest tests/test_sharded_gpu.py -x -q > gpurun_out/shard
 timeout 2400 python -m pytest tests -m gpu -q -x > gpurun_out/gpu_all.log 2>&1
 timeout 900 python bench.py > gpurun_out/bench.log 2> gpurun_out/bench.err
 timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.log 2>&1
-tail -3 gpurun_out/sharded.log gpurun_out/gpu_all.log; cat gpurun_out/bench.log gpurun_out/bench_ref.log
+tail -n 3 gpurun_out/sharded.log; tail -n 3 gpurun_out/gpu_all.log; cat gpurun_out/bench.log gpurun_out/bench_ref.log
