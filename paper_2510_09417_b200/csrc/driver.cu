@@ -131,6 +131,7 @@ class Engine {
         occ_level_ = std::max(1, occupancy_level(false));
         occ_level_stable_ = std::max(1, occupancy_level(true));
         occ_fin_ = std::max(1, occupancy_finisher());
+        occ_fb_ = std::max(1, occupancy_finisher_batch());
         occ_filt_ = std::max(1, occupancy_filtered());
         occ_filter_ = std::max(1, occupancy_filter());
         occ_tail_ = std::max(1, std::min(getenv("VQHULL_TAIL_OCC") ? atoi(getenv("VQHULL_TAIL_OCC")) : 1, occupancy_tail()));
@@ -281,9 +282,14 @@ class Engine {
                 // finishers: whole subtrees of every segment of <= kFinMax
                 // points (a warp each up to kFinSmall, a CTA each above)
                 tk(4, st, [&] {
-                    launch_finisher(T.fins.as<FinRec>(), dinfo, S1, bufs_[in].x.as<double>(),
-                                    bufs_[in].y.as<double>(), bufs_[in].id.as<uint32_t>(), chain_.as<uint32_t>(),
-                                    T.fin_count.as<uint32_t>(), S1, sms_ * occ_fin_, st);
+                    if (use_fb_)
+                        launch_finisher_batch(T.fins.as<FinRec>(), dinfo, S1, bufs_[in].x.as<double>(),
+                                              bufs_[in].y.as<double>(), bufs_[in].id.as<uint32_t>(),
+                                              chain_.as<uint32_t>(), T.fin_count.as<uint32_t>(), S1, sms_ * occ_fb_, st);
+                    else
+                        launch_finisher(T.fins.as<FinRec>(), dinfo, S1, bufs_[in].x.as<double>(),
+                                        bufs_[in].y.as<double>(), bufs_[in].id.as<uint32_t>(), chain_.as<uint32_t>(),
+                                        T.fin_count.as<uint32_t>(), S1, sms_ * occ_fin_, st);
                 });
                 // K2 over all internal segments of this level
                 const int out = in ^ 1;
@@ -590,7 +596,7 @@ class Engine {
         cert_asc_.ensure(size_t(2 * kCertMax) * 4, st);
         cert_tab_.ensure(size_t(kCertBuckets) * 4, st);
         resid_.ensure(std::max<uint64_t>(m, 1), st);
-        ck(cudaMemsetAsync(ctrs_ + 20, 0, 12, st), "memset cert counters");  // count + amax bits
+        ck(cudaMemsetAsync(ctrs_ + 20, 0, 16, st), "memset cert counters");  // count, pad, amax bits (8-byte aligned)
         tk(5, st, [&] {
             launch_cert_build(out_.as<uint32_t>(), uint32_t(h), dx, dy, floor_m, cert_head_.as<CertHead>(),
                               cert_rec_.as<CertRec>(), cert_asc_.as<float>(), cert_tab_.as<uint32_t>(), st);
@@ -603,14 +609,14 @@ class Engine {
                            reinterpret_cast<unsigned long long*>(ctrs_ + 22), sms_ * 8, st);
         });
         CertHead ch;
-        ck(cudaMemcpyAsync(h_word_ + 4, ctrs_ + 20, 12, cudaMemcpyDeviceToHost, st), "d2h cert counters");
+        ck(cudaMemcpyAsync(h_word_ + 4, ctrs_ + 20, 16, cudaMemcpyDeviceToHost, st), "d2h cert counters");
         ck(cudaMemcpyAsync(h_dbl_ + 1, cert_head_.p, sizeof(CertHead), cudaMemcpyDeviceToHost, st), "d2h cert");
         ck(cudaStreamSynchronize(st), "sync");
         std::memcpy(&ch, h_dbl_ + 1, sizeof ch);
         const uint32_t k = h_word_[4];
         double amax;
         {
-            uint64_t bits = uint64_t(h_word_[5]) | (uint64_t(h_word_[6]) << 32);
+            uint64_t bits = uint64_t(h_word_[6]) | (uint64_t(h_word_[7]) << 32);
             std::memcpy(&amax, &bits, 8);
         }
         double m_eff = kInf;
@@ -1292,7 +1298,9 @@ class Engine {
    private:
     int dev_ = 0;
     int sms_ = 148;
-    int occ_root_ = 1, occ_root_stable_ = 1, occ_level_ = 1, occ_level_stable_ = 1, occ_fin_ = 1;
+    int occ_root_ = 1, occ_root_stable_ = 1, occ_level_ = 1, occ_level_stable_ = 1, occ_fin_ = 1, occ_fb_ = 1;
+    // VQHULL_FIN_OLD=1: the one-segment-per-CTA finisher (A/B runs)
+    bool use_fb_ = getenv("VQHULL_FIN_OLD") == nullptr;
     int stream_grid_ = 592, grid_ext_ = 592, grid_boot_ = 592, grid_poly_ = 592, occ_filt_ = 1, occ_filter_ = 1;
     bool force_reference_ = false;
     int occ_tail_ = 1;

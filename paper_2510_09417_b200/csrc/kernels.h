@@ -31,6 +31,11 @@ void launch_tilemap(const SegRec* segs, const LevelInfo* info, uint32_t* tile_se
 void launch_finisher(const FinRec* fins, const LevelInfo* info, uint32_t fin_cap, const double* ix,
                      const double* iy, const uint32_t* iid, uint32_t* chain, uint32_t* fin_count,
                      uint32_t nfin_hint, int max_grid, cudaStream_t st);
+// batch finisher (finisher.cu): several segments per CTA, nodes named by their apex
+void launch_finisher_batch(const FinRec* fins, const LevelInfo* info, uint32_t fin_cap, const double* ix,
+                           const double* iy, const uint32_t* iid, uint32_t* chain, uint32_t* fin_count,
+                           uint32_t nfin_hint, int max_grid, cudaStream_t st);
+int occupancy_finisher_batch();
 void launch_size(uint32_t nslots, const uint8_t* kind, const uint32_t* link,
                  const uint32_t* fin_count, const uint32_t* child_size, uint32_t* size,
                  cudaStream_t st);

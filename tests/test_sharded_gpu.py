@@ -127,6 +127,8 @@ def test_shard_candidates_pack_layout(vq, cuda, oracle):
     P = pack.cpu().numpy()
     assert P[0, 0] == k and 0 < k < 20_000
     assert 0.9 < P[0, 1] <= 1.0 and P[0, 2] <= 1.0
+    # A = the largest |coordinate| in play: at least the candidates', at most the shard's
+    assert np.abs(P[1:1 + k, :2]).max() <= P[0, 2] <= max(np.abs(xs).max(), np.abs(ys).max())
     g = P[1:1 + k, 2].copy().view(np.int64)
     assert np.all(np.diff(g) > 0) and g.min() >= off
     loc = g - off
@@ -142,6 +144,23 @@ def test_shard_candidates_pack_layout(vq, cuda, oracle):
     big = torch.empty((k + 1, 3), dtype=torch.float64, device="cuda")
     vq.shard_repack(big)
     assert np.array_equal(big.cpu().numpy()[: k + 1], P[: k + 1])
+
+
+@pytest.mark.parametrize("n,seed", [(2_000_000, 5), (700_000, 1), (5_000_000, 2)])
+def test_shard_header_scale(vq, cuda, n, seed):
+    """A in the header is a real magnitude on every shard (a stale counter
+    word once made it garbage and forced a needless margin retry)."""
+    import torch
+
+    xs, ys = vq.generate("disk", n, seed)
+    for lo, hi in ((0, n // 2), (n // 2, n)):
+        X, Y = torch.from_numpy(xs[lo:hi]).cuda(), torch.from_numpy(ys[lo:hi]).cuda()
+        for _ in range(2):
+            pack, k = vq.shard_candidates(X, Y, lo, cap=1 << 16)
+            P = pack.cpu().numpy()
+            cand = np.abs(P[1:1 + k, :2]).max()
+            assert cand <= P[0, 2] <= max(np.abs(xs[lo:hi]).max(), np.abs(ys[lo:hi]).max()), P[0]
+            assert 0.9 < P[0, 1] <= 1.0
 
 
 # --- torch.distributed at world size 2 on one GPU (gloo, host staging) -------

@@ -15,5 +15,7 @@ for _ in range(K): vq.hull_device(X, Y, out=out, u32=True)
 e1.record(); torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / K
 vq.set_timing(True); vq.hull_device(X, Y, out=out, u32=True); s = vq.stats(); vq.set_timing(False)
+hh = vq.hull_device(X, Y, out=out, u32=True).long()
+sig = int((hh * torch.arange(1, hh.numel() + 1, device='cuda')).sum().item()) & 0xffffffffffff
 fam = {k[3:]: round(v, 3) for k, v in s.items() if k.startswith('ms_')}
-print(f"{kind} n={n}: {ms:.3f} ms/hull  {n/ms/1e6:.3g} Gpts/s  levels={s['levels']} launches={s['launches']} {fam}")
+print(f"{kind} n={n}: {ms:.3f} ms/hull  {n/ms/1e6:.3g} Gpts/s  levels={s['levels']} launches={s['launches']} h={hh.numel()} sig={sig:012x} {fam}")
