@@ -152,9 +152,11 @@ int vqhull_cuda_set_root_mode(int mode);
 /* The filter pass's fast inner test (a drop region verified inside the
  * filter polygon, tested before the chord test): -1 = automatic (the sample
  * pass picks the region of largest area, default), 0 = the box only,
- * 1 = box | octagon, 2 = box | disk (a forced region that does not exist for
- * the input falls back to the automatic choice).  The hull never depends on
- * it; tests use it to show that.  Returns VQHULL_EINVAL outside -1..2. */
+ * 1 = box | octagon, 2 = box | disk, 3 = the disk alone (what the automatic
+ * choice takes when the disk covers the box; a forced region that does not
+ * exist for the input falls back to the automatic choice).  The hull never
+ * depends on it; tests use it to show that.  Returns VQHULL_EINVAL outside
+ * -1..3. */
 int vqhull_cuda_set_filter_inner(int mode);
 
 /* Frees this thread's device engine buffers (points, level tables) and

@@ -387,7 +387,7 @@ def set_root_mode(mode: str) -> None:
     _check(lib().vqhull_cuda_set_root_mode(ROOT_MODES[mode]), "vqhull_cuda_set_root_mode")
 
 
-FILTER_INNER = {"auto": -1, "box": 0, "octagon": 1, "disk": 2}
+FILTER_INNER = {"auto": -1, "box": 0, "octagon": 1, "disk": 2, "disk_only": 3}
 
 
 def set_filter_inner(mode: str) -> None:

@@ -363,6 +363,8 @@ class Engine {
         }
         for (int l = 2; l <= lmax_; ++l) {
             const LevelInfo& li = hinfo_[l];
+            VQB_TRACE("level %d: slots %u internal %u (points %u) finisher %u+%u (points %u) leaves %u", l, li.nslots,
+                      li.nseg, li.out_total, li.nfin, li.nfin2, li.fin_total, li.nleaf);
             // every point of this level's slots was written (20 B) by the
             // previous partition (KB for level 2, K2 otherwise)
             const uint64_t written = uint64_t(li.out_total) + li.fin_total + li.nleaf;
@@ -1698,7 +1700,7 @@ int vqhull_cuda_set_root_mode(int mode) {
 }
 
 int vqhull_cuda_set_filter_inner(int mode) {
-    if (mode < -1 || mode > 2) return VQHULL_EINVAL;
+    if (mode < -1 || mode > 3) return VQHULL_EINVAL;
     try {
         Engine& e = vqb::engine();
         std::lock_guard<std::mutex> lk(e.mutex());

@@ -32,10 +32,16 @@
 
 namespace vqb {
 
-constexpr int kFbThreads = 256;
+#ifndef VQB_FB_THREADS
+#define VQB_FB_THREADS 256
+#endif
 #ifndef VQB_FB_ITEMS
 #define VQB_FB_ITEMS 3
 #endif
+#ifndef VQB_FB_MINB
+#define VQB_FB_MINB 4  // 64 registers (a few spilled words): 4 CTAs per SM beat 3 at 76 registers (1.27 -> 1.10 ms on circle 1e7)
+#endif
+constexpr int kFbThreads = VQB_FB_THREADS;
 constexpr int kFbItems = VQB_FB_ITEMS;             // point slots per thread
 constexpr int kFbCap = kFbThreads * kFbItems;      // point slots per batch
 constexpr int kFbSegs = 32;                        // segments per batch (one warp plans a batch)
@@ -270,7 +276,7 @@ __device__ __forceinline__ void fb_run_list(FbSmem& S, const FinRec* fins, int64
     }
 }
 
-__global__ void __launch_bounds__(kFbThreads) finisher_batch_kernel(const FinRec* fins, const LevelInfo* info,
+__global__ void __launch_bounds__(kFbThreads, VQB_FB_MINB) finisher_batch_kernel(const FinRec* fins, const LevelInfo* info,
                                                                     uint32_t fin_cap,
                                                                     const double* __restrict__ ix,
                                                                     const double* __restrict__ iy,

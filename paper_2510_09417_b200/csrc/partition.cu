@@ -20,6 +20,7 @@
 // The arg-max does not ride the look-back: each CTA keeps a running best per
 // segment and publishes it once per segment visit; the CTA that completes a
 // segment's tile count reduces those few partials and emits the children.
+#include <type_traits>
 #include <cstdint>
 #include <cstdlib>
 
@@ -1352,6 +1353,7 @@ __global__ void __launch_bounds__(kCtlThreads, 3) root_filtered_tma(RootArgs a) 
                 run1 += __popc(b1);
             }
         };
+        uint32_t sn_prev = 0;  // this warp's survivors of the tile before
         for (uint32_t k = 0; k < nt; ++k) {
             const uint32_t t = blockIdx.x + k * G;
             const uint32_t tbase = t * uint32_t(kTile);
@@ -1587,12 +1589,14 @@ __global__ void __launch_bounds__(kCtlThreads, 3) root_filter_tma(FilterArgs a) 
         const double bx0 = filter ? P.bx0 : kInf, bx1 = filter ? P.bx1 : -kInf;
         const double by0 = filter ? P.by0 : kInf, by1 = filter ? P.by1 : -kInf;
         const unsigned lt = lanemask_lt();
-        auto store_tile = [&](uint32_t k) {  // tile k's survivors, offsets behind barrier B
+        auto store_tile = [&](uint32_t k, uint32_t sn) {  // tile k's survivors, offsets behind barrier B
             const int par = int(k & 1);
+            // (every warp syncs, survivors or not: the wait bounds the warps'
+            // skew to one tile, which is what lets two barrier parities do)
             named_sync<3>(par, kCtlThreads);
+            if (sn == 0) return;  // (warp-uniform) nothing to place
             const uint32_t tbase = (blockIdx.x + k * G) * uint32_t(kTile);
             const int s = int(k % kRing4);
-            const uint32_t sn = s_cnt[par][warp];
             const uint32_t o = s_org[par][warp];
             for (uint32_t j = lane; j < sn; j += 32) {
                 const uint32_t idx = s_surv[par][warp][j];
@@ -1609,6 +1613,7 @@ __global__ void __launch_bounds__(kCtlThreads, 3) root_filter_tma(FilterArgs a) 
                 }
             }
         };
+        uint32_t sn_prev = 0;  // this warp's survivors of the tile before
         for (uint32_t k = 0; k < nt; ++k) {
             const uint32_t t = blockIdx.x + k * G;
             const uint32_t tbase = t * uint32_t(kTile);
@@ -1628,30 +1633,36 @@ __global__ void __launch_bounds__(kCtlThreads, 3) root_filter_tma(FilterArgs a) 
             // phase A: strictly inside the inner box, or (a uniform choice,
             // when it adds coverage) inside the inner octagon or disk -> dropped
             uint32_t qn = 0;
-            auto phase_a = [&](auto inner) {
+            auto phase_a = [&](auto inner, auto with_box) {
 #pragma unroll
                 for (int i = 0; i < kItems; ++i) {
                     const uint32_t idx = uint32_t(i) * kThreads + tid;
                     const double u = ring.x[s][idx], w = ring.y[s][idx];
-                    const bool in = ((u > bx0) & (u < bx1) & (w > by0) & (w < by1)) | inner(u, w);
+                    const bool in = (decltype(with_box)::value && ((u > bx0) & (u < bx1) & (w > by0) & (w < by1))) |
+                                    inner(u, w);
                     const bool need = (tbase + idx < n) & !in;
                     const unsigned b = __ballot_sync(kFull, need);
                     if (need) s_q[warp][qn + __popc(b & lt)] = uint16_t(idx);
                     qn += __popc(b);
                 }
             };
-            if (mode >= 2u) {
+            if (mode == 3u) {  // the disk covers the box: one test
                 phase_a([&](double u, double w) {
                     const double du = u - P.dcx, dw = w - P.dcy;
                     return __fma_rn(du, du, __dmul_rn(dw, dw)) < P.dr2;
-                });
+                }, std::false_type{});
+            } else if (mode == 2u) {
+                phase_a([&](double u, double w) {
+                    const double du = u - P.dcx, dw = w - P.dcy;
+                    return __fma_rn(du, du, __dmul_rn(dw, dw)) < P.dr2;
+                }, std::true_type{});
             } else if (mode == 1u) {
                 phase_a([&](double u, double w) {
                     const double du = fabs(u - P.ocx), dw = fabs(w - P.ocy);
                     return (du < P.ohx) & (dw < P.ohy) & (du + dw < P.od);
-                });
+                }, std::true_type{});
             } else {
-                phase_a([](double, double) { return false; });
+                phase_a([](double, double) { return false; }, std::true_type{});
             }
             // phase C: the chord test for the rest, 32 at a time
             uint32_t sn = 0;
@@ -1691,9 +1702,10 @@ __global__ void __launch_bounds__(kCtlThreads, 3) root_filter_tma(FilterArgs a) 
             }
             if (lane == 0) s_cnt[par][warp] = sn;
             named_arrive<1>(par, kCtlThreads);
-            if (k >= 1) store_tile(k - 1);
+            if (k >= 1) store_tile(k - 1, sn_prev);
+            sn_prev = sn;
         }
-        if (nt >= 1) store_tile(nt - 1);
+        if (nt >= 1) store_tile(nt - 1, sn_prev);
     }
     // CTA partial -> the last CTA folds them and writes p, q and the slot
     uint32_t nb = bad;
@@ -2071,7 +2083,6 @@ __global__ void __launch_bounds__(kCtlThreads, 3) level_tma(LevelArgs a) {
     LevelRing& ring = *reinterpret_cast<LevelRing*>(dsm);
     __shared__ FastSmem S;
     __shared__ SegRec s_cur;
-    __shared__ uint32_t s_cur_k, s_cur_tiles;
     __shared__ uint32_t s_org[2][kWarps];
     __shared__ Best s_run[2];
     __shared__ bool s_last;
@@ -2108,8 +2119,6 @@ __global__ void __launch_bounds__(kCtlThreads, 3) level_tma(LevelArgs a) {
     };
     if (threadIdx.x == kThreads) {
         s_ntiles = a.info->ntiles;
-        s_cur_k = 0xffffffffu;
-        s_cur_tiles = 0;
         for (int s = 0; s < kRing; ++s) mbar_init(&ring.bar[s], 1);
         mbar_fence_init();
         for (uint32_t kk = 0; kk < kRing; ++kk) issue(kk);
@@ -2120,6 +2129,10 @@ __global__ void __launch_bounds__(kCtlThreads, 3) level_tma(LevelArgs a) {
     double bo[2] = {kInf, kInf};
     uint32_t bi[2] = {kNoIdx, kNoIdx};
 
+    // the current segment and the CTA's tile count in it: every thread keeps
+    // them (they follow the same tile sequence), so a new tile needs no
+    // snapshot barrier
+    uint32_t cur_k = 0xffffffffu, cur_tiles = 0;
     auto finalize = [&]() {
         // both classes' winners first, then their coordinates in one round
         // trip (they are random accesses to the input)
@@ -2143,14 +2156,14 @@ __global__ void __launch_bounds__(kCtlThreads, 3) level_tma(LevelArgs a) {
             s_run[1] = b1;
         }
         if (threadIdx.x == 0) {
-            const uint32_t k = s_cur_k;
+            const uint32_t k = cur_k;
             const uint32_t slot = atomicAdd(&a.seg_pcnt[k], 1u);
             VQB_CHECK(slot < s_cur.ntiles && 2 * (uint64_t(s_cur.tile0) + slot) + 1 < a.part_cap,
                       50, slot, s_cur.ntiles);
             a.tile_part[2 * (uint64_t(s_cur.tile0) + slot)] = s_run[0];
             a.tile_part[2 * (uint64_t(s_cur.tile0) + slot) + 1] = s_run[1];
             __threadfence();
-            const uint32_t done = atomicAdd(&a.seg_done[k], s_cur_tiles) + s_cur_tiles;
+            const uint32_t done = atomicAdd(&a.seg_done[k], cur_tiles) + cur_tiles;
             s_last = (done == s_cur.ntiles);
         }
         __syncthreads();
@@ -2158,7 +2171,7 @@ __global__ void __launch_bounds__(kCtlThreads, 3) level_tma(LevelArgs a) {
             __threadfence();
             if (warp < 2) {
                 const int c = warp;
-                const uint32_t np = __ldcg(&a.seg_pcnt[s_cur_k]);
+                const uint32_t np = __ldcg(&a.seg_pcnt[cur_k]);
                 Best b = best_none();
                 for (uint32_t jj = lane; jj < np; jj += 32) {
                     const Best o = ldcg_best(&a.tile_part[2 * (uint64_t(s_cur.tile0) + jj) + c]);
@@ -2168,7 +2181,7 @@ __global__ void __launch_bounds__(kCtlThreads, 3) level_tma(LevelArgs a) {
                 ChildRec ch;
                 if (lane == 0) {
                     const SegRec& g = s_cur;
-                    const uint2 w = read_pair(&a.seg_ctr[s_cur_k]);
+                    const uint2 w = read_pair(&a.seg_ctr[cur_k]);
                     const uint32_t m = c == 0 ? w.x : w.y;
                     if (c == 0) {  // left of p->r: triangle (p, rL, r)
                         ch.px = g.px; ch.py = g.py; ch.qx = g.rx; ch.qy = g.ry;
@@ -2182,10 +2195,10 @@ __global__ void __launch_bounds__(kCtlThreads, 3) level_tma(LevelArgs a) {
                     ch.ry = b.y;
                     ch.r_idx = b.idx;
                     ch.m = m;
-                    VQB_CHECK(2 * uint64_t(s_cur_k) + c < a.children_cap, 57, s_cur_k, a.children_cap);
-                    a.children[2 * uint64_t(s_cur_k) + c] = ch;
+                    VQB_CHECK(2 * uint64_t(cur_k) + c < a.children_cap, 57, cur_k, a.children_cap);
+                    a.children[2 * uint64_t(cur_k) + c] = ch;
                 }
-                if (a.n_kind) plan_child(a, 2 * uint64_t(s_cur_k) + c, ch);
+                if (a.n_kind) plan_child(a, 2 * uint64_t(cur_k) + c, ch);
             }
         }
         __syncthreads();
@@ -2224,16 +2237,13 @@ __global__ void __launch_bounds__(kCtlThreads, 3) level_tma(LevelArgs a) {
     const uint32_t t_end = min(ntiles, (blockIdx.x + 1) * chunk);
     for (uint32_t t = blockIdx.x * chunk; t < t_end; ++t, ++kk) {
         const int s = int(kk % kRing), par = int(kk & 1);
-        // entering a new segment?  all threads decide on one snapshot
-        const uint32_t k_now = ring.k[s], k_cur = s_cur_k;
-        __syncthreads();
-        if (k_now != k_cur) {
-            if (k_cur != 0xffffffffu) finalize();
-            if (threadIdx.x == 0) {
-                s_cur = ring.seg[s];
-                s_cur_k = k_now;
-                s_cur_tiles = 0;
-            }
+        // entering a new segment?  (ring.k[s] was written two barriers ago)
+        const uint32_t k_now = ring.k[s];
+        if (k_now != cur_k) {
+            if (cur_k != 0xffffffffu) finalize();
+            if (threadIdx.x == 0) s_cur = ring.seg[s];
+            cur_k = k_now;
+            cur_tiles = 0;
             __syncthreads();
         }
         if (!ctl) {
@@ -2293,10 +2303,10 @@ __global__ void __launch_bounds__(kCtlThreads, 3) level_tma(LevelArgs a) {
             fence_proxy_async_smem();
             issue(kk - 1 + kRing);  // refill tile kk-1's stage
         }
-        if (threadIdx.x == 0) ++s_cur_tiles;
+        ++cur_tiles;
     }
     if (kk >= 1 && !ctl) store_tile(kk - 1);
-    if (s_cur_k != 0xffffffffu) finalize();
+    if (cur_k != 0xffffffffu) finalize();
 }
 
 // ===========================================================================

@@ -335,7 +335,7 @@ def test_filter_inner_modes_agree(vq, cuda):
         a = gpu_indices(vq, xs, ys)
         s0 = vq.stats()
         assert s0["root_filtered"] == 2
-        for mode in ("box", "octagon", "disk"):
+        for mode in ("box", "octagon", "disk", "disk_only"):
             vq.set_filter_inner(mode)
             try:
                 b = gpu_indices(vq, xs, ys)
