@@ -1795,11 +1795,9 @@ __global__ void __launch_bounds__(kCtlThreads, 3) root_filter_tma(FilterArgs a) 
 constexpr uint32_t kSegCtaTiles = 4;
 
 struct SegCtaSmem {
-    uint32_t wc[2][kWarps];
-    uint32_t wex[2][kWarps];
-    uint32_t tot[2];
-    unsigned long long rkey[2][kWarps];
-    uint32_t ridx[2][kWarps];
+    uint32_t wc[2][2][kWarps];               // counts per (tile parity, class, warp)
+    unsigned long long rkey[2][2][kWarps];   // warp winners per (segment parity, class, warp)
+    uint32_t ridx[2][2][kWarps];
 };
 
 // ===========================================================================
@@ -1936,7 +1934,8 @@ __device__ __forceinline__ void level_segcta_tma(const LevelArgs& a, uint32_t ns
     }
     __syncthreads();
     uint32_t n = 0;  // CTA-local tile counter (every thread)
-    for (uint32_t k = blockIdx.x; k < nseg; k += G) {
+    int sp = 0;      // parity of the CTA-local segment counter
+    for (uint32_t k = blockIdx.x; k < nseg; k += G, sp ^= 1) {
         const SegRec g = a.segs[k];
         const double px = g.px, py = g.py, rx = g.rx, ry = g.ry, qx = g.qx, qy = g.qy;
         const double adx = g.adx, ady = g.ady, bdx = g.bdx, bdy = g.bdy;
@@ -1977,34 +1976,36 @@ __device__ __forceinline__ void level_segcta_tma(const LevelArgs& a, uint32_t ns
                     const unsigned long long key = key_of(lat_off(c == 0 ? adx : bdx, c == 0 ? ady : bdy, u, w));
                     running_best<2>(kb, ib, c, key, uid[i], a.gx, a.gy);
                 }
-                if (lane < 2) S.wc[lane][warp] = wrun;
+                if (lane < 2) S.wc[n & 1][lane][warp] = wrun;
             }
-            __syncthreads();  // A: counts posted; the stage's points are in registers
+            // The tile's only CTA barrier: counts posted; the stage's points
+            // are in registers.  Every warp then scans the 2 x 8 counts itself
+            // (the counts are double-buffered by tile parity: a warp is at
+            // most one tile ahead of another).
+            __syncthreads();
             if (ctl) {
                 if (lane == 0) {
                     fence_proxy_async_smem();
                     issue_next(n + kRing);  // refill this stage
                 }
-            } else if (warp == 0) {  // per-class exclusive scan over the warps
-                const int c = (lane >> 3) & 1, w8 = lane & 7;
-                const uint32_t v = lane < 16 ? S.wc[c][w8] : 0u;
+            } else {
+                const int c16 = (lane >> 3) & 1, w8 = lane & 7;
+                const uint32_t v = lane < 16 ? S.wc[n & 1][c16][w8] : 0u;
                 uint32_t incl = v;
 #pragma unroll
                 for (int d = 1; d < kWarps; d <<= 1) {
                     const uint32_t o = __shfl_up_sync(kFull, incl, d, kWarps);
                     if (w8 >= d) incl += o;
                 }
-                if (lane < 16) S.wex[c][w8] = incl - v;
-                if (lane == 7) S.tot[0] = incl;
-                if (lane == 15) S.tot[1] = incl;
-            }
-            __syncthreads();  // B: offsets ready
-            if (!ctl) {
+                const uint32_t ex0 = __shfl_sync(kFull, incl - v, warp);
+                const uint32_t ex1 = __shfl_sync(kFull, incl - v, kWarps + warp);
+                const uint32_t tot0 = __shfl_sync(kFull, incl, kWarps - 1);
+                const uint32_t tot1 = __shfl_sync(kFull, incl, 2 * kWarps - 1);
 #pragma unroll
                 for (int i = 0; i < kItems; ++i) {
                     const int c = cls[i];
                     if (c < 2) {
-                        const uint32_t off = (c ? run1 : run0) + S.wex[c][warp] + rk[i];
+                        const uint32_t off = (c ? run1 + ex1 : run0 + ex0) + rk[i];
                         const uint64_t pos = c ? g.out + g.m - 1u - off : g.out + off;
                         VQB_CHECK(pos < a.out_cap, 16, pos, a.out_cap);
                         a.ox[pos] = ux[i];
@@ -2012,30 +2013,32 @@ __device__ __forceinline__ void level_segcta_tma(const LevelArgs& a, uint32_t ns
                         a.oid[pos] = uid[i];
                     }
                 }
+                run0 += tot0;
+                run1 += tot1;
             }
-            run0 += S.tot[0];
-            run1 += S.tot[1];
         }
-        // the segment's two children (farthest point: block reduction)
+        // the segment's two children (farthest point: block reduction; the
+        // warp winners are double-buffered by segment parity, so the next
+        // segment starts without a second barrier)
         for (int c = 0; c < 2; ++c) {
             unsigned long long kk = kb[c];
             uint32_t ii = ib[c];
             if (!ctl) warp_key_best(kk, ii, a.gx, a.gy);
             if (lane == 0 && !ctl) {
-                S.rkey[c][warp] = kk;
-                S.ridx[c][warp] = ii;
+                S.rkey[sp][c][warp] = kk;
+                S.ridx[sp][c][warp] = ii;
             }
         }
-        __syncthreads();  // (also: every thread has read S.tot of the last tile)
+        __syncthreads();
         if (warp < 2) {
             const int c = warp;
             ChildRec ch;
             if (lane == 0) {
-                unsigned long long ko = S.rkey[c][0];
-                uint32_t io = S.ridx[c][0];
+                unsigned long long ko = S.rkey[sp][c][0];
+                uint32_t io = S.ridx[sp][c][0];
                 for (int w = 1; w < kWarps; ++w) {
-                    const unsigned long long kk = S.rkey[c][w];
-                    const uint32_t ii = S.ridx[c][w];
+                    const unsigned long long kk = S.rkey[sp][c][w];
+                    const uint32_t ii = S.ridx[sp][c][w];
                     if (kk < ko || (kk == ko && key_better(kk, ii, ko, io, a.gx, a.gy))) {
                         ko = kk;
                         io = ii;
@@ -2060,7 +2063,6 @@ __device__ __forceinline__ void level_segcta_tma(const LevelArgs& a, uint32_t ns
             }
             if (a.n_kind) plan_child(a, 2 * uint64_t(k) + c, ch);
         }
-        __syncthreads();  // S reused by the next segment
     }
 }
 
