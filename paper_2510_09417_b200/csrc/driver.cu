@@ -402,7 +402,18 @@ class Engine {
             }
             tk(5, st, [&] { launch_emit_small(E, root_, chain_.as<uint32_t>(), d_out, hword_, st); });
         } else {
-        for (int l = lmax_; l >= 2; --l) {
+        // a large tree: its top levels (few slots each, many launches
+        // otherwise) in the one-CTA kernel, the levels below one launch each
+        int ltop = 1;  // last level done by the one-CTA kernel
+        {
+            uint64_t acc = 0;
+            while (ltop + 1 < lmax_ && ltop - 1 < kEmitMaxLevels && acc + hinfo_[ltop + 1].nslots <= kEmitTopSlots) {
+                acc += hinfo_[ltop + 1].nslots;
+                ++ltop;
+            }
+            if (ltop < 4) ltop = 1;  // not worth a launch of its own
+        }
+        for (int l = lmax_; l > ltop && l >= 2; --l) {
             LevelTables& T = level(l);
             const uint32_t ns = hinfo_[l].nslots;
             const uint32_t* child_size = (l < lmax_) ? level(l + 1).size.as<uint32_t>() : nullptr;
@@ -411,11 +422,28 @@ class Engine {
                             child_size, T.size.as<uint32_t>(), st);
             });
         }
-        tk(5, st, [&] {
-            launch_poly_frame(root_, level(2).size.as<uint32_t>(), level(2).start.as<uint32_t>(), d_out,
-                              hword_, st);
-        });
-        for (int l = 2; l <= lmax_; ++l) {
+        if (ltop >= 2) {
+            EmitAll E;
+            std::memset(&E, 0, sizeof E);
+            E.nlev = ltop - 1;
+            for (int l = 2; l <= ltop; ++l) {
+                LevelTables& T = level(l);
+                EmitLevel& el = E.lv[l - 2];
+                el.kind = T.kind.as<uint8_t>(); el.link = T.link.as<uint32_t>(); el.slots = T.slots.as<ChildRec>();
+                el.fins = T.fins.as<FinRec>(); el.fin_count = T.fin_count.as<uint32_t>();
+                el.size = T.size.as<uint32_t>(); el.start = T.start.as<uint32_t>();
+                el.nslots = hinfo_[l].nslots;
+            }
+            E.below_size = level(ltop + 1).size.as<uint32_t>();
+            E.below_start = level(ltop + 1).start.as<uint32_t>();
+            tk(5, st, [&] { launch_emit_small(E, root_, chain_.as<uint32_t>(), d_out, hword_, st); });
+        } else {
+            tk(5, st, [&] {
+                launch_poly_frame(root_, level(2).size.as<uint32_t>(), level(2).start.as<uint32_t>(), d_out,
+                                  hword_, st);
+            });
+        }
+        for (int l = std::max(2, ltop + 1); l <= lmax_; ++l) {
             LevelTables& T = level(l);
             const uint32_t ns = hinfo_[l].nslots;
             const bool has_child = l < lmax_;
@@ -1442,6 +1470,7 @@ class Engine {
     int lmax_ = 2;
     static constexpr int kLevelBatch = 8;  // levels queued per host synchronization (4: disk 1e8 +2 %, 16: +6 %)
     static constexpr uint64_t kLeanN = 1ull << 29;
+    static constexpr uint64_t kEmitTopSlots = 2048;  // a large tree's top levels done by the one-CTA emission kernel
     static constexpr uint64_t kEmitSmallSlots = 1u << 14;  // trees this small: one emission kernel  // above: exact per-level sizing (one sync per level)
     uint32_t epoch_ = 0;
     uint32_t launches_ = 0;

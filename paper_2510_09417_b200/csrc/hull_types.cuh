@@ -323,6 +323,10 @@ struct EmitLevel {
 struct EmitAll {
     EmitLevel lv[kEmitMaxLevels];
     int nlev;
+    // the level below the last one listed, emitted by its own launches
+    // (nullptr: the listed levels are the whole tree)
+    const uint32_t* below_size;
+    uint32_t* below_start;
 };
 
 // Look-back payload of the planner scan.

@@ -1538,13 +1538,16 @@ __global__ void emit_kernel(uint32_t nslots, const uint8_t* kind, const uint32_t
 // Whole emission of a small tree (few slots) in ONE CTA: bottom-up sizes,
 // the root frame, top-down starts and writes — the same steps as
 // size_kernel / poly_frame_kernel / emit_kernel, without one launch each.
+// For a large tree the same kernel does its top levels (the many levels of
+// few slots each), between the size launches and the emit launches of the
+// levels below (E.below_size / E.below_start).
 __global__ void __launch_bounds__(1024) emit_small_kernel(EmitAll E, const RootInfo* root, const uint32_t* chain,
                                                           uint32_t* out, uint32_t* h_out) {
     VQB_PDL();
     const int lane = threadIdx.x & 31;
     for (int l = E.nlev - 1; l >= 0; --l) {
         const EmitLevel& L = E.lv[l];
-        const uint32_t* child_size = l + 1 < E.nlev ? E.lv[l + 1].size : nullptr;
+        const uint32_t* child_size = l + 1 < E.nlev ? E.lv[l + 1].size : E.below_size;
         for (uint32_t s = threadIdx.x; s < L.nslots; s += blockDim.x) {
             const uint8_t k = L.kind[s];
             uint32_t v = 0;
@@ -1571,7 +1574,9 @@ __global__ void __launch_bounds__(1024) emit_small_kernel(EmitAll E, const RootI
     const uint32_t wpb = blockDim.x >> 5;
     for (int l = 0; l < E.nlev; ++l) {
         const EmitLevel& L = E.lv[l];
-        const bool has_child = l + 1 < E.nlev;
+        const uint32_t* csize = l + 1 < E.nlev ? E.lv[l + 1].size : E.below_size;
+        uint32_t* cstart = l + 1 < E.nlev ? E.lv[l + 1].start : E.below_start;
+        const bool has_child = cstart != nullptr;
         for (uint32_t s = threadIdx.x >> 5; s < L.nslots; s += wpb) {  // one warp per slot
             const uint8_t k = L.kind[s];
             const uint32_t st = L.start[s];
@@ -1580,10 +1585,10 @@ __global__ void __launch_bounds__(1024) emit_small_kernel(EmitAll E, const RootI
             } else if (k == kInternal && has_child) {
                 if (lane == 0) {
                     const uint32_t c = L.link[s];
-                    const uint32_t sl = E.lv[l + 1].size[2 * c];
+                    const uint32_t sl = csize[2 * c];
                     out[st + sl] = L.slots[s].r_idx;
-                    E.lv[l + 1].start[2 * c] = st;
-                    E.lv[l + 1].start[2 * c + 1] = st + sl + 1;
+                    cstart[2 * c] = st;
+                    cstart[2 * c + 1] = st + sl + 1;
                 }
             } else if (k == kFin) {
                 const uint32_t f = L.link[s];
