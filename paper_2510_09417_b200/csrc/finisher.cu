@@ -61,11 +61,15 @@ struct FbSmem {
         } t;                                    // (emission)
     } u;
     uint32_t apex[2 * kFbSlots];                // per child: its apex slot (kFbNone: empty child)
+    uint16_t vlist[kFbCap];                     // the vertices in the order they retired (by depth)
+    uint16_t dstart[kFbCap + 2];                // first vlist entry of each depth
+    uint8_t sseg[kFbCap];                       // per point slot: its segment in the batch
     uint32_t seg_off[kFbSegs + 1];              // first point slot of each segment
     uint32_t seg_fi[kFbSegs];                   // its FinRec
     uint32_t seg_begin[kFbSegs];                // its first point in the level's buffer
     uint64_t seg_chain[kFbSegs];                // where its chain goes
     uint32_t nb;                                // segments in this batch
+    uint32_t nv;                                // vertices so far
 };
 
 // exact key tie: a strictly preferred over b
@@ -87,6 +91,7 @@ __device__ __forceinline__ void fb_run_list(FbSmem& S, const FinRec* fins, int64
                                             const uint32_t* __restrict__ iid, uint32_t* chain,
                                             uint32_t* fin_count) {
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const unsigned lt = lanemask_lt();
     uint32_t f = uint32_t(uint64_t(count) * blockIdx.x / gridDim.x);
     const uint32_t f_end = uint32_t(uint64_t(count) * (blockIdx.x + 1) / gridDim.x);
     while (f < f_end) {
@@ -118,6 +123,7 @@ __device__ __forceinline__ void fb_run_list(FbSmem& S, const FinRec* fins, int64
                 if (lane == int(nb) - 1) {
                     S.seg_off[nb] = incl;
                     S.nb = nb;
+                    S.nv = 0;
                 }
             }
         }
@@ -133,12 +139,10 @@ __device__ __forceinline__ void fb_run_list(FbSmem& S, const FinRec* fins, int64
         double u[kFbItems], w[kFbItems], px[kFbItems], py[kFbItems], qx[kFbItems], qy[kFbItems];
         unsigned long long key[kFbItems];
         uint32_t node[kFbItems];   // live: its node (the apex's slot), then its child; kFbNone: retired
-        uint32_t meta[kFbItems];   // segment << 16 | depth at which it became a vertex (0xffff: not one)
 #pragma unroll
         for (int k = 0; k < kFbItems; ++k) {
             const uint32_t i = uint32_t(k) * kFbThreads + tid;
             node[k] = kFbNone;
-            meta[k] = 0xffffu;
             u[k] = w[k] = px[k] = py[k] = qx[k] = qy[k] = 0.0;
             if (i < total) {
                 uint32_t lo = 0, hi = nb;  // segment: seg_off[lo] <= i < seg_off[lo + 1]
@@ -155,7 +159,7 @@ __device__ __forceinline__ void fb_run_list(FbSmem& S, const FinRec* fins, int64
                 const double2 P = S.xy[b], Q = S.xy[b + 1];
                 px[k] = P.x; py[k] = P.y; qx[k] = Q.x; qy[k] = Q.y;
                 node[k] = uint32_t(b + 2);
-                meta[k] = (lo << 16) | 0xffffu;
+                S.sseg[i] = uint8_t(lo);
             }
         }
         __syncthreads();
@@ -204,7 +208,11 @@ __device__ __forceinline__ void fb_run_list(FbSmem& S, const FinRec* fins, int64
                     if (key[k] < S.u.ckey[c]) atomicMin(&S.u.ckey[c], key[k]);
                 }
             }
-            if (!__syncthreads_or(any)) break;
+            const bool go = __syncthreads_or(any);
+            // every warp has appended the vertices of the depths before this
+            // one, and none appends before the next barrier
+            if (tid == 0) S.dstart[depth] = uint16_t(S.nv);
+            if (!go) break;
             // (2) the holders of the minimal key: the child's apex
 #pragma unroll
             for (int k = 0; k < kFbItems; ++k) {
@@ -221,30 +229,44 @@ __device__ __forceinline__ void fb_run_list(FbSmem& S, const FinRec* fins, int64
             __syncthreads();
             // (3) next node, or retire as this depth's vertex
 #pragma unroll
+            unsigned retired[kFbItems];
+            uint32_t nret = 0;
+#pragma unroll
             for (int k = 0; k < kFbItems; ++k) {
                 const uint32_t c = node[k];
-                if (c == kFbNone) continue;
-                const uint32_t a = S.apex[c];
-                if (a == uint32_t(k) * kFbThreads + tid) {
-                    node[k] = kFbNone;
-                    meta[k] = (meta[k] & 0xffff0000u) | (depth < 0xffffu ? depth : 0xfffeu);
-                } else {
-                    node[k] = a;
+                bool ret = false;
+                if (c != kFbNone) {
+                    const uint32_t a = S.apex[c];
+                    ret = a == uint32_t(k) * kFbThreads + tid;
+                    node[k] = ret ? kFbNone : a;
+                }
+                retired[k] = __ballot_sync(kFull, ret);
+                nret += uint32_t(__popc(retired[k]));
+            }
+            if (nret) {  // (warp-uniform) this warp's new vertices join the list of their depth
+                uint32_t base = 0;
+                if (lane == 0) base = atomicAdd(&S.nv, nret);
+                base = __shfl_sync(kFull, base, 0);
+#pragma unroll
+                for (int k = 0; k < kFbItems; ++k) {
+                    if (retired[k] & (1u << lane))
+                        S.vlist[base + uint32_t(__popc(retired[k] & lt))] = uint16_t(uint32_t(k) * kFbThreads + tid);
+                    base += uint32_t(__popc(retired[k]));
                 }
             }
             ++depth;
-            if (depth >= 0xfffeu) {  // cannot happen: every depth retires >= 1 point of <= kFbCap
+            if (depth > uint32_t(kFbCap)) {  // cannot happen: every depth retires >= 1 point of <= kFbCap
                 if (tid == 0) g_vqb_fault = 5u;
                 break;
             }
         }
-        // ---- emission: sizes bottom-up (ckey is dead: every thread is past its last (2))
+        // ---- emission (ckey is dead: every thread is past its last (2)).
+        // Sizes bottom-up, then positions top-down, over each depth's vertices.
+        __syncthreads();
         for (int d = int(depth) - 1; d >= 0; --d) {
-#pragma unroll
-            for (int k = 0; k < kFbItems; ++k) {
-                if ((meta[k] & 0xffffu) != uint32_t(d)) continue;
-                const uint32_t me = uint32_t(k) * kFbThreads + tid;
-                S.u.t.tsize[me] = uint16_t(fb_size(S, S.apex[2 * me]) + 1u + fb_size(S, S.apex[2 * me + 1]));
+            for (uint32_t i = S.dstart[d] + tid; i < S.dstart[d + 1]; i += kFbThreads) {
+                const uint32_t v = S.vlist[i];
+                S.u.t.tsize[v] = uint16_t(fb_size(S, S.apex[2 * v]) + 1u + fb_size(S, S.apex[2 * v + 1]));
             }
             __syncthreads();
         }
@@ -259,14 +281,12 @@ __device__ __forceinline__ void fb_run_list(FbSmem& S, const FinRec* fins, int64
         }
         __syncthreads();
         for (uint32_t d = 0; d < depth; ++d) {
-#pragma unroll
-            for (int k = 0; k < kFbItems; ++k) {
-                if ((meta[k] & 0xffffu) != d) continue;
-                const uint32_t me = uint32_t(k) * kFbThreads + tid;
-                const uint32_t L = S.apex[2 * me], R = S.apex[2 * me + 1];
-                const uint32_t s0 = S.u.t.tstart[me];
+            for (uint32_t i = S.dstart[d] + tid; i < S.dstart[d + 1]; i += kFbThreads) {
+                const uint32_t v = S.vlist[i];
+                const uint32_t L = S.apex[2 * v], R = S.apex[2 * v + 1];
+                const uint32_t s0 = S.u.t.tstart[v];
                 const uint32_t pos = s0 + fb_size(S, L);
-                chain[S.seg_chain[meta[k] >> 16] + pos] = S.gid[me];
+                chain[S.seg_chain[S.sseg[v]] + pos] = S.gid[v];
                 if (L != kFbNone) S.u.t.tstart[L] = uint16_t(s0);
                 if (R != kFbNone) S.u.t.tstart[R] = uint16_t(pos + 1);
             }
