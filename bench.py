@@ -468,7 +468,7 @@ def run_ours(args) -> int:
         pass
     kname = {"root_partition": ("root_filter_tma (split root pass 1: polygon filter over every point)"
                                 if st.get("root_filtered") == 2 else "root pass"),
-             "levels": "tail_kernel / level kernels (recursion)",
+             "levels": "cluster_tail_kernel / tail_kernel / level kernels (recursion)",
              "extremes": "poly_sample_kernel" if st.get("root_filtered") == 2 else "extremes"}.get(dom, dom)
     result["roofline"] = {
         "bound": "hbm", "kernel": kname, "family": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",

@@ -20,6 +20,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <deque>
+#include <initializer_list>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -561,15 +562,105 @@ class Engine {
         return VQHULL_OK;
     }
 
+    // Host -> device copy of caller arrays.  Page-locked (or registered)
+    // memory goes to the copy engine as it is.  Pageable memory — what a
+    // drop-in C caller of vqhull_compute passes — would be staged by the
+    // driver through its own small pinned buffer at ~11 GB/s; here worker
+    // threads copy 8 MB chunks into a ring of pinned buffers, each chunk
+    // followed by its asynchronous H2D copy, so the host memcpy of one chunk
+    // overlaps the PCIe transfer of the others (the copies stay ordered
+    // before the hull on the stream).
+    struct HostPart {
+        void* dst;
+        const void* src;
+        size_t bytes;
+    };
+    static bool pageable(const void* p) {
+        cudaPointerAttributes at{};
+        if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+            (void)cudaGetLastError();
+            return true;
+        }
+        return at.type == cudaMemoryTypeUnregistered;
+    }
+    void h2d(std::initializer_list<HostPart> parts, cudaStream_t st) {
+        static const bool staging = !(getenv("VQHULL_STAGING") && getenv("VQHULL_STAGING")[0] == '0');
+        size_t total = 0;
+        bool paged = false;
+        for (const HostPart& q : parts) {
+            total += q.bytes;
+            paged |= q.bytes && pageable(q.src);
+        }
+        if (!staging || !paged || total < (size_t(64) << 20)) {
+            for (const HostPart& q : parts)
+                if (q.bytes) ck(cudaMemcpyAsync(q.dst, q.src, q.bytes, cudaMemcpyHostToDevice, st), "h2d");
+            return;
+        }
+        constexpr size_t kChunk = size_t(8) << 20;
+        constexpr int kBufsPerThread = 3;
+        const int nthr = int(std::max(1u, std::min(8u, std::thread::hardware_concurrency() / 2)));
+        const size_t need = size_t(nthr) * kBufsPerThread * kChunk;
+        if (stage_bytes_ < need) {
+            if (stage_) cudaFreeHost(stage_);
+            stage_ = nullptr;
+            stage_bytes_ = 0;
+            ck(cudaHostAlloc(&stage_, need, cudaHostAllocDefault), "cudaHostAlloc staging");
+            stage_bytes_ = need;
+        }
+        struct Chunk {
+            char* dst;
+            const char* src;
+            size_t bytes;
+        };
+        std::vector<Chunk> chunks;
+        for (const HostPart& q : parts)
+            for (size_t o = 0; o < q.bytes; o += kChunk)
+                chunks.push_back({static_cast<char*>(q.dst) + o, static_cast<const char*>(q.src) + o,
+                                  std::min(kChunk, q.bytes - o)});
+        std::atomic<size_t> next{0};
+        std::atomic<int> failed{0};
+        auto work = [&](int t) {
+            if (cudaSetDevice(dev_) != cudaSuccess) { failed = 1; return; }
+            cudaEvent_t ev[kBufsPerThread];
+            bool used[kBufsPerThread] = {};
+            for (cudaEvent_t& e : ev)
+                if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) { failed = 1; return; }
+            char* base = static_cast<char*>(stage_) + size_t(t) * kBufsPerThread * kChunk;
+            for (int b = 0; !failed; b = (b + 1) % kBufsPerThread) {
+                const size_t i = next.fetch_add(1);
+                if (i >= chunks.size()) break;
+                if (used[b] && cudaEventSynchronize(ev[b]) != cudaSuccess) { failed = 1; break; }
+                char* buf = base + size_t(b) * kChunk;
+                std::memcpy(buf, chunks[i].src, chunks[i].bytes);
+                if (cudaMemcpyAsync(chunks[i].dst, buf, chunks[i].bytes, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+                    cudaEventRecord(ev[b], st) != cudaSuccess) { failed = 1; break; }
+                used[b] = true;
+            }
+            for (int b = 0; b < kBufsPerThread; ++b) {
+                if (used[b]) cudaEventSynchronize(ev[b]);  // the buffer is reused by the next call
+                cudaEventDestroy(ev[b]);
+            }
+        };
+        std::vector<std::thread> pool;
+        for (int t = 1; t < nthr; ++t) pool.emplace_back(work, t);
+        work(0);
+        for (std::thread& th : pool) th.join();
+        if (failed) {
+            (void)cudaGetLastError();
+            g_last_error = "staged host-to-device copy failed";
+            throw CudaError{cudaErrorUnknown};
+        }
+    }
+
     // host-input path (vqhull_compute)
     int compute_host(const double* xs, const double* ys, uint64_t n, uint32_t* h_out_u32, uint64_t* h,
                      cudaStream_t st) {
         VQB_TRACE("compute_host: n=%llu", (unsigned long long)n);
         if (n >= 0xffffffffull) return VQHULL_ESIZE;  // before any allocation or copy
+        if (st == nullptr) st = own_stream();
         in_.x.ensure(n * 8, st);
         in_.y.ensure(n * 8, st);
-        ck(cudaMemcpyAsync(in_.x.p, xs, n * 8, cudaMemcpyHostToDevice, st), "h2d x");
-        ck(cudaMemcpyAsync(in_.y.p, ys, n * 8, cudaMemcpyHostToDevice, st), "h2d y");
+        h2d({{in_.x.p, xs, size_t(n) * 8}, {in_.y.p, ys, size_t(n) * 8}}, st);
         out_.ensure(n * 4, st);
         const int rc = hull(in_.x.as<double>(), in_.y.as<double>(), n, out_.as<uint32_t>(), h, st);
         if (rc) return rc;
@@ -767,8 +858,7 @@ class Engine {
     void load_host(const double* xs, const double* ys, uint64_t n, cudaStream_t st) {
         in_.x.ensure(n * 8, st);
         in_.y.ensure(n * 8, st);
-        ck(cudaMemcpyAsync(in_.x.p, xs, n * 8, cudaMemcpyHostToDevice, st), "h2d x");
-        ck(cudaMemcpyAsync(in_.y.p, ys, n * 8, cudaMemcpyHostToDevice, st), "h2d y");
+        h2d({{in_.x.p, xs, size_t(n) * 8}, {in_.y.p, ys, size_t(n) * 8}}, st);
     }
     const double* in_x() const { return in_.x.as<double>(); }
     const double* in_y() const { return in_.y.as<double>(); }
@@ -797,6 +887,9 @@ class Engine {
                 cudaGraphExecDestroy(e.exec);
                 e.exec = nullptr;
             }
+        if (stage_) cudaFreeHost(stage_);
+        stage_ = nullptr;
+        stage_bytes_ = 0;
         cudaMemPool_t pool;
         if (cudaDeviceGetDefaultMemPool(&pool, dev_) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
         ck(cudaDeviceSynchronize(), "trim sync");
@@ -1327,6 +1420,8 @@ class Engine {
 
    private:
     int dev_ = 0;
+    void* stage_ = nullptr;     // pinned staging ring of h2d()
+    size_t stage_bytes_ = 0;
     int sms_ = 148;
     int occ_root_ = 1, occ_root_stable_ = 1, occ_level_ = 1, occ_level_stable_ = 1, occ_fin_ = 1, occ_fb_ = 1;
     // VQHULL_FIN_OLD=1: the one-segment-per-CTA finisher (A/B runs)

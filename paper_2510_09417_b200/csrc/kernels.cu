@@ -539,16 +539,28 @@ __device__ __noinline__ void poly_finish_warp(const PolyPartial& F, const double
         P.fa[j] = fa; P.fb[j] = fb; P.fc[j] = fc; P.ft[j] = ft;
         P.fg[j] = ft - fc;
     }
-    // how much of the box lies outside the disk (64 midpoint samples, two per lane)
-    uint32_t box_out = 0;
+    // the inner test that adds the most area (a uniform choice per call);
+    // when the disk wins and the box adds next to nothing to it (< 1 % of the
+    // disk's area lies in the box but outside the disk: 64 midpoint samples,
+    // two per lane), the disk is tested alone (3)
+    uint32_t inner_mode;
     {
+        const double box_area = bx0 < bx1 ? (bx1 - bx0) * (by1 - by0) : 0.0;
+        const double cut = fmax(0.0, ohx + ohy - od);
+        const double oct_area = ohx > 0.0 ? 4.0 * ohx * ohy - 2.0 * cut * cut : 0.0;
+        const double disk_area = dr2 > 0.0 ? 3.14159 * dr2 : 0.0;
+        inner_mode = disk_area > 1.02 * fmax(oct_area, box_area) ? 2u : (oct_area > 1.02 * box_area ? 1u : 0u);
+        if (inner_mode == 2u) {  // (warp-uniform)
+            uint32_t box_out = 0;
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int sidx = lane + 32 * h;
-            const double sx = bx0 + (bx1 - bx0) * (0.0625 + 0.125 * double(sidx & 7));
-            const double sy = by0 + (by1 - by0) * (0.0625 + 0.125 * double(sidx >> 3));
-            const bool out = bx0 < bx1 && dr2 > 0.0 && (sx - dcx) * (sx - dcx) + (sy - dcy) * (sy - dcy) >= dr2;
-            box_out += uint32_t(__popc(__ballot_sync(kFull, out)));
+            for (int h = 0; h < 2; ++h) {
+                const int sidx = lane + 32 * h;
+                const double sx = bx0 + (bx1 - bx0) * (0.0625 + 0.125 * double(sidx & 7));
+                const double sy = by0 + (by1 - by0) * (0.0625 + 0.125 * double(sidx >> 3));
+                const bool out = bx0 < bx1 && (sx - dcx) * (sx - dcx) + (sy - dcy) * (sy - dcy) >= dr2;
+                box_out += uint32_t(__popc(__ballot_sync(kFull, out)));
+            }
+            if (double(box_out) * (1.0 / 64.0) * box_area < 0.01 * disk_area) inner_mode = 3u;
         }
     }
     if (lane != 0) return;
@@ -557,17 +569,7 @@ __device__ __noinline__ void poly_finish_warp(const PolyPartial& F, const double
     P.ocx = ocx; P.ocy = ocy; P.ohx = ohx; P.ohy = ohy; P.od = od;
     P.dcx = dcx; P.dcy = dcy; P.dr2 = dr2;
     {
-        const double box_area = bx0 < bx1 ? (bx1 - bx0) * (by1 - by0) : 0.0;
-        const double cut = fmax(0.0, ohx + ohy - od);
-        const double oct_area = ohx > 0.0 ? 4.0 * ohx * ohy - 2.0 * cut * cut : 0.0;
-        const double disk_area = dr2 > 0.0 ? 3.14159 * dr2 : 0.0;
-        // the inner test that adds the most area (a uniform choice per call)
-        P.oct_on = disk_area > 1.02 * fmax(oct_area, box_area) ? 2u : (oct_area > 1.02 * box_area ? 1u : 0u);
-        if (P.oct_on == 2u) {
-            // the box adds next to nothing (< 1 % of the disk's area lies in
-            // the box but outside the disk): test the disk alone (3)
-            if (double(box_out) * (1.0 / 64.0) * box_area < 0.01 * disk_area) P.oct_on = 3u;
-        }
+        P.oct_on = inner_mode;
         const int f = g_inner_force;  // test knob: a forced choice, when that region exists
         if (f == 0 || (f == 1 && ohx > 0.0) || (f >= 2 && f <= 3 && dr2 > 0.0)) P.oct_on = uint32_t(f);
         P.pad2 = 0u;

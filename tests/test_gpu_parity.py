@@ -515,3 +515,24 @@ def test_sharded_hull_nccl_world1(vq, cuda, oracle):
             assert np.array_equal(got, oracle.hull_indices(xs, ys)), kind
     finally:
         dist.destroy_process_group()
+
+
+def test_vqhull_compute_pageable_staged_copy(vq, cuda, oracle):
+    """vqhull_compute on pageable host arrays large enough for the staged
+    copy (worker threads -> pinned ring -> async H2D, driver.cu h2d()): the
+    same list as from page-locked arrays and as the oracle's; odd sizes so
+    the last chunk of each array is partial."""
+    import torch
+
+    n = 9_000_001
+    xs, ys = vq.generate("disk", n, 9)
+    ref = oracle.hull_indices(xs, ys)
+    rc, got = vq.vqhull_compute(xs, ys)  # pageable numpy arrays
+    assert rc == 0 and np.array_equal(got, ref)
+    X = torch.from_numpy(xs).pin_memory()
+    Y = torch.from_numpy(ys).pin_memory()
+    rc, got2 = vq.vqhull_compute(X.numpy(), Y.numpy())
+    assert rc == 0 and np.array_equal(got2, ref)
+    # one pageable, one page-locked
+    rc, got3 = vq.vqhull_compute(xs, Y.numpy())
+    assert rc == 0 and np.array_equal(got3, ref)
