@@ -202,3 +202,25 @@ def test_bench_workload_strings_match_between_arms():
     assert sum(c for _, c in offs) == 4 * 10**9 and offs[1][0] == 5 * 10**8
     # the reference arm prints the same config object for the same flags
     assert b.Workload(a8, 8).config() == w8.config()
+
+
+def test_reference_arm_never_loads_the_product_library(reference):
+    """`bench.py --impl reference` times the reference library only: it runs
+    with the product library made unloadable (VQHULL_LIB pointing nowhere) and
+    no GPU visible, and prints the driver's line for the reference arm."""
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, VQHULL_LIB="/nonexistent/libvqhull_b200.so", CUDA_VISIBLE_DEVICES="")
+    env.pop("WORLD_SIZE", None)
+    p = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference", "--config", "1",
+                        "--points", "200000", "--steps", "2", "--warmup", "1"],
+                       capture_output=True, text=True, env=env, timeout=600, cwd=root)
+    assert p.returncode == 0, p.stderr[-2000:]
+    d = json.loads([l for l in p.stdout.splitlines() if l.startswith("{")][-1])
+    assert d["impl"] == "reference" and d["unit"] == "points/s" and d["value"] > 0
+    assert d["cpu_baseline"]["kind"] == "reference" and d["cpu_baseline"]["cores"] >= 1
+    assert d["e2e"]["value"] == d["value"] and d["e2e"]["h2d_bytes_per_step"] == 0
+    assert d["config"]["workload"].startswith("config1: disk seed=1, n=200000")
