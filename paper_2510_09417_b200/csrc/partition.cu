@@ -2071,15 +2071,23 @@ __global__ void __launch_bounds__(kCtlThreads, 3) level_tma(LevelArgs a) {
     VQB_PDL();
     plan_level_start(a);
     {
-        // many small segments (at most kSegCtaTiles tiles on average): one
-        // CTA per segment, no cross-CTA claims or partials (uniform branch)
+        // (-DVQB_SEGCTA) many small segments (at most kSegCtaTiles tiles on
+        // average): one CTA per segment, no cross-CTA claims or partials
+        // (uniform branch).  Off by default since the wide path lost its third
+        // barrier per tile: compiled into the same kernel the second path costs
+        // the first one its registers (168 B of spills), and alone the wide path
+        // is faster on every input measured (profiles/r02_ncu_summary.md).
         const uint32_t nseg = a.info->nseg, nt = a.info->ntiles;
+#ifdef VQB_SEGCTA
         if (nseg >= gridDim.x && nt <= kSegCtaTiles * nseg) {
             __shared__ SegCtaSmem SC;
             extern __shared__ __align__(128) unsigned char dsm_sc[];
             level_segcta_tma<GENERAL>(a, nseg, *reinterpret_cast<LevelRing*>(dsm_sc), SC);
             return;
         }
+#else
+        (void)nseg; (void)nt;
+#endif
     }
     extern __shared__ __align__(128) unsigned char dsm[];
     LevelRing& ring = *reinterpret_cast<LevelRing*>(dsm);
