@@ -2165,7 +2165,11 @@ __global__ void __launch_bounds__(kCtlThreads, 3) level_tma(LevelArgs a) {
             s_run[0] = b0;
             s_run[1] = b1;
         }
-        if (threadIdx.x == 0) {
+        // A segment whose tiles were all this CTA's (the rule on deep levels:
+        // a CTA's tiles are a contiguous chunk) needs no partials: the CTA's
+        // own winners are the segment's, its own claims the final counts.
+        const bool own = cur_tiles == s_cur.ntiles;  // (uniform)
+        if (threadIdx.x == 0 && !own) {
             const uint32_t k = cur_k;
             const uint32_t slot = atomicAdd(&a.seg_pcnt[k], 1u);
             VQB_CHECK(slot < s_cur.ntiles && 2 * (uint64_t(s_cur.tile0) + slot) + 1 < a.part_cap,
@@ -2177,17 +2181,21 @@ __global__ void __launch_bounds__(kCtlThreads, 3) level_tma(LevelArgs a) {
             s_last = (done == s_cur.ntiles);
         }
         __syncthreads();
-        if (s_last) {
-            __threadfence();
+        if (own || s_last) {
+            if (!own) __threadfence();
             if (warp < 2) {
                 const int c = warp;
-                const uint32_t np = __ldcg(&a.seg_pcnt[cur_k]);
                 Best b = best_none();
-                for (uint32_t jj = lane; jj < np; jj += 32) {
-                    const Best o = ldcg_best(&a.tile_part[2 * (uint64_t(s_cur.tile0) + jj) + c]);
-                    if (prefer(o, b)) b = o;
+                if (own) {
+                    b = s_run[c];
+                } else {
+                    const uint32_t np = __ldcg(&a.seg_pcnt[cur_k]);
+                    for (uint32_t jj = lane; jj < np; jj += 32) {
+                        const Best o = ldcg_best(&a.tile_part[2 * (uint64_t(s_cur.tile0) + jj) + c]);
+                        if (prefer(o, b)) b = o;
+                    }
+                    b = warp_best(b);
                 }
-                b = warp_best(b);
                 ChildRec ch;
                 if (lane == 0) {
                     const SegRec& g = s_cur;
