@@ -2146,11 +2146,35 @@ __global__ void __launch_bounds__(kCtlThreads, 3) level_tma(LevelArgs a) {
     auto finalize = [&]() {
         // both classes' winners first, then their coordinates in one round
         // trip (they are random accesses to the input)
-        double oo;
-        uint32_t io0, io1;
-        block_best_d<2>(S, 0, bo[0], bi[0], a.gx, a.gy, oo, io0);
-        block_best_d<2>(S, 1, bo[1], bi[1], a.gx, a.gy, oo, io1);
+        // (both classes through one barrier: block_best_d twice was four)
+        {
+            unsigned long long k0 = bi[0] == kNoIdx ? kNoKey : key_of(bo[0]);
+            unsigned long long k1 = bi[1] == kNoIdx ? kNoKey : key_of(bo[1]);
+            uint32_t i0 = bi[0], i1 = bi[1];
+            warp_key_best(k0, i0, a.gx, a.gy);
+            warp_key_best(k1, i1, a.gx, a.gy);
+            if (lane == 0 && warp < kWarps) {  // (the control warp holds no points)
+                S.rkey[0][warp] = k0; S.ridx[0][warp] = i0;
+                S.rkey[1][warp] = k1; S.ridx[1][warp] = i1;
+            }
+        }
+        __syncthreads();
         if (threadIdx.x == 0) {
+            uint32_t io[2];
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                unsigned long long ko = S.rkey[c][0];
+                io[c] = S.ridx[c][0];
+                for (int w = 1; w < kWarps; ++w) {
+                    const unsigned long long kk2 = S.rkey[c][w];
+                    const uint32_t ii = S.ridx[c][w];
+                    if (kk2 < ko || (kk2 == ko && key_better(kk2, ii, ko, io[c], a.gx, a.gy))) {
+                        ko = kk2;
+                        io[c] = ii;
+                    }
+                }
+            }
+            const uint32_t io0 = io[0], io1 = io[1];
             const double x0 = io0 != kNoIdx ? a.gx[io0] : 0.0, y0 = io0 != kNoIdx ? a.gy[io0] : 0.0;
             const double x1 = io1 != kNoIdx ? a.gx[io1] : 0.0, y1 = io1 != kNoIdx ? a.gy[io1] : 0.0;
             Best b0 = best_none(), b1 = best_none();
