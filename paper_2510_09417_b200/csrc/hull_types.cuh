@@ -1,6 +1,7 @@
 // Device data layout of the B200 VQhull driver.
 #pragma once
 
+#include <cstddef>
 #include <cstdint>
 
 #include "common.cuh"
@@ -120,16 +121,21 @@ enum : uint8_t { kEmpty = 0, kLeaf = 1, kFin = 2, kInternal = 3 };
 // Per-level planner output.
 struct LevelInfo {
     uint32_t nslots;
-    uint32_t nseg;
     uint32_t nfin;
+    // (nseg, ntiles) and (fin_total, nfin2) are 8-byte aligned pairs: the level
+    // kernels advance each pair with ONE packed 64-bit atomic per planned child
+    uint32_t nseg;
     uint32_t ntiles;
     uint32_t out_total;   // points handed to the level kernel
-    uint32_t fin_total;   // points handed to the finisher
     uint32_t nleaf;
-    uint32_t fin_base;    // first chain entry of this level's finisher segments
+    uint32_t fin_total;   // points handed to the finisher
     uint32_t nfin2;       // CTA-finisher segments (FinRec array from the back)
+    uint32_t fin_base;    // first chain entry of this level's finisher segments
     uint32_t pad;
 };
+static_assert(offsetof(LevelInfo, nseg) % 8 == 0 && offsetof(LevelInfo, ntiles) == offsetof(LevelInfo, nseg) + 4 &&
+              offsetof(LevelInfo, fin_total) % 8 == 0 && offsetof(LevelInfo, nfin2) == offsetof(LevelInfo, fin_total) + 4,
+              "packed LevelInfo pairs");
 
 // Look-back status of one tile (one side) of the partition kernels: two
 // 8-byte words for the aggregate and two for the inclusive prefix, each

@@ -1840,8 +1840,11 @@ __device__ __forceinline__ void plan_child(const LevelArgs& a, uint64_t s, const
         a.n_kind[s] = kd;
         if (kd == kInternal) {
             ntl = (m + kTile - 1) / kTile;
-            j = atomicAdd(&a.n_info->nseg, 1u);
-            t0 = atomicAdd(&a.n_info->ntiles, ntl);
+            {  // one packed atomic for the segment's index and its first tile
+                const uint2 c2 = claim_pair(reinterpret_cast<unsigned long long*>(&a.n_info->nseg), 1u, ntl);
+                j = c2.x;
+                t0 = c2.y;
+            }
             const uint32_t out = atomicAdd(&a.n_info->out_total, m);
             SegRec g;
             g.px = ch.px; g.py = ch.py; g.rx = ch.rx; g.ry = ch.ry; g.qx = ch.qx; g.qy = ch.qy;
@@ -1860,11 +1863,18 @@ __device__ __forceinline__ void plan_child(const LevelArgs& a, uint64_t s, const
             a.n_seg_ctr[j] = 0ull;
             a.n_link[s] = j;
         } else if (kd == kFin) {
-            const uint32_t f = m <= kFinSmall ? atomicAdd(&a.n_info->nfin, 1u)
-                                              : a.n_fin_cap - 1u - atomicAdd(&a.n_info->nfin2, 1u);
+            uint32_t f, before;  // its place in the list, the finisher points planned before it
+            if (m <= kFinSmall) {
+                f = atomicAdd(&a.n_info->nfin, 1u);
+                before = atomicAdd(&a.n_info->fin_total, m);
+            } else {  // one packed atomic for both
+                const uint2 c2 = claim_pair(reinterpret_cast<unsigned long long*>(&a.n_info->fin_total), m, 1u);
+                before = c2.x;
+                f = a.n_fin_cap - 1u - c2.y;
+            }
             FinRec fr;
             fr.c = ch;
-            fr.chain_base = uint64_t(a.info->fin_base) + a.info->fin_total + atomicAdd(&a.n_info->fin_total, m);
+            fr.chain_base = uint64_t(a.info->fin_base) + a.info->fin_total + before;
             fr.slot = uint32_t(s);
             fr.pad = 0;
             a.n_fins[f] = fr;
