@@ -2076,8 +2076,11 @@ __device__ __forceinline__ void level_segcta_tma(const LevelArgs& a, uint32_t ns
     }
 }
 
+#ifndef VQB_LEVEL_MINB
+#define VQB_LEVEL_MINB 3
+#endif
 template <bool GENERAL>
-__global__ void __launch_bounds__(kCtlThreads, 3) level_tma(LevelArgs a) {
+__global__ void __launch_bounds__(kCtlThreads, VQB_LEVEL_MINB) level_tma(LevelArgs a) {
     VQB_PDL();
     plan_level_start(a);
     {
