@@ -186,8 +186,12 @@ class Engine {
             return run_tiny(dx, dy, n, d_out, h, st);
 
         // ---- root stage: polygon + first partition (levels 1+2 in reference mode)
+        // (f64 arrays are 8-byte aligned; the split root's filter pass also takes
+        // arrays that are not 16-byte aligned, the one-pass octagon root does not)
         const bool aligned = ((reinterpret_cast<uintptr_t>(dx) | reinterpret_cast<uintptr_t>(dy)) & 15u) == 0;
-        const bool filtered = !stable_ && !root_reference_ && !force_reference_ && aligned && !getenv("VQB_NO_TMA");
+        const bool aligned8 = ((reinterpret_cast<uintptr_t>(dx) | reinterpret_cast<uintptr_t>(dy)) & 7u) == 0;
+        const bool filtered = !stable_ && !root_reference_ && !force_reference_ && !getenv("VQB_NO_TMA") &&
+                              (root_octagon_ ? aligned : aligned8);
         const bool split = filtered && !root_octagon_;
         // the common small-recursion case (split root + KT) replays one
         // captured CUDA graph: sample, filter, KT and the report copy
@@ -1240,6 +1244,8 @@ class Engine {
         FilterArgs fa;
         std::memset(&fa, 0, sizeof fa);
         fa.xs = dx; fa.ys = dy; fa.n = n; fa.ntiles = ntiles;
+        fa.xoff = uint32_t((reinterpret_cast<uintptr_t>(dx) >> 3) & 1u);
+        fa.yoff = uint32_t((reinterpret_cast<uintptr_t>(dy) >> 3) & 1u);
         fa.ox = bufs_[0].x.as<double>(); fa.oy = bufs_[0].y.as<double>(); fa.oid = bufs_[0].id.as<uint32_t>();
         fa.out_cap = bufs_[0].x.cap / 8;
         fa.ctr = &ctrs_[12]; fa.ticket = &ctrs_[13]; fa.part = fpart_.p;

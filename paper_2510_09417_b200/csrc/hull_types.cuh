@@ -187,6 +187,7 @@ struct FilterArgs {
     double* kx;          // sharded hull: a second copy of the survivors (nullptr: none)
     double* ky;
     uint32_t* kid;
+    uint32_t xoff, yoff; // xs / ys sit this many elements (0 or 1) above a 16-byte boundary
 };
 
 struct LevelArgs {

@@ -1228,6 +1228,13 @@ struct RootRing4 {
     double y[kRing4][kTile];
     unsigned long long bar[kRing4];
 };
+// the filter pass's ring: two spare elements per stage for callers' arrays
+// that are not 16-byte aligned (root_filter_tma)
+struct FilterRing {
+    double x[kRing4][kTile + 2];
+    double y[kRing4][kTile + 2];
+    unsigned long long bar[kRing4];
+};
 
 // named barriers with immediate ids (ptxas then reserves only those)
 template <int ID>
@@ -1523,7 +1530,7 @@ __global__ void __launch_bounds__(kCtlThreads, 3) root_filter_tma(FilterArgs a) 
     VQB_PDL();
     VQB_STAMP(if (threadIdx.x == 0) atomicMin(&g_strace[5], gtimer_ns());)
     extern __shared__ __align__(128) unsigned char dsm[];
-    RootRing4& ring = *reinterpret_cast<RootRing4*>(dsm);
+    FilterRing& ring = *reinterpret_cast<FilterRing*>(dsm);
     __shared__ uint32_t s_cnt[2][kWarps];                      // survivors per warp and tile
     __shared__ uint32_t s_org[2][kWarps];                      // their first output position
     __shared__ uint16_t s_q[kWarps][kTile / kWarps];           // a warp's points needing the chord test
@@ -1533,7 +1540,16 @@ __global__ void __launch_bounds__(kCtlThreads, 3) root_filter_tma(FilterArgs a) 
     const RootPoly& P = c_root.poly;
     const uint32_t n = uint32_t(a.n);
     const uint32_t G = gridDim.x;
-    const uint32_t nfull = n / kTile;
+    // Caller arrays that are 8- but not 16-byte aligned (an odd offset into a
+    // larger array): a tile's bulk copy starts at the 16-byte boundary below
+    // its first element (one element early: a pointer that is not 16-byte
+    // aligned is not the start of an allocation) and brings two elements
+    // more; the points are read at a.xoff / a.yoff in the stage.  A tile whose
+    // copy would run past the arrays' end is staged by the warps themselves,
+    // like the partial last tile.
+    const bool mis = (a.xoff | a.yoff) != 0;
+    const uint32_t nfull = mis ? (n >= 2u ? (n - 2u) / kTile : 0u) : n / kTile;
+    const uint32_t tile_bytes = (kTile + (mis ? 2u : 0u)) * 8u;
     const uint32_t nt = a.ntiles > blockIdx.x ? (a.ntiles - blockIdx.x + G - 1) / G : 0u;
     const bool ctl = threadIdx.x >= kThreads;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1542,10 +1558,10 @@ __global__ void __launch_bounds__(kCtlThreads, 3) root_filter_tma(FilterArgs a) 
         const uint32_t t = blockIdx.x + k * G;
         if (t >= nfull) return;
         const int s = int(k % kRing4);
-        mbar_expect_tx(&ring.bar[s], 2u * kTile * 8u);
+        mbar_expect_tx(&ring.bar[s], 2u * tile_bytes);
         const unsigned long long pol = l2_evict_first_policy();
-        tma_load_1d_stream(ring.x[s], a.xs + uint64_t(t) * kTile, kTile * 8u, &ring.bar[s], pol);
-        tma_load_1d_stream(ring.y[s], a.ys + uint64_t(t) * kTile, kTile * 8u, &ring.bar[s], pol);
+        tma_load_1d_stream(ring.x[s], a.xs - a.xoff + uint64_t(t) * kTile, tile_bytes, &ring.bar[s], pol);
+        tma_load_1d_stream(ring.y[s], a.ys - a.yoff + uint64_t(t) * kTile, tile_bytes, &ring.bar[s], pol);
     };
     if (threadIdx.x == kThreads) {
         for (int s = 0; s < kRing4; ++s) mbar_init(&ring.bar[s], 1);
@@ -1602,7 +1618,7 @@ __global__ void __launch_bounds__(kCtlThreads, 3) root_filter_tma(FilterArgs a) 
                 const uint32_t idx = s_surv[par][warp][j];
                 const uint32_t p = o + j;
                 VQB_CHECK(p < a.out_cap, 15, p, a.out_cap);
-                const double u = ring.x[s][idx], w = ring.y[s][idx];
+                const double u = ring.x[s][a.xoff + idx], w = ring.y[s][a.yoff + idx];
                 a.ox[p] = u;
                 a.oy[p] = w;
                 a.oid[p] = tbase + idx;
@@ -1625,8 +1641,8 @@ __global__ void __launch_bounds__(kCtlThreads, 3) root_filter_tma(FilterArgs a) 
 #pragma unroll
                 for (int i = 0; i < kItems; ++i) {
                     const uint32_t idx = uint32_t(i) * kThreads + tid;
-                    ring.x[s][idx] = tbase + idx < n ? a.xs[tbase + idx] : 0.0;
-                    ring.y[s][idx] = tbase + idx < n ? a.ys[tbase + idx] : 0.0;
+                    ring.x[s][a.xoff + idx] = tbase + idx < n ? a.xs[tbase + idx] : 0.0;
+                    ring.y[s][a.yoff + idx] = tbase + idx < n ? a.ys[tbase + idx] : 0.0;
                 }
                 __syncwarp();
             }
@@ -1637,7 +1653,7 @@ __global__ void __launch_bounds__(kCtlThreads, 3) root_filter_tma(FilterArgs a) 
 #pragma unroll
                 for (int i = 0; i < kItems; ++i) {
                     const uint32_t idx = uint32_t(i) * kThreads + tid;
-                    const double u = ring.x[s][idx], w = ring.y[s][idx];
+                    const double u = ring.x[s][a.xoff + idx], w = ring.y[s][a.yoff + idx];
                     const bool in = (decltype(with_box)::value && ((u > bx0) & (u < bx1) & (w > by0) & (w < by1))) |
                                     inner(u, w);
                     const bool need = (tbase + idx < n) & !in;
@@ -1667,7 +1683,7 @@ __global__ void __launch_bounds__(kCtlThreads, 3) root_filter_tma(FilterArgs a) 
             // phase C: the chord test for the rest, 32 at a time
             uint32_t sn = 0;
             auto chord_round = [&](uint32_t idx, bool valid) {
-                const double u = ring.x[s][idx], w = ring.y[s][idx];
+                const double u = ring.x[s][a.xoff + idx], w = ring.y[s][a.yoff + idx];
                 bool keep = false;
                 if (valid) {
                     bad |= uint32_t(nonfinite_bits(u) | nonfinite_bits(w));
@@ -2401,17 +2417,17 @@ cudaError_t launch_root_filtered(const RootArgs& a, int grid, cudaStream_t st) {
 cudaError_t launch_root_filter(const FilterArgs& a, int grid, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(root_filter_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(RootRing4)));
+        cudaFuncSetAttribute(root_filter_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(FilterRing)));
         attr = true;
     }
-    pdl_launch(root_filter_tma, grid, kCtlThreads, sizeof(RootRing4), st, a);
+    pdl_launch(root_filter_tma, grid, kCtlThreads, sizeof(FilterRing), st, a);
     return cudaGetLastError();
 }
 
 int occupancy_filter() {
     int b = 0;
-    cudaFuncSetAttribute(root_filter_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(RootRing4)));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, root_filter_tma, kCtlThreads, sizeof(RootRing4));
+    cudaFuncSetAttribute(root_filter_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(FilterRing)));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, root_filter_tma, kCtlThreads, sizeof(FilterRing));
     return b;
 }
 

@@ -359,10 +359,11 @@ def test_root_mode_selection(vq, cuda):
         assert vq.stats()["root_filtered"] == 1
     finally:
         vq.set_root_mode("split")
-    # inputs not 16-byte aligned cannot be TMA-streamed: unfiltered root
+    # inputs that are 8- but not 16-byte aligned still take the split root
+    # (the filter pass streams them from the 16-byte boundary below)
     X, Y = dev(np.concatenate([[0.0], xs])), dev(np.concatenate([[0.0], ys]))
     got = vq.hull_device(X[1:], Y[1:]).cpu().numpy().astype(np.uint64)
-    assert vq.stats()["root_filtered"] == 0
+    assert vq.stats()["root_filtered"] == 2
     assert np.array_equal(got, vq.hull_indices(xs, ys))
     vq.set_stable(True)
     try:
@@ -536,3 +537,26 @@ def test_vqhull_compute_pageable_staged_copy(vq, cuda, oracle):
     # one pageable, one page-locked
     rc, got3 = vq.vqhull_compute(xs, Y.numpy())
     assert rc == 0 and np.array_equal(got3, ref)
+
+
+def test_filter_pass_unaligned_arrays(vq, cuda, oracle):
+    """Caller arrays at odd element offsets (8- but not 16-byte aligned), x
+    and y independently, at sizes around the tile size: the filter pass reads
+    them through shifted bulk copies; same list as the oracle's."""
+    import torch
+
+    rng = np.random.default_rng(5)
+    for n in (1023, 1024, 1025, 1026, 2047, 2048, 2049, 5 * 1024 + 1, 300_001, 2_000_000):
+        t = rng.uniform(0, 2 * np.pi, n)
+        r = np.sqrt(rng.uniform(0, 1, n))
+        xs, ys = r * np.cos(t), r * np.sin(t)
+        ref = oracle.hull_indices(xs, ys)
+        for ox, oy in ((1, 1), (1, 0), (0, 1), (3, 2)):
+            X = torch.zeros(n + 4, dtype=torch.float64, device="cuda")
+            Y = torch.zeros(n + 4, dtype=torch.float64, device="cuda")
+            X[ox:ox + n] = torch.from_numpy(xs).cuda()
+            Y[oy:oy + n] = torch.from_numpy(ys).cuda()
+            got = vq.hull_device(X[ox:ox + n], Y[oy:oy + n]).cpu().numpy().astype(np.uint64)
+            assert np.array_equal(got, ref), (n, ox, oy)
+            if n > 1024:
+                assert vq.stats()["root_filtered"] == 2
