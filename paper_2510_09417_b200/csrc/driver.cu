@@ -602,7 +602,10 @@ class Engine {
         }
         constexpr size_t kChunk = size_t(8) << 20;
         constexpr int kBufsPerThread = 3;
-        const int nthr = int(std::max(1u, std::min(8u, std::thread::hardware_concurrency() / 2)));
+        // (VQHULL_STAGE_THREADS overrides the worker count)
+        static const int env_thr = getenv("VQHULL_STAGE_THREADS") ? atoi(getenv("VQHULL_STAGE_THREADS")) : 0;
+        const int nthr = env_thr > 0 ? std::min(env_thr, 64)
+                                     : int(std::max(1u, std::min(8u, std::thread::hardware_concurrency() / 2)));
         const size_t need = size_t(nthr) * kBufsPerThread * kChunk;
         if (stage_bytes_ < need) {
             if (stage_) cudaFreeHost(stage_);
