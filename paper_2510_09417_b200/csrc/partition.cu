@@ -1526,11 +1526,13 @@ __device__ __forceinline__ void filter_warp_fold(ExtKey& lo, ExtKey& hi, double&
     }
 }
 
+template <bool MIS>  // MIS: caller arrays not 16-byte aligned (the aligned instance carries no offsets)
 __global__ void __launch_bounds__(kCtlThreads, 3) root_filter_tma(FilterArgs a) {
     VQB_PDL();
     VQB_STAMP(if (threadIdx.x == 0) atomicMin(&g_strace[5], gtimer_ns());)
     extern __shared__ __align__(128) unsigned char dsm[];
-    FilterRing& ring = *reinterpret_cast<FilterRing*>(dsm);
+    using Ring = std::conditional_t<MIS, FilterRing, RootRing4>;
+    Ring& ring = *reinterpret_cast<Ring*>(dsm);
     __shared__ uint32_t s_cnt[2][kWarps];                      // survivors per warp and tile
     __shared__ uint32_t s_org[2][kWarps];                      // their first output position
     __shared__ uint16_t s_q[kWarps][kTile / kWarps];           // a warp's points needing the chord test
@@ -1547,7 +1549,8 @@ __global__ void __launch_bounds__(kCtlThreads, 3) root_filter_tma(FilterArgs a) 
     // more; the points are read at a.xoff / a.yoff in the stage.  A tile whose
     // copy would run past the arrays' end is staged by the warps themselves,
     // like the partial last tile.
-    const bool mis = (a.xoff | a.yoff) != 0;
+    constexpr bool mis = MIS;
+    const uint32_t xoff = MIS ? a.xoff : 0u, yoff = MIS ? a.yoff : 0u;
     const uint32_t nfull = mis ? (n >= 2u ? (n - 2u) / kTile : 0u) : n / kTile;
     const uint32_t tile_bytes = (kTile + (mis ? 2u : 0u)) * 8u;
     const uint32_t nt = a.ntiles > blockIdx.x ? (a.ntiles - blockIdx.x + G - 1) / G : 0u;
@@ -1560,8 +1563,8 @@ __global__ void __launch_bounds__(kCtlThreads, 3) root_filter_tma(FilterArgs a) 
         const int s = int(k % kRing4);
         mbar_expect_tx(&ring.bar[s], 2u * tile_bytes);
         const unsigned long long pol = l2_evict_first_policy();
-        tma_load_1d_stream(ring.x[s], a.xs - a.xoff + uint64_t(t) * kTile, tile_bytes, &ring.bar[s], pol);
-        tma_load_1d_stream(ring.y[s], a.ys - a.yoff + uint64_t(t) * kTile, tile_bytes, &ring.bar[s], pol);
+        tma_load_1d_stream(ring.x[s], a.xs - xoff + uint64_t(t) * kTile, tile_bytes, &ring.bar[s], pol);
+        tma_load_1d_stream(ring.y[s], a.ys - yoff + uint64_t(t) * kTile, tile_bytes, &ring.bar[s], pol);
     };
     if (threadIdx.x == kThreads) {
         for (int s = 0; s < kRing4; ++s) mbar_init(&ring.bar[s], 1);
@@ -1618,7 +1621,7 @@ __global__ void __launch_bounds__(kCtlThreads, 3) root_filter_tma(FilterArgs a) 
                 const uint32_t idx = s_surv[par][warp][j];
                 const uint32_t p = o + j;
                 VQB_CHECK(p < a.out_cap, 15, p, a.out_cap);
-                const double u = ring.x[s][a.xoff + idx], w = ring.y[s][a.yoff + idx];
+                const double u = ring.x[s][xoff + idx], w = ring.y[s][yoff + idx];
                 a.ox[p] = u;
                 a.oy[p] = w;
                 a.oid[p] = tbase + idx;
@@ -1641,8 +1644,8 @@ __global__ void __launch_bounds__(kCtlThreads, 3) root_filter_tma(FilterArgs a) 
 #pragma unroll
                 for (int i = 0; i < kItems; ++i) {
                     const uint32_t idx = uint32_t(i) * kThreads + tid;
-                    ring.x[s][a.xoff + idx] = tbase + idx < n ? a.xs[tbase + idx] : 0.0;
-                    ring.y[s][a.yoff + idx] = tbase + idx < n ? a.ys[tbase + idx] : 0.0;
+                    ring.x[s][xoff + idx] = tbase + idx < n ? a.xs[tbase + idx] : 0.0;
+                    ring.y[s][yoff + idx] = tbase + idx < n ? a.ys[tbase + idx] : 0.0;
                 }
                 __syncwarp();
             }
@@ -1653,7 +1656,7 @@ __global__ void __launch_bounds__(kCtlThreads, 3) root_filter_tma(FilterArgs a) 
 #pragma unroll
                 for (int i = 0; i < kItems; ++i) {
                     const uint32_t idx = uint32_t(i) * kThreads + tid;
-                    const double u = ring.x[s][a.xoff + idx], w = ring.y[s][a.yoff + idx];
+                    const double u = ring.x[s][xoff + idx], w = ring.y[s][yoff + idx];
                     const bool in = (decltype(with_box)::value && ((u > bx0) & (u < bx1) & (w > by0) & (w < by1))) |
                                     inner(u, w);
                     const bool need = (tbase + idx < n) & !in;
@@ -1683,7 +1686,7 @@ __global__ void __launch_bounds__(kCtlThreads, 3) root_filter_tma(FilterArgs a) 
             // phase C: the chord test for the rest, 32 at a time
             uint32_t sn = 0;
             auto chord_round = [&](uint32_t idx, bool valid) {
-                const double u = ring.x[s][a.xoff + idx], w = ring.y[s][a.yoff + idx];
+                const double u = ring.x[s][xoff + idx], w = ring.y[s][yoff + idx];
                 bool keep = false;
                 if (valid) {
                     bad |= uint32_t(nonfinite_bits(u) | nonfinite_bits(w));
@@ -2417,17 +2420,23 @@ cudaError_t launch_root_filtered(const RootArgs& a, int grid, cudaStream_t st) {
 cudaError_t launch_root_filter(const FilterArgs& a, int grid, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(root_filter_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(FilterRing)));
+        cudaFuncSetAttribute(root_filter_tma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(FilterRing)));
+        cudaFuncSetAttribute(root_filter_tma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(FilterRing)));
         attr = true;
     }
-    pdl_launch(root_filter_tma, grid, kCtlThreads, sizeof(FilterRing), st, a);
+    if (a.xoff | a.yoff) pdl_launch(root_filter_tma<true>, grid, kCtlThreads, sizeof(FilterRing), st, a);
+    else pdl_launch(root_filter_tma<false>, grid, kCtlThreads, sizeof(RootRing4), st, a);
     return cudaGetLastError();
 }
 
 int occupancy_filter() {
     int b = 0;
-    cudaFuncSetAttribute(root_filter_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(FilterRing)));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, root_filter_tma, kCtlThreads, sizeof(FilterRing));
+    int c = 0;
+    cudaFuncSetAttribute(root_filter_tma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(FilterRing)));
+    cudaFuncSetAttribute(root_filter_tma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(FilterRing)));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, root_filter_tma<false>, kCtlThreads, sizeof(FilterRing));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, root_filter_tma<true>, kCtlThreads, sizeof(FilterRing));
+    b = b < c ? b : c;
     return b;
 }
 
