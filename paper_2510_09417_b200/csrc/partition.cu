@@ -1360,7 +1360,6 @@ __global__ void __launch_bounds__(kCtlThreads, 3) root_filtered_tma(RootArgs a) 
                 run1 += __popc(b1);
             }
         };
-        uint32_t sn_prev = 0;  // this warp's survivors of the tile before
         for (uint32_t k = 0; k < nt; ++k) {
             const uint32_t t = blockIdx.x + k * G;
             const uint32_t tbase = t * uint32_t(kTile);
