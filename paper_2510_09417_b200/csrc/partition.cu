@@ -1631,6 +1631,10 @@ __global__ void __launch_bounds__(kCtlThreads, 3) root_filter_tma(FilterArgs a) 
                 }
             }
         };
+        // the tile loop, instantiated per inner test (a uniform choice per call:
+        // each instance keeps only its own region's constants live)
+        auto tiles = [&](auto mode_tag) {
+        constexpr int kMode = decltype(mode_tag)::value;
         uint32_t sn_prev = 0;  // this warp's survivors of the tile before
         for (uint32_t k = 0; k < nt; ++k) {
             const uint32_t t = blockIdx.x + k * G;
@@ -1664,17 +1668,17 @@ __global__ void __launch_bounds__(kCtlThreads, 3) root_filter_tma(FilterArgs a) 
                     qn += __popc(b);
                 }
             };
-            if (mode == 3u) {  // the disk covers the box: one test
+            if constexpr (kMode == 3) {  // the disk covers the box: one test
                 phase_a([&](double u, double w) {
                     const double du = u - P.dcx, dw = w - P.dcy;
                     return __fma_rn(du, du, __dmul_rn(dw, dw)) < P.dr2;
                 }, std::false_type{});
-            } else if (mode == 2u) {
+            } else if constexpr (kMode == 2) {
                 phase_a([&](double u, double w) {
                     const double du = u - P.dcx, dw = w - P.dcy;
                     return __fma_rn(du, du, __dmul_rn(dw, dw)) < P.dr2;
                 }, std::true_type{});
-            } else if (mode == 1u) {
+            } else if constexpr (kMode == 1) {
                 phase_a([&](double u, double w) {
                     const double du = fabs(u - P.ocx), dw = fabs(w - P.ocy);
                     return (du < P.ohx) & (dw < P.ohy) & (du + dw < P.od);
@@ -1724,6 +1728,11 @@ __global__ void __launch_bounds__(kCtlThreads, 3) root_filter_tma(FilterArgs a) 
             sn_prev = sn;
         }
         if (nt >= 1) store_tile(nt - 1, sn_prev);
+        };
+        if (mode == 3u) tiles(std::integral_constant<int, 3>{});
+        else if (mode == 2u) tiles(std::integral_constant<int, 2>{});
+        else if (mode == 1u) tiles(std::integral_constant<int, 1>{});
+        else tiles(std::integral_constant<int, 0>{});
     }
     // CTA partial -> the last CTA folds them and writes p, q and the slot
     uint32_t nb = bad;
