@@ -376,7 +376,7 @@ class Engine {
             if (l == 2) stats_.survivors_root = written;
             else stats_.bytes_levels += 20 * written;
             stats_.finisher_points += li.fin_total;
-            stats_.finisher_segments += li.nfin;
+            stats_.finisher_segments += li.nfin + li.nfin2;
             stats_.bytes_finisher += uint64_t(li.fin_total) * 20 + uint64_t(li.fin_total) * 4;
             stats_.segments += li.nseg;
             stats_.level_points += li.out_total;

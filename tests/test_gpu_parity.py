@@ -560,3 +560,28 @@ def test_filter_pass_unaligned_arrays(vq, cuda, oracle):
             assert np.array_equal(got, ref), (n, ox, oy)
             if n > 1024:
                 assert vq.stats()["root_filtered"] == 2
+
+
+def test_large_trees_hybrid_emission(vq, cuda, oracle):
+    """Recursion trees too large for the one-CTA emission kernel: their top
+    levels are emitted by that kernel, the levels below by one launch each
+    (driver.cu, the emission section).  Circle-like inputs of several sizes
+    and shapes (every point a vertex; an ellipse; a circle with interior
+    points and duplicated vertices), against the oracle."""
+    rng = np.random.default_rng(11)
+    cases = []
+    for n in (1_200_000, 2_500_000):
+        t = rng.uniform(0, 2 * np.pi, n)
+        cases.append((np.cos(t), np.sin(t)))
+    t = rng.uniform(0, 2 * np.pi, 1_500_000)
+    cases.append((3.0 * np.cos(t), 0.25 * np.sin(t)))
+    t = rng.uniform(0, 2 * np.pi, 2_000_000)
+    r = np.where(rng.random(t.size) < 0.7, 1.0, np.sqrt(rng.uniform(0, 1, t.size)))
+    xs, ys = r * np.cos(t), r * np.sin(t)
+    xs[-50_000:], ys[-50_000:] = xs[:50_000], ys[:50_000]  # duplicated vertices: first occurrence wins
+    cases.append((xs, ys))
+    for i, (xs, ys) in enumerate(cases):
+        got = gpu_indices(vq, xs, ys)
+        s = vq.stats()
+        assert np.array_equal(got, oracle.hull_indices(xs, ys)), f"case {i}"
+        assert s["finisher_segments"] > 1000 and s["launches"] > 20, s  # host-driven levels + finisher + emission
