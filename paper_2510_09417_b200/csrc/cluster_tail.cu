@@ -69,8 +69,6 @@ struct KcSmem {
     uint32_t gcnt[kKcChildren];
     unsigned long long gkey[kKcChildren];
     uint16_t cmap[kKcChildren];
-    double ax[kKcChildren], ay[kKcChildren];  // each child's apex
-    uint32_t agid[kKcChildren];             // apex as rank << 16 | local index
     uint32_t wsum[kKcThreads / 32], wsum2[kKcThreads / 32];
     uint16_t tlist[kKcPts];                 // local extra candidates (ties)
     uint32_t ntie;
@@ -249,7 +247,12 @@ __global__ void __launch_bounds__(kKcThreads, 1) cluster_tail_kernel(const __gri
         // candidate slots at once, then the coordinates of the (almost always
         // single) candidate; the apex is recorded as (rank, local index) and
         // its input index looked up only at emission
-        for (uint32_t c = tid; c < nch; c += kKcThreads) {
+        // (nch <= kKcChildren <= kKcThreads: child c = tid, so the apex stays in
+        // this thread's registers for the node table below — no barrier between)
+        double apx = 0.0, apy = 0.0;
+        uint32_t apref = kKcNone;
+        if (tid < nch) {
+            const uint32_t c = tid;
             uint32_t lv[kKcCtas];
 #pragma unroll
             for (int r = 0; r < kKcCtas; ++r) lv[r] = cluster.map_shared_rank(&S, r)->lcand[b][c];
@@ -284,11 +287,10 @@ __global__ void __launch_bounds__(kKcThreads, 1) cluster_tail_kernel(const __gri
                     }
                 }
             }
-            S.ax[c] = bx;
-            S.ay[c] = by;
-            S.agid[c] = bref;
+            apx = bx;
+            apy = by;
+            apref = bref;
         }
-        __syncthreads();
         // next level's nodes (block scan over the internal children), leaves, links
         uint32_t nnext = 0, nlv = 0, out_pts = 0;
         {
@@ -332,19 +334,19 @@ __global__ void __launch_bounds__(kKcThreads, 1) cluster_tail_kernel(const __gri
                     nn2.py = side ? nd.ry : nd.py;
                     nn2.qx = side ? nd.qx : nd.rx;
                     nn2.qy = side ? nd.qy : nd.ry;
-                    nn2.rx = S.ax[c];
-                    nn2.ry = S.ay[c];
+                    nn2.rx = apx;
+                    nn2.ry = apy;
                     S.ntree[nxt][nid] = uint16_t(tnew);
                     link = kKcLinkNode | tnew;
                     map = uint16_t(nid);
                     if (rank == 0) {
-                        S.tapex[tnew] = S.agid[c];
+                        S.tapex[tnew] = apref;
                         S.tleft[tnew] = kKcLinkEmpty;
                         S.tright[tnew] = kKcLinkEmpty;
                     }
                 } else if (leaf) {
                     link = kKcLinkLeaf | lid;
-                    if (rank == 0) S.leaf_gid[lid] = S.agid[c];
+                    if (rank == 0) S.leaf_gid[lid] = apref;
                 }
                 S.cmap[c] = map;
                 if (rank == 0) {
@@ -396,7 +398,8 @@ __global__ void __launch_bounds__(kKcThreads, 1) cluster_tail_kernel(const __gri
         }
         nn = nnext;
         cur = nxt;
-        __syncthreads();
+        // (no barrier: the relabelling above is warp-local, and everything the
+        // next level reads was complete at "cmap complete")
         if (nn == 0) break;
     }
     cluster.sync();  // no CTA leaves while another may read its shared memory
